@@ -1,0 +1,32 @@
+# Build of the product library (libvpb.so, sm_100a) and the test-only oracles.
+NVCC     ?= /usr/local/cuda/bin/nvcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2103_01954_b200
+SRC      := $(PKG)/csrc
+OBJ      := build/obj
+# -fmad=false + IEEE div/sqrt on the device, -ffp-contract=off on the host: the reference's
+# binary32 operation sequence is reproduced exactly (see vpb_device.cuh).
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -prec-div=true -prec-sqrt=true \
+            -Xcompiler -fPIC,-ffp-contract=off,-O3 -Xptxas -v
+HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.hpp $(SRC)/*.cuh) include/vpb.h
+
+.PHONY: all lib oracle clean
+all: lib oracle
+lib: $(PKG)/libvpb.so
+oracle:
+	$(MAKE) -C oracle all
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/$*.ptxas.log || (cat $(OBJ)/$*.ptxas.log; false)
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
+
+$(PKG)/libvpb.so: $(OBJ)/vpb_kernels.o $(OBJ)/vpb_api.o $(OBJ)/vpb_synth.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+
+clean:
+	rm -rf build $(PKG)/libvpb.so
+	$(MAKE) -C oracle clean

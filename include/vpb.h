@@ -1,0 +1,159 @@
+/* vpb.h — C-ABI of the B200-native MVP raymarcher (libvpb.so).
+ *
+ * Drop-in boundary for the reference's forward raymarcher:
+ *
+ *   RenderOutput volprim::render(const Scene &, int frame, const Camera &, const MarchConfig &)
+ *     (/root/reference/proj/src/volprim/march.h:59, body march.cpp:95-132)
+ *
+ * The reference has no FFI of its own (it is a C++ library); these are the
+ * entry points a C++ caller binds through a thin adapter. Plain
+ * pointers and sizes only. Every entry point returns an int status that mirrors
+ * volprim::ErrorCategory (errors.h:11-17): 0 ok, 2 usage, 6 numeric, plus 7 for a CUDA /
+ * device failure. vp_last_error() returns the message of the last failure on a context
+ * (or of the last context-free call when ctx is NULL).
+ *
+ * Flat layouts (matrices are column-major exactly like volprim::Mat3::m, math.h:71-73):
+ *   PrimitiveTransform (primitive.h:45-52) = 24 floats
+ *       tBase[3] rBase[9] sBase[3] deltaT[3] deltaR[3] deltaS[3]
+ *   AffineXf (primitive.h:56-64)           = 15 floats  t[3] rot[9] scale[3]
+ *   PrimitiveSlab payload (primitive.h:25-41) = K*4*M^3 floats, planar (k, channel, z, y, x)
+ *   Image outputs (image.h:14-25): rgb H*W*3 interleaved, alpha H*W, samples H*W (int32)
+ *
+ * Output / input pointers may be host memory (pageable or pinned) or device memory of the
+ * context's device; the library detects which (cudaPointerGetAttributes). A context is not
+ * thread-safe: use one context per device per host thread (the reference render() is
+ * re-entrant because it holds no state; here the state is the resident scene).
+ */
+#ifndef VPB_H
+#define VPB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPB_VERSION 1
+
+enum {
+    VP_OK = 0,
+    VP_ERR_USAGE = 2,   /* ErrorCategory::Usage   (errors.h:12) */
+    VP_ERR_NUMERIC = 6, /* ErrorCategory::Numeric (errors.h:16) */
+    VP_ERR_DEVICE = 7   /* CUDA / device failure (no reference counterpart) */
+};
+
+typedef struct vp_ctx vp_ctx;
+
+/* volprim::Camera (camera.h:21-29): intrinsics K, world-to-camera rotation R and
+ * translation t (x_cam = R x_world + t), image size. Rotation::axisAngle is not read by
+ * render() and is therefore not part of the boundary. */
+typedef struct vp_camera {
+    float K[9];
+    float R[9];
+    float t[3];
+    int32_t width;
+    int32_t height;
+} vp_camera;
+
+/* volprim::MarchConfig (march.h:11-20). accumulation_permutation is the reference's test
+ * hook; a non-zero value returns VP_ERR_USAGE. */
+typedef struct vp_march {
+    float step_size;   /* metres, > 0 */
+    float early_eps;   /* terminate once T > 1 - early_eps */
+    int32_t jitter;    /* 0/1: per-pixel hashToUnit(hashCombine(seed, pixelId)) offset */
+    int32_t reserved;
+    uint64_t seed;
+    uint64_t accumulation_permutation;
+} vp_march;
+
+/* Per-render counters (device atomics; the reference's only diagnostic is the per-pixel
+ * sample count, march.h:49-55). */
+typedef struct vp_stats {
+    int64_t ray_samples;   /* sum of per-pixel samples (RenderOutput::totalSamples) */
+    int64_t prim_samples;  /* primitive evaluations (body of march.cpp:63-70) */
+    int64_t hit_rays;      /* rays with a non-empty segment list */
+    int64_t early_exits;   /* rays stopped by T > 1 - eps (march.cpp:87) */
+    int64_t saturated;     /* rays stopped by the saturation clamp (march.cpp:75-84) */
+    int64_t overflow_rays; /* rays re-marched by the wide-window fallback kernel */
+    int64_t keys;          /* (tile, depth) keys emitted by the binning pass */
+    int64_t refills;       /* per-ray window refills (rays with > window hits) */
+    float ms;              /* device time of the render (CUDA events), ms */
+    float reserved;
+} vp_stats;
+
+int vp_version(void);
+
+/* ---- context ------------------------------------------------------------------------- */
+int vp_create(int32_t device, vp_ctx **out);
+int vp_destroy(vp_ctx *ctx);
+const char *vp_last_error(const vp_ctx *ctx);
+/* The CUDA stream the context launches on (cudaStream_t as void*). */
+void *vp_stream(vp_ctx *ctx);
+
+/* ---- host-side scene preparation (exact reference arithmetic, no device work) --------- */
+/* Frame::composed() / compose() (scene.h:19-24, primitive.cpp:41-49): 24 -> 15 floats per
+ * primitive. VP_ERR_USAGE on a non-positive composed scale, like the reference. */
+int vp_compose(int32_t n_prim, const float *transforms24, float *xf15);
+
+/* ---- resident scene ---------------------------------------------------------------------
+ * Uploads a frame: composed transforms and the planar slab, which kernel K0 repacks on the
+ * device into channel-interleaved float4 voxels (k, z, y, x, rgba). window = WindowParams
+ * (primitive.h:14-17). VP_ERR_USAGE on K < 0, M < 1 (when K > 0), odd or negative beta,
+ * non-positive scale. */
+int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
+                 const float *payload_planar, float window_alpha, int32_t window_beta);
+/* Replace only the transforms (same K), e.g. a new frame with the same payload. */
+int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15);
+/* Adopt an already-interleaved payload (K*M^3 float4 = K*M^3*4 floats, host or device),
+ * e.g. after an NCCL broadcast of the repacked buffer. Keeps the current transforms. */
+int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m,
+                               const float *payload_interleaved);
+/* Device pointer / float count of the resident interleaved payload (for broadcasts). */
+int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats);
+
+/* ---- render (the drop-in for volprim::render) --------------------------------------------
+ * Synchronous. rgb: H*W*3, alpha: H*W, samples: H*W (nullable), stats nullable. */
+int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb,
+              float *alpha, int32_t *samples, vp_stats *stats);
+/* Asynchronous variant: device output pointers only (samples nullable), enqueued on
+ * `stream` (cudaStream_t; NULL = the context's stream). Counters can be read afterwards
+ * with vp_read_stats (which synchronises that stream). */
+int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb_dev,
+                    float *alpha_dev, int32_t *samples_dev, void *stream);
+int vp_read_stats(vp_ctx *ctx, vp_stats *stats);
+
+/* march() over arbitrary rays (march.h:42-44 with intersect(), lbvh.cpp:207-234, as the
+ * candidate source over all K primitives). jitter01 nullable (0.5). Synchronous. */
+int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
+                  const float *jitter01, const vp_march *cfg, float *rgb, float *alpha,
+                  int32_t *samples);
+
+/* composite() (march.cpp:134-147): out = A*I + (1-A)*B, all H*W(*3) arrays. */
+int vp_composite(vp_ctx *ctx, int32_t width, int32_t height, const float *rgb,
+                 const float *alpha, const float *background, float *out);
+
+/* ---- binning artefacts (parity checks of cull / keys / per-tile sorted lists) -----------
+ * rect4: K*4 {tx0,ty0,tx1,ty1} (empty = {0,0,-1,-1}); depth_key: K; tile_offsets:
+ * n_tiles+1; tile_prims: up to cap entries. *n_keys receives the total. Synchronous. */
+int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *depth_key,
+                   int32_t *tile_offsets, int32_t *tile_prims, int64_t cap, int64_t *n_keys);
+
+/* Test hook: evaluates the device port of glibc expf used by window() (primitive.cpp:27)
+ * elementwise, so the port can be checked exhaustively against the host libm. */
+int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y);
+
+/* ---- synthetic benchmark inputs ("mvp_shell"), host only ------------------ */
+/* transforms24: K*24, payload_planar: K*4*M^3 (either may be NULL to skip). */
+int vp_make_shell_scene(int32_t n_prim, int32_t m, float *transforms24, float *payload_planar);
+/* lookAtCamera (synthetic.cpp:15-38). axis_angle nullable. */
+int vp_look_at_camera(const float *position, const float *target, const float *up,
+                      float focal_px, int32_t width, int32_t height, vp_camera *out,
+                      float *axis_angle);
+/* view < 0: the single headline view; else view v of the n_views ring. */
+int vp_shell_camera(int32_t view, int32_t n_views, int32_t width, vp_camera *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VPB_H */

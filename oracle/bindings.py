@@ -1,0 +1,278 @@
+"""TEST INFRASTRUCTURE — ctypes bindings of the parity checkers. NOT PRODUCT CODE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module, and only as the checker or the timed CPU baseline.
+
+  Oracle   -> oracle/liboracle.so           plain-C restatement (vp_oracle.c)
+  RefCore  -> oracle/_ref/libvolprim_ref.so the unmodified reference core + ref_glue.cpp
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libvolprim_ref.so"
+
+f32p = C.POINTER(C.c_float)
+i32p = C.POINTER(C.c_int32)
+u32p = C.POINTER(C.c_uint32)
+
+
+def _p(a, t=f32p):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _f(a, n=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    return a if n is None else a.reshape(n)
+
+
+def cam_arrays(cam):
+    """(K9, R9, t3) column-major float32 arrays from an api.Camera."""
+    return (_f(np.asarray(cam.intrinsics, np.float32).T.reshape(-1)),
+            _f(np.asarray(cam.rotation, np.float32).T.reshape(-1)),
+            _f(np.asarray(cam.translation, np.float32).reshape(-1)))
+
+
+def build(ref: bool = True) -> None:
+    """make -C oracle (and the reference core when /root/reference is present)."""
+    import subprocess
+    targets = ["oracle"]
+    if ref and pathlib.Path(os.environ.get("VPB_REFERENCE", "/root/reference/proj")).exists():
+        targets.append("ref")
+    subprocess.run(["make", "-C", str(HERE), *targets], check=True,
+                   stdout=subprocess.DEVNULL)
+
+
+class Oracle:
+    """The C restatement (liboracle.so)."""
+
+    def __init__(self, path: pathlib.Path = ORACLE_SO):
+        if not path.exists():
+            build(ref=False)
+        self.lib = C.CDLL(str(path))
+        L = self.lib
+        L.vpo_compose.argtypes = [C.c_int32, f32p, f32p]
+        L.vpo_generate_ray.argtypes = [f32p, f32p, f32p, C.c_float, C.c_float, f32p, f32p]
+        L.vpo_intersect.restype = C.c_int32
+        L.vpo_intersect.argtypes = [C.c_int32, f32p, f32p, f32p, C.c_int32, i32p, f32p, f32p]
+        L.vpo_window.restype = C.c_float
+        L.vpo_window.argtypes = [C.c_float] * 4 + [C.c_int32]
+        L.vpo_march_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32,
+                                     C.c_int64, f32p, f32p, f32p, C.c_float, C.c_float,
+                                     C.c_uint64, f32p, f32p, i32p]
+        L.vpo_render.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, f32p,
+                                 f32p, f32p, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                 C.c_int32, C.c_uint64, C.c_uint64, f32p, f32p, i32p, C.c_int32]
+        L.vpo_composite.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]
+        L.vpo_cull.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, i32p, u32p]
+        L.vpo_tile_lists.restype = C.c_int64
+        L.vpo_tile_lists.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32,
+                                     i32p, i32p, C.c_int64]
+        L.vpo_expf_port.restype = C.c_float
+        L.vpo_expf_port.argtypes = [C.c_float]
+        L.vpo_expf_mismatches.restype = C.c_int64
+        L.vpo_expf_mismatches.argtypes = [C.c_uint32, C.c_uint32, f32p]
+
+    def compose(self, tr24):
+        tr = _f(tr24).reshape(-1, 24)
+        out = np.zeros((tr.shape[0], 15), np.float32)
+        rc = self.lib.vpo_compose(tr.shape[0], _p(tr), _p(out))
+        return rc, out
+
+    def render(self, xf15, m, payload, window, cam, cfg, n_threads=None):
+        xf = _f(xf15).reshape(-1, 15)
+        k9, r9, t3 = cam_arrays(cam)
+        w, h = int(cam.width), int(cam.height)
+        rgb = np.zeros((h, w, 3), np.float32)
+        alpha = np.zeros((h, w, 1), np.float32)
+        samples = np.zeros(h * w, np.int32)
+        nt = n_threads if n_threads else (os.cpu_count() or 1)
+        rc = self.lib.vpo_render(xf.shape[0], int(m), _p(xf), _p(_f(payload)), float(window.alpha),
+                                 int(window.beta), _p(k9), _p(r9), _p(t3), w, h,
+                                 float(cfg.step_size), float(cfg.early_eps), int(bool(cfg.jitter)),
+                                 int(cfg.seed), int(cfg.accumulation_permutation), _p(rgb), _p(alpha),
+                                 _p(samples, i32p), int(nt))
+        assert rc == 0
+        return rgb, alpha, samples
+
+    def march_rays(self, xf15, m, payload, window, origins, dirs, cfg, jitter=None):
+        xf = _f(xf15).reshape(-1, 15)
+        o = _f(origins).reshape(-1, 3)
+        d = _f(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        j = None if jitter is None else _f(jitter).reshape(n)
+        rgb = np.zeros((n, 3), np.float32)
+        alpha = np.zeros(n, np.float32)
+        samples = np.zeros(n, np.int32)
+        self.lib.vpo_march_rays(xf.shape[0], int(m), _p(xf), _p(_f(payload)), float(window.alpha),
+                                int(window.beta), n, _p(o), _p(d), _p(j), float(cfg.step_size),
+                                float(cfg.early_eps), int(cfg.accumulation_permutation), _p(rgb),
+                                _p(alpha), _p(samples, i32p))
+        return rgb, alpha, samples
+
+    def generate_ray(self, cam, px, py):
+        k9, r9, t3 = cam_arrays(cam)
+        o = np.zeros(3, np.float32)
+        d = np.zeros(3, np.float32)
+        self.lib.vpo_generate_ray(_p(k9), _p(r9), _p(t3), float(px), float(py), _p(o), _p(d))
+        return o, d
+
+    def intersect(self, xf15, origin, direction):
+        xf = _f(xf15).reshape(-1, 15)
+        k = xf.shape[0]
+        prims = np.zeros(max(k, 1), np.int32)
+        te = np.zeros(max(k, 1), np.float32)
+        tx = np.zeros(max(k, 1), np.float32)
+        n = self.lib.vpo_intersect(k, _p(xf), _p(_f(origin, 3)), _p(_f(direction, 3)), k,
+                                   _p(prims, i32p), _p(te), _p(tx))
+        return prims[:n], te[:n], tx[:n]
+
+    def cull(self, xf15, cam):
+        xf = _f(xf15).reshape(-1, 15)
+        k = xf.shape[0]
+        k9, r9, t3 = cam_arrays(cam)
+        rects = np.zeros((max(k, 1), 4), np.int32)
+        keys = np.zeros(max(k, 1), np.uint32)
+        self.lib.vpo_cull(k, _p(xf), _p(k9), _p(r9), _p(t3), int(cam.width), int(cam.height),
+                          _p(rects, i32p), _p(keys, u32p))
+        return rects[:k], keys[:k]
+
+    def tile_lists(self, xf15, cam):
+        xf = _f(xf15).reshape(-1, 15)
+        k9, r9, t3 = cam_arrays(cam)
+        tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        offs = np.zeros(tiles + 1, np.int32)
+        total = self.lib.vpo_tile_lists(xf.shape[0], _p(xf), _p(k9), _p(r9), _p(t3),
+                                        int(cam.width), int(cam.height), _p(offs, i32p), None, 0)
+        prims = np.zeros(max(total, 1), np.int32)
+        self.lib.vpo_tile_lists(xf.shape[0], _p(xf), _p(k9), _p(r9), _p(t3), int(cam.width),
+                                int(cam.height), _p(offs, i32p), _p(prims, i32p), total)
+        return offs, prims[:total]
+
+    def window(self, x, y, z, alpha=8.0, beta=8):
+        return self.lib.vpo_window(x, y, z, alpha, beta)
+
+    def expf_port(self, x):
+        return self.lib.vpo_expf_port(float(x))
+
+    def expf_mismatches(self, lo_bits: int, hi_bits: int, values: np.ndarray) -> int:
+        v = _f(values)
+        assert v.size == hi_bits - lo_bits + 1
+        return int(self.lib.vpo_expf_mismatches(lo_bits, hi_bits, _p(v)))
+
+    def composite(self, rgb, alpha, bg):
+        h, w = rgb.shape[:2]
+        out = np.zeros((h, w, 3), np.float32)
+        self.lib.vpo_composite(w, h, _p(_f(rgb)), _p(_f(alpha)), _p(_f(bg)), _p(out))
+        return out
+
+
+class RefCore:
+    """The unmodified reference core (oracle/_ref/libvolprim_ref.so)."""
+
+    @staticmethod
+    def available() -> bool:
+        return REF_SO.exists()
+
+    def __init__(self, path: pathlib.Path = REF_SO):
+        self.lib = C.CDLL(str(path))
+        L = self.lib
+        L.vpref_last_error.restype = C.c_char_p
+        L.vpref_compose.argtypes = [C.c_int32, f32p, f32p]
+        L.vpref_render.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, f32p,
+                                   f32p, f32p, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                   C.c_int32, C.c_uint64, C.c_uint64, f32p, f32p, i32p]
+        L.vpref_look_at.argtypes = [f32p, f32p, f32p, C.c_float, C.c_int32, C.c_int32, f32p,
+                                    f32p, f32p, f32p]
+        L.vpref_generate_ray.argtypes = [f32p, f32p, f32p, C.c_int32, C.c_int32, C.c_float,
+                                         C.c_float, f32p, f32p]
+        L.vpref_intersect.argtypes = [C.c_int32, f32p, f32p, f32p, C.c_int32, i32p, i32p, f32p,
+                                      f32p, f32p, f32p]
+        L.vpref_march_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32,
+                                       C.c_int64, f32p, f32p, f32p, C.c_float, C.c_float,
+                                       C.c_uint64, f32p, f32p, i32p]
+        L.vpref_window.restype = C.c_float
+        L.vpref_window.argtypes = [C.c_float] * 4 + [C.c_int32]
+
+    def error(self):
+        return self.lib.vpref_last_error().decode()
+
+    def compose(self, tr24):
+        tr = _f(tr24).reshape(-1, 24)
+        out = np.zeros((tr.shape[0], 15), np.float32)
+        rc = self.lib.vpref_compose(tr.shape[0], _p(tr), _p(out))
+        return rc, out
+
+    def render(self, tr24, m, payload, window, cam, cfg):
+        """volprim::render on a one-frame scene built from PrimitiveTransform records."""
+        tr = _f(tr24).reshape(-1, 24)
+        k9, r9, t3 = cam_arrays(cam)
+        w, h = int(cam.width), int(cam.height)
+        rgb = np.zeros((h, w, 3), np.float32)
+        alpha = np.zeros((h, w, 1), np.float32)
+        samples = np.zeros(h * w, np.int32)
+        rc = self.lib.vpref_render(tr.shape[0], int(m), _p(tr), _p(_f(payload)), float(window.alpha),
+                                   int(window.beta), _p(k9), _p(r9), _p(t3), w, h,
+                                   float(cfg.step_size), float(cfg.early_eps), int(bool(cfg.jitter)),
+                                   int(cfg.seed), int(cfg.accumulation_permutation), _p(rgb),
+                                   _p(alpha), _p(samples, i32p))
+        if rc != 0:
+            raise RuntimeError(f"reference render failed ({rc}): {self.error()}")
+        return rgb, alpha, samples
+
+    def look_at(self, pos, target, up, focal, w, h):
+        k9 = np.zeros(9, np.float32)
+        r9 = np.zeros(9, np.float32)
+        t3 = np.zeros(3, np.float32)
+        aa = np.zeros(3, np.float32)
+        self.lib.vpref_look_at(_p(_f(pos, 3)), _p(_f(target, 3)), _p(_f(up, 3)), float(focal),
+                               int(w), int(h), _p(k9), _p(r9), _p(t3), _p(aa))
+        return k9, r9, t3, aa
+
+    def generate_ray(self, cam, px, py):
+        k9, r9, t3 = cam_arrays(cam)
+        o = np.zeros(3, np.float32)
+        d = np.zeros(3, np.float32)
+        self.lib.vpref_generate_ray(_p(k9), _p(r9), _p(t3), int(cam.width), int(cam.height),
+                                    float(px), float(py), _p(o), _p(d))
+        return o, d
+
+    def intersect(self, xf15, origin, direction):
+        xf = _f(xf15).reshape(-1, 15)
+        k = xf.shape[0]
+        n = C.c_int32()
+        prims = np.zeros(max(k, 1), np.int32)
+        te = np.zeros(max(k, 1), np.float32)
+        tx = np.zeros(max(k, 1), np.float32)
+        tmin = C.c_float()
+        tmax = C.c_float()
+        self.lib.vpref_intersect(k, _p(xf), _p(_f(origin, 3)), _p(_f(direction, 3)), k, C.byref(n),
+                                 _p(prims, i32p), _p(te), _p(tx), C.byref(tmin), C.byref(tmax))
+        return prims[:n.value], te[:n.value], tx[:n.value]
+
+    def march_rays(self, xf15, m, payload, window, origins, dirs, cfg, jitter=None):
+        xf = _f(xf15).reshape(-1, 15)
+        o = _f(origins).reshape(-1, 3)
+        d = _f(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        j = None if jitter is None else _f(jitter).reshape(n)
+        rgb = np.zeros((n, 3), np.float32)
+        alpha = np.zeros(n, np.float32)
+        samples = np.zeros(n, np.int32)
+        rc = self.lib.vpref_march_rays(xf.shape[0], int(m), _p(xf), _p(_f(payload)),
+                                       float(window.alpha), int(window.beta), n, _p(o), _p(d),
+                                       _p(j), float(cfg.step_size), float(cfg.early_eps),
+                                       int(cfg.accumulation_permutation), _p(rgb), _p(alpha),
+                                       _p(samples, i32p))
+        if rc != 0:
+            raise RuntimeError(f"reference march failed ({rc}): {self.error()}")
+        return rgb, alpha, samples
+
+    def window(self, x, y, z, alpha=8.0, beta=8):
+        return self.lib.vpref_window(x, y, z, alpha, beta)

@@ -1,0 +1,226 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// extern "C" glue around the *unmodified* reference volprim core
+// (/root/reference/proj/src/volprim/*.cpp, compiled in place by oracle/Makefile into
+// oracle/_ref/libvolprim_ref.so). It only marshals flat arrays into the reference's own
+// types and calls the reference's own functions, so tests and bench.py's cpu_baseline /
+// --impl reference legs can drive the real reference through ctypes:
+//
+//   vpref_render        -> volprim::render            (march.h:59, march.cpp:95-132)
+//   vpref_compose       -> volprim::compose           (primitive.cpp:41-49)
+//   vpref_look_at       -> volprim::lookAtCamera      (synthetic.cpp:15-38)
+//   vpref_intersect     -> buildLbvh + intersect      (lbvh.cpp:81-156, 207-234)
+//   vpref_march_rays    -> intersect + march          (march.cpp:18-93)
+//   vpref_generate_ray  -> generateRay                (camera.cpp:14-23)
+//   vpref_window        -> window                     (primitive.cpp:25-28)
+//
+// Flat layouts (shared with include/vpb.h):
+//   PrimitiveTransform = 24 floats: tBase[3] rBase[9] (column-major) sBase[3] deltaT[3]
+//                        deltaR[3] deltaS[3]
+//   AffineXf           = 15 floats: t[3] rot[9] (column-major) scale[3]
+//   Camera             = K[9] (column-major), R[9] (column-major), t[3], width, height
+// Return codes: 0 ok, volprim::ErrorCategory value on volprim::Error, 1 on other exceptions.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "volprim/errors.h"
+#include "volprim/lbvh.h"
+#include "volprim/march.h"
+#include "volprim/primitive.h"
+#include "volprim/scene.h"
+#include "volprim/synthetic.h"
+
+using namespace volprim;
+
+namespace {
+
+thread_local std::string g_err;
+
+Vec3 v3(const float *p) { return Vec3(p[0], p[1], p[2]); }
+Mat3 m3(const float *p) {
+    Mat3 m;
+    for (int i = 0; i < 9; ++i) m.m[i] = p[i];
+    return m;
+}
+void put3(float *o, const Vec3 &v) { o[0] = v.x; o[1] = v.y; o[2] = v.z; }
+void put9(float *o, const Mat3 &m) { for (int i = 0; i < 9; ++i) o[i] = m.m[i]; }
+
+PrimitiveTransform transformFrom24(const float *p) {
+    PrimitiveTransform xf;
+    xf.tBase = v3(p + 0);
+    xf.rBase = m3(p + 3);
+    xf.sBase = v3(p + 12);
+    xf.deltaT = v3(p + 15);
+    xf.deltaR = v3(p + 18);
+    xf.deltaS = v3(p + 21);
+    return xf;
+}
+
+AffineXf xfFrom15(const float *p) {
+    AffineXf xf;
+    xf.t = v3(p + 0);
+    xf.rot = m3(p + 3);
+    xf.scale = v3(p + 12);
+    return xf;
+}
+
+Camera cameraFrom(const float *k9, const float *r9, const float *t3, int w, int h) {
+    Camera cam;
+    cam.intrinsics = m3(k9);
+    cam.rotation.matrix = m3(r9); // render() only reads rotation.matrix
+    cam.translation = v3(t3);
+    cam.width = w;
+    cam.height = h;
+    return cam;
+}
+
+template <class F> int guarded(F &&f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error &e) {
+        g_err = e.what();
+        return int(e.category());
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+const char *vpref_last_error() { return g_err.c_str(); }
+
+int vpref_sizeof_real() { return int(sizeof(real)); }
+
+int vpref_compose(int32_t n, const float *tr24, float *xf15) {
+    return guarded([&] {
+        for (int k = 0; k < n; ++k) {
+            const AffineXf xf = compose(transformFrom24(tr24 + 24 * size_t(k)));
+            put3(xf15 + 15 * size_t(k) + 0, xf.t);
+            put9(xf15 + 15 * size_t(k) + 3, xf.rot);
+            put3(xf15 + 15 * size_t(k) + 12, xf.scale);
+        }
+    });
+}
+
+int vpref_render(int32_t nPrim, int32_t m, const float *tr24, const float *payload, float wAlpha,
+                 int32_t wBeta, const float *k9, const float *r9, const float *t3, int32_t width,
+                 int32_t height, float stepSize, float earlyEps, int32_t jitter, uint64_t seed,
+                 uint64_t perm, float *rgb, float *alpha, int32_t *samples) {
+    return guarded([&] {
+        Scene scene;
+        scene.window = WindowParams{wAlpha, wBeta};
+        Frame fr;
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        scene.frames.push_back(std::move(fr));
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        cfg.jitter = jitter != 0;
+        cfg.seed = seed;
+        cfg.accumulationPermutation = perm;
+        const Camera cam = cameraFrom(k9, r9, t3, width, height);
+        const RenderOutput out = render(scene, 0, cam, cfg);
+        std::memcpy(rgb, out.color.data.data(), out.color.data.size() * sizeof(float));
+        std::memcpy(alpha, out.alpha.data.data(), out.alpha.data.size() * sizeof(float));
+        for (size_t i = 0; i < out.sampleCounts.size(); ++i) samples[i] = out.sampleCounts[i];
+    });
+}
+
+int vpref_look_at(const float *pos, const float *target, const float *up, float focalPx,
+                  int32_t width, int32_t height, float *k9, float *r9, float *t3,
+                  float *axisAngle3) {
+    return guarded([&] {
+        const Camera cam = lookAtCamera(v3(pos), v3(target), v3(up), focalPx, width, height);
+        put9(k9, cam.intrinsics);
+        put9(r9, cam.rotation.matrix);
+        put3(t3, cam.translation);
+        put3(axisAngle3, cam.rotation.axisAngle);
+    });
+}
+
+int vpref_generate_ray(const float *k9, const float *r9, const float *t3, int32_t width,
+                       int32_t height, float px, float py, float *origin, float *dir) {
+    return guarded([&] {
+        const Camera cam = cameraFrom(k9, r9, t3, width, height);
+        const Ray ray = generateRay(cam, Vec2(px, py));
+        put3(origin, ray.origin);
+        put3(dir, ray.direction);
+    });
+}
+
+// Segment list of one ray via the reference's LBVH traversal. Writes up to cap entries and
+// returns the total count in *nSeg.
+int vpref_intersect(int32_t nPrim, const float *xf15, const float *origin, const float *dir,
+                    int32_t cap, int32_t *nSeg, int32_t *prims, float *tEnter, float *tExit,
+                    float *tMin, float *tMax) {
+    return guarded([&] {
+        std::vector<AffineXf> xfs;
+        std::vector<Aabb> boxes;
+        for (int k = 0; k < nPrim; ++k) {
+            xfs.push_back(xfFrom15(xf15 + 15 * size_t(k)));
+            boxes.push_back(primitiveAabb(xfs.back()));
+        }
+        Ray ray;
+        ray.origin = v3(origin);
+        ray.direction = v3(dir);
+        const RaySegmentList segs = intersect(buildLbvh(boxes), xfs, ray);
+        *nSeg = int32_t(segs.segments.size());
+        for (int i = 0; i < int(segs.segments.size()) && i < cap; ++i) {
+            prims[i] = segs.segments[i].primitive;
+            tEnter[i] = segs.segments[i].tEnter;
+            tExit[i] = segs.segments[i].tExit;
+        }
+        *tMin = segs.tMin;
+        *tMax = segs.tMax;
+    });
+}
+
+// march() over arbitrary rays (the reference's lower-level entry point, march.h:42-44).
+int vpref_march_rays(int32_t nPrim, int32_t m, const float *xf15, const float *payload,
+                     float wAlpha, int32_t wBeta, int64_t nRays, const float *origins,
+                     const float *dirs, const float *jitter01, float stepSize, float earlyEps,
+                     uint64_t perm, float *rgb, float *alpha, int32_t *samples) {
+    return guarded([&] {
+        std::vector<AffineXf> xfs;
+        std::vector<Aabb> boxes;
+        for (int k = 0; k < nPrim; ++k) {
+            xfs.push_back(xfFrom15(xf15 + 15 * size_t(k)));
+            boxes.push_back(primitiveAabb(xfs.back()));
+        }
+        PrimitiveSlab slab;
+        slab.resize(nPrim, m);
+        std::memcpy(slab.payload.data(), payload, slab.payload.size() * sizeof(float));
+        const Lbvh bvh = buildLbvh(boxes);
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        cfg.accumulationPermutation = perm;
+        const WindowParams w{wAlpha, wBeta};
+        for (int64_t r = 0; r < nRays; ++r) {
+            Ray ray;
+            ray.origin = v3(origins + 3 * r);
+            ray.direction = v3(dirs + 3 * r);
+            const RaySegmentList segs = intersect(bvh, xfs, ray);
+            const MarchResult mr =
+                march(ray, segs, slab, xfs, w, cfg, jitter01 ? jitter01[r] : real(0.5));
+            put3(rgb + 3 * r, mr.rgb);
+            alpha[r] = mr.alpha;
+            samples[r] = mr.samples;
+        }
+    });
+}
+
+float vpref_window(float x, float y, float z, float wAlpha, int32_t wBeta) {
+    return window(Vec3(x, y, z), WindowParams{wAlpha, wBeta});
+}
+
+} // extern "C"

@@ -1,0 +1,599 @@
+/* TEST INFRASTRUCTURE — the CPU parity oracle. NOT PRODUCT CODE. See vp_oracle.h.
+ *
+ * Arithmetic contract: binary32 with no contraction (built with -ffp-contract=off, like the
+ * reference objects, which contain no vfmadd), the same operation order as the reference's
+ * Vec3/Mat3 operators (math.h:36-160), libm expf/sinf/cosf/sqrtf/floorf/ceil. */
+#include "vp_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct { float x, y, z; } v3;
+
+static v3 mk(float x, float y, float z) { v3 r = {x, y, z}; return r; }
+static v3 add3(v3 a, v3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+static v3 sub3(v3 a, v3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+static v3 scl3(v3 a, float s) { return mk(a.x * s, a.y * s, a.z * s); }
+static v3 div3(v3 a, float s) { return mk(a.x / s, a.y / s, a.z / s); }
+static v3 cdiv3(v3 a, v3 b) { return mk(a.x / b.x, a.y / b.y, a.z / b.z); }
+static float dot3(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static float comp(v3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+static v3 ld3(const float *p) { return mk(p[0], p[1], p[2]); }
+
+/* math.h:122-124: col(0)*v.x + col(1)*v.y + col(2)*v.z, column-major m[9]. */
+static v3 matvec(const float *m, v3 v) {
+    return add3(add3(scl3(mk(m[0], m[1], m[2]), v.x), scl3(mk(m[3], m[4], m[5]), v.y)),
+                scl3(mk(m[6], m[7], m[8]), v.z));
+}
+/* transpose() then operator*(Vec3): column j of R^T is row j of R. */
+static v3 matTvec(const float *m, v3 v) {
+    return add3(add3(scl3(mk(m[0], m[3], m[6]), v.x), scl3(mk(m[1], m[4], m[7]), v.y)),
+                scl3(mk(m[2], m[5], m[8]), v.z));
+}
+/* math.h:115-121: r(i,c) += a(i,k) * o(k,c), k outer-middle, starting from zero. */
+static void matmul(const float *a, const float *o, float *r) {
+    float t[9];
+    for (int i = 0; i < 9; ++i) t[i] = 0;
+    for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < 3; ++k)
+            for (int i = 0; i < 3; ++i) t[c * 3 + i] += a[k * 3 + i] * o[c * 3 + k];
+    memcpy(r, t, sizeof t);
+}
+
+/* math.h:141-160 */
+static void matinv(const float *m, float *r) {
+    const float d = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[3] * (m[1] * m[8] - m[2] * m[7]) +
+                    m[6] * (m[1] * m[5] - m[2] * m[4]);
+#define A(i, j) m[(j) * 3 + (i)]
+#define R(i, j) t[(j) * 3 + (i)]
+    float t[9];
+    R(0, 0) = A(1, 1) * A(2, 2) - A(1, 2) * A(2, 1);
+    R(0, 1) = A(0, 2) * A(2, 1) - A(0, 1) * A(2, 2);
+    R(0, 2) = A(0, 1) * A(1, 2) - A(0, 2) * A(1, 1);
+    R(1, 0) = A(1, 2) * A(2, 0) - A(1, 0) * A(2, 2);
+    R(1, 1) = A(0, 0) * A(2, 2) - A(0, 2) * A(2, 0);
+    R(1, 2) = A(0, 2) * A(1, 0) - A(0, 0) * A(1, 2);
+    R(2, 0) = A(1, 0) * A(2, 1) - A(1, 1) * A(2, 0);
+    R(2, 1) = A(0, 1) * A(2, 0) - A(0, 0) * A(2, 1);
+    R(2, 2) = A(0, 0) * A(1, 1) - A(0, 1) * A(1, 0);
+#undef A
+#undef R
+    const float s = 1.0f / d;
+    for (int i = 0; i < 9; ++i) r[i] = t[i] * s;
+}
+
+/* rotation.cpp:8-28 (Rodrigues, series branch below 1e-4) */
+static void rotation_from_axis_angle(v3 v, float *out) {
+    static const float I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    const float t2 = dot3(v, v);
+    if (t2 == 0) {
+        memcpy(out, I, sizeof I);
+        return;
+    }
+    const float theta = sqrtf(t2);
+    float a, b;
+    if (theta < 1e-4f) {
+        a = 1 - t2 / 6;
+        b = 0.5f - t2 / 24;
+    } else {
+        a = sinf(theta) / theta;
+        b = (1 - cosf(theta)) / t2;
+    }
+    float k[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, kk[9];
+    k[3] = -v.z; /* (0,1) */
+    k[6] = v.y;  /* (0,2) */
+    k[1] = v.z;  /* (1,0) */
+    k[7] = -v.x; /* (1,2) */
+    k[2] = -v.y; /* (2,0) */
+    k[5] = v.x;  /* (2,1) */
+    matmul(k, k, kk);
+    for (int i = 0; i < 9; ++i) out[i] = (I[i] + k[i] * a) + kk[i] * b;
+}
+
+int vpo_compose(int32_t n, const float *tr24, float *xf15) {
+    for (int32_t k = 0; k < n; ++k) {
+        const float *p = tr24 + 24 * (size_t)k;
+        float *o = xf15 + 15 * (size_t)k;
+        const v3 s = add3(ld3(p + 12), ld3(p + 21));
+        if (s.x <= 0 || s.y <= 0 || s.z <= 0) return 2;
+        float r[9];
+        rotation_from_axis_angle(ld3(p + 18), r);
+        const v3 t = add3(ld3(p + 0), ld3(p + 15));
+        o[0] = t.x; o[1] = t.y; o[2] = t.z;
+        matmul(r, p + 3, o + 3);
+        o[12] = s.x; o[13] = s.y; o[14] = s.z;
+    }
+    return 0;
+}
+
+/* camera.cpp:14-23, camera.h:28 */
+void vpo_generate_ray(const float *k9, const float *r9, const float *t3, float px, float py,
+                      float *origin, float *dir) {
+    float kinv[9];
+    matinv(k9, kinv);
+    const v3 dirCam = matvec(kinv, mk(px, py, 1));
+    const v3 c = matTvec(r9, ld3(t3));
+    const v3 d = matTvec(r9, dirCam);
+    const v3 n = div3(d, sqrtf(dot3(d, d)));
+    origin[0] = -c.x; origin[1] = -c.y; origin[2] = -c.z;
+    dir[0] = n.x; dir[1] = n.y; dir[2] = n.z;
+}
+
+/* primitive.h:61-63: (R^T (p - t)) ./ s */
+static v3 to_model(const float *xf, v3 p) {
+    return cdiv3(matTvec(xf + 3, sub3(p, ld3(xf))), ld3(xf + 12));
+}
+
+int vpo_intersect_obb(const float *xf, const float *op, const float *dp, float *tEnterOut,
+                      float *tExitOut) {
+    const v3 om = to_model(xf, ld3(op));
+    const v3 dm = cdiv3(matTvec(xf + 3, ld3(dp)), ld3(xf + 12));
+    float tEnter = -FLT_MAX, tExit = FLT_MAX;
+    for (int a = 0; a < 3; ++a) {
+        const float oa = comp(om, a), da = comp(dm, a);
+        if (da == 0) {
+            if (oa < -1 || oa > 1) return 0;
+            continue;
+        }
+        const float inv = 1 / da;
+        const float cNear = da > 0 ? -1.0f : 1.0f;
+        const float t1 = (cNear - oa) * inv;
+        const float t2 = (-cNear - oa) * inv;
+        if (t1 > tEnter) tEnter = t1;
+        tExit = t2 < tExit ? t2 : tExit; /* std::min(tExit, t2) */
+    }
+    if (tEnter < 0) tEnter = 0;
+    if (tEnter >= tExit || tExit <= 0) return 0;
+    *tEnterOut = tEnter;
+    *tExitOut = tExit;
+    return 1;
+}
+
+typedef struct { int32_t prim; float tEnter, tExit; } seg_t;
+
+static int seg_less(const seg_t *a, const seg_t *b) {
+    return a->tEnter != b->tEnter ? a->tEnter < b->tEnter : a->prim < b->prim;
+}
+
+/* Insertion sort by (tEnter, prim): the comparator of lbvh.cpp:225-227 (a total order, so
+ * any correct sort gives the same list). */
+static void sort_segs(seg_t *s, int n) {
+    for (int i = 1; i < n; ++i) {
+        seg_t x = s[i];
+        int j = i;
+        while (j > 0 && seg_less(&x, &s[j - 1])) {
+            s[j] = s[j - 1];
+            --j;
+        }
+        s[j] = x;
+    }
+}
+
+static int collect(int32_t n_prim, const float *xf15, v3 o, v3 d, seg_t *out) {
+    int n = 0;
+    const float op[3] = {o.x, o.y, o.z}, dp[3] = {d.x, d.y, d.z};
+    for (int32_t k = 0; k < n_prim; ++k) {
+        float te, tx;
+        if (vpo_intersect_obb(xf15 + 15 * (size_t)k, op, dp, &te, &tx)) {
+            out[n].prim = k;
+            out[n].tEnter = te;
+            out[n].tExit = tx;
+            ++n;
+        }
+    }
+    sort_segs(out, n);
+    return n;
+}
+
+int32_t vpo_intersect(int32_t n_prim, const float *xf15, const float *o, const float *d,
+                      int32_t cap, int32_t *prims, float *tEnter, float *tExit) {
+    seg_t *s = (seg_t *)malloc(sizeof(seg_t) * (size_t)(n_prim > 0 ? n_prim : 1));
+    const int n = collect(n_prim, xf15, ld3(o), ld3(d), s);
+    for (int i = 0; i < n && i < cap; ++i) {
+        prims[i] = s[i].prim;
+        tEnter[i] = s[i].tEnter;
+        tExit[i] = s[i].tExit;
+    }
+    free(s);
+    return n;
+}
+
+/* primitive.cpp:12-22 */
+static float pow_even(float x, int beta) {
+    float r = 1, b = fabsf(x);
+    int e = beta;
+    while (e > 0) {
+        if (e & 1) r *= b;
+        b *= b;
+        e >>= 1;
+    }
+    return r;
+}
+
+float vpo_window(float x, float y, float z, float alpha, int32_t beta) {
+    if (alpha == 0) return 1;
+    return expf(-alpha * (pow_even(x, beta) + pow_even(y, beta) + pow_even(z, beta)));
+}
+
+/* primitive.cpp:51-69 */
+typedef struct { int lo[3]; float frac[3]; } stencil_t;
+static stencil_t trilinear_stencil(int m, v3 p) {
+    stencil_t st;
+    for (int a = 0; a < 3; ++a) {
+        float u = (comp(p, a) + 1) * 0.5f * (float)m - 0.5f;
+        if (u <= 0) u = 0;
+        else if (u >= (float)(m - 1)) u = (float)(m - 1);
+        int i0 = (int)floorf(u);
+        if (i0 > m - 2) i0 = (m - 2) > 0 ? (m - 2) : 0;
+        st.lo[a] = i0;
+        st.frac[a] = m > 1 ? u - (float)i0 : 0;
+    }
+    return st;
+}
+
+/* primitive.cpp:71-90 (cornerWeight + gatherChannel) on the planar slab, primitive.h:36-39 */
+static float gather_channel(const float *payload, int m, int k, int ch, const stencil_t *st) {
+    float acc = 0;
+    for (int cz = 0; cz < 2; ++cz)
+        for (int cy = 0; cy < 2; ++cy)
+            for (int cx = 0; cx < 2; ++cx) {
+                const int z = st->lo[2] + cz < m - 1 ? st->lo[2] + cz : m - 1;
+                const int y = st->lo[1] + cy < m - 1 ? st->lo[1] + cy : m - 1;
+                const int x = st->lo[0] + cx < m - 1 ? st->lo[0] + cx : m - 1;
+                const float wx = cx ? st->frac[0] : 1 - st->frac[0];
+                const float wy = cy ? st->frac[1] : 1 - st->frac[1];
+                const float wz = cz ? st->frac[2] : 1 - st->frac[2];
+                const size_t mm = (size_t)m;
+                const size_t idx = ((((size_t)k * 4 + ch) * mm + z) * mm + y) * mm + x;
+                acc += wx * wy * wz * payload[idx];
+            }
+    return acc;
+}
+
+static float clampc(float v) {
+    /* cwiseMax(Vec3(-1), cwiseMin(Vec3(1), p)) with std::min/std::max semantics */
+    const float lo = v < 1 ? v : 1;
+    return -1 < lo ? lo : -1;
+}
+
+static uint64_t hash_combine(uint64_t seed, uint64_t value) { /* math.h:170-175 */
+    uint64_t z = seed + 0x9e3779b97f4a7c15ull + value;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+static float hash_to_unit(uint64_t h) { /* math.h:177-179 */
+    return (float)(h >> 11) * (float)(1.0 / 9007199254740992.0);
+}
+
+typedef struct {
+    int32_t n_prim, m;
+    const float *xf15, *payload;
+    float w_alpha;
+    int32_t w_beta;
+    float step, early_eps;
+    uint64_t perm;
+} march_ctx;
+
+/* march.cpp:18-93 */
+static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSegs, int *active,
+                      float jitter01, float *rgb, float *alpha, int32_t *samples) {
+    float color[3] = {0, 0, 0};
+    float transmittance = 0;
+    int nsamp = 0;
+    if (nSegs > 0) {
+        const float dt = c->step;
+        const float t0 = segs[0].tEnter;
+        float tMax = 0;
+        for (int s = 0; s < nSegs; ++s) tMax = tMax < segs[s].tExit ? segs[s].tExit : tMax;
+        int nActive = 0, next = 0;
+        for (int64_t i = 0;; ++i) {
+            const float ts = t0 + ((float)i + jitter01) * dt;
+            if (ts >= tMax) break;
+            while (next < nSegs && segs[next].tEnter <= ts) active[nActive++] = next++;
+            int w = 0;
+            for (int a = 0; a < nActive; ++a)
+                if (!(segs[active[a]].tExit <= ts)) active[w++] = active[a];
+            nActive = w;
+            if (nActive == 0) {
+                if (next >= nSegs) break;
+                const float tNext = segs[next].tEnter;
+                const int64_t skipTo = (int64_t)ceil((double)((tNext - t0) / dt) - (double)jitter01);
+                if (skipTo > i + 1) i = skipTo - 1;
+                continue;
+            }
+            if (c->perm != 0) {
+                for (size_t a = (size_t)nActive; a > 1; --a) {
+                    const uint64_t h = hash_combine(c->perm, (uint64_t)i * 1315423911u + a);
+                    const int j = (int)(h % a);
+                    const int tmp = active[a - 1];
+                    active[a - 1] = active[j];
+                    active[j] = tmp;
+                }
+            }
+            const v3 pw = add3(o, scl3(d, ts));
+            float sigmaSum = 0;
+            float rw[3] = {0, 0, 0};
+            for (int a = 0; a < nActive; ++a) {
+                const int k = segs[active[a]].prim;
+                const v3 q = to_model(c->xf15 + 15 * (size_t)k, pw);
+                const v3 pm = mk(clampc(q.x), clampc(q.y), clampc(q.z));
+                const stencil_t st = trilinear_stencil(c->m, pm);
+                const float sigma = gather_channel(c->payload, c->m, k, 3, &st) *
+                                    vpo_window(pm.x, pm.y, pm.z, c->w_alpha, c->w_beta);
+                sigmaSum += sigma;
+                const float r0 = gather_channel(c->payload, c->m, k, 0, &st);
+                const float r1 = gather_channel(c->payload, c->m, k, 1, &st);
+                const float r2 = gather_channel(c->payload, c->m, k, 2, &st);
+                rw[0] += r0 * sigma;
+                rw[1] += r1 * sigma;
+                rw[2] += r2 * sigma;
+            }
+            ++nsamp;
+            const float dT = sigmaSum * dt;
+            if (transmittance + dT >= 1) {
+                const float frac = (1 - transmittance) / dT;
+                const float f = dt * frac;
+                for (int ch = 0; ch < 3; ++ch) color[ch] += rw[ch] * f;
+                transmittance = 1;
+                break;
+            }
+            for (int ch = 0; ch < 3; ++ch) color[ch] += rw[ch] * dt;
+            transmittance += dT;
+            if (transmittance > 1 - c->early_eps) break;
+        }
+    }
+    rgb[0] = color[0];
+    rgb[1] = color[1];
+    rgb[2] = color[2];
+    *alpha = transmittance;
+    *samples = nsamp;
+}
+
+int vpo_march_rays(int32_t n_prim, int32_t m, const float *xf15, const float *payload,
+                   float w_alpha, int32_t w_beta, int64_t n_rays, const float *origins,
+                   const float *dirs, const float *jitter01, float step, float early_eps,
+                   uint64_t perm, float *rgb, float *alpha, int32_t *samples) {
+    const march_ctx c = {n_prim, m, xf15, payload, w_alpha, w_beta, step, early_eps, perm};
+    const size_t cap = (size_t)(n_prim > 0 ? n_prim : 1);
+    seg_t *segs = (seg_t *)malloc(sizeof(seg_t) * cap);
+    int *active = (int *)malloc(sizeof(int) * cap);
+    for (int64_t r = 0; r < n_rays; ++r) {
+        const v3 o = ld3(origins + 3 * r), d = ld3(dirs + 3 * r);
+        const int n = collect(n_prim, xf15, o, d, segs);
+        march_one(&c, o, d, segs, n, active, jitter01 ? jitter01[r] : 0.5f, rgb + 3 * r,
+                  alpha + r, samples + r);
+    }
+    free(segs);
+    free(active);
+    return 0;
+}
+
+typedef struct {
+    const march_ctx *c;
+    const float *k9, *r9, *t3;
+    int32_t width, height, jitter;
+    uint64_t seed;
+    int64_t y0, y1;
+    float *rgb, *alpha;
+    int32_t *samples;
+} render_job;
+
+static void *render_rows(void *arg) {
+    const render_job *j = (const render_job *)arg;
+    const size_t cap = (size_t)(j->c->n_prim > 0 ? j->c->n_prim : 1);
+    seg_t *segs = (seg_t *)malloc(sizeof(seg_t) * cap);
+    int *active = (int *)malloc(sizeof(int) * cap);
+    for (int64_t y = j->y0; y < j->y1; ++y)
+        for (int x = 0; x < j->width; ++x) {
+            const int pixelId = (int)y * j->width + x;
+            float o[3], d[3];
+            vpo_generate_ray(j->k9, j->r9, j->t3, (float)x + 0.5f, (float)y + 0.5f, o, d);
+            const int n = collect(j->c->n_prim, j->c->xf15, ld3(o), ld3(d), segs);
+            const float jit = j->jitter ? hash_to_unit(hash_combine(j->seed, (uint64_t)pixelId)) : 0.5f;
+            march_one(j->c, ld3(o), ld3(d), segs, n, active, jit, j->rgb + 3 * (size_t)pixelId,
+                      j->alpha + pixelId, j->samples + pixelId);
+        }
+    free(segs);
+    free(active);
+    return NULL;
+}
+
+int vpo_render(int32_t n_prim, int32_t m, const float *xf15, const float *payload, float w_alpha,
+               int32_t w_beta, const float *k9, const float *r9, const float *t3, int32_t width,
+               int32_t height, float step, float early_eps, int32_t jitter, uint64_t seed,
+               uint64_t perm, float *rgb, float *alpha, int32_t *samples, int32_t n_threads) {
+    const size_t np = (size_t)width * (size_t)height;
+    memset(rgb, 0, np * 3 * sizeof(float));
+    memset(alpha, 0, np * sizeof(float));
+    memset(samples, 0, np * sizeof(int32_t));
+    if (n_prim == 0 || np == 0) return 0; /* march.cpp:108 */
+    const march_ctx c = {n_prim, m, xf15, payload, w_alpha, w_beta, step, early_eps, perm};
+    if (n_threads <= 1) n_threads = 1;
+    if (n_threads > height) n_threads = height;
+    pthread_t th[256];
+    render_job jobs[256];
+    if (n_threads > 256) n_threads = 256;
+    const int64_t chunk = (height + n_threads - 1) / n_threads;
+    int started = 0;
+    for (int w = 0; w < n_threads; ++w) {
+        render_job j = {&c, k9, r9, t3, width, height, jitter, seed, w * chunk,
+                        (w + 1) * chunk < height ? (w + 1) * chunk : height, rgb, alpha, samples};
+        if (j.y0 >= j.y1) break;
+        jobs[w] = j;
+        pthread_create(&th[w], NULL, render_rows, &jobs[w]);
+        ++started;
+    }
+    for (int w = 0; w < started; ++w) pthread_join(th[w], NULL);
+    return 0;
+}
+
+void vpo_composite(int32_t width, int32_t height, const float *rgb, const float *alpha,
+                   const float *bg, float *out) {
+    for (int64_t p = 0; p < (int64_t)width * height; ++p) {
+        const float a = alpha[p];
+        for (int ch = 0; ch < 3; ++ch) out[3 * p + ch] = a * rgb[3 * p + ch] + (1 - a) * bg[3 * p + ch];
+    }
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Tile binning restatement (no reference counterpart; replaces lbvh.cpp:13-156).
+ * Identical float operation sequence to k_cull in paper_2103_01954_b200/csrc/vpb_kernels.cu.
+ */
+static void cull_one(const float *xf, const float *k9, const float *r9, const float *t3,
+                     int32_t width, int32_t height, int32_t *rect, uint32_t *key) {
+    const v3 s = ld3(xf + 12);
+    const float r = sqrtf(dot3(s, s));
+    const float rr = r * 1.001f + 1e-6f;
+    const v3 cc = add3(matvec(r9, ld3(xf)), ld3(t3));
+    const float dist = sqrtf(dot3(cc, cc));
+    float depth = dist - rr;
+    if (!(depth > 0)) depth = 0;
+    uint32_t kb;
+    memcpy(&kb, &depth, 4);
+    *key = kb;
+    const int32_t tiles_x = (width + VPO_TILE - 1) / VPO_TILE;
+    const int32_t tiles_y = (height + VPO_TILE - 1) / VPO_TILE;
+    rect[0] = 0; rect[1] = 0; rect[2] = -1; rect[3] = -1;
+    if (width <= 0 || height <= 0) return;
+    if (cc.z + rr < 0) return; /* entirely behind the camera plane */
+    if (cc.z - rr <= 1e-3f * rr) { /* straddles or hugs the camera plane: every tile */
+        rect[2] = tiles_x - 1;
+        rect[3] = tiles_y - 1;
+        return;
+    }
+    float umin = FLT_MAX, umax = -FLT_MAX, vmin = FLT_MAX, vmax = -FLT_MAX;
+    for (int c = 0; c < 8; ++c) {
+        const v3 corner = mk(c & 1 ? 1.0f : -1.0f, c & 2 ? 1.0f : -1.0f, c & 4 ? 1.0f : -1.0f);
+        const v3 pw = add3(ld3(xf), matvec(xf + 3, mk(s.x * corner.x, s.y * corner.y, s.z * corner.z)));
+        const v3 pc = add3(matvec(r9, pw), ld3(t3));
+        const v3 hp = matvec(k9, pc);
+        const float u = hp.x / hp.z, v = hp.y / hp.z;
+        umin = u < umin ? u : umin;
+        umax = u > umax ? u : umax;
+        vmin = v < vmin ? v : vmin;
+        vmax = v > vmax ? v : vmax;
+    }
+    const float mu = 2.0f + 1e-3f * (fabsf(umin) + fabsf(umax));
+    const float mv = 2.0f + 1e-3f * (fabsf(vmin) + fabsf(vmax));
+    float x0 = floorf(umin - mu), x1 = floorf(umax + mu);
+    float y0 = floorf(vmin - mv), y1 = floorf(vmax + mv);
+    const float wl = (float)(width - 1), hl = (float)(height - 1);
+    if (!(x1 >= 0) || !(x0 <= wl) || !(y1 >= 0) || !(y0 <= hl)) return;
+    x0 = x0 > 0 ? x0 : 0;
+    y0 = y0 > 0 ? y0 : 0;
+    x1 = x1 < wl ? x1 : wl;
+    y1 = y1 < hl ? y1 : hl;
+    rect[0] = (int32_t)x0 / VPO_TILE;
+    rect[1] = (int32_t)y0 / VPO_TILE;
+    rect[2] = (int32_t)x1 / VPO_TILE;
+    rect[3] = (int32_t)y1 / VPO_TILE;
+}
+
+void vpo_cull(int32_t n_prim, const float *xf15, const float *k9, const float *r9,
+              const float *t3, int32_t width, int32_t height, int32_t *rect4,
+              uint32_t *depth_key) {
+    for (int32_t k = 0; k < n_prim; ++k)
+        cull_one(xf15 + 15 * (size_t)k, k9, r9, t3, width, height, rect4 + 4 * (size_t)k,
+                 depth_key + k);
+}
+
+static int cmp_u64(const void *a, const void *b) {
+    const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+int64_t vpo_tile_lists(int32_t n_prim, const float *xf15, const float *k9, const float *r9,
+                       const float *t3, int32_t width, int32_t height, int32_t *tile_offsets,
+                       int32_t *tile_prims, int64_t cap) {
+    const int32_t tiles_x = (width + VPO_TILE - 1) / VPO_TILE;
+    const int32_t tiles_y = (height + VPO_TILE - 1) / VPO_TILE;
+    const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
+    int32_t *rect = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)(n_prim > 0 ? n_prim : 1));
+    uint32_t *key = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(n_prim > 0 ? n_prim : 1));
+    vpo_cull(n_prim, xf15, k9, r9, t3, width, height, rect, key);
+    int64_t *count = (int64_t *)calloc((size_t)(n_tiles + 1), sizeof(int64_t));
+    for (int32_t k = 0; k < n_prim; ++k)
+        for (int32_t ty = rect[4 * k + 1]; ty <= rect[4 * k + 3]; ++ty)
+            for (int32_t tx = rect[4 * k + 0]; tx <= rect[4 * k + 2]; ++tx)
+                count[(int64_t)ty * tiles_x + tx]++;
+    int64_t total = 0;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        tile_offsets[t] = (int32_t)total;
+        total += count[t];
+    }
+    tile_offsets[n_tiles] = (int32_t)total;
+    uint64_t *ent = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(total > 0 ? total : 1));
+    int64_t *cur = (int64_t *)calloc((size_t)(n_tiles + 1), sizeof(int64_t));
+    for (int32_t k = 0; k < n_prim; ++k)
+        for (int32_t ty = rect[4 * k + 1]; ty <= rect[4 * k + 3]; ++ty)
+            for (int32_t tx = rect[4 * k + 0]; tx <= rect[4 * k + 2]; ++tx) {
+                const int64_t t = (int64_t)ty * tiles_x + tx;
+                ent[tile_offsets[t] + cur[t]++] = ((uint64_t)key[k] << 32) | (uint32_t)k;
+            }
+    for (int64_t t = 0; t < n_tiles; ++t)
+        qsort(ent + tile_offsets[t], (size_t)count[t], sizeof(uint64_t), cmp_u64);
+    for (int64_t i = 0; i < total && i < cap; ++i) tile_prims[i] = (int32_t)(ent[i] & 0xffffffffu);
+    free(rect);
+    free(key);
+    free(count);
+    free(ent);
+    free(cur);
+    return total;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * C port of glibc 2.39 expf (sysdeps/ieee754/flt-32/e_expf.c, the ARM optimized-routines
+ * algorithm: 32-entry 2^(i/32) table, cubic in double) as ported to the device in
+ * paper_2103_01954_b200/csrc/vpb_device.cuh. Tests compare it with libm expf. */
+static const uint64_t kExp2fTab[32] = {
+    0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
+    0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
+    0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
+    0x3feebfdad5362a27ULL, 0x3feeb42b569d4f82ULL, 0x3feeab07dd485429ULL, 0x3feea47eb03a5585ULL,
+    0x3feea09e667f3bcdULL, 0x3fee9f75e8ec5f74ULL, 0x3feea11473eb0187ULL, 0x3feea589994cce13ULL,
+    0x3feeace5422aa0dbULL, 0x3feeb737b0cdc5e5ULL, 0x3feec49182a3f090ULL, 0x3feed503b23e255dULL,
+    0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
+    0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
+
+float vpo_expf_port(float x) {
+    if (x != x) return x + x;
+    if (x < -0x1.9fe368p6f) return 0.0f;
+    if (x > 0x1.62e42ep6f) return INFINITY;
+    if (x == -0x1.f8cbb2p+5f) return 0x1.f45326p-92f; /* the two inputs where glibc 2.39 */
+    if (x == 0x1.04845ep+5f) return 0x1.f93e38p+46f;  /* differs from the bare algorithm */
+    const double InvLn2N = 0x1.71547652b82fep+0 * 32, Shift = 0x1.8p+52;
+    const double C0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32, C1 = 0x1.ebfce50fac4f3p-3 / 32 / 32,
+                 C2 = 0x1.62e42ff0c52d6p-1 / 32;
+    const double z = InvLn2N * (double)x;
+    double kd = z + Shift;
+    uint64_t ki;
+    memcpy(&ki, &kd, 8);
+    kd -= Shift;
+    const double r = z - kd;
+    uint64_t t = kExp2fTab[ki % 32] + (ki << 47);
+    double s;
+    memcpy(&s, &t, 8);
+    const double zz = fma(C0, r, C1);
+    const double r2 = r * r;
+    double y = fma(C2, r, 1.0);
+    y = fma(zz, r2, y);
+    return (float)(y * s);
+}
+
+/* Counts inputs in [lo_bits, hi_bits] (float bit patterns, walked upward) whose value in
+ * `values` differs bitwise from libm expf. values[i] corresponds to lo_bits + i. */
+int64_t vpo_expf_mismatches(uint32_t lo_bits, uint32_t hi_bits, const float *values) {
+    int64_t bad = 0;
+    for (uint64_t u = lo_bits; u <= hi_bits; ++u) {
+        float x, e;
+        const uint32_t b = (uint32_t)u;
+        memcpy(&x, &b, 4);
+        e = expf(x);
+        if (memcmp(&e, &values[u - lo_bits], 4) != 0) ++bad;
+    }
+    return bad;
+}

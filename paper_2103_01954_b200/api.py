@@ -1,0 +1,348 @@
+"""Python mirror of the reference renderer interface (volprim::render and friends).
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/src/volprim/{march.h,scene.h,primitive.h,camera.h,errors.h}:
+
+    render(scene, frame, cam, cfg) -> RenderOutput          march.h:59 / march.cpp:95-132
+    composite(out, background) -> image                      march.h:62 / march.cpp:134-147
+    compose(transforms) -> AffineXf records                  primitive.cpp:41-49
+    Error(category, message), ErrorCategory                  errors.h:11-38
+
+All compute runs through libvpb.so (include/vpb.h) on an sm_100a GPU; there is no CPU path.
+Arrays are numpy float32; matrices are 3x3 arrays in (row, col) indexing and are passed to
+the C-ABI column-major, like volprim::Mat3::m.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import f32p, i32p, u32p, vp_camera, vp_march, vp_stats
+
+
+class ErrorCategory(enum.IntEnum):
+    """errors.h:11-17, plus DEVICE for CUDA failures (no reference counterpart)."""
+    USAGE = 2
+    IO = 3
+    FORMAT = 4
+    VERSION = 5
+    NUMERIC = 6
+    DEVICE = 7
+
+
+class Error(RuntimeError):
+    """volprim::Error: a message plus a category whose value is the CLI exit code."""
+
+    def __init__(self, category: int, message: str):
+        super().__init__(message)
+        try:
+            self.category = ErrorCategory(category)
+        except ValueError:
+            self.category = ErrorCategory.DEVICE
+        self.exit_code = int(self.category)
+
+
+def _check(rc: int, ctx=None):
+    if rc != 0:
+        lib = _lib.load()
+        msg = lib.vp_last_error(ctx)
+        raise Error(rc, msg.decode() if msg else f"libvpb error {rc}")
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(f32p)
+
+
+def _f32(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    if shape is not None:
+        out = out.reshape(shape)
+    return out
+
+
+# ----------------------------------------------------------------------------------------
+# Scene model (primitive.h, scene.h, march.h, camera.h)
+
+@dataclass
+class WindowParams:
+    """primitive.h:14-17"""
+    alpha: float = 8.0
+    beta: int = 8
+
+
+@dataclass
+class MarchConfig:
+    """march.h:11-20"""
+    step_size: float = 0.001
+    early_eps: float = 0.01
+    jitter: bool = False
+    seed: int = 0
+    accumulation_permutation: int = 0
+
+    def to_c(self) -> vp_march:
+        return vp_march(float(self.step_size), float(self.early_eps), 1 if self.jitter else 0, 0,
+                        int(self.seed) & (2**64 - 1), int(self.accumulation_permutation) & (2**64 - 1))
+
+
+def transform_records(t_base, r_base, s_base, delta_t=None, delta_r=None, delta_s=None) -> np.ndarray:
+    """Packs PrimitiveTransform fields (primitive.h:45-52) into K x 24 float32 records:
+    tBase[3] rBase[9] (column-major) sBase[3] deltaT[3] deltaR[3] deltaS[3]."""
+    t_base = _f32(t_base).reshape(-1, 3)
+    k = t_base.shape[0]
+    r_base = _f32(r_base).reshape(k, 3, 3)
+    rec = np.zeros((k, 24), np.float32)
+    rec[:, 0:3] = t_base
+    rec[:, 3:12] = np.transpose(r_base, (0, 2, 1)).reshape(k, 9)  # column-major
+    rec[:, 12:15] = _f32(s_base).reshape(k, 3)
+    for off, arr in ((15, delta_t), (18, delta_r), (21, delta_s)):
+        if arr is not None:
+            rec[:, off:off + 3] = _f32(arr).reshape(k, 3)
+    return rec
+
+
+@dataclass
+class PrimitiveSlab:
+    """primitive.h:25-41: planar payload (k, channel, z, y, x)."""
+    num_primitives: int = 0
+    voxels_per_axis: int = 0
+    payload: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+    @staticmethod
+    def zeros(n_prim: int, m: int) -> "PrimitiveSlab":
+        return PrimitiveSlab(n_prim, m, np.zeros(n_prim * 4 * m ** 3, np.float32))
+
+    def index(self, k: int, channel: int, z: int, y: int, x: int) -> int:
+        m = self.voxels_per_axis
+        return (((k * 4 + channel) * m + z) * m + y) * m + x
+
+    def view(self) -> np.ndarray:
+        m = self.voxels_per_axis
+        return self.payload.reshape(self.num_primitives, 4, m, m, m)
+
+
+@dataclass
+class Frame:
+    """scene.h:14-28. transforms: K x 24 PrimitiveTransform records (transform_records)."""
+    transforms: np.ndarray = field(default_factory=lambda: np.zeros((0, 24), np.float32))
+    slab: PrimitiveSlab = field(default_factory=PrimitiveSlab)
+
+    def composed(self) -> np.ndarray:
+        return compose(self.transforms)
+
+
+@dataclass
+class Scene:
+    """scene.h:30-34 (the guide mesh is not read by render())."""
+    window: WindowParams = field(default_factory=WindowParams)
+    march: MarchConfig = field(default_factory=MarchConfig)
+    frames: List[Frame] = field(default_factory=list)
+
+
+@dataclass
+class Camera:
+    """camera.h:21-29: x_cam = R x_world + t, pixel = K x_cam / z."""
+    intrinsics: np.ndarray = field(default_factory=lambda: np.eye(3, dtype=np.float32))
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3, dtype=np.float32))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3, np.float32))
+    width: int = 0
+    height: int = 0
+
+    def to_c(self) -> vp_camera:
+        c = vp_camera()
+        c.K[:] = _f32(self.intrinsics).reshape(3, 3).T.reshape(-1).tolist()
+        c.R[:] = _f32(self.rotation).reshape(3, 3).T.reshape(-1).tolist()
+        c.t[:] = _f32(self.translation).reshape(3).tolist()
+        c.width = int(self.width)
+        c.height = int(self.height)
+        return c
+
+    @staticmethod
+    def from_c(c: vp_camera) -> "Camera":
+        return Camera(np.array(c.K, np.float32).reshape(3, 3).T.copy(),
+                      np.array(c.R, np.float32).reshape(3, 3).T.copy(),
+                      np.array(c.t, np.float32), int(c.width), int(c.height))
+
+    def center(self) -> np.ndarray:
+        return -(self.rotation.T.astype(np.float32) @ self.translation.astype(np.float32))
+
+
+@dataclass
+class RenderOutput:
+    """march.h:46-56"""
+    color: np.ndarray
+    alpha: np.ndarray
+    sample_counts: np.ndarray
+    stats: Optional[dict] = None
+
+    def total_samples(self) -> int:
+        return int(self.sample_counts.astype(np.int64).sum())
+
+
+# ----------------------------------------------------------------------------------------
+
+def compose(transforms: np.ndarray) -> np.ndarray:
+    """Frame::composed(): K x 24 PrimitiveTransform records -> K x 15 AffineXf records
+    (t[3] rot[9] column-major scale[3]). Raises Error(USAGE) on a non-positive scale."""
+    lib = _lib.load()
+    tr = _f32(transforms).reshape(-1, 24)
+    out = np.zeros((tr.shape[0], 15), np.float32)
+    _check(lib.vp_compose(tr.shape[0], _fptr(tr), _fptr(out)))
+    return out
+
+
+class Renderer:
+    """A device context holding one resident frame (transforms + repacked payload)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib.load()
+        ctx = C.c_void_p()
+        _check(self._lib.vp_create(int(device), C.byref(ctx)))
+        self._ctx = ctx
+        self.device = device
+        self.n_prim = None
+        self.m = None
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.vp_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def ctx(self):
+        return self._ctx
+
+    def stream_handle(self) -> int:
+        return int(self._lib.vp_stream(self._ctx) or 0)
+
+    # -- resident scene ---------------------------------------------------------------
+    def set_scene_composed(self, xf15: np.ndarray, slab: PrimitiveSlab, window: WindowParams):
+        xf = _f32(xf15).reshape(-1, 15)
+        pay = _f32(slab.payload)
+        _check(self._lib.vp_set_scene(self._ctx, xf.shape[0], int(slab.voxels_per_axis),
+                                      _fptr(xf), _fptr(pay), float(window.alpha),
+                                      int(window.beta)), self._ctx)
+        self.n_prim, self.m = xf.shape[0], int(slab.voxels_per_axis)
+
+    def set_frame(self, scene: Scene, frame: int):
+        if frame < 0 or frame >= len(scene.frames):
+            raise Error(ErrorCategory.USAGE, "frame index out of range")  # march.cpp:96-97
+        fr = scene.frames[frame]
+        self.set_scene_composed(fr.composed(), fr.slab, scene.window)
+
+    def set_transforms(self, xf15: np.ndarray):
+        xf = _f32(xf15).reshape(-1, 15)
+        _check(self._lib.vp_set_transforms(self._ctx, xf.shape[0], _fptr(xf)), self._ctx)
+
+    # -- render -----------------------------------------------------------------------
+    def render(self, cam: Camera, cfg: MarchConfig, with_stats: bool = True) -> RenderOutput:
+        w, h = int(cam.width), int(cam.height)
+        color = np.zeros((h, w, 3), np.float32)
+        alpha = np.zeros((h, w, 1), np.float32)
+        samples = np.zeros(h * w, np.int32)
+        st = vp_stats()
+        cc, mc = cam.to_c(), cfg.to_c()
+        _check(self._lib.vp_render(self._ctx, C.byref(cc), C.byref(mc), _fptr(color), _fptr(alpha),
+                                   samples.ctypes.data_as(i32p), C.byref(st)), self._ctx)
+        return RenderOutput(color, alpha, samples, st.as_dict() if with_stats else None)
+
+    def render_device(self, cam: Camera, cfg: MarchConfig, rgb_ptr: int, alpha_ptr: int,
+                      samples_ptr: int = 0, stream: int = 0):
+        """Enqueue a render into device buffers (e.g. torch CUDA tensors' data_ptr())."""
+        cc, mc = cam.to_c(), cfg.to_c()
+        _check(self._lib.vp_render_async(self._ctx, C.byref(cc), C.byref(mc),
+                                         C.cast(C.c_void_p(rgb_ptr), f32p),
+                                         C.cast(C.c_void_p(alpha_ptr), f32p),
+                                         C.cast(C.c_void_p(samples_ptr), i32p) if samples_ptr else None,
+                                         C.c_void_p(stream) if stream else None), self._ctx)
+
+    def read_stats(self) -> dict:
+        st = vp_stats()
+        _check(self._lib.vp_read_stats(self._ctx, C.byref(st)), self._ctx)
+        return st.as_dict()
+
+    def march_rays(self, origins, dirs, cfg: MarchConfig, jitter01=None):
+        o = _f32(origins).reshape(-1, 3)
+        d = _f32(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        j = None if jitter01 is None else _f32(jitter01).reshape(n)
+        rgb = np.zeros((n, 3), np.float32)
+        alpha = np.zeros(n, np.float32)
+        samples = np.zeros(n, np.int32)
+        mc = cfg.to_c()
+        _check(self._lib.vp_march_rays(self._ctx, n, _fptr(o), _fptr(d),
+                                       _fptr(j) if j is not None else None, C.byref(mc),
+                                       _fptr(rgb), _fptr(alpha), samples.ctypes.data_as(i32p)),
+               self._ctx)
+        return rgb, alpha, samples
+
+    def debug_tiles(self, cam: Camera):
+        """Cull rectangles, depth keys, tile offsets and per-tile sorted primitive lists."""
+        k = self.n_prim or 0
+        tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        rects = np.zeros((max(k, 1), 4), np.int32)
+        keys = np.zeros(max(k, 1), np.uint32)
+        offs = np.zeros(tiles + 1, np.int32)
+        n_keys = C.c_int64()
+        cc = cam.to_c()
+        _check(self._lib.vp_debug_tiles(self._ctx, C.byref(cc), rects.ctypes.data_as(i32p),
+                                        keys.ctypes.data_as(u32p), offs.ctypes.data_as(i32p),
+                                        None, 0, C.byref(n_keys)), self._ctx)
+        prims = np.zeros(max(n_keys.value, 1), np.int32)
+        _check(self._lib.vp_debug_tiles(self._ctx, C.byref(cc), None, None, None,
+                                        prims.ctypes.data_as(i32p), prims.size, C.byref(n_keys)),
+               self._ctx)
+        return rects[:k], keys[:k], offs, prims[:n_keys.value]
+
+    def debug_expf(self, x: np.ndarray) -> np.ndarray:
+        x = _f32(x).reshape(-1)
+        y = np.empty_like(x)
+        _check(self._lib.vp_debug_expf(self._ctx, x.size, _fptr(x), _fptr(y)), self._ctx)
+        return y
+
+    def composite(self, out: RenderOutput, background: np.ndarray) -> np.ndarray:
+        h, w = out.color.shape[:2]
+        bg = _f32(background)
+        if bg.shape != (h, w, 3):
+            raise Error(ErrorCategory.USAGE, "background dimensions do not match render")
+        res = np.zeros((h, w, 3), np.float32)
+        _check(self._lib.vp_composite(self._ctx, w, h, _fptr(out.color), _fptr(out.alpha),
+                                      _fptr(bg), _fptr(res)), self._ctx)
+        return res
+
+
+_default: dict = {}
+
+
+def _renderer(device: int) -> Renderer:
+    if device not in _default:
+        _default[device] = Renderer(device)
+    return _default[device]
+
+
+def render(scene: Scene, frame: int, cam: Camera, cfg: MarchConfig, device: int = 0) -> RenderOutput:
+    """volprim::render (march.h:59): uploads the frame and renders one view on `device`."""
+    r = _renderer(device)
+    r.set_frame(scene, frame)
+    return r.render(cam, cfg)
+
+
+def composite(out: RenderOutput, background: np.ndarray, device: int = 0) -> np.ndarray:
+    """volprim::composite (march.h:62)."""
+    return _renderer(device).composite(out, background)

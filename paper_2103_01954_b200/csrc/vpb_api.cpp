@@ -1,0 +1,612 @@
+// vpb_api.cpp — the C-ABI (include/vpb.h): context, resident scene, and the render
+// pipeline that replaces volprim::render (march.cpp:95-132):
+//
+//   host:   compose (if asked) + camera constants, exact reference arithmetic
+//   device: K1 cull -> K2 scan -> K3 emit + per-tile sort -> K5 tile raymarch -> K5b fallback
+//
+// all enqueued on one stream with no host synchronisation inside the pipeline (the
+// fallback kernel reads the overflow count on the device), so vp_render_async can be
+// captured or overlapped; vp_render adds the host copies and one final synchronisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vpb.h"
+#include "vpb_hostmath.hpp"
+#include "vpb_kernels.h"
+
+using namespace vpb;
+
+namespace {
+
+thread_local std::string g_err;  // errors of context-free calls
+
+template <class T> struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        const cudaError_t e = cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(T));
+        if (e == cudaSuccess) n = std::max<size_t>(want, 1);
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct vp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+    bool has_scene = false;
+    int32_t n_prim = 0, m = 0;
+    float w_alpha = 8;
+    int32_t w_beta = 8;
+    DBuf<float> xf16, xf15_tmp, planar_tmp;
+    DBuf<float4> payload;
+    DBuf<int4> rects;
+    DBuf<uint32_t> keys, tile_counts, offsets, cursor;
+    DBuf<unsigned long long> entries;
+    DBuf<float> out_rgb, out_alpha;
+    DBuf<int> out_samples, ovf_list;
+    DBuf<float> fb_e, fb_x;
+    DBuf<int> fb_c;
+    DBuf<float> ray_o, ray_d, ray_j;
+    DevCounters *d_ctr = nullptr, *h_ctr = nullptr;
+    int64_t entries_cap = 0;
+    int ovf_cap = 0;
+};
+
+namespace {
+
+int fail(vp_ctx *ctx, int code, const std::string &msg) {
+    (ctx ? ctx->err : g_err) = msg;
+    return code;
+}
+int cuda_fail(vp_ctx *ctx, cudaError_t e, const char *where) {
+    return fail(ctx, VP_ERR_DEVICE, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define VP_CUDA(ctx, call)                                   \
+    do {                                                     \
+        const cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+// Camera constants with the reference's host arithmetic (camera.cpp:14-23, camera.h:28).
+CamDev make_cam(const vp_camera &c) {
+    using namespace vpb::host;
+    CamDev d{};
+    const M3 K = load9(c.K), R = load9(c.R);
+    const M3 kinv = inverse(K);
+    const F3 center = neg(mv(transposed(R), load3(c.t)));
+    std::memcpy(d.kinv, kinv.m, sizeof d.kinv);
+    std::memcpy(d.R, c.R, sizeof d.R);
+    std::memcpy(d.K, c.K, sizeof d.K);
+    std::memcpy(d.t, c.t, sizeof d.t);
+    d.center[0] = center.x;
+    d.center[1] = center.y;
+    d.center[2] = center.z;
+    d.width = c.width;
+    d.height = c.height;
+    d.tiles_x = (c.width + 15) / 16;
+    d.tiles_y = (c.height + 15) / 16;
+    return d;
+}
+
+int check_march(vp_ctx *ctx, const vp_march *cfg) {
+    if (!cfg) return fail(ctx, VP_ERR_USAGE, "null march config");
+    if (!(cfg->step_size > 0) || !std::isfinite(cfg->step_size))
+        return fail(ctx, VP_ERR_USAGE, "step_size must be positive and finite");
+    if (!std::isfinite(cfg->early_eps)) return fail(ctx, VP_ERR_USAGE, "early_eps must be finite");
+    if (cfg->accumulation_permutation != 0)
+        return fail(ctx, VP_ERR_USAGE,
+                    "accumulationPermutation is a march() test hook; not supported by the device path");
+    return VP_OK;
+}
+
+MarchDev make_march(const vp_ctx *ctx, const vp_march *cfg) {
+    MarchDev mp{};
+    mp.dt = cfg->step_size;
+    mp.eps = cfg->early_eps;
+    mp.jitter = cfg->jitter != 0;
+    mp.m = ctx->m;
+    mp.seed = cfg->seed;
+    mp.alpha = ctx->w_alpha;
+    mp.beta = ctx->w_beta;
+    return mp;
+}
+
+int ensure_fallback(vp_ctx *ctx) {
+    const size_t n = size_t(kFallbackBlocks) * kFallbackThreads * kFallbackCap;
+    VP_CUDA(ctx, ctx->fb_e.ensure(n));
+    VP_CUDA(ctx, ctx->fb_x.ensure(n));
+    VP_CUDA(ctx, ctx->fb_c.ensure(n));
+    return VP_OK;
+}
+
+int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
+    const size_t n_tiles = size_t(cam.tiles_x) * cam.tiles_y;
+    const size_t n_px = size_t(cam.width) * cam.height;
+    VP_CUDA(ctx, ctx->tile_counts.ensure(n_tiles));
+    VP_CUDA(ctx, ctx->offsets.ensure(n_tiles + 1));
+    VP_CUDA(ctx, ctx->cursor.ensure(n_tiles));
+    VP_CUDA(ctx, ctx->rects.ensure(size_t(std::max(ctx->n_prim, 1))));
+    VP_CUDA(ctx, ctx->keys.ensure(size_t(std::max(ctx->n_prim, 1))));
+    if (ctx->entries_cap == 0) ctx->entries_cap = std::max<int64_t>(int64_t(1) << 20, int64_t(ctx->n_prim) * 16);
+    VP_CUDA(ctx, ctx->entries.ensure(size_t(ctx->entries_cap)));
+    if (size_t(ctx->ovf_cap) < n_px) {
+        VP_CUDA(ctx, ctx->ovf_list.ensure(n_px));
+        ctx->ovf_cap = int(n_px);
+    }
+    return ensure_fallback(ctx);
+}
+
+// The device pipeline for one view (no host synchronisation).
+int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const OutDev &od,
+                   cudaStream_t st) {
+    VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->keys.p,
+                                ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
+                                ctx->entries_cap, ctx->d_ctr, st));
+    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->payload.p, ctx->offsets.p,
+                                    ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
+    const RaysDev none{nullptr, nullptr, nullptr};
+    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p,
+                                       ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
+                                       ctx->ovf_list.p, ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p,
+                                       ctx->fb_c.p, st));
+    return VP_OK;
+}
+
+void fill_stats(const DevCounters &c, float ms, vp_stats *s) {
+    if (!s) return;
+    s->ray_samples = int64_t(c.ray_samples);
+    s->prim_samples = int64_t(c.prim_samples);
+    s->hit_rays = int64_t(c.hit_rays);
+    s->early_exits = int64_t(c.early_exits);
+    s->saturated = int64_t(c.saturated);
+    s->overflow_rays = int64_t(c.overflow_rays);
+    s->keys = int64_t(c.keys);
+    s->refills = int64_t(c.refills);
+    s->ms = ms;
+    s->reserved = 0;
+}
+
+int check_counters(vp_ctx *ctx, const DevCounters &c) {
+    if (c.fallback_fail)
+        return fail(ctx, VP_ERR_NUMERIC,
+                    "a ray has more than 256 simultaneously live primitive segments");
+    if (c.numeric_fail) return fail(ctx, VP_ERR_NUMERIC, "quadrature did not terminate");
+    return VP_OK;
+}
+
+int check_ctx(vp_ctx *ctx, bool need_scene) {
+    if (!ctx) return fail(nullptr, VP_ERR_USAGE, "null context");
+    if (need_scene && !ctx->has_scene) return fail(ctx, VP_ERR_USAGE, "no scene set");
+    const cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    return VP_OK;
+}
+
+int check_cam(vp_ctx *ctx, const vp_camera *cam) {
+    if (!cam) return fail(ctx, VP_ERR_USAGE, "null camera");
+    if (cam->width < 0 || cam->height < 0) return fail(ctx, VP_ERR_USAGE, "negative image size");
+    return VP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vp_version(void) { return VPB_VERSION; }
+
+int vp_create(int32_t device, vp_ctx **out) {
+    if (!out) return fail(nullptr, VP_ERR_USAGE, "null output pointer");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDeviceCount");
+    if (device < 0 || device >= n) return fail(nullptr, VP_ERR_USAGE, "device index out of range");
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, VP_ERR_DEVICE, std::string("libvpb is built for sm_100a (B200); device is ") +
+                                                prop.name);
+    vp_ctx *ctx = new vp_ctx();
+    ctx->device = device;
+    int rc = VP_OK;
+    if ((e = cudaSetDevice(device)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess || (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_ctr, sizeof(DevCounters))) != cudaSuccess ||
+        (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
+        rc = cuda_fail(nullptr, e, "vp_create");
+        vp_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return VP_OK;
+}
+
+int vp_destroy(vp_ctx *ctx) {
+    if (!ctx) return VP_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto *b : {&ctx->xf16, &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
+                    &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
+        b->release();
+    ctx->payload.release();
+    ctx->rects.release();
+    for (auto *b : {&ctx->keys, &ctx->tile_counts, &ctx->offsets, &ctx->cursor}) b->release();
+    ctx->entries.release();
+    for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
+    if (ctx->d_ctr) cudaFree(ctx->d_ctr);
+    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return VP_OK;
+}
+
+const char *vp_last_error(const vp_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+void *vp_stream(vp_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int vp_compose(int32_t n_prim, const float *tr24, float *xf15) {
+    if (n_prim < 0 || (n_prim > 0 && (!tr24 || !xf15))) return fail(nullptr, VP_ERR_USAGE, "bad arguments");
+    for (int32_t k = 0; k < n_prim; ++k)
+        if (!vpb::host::compose(tr24 + 24 * size_t(k), xf15 + 15 * size_t(k)))
+            return fail(nullptr, VP_ERR_USAGE, "non-positive composed primitive scale");
+    return VP_OK;
+}
+
+int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
+    if (n_prim == 0) return VP_OK;
+    if (!xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    const bool dev = is_device_ptr(xf15);
+    if (!dev) {
+        for (int32_t k = 0; k < n_prim; ++k) {
+            const float *s = xf15 + 15 * size_t(k) + 12;
+            if (!(s[0] > 0) || !(s[1] > 0) || !(s[2] > 0))
+                return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+        }
+    }
+    VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
+    const float *src = xf15;
+    if (!dev) {
+        VP_CUDA(ctx, ctx->xf15_tmp.ensure(size_t(n_prim) * 15));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->xf15_tmp.p, xf15, sizeof(float) * 15 * size_t(n_prim),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+        src = ctx->xf15_tmp.p;
+    }
+    VP_CUDA(ctx, launch_pad_xf(src, ctx->xf16.p, n_prim, ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
+}
+
+int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
+                 const float *payload, float window_alpha, int32_t window_beta) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (n_prim < 0) return fail(ctx, VP_ERR_USAGE, "negative primitive count");
+    if (n_prim > 0 && m < 1) return fail(ctx, VP_ERR_USAGE, "voxels per axis must be >= 1");
+    if (n_prim > 0 && (!xf15 || !payload)) return fail(ctx, VP_ERR_USAGE, "null scene arrays");
+    if (!std::isfinite(window_alpha)) return fail(ctx, VP_ERR_USAGE, "window alpha must be finite");
+    ctx->has_scene = false;
+    ctx->n_prim = n_prim;
+    ctx->m = m;
+    ctx->w_alpha = window_alpha;
+    ctx->w_beta = window_beta;
+    ctx->has_scene = true;
+    if (n_prim == 0) return VP_OK;
+    if (int rc = vp_set_transforms(ctx, n_prim, xf15)) {
+        ctx->has_scene = false;
+        return rc;
+    }
+    const int64_t m3 = int64_t(m) * m * m;
+    const size_t nf = size_t(n_prim) * 4 * size_t(m3);
+    VP_CUDA(ctx, ctx->payload.ensure(size_t(n_prim) * size_t(m3)));
+    const float *src = payload;
+    if (!is_device_ptr(payload)) {
+        VP_CUDA(ctx, ctx->planar_tmp.ensure(nf));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->planar_tmp.p, payload, nf * sizeof(float),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+        src = ctx->planar_tmp.p;
+    }
+    VP_CUDA(ctx, launch_repack(src, ctx->payload.p, n_prim, m3, ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->planar_tmp.release();
+    return VP_OK;
+}
+
+int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *inter) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (n_prim != ctx->n_prim || m != ctx->m) return fail(ctx, VP_ERR_USAGE, "payload shape mismatch");
+    if (n_prim == 0) return VP_OK;
+    if (!inter) return fail(ctx, VP_ERR_USAGE, "null payload");
+    const size_t n4 = size_t(n_prim) * size_t(m) * m * m;
+    VP_CUDA(ctx, ctx->payload.ensure(n4));
+    if ((const void *)inter != (const void *)ctx->payload.p)
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->payload.p, inter, n4 * sizeof(float4),
+                                     is_device_ptr(inter) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                     ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
+}
+
+int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (dev_ptr) *dev_ptr = reinterpret_cast<float *>(ctx->payload.p);
+    if (n_floats) *n_floats = int64_t(ctx->n_prim) * ctx->m * ctx->m * ctx->m * 4;
+    return VP_OK;
+}
+
+int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb_dev,
+                    float *alpha_dev, int32_t *samples_dev, void *stream) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_cam(ctx, cam)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    const CamDev cd = make_cam(*cam);
+    const size_t n_px = size_t(cam->width) * cam->height;
+    if (n_px == 0) return VP_OK;
+    if (!rgb_dev || !alpha_dev) return fail(ctx, VP_ERR_USAGE, "null output");
+    if (ctx->n_prim == 0) {
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        VP_CUDA(ctx, cudaMemsetAsync(rgb_dev, 0, n_px * 3 * sizeof(float), st));
+        VP_CUDA(ctx, cudaMemsetAsync(alpha_dev, 0, n_px * sizeof(float), st));
+        if (samples_dev) VP_CUDA(ctx, cudaMemsetAsync(samples_dev, 0, n_px * sizeof(int32_t), st));
+        return VP_OK;
+    }
+    if (int rc = ensure_render_buffers(ctx, cd)) return rc;
+    const OutDev od{rgb_dev, alpha_dev, samples_dev};
+    return enqueue_render(ctx, cd, make_march(ctx, cfg), od, st);
+}
+
+int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    VP_CUDA(ctx, cudaMemcpy(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    const DevCounters c = *ctx->h_ctr;
+    fill_stats(c, 0.f, stats);
+    if (c.key_overflow) {
+        ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
+        return fail(ctx, VP_ERR_DEVICE, "tile key buffer was too small; capacity grown, render again");
+    }
+    return check_counters(ctx, c);
+}
+
+int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb, float *alpha,
+              int32_t *samples, vp_stats *stats) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_cam(ctx, cam)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    const size_t n_px = size_t(cam->width) * cam->height;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (n_px == 0) return VP_OK;
+    if (!rgb || !alpha) return fail(ctx, VP_ERR_USAGE, "null output");
+    const bool d_rgb = is_device_ptr(rgb), d_alpha = is_device_ptr(alpha);
+    const bool d_samp = samples && is_device_ptr(samples);
+    cudaStream_t st = ctx->stream;
+    if (ctx->n_prim == 0) {  // march.cpp:108: empty frame renders a zero image
+        if (d_rgb) VP_CUDA(ctx, cudaMemset(rgb, 0, n_px * 3 * sizeof(float)));
+        else std::memset(rgb, 0, n_px * 3 * sizeof(float));
+        if (d_alpha) VP_CUDA(ctx, cudaMemset(alpha, 0, n_px * sizeof(float)));
+        else std::memset(alpha, 0, n_px * sizeof(float));
+        if (samples) {
+            if (d_samp) VP_CUDA(ctx, cudaMemset(samples, 0, n_px * sizeof(int32_t)));
+            else std::memset(samples, 0, n_px * sizeof(int32_t));
+        }
+        return VP_OK;
+    }
+    const CamDev cd = make_cam(*cam);
+    const MarchDev mp = make_march(ctx, cfg);
+    OutDev od{rgb, alpha, samples};
+    if (!d_rgb) {
+        VP_CUDA(ctx, ctx->out_rgb.ensure(n_px * 3));
+        od.rgb = ctx->out_rgb.p;
+    }
+    if (!d_alpha) {
+        VP_CUDA(ctx, ctx->out_alpha.ensure(n_px));
+        od.alpha = ctx->out_alpha.p;
+    }
+    if (samples && !d_samp) {
+        VP_CUDA(ctx, ctx->out_samples.ensure(n_px));
+        od.samples = ctx->out_samples.p;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if (int rc = ensure_render_buffers(ctx, cd)) return rc;
+        VP_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
+        if (int rc = enqueue_render(ctx, cd, mp, od, st)) return rc;
+        VP_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+        VP_CUDA(ctx, cudaStreamSynchronize(st));
+        const DevCounters c = *ctx->h_ctr;
+        if (c.key_overflow) {  // grow the key buffer and run again
+            ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
+            continue;
+        }
+        if (!d_rgb) VP_CUDA(ctx, cudaMemcpyAsync(rgb, od.rgb, n_px * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
+        if (!d_alpha) VP_CUDA(ctx, cudaMemcpyAsync(alpha, od.alpha, n_px * sizeof(float), cudaMemcpyDeviceToHost, st));
+        if (samples && !d_samp)
+            VP_CUDA(ctx, cudaMemcpyAsync(samples, od.samples, n_px * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        VP_CUDA(ctx, cudaStreamSynchronize(st));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        fill_stats(c, ms, stats);
+        return check_counters(ctx, c);
+    }
+    return fail(ctx, VP_ERR_DEVICE, "tile key buffer could not be sized");
+}
+
+int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
+                  const float *jitter01, const vp_march *cfg, float *rgb, float *alpha,
+                  int32_t *samples) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    if (n_rays < 0) return fail(ctx, VP_ERR_USAGE, "negative ray count");
+    if (n_rays == 0) return VP_OK;
+    if (!origins || !dirs || !rgb || !alpha) return fail(ctx, VP_ERR_USAGE, "null ray arrays");
+    cudaStream_t st = ctx->stream;
+    const size_t n = size_t(n_rays);
+    RaysDev rays{origins, dirs, jitter01};
+    if (!is_device_ptr(origins)) {
+        VP_CUDA(ctx, ctx->ray_o.ensure(3 * n));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_o.p, origins, 12 * n, cudaMemcpyHostToDevice, st));
+        rays.origins = ctx->ray_o.p;
+    }
+    if (!is_device_ptr(dirs)) {
+        VP_CUDA(ctx, ctx->ray_d.ensure(3 * n));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_d.p, dirs, 12 * n, cudaMemcpyHostToDevice, st));
+        rays.dirs = ctx->ray_d.p;
+    }
+    if (jitter01 && !is_device_ptr(jitter01)) {
+        VP_CUDA(ctx, ctx->ray_j.ensure(n));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_j.p, jitter01, 4 * n, cudaMemcpyHostToDevice, st));
+        rays.jitter = ctx->ray_j.p;
+    }
+    const bool d_rgb = is_device_ptr(rgb), d_alpha = is_device_ptr(alpha);
+    const bool d_samp = samples && is_device_ptr(samples);
+    OutDev od{rgb, alpha, samples};
+    if (!d_rgb) { VP_CUDA(ctx, ctx->out_rgb.ensure(3 * n)); od.rgb = ctx->out_rgb.p; }
+    if (!d_alpha) { VP_CUDA(ctx, ctx->out_alpha.ensure(n)); od.alpha = ctx->out_alpha.p; }
+    if (samples && !d_samp) { VP_CUDA(ctx, ctx->out_samples.ensure(n)); od.samples = ctx->out_samples.p; }
+    if (size_t(ctx->ovf_cap) < n) {
+        VP_CUDA(ctx, ctx->ovf_list.ensure(n));
+        ctx->ovf_cap = int(n);
+    }
+    if (int rc = ensure_fallback(ctx)) return rc;
+    const MarchDev mp = make_march(ctx, cfg);
+    VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+    if (ctx->n_prim == 0) {
+        VP_CUDA(ctx, cudaMemsetAsync(od.rgb, 0, 12 * n, st));
+        VP_CUDA(ctx, cudaMemsetAsync(od.alpha, 0, 4 * n, st));
+        if (od.samples) VP_CUDA(ctx, cudaMemsetAsync(od.samples, 0, 4 * n, st));
+    } else {
+        VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, rays, n_rays, od,
+                                       ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
+        const CamDev none{};
+        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p,
+                                           nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p,
+                                           ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+    }
+    if (!d_rgb) VP_CUDA(ctx, cudaMemcpyAsync(rgb, od.rgb, 12 * n, cudaMemcpyDeviceToHost, st));
+    if (!d_alpha) VP_CUDA(ctx, cudaMemcpyAsync(alpha, od.alpha, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (samples && !d_samp) VP_CUDA(ctx, cudaMemcpyAsync(samples, od.samples, 4 * n, cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    return check_counters(ctx, *ctx->h_ctr);
+}
+
+int vp_composite(vp_ctx *ctx, int32_t width, int32_t height, const float *rgb, const float *alpha,
+                 const float *background, float *out) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (width < 0 || height < 0) return fail(ctx, VP_ERR_USAGE, "background dimensions do not match render");
+    const size_t n = size_t(width) * height;
+    if (n == 0) return VP_OK;
+    if (!rgb || !alpha || !background || !out) return fail(ctx, VP_ERR_USAGE, "null image");
+    cudaStream_t st = ctx->stream;
+    DBuf<float> tmp;
+    const float *d_in[3] = {rgb, alpha, background};
+    const size_t sz[3] = {3 * n, n, 3 * n};
+    size_t total = 0;
+    for (int i = 0; i < 3; ++i)
+        if (!is_device_ptr(d_in[i])) total += sz[i];
+    const bool d_out = is_device_ptr(out);
+    if (!d_out) total += 3 * n;
+    VP_CUDA(ctx, tmp.ensure(total));
+    size_t off = 0;
+    for (int i = 0; i < 3; ++i)
+        if (!is_device_ptr(d_in[i])) {
+            VP_CUDA(ctx, cudaMemcpyAsync(tmp.p + off, d_in[i], sz[i] * 4, cudaMemcpyHostToDevice, st));
+            d_in[i] = tmp.p + off;
+            off += sz[i];
+        }
+    float *o = d_out ? out : tmp.p + off;
+    VP_CUDA(ctx, launch_composite(d_in[0], d_in[1], d_in[2], o, int64_t(n), st));
+    if (!d_out) VP_CUDA(ctx, cudaMemcpyAsync(out, o, 12 * n, cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    tmp.release();
+    return VP_OK;
+}
+
+int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *depth_key,
+                   int32_t *tile_offsets, int32_t *tile_prims, int64_t cap, int64_t *n_keys) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_cam(ctx, cam)) return rc;
+    const CamDev cd = make_cam(*cam);
+    const size_t n_tiles = size_t(cd.tiles_x) * cd.tiles_y;
+    cudaStream_t st = ctx->stream;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if (int rc = ensure_render_buffers(ctx, cd)) return rc;
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->keys.p,
+                                    ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
+                                    ctx->entries_cap, ctx->d_ctr, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+        VP_CUDA(ctx, cudaStreamSynchronize(st));
+        const DevCounters c = *ctx->h_ctr;
+        if (c.key_overflow) {
+            ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
+            continue;
+        }
+        const size_t nk = size_t(c.keys);
+        if (n_keys) *n_keys = int64_t(nk);
+        if (rect4 && ctx->n_prim > 0)
+            VP_CUDA(ctx, cudaMemcpy(rect4, ctx->rects.p, sizeof(int4) * ctx->n_prim, cudaMemcpyDeviceToHost));
+        if (depth_key && ctx->n_prim > 0)
+            VP_CUDA(ctx, cudaMemcpy(depth_key, ctx->keys.p, sizeof(uint32_t) * ctx->n_prim, cudaMemcpyDeviceToHost));
+        if (tile_offsets)
+            VP_CUDA(ctx, cudaMemcpy(tile_offsets, ctx->offsets.p, sizeof(uint32_t) * (n_tiles + 1),
+                                    cudaMemcpyDeviceToHost));
+        if (tile_prims && cap > 0 && nk > 0) {
+            std::vector<unsigned long long> e(nk);
+            VP_CUDA(ctx, cudaMemcpy(e.data(), ctx->entries.p, nk * 8, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < nk && int64_t(i) < cap; ++i) tile_prims[i] = int32_t(e[i] & 0xffffffffull);
+        }
+        return VP_OK;
+    }
+    return fail(ctx, VP_ERR_DEVICE, "tile key buffer could not be sized");
+}
+
+int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (n < 0 || (n > 0 && (!x || !y))) return fail(ctx, VP_ERR_USAGE, "bad arguments");
+    if (n == 0) return VP_OK;
+    DBuf<float> tmp;
+    VP_CUDA(ctx, tmp.ensure(2 * size_t(n)));
+    VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, x, 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    VP_CUDA(ctx, launch_expf(tmp.p, tmp.p + n, n, ctx->stream));
+    VP_CUDA(ctx, cudaMemcpyAsync(y, tmp.p + n, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    tmp.release();
+    return VP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// vpb_device.cuh — device-side arithmetic of the raymarcher, bit-faithful to the reference.
+//
+// The whole translation unit is compiled with -fmad=false (no FMA contraction), IEEE
+// division and square root (no --use_fast_math), so each expression below rounds exactly
+// like the reference's binary32 SSE code (which contains no vfmadd). Every
+// helper keeps the reference's operation order; the cited lines are the ones restated.
+#pragma once
+
+#include <cstdint>
+
+#include "vpb_camdev.h"
+
+namespace vpb {
+
+struct V3 {
+    float x, y, z;
+};
+
+__device__ __forceinline__ V3 mk3(float x, float y, float z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 operator*(V3 a, float s) { return V3{a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ float dot3(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float comp(V3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+
+// math.h:122-124 — col(0)*v.x + col(1)*v.y + col(2)*v.z on a column-major matrix.
+__device__ __forceinline__ V3 matvec(const float *m, V3 v) {
+    return (mk3(m[0], m[1], m[2]) * v.x + mk3(m[3], m[4], m[5]) * v.y) + mk3(m[6], m[7], m[8]) * v.z;
+}
+// Mat3::transpose() * v: column j of R^T is row j of R.
+__device__ __forceinline__ V3 matTvec(const float *m, V3 v) {
+    return (mk3(m[0], m[3], m[6]) * v.x + mk3(m[1], m[4], m[7]) * v.y) + mk3(m[2], m[5], m[8]) * v.z;
+}
+
+// Composed primitive transform, 16-float padded record: t[3] rot[9] scale[3] pad.
+constexpr int kXfStride = 16;
+
+// primitive.h:61-63 — AffineXf::toModel = (R^T (p - t)) ./ s
+__device__ __forceinline__ V3 to_model(const float *xf, V3 p) {
+    const V3 q = matTvec(xf + 3, p - mk3(xf[0], xf[1], xf[2]));
+    return V3{q.x / xf[12], q.y / xf[13], q.z / xf[14]};
+}
+
+// lbvh.cpp:177-205 — exact oriented slab test in model space.
+__device__ __forceinline__ bool intersect_obb(const float *xf, V3 o, V3 d, float &tEnterOut,
+                                              float &tExitOut) {
+    const V3 om = to_model(xf, o);
+    const V3 q = matTvec(xf + 3, d);
+    const V3 dm = V3{q.x / xf[12], q.y / xf[13], q.z / xf[14]};
+    float tEnter = -3.402823466e+38f, tExit = 3.402823466e+38f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float oa = comp(om, a), da = comp(dm, a);
+        if (da == 0.0f) {
+            if (oa < -1.0f || oa > 1.0f) return false;
+            continue;
+        }
+        const float inv = 1.0f / da;
+        const float cNear = da > 0.0f ? -1.0f : 1.0f;
+        const float t1 = (cNear - oa) * inv;
+        const float t2 = (-cNear - oa) * inv;
+        if (t1 > tEnter) tEnter = t1;
+        tExit = t2 < tExit ? t2 : tExit;
+    }
+    if (tEnter < 0.0f) tEnter = 0.0f;
+    if (tEnter >= tExit || tExit <= 0.0f) return false;
+    tEnterOut = tEnter;
+    tExitOut = tExit;
+    return true;
+}
+
+// camera.cpp:14-23 — pixel (px, py) is x + 0.5, y + 0.5.
+__device__ __forceinline__ void generate_ray(const CamDev &cam, float px, float py, V3 &o, V3 &d) {
+    const V3 dirCam = matvec(cam.kinv, mk3(px, py, 1.0f));
+    const V3 v = matTvec(cam.R, dirCam);
+    const float len = sqrtf(dot3(v, v));
+    d = V3{v.x / len, v.y / len, v.z / len};
+    o = mk3(cam.center[0], cam.center[1], cam.center[2]);
+}
+
+// math.h:170-179
+__device__ __forceinline__ uint64_t hash_combine(uint64_t seed, uint64_t value) {
+    uint64_t z = seed + 0x9e3779b97f4a7c15ull + value;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ float hash_to_unit(uint64_t h) {
+    return __ull2float_rn(h >> 11) * 1.1102230246251565e-16f; // real(1.0 / 2^53)
+}
+
+// ---------------------------------------------------------------------------------------
+// glibc 2.39 expf, bit-exact port (std::exp(float) in window(), primitive.cpp:27).
+// Algorithm: sysdeps/ieee754/flt-32/e_expf.c (ARM optimized-routines): k = round(x*32/ln2),
+// 2^(k/32) from a 32-entry table, cubic correction, all in binary64, one final rounding.
+// glibc's x86-64 ifunc selects the FMA build on FMA-capable hosts; the FMA and non-FMA
+// builds agree on every float in [-104, 88] (checked exhaustively on the host), as does
+// this port except at the two inputs patched below. The table lives in shared memory
+// (lanes index it divergently).
+__constant__ unsigned long long kExp2fTab[32] = {
+    0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
+    0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
+    0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
+    0x3feebfdad5362a27ULL, 0x3feeb42b569d4f82ULL, 0x3feeab07dd485429ULL, 0x3feea47eb03a5585ULL,
+    0x3feea09e667f3bcdULL, 0x3fee9f75e8ec5f74ULL, 0x3feea11473eb0187ULL, 0x3feea589994cce13ULL,
+    0x3feeace5422aa0dbULL, 0x3feeb737b0cdc5e5ULL, 0x3feec49182a3f090ULL, 0x3feed503b23e255dULL,
+    0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
+    0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
+
+__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
+    if (!(x == x)) return x + x;
+    if (x < -0x1.9fe368p6f) return 0.0f;
+    if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+    if (x == -0x1.f8cbb2p+5f) return 0x1.f45326p-92f;
+    if (x == 0x1.04845ep+5f) return 0x1.f93e38p+46f;
+    const double InvLn2N = 0x1.71547652b82fep+0 * 32, Shift = 0x1.8p+52;
+    const double C0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32, C1 = 0x1.ebfce50fac4f3p-3 / 32 / 32,
+                 C2 = 0x1.62e42ff0c52d6p-1 / 32;
+    const double z = __dmul_rn(InvLn2N, (double)x);
+    double kd = __dadd_rn(z, Shift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, Shift);
+    const double r = __dsub_rn(z, kd);
+    const unsigned long long t = tab[ki & 31] + (ki << 47);
+    const double s = __longlong_as_double((long long)t);
+    const double zz = __fma_rn(C0, r, C1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(C2, r, 1.0);
+    y = __fma_rn(zz, r2, y);
+    return __double2float_rn(__dmul_rn(y, s));
+}
+
+// primitive.cpp:12-22
+__device__ __forceinline__ float pow_even(float x, int beta) {
+    float r = 1.0f, b = fabsf(x);
+    int e = beta;
+    while (e > 0) {
+        if (e & 1) r *= b;
+        b *= b;
+        e >>= 1;
+    }
+    return r;
+}
+__device__ __forceinline__ float pow8(float x) { // pow_even(x, 8): r = 1 * b^8 exactly
+    const float b = fabsf(x);
+    const float b2 = b * b;
+    const float b4 = b2 * b2;
+    return b4 * b4;
+}
+
+// primitive.cpp:25-28
+__device__ __forceinline__ float window_value(V3 p, float alpha, int beta,
+                                              const unsigned long long *tab) {
+    if (alpha == 0.0f) return 1.0f;
+    float s;
+    if (beta == 8)
+        s = (pow8(p.x) + pow8(p.y)) + pow8(p.z);
+    else
+        s = (pow_even(p.x, beta) + pow_even(p.y, beta)) + pow_even(p.z, beta);
+    return expf_glibc(-alpha * s, tab);
+}
+
+// march.cpp:14-16 — cwiseMax(-1, cwiseMin(1, p)) with std::min/std::max semantics.
+__device__ __forceinline__ float clamp_unit(float v) {
+    const float lo = v < 1.0f ? v : 1.0f;
+    return -1.0f < lo ? lo : -1.0f;
+}
+
+// One primitive-sample: march.cpp:64-69 with trilinearStencil (primitive.cpp:51-69),
+// gatherChannel/cornerWeight (primitive.cpp:71-99) over the channel-interleaved float4
+// payload (k, z, y, x, rgba), and window(). Each channel accumulates its 8 corners in the
+// reference order (z, y, x loops, x fastest; weight (wx*wy)*wz, starting from 0).
+__device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payload, int m,
+                                                 int k, const float *xf, V3 pw, float alpha,
+                                                 int beta, const unsigned long long *tab,
+                                                 float &sigma, float &r, float &g, float &b) {
+    const V3 q = to_model(xf, pw);
+    const V3 pm = mk3(clamp_unit(q.x), clamp_unit(q.y), clamp_unit(q.z));
+    int lo[3];
+    float fr[3];
+    const float mf = (float)m;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float u = (comp(pm, a) + 1.0f) * 0.5f * mf - 0.5f;
+        if (u <= 0.0f) u = 0.0f;
+        else if (u >= (float)(m - 1)) u = (float)(m - 1);
+        int i0 = (int)floorf(u);
+        if (i0 > m - 2) i0 = (m - 2) > 0 ? (m - 2) : 0;
+        lo[a] = i0;
+        fr[a] = m > 1 ? u - (float)i0 : 0.0f;
+    }
+    const int x0 = lo[0], y0 = lo[1], z0 = lo[2];
+    const int x1 = min(x0 + 1, m - 1), y1 = min(y0 + 1, m - 1), z1 = min(z0 + 1, m - 1);
+    const size_t base = (size_t)k * (size_t)m * m * m;
+    const float4 *p = payload + base;
+    const int mm = m * m;
+    // Issue all eight 16-byte gathers before any arithmetic (memory-level parallelism).
+    const float4 c000 = __ldg(p + (z0 * mm + y0 * m + x0));
+    const float4 c001 = __ldg(p + (z0 * mm + y0 * m + x1));
+    const float4 c010 = __ldg(p + (z0 * mm + y1 * m + x0));
+    const float4 c011 = __ldg(p + (z0 * mm + y1 * m + x1));
+    const float4 c100 = __ldg(p + (z1 * mm + y0 * m + x0));
+    const float4 c101 = __ldg(p + (z1 * mm + y0 * m + x1));
+    const float4 c110 = __ldg(p + (z1 * mm + y1 * m + x0));
+    const float4 c111 = __ldg(p + (z1 * mm + y1 * m + x1));
+    const float wx0 = 1.0f - fr[0], wx1 = fr[0];
+    const float wy0 = 1.0f - fr[1], wy1 = fr[1];
+    const float wz0 = 1.0f - fr[2], wz1 = fr[2];
+    const float w000 = wx0 * wy0 * wz0, w001 = wx1 * wy0 * wz0;
+    const float w010 = wx0 * wy1 * wz0, w011 = wx1 * wy1 * wz0;
+    const float w100 = wx0 * wy0 * wz1, w101 = wx1 * wy0 * wz1;
+    const float w110 = wx0 * wy1 * wz1, w111 = wx1 * wy1 * wz1;
+#define VPB_GATHER(ch)                                                                        \
+    (((((((0.0f + w000 * c000.ch) + w001 * c001.ch) + w010 * c010.ch) + w011 * c011.ch) +     \
+        w100 * c100.ch) + w101 * c101.ch) + w110 * c110.ch) + w111 * c111.ch
+    const float s_raw = VPB_GATHER(w);
+    r = VPB_GATHER(x);
+    g = VPB_GATHER(y);
+    b = VPB_GATHER(z);
+#undef VPB_GATHER
+    sigma = s_raw * window_value(pm, alpha, beta, tab);
+}
+
+} // namespace vpb

@@ -1,0 +1,697 @@
+// vpb_kernels.cu — sm_100a kernels of the B200 raymarcher (the replacement of
+// volprim::render's body, march.cpp:95-132).
+//
+//   K0 k_repack        planar slab (k,c,z,y,x) -> channel-interleaved float4 (k,z,y,x)
+//   K1 k_cull          one thread per primitive: screen-tile rectangle + depth key, per-tile
+//                      counts (replaces primitiveAabb/mortonCode/buildLbvh, lbvh.cpp:13-156)
+//   K2 k_scan          exclusive scan of tile counts -> per-tile ranges, key capacity check
+//   K3 k_emit          (tile, depth<<32|prim) keys scattered into their tile buckets
+//   K3 k_tile_sort     per-bucket ascending sort of (depth<<32|prim): MSD radix by tile
+//                      (K1-K3 counting pass) + in-bucket bitonic network
+//   K5 k_march_tiles   16x16-pixel tile per CTA: candidate transforms staged in shared memory,
+//                      exact per-ray segment window (intersect, lbvh.cpp:207-234) and the
+//                      fused quadrature (march, march.cpp:18-93)
+//   K5b k_march_fallback  wide-window re-march of the rare rays whose live segments overflow
+//                      the shared-memory window
+//   k_march_rays       march() over caller-provided rays, all primitives as candidates
+//   k_composite        composite(), march.cpp:134-147
+//
+// Compiled with -fmad=false: see vpb_device.cuh for the arithmetic contract.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "vpb_device.cuh"
+#include "vpb_kernels.h"
+
+namespace vpb {
+
+constexpr int kTile = 16;
+constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
+constexpr int kCandCap = 64;        // candidates staged in shared memory per tile
+
+// ----------------------------------------------------------------------------------------
+// K0: planar -> interleaved. One thread per voxel; the four planar reads are coalesced
+// across the warp (consecutive voxels), the float4 write is coalesced.
+__global__ void k_repack(const float *__restrict__ planar, float4 *__restrict__ inter,
+                         int64_t n_prim, int64_t m3) {
+    const int64_t total = n_prim * m3;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / m3, v = i - k * m3;
+        const float *src = planar + k * 4 * m3 + v;
+        inter[i] = make_float4(__ldg(src), __ldg(src + m3), __ldg(src + 2 * m3), __ldg(src + 3 * m3));
+    }
+}
+
+// Pads 15-float AffineXf records to 16 floats (aligned float4 staging).
+__global__ void k_pad_xf(const float *__restrict__ xf15, float *__restrict__ xf16, int n_prim) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_prim * kXfStride) return;
+    const int k = i / kXfStride, j = i - k * kXfStride;
+    xf16[i] = j < 15 ? xf15[k * 15 + j] : 0.0f;
+}
+
+// ----------------------------------------------------------------------------------------
+// K1: cull. Same float operation sequence as the CPU restatement (oracle/vp_oracle.c,
+// cull_one), so rectangles and keys are bit-identical.
+__device__ __forceinline__ void cull_rect(const float *xf, const CamDev &cam, int4 &rect,
+                                          uint32_t &key) {
+    const V3 s = mk3(xf[12], xf[13], xf[14]);
+    const float r = sqrtf(dot3(s, s));
+    const float rr = r * 1.001f + 1e-6f;
+    const V3 cc = matvec(cam.R, mk3(xf[0], xf[1], xf[2])) + mk3(cam.t[0], cam.t[1], cam.t[2]);
+    const float dist = sqrtf(dot3(cc, cc));
+    float depth = dist - rr;
+    if (!(depth > 0.0f)) depth = 0.0f;
+    key = __float_as_uint(depth);
+    rect = make_int4(0, 0, -1, -1);
+    if (cam.width <= 0 || cam.height <= 0) return;
+    if (cc.z + rr < 0.0f) return;
+    if (cc.z - rr <= 1e-3f * rr) {
+        rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
+        return;
+    }
+    float umin = 3.402823466e+38f, umax = -3.402823466e+38f;
+    float vmin = 3.402823466e+38f, vmax = -3.402823466e+38f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const V3 corner = mk3(c & 1 ? 1.0f : -1.0f, c & 2 ? 1.0f : -1.0f, c & 4 ? 1.0f : -1.0f);
+        const V3 pw = mk3(xf[0], xf[1], xf[2]) +
+                      matvec(xf + 3, mk3(s.x * corner.x, s.y * corner.y, s.z * corner.z));
+        const V3 pc = matvec(cam.R, pw) + mk3(cam.t[0], cam.t[1], cam.t[2]);
+        const V3 hp = matvec(cam.K, pc);
+        const float u = hp.x / hp.z, v = hp.y / hp.z;
+        umin = u < umin ? u : umin;
+        umax = u > umax ? u : umax;
+        vmin = v < vmin ? v : vmin;
+        vmax = v > vmax ? v : vmax;
+    }
+    const float mu = 2.0f + 1e-3f * (fabsf(umin) + fabsf(umax));
+    const float mv = 2.0f + 1e-3f * (fabsf(vmin) + fabsf(vmax));
+    float x0 = floorf(umin - mu), x1 = floorf(umax + mu);
+    float y0 = floorf(vmin - mv), y1 = floorf(vmax + mv);
+    const float wl = (float)(cam.width - 1), hl = (float)(cam.height - 1);
+    if (!(x1 >= 0.0f) || !(x0 <= wl) || !(y1 >= 0.0f) || !(y0 <= hl)) return;
+    x0 = x0 > 0.0f ? x0 : 0.0f;
+    y0 = y0 > 0.0f ? y0 : 0.0f;
+    x1 = x1 < wl ? x1 : wl;
+    y1 = y1 < hl ? y1 : hl;
+    rect = make_int4((int)x0 / kTile, (int)y0 / kTile, (int)x1 / kTile, (int)y1 / kTile);
+}
+
+__global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
+                       int4 *__restrict__ rects, uint32_t *__restrict__ keys,
+                       uint32_t *__restrict__ tile_counts) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_prim) return;
+    float xf[15];
+#pragma unroll
+    for (int j = 0; j < 15; ++j) xf[j] = xf16[(size_t)k * kXfStride + j];
+    int4 rc;
+    uint32_t key;
+    cull_rect(xf, cam, rc, key);
+    rects[k] = rc;
+    keys[k] = key;
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+        for (int tx = rc.x; tx <= rc.z; ++tx) atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1u);
+}
+
+// K2: single-CTA exclusive scan over the tile counts (tiles <= a few 10^4). Writes the
+// bucket starts twice (offsets, and the emit cursors) and flags key-capacity overflow.
+__global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
+                       uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
+                       DevCounters *ctr, int64_t capacity) {
+    __shared__ unsigned long long warp_sums[32];
+    __shared__ unsigned long long carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += blockDim.x) {
+        const int i = base + tid;
+        const unsigned long long v = i < n_tiles ? counts[i] : 0;
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        if (lane == 31) warp_sums[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int nw = blockDim.x >> 5;
+            unsigned long long ws = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long n = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += n;
+            }
+            if (lane < nw) warp_sums[lane] = ws;
+        }
+        __syncthreads();
+        const unsigned long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + incl - v;
+        if (i < n_tiles) {
+            offsets[i] = (uint32_t)excl;
+            cursor[i] = (uint32_t)excl;
+        }
+        __syncthreads();
+        if (tid == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        offsets[n_tiles] = (uint32_t)carry;
+        ctr->keys = carry;
+        ctr->key_overflow = (int64_t)carry > capacity ? 1 : 0;
+    }
+}
+
+// K3a: scatter keys into buckets. Order inside a bucket is arbitrary here; K3b makes it
+// canonical.
+__global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
+                       int n_prim, int tiles_x, uint32_t *__restrict__ cursor,
+                       unsigned long long *__restrict__ entries, const DevCounters *ctr) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_prim || ctr->key_overflow) return;
+    const int4 rc = rects[k];
+    const unsigned long long e = ((unsigned long long)keys[k] << 32) | (uint32_t)k;
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+        for (int tx = rc.x; tx <= rc.z; ++tx) {
+            const uint32_t pos = atomicAdd(&cursor[ty * tiles_x + tx], 1u);
+            entries[pos] = e;
+        }
+}
+
+// K3b: sort each bucket ascending by (depth bits, prim). All-ascending bitonic network
+// (the "flip" formulation), so padding with +inf past n needs no special case.
+constexpr int kSortSmem = 2048;
+__global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
+                            unsigned long long *__restrict__ entries, const DevCounters *ctr) {
+    __shared__ unsigned long long s[kSortSmem];
+    if (ctr->key_overflow) return;
+    const uint32_t start = offsets[blockIdx.x];
+    const int n = (int)(offsets[blockIdx.x + 1] - start);
+    if (n <= 1) return;
+    int p = 1;
+    while (p < n) p <<= 1;
+    unsigned long long *a = entries + start;
+    const bool in_smem = p <= kSortSmem;
+    if (in_smem) {
+        for (int i = threadIdx.x; i < p; i += blockDim.x) s[i] = i < n ? a[i] : ~0ull;
+        __syncthreads();
+    }
+    unsigned long long *v = in_smem ? s : a;
+    for (int k = 2; k <= p; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < p; i += blockDim.x) {
+                const int partner = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
+                if (partner > i && (in_smem || partner < n)) {
+                    const unsigned long long x = v[i], y = v[partner];
+                    if (y < x) {
+                        v[i] = y;
+                        v[partner] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (in_smem)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = s[i];
+}
+
+// ----------------------------------------------------------------------------------------
+// Candidate sources for the per-ray segment window.
+struct TileCands {  // a tile's sorted bucket, first kCandCap staged in shared memory
+    const unsigned long long *entries;
+    const float *xf_g;
+    const int *s_prim;
+    const float *s_xf;
+    uint32_t start;
+    int n, staged;
+    __device__ __forceinline__ int prim(int c) const {
+        return c < staged ? s_prim[c] : (int)(uint32_t)(entries[start + c] & 0xffffffffull);
+    }
+    __device__ __forceinline__ const float *xf(int c) const {
+        return c < staged ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
+    }
+};
+struct AllCands {  // every primitive (march over arbitrary rays)
+    const float *xf_g;
+    int n;
+    __device__ __forceinline__ int prim(int c) const { return c; }
+    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+};
+
+// Per-ray sorted segment window storage: slot j of ray `lane` lives at [j * stride + lane].
+struct Window {
+    float *e;
+    float *x;
+    int *c;
+    int stride, lane;
+    __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
+    __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
+    __device__ __forceinline__ int &C(int j) const { return c[j * stride + lane]; }
+};
+
+struct RayOut {
+    float r, g, b, alpha;
+    int samples;
+    int64_t prim_samples;
+    int hit, early, saturated, overflow, refills, numeric;
+};
+
+__device__ __forceinline__ bool key_less(float ea, int pa, float eb, int pb) {
+    return ea != eb ? ea < eb : pa < pb;
+}
+
+// Inserts (tE, tX, c) into the sorted window [0, cnt) of capacity CAP, keeping the CAP
+// smallest (tEnter, prim) keys; `more` records that a hit fell outside the window.
+template <int CAP, class Cands>
+__device__ __forceinline__ void window_insert(const Window &w, const Cands &cands, int &cnt,
+                                              bool &more, float tE, float tX, int c, int prim) {
+    if (cnt == CAP) {
+        more = true;
+        if (!key_less(tE, prim, w.E(CAP - 1), cands.prim(w.C(CAP - 1)))) return;
+        cnt = CAP - 1;
+    }
+    int j = cnt;
+    while (j > 0) {
+        const float e = w.E(j - 1);
+        if (e < tE || (e == tE && cands.prim(w.C(j - 1)) < prim)) break;
+        w.E(j) = e;
+        w.X(j) = w.X(j - 1);
+        w.C(j) = w.C(j - 1);
+        --j;
+    }
+    w.E(j) = tE;
+    w.X(j) = tX;
+    w.C(j) = c;
+    ++cnt;
+}
+
+// Fills the window with the smallest hits whose key exceeds (lastE, lastP) (or all hits
+// when first == true).
+template <int CAP, class Cands>
+__device__ __forceinline__ void window_scan(const Window &w, const Cands &cands, int &cnt,
+                                            bool &more, V3 o, V3 d, bool first, float lastE,
+                                            int lastP) {
+    for (int c = 0; c < cands.n; ++c) {
+        float tE, tX;
+        if (!intersect_obb(cands.xf(c), o, d, tE, tX)) continue;
+        const int prim = cands.prim(c);
+        if (!first && !key_less(lastE, lastP, tE, prim)) continue;
+        window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
+    }
+}
+
+// The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
+// segment list. Entries [0, nxt) are admitted; an admitted entry is live while
+// tExit > ts. The reference's `ts >= tMax` break is implied: it only fires once every
+// segment is admitted and retired, where the empty-active-set branch breaks on the same step.
+template <int CAP, class Cands>
+__device__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d, float jit,
+                            const MarchDev &mp, const float4 *__restrict__ payload,
+                            const unsigned long long *tab) {
+    RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    bool more = false;
+    window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
+    if (cnt == 0) return out;
+    out.hit = 1;
+    const float dt = mp.dt;
+    const float t0 = w.E(0);
+    int nxt = 0, lo = 0;
+    float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    for (long long i = 0;; ++i) {
+        if (i > (1ll << 40)) {  // the reference would spin here; report instead of hanging
+            out.numeric = 1;
+            break;
+        }
+        const float ts = t0 + (__ll2float_rn(i) + jit) * dt;
+        // Admission, refilling the window when it runs dry while hits remain.
+        for (;;) {
+            while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
+            if (nxt < cnt || !more) break;
+            const float lastE = w.E(cnt - 1);
+            const int lastP = cands.prim(w.C(cnt - 1));
+            int live = 0;
+            for (int j = 0; j < nxt; ++j) {
+                if (w.X(j) > ts) {
+                    if (live != j) {
+                        w.E(live) = w.E(j);
+                        w.X(live) = w.X(j);
+                        w.C(live) = w.C(j);
+                    }
+                    ++live;
+                }
+            }
+            if (live == CAP) {
+                out.overflow = 1;
+                return out;
+            }
+            cnt = live;
+            nxt = live;
+            lo = 0;
+            more = false;
+            ++out.refills;
+            window_scan<CAP>(w, cands, cnt, more, o, d, false, lastE, lastP);
+        }
+        while (lo < nxt && w.X(lo) <= ts) ++lo;
+        bool any = false;
+        for (int j = lo; j < nxt; ++j)
+            if (w.X(j) > ts) {
+                any = true;
+                break;
+            }
+        if (!any) {
+            if (nxt >= cnt) break;
+            const float tNext = w.E(nxt);
+            const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
+            if (skipTo > i + 1) i = skipTo - 1;
+            continue;
+        }
+        const V3 pw = o + d * ts;
+        float sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+        for (int j = lo; j < nxt; ++j) {
+            if (!(w.X(j) > ts)) continue;
+            const int c = w.C(j);
+            float sg, r, g, b;
+            sample_primitive(payload, mp.m, cands.prim(c), cands.xf(c), pw, mp.alpha, mp.beta,
+                             tab, sg, r, g, b);
+            sigmaSum += sg;
+            rw += r * sg;
+            gw += g * sg;
+            bw += b * sg;
+            ++out.prim_samples;
+        }
+        ++out.samples;
+        const float dT = sigmaSum * dt;
+        if (transmittance + dT >= 1.0f) {
+            const float frac = (1.0f - transmittance) / dT;
+            const float f = dt * frac;
+            cr += rw * f;
+            cg += gw * f;
+            cb += bw * f;
+            transmittance = 1.0f;
+            out.saturated = 1;
+            break;
+        }
+        cr += rw * dt;
+        cg += gw * dt;
+        cb += bw * dt;
+        transmittance += dT;
+        if (transmittance > 1.0f - mp.eps) {
+            out.early = 1;
+            break;
+        }
+    }
+    out.r = cr;
+    out.g = cg;
+    out.b = cb;
+    out.alpha = transmittance;
+    return out;
+}
+
+__device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
+    od.rgb[3 * p + 0] = ro.r;
+    od.rgb[3 * p + 1] = ro.g;
+    od.rgb[3 * p + 2] = ro.b;
+    od.alpha[p] = ro.alpha;
+    if (od.samples) od.samples[p] = ro.samples;
+}
+
+// Warp-aggregated counter update: one atomic per warp per counter.
+__device__ __forceinline__ void add_counters(DevCounters *ctr, const RayOut &ro, bool valid) {
+    unsigned long long v[7] = {(unsigned long long)(valid ? ro.samples : 0),
+                               (unsigned long long)(valid ? ro.prim_samples : 0),
+                               (unsigned long long)(valid ? ro.hit : 0),
+                               (unsigned long long)(valid ? ro.early : 0),
+                               (unsigned long long)(valid ? ro.saturated : 0),
+                               (unsigned long long)(valid ? ro.refills : 0),
+                               (unsigned long long)(valid ? ro.numeric : 0)};
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+    if ((threadIdx.x & 31) == 0) {
+        if (v[0]) atomicAdd(&ctr->ray_samples, v[0]);
+        if (v[1]) atomicAdd(&ctr->prim_samples, v[1]);
+        if (v[2]) atomicAdd(&ctr->hit_rays, v[2]);
+        if (v[3]) atomicAdd(&ctr->early_exits, v[3]);
+        if (v[4]) atomicAdd(&ctr->saturated, v[4]);
+        if (v[5]) atomicAdd(&ctr->refills, v[5]);
+        if (v[6]) atomicAdd(&ctr->numeric_fail, v[6]);
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// K5: one CTA per 16x16 tile. Warps cover 8x4 pixel blocks (better ray coherence than 16x2
+// rows). Shared memory: staged candidate transforms + the per-ray segment windows.
+template <int CAP>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
+              const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
+              const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
+              int *__restrict__ ovf_list, int ovf_cap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4 *s_xf4 = reinterpret_cast<float4 *>(smem);                      // kCandCap*16 f
+    int *s_prim = reinterpret_cast<int *>(s_xf4 + kCandCap * 4);           // kCandCap
+    unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(s_prim + kCandCap);  // 32
+    float *s_we = reinterpret_cast<float *>(s_tab + 32);                   // CAP*256
+    float *s_wx = s_we + CAP * kMarchThreads;
+    int *s_wc = reinterpret_cast<int *>(s_wx + CAP * kMarchThreads);
+
+    if (ctr->key_overflow) return;
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const uint32_t start = offsets[tile];
+    const int n = (int)(offsets[tile + 1] - start);
+    const int staged = n < kCandCap ? n : kCandCap;
+    const int tid = threadIdx.x;
+    if (tid < 32) s_tab[tid] = kExp2fTab[tid];
+    for (int i = tid; i < staged * 4; i += kMarchThreads) {
+        const int c = i >> 2, q = i & 3;
+        const int prim = (int)(uint32_t)(entries[start + c] & 0xffffffffull);
+        if (q == 0) s_prim[c] = prim;
+        s_xf4[i] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
+    }
+    __syncthreads();
+
+    const int wid = tid >> 5, lane = tid & 31;
+    const int px = tx * kTile + (wid & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (wid >> 1) * 4 + (lane >> 3);
+    const bool valid = px < cam.width && py < cam.height;
+    RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t p = (int64_t)py * cam.width + px;
+    if (valid && n > 0) {
+        V3 o, d;
+        generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+        const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
+        TileCands cands{entries, xf_g, s_prim, reinterpret_cast<const float *>(s_xf4), start, n, staged};
+        Window w{s_we, s_wx, s_wc, kMarchThreads, tid};
+        ro = march_ray<CAP>(cands, w, o, d, jit, mp, payload, s_tab);
+        if (ro.overflow) {
+            const int slot = atomicAdd(&ctr->overflow_rays, 1ull);
+            if (slot < ovf_cap) ovf_list[slot] = (int)p;
+        }
+    }
+    if (valid && !ro.overflow) write_pixel(od, p, ro);
+    add_counters(ctr, ro, valid && !ro.overflow);
+}
+
+// K5b: rays whose live segments overflowed the shared-memory window are re-marched with a
+// kFallbackCap-entry window in global scratch (one window per thread of a fixed grid).
+template <bool kRays>
+__global__ void __launch_bounds__(kFallbackThreads)
+k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+                 const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
+                 const unsigned long long *__restrict__ entries, OutDev od, RaysDev rays,
+                 DevCounters *ctr, const int *__restrict__ ovf_list, int ovf_cap,
+                 float *scratch_e, float *scratch_x, int *scratch_c) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    if (!kRays && ctr->key_overflow) return;
+    const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    Window w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    for (int q = gtid; q < n_ovf; q += nthreads) {
+        const int p = ovf_list[q];
+        V3 o, d;
+        float jit = 0.5f;
+        RayOut ro;
+        if (kRays) {
+            o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
+            d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
+            if (rays.jitter) jit = rays.jitter[p];
+            AllCands cands{xf_g, n_prim};
+            ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
+        } else {
+            const int px = p % cam.width, py = p / cam.width;
+            const int tile = (py / kTile) * cam.tiles_x + px / kTile;
+            generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+            if (mp.jitter) jit = hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p));
+            const uint32_t start = offsets[tile];
+            TileCands cands{entries, xf_g, nullptr, nullptr, start, (int)(offsets[tile + 1] - start), 0};
+            ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
+        }
+        if (ro.overflow) {
+            atomicAdd(&ctr->fallback_fail, 1);
+            continue;
+        }
+        write_pixel(od, p, ro);
+        // counters: plain atomics (rare path)
+        atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);
+        atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
+        atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
+        atomicAdd(&ctr->early_exits, (unsigned long long)ro.early);
+        atomicAdd(&ctr->saturated, (unsigned long long)ro.saturated);
+        atomicAdd(&ctr->refills, (unsigned long long)ro.refills);
+        if (ro.numeric) atomicAdd(&ctr->numeric_fail, 1ull);
+    }
+}
+
+// march() over caller rays (one thread per ray, all primitives as candidates).
+constexpr int kRayThreads = 128;
+template <int CAP>
+__global__ void __launch_bounds__(kRayThreads)
+k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+             const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, OutDev od,
+             DevCounters *ctr, int *__restrict__ ovf_list, int ovf_cap) {
+    __shared__ unsigned long long s_tab[32];
+    __shared__ float s_we[CAP * kRayThreads], s_wx[CAP * kRayThreads];
+    __shared__ int s_wc[CAP * kRayThreads];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    const int64_t r = blockIdx.x * (int64_t)kRayThreads + threadIdx.x;
+    const bool valid = r < n_rays;
+    RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (valid) {
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        AllCands cands{xf_g, n_prim};
+        Window w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
+        ro = march_ray<CAP>(cands, w, o, d, jit, mp, payload, s_tab);
+        if (ro.overflow) {
+            const int slot = atomicAdd(&ctr->overflow_rays, 1ull);
+            if (slot < ovf_cap) ovf_list[slot] = (int)r;
+        }
+    }
+    if (valid && !ro.overflow) write_pixel(od, r, ro);
+    add_counters(ctr, ro, valid && !ro.overflow);
+}
+
+// Zero the outputs of tiles without candidates is implicit in k_march_tiles (n == 0 path);
+// composite() is elementwise.
+__global__ void k_composite(const float *__restrict__ rgb, const float *__restrict__ alpha,
+                            const float *__restrict__ bg, float *__restrict__ out, int64_t n_px) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n_px) return;
+    const float a = alpha[p];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[3 * p + c] = a * rgb[3 * p + c] + (1.0f - a) * bg[3 * p + c];
+}
+
+__global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64_t n) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = expf_glibc(x[i], s_tab);
+}
+
+// ----------------------------------------------------------------------------------------
+// Host-side launchers (plain C++ signatures for vpb_api.cpp).
+constexpr int kWindowCap = 16;
+
+size_t march_tiles_smem() {
+    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 4 + 32 * 8 +
+           (size_t)kWindowCap * kMarchThreads * 12;
+}
+
+cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
+                          cudaStream_t st) {
+    const int64_t total = n_prim * m3;
+    if (total == 0) return cudaSuccess;
+    const int blocks = (int)((total + 255) / 256 < 148 * 64 ? (total + 255) / 256 : 148 * 64);
+    k_repack<<<blocks, 256, 0, st>>>(planar, inter, n_prim, m3);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream_t st) {
+    if (n_prim == 0) return cudaSuccess;
+    k_pad_xf<<<(n_prim * kXfStride + 255) / 256, 256, 0, st>>>(xf15, xf16, n_prim);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
+                           uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
+                           uint32_t *cursor, unsigned long long *entries, int64_t capacity,
+                           DevCounters *ctr, cudaStream_t st) {
+    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
+    if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, keys, tile_counts);
+    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, ctr, capacity);
+    if (n_prim > 0) k_emit<<<(n_prim + 127) / 128, 128, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
+    k_tile_sort<<<n_tiles, 128, 0, st>>>(offsets, entries, ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                               const float4 *payload, const uint32_t *offsets,
+                               const unsigned long long *entries, const OutDev &od,
+                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
+    static bool attr_set = false;
+    const size_t smem = march_tiles_smem();
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_march_tiles<kWindowCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    const int n_tiles = cam.tiles_x * cam.tiles_y;
+    if (n_tiles == 0) return cudaSuccess;
+    k_march_tiles<kWindowCap><<<n_tiles, kMarchThreads, smem, st>>>(cam, mp, xf16, payload, offsets,
+                                                                  entries, od, ctr, ovf_list, ovf_cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
+                                  const float *xf16, int n_prim, const float4 *payload,
+                                  const uint32_t *offsets, const unsigned long long *entries,
+                                  const OutDev &od, const RaysDev &rays, DevCounters *ctr,
+                                  const int *ovf_list, int ovf_cap, float *se, float *sx,
+                                  int *sc, cudaStream_t st) {
+    if (rays_mode)
+        k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
+            cam, mp, xf16, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+    else
+        k_march_fallback<false><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
+            cam, mp, xf16, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
+                              const float4 *payload, const RaysDev &rays, int64_t n_rays,
+                              const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                              cudaStream_t st) {
+    if (n_rays == 0) return cudaSuccess;
+    k_march_rays<kWindowCap><<<(unsigned)((n_rays + kRayThreads - 1) / kRayThreads), kRayThreads, 0, st>>>(
+        mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
+                             int64_t n_px, cudaStream_t st) {
+    if (n_px == 0) return cudaSuccess;
+    k_composite<<<(unsigned)((n_px + 255) / 256), 256, 0, st>>>(rgb, alpha, bg, out, n_px);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_expf<<<148 * 8, 256, 0, st>>>(x, y, n);
+    return cudaGetLastError();
+}
+
+} // namespace vpb

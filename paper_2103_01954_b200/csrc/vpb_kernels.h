@@ -1,0 +1,76 @@
+// vpb_kernels.h — launch interface between the C-ABI host code (vpb_api.cpp) and the
+// sm_100a kernels (vpb_kernels.cu). Internal header; not part of the public boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "vpb_camdev.h"
+
+namespace vpb {
+
+struct DevCounters {
+    unsigned long long ray_samples, prim_samples, hit_rays, early_exits, saturated;
+    unsigned long long overflow_rays, refills, keys, numeric_fail;
+    int key_overflow;
+    int fallback_fail;
+};
+
+struct MarchDev {
+    float dt, eps;
+    int jitter, m;
+    unsigned long long seed;
+    float alpha;
+    int beta;
+};
+
+struct OutDev {
+    float *rgb;
+    float *alpha;
+    int *samples;
+};
+
+struct RaysDev {
+    const float *origins;
+    const float *dirs;
+    const float *jitter;
+};
+
+constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
+constexpr int kFallbackBlocks = 148;   // one CTA per SM
+constexpr int kFallbackThreads = 128;
+
+size_t march_tiles_smem();
+
+}  // namespace vpb
+
+namespace vpb {
+
+cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
+                          cudaStream_t st);
+cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream_t st);
+cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
+                           uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
+                           uint32_t *cursor, unsigned long long *entries, int64_t capacity,
+                           DevCounters *ctr, cudaStream_t st);
+cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                               const float4 *payload, const uint32_t *offsets,
+                               const unsigned long long *entries, const OutDev &od,
+                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st);
+cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
+                                  const float *xf16, int n_prim, const float4 *payload,
+                                  const uint32_t *offsets, const unsigned long long *entries,
+                                  const OutDev &od, const RaysDev &rays, DevCounters *ctr,
+                                  const int *ovf_list, int ovf_cap, float *se, float *sx,
+                                  int *sc, cudaStream_t st);
+cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
+                              const float4 *payload, const RaysDev &rays, int64_t n_rays,
+                              const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                              cudaStream_t st);
+cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
+cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
+                             int64_t n_px, cudaStream_t st);
+
+}  // namespace vpb

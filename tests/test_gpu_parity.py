@@ -1,0 +1,161 @@
+"""GPU parity: the sm_100a path through the C-ABI against the reference's own outputs.
+
+Bar: bit-exact. Every expected value in tests/golden was produced by the unmodified reference
+(oracle/gen_golden.py); the binning artefacts (no reference counterpart) are compared with
+the CPU restatement in oracle/vp_oracle.c.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_groups
+from golden_cases import render_cases, sha
+from paper_2103_01954_b200 import api, synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_bit_equal(name, got, want):
+    g, w = np.asarray(got), np.asarray(want)
+    assert g.shape == w.shape, f"{name}: shape {g.shape} != {w.shape}"
+    if g.dtype == np.float32:
+        neq = bits(g) != bits(w)
+    else:
+        neq = g != w
+    if neq.any():
+        idx = np.argwhere(neq)[:5]
+        diff = np.abs(g.astype(np.float64) - w.astype(np.float64)).max()
+        raise AssertionError(f"{name}: {int(neq.sum())} elements differ (max abs {diff:.3g}); first {idx.tolist()}")
+
+
+@pytest.mark.parametrize("case", sorted(load_groups("renders")))
+def test_render_matches_reference(renderer, case):
+    c = render_cases()[case]
+    renderer.set_scene_composed(api.compose(c["tr"]) if len(c["tr"]) else np.zeros((0, 15), np.float32),
+                                api.PrimitiveSlab(len(c["tr"]), c["m"], c["payload"]), c["window"])
+    out = renderer.render(c["cam"], c["cfg"])
+    assert_bit_equal(f"{case}.rgb", out.color, c["rgb"])
+    assert_bit_equal(f"{case}.alpha", out.alpha, c["alpha"])
+    assert_bit_equal(f"{case}.samples", out.sample_counts, c["samples"])
+    if out.stats is not None and len(c["tr"]):
+        assert out.stats["ray_samples"] == int(c["samples"].sum())
+
+
+DIGESTS = json.loads((GOLDEN / "digests.json").read_text())
+
+
+@pytest.mark.parametrize("key", sorted(DIGESTS["renders"]))
+def test_full_size_render_digest(renderer, key):
+    """BASELINE.json configs 1-4 (+ four views of config 5) at full size, bit-exact."""
+    d = DIGESTS["renders"][key]
+    tr, pay = synthetic.shell_arrays(d["K"], d["M"])
+    gen = DIGESTS["generator"][f"{d['K']}x{d['M']}"]
+    assert sha(tr) == gen["tr"] and sha(pay) == gen["payload"], "synthetic generator drifted"
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(d["K"], d["M"], pay), api.WindowParams())
+    cam = synthetic.shell_camera(d["view"], d["n_views"], d["W"])
+    out = renderer.render(cam, api.MarchConfig())
+    assert out.total_samples() == d["total_samples"]
+    assert int((out.sample_counts > 0).sum()) == d["hit_pixels"]
+    assert sha(out.sample_counts) == d["samples"]
+    assert sha(out.alpha) == d["alpha"]
+    assert sha(out.color) == d["rgb"]
+    assert out.stats["ray_samples"] == d["total_samples"]
+
+
+def test_march_kats_match_reference(renderer):
+    """test_march.cpp:50-194 scenarios plus random rays, through vp_march_rays."""
+    for name, g in load_groups("march_kats").items():
+        k = g["xf"].shape[0]
+        renderer.set_scene_composed(g["xf"], api.PrimitiveSlab(k, int(g["m"]), g["payload"]),
+                                    api.WindowParams(float(g["window"][0]), int(g["window"][1])))
+        cfg = api.MarchConfig(float(g["cfg"][0]), float(g["cfg"][1]))
+        rgb, alpha, samples = renderer.march_rays(g["o"], g["d"], cfg, g["jit"])
+        assert_bit_equal(f"{name}.rgb", rgb, g["rgb"])
+        assert_bit_equal(f"{name}.alpha", alpha, g["alpha"])
+        assert_bit_equal(f"{name}.samples", samples, g["samples"])
+
+
+def test_march_kat_properties(renderer):
+    """The analytic statements of test_march.cpp on the device results."""
+    g = load_groups("march_kats")
+    res = {}
+    for name in ("constant_medium", "saturation", "early_exact", "early_lazy"):
+        c = g[name]
+        renderer.set_scene_composed(c["xf"], api.PrimitiveSlab(c["xf"].shape[0], int(c["m"]), c["payload"]),
+                                    api.WindowParams(float(c["window"][0]), int(c["window"][1])))
+        res[name] = renderer.march_rays(c["o"], c["d"], api.MarchConfig(float(c["cfg"][0]), float(c["cfg"][1])))
+    rgb, alpha, samples = res["constant_medium"]
+    assert abs(alpha[0] - 0.4) < 0.004 and abs(rgb[0, 0] - 0.32) < 0.0032 and abs(samples[0] - 2000) < 20
+    rgb, alpha, samples = res["saturation"]
+    assert alpha[0] == 1.0 and samples[0] < 600
+    assert np.allclose(rgb[0], [0.3, 0.9, 0.5], rtol=1e-4)
+    assert res["early_lazy"][2][0] < res["early_exact"][2][0]
+
+
+def test_binning_matches_cpu_restatement(renderer, oracle):
+    """Cull rectangles, depth keys and per-tile (depth, prim)-sorted lists: bit-exact."""
+    cases = render_cases()
+    for name in ("shell64_m16_w64", "random_boxes_96x72", "camera_inside_40x32"):
+        c = cases[name]
+        xf = api.compose(c["tr"])
+        renderer.set_scene_composed(xf, api.PrimitiveSlab(len(xf), c["m"], c["payload"]), c["window"])
+        rects, keys, offs, prims = renderer.debug_tiles(c["cam"])
+        orects, okeys = oracle.cull(xf, c["cam"])
+        ooffs, oprims = oracle.tile_lists(xf, c["cam"])
+        assert np.array_equal(rects, orects), name
+        assert np.array_equal(keys, okeys), name
+        assert np.array_equal(offs, ooffs), name
+        assert np.array_equal(prims, oprims), name
+    for k, m, w in ((4096, 16, 1024), (32768, 8, 1024)):
+        tr, pay = synthetic.shell_arrays(k, m)
+        xf = api.compose(tr)
+        renderer.set_scene_composed(xf, api.PrimitiveSlab(k, m, pay), api.WindowParams())
+        cam = synthetic.shell_camera(-1, 0, w)
+        rects, keys, offs, prims = renderer.debug_tiles(cam)
+        ooffs, oprims = oracle.tile_lists(xf, cam)
+        assert np.array_equal(offs, ooffs) and np.array_equal(prims, oprims), (k, m)
+
+
+def test_expf_port_is_glibc_exact_on_window_range(renderer, oracle):
+    """Every float in [-24, 0] (the window argument range at alpha = 8): device == libm expf."""
+    lo, hi = 0x80000000, 0xC1C00000  # -0.0 .. -24.0
+    step = 1 << 26
+    bad = 0
+    for start in range(lo, hi + 1, step):
+        end = min(start + step - 1, hi)
+        x = np.arange(start, end + 1, dtype=np.uint64).astype(np.uint32).view(np.float32)
+        y = renderer.debug_expf(x)
+        bad += oracle.expf_mismatches(start, end, y)
+    assert bad == 0
+
+
+def test_render_is_deterministic_and_stats_consistent(renderer):
+    tr, pay = synthetic.shell_arrays(512, 8)
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(512, 8, pay), api.WindowParams())
+    cam = synthetic.shell_camera(7, 64, 512)
+    a = renderer.render(cam, api.MarchConfig(jitter=True, seed=3))
+    b = renderer.render(cam, api.MarchConfig(jitter=True, seed=3))
+    c = renderer.render(cam, api.MarchConfig(jitter=True, seed=4))
+    assert np.array_equal(bits(a.color), bits(b.color)) and np.array_equal(a.sample_counts, b.sample_counts)
+    assert not np.array_equal(bits(a.color), bits(c.color))
+    assert a.stats["ray_samples"] == a.total_samples()
+    # a ray can intersect a segment shorter than the lattice spacing and take no sample
+    assert a.stats["hit_rays"] >= int((a.sample_counts > 0).sum())
+
+
+def test_composite_matches_reference_formula(renderer, oracle):
+    rng = np.random.default_rng(1)
+    out = api.RenderOutput(rng.uniform(0, 1, (24, 40, 3)).astype(np.float32),
+                           rng.uniform(0, 1, (24, 40, 1)).astype(np.float32), np.zeros(960, np.int32))
+    bg = rng.uniform(0, 1, (24, 40, 3)).astype(np.float32)
+    got = renderer.composite(out, bg)
+    want = oracle.composite(out.color, out.alpha, bg)
+    assert_bit_equal("composite", got, want)
+    with pytest.raises(api.Error) as e:
+        renderer.composite(out, bg[:, :39])
+    assert e.value.category == api.ErrorCategory.USAGE
