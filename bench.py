@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 raymarcher (BASELINE.json: Msamples/s and frames/s at 1024^2, HBM
+GB/s against the B200 peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+Workload (one "step"): each GPU renders `--views-per-gpu` views (default 8) of the 64-view
+ring around the headline scene, mvp_shell K=4096 primitives x 16^3 voxels (BASELINE config 3)
+at 1024x1024: rank r renders views [8r, 8r+8) mod 64, so at 8 GPUs one step is the whole
+config-5 batch (view sharding, fixed work per GPU -> "weak" scaling). With N > 1 every view's
+outputs (rgb, alpha, sample count: 20 B/pixel) are gathered to rank 0 with NCCL, overlapped
+with rendering the next view.
+
+Printed JSON line (rank 0): value = ray-samples of all ranks / max-over-ranks device time of
+the K timed steps; roofline = the raymarch kernel's algorithmic bytes (128 B per
+primitive-sample + 20 B per pixel) per launch / its CUDA-event duration vs the
+measured HBM peak; e2e = the same metric through the public C-ABI with pinned host buffers
+(per step: H2D of the frame's transforms, D2H of every view's outputs); cpu_baseline = the
+unmodified reference renderer (oracle/_ref) on this host's cores, bounded sample.
+`--impl reference` times that reference renderer alone (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_RING = 64
+BYTES_PER_PRIM_SAMPLE = 128   # 8 trilinear corners x float4 (primitive.cpp:78-90 x 4 channels)
+BYTES_PER_PIXEL = 20          # rgb 12 + alpha 4 + sample count 4
+METRIC = "Msamples/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--k", type=int, default=4096)
+    p.add_argument("--m", type=int, default=16)
+    p.add_argument("--width", type=int, default=1024)
+    p.add_argument("--views-per-gpu", type=int, default=8)
+    p.add_argument("--no-gather", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--quick", action="store_true", help="profiling mode: no baseline / e2e")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        time.sleep(0.05)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        loaded = [s for s in sm if s > 600] or sm
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+class CpuReference:
+    """The unmodified reference volprim::render (oracle/_ref/libvolprim_ref.so) on this host's
+    cores (std::thread x hardware_concurrency, threads.h:16-36); the C restatement when the
+    reference core was not built ("port")."""
+
+    def __init__(self, k, m, width):
+        from oracle.bindings import Oracle, RefCore
+        from paper_2103_01954_b200 import api, synthetic
+        self.k, self.m, self.width = k, m, width
+        self.tr, self.pay = synthetic.shell_arrays(k, m)
+        self.win, self.cfg = api.WindowParams(), api.MarchConfig()
+        self.synthetic = synthetic
+        if RefCore.available():
+            self.core, self.kind, self.xf = RefCore(), "reference", self.tr
+        else:
+            self.core, self.kind, self.xf = Oracle(), "port", api.compose(self.tr)
+        self.cores = os.cpu_count() or 1
+
+    def render(self, view):
+        cam = self.synthetic.shell_camera(view, N_RING, self.width)
+        return int(self.core.render(self.xf, self.m, self.pay, self.win, cam, self.cfg)[2].sum())
+
+    def sample(self, views, budget_s):
+        """(ray-samples, seconds, n_views) for views rendered until budget_s is spent."""
+        total, t0, n = 0, time.perf_counter(), 0
+        for v in views:
+            total += self.render(v)
+            n += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        return total, time.perf_counter() - t0, n
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference's own CPU renderer, rank 0 only."""
+    if rank != 0:
+        return
+    views = [i % N_RING for i in range(args.warmup + args.steps)]
+    step_s, step_samples = [], []
+    ref = CpuReference(args.k, args.m, args.width)
+    kind, cores = ref.kind, ref.cores
+    for i, v in enumerate(views):
+        s, dt, _ = ref.sample([v], 1e9)
+        if i >= args.warmup:
+            step_s.append(dt)
+            step_samples.append(s)
+    t = sum(step_s)
+    value = sum(step_samples) / t / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": METRIC,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, 1, False) | {"views_per_step": 1},
+            "frames_per_s": round(args.steps / t, 4),
+            "cpu_baseline": {"value": round(value, 3), "unit": METRIC, "cores": cores, "kind": kind,
+                             "sample": f"1 view of the 64-view ring per step, {args.steps} steps "
+                                       f"(reference volprim::render, std::thread x hardware_concurrency)"},
+            "e2e": {"value": round(value, 3), "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world, gather):
+    return {"workload": f"mvp_shell K={args.k} M={args.m} at {args.width}x{args.width}: "
+                        f"{args.views_per_gpu} views/GPU/step of the 64-view ring (BASELINE configs 3+5, "
+                        f"view-sharded)",
+            "K": args.k, "M": args.m, "width": args.width, "height": args.width,
+            "views_per_gpu": args.views_per_gpu, "parallelism": f"view-shard x{world}",
+            "gather_to_rank0": gather, "march": "dt=1mm earlyEps=0.01 window 8/8 no jitter",
+            "l2": "flushed (256 MiB write) before every timed step; payload 268 MB > 126 MB L2"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_01954_b200 import Renderer, api, synthetic
+    from paper_2103_01954_b200._lib import f32p, i32p, vp_camera, vp_march, vp_stats
+    from paper_2103_01954_b200.dist import ViewGather, broadcast_scene, view_shard
+    import ctypes as C
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    gather = world > 1 and not args.no_gather
+    k, m, w = args.k, args.m, args.width
+    V = args.views_per_gpu
+    r = Renderer(local)
+
+    # scene: built on rank 0, broadcast once (payload already repacked)
+    xf = slab = None
+    if rank == 0:
+        tr, pay = synthetic.shell_arrays(k, m)
+        xf = api.compose(tr)
+        slab = api.PrimitiveSlab(k, m, pay)
+    win = api.WindowParams()
+    if world > 1:
+        bcast_bytes = broadcast_scene(r, xf, slab, win, k, m, device)
+    else:
+        r.set_scene_composed(xf, slab, win)
+        bcast_bytes = 0
+    views = view_shard(N_RING, world, rank, per_rank=V)
+    cams = [synthetic.shell_camera(v, N_RING, w).to_c() for v in views]
+    cfg = api.MarchConfig()
+    mc = cfg.to_c()
+
+    # deterministic per-view counts (bit-exact renders), measured once outside the timed region
+    per_view = []
+    for cam in cams:
+        out = r.render(api.Camera.from_c(cam), cfg)
+        per_view.append(out.stats)
+    ray_samples = sum(s["ray_samples"] for s in per_view)
+    prim_samples = sum(s["prim_samples"] for s in per_view)
+    r.kernel_times()
+
+    vg = ViewGather(V, w, w, device, world, rank)
+    # a dedicated (non-default) stream: the renders, the timing events and the NCCL gathers'
+    # dependencies all hang off it
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
+    sh = stream.cuda_stream
+    assert sh != 0
+    lib = r._lib
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    rgb, alpha, samples = vg.views()
+
+    def step(i):
+        for j, cam in enumerate(cams):
+            rc = lib.vp_render_async(r.ctx, C.byref(cam), C.byref(mc), C.cast(rgb[j].data_ptr(), f32p),
+                                     C.cast(alpha[j].data_ptr(), f32p), C.cast(samples[j].data_ptr(), i32p),
+                                     C.c_void_p(sh))
+            if rc:
+                raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+            if gather:
+                vg.gather_view(j)
+        if gather:
+            vg.finish()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    rc_stats = vp_stats()
+    if lib.vp_read_stats(r.ctx, C.byref(rc_stats)):
+        raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+    r.kernel_times()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)                 # evict L2 (untimed)
+        evs[i][0].record(stream)
+        step(args.warmup + i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_local = sum(step_ms) / 1e3
+    march_ms = r.kernel_times(4096)
+    t = torch.tensor([t_local], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    totals = torch.tensor([ray_samples * args.steps, prim_samples * args.steps, V * args.steps],
+                          dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(totals)
+    all_ray, all_prim, all_views = (float(x) for x in totals.tolist())
+    value = all_ray / t_max / 1e6
+
+    # roofline of the dominant kernel (raymarch K5 + fallback K5b), per launch
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    alg_bytes_per_launch = (BYTES_PER_PRIM_SAMPLE * prim_samples + BYTES_PER_PIXEL * w * w * V) / V
+    march_avg_s = float(np.mean(march_ms)) / 1e3 if len(march_ms) else float("nan")
+    achieved = alg_bytes_per_launch / march_avg_s / 1e9
+    frame_s = t_local / (V * args.steps)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "kernel": "k_march_tiles (+k_march_fallback)", "peak_kind": pk_kind,
+                "alg_bytes_per_launch": int(alg_bytes_per_launch), "avg_launch_ms": round(march_avg_s * 1e3, 4),
+                "march_share_of_step": round(float(np.sum(march_ms)) / max(sum(step_ms), 1e-9), 4),
+                "frame_ms": round(frame_s * 1e3, 4),
+                "frame_frac": round(alg_bytes_per_launch / frame_s / 1e9 / hbm, 4)}
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            tr_ = json.loads(prof.read_text())
+            key = f"K{k}_M{m}_W{w}"
+            if key in tr_:
+                roofline["traffic"] = tr_[key]["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tr_[key]["source"]
+        except Exception:
+            pass
+
+    # e2e: public C-ABI, pinned host buffers, per step: transforms H2D + outputs D2H
+    e2e = None
+    if not (args.no_e2e or args.quick):
+        n_px = w * w
+        h_rgb = torch.empty(n_px * 3, dtype=torch.float32, pin_memory=True)
+        h_alpha = torch.empty(n_px, dtype=torch.float32, pin_memory=True)
+        h_samp = torch.empty(n_px, dtype=torch.int32, pin_memory=True)
+        if world > 1:
+            xf_host = torch.empty((k, 15), dtype=torch.float32)
+            xf_dev = torch.empty((k, 15), dtype=torch.float32, device=device)
+            if rank == 0:
+                xf_dev.copy_(torch.from_numpy(xf))
+            dist.broadcast(xf_dev, 0)
+            xf_host = xf_dev.cpu().pin_memory()
+        else:
+            xf_host = torch.from_numpy(xf).pin_memory()
+        st = vp_stats()
+
+        def e2e_step():
+            if lib.vp_set_transforms(r.ctx, k, C.cast(xf_host.data_ptr(), f32p)):
+                raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+            for cam in cams:
+                if lib.vp_render(r.ctx, C.byref(cam), C.byref(mc), C.cast(h_rgb.data_ptr(), f32p),
+                                 C.cast(h_alpha.data_ptr(), f32p), C.cast(h_samp.data_ptr(), i32p), C.byref(st)):
+                    raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        n_e2e = max(3, args.steps // 2)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(all_ray / args.steps * n_e2e / float(te.item()) / 1e6, 3), "unit": METRIC,
+               "h2d_bytes_per_step": 15 * 4 * k, "d2h_bytes_per_step": BYTES_PER_PIXEL * n_px * V,
+               "steps": n_e2e, "api": "vp_set_transforms + vp_render (pinned host outputs)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
+        ref = CpuReference(k, m, w)
+        s, dt, nv = ref.sample(views, args.cpu_seconds)
+        cpu = {"value": round(s / dt / 1e6, 3), "unit": METRIC, "cores": ref.cores, "kind": ref.kind,
+               "sample": f"{nv} view(s) of this rank's views, full {w}x{w} frames, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": METRIC, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": workload_config(args, world, gather),
+                "frames_per_s": round(all_views / t_max, 2),
+                "prim_samples_per_s": round(all_prim / t_max / 1e6, 3),
+                "ray_samples_per_view": ray_samples // V, "prim_samples_per_view": prim_samples // V,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": 6 * V * args.steps,
+                "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
+                "stats_last_view": rc_stats.as_dict()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    r.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,10 @@ int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m,
                                const float *payload_interleaved);
 /* Device pointer / float count of the resident interleaved payload (for broadcasts). */
 int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats);
+/* Copy the resident interleaved payload to dst (host or device, K*M^3*4 floats). */
+int vp_copy_payload(vp_ctx *ctx, float *dst);
+/* (vp_set_scene accepts payload_planar == NULL: the payload is then allocated but
+ *  undefined until vp_set_payload_interleaved.) */
 
 /* ---- render (the drop-in for volprim::render) --------------------------------------------
  * Synchronous. rgb: H*W*3, alpha: H*W, samples: H*W (nullable), stats nullable. */
@@ -121,6 +125,10 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
 int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb_dev,
                     float *alpha_dev, int32_t *samples_dev, void *stream);
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats);
+/* Device durations (CUDA events on the launching stream) of the raymarch kernels (K5 + K5b)
+ * of the renders enqueued since the previous call, oldest first, at most the last 256.
+ * Synchronises on those events; *n receives the count written. */
+int vp_kernel_times(vp_ctx *ctx, int64_t max, float *march_ms, int64_t *n);
 
 /* march() over arbitrary rays (march.h:42-44 with intersect(), lbvh.cpp:207-234, as the
  * candidate source over all K primitives). jitter01 nullable (0.5). Synchronous. */

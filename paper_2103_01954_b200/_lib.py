@@ -52,6 +52,8 @@ SIGNATURES = {
     "vp_set_transforms": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
     "vp_set_payload_interleaved": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p]),
     "vp_payload_device": (C.c_int, [C.c_void_p, C.POINTER(f32p), i64p]),
+    "vp_copy_payload": (C.c_int, [C.c_void_p, f32p]),
+    "vp_kernel_times": (C.c_int, [C.c_void_p, C.c_int64, f32p, i64p]),
     "vp_render": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march), f32p, f32p,
                             i32p, C.POINTER(vp_stats)]),
     "vp_render_async": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march), f32p,

@@ -233,12 +233,33 @@ class Renderer:
 
     # -- resident scene ---------------------------------------------------------------
     def set_scene_composed(self, xf15: np.ndarray, slab: PrimitiveSlab, window: WindowParams):
+        """Upload composed transforms and the planar slab (repacked on the device). A slab
+        with payload=None only allocates (fill it with set_payload_interleaved)."""
         xf = _f32(xf15).reshape(-1, 15)
-        pay = _f32(slab.payload)
+        pay = None if slab.payload is None else _f32(slab.payload)
         _check(self._lib.vp_set_scene(self._ctx, xf.shape[0], int(slab.voxels_per_axis),
-                                      _fptr(xf), _fptr(pay), float(window.alpha),
-                                      int(window.beta)), self._ctx)
+                                      _fptr(xf), _fptr(pay) if pay is not None else None,
+                                      float(window.alpha), int(window.beta)), self._ctx)
         self.n_prim, self.m = xf.shape[0], int(slab.voxels_per_axis)
+
+    def payload_floats(self) -> int:
+        return int(self.n_prim or 0) * int(self.m or 0) ** 3 * 4
+
+    def copy_payload_to(self, ptr: int):
+        """Copy the resident channel-interleaved payload to `ptr` (device or host)."""
+        _check(self._lib.vp_copy_payload(self._ctx, C.cast(C.c_void_p(ptr), f32p)), self._ctx)
+
+    def set_payload_interleaved(self, ptr: int):
+        """Adopt an interleaved payload at `ptr` (device or host), e.g. after a broadcast."""
+        _check(self._lib.vp_set_payload_interleaved(self._ctx, int(self.n_prim), int(self.m),
+                                                    C.cast(C.c_void_p(ptr), f32p)), self._ctx)
+
+    def kernel_times(self, max_n: int = 256) -> np.ndarray:
+        """Raymarch-kernel device durations (ms) of the renders since the last call."""
+        out = np.zeros(max_n, np.float32)
+        n = C.c_int64()
+        _check(self._lib.vp_kernel_times(self._ctx, max_n, _fptr(out), C.byref(n)), self._ctx)
+        return out[:n.value]
 
     def set_frame(self, scene: Scene, frame: int):
         if frame < 0 or frame >= len(scene.frames):

@@ -55,6 +55,8 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+constexpr int kTimingSlots = 256;  // march-kernel event pairs kept for vp_kernel_times
+
 }  // namespace
 
 struct vp_ctx {
@@ -79,6 +81,8 @@ struct vp_ctx {
     DevCounters *d_ctr = nullptr, *h_ctr = nullptr;
     int64_t entries_cap = 0;
     int ovf_cap = 0;
+    cudaEvent_t t_ev[2 * kTimingSlots] = {};
+    int64_t t_count = 0;
 };
 
 namespace {
@@ -172,6 +176,8 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
     VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->keys.p,
                                 ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
                                 ctx->entries_cap, ctx->d_ctr, st));
+    const int slot = int(ctx->t_count % kTimingSlots);
+    VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
     VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->payload.p, ctx->offsets.p,
                                     ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
     const RaysDev none{nullptr, nullptr, nullptr};
@@ -179,6 +185,8 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
                                        ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
                                        ctx->ovf_list.p, ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p,
                                        ctx->fb_c.p, st));
+    VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
+    ++ctx->t_count;
     return VP_OK;
 }
 
@@ -249,6 +257,12 @@ int vp_create(int32_t device, vp_ctx **out) {
         vp_destroy(ctx);
         return rc;
     }
+    for (cudaEvent_t &ev : ctx->t_ev)
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) {
+        rc = cuda_fail(nullptr, e, "vp_create");
+        vp_destroy(ctx);
+        return rc;
+    }
     *out = ctx;
     return VP_OK;
 }
@@ -269,6 +283,8 @@ int vp_destroy(vp_ctx *ctx) {
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (cudaEvent_t ev : ctx->t_ev)
+        if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return VP_OK;
@@ -317,7 +333,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     if (int rc = check_ctx(ctx, false)) return rc;
     if (n_prim < 0) return fail(ctx, VP_ERR_USAGE, "negative primitive count");
     if (n_prim > 0 && m < 1) return fail(ctx, VP_ERR_USAGE, "voxels per axis must be >= 1");
-    if (n_prim > 0 && (!xf15 || !payload)) return fail(ctx, VP_ERR_USAGE, "null scene arrays");
+    if (n_prim > 0 && !xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
     if (!std::isfinite(window_alpha)) return fail(ctx, VP_ERR_USAGE, "window alpha must be finite");
     ctx->has_scene = false;
     ctx->n_prim = n_prim;
@@ -333,6 +349,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     const int64_t m3 = int64_t(m) * m * m;
     const size_t nf = size_t(n_prim) * 4 * size_t(m3);
     VP_CUDA(ctx, ctx->payload.ensure(size_t(n_prim) * size_t(m3)));
+    if (!payload) return VP_OK;  // filled later by vp_set_payload_interleaved
     const float *src = payload;
     if (!is_device_ptr(payload)) {
         VP_CUDA(ctx, ctx->planar_tmp.ensure(nf));
@@ -365,6 +382,35 @@ int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats) {
     if (int rc = check_ctx(ctx, true)) return rc;
     if (dev_ptr) *dev_ptr = reinterpret_cast<float *>(ctx->payload.p);
     if (n_floats) *n_floats = int64_t(ctx->n_prim) * ctx->m * ctx->m * ctx->m * 4;
+    return VP_OK;
+}
+
+int vp_copy_payload(vp_ctx *ctx, float *dst) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    const size_t n4 = size_t(ctx->n_prim) * size_t(ctx->m) * ctx->m * ctx->m;
+    if (n4 == 0) return VP_OK;
+    if (!dst) return fail(ctx, VP_ERR_USAGE, "null destination");
+    VP_CUDA(ctx, cudaMemcpyAsync(dst, ctx->payload.p, n4 * sizeof(float4),
+                                 is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
+}
+
+int vp_kernel_times(vp_ctx *ctx, int64_t max, float *march_ms, int64_t *n) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    const int64_t avail = std::min<int64_t>(ctx->t_count, kTimingSlots);
+    const int64_t first = ctx->t_count - avail;
+    int64_t w = 0;
+    for (int64_t i = first; i < ctx->t_count && w < max; ++i, ++w) {
+        const int slot = int(i % kTimingSlots);
+        VP_CUDA(ctx, cudaEventSynchronize(ctx->t_ev[2 * slot + 1]));
+        float ms = 0.f;
+        VP_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->t_ev[2 * slot], ctx->t_ev[2 * slot + 1]));
+        if (march_ms) march_ms[w] = ms;
+    }
+    if (n) *n = w;
+    ctx->t_count = 0;
     return VP_OK;
 }
 

@@ -1,0 +1,106 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL over NVLink/NVSwitch).
+
+The raymarcher shards by view: rays are independent and the scene is
+read-only, so each rank renders its own views with no data-path collective. The only
+communication is
+  * a one-time broadcast of the repacked, channel-interleaved payload (K*M^3*16 bytes) and the
+    composed transforms from rank 0 (`broadcast_scene`), and
+  * optionally, gathering each step's rendered views to rank 0 (`ViewGather`), double-buffered
+    so the transfer of step s overlaps the rendering of step s+1.
+Everything here also runs on CPU tensors with the gloo backend (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import numpy as np
+
+
+def view_shard(n_views: int, world: int, rank: int, per_rank: Optional[int] = None) -> List[int]:
+    """Views rendered by `rank`. With per_rank=None the n_views batch is split into contiguous
+    blocks (strong sharding of a fixed batch); with per_rank=p, rank r renders
+    [r*p, (r+1)*p) modulo n_views (fixed work per GPU)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    if per_rank is None:
+        base, extra = divmod(n_views, world)
+        start = rank * base + min(rank, extra)
+        return list(range(start, start + base + (1 if rank < extra else 0)))
+    return [(rank * per_rank + i) % n_views for i in range(per_rank)]
+
+
+def broadcast_scene(renderer, xf15: Optional[np.ndarray], slab, window, n_prim: int, m: int,
+                    device, src: int = 0):
+    """Rank `src` uploads (and repacks) the frame; the interleaved payload and the composed
+    transforms are broadcast once; the other ranks adopt them without a repack."""
+    import torch
+    import torch.distributed as dist
+
+    from .api import PrimitiveSlab
+
+    rank = dist.get_rank()
+    xf_t = torch.empty((n_prim, 15), dtype=torch.float32, device=device)
+    if rank == src:
+        xf_t.copy_(torch.from_numpy(np.ascontiguousarray(xf15, np.float32)))
+    dist.broadcast(xf_t, src)
+    xf = xf_t.cpu().numpy()
+    if rank == src:
+        renderer.set_scene_composed(xf, slab, window)
+    else:
+        renderer.set_scene_composed(xf, PrimitiveSlab(n_prim, m, None), window)
+    pay = torch.empty(renderer.payload_floats(), dtype=torch.float32, device=device)
+    if rank == src:
+        renderer.copy_payload_to(pay.data_ptr())
+    dist.broadcast(pay, src)
+    if rank != src:
+        renderer.set_payload_interleaved(pay.data_ptr())
+    return pay.numel() * 4
+
+
+class ViewGather:
+    """Per-step output buffer ([views, H*W*5] float32 rows: rgb, alpha, samples as int32
+    bits) and the per-view asynchronous gather to rank `dst`, so the transfer of view j
+    overlaps the rendering of view j+1 (NCCL runs on its own stream after the view's
+    kernels, which are enqueued on torch's current stream)."""
+
+    def __init__(self, n_local: int, width: int, height: int, device, world: int, rank: int,
+                 dst: int = 0):
+        import torch
+        self.hw = width * height
+        self.buf = torch.zeros((n_local, 5 * self.hw), dtype=torch.float32, device=device)
+        self.world, self.rank, self.dst = world, rank, dst
+        self.recv = ([[torch.empty(5 * self.hw, dtype=torch.float32, device=device) for _ in range(world)]
+                      for _ in range(n_local)] if rank == dst else None)
+        self.works = []
+
+    def views(self):
+        """(rgb, alpha, samples) row views, one row per local view."""
+        import torch
+        hw = self.hw
+        return self.buf[:, :3 * hw], self.buf[:, 3 * hw:4 * hw], self.buf[:, 4 * hw:].view(torch.int32)
+
+    def gather_view(self, j: int, async_op: bool = True):
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        w = dist.gather(self.buf[j], self.recv[j] if self.rank == self.dst else None,
+                        dst=self.dst, async_op=async_op)
+        if async_op:
+            self.works.append(w)
+
+    def finish(self):
+        for w in self.works:
+            w.wait()
+        self.works.clear()
+
+    def gathered(self, j: int):
+        """On rank dst: per-rank [5*H*W] rows of local view j."""
+        return self.recv[j]
+
+    @staticmethod
+    def unpack(row, width: int, height: int):
+        """(rgb [H,W,3], alpha [H,W,1], samples [H*W] int32) from one gathered row."""
+        import torch
+        hw = width * height
+        return (row[:3 * hw].reshape(height, width, 3), row[3 * hw:4 * hw].reshape(height, width, 1),
+                row[4 * hw:].view(torch.int32))
