@@ -78,6 +78,8 @@ class Oracle:
         L.vpo_expf_port.argtypes = [C.c_float]
         L.vpo_expf_mismatches.restype = C.c_int64
         L.vpo_expf_mismatches.argtypes = [C.c_uint32, C.c_uint32, f32p]
+        L.vpo_expf_port_mismatches.restype = C.c_int64
+        L.vpo_expf_port_mismatches.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
 
     def compose(self, tr24):
         tr = _f(tr24).reshape(-1, 24)
@@ -165,6 +167,9 @@ class Oracle:
         v = _f(values)
         assert v.size == hi_bits - lo_bits + 1
         return int(self.lib.vpo_expf_mismatches(lo_bits, hi_bits, _p(v)))
+
+    def expf_port_mismatches(self, lo_bits: int, hi_bits: int, stride: int = 1) -> int:
+        return int(self.lib.vpo_expf_port_mismatches(lo_bits, hi_bits, stride))
 
     def composite(self, rgb, alpha, bg):
         h, w = rgb.shape[:2]

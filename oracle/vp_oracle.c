@@ -597,3 +597,18 @@ int64_t vpo_expf_mismatches(uint32_t lo_bits, uint32_t hi_bits, const float *val
     }
     return bad;
 }
+
+/* Counts floats x = bits lo, lo+stride, ... <= hi where vpo_expf_port(x) != libm expf(x). */
+int64_t vpo_expf_port_mismatches(uint32_t lo_bits, uint32_t hi_bits, uint32_t stride) {
+    int64_t bad = 0;
+    if (stride == 0) stride = 1;
+    for (uint64_t u = lo_bits; u <= hi_bits; u += stride) {
+        float x, a, b;
+        const uint32_t w = (uint32_t)u;
+        memcpy(&x, &w, 4);
+        a = expf(x);
+        b = vpo_expf_port(x);
+        if (memcmp(&a, &b, 4) != 0) ++bad;
+    }
+    return bad;
+}

@@ -41,10 +41,10 @@ __device__ __forceinline__ V3 to_model(const float *xf, V3 p) {
     return V3{q.x / xf[12], q.y / xf[13], q.z / xf[14]};
 }
 
-// lbvh.cpp:177-205 — exact oriented slab test in model space.
-__device__ __forceinline__ bool intersect_obb(const float *xf, V3 o, V3 d, float &tEnterOut,
-                                              float &tExitOut) {
-    const V3 om = to_model(xf, o);
+// lbvh.cpp:177-205 — exact oriented slab test in model space, with om = toModel(origin)
+// supplied by the caller (it depends only on the primitive and the ray origin).
+__device__ __forceinline__ bool intersect_obb_om(const float *xf, V3 om, V3 d, float &tEnterOut,
+                                                 float &tExitOut) {
     const V3 q = matTvec(xf + 3, d);
     const V3 dm = V3{q.x / xf[12], q.y / xf[13], q.z / xf[14]};
     float tEnter = -3.402823466e+38f, tExit = 3.402823466e+38f;
@@ -67,6 +67,11 @@ __device__ __forceinline__ bool intersect_obb(const float *xf, V3 o, V3 d, float
     tEnterOut = tEnter;
     tExitOut = tExit;
     return true;
+}
+
+__device__ __forceinline__ bool intersect_obb(const float *xf, V3 o, V3 d, float &tEnterOut,
+                                              float &tExitOut) {
+    return intersect_obb_om(xf, to_model(xf, o), d, tEnterOut, tExitOut);
 }
 
 // camera.cpp:14-23 — pixel (px, py) is x + 0.5, y + 0.5.

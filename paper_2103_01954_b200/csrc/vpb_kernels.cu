@@ -220,12 +220,15 @@ __global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
 }
 
 // ----------------------------------------------------------------------------------------
-// Candidate sources for the per-ray segment window.
+// Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205);
+// for a tile the camera centre is every ray's origin, so om = toModel(origin) is computed
+// once per staged candidate (same operations, same bits) instead of once per ray.
 struct TileCands {  // a tile's sorted bucket, first kCandCap staged in shared memory
     const unsigned long long *entries;
     const float *xf_g;
     const int *s_prim;
     const float *s_xf;
+    const float4 *s_om;
     uint32_t start;
     int n, staged;
     __device__ __forceinline__ int prim(int c) const {
@@ -234,12 +237,22 @@ struct TileCands {  // a tile's sorted bucket, first kCandCap staged in shared m
     __device__ __forceinline__ const float *xf(int c) const {
         return c < staged ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
     }
+    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
+        if (c < staged) {
+            const float4 om = s_om[c];
+            return intersect_obb_om(s_xf + c * kXfStride, mk3(om.x, om.y, om.z), d, tE, tX);
+        }
+        return intersect_obb(xf(c), o, d, tE, tX);
+    }
 };
 struct AllCands {  // every primitive (march over arbitrary rays)
     const float *xf_g;
     int n;
     __device__ __forceinline__ int prim(int c) const { return c; }
     __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
+        return intersect_obb(xf(c), o, d, tE, tX);
+    }
 };
 
 // Per-ray sorted segment window storage: slot j of ray `lane` lives at [j * stride + lane].
@@ -256,7 +269,7 @@ struct Window {
 struct RayOut {
     float r, g, b, alpha;
     int samples;
-    int64_t prim_samples;
+    int prim_samples;
     int hit, early, saturated, overflow, refills, numeric;
 };
 
@@ -290,14 +303,14 @@ __device__ __forceinline__ void window_insert(const Window &w, const Cands &cand
 }
 
 // Fills the window with the smallest hits whose key exceeds (lastE, lastP) (or all hits
-// when first == true).
+// when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order).
 template <int CAP, class Cands>
 __device__ __forceinline__ void window_scan(const Window &w, const Cands &cands, int &cnt,
                                             bool &more, V3 o, V3 d, bool first, float lastE,
                                             int lastP) {
     for (int c = 0; c < cands.n; ++c) {
         float tE, tX;
-        if (!intersect_obb(cands.xf(c), o, d, tE, tX)) continue;
+        if (!cands.hit(c, o, d, tE, tX)) continue;
         const int prim = cands.prim(c);
         if (!first && !key_less(lastE, lastP, tE, prim)) continue;
         window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
@@ -305,75 +318,81 @@ __device__ __forceinline__ void window_scan(const Window &w, const Cands &cands,
 }
 
 // The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
-// segment list. Entries [0, nxt) are admitted; an admitted entry is live while
-// tExit > ts. The reference's `ts >= tMax` break is implied: it only fires once every
+// segment list (filled by window_scan). Entries [0, nxt) are admitted; an admitted entry is
+// live while tExit > ts, and the live ones in window order are exactly the reference's
+// `active` list. The reference's `ts >= tMax` break is implied: it only fires once every
 // segment is admitted and retired, where the empty-active-set branch breaks on the same step.
+//
+// The loop is flattened to one primitive-sample per iteration: a lane first finds its next
+// lattice step with a non-empty active set (admission, retirement, gap skip), then evaluates
+// one active primitive; the step's accumulation happens after its last active primitive. Lanes
+// whose steps have different numbers of active primitives therefore stay in lock-step on
+// primitive-samples instead of waiting for the widest step of the warp.
 template <int CAP, class Cands>
-__device__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d, float jit,
-                            const MarchDev &mp, const float4 *__restrict__ payload,
-                            const unsigned long long *tab) {
+__device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, bool more, V3 o,
+                               V3 d, float jit, const MarchDev &mp,
+                               const float4 *__restrict__ payload, const unsigned long long *tab) {
     RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
-    int cnt = 0;
-    bool more = false;
-    window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
     if (cnt == 0) return out;
     out.hit = 1;
     const float dt = mp.dt;
     const float t0 = w.E(0);
-    int nxt = 0, lo = 0;
+    int nxt = 0, lo = 0, j = 0;
+    long long i = 0;
     float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    for (long long i = 0;; ++i) {
-        if (i > (1ll << 40)) {  // the reference would spin here; report instead of hanging
-            out.numeric = 1;
-            break;
-        }
-        const float ts = t0 + (__ll2float_rn(i) + jit) * dt;
-        // Admission, refilling the window when it runs dry while hits remain.
-        for (;;) {
-            while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
-            if (nxt < cnt || !more) break;
-            const float lastE = w.E(cnt - 1);
-            const int lastP = cands.prim(w.C(cnt - 1));
-            int live = 0;
-            for (int j = 0; j < nxt; ++j) {
-                if (w.X(j) > ts) {
-                    if (live != j) {
-                        w.E(live) = w.E(j);
-                        w.X(live) = w.X(j);
-                        w.C(live) = w.C(j);
-                    }
-                    ++live;
+    float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+    V3 pw = o;
+    bool sampling = false;
+    for (;;) {
+        if (!sampling) {
+            for (;;) {  // next lattice step with a non-empty active set
+                if (i > (1ll << 40)) {  // the reference would spin; report instead of hanging
+                    out.numeric = 1;
+                    goto done;
                 }
+                ts = t0 + (__ll2float_rn(i) + jit) * dt;
+                for (;;) {  // admission, refilling the window when it runs dry
+                    while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
+                    if (nxt < cnt || !more) break;
+                    const float lastE = w.E(cnt - 1);
+                    const int lastP = cands.prim(w.C(cnt - 1));
+                    int live = 0;
+                    for (int q = 0; q < nxt; ++q) {
+                        if (w.X(q) > ts) {
+                            if (live != q) {
+                                w.E(live) = w.E(q);
+                                w.X(live) = w.X(q);
+                                w.C(live) = w.C(q);
+                            }
+                            ++live;
+                        }
+                    }
+                    if (live == CAP) {
+                        out.overflow = 1;
+                        return out;
+                    }
+                    cnt = live;
+                    nxt = live;
+                    lo = 0;
+                    more = false;
+                    ++out.refills;
+                    window_scan<CAP>(w, cands, cnt, more, o, d, false, lastE, lastP);
+                }
+                while (lo < nxt && w.X(lo) <= ts) ++lo;
+                j = lo;
+                while (j < nxt && !(w.X(j) > ts)) ++j;
+                if (j < nxt) break;
+                if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:44
+                const float tNext = w.E(nxt);  // gap skip, march.cpp:45-49
+                const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
+                i = skipTo > i + 1 ? skipTo : i + 1;
             }
-            if (live == CAP) {
-                out.overflow = 1;
-                return out;
-            }
-            cnt = live;
-            nxt = live;
-            lo = 0;
-            more = false;
-            ++out.refills;
-            window_scan<CAP>(w, cands, cnt, more, o, d, false, lastE, lastP);
+            sampling = true;
+            sigmaSum = 0.f;
+            rw = gw = bw = 0.f;
+            pw = o + d * ts;
         }
-        while (lo < nxt && w.X(lo) <= ts) ++lo;
-        bool any = false;
-        for (int j = lo; j < nxt; ++j)
-            if (w.X(j) > ts) {
-                any = true;
-                break;
-            }
-        if (!any) {
-            if (nxt >= cnt) break;
-            const float tNext = w.E(nxt);
-            const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
-            if (skipTo > i + 1) i = skipTo - 1;
-            continue;
-        }
-        const V3 pw = o + d * ts;
-        float sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
-        for (int j = lo; j < nxt; ++j) {
-            if (!(w.X(j) > ts)) continue;
+        {  // one primitive-sample (march.cpp:63-70)
             const int c = w.C(j);
             float sg, r, g, b;
             sample_primitive(payload, mp.m, cands.prim(c), cands.xf(c), pw, mp.alpha, mp.beta,
@@ -384,6 +403,11 @@ __device__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d, flo
             bw += b * sg;
             ++out.prim_samples;
         }
+        ++j;
+        while (j < nxt && !(w.X(j) > ts)) ++j;
+        if (j < nxt) continue;
+        // step complete: march.cpp:71-88
+        sampling = false;
         ++out.samples;
         const float dT = sigmaSum * dt;
         if (transmittance + dT >= 1.0f) {
@@ -404,12 +428,25 @@ __device__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d, flo
             out.early = 1;
             break;
         }
+        ++i;
     }
+done:
     out.r = cr;
     out.g = cg;
     out.b = cb;
     out.alpha = transmittance;
     return out;
+}
+
+template <int CAP, class Cands>
+__device__ __forceinline__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d,
+                                            float jit, const MarchDev &mp,
+                                            const float4 *__restrict__ payload,
+                                            const unsigned long long *tab) {
+    int cnt = 0;
+    bool more = false;
+    window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
+    return march_window<CAP>(cands, w, cnt, more, o, d, jit, mp, payload, tab);
 }
 
 __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
@@ -444,9 +481,18 @@ __device__ __forceinline__ void add_counters(DevCounters *ctr, const RayOut &ro,
     }
 }
 
+__device__ __forceinline__ int2 tile_pixel(int tx, int ty, int tid) {
+    // warps cover 8x4 pixel blocks (better ray coherence than 16x2 rows)
+    const int wid = tid >> 5, lane = tid & 31;
+    return make_int2(tx * kTile + (wid & 1) * 8 + (lane & 7), ty * kTile + (wid >> 1) * 4 + (lane >> 3));
+}
+
 // ----------------------------------------------------------------------------------------
-// K5: one CTA per 16x16 tile. Warps cover 8x4 pixel blocks (better ray coherence than 16x2
-// rows). Shared memory: staged candidate transforms + the per-ray segment windows.
+// K5: one CTA per 16x16 tile.
+//   staging  the tile's candidates (transform + toModel(camera centre)) -> shared memory
+//   phase 1  every pixel: generateRay + exact segment window (all candidates)
+//   compact  rays with a non-empty window, in pixel order (misses write zeros and retire)
+//   phase 2  the first n_hit threads march the hit rays, so warps are full of live rays
 template <int CAP>
 __global__ void __launch_bounds__(kMarchThreads, 2)
 k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
@@ -454,10 +500,14 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
               const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
               int *__restrict__ ovf_list, int ovf_cap) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float4 *s_xf4 = reinterpret_cast<float4 *>(smem);                      // kCandCap*16 f
-    int *s_prim = reinterpret_cast<int *>(s_xf4 + kCandCap * 4);           // kCandCap
+    float4 *s_xf4 = reinterpret_cast<float4 *>(smem);                       // kCandCap * 4
+    float4 *s_om = s_xf4 + kCandCap * 4;                                    // kCandCap
+    int *s_prim = reinterpret_cast<int *>(s_om + kCandCap);                 // kCandCap
     unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(s_prim + kCandCap);  // 32
-    float *s_we = reinterpret_cast<float *>(s_tab + 32);                   // CAP*256
+    int *s_state = reinterpret_cast<int *>(s_tab + 32);                     // 256: cnt | more<<8
+    int *s_list = s_state + kMarchThreads;                                  // 256
+    int *s_warp = s_list + kMarchThreads;                                   // 8
+    float *s_we = reinterpret_cast<float *>(s_warp + 8);                    // CAP * 256
     float *s_wx = s_we + CAP * kMarchThreads;
     int *s_wc = reinterpret_cast<int *>(s_wx + CAP * kMarchThreads);
 
@@ -468,6 +518,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     const int n = (int)(offsets[tile + 1] - start);
     const int staged = n < kCandCap ? n : kCandCap;
     const int tid = threadIdx.x;
+    const V3 o = mk3(cam.center[0], cam.center[1], cam.center[2]);
     if (tid < 32) s_tab[tid] = kExp2fTab[tid];
     for (int i = tid; i < staged * 4; i += kMarchThreads) {
         const int c = i >> 2, q = i & 3;
@@ -476,27 +527,62 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
         s_xf4[i] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
     }
     __syncthreads();
+    if (tid < staged) {
+        const V3 om = to_model(reinterpret_cast<const float *>(s_xf4 + tid * 4), o);
+        s_om[tid] = make_float4(om.x, om.y, om.z, 0.f);
+    }
+    __syncthreads();
+    const TileCands cands{entries, xf_g, s_prim, reinterpret_cast<const float *>(s_xf4), s_om,
+                          start, n, staged};
 
-    const int wid = tid >> 5, lane = tid & 31;
-    const int px = tx * kTile + (wid & 1) * 8 + (lane & 7);
-    const int py = ty * kTile + (wid >> 1) * 4 + (lane >> 3);
-    const bool valid = px < cam.width && py < cam.height;
-    RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
-    const int64_t p = (int64_t)py * cam.width + px;
+    // phase 1: segment windows
+    const int2 px = tile_pixel(tx, ty, tid);
+    const bool valid = px.x < cam.width && px.y < cam.height;
+    int cnt = 0;
+    bool more = false;
     if (valid && n > 0) {
-        V3 o, d;
-        generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+        V3 rd, d;
+        generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
+        const Window w{s_we, s_wx, s_wc, kMarchThreads, tid};
+        window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
+    }
+    s_state[tid] = cnt | (more ? 256 : 0);
+    if (valid && cnt == 0) write_pixel(od, (int64_t)px.y * cam.width + px.x, RayOut{});
+    // compaction of hit rays (block-wide exclusive scan of the hit flags)
+    const bool hit = cnt > 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    const int wid = tid >> 5, lane = tid & 31;
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    int base = 0, n_hit = 0;
+    for (int q = 0; q < kMarchThreads / 32; ++q) {
+        base += q < wid ? s_warp[q] : 0;
+        n_hit += s_warp[q];
+    }
+    if (hit) s_list[base + __popc(bal & ((1u << lane) - 1))] = tid;
+    __syncthreads();
+
+    // phase 2: march the hit rays
+    RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    const bool live = tid < n_hit;
+    if (live) {
+        const int r = s_list[tid];
+        const int2 rp = tile_pixel(tx, ty, r);
+        const int64_t p = (int64_t)rp.y * cam.width + rp.x;
+        V3 rd, d;
+        generate_ray(cam, (float)rp.x + 0.5f, (float)rp.y + 0.5f, rd, d);
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
-        TileCands cands{entries, xf_g, s_prim, reinterpret_cast<const float *>(s_xf4), start, n, staged};
-        Window w{s_we, s_wx, s_wc, kMarchThreads, tid};
-        ro = march_ray<CAP>(cands, w, o, d, jit, mp, payload, s_tab);
+        const int st = s_state[r];
+        const Window w{s_we, s_wx, s_wc, kMarchThreads, r};
+        ro = march_window<CAP>(cands, w, st & 255, (st & 256) != 0, o, d, jit, mp, payload, s_tab);
         if (ro.overflow) {
-            const int slot = atomicAdd(&ctr->overflow_rays, 1ull);
+            const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)p;
+        } else {
+            write_pixel(od, p, ro);
         }
     }
-    if (valid && !ro.overflow) write_pixel(od, p, ro);
-    add_counters(ctr, ro, valid && !ro.overflow);
+    add_counters(ctr, ro, live && !ro.overflow);
 }
 
 // K5b: rays whose live segments overflowed the shared-memory window are re-marched with a
@@ -515,7 +601,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_
     const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    Window w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const Window w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
     for (int q = gtid; q < n_ovf; q += nthreads) {
         const int p = ovf_list[q];
         V3 o, d;
@@ -525,7 +611,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_
             o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
             d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
             if (rays.jitter) jit = rays.jitter[p];
-            AllCands cands{xf_g, n_prim};
+            const AllCands cands{xf_g, n_prim};
             ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
         } else {
             const int px = p % cam.width, py = p / cam.width;
@@ -533,7 +619,8 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_
             generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
             if (mp.jitter) jit = hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p));
             const uint32_t start = offsets[tile];
-            TileCands cands{entries, xf_g, nullptr, nullptr, start, (int)(offsets[tile + 1] - start), 0};
+            const TileCands cands{entries, xf_g, nullptr, nullptr, nullptr, start,
+                                  (int)(offsets[tile + 1] - start), 0};
             ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
         }
         if (ro.overflow) {
@@ -541,8 +628,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_
             continue;
         }
         write_pixel(od, p, ro);
-        // counters: plain atomics (rare path)
-        atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);
+        atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);  // rare path: plain atomics
         atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
         atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
         atomicAdd(&ctr->early_exits, (unsigned long long)ro.early);
@@ -571,11 +657,11 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        AllCands cands{xf_g, n_prim};
-        Window w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
+        const AllCands cands{xf_g, n_prim};
+        const Window w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
         ro = march_ray<CAP>(cands, w, o, d, jit, mp, payload, s_tab);
         if (ro.overflow) {
-            const int slot = atomicAdd(&ctr->overflow_rays, 1ull);
+            const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)r;
         }
     }
@@ -607,8 +693,8 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 constexpr int kWindowCap = 16;
 
 size_t march_tiles_smem() {
-    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 4 + 32 * 8 +
-           (size_t)kWindowCap * kMarchThreads * 12;
+    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 + kCandCap * 4 + 32 * 8 +
+           kMarchThreads * 4 * 2 + 8 * 4 + (size_t)kWindowCap * kMarchThreads * 12;
 }
 
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
@@ -647,6 +733,7 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
     const size_t smem = march_tiles_smem();
     if (!attr_set) {
         cudaFuncSetAttribute(k_march_tiles<kWindowCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_march_tiles<kWindowCap>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     const int n_tiles = cam.tiles_x * cam.tiles_y;

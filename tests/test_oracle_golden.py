@@ -1,0 +1,96 @@
+"""CPU: pin the oracle (oracle/vp_oracle.c) against the reference's own outputs.
+
+tests/golden/* was produced by the unmodified reference core (oracle/gen_golden.py); the C
+restatement must reproduce every fixture bit-for-bit before it may serve as the checker.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_groups
+from golden_cases import render_cases, sha
+from paper_2103_01954_b200 import api, synthetic
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def test_compose_matches_reference(oracle):
+    z = np.load(GOLDEN / "compose.npz")
+    rc, xf = oracle.compose(z["tr"])
+    assert rc == 0 and np.array_equal(bits(xf), bits(z["xf"]))
+    rc_bad, _ = oracle.compose(z["bad"])
+    assert rc_bad == int(z["rc_bad"]) == 2
+
+
+def test_generate_ray_matches_reference(oracle):
+    z = np.load(GOLDEN / "cameras.npz")
+    cam = api.Camera(z["K"], z["R"], z["t"], int(z["wh"][0]), int(z["wh"][1]))
+    for (x, y), want in zip(z["rays_px"], z["rays"]):
+        o, d = oracle.generate_ray(cam, x, y)
+        assert np.array_equal(bits(np.concatenate([o, d])), bits(want))
+
+
+def test_intersect_matches_reference(oracle):
+    z = np.load(GOLDEN / "intersect.npz")
+    off = 0
+    for o, d, n in zip(z["origins"], z["dirs"], z["lens"]):
+        p, te, tx = oracle.intersect(z["xf"], o, d)
+        want = z["segs"][off:off + n]
+        off += n
+        assert len(p) == n
+        assert np.array_equal(p, want[:, 0].astype(np.int32))
+        assert np.array_equal(bits(te), bits(want[:, 1])) and np.array_equal(bits(tx), bits(want[:, 2]))
+
+
+def test_march_kats_match_reference(oracle):
+    for name, g in load_groups("march_kats").items():
+        win = api.WindowParams(float(g["window"][0]), int(g["window"][1]))
+        cfg = api.MarchConfig(float(g["cfg"][0]), float(g["cfg"][1]))
+        rgb, alpha, samples = oracle.march_rays(g["xf"], int(g["m"]), g["payload"], win, g["o"], g["d"],
+                                                cfg, g["jit"])
+        assert np.array_equal(bits(rgb), bits(g["rgb"])), name
+        assert np.array_equal(bits(alpha), bits(g["alpha"])), name
+        assert np.array_equal(samples, g["samples"]), name
+
+
+@pytest.mark.parametrize("case", sorted(load_groups("renders")))
+def test_render_matches_reference(oracle, case):
+    c = render_cases()[case]
+    xf = api.compose(c["tr"]) if len(c["tr"]) else np.zeros((0, 15), np.float32)
+    rgb, alpha, samples = oracle.render(xf, c["m"], c["payload"], c["window"], c["cam"], c["cfg"])
+    assert np.array_equal(bits(rgb), bits(c["rgb"]))
+    assert np.array_equal(bits(alpha), bits(c["alpha"]))
+    assert np.array_equal(samples, c["samples"])
+
+
+def test_oracle_config1_full_size_digest(oracle):
+    """BASELINE config 1 (64 x 16^3 at 256^2, the reference's CPU oracle run), bit-exact."""
+    d = json.loads((GOLDEN / "digests.json").read_text())["renders"]["oracle_64x16_256_view-1"]
+    tr, pay = synthetic.shell_arrays(64, 16)
+    rgb, alpha, samples = oracle.render(api.compose(tr), 16, pay, api.WindowParams(),
+                                        synthetic.shell_camera(-1, 64, 256), api.MarchConfig())
+    assert int(samples.sum()) == d["total_samples"]
+    assert sha(samples) == d["samples"] and sha(alpha) == d["alpha"] and sha(rgb) == d["rgb"]
+
+
+def test_window_known_answers(oracle):
+    """test_primitive.cpp:13-25."""
+    assert oracle.window(0, 0, 0) == 1.0
+    assert oracle.window(1, 0, 0) == pytest.approx(np.exp(-8.0), rel=1e-6)
+    assert oracle.window(1, 1, 1) == pytest.approx(np.exp(-24.0), rel=1e-6)
+    assert oracle.window(0.5, 0, 0) == pytest.approx(np.exp(-0.03125), rel=1e-6)
+    assert oracle.window(-0.7, 0.2, 0) == oracle.window(0.7, -0.2, 0)
+    assert oracle.window(0.9, 0.9, 0.9, 0.0, 8) == 1.0
+
+
+def test_expf_port_matches_libm(oracle):
+    """The binary64 expf port (the algorithm ported to the device) equals this host's glibc
+    expf: a stride-7 walk over [-24, 0] (the window argument range at alpha = 8) and a
+    stride-4099 walk over [-104, 88] (the GPU test checks every float of [-24, 0] on the
+    device)."""
+    assert oracle.expf_port_mismatches(0x80000000, 0xC1C00000, 7) == 0
+    assert oracle.expf_port_mismatches(0x80000000, 0xC2D00000, 4099) == 0
+    assert oracle.expf_port_mismatches(0x00000000, 0x42B00000, 4099) == 0
