@@ -70,7 +70,7 @@ struct vp_ctx {
     int32_t w_beta = 8;
     DBuf<float> xf16, xf15_tmp, planar_tmp;
     DBuf<float4> payload;
-    DBuf<int4> rects;
+    DBuf<int4> rects, prects;
     DBuf<uint32_t> keys, tile_counts, offsets, cursor;
     DBuf<unsigned long long> entries;
     DBuf<float> out_rgb, out_alpha;
@@ -159,6 +159,7 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
     VP_CUDA(ctx, ctx->offsets.ensure(n_tiles + 1));
     VP_CUDA(ctx, ctx->cursor.ensure(n_tiles));
     VP_CUDA(ctx, ctx->rects.ensure(size_t(std::max(ctx->n_prim, 1))));
+    VP_CUDA(ctx, ctx->prects.ensure(size_t(std::max(ctx->n_prim, 1))));
     VP_CUDA(ctx, ctx->keys.ensure(size_t(std::max(ctx->n_prim, 1))));
     if (ctx->entries_cap == 0) ctx->entries_cap = std::max<int64_t>(int64_t(1) << 20, int64_t(ctx->n_prim) * 16);
     VP_CUDA(ctx, ctx->entries.ensure(size_t(ctx->entries_cap)));
@@ -173,15 +174,15 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
 int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const OutDev &od,
                    cudaStream_t st) {
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->keys.p,
+    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
                                 ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
                                 ctx->entries_cap, ctx->d_ctr, st));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
-    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->payload.p, ctx->offsets.p,
+    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->prects.p, ctx->payload.p, ctx->offsets.p,
                                     ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
     const RaysDev none{nullptr, nullptr, nullptr};
-    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p,
+    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->prects.p, ctx->n_prim, ctx->payload.p,
                                        ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
                                        ctx->ovf_list.p, ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p,
                                        ctx->fb_c.p, st));
@@ -276,6 +277,7 @@ int vp_destroy(vp_ctx *ctx) {
         b->release();
     ctx->payload.release();
     ctx->rects.release();
+    ctx->prects.release();
     for (auto *b : {&ctx->keys, &ctx->tile_counts, &ctx->offsets, &ctx->cursor}) b->release();
     ctx->entries.release();
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
@@ -558,7 +560,7 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, rays, n_rays, od,
                                        ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
         const CamDev none{};
-        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p,
+        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, ctx->n_prim, ctx->payload.p,
                                            nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p,
                                            ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
     }
@@ -612,7 +614,7 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->keys.p,
+        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
                                     ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
                                     ctx->entries_cap, ctx->d_ctr, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));

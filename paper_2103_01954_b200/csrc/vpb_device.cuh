@@ -175,10 +175,17 @@ __device__ __forceinline__ float clamp_unit(float v) {
 // gatherChannel/cornerWeight (primitive.cpp:71-99) over the channel-interleaved float4
 // payload (k, z, y, x, rgba), and window(). Each channel accumulates its 8 corners in the
 // reference order (z, y, x loops, x fastest; weight (wx*wy)*wz, starting from 0).
-__device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payload, int m,
+//
+// MT > 0 makes the voxel count a compile-time constant: the stencil folds to constants and
+// the eight corner loads become one address plus immediate offsets. Because
+// trilinearStencil clamps lo to [0, M-2], the upper corner is always lo+1 for M >= 2
+// (gatherChannel's min(lo+c, M-1) never bites); for M == 1 all corners are voxel 0.
+template <int MT>
+__device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payload, int m_rt,
                                                  int k, const float *xf, V3 pw, float alpha,
                                                  int beta, const unsigned long long *tab,
                                                  float &sigma, float &r, float &g, float &b) {
+    const int m = MT > 0 ? MT : m_rt;
     const V3 q = to_model(xf, pw);
     const V3 pm = mk3(clamp_unit(q.x), clamp_unit(q.y), clamp_unit(q.z));
     int lo[3];
@@ -194,27 +201,35 @@ __device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payl
         lo[a] = i0;
         fr[a] = m > 1 ? u - (float)i0 : 0.0f;
     }
-    const int x0 = lo[0], y0 = lo[1], z0 = lo[2];
-    const int x1 = min(x0 + 1, m - 1), y1 = min(y0 + 1, m - 1), z1 = min(z0 + 1, m - 1);
-    const size_t base = (size_t)k * (size_t)m * m * m;
-    const float4 *p = payload + base;
-    const int mm = m * m;
-    // Issue all eight 16-byte gathers before any arithmetic (memory-level parallelism).
-    const float4 c000 = __ldg(p + (z0 * mm + y0 * m + x0));
-    const float4 c001 = __ldg(p + (z0 * mm + y0 * m + x1));
-    const float4 c010 = __ldg(p + (z0 * mm + y1 * m + x0));
-    const float4 c011 = __ldg(p + (z0 * mm + y1 * m + x1));
-    const float4 c100 = __ldg(p + (z1 * mm + y0 * m + x0));
-    const float4 c101 = __ldg(p + (z1 * mm + y0 * m + x1));
-    const float4 c110 = __ldg(p + (z1 * mm + y1 * m + x0));
-    const float4 c111 = __ldg(p + (z1 * mm + y1 * m + x1));
+    const float4 *p = payload + (size_t)k * (unsigned)(m * m * m) +
+                      (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
+    float4 c000, c001, c010, c011, c100, c101, c110, c111;
+    if (MT >= 2) {  // immediate offsets
+        c000 = __ldg(p);
+        c001 = __ldg(p + 1);
+        c010 = __ldg(p + MT);
+        c011 = __ldg(p + MT + 1);
+        c100 = __ldg(p + MT * MT);
+        c101 = __ldg(p + MT * MT + 1);
+        c110 = __ldg(p + MT * MT + MT);
+        c111 = __ldg(p + MT * MT + MT + 1);
+    } else {
+        const int dx = m > 1 ? 1 : 0, dy = m > 1 ? m : 0, dz = m > 1 ? m * m : 0;
+        c000 = __ldg(p);
+        c001 = __ldg(p + dx);
+        c010 = __ldg(p + dy);
+        c011 = __ldg(p + dy + dx);
+        c100 = __ldg(p + dz);
+        c101 = __ldg(p + dz + dx);
+        c110 = __ldg(p + dz + dy);
+        c111 = __ldg(p + dz + dy + dx);
+    }
     const float wx0 = 1.0f - fr[0], wx1 = fr[0];
     const float wy0 = 1.0f - fr[1], wy1 = fr[1];
     const float wz0 = 1.0f - fr[2], wz1 = fr[2];
-    const float w000 = wx0 * wy0 * wz0, w001 = wx1 * wy0 * wz0;
-    const float w010 = wx0 * wy1 * wz0, w011 = wx1 * wy1 * wz0;
-    const float w100 = wx0 * wy0 * wz1, w101 = wx1 * wy0 * wz1;
-    const float w110 = wx0 * wy1 * wz1, w111 = wx1 * wy1 * wz1;
+    const float w00 = wx0 * wy0, w01 = wx1 * wy0, w10 = wx0 * wy1, w11 = wx1 * wy1;
+    const float w000 = w00 * wz0, w001 = w01 * wz0, w010 = w10 * wz0, w011 = w11 * wz0;
+    const float w100 = w00 * wz1, w101 = w01 * wz1, w110 = w10 * wz1, w111 = w11 * wz1;
 #define VPB_GATHER(ch)                                                                        \
     (((((((0.0f + w000 * c000.ch) + w001 * c001.ch) + w010 * c010.ch) + w011 * c011.ch) +     \
         w100 * c100.ch) + w101 * c101.ch) + w110 * c110.ch) + w111 * c111.ch

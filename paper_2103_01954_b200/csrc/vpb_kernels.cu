@@ -54,9 +54,11 @@ __global__ void k_pad_xf(const float *__restrict__ xf15, float *__restrict__ xf1
 
 // ----------------------------------------------------------------------------------------
 // K1: cull. Same float operation sequence as the CPU restatement (oracle/vp_oracle.c,
-// cull_one), so rectangles and keys are bit-identical.
+// cull_one), so rectangles and keys are bit-identical. `prect` is the conservative pixel
+// rectangle the tile rectangle is derived from (empty = {0, 0, -1, -1}); the raymarch uses it
+// to skip the exact box test for candidates whose rectangle excludes the pixel.
 __device__ __forceinline__ void cull_rect(const float *xf, const CamDev &cam, int4 &rect,
-                                          uint32_t &key) {
+                                          int4 &prect, uint32_t &key) {
     const V3 s = mk3(xf[12], xf[13], xf[14]);
     const float r = sqrtf(dot3(s, s));
     const float rr = r * 1.001f + 1e-6f;
@@ -66,10 +68,12 @@ __device__ __forceinline__ void cull_rect(const float *xf, const CamDev &cam, in
     if (!(depth > 0.0f)) depth = 0.0f;
     key = __float_as_uint(depth);
     rect = make_int4(0, 0, -1, -1);
+    prect = rect;
     if (cam.width <= 0 || cam.height <= 0) return;
     if (cc.z + rr < 0.0f) return;
     if (cc.z - rr <= 1e-3f * rr) {
         rect = make_int4(0, 0, cam.tiles_x - 1, cam.tiles_y - 1);
+        prect = make_int4(0, 0, cam.width - 1, cam.height - 1);
         return;
     }
     float umin = 3.402823466e+38f, umax = -3.402823466e+38f;
@@ -97,21 +101,23 @@ __device__ __forceinline__ void cull_rect(const float *xf, const CamDev &cam, in
     y0 = y0 > 0.0f ? y0 : 0.0f;
     x1 = x1 < wl ? x1 : wl;
     y1 = y1 < hl ? y1 : hl;
-    rect = make_int4((int)x0 / kTile, (int)y0 / kTile, (int)x1 / kTile, (int)y1 / kTile);
+    prect = make_int4((int)x0, (int)y0, (int)x1, (int)y1);
+    rect = make_int4(prect.x / kTile, prect.y / kTile, prect.z / kTile, prect.w / kTile);
 }
 
 __global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
-                       int4 *__restrict__ rects, uint32_t *__restrict__ keys,
-                       uint32_t *__restrict__ tile_counts) {
+                       int4 *__restrict__ rects, int4 *__restrict__ prects,
+                       uint32_t *__restrict__ keys, uint32_t *__restrict__ tile_counts) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_prim) return;
     float xf[15];
 #pragma unroll
     for (int j = 0; j < 15; ++j) xf[j] = xf16[(size_t)k * kXfStride + j];
-    int4 rc;
+    int4 rc, prc;
     uint32_t key;
-    cull_rect(xf, cam, rc, key);
+    cull_rect(xf, cam, rc, prc, key);
     rects[k] = rc;
+    prects[k] = prc;
     keys[k] = key;
     for (int ty = rc.y; ty <= rc.w; ++ty)
         for (int tx = rc.x; tx <= rc.z; ++tx) atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1u);
@@ -226,11 +232,18 @@ __global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
 struct TileCands {  // a tile's sorted bucket, first kCandCap staged in shared memory
     const unsigned long long *entries;
     const float *xf_g;
+    const int4 *prects_g;
     const int *s_prim;
     const float *s_xf;
     const float4 *s_om;
+    const int4 *s_prect;
     uint32_t start;
     int n, staged;
+    // the candidate's conservative pixel rectangle (k_cull) contains the pixel
+    __device__ __forceinline__ bool covers(int c, int2 px) const {
+        const int4 r = c < staged ? s_prect[c] : prects_g[prim(c)];
+        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
+    }
     __device__ __forceinline__ int prim(int c) const {
         return c < staged ? s_prim[c] : (int)(uint32_t)(entries[start + c] & 0xffffffffull);
     }
@@ -250,6 +263,7 @@ struct AllCands {  // every primitive (march over arbitrary rays)
     int n;
     __device__ __forceinline__ int prim(int c) const { return c; }
     __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ bool covers(int, int2) const { return true; }
     __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
         return intersect_obb(xf(c), o, d, tE, tX);
     }
@@ -306,11 +320,11 @@ __device__ __forceinline__ void window_insert(const Window &w, const Cands &cand
 // when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order).
 template <int CAP, class Cands>
 __device__ __forceinline__ void window_scan(const Window &w, const Cands &cands, int &cnt,
-                                            bool &more, V3 o, V3 d, bool first, float lastE,
-                                            int lastP) {
+                                            bool &more, V3 o, V3 d, int2 px, bool first,
+                                            float lastE, int lastP) {
     for (int c = 0; c < cands.n; ++c) {
         float tE, tX;
-        if (!cands.hit(c, o, d, tE, tX)) continue;
+        if (!cands.covers(c, px) || !cands.hit(c, o, d, tE, tX)) continue;
         const int prim = cands.prim(c);
         if (!first && !key_less(lastE, lastP, tE, prim)) continue;
         window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
@@ -328,9 +342,9 @@ __device__ __forceinline__ void window_scan(const Window &w, const Cands &cands,
 // one active primitive; the step's accumulation happens after its last active primitive. Lanes
 // whose steps have different numbers of active primitives therefore stay in lock-step on
 // primitive-samples instead of waiting for the widest step of the warp.
-template <int CAP, class Cands>
+template <int CAP, int MT, class Cands>
 __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, bool more, V3 o,
-                               V3 d, float jit, const MarchDev &mp,
+                               V3 d, int2 px, float jit, const MarchDev &mp,
                                const float4 *__restrict__ payload, const unsigned long long *tab) {
     RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
     if (cnt == 0) return out;
@@ -376,7 +390,7 @@ __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, boo
                     lo = 0;
                     more = false;
                     ++out.refills;
-                    window_scan<CAP>(w, cands, cnt, more, o, d, false, lastE, lastP);
+                    window_scan<CAP>(w, cands, cnt, more, o, d, px, false, lastE, lastP);
                 }
                 while (lo < nxt && w.X(lo) <= ts) ++lo;
                 j = lo;
@@ -395,7 +409,7 @@ __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, boo
         {  // one primitive-sample (march.cpp:63-70)
             const int c = w.C(j);
             float sg, r, g, b;
-            sample_primitive(payload, mp.m, cands.prim(c), cands.xf(c), pw, mp.alpha, mp.beta,
+            sample_primitive<MT>(payload, mp.m, cands.prim(c), cands.xf(c), pw, mp.alpha, mp.beta,
                              tab, sg, r, g, b);
             sigmaSum += sg;
             rw += r * sg;
@@ -440,13 +454,13 @@ done:
 
 template <int CAP, class Cands>
 __device__ __forceinline__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d,
-                                            float jit, const MarchDev &mp,
+                                            int2 px, float jit, const MarchDev &mp,
                                             const float4 *__restrict__ payload,
                                             const unsigned long long *tab) {
     int cnt = 0;
     bool more = false;
-    window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
-    return march_window<CAP>(cands, w, cnt, more, o, d, jit, mp, payload, tab);
+    window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+    return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, payload, tab);
 }
 
 __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
@@ -493,16 +507,20 @@ __device__ __forceinline__ int2 tile_pixel(int tx, int ty, int tid) {
 //   phase 1  every pixel: generateRay + exact segment window (all candidates)
 //   compact  rays with a non-empty window, in pixel order (misses write zeros and retire)
 //   phase 2  the first n_hit threads march the hit rays, so warps are full of live rays
-template <int CAP>
-__global__ void __launch_bounds__(kMarchThreads, 2)
+#ifndef VPB_MARCH_MINB
+#define VPB_MARCH_MINB 3
+#endif
+template <int CAP, int MT>
+__global__ void __launch_bounds__(kMarchThreads, VPB_MARCH_MINB)
 k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
-              const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
+              const int4 *__restrict__ prects, const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
               const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
               int *__restrict__ ovf_list, int ovf_cap) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *s_xf4 = reinterpret_cast<float4 *>(smem);                       // kCandCap * 4
     float4 *s_om = s_xf4 + kCandCap * 4;                                    // kCandCap
-    int *s_prim = reinterpret_cast<int *>(s_om + kCandCap);                 // kCandCap
+    int4 *s_prect = reinterpret_cast<int4 *>(s_om + kCandCap);             // kCandCap
+    int *s_prim = reinterpret_cast<int *>(s_prect + kCandCap);              // kCandCap
     unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(s_prim + kCandCap);  // 32
     int *s_state = reinterpret_cast<int *>(s_tab + 32);                     // 256: cnt | more<<8
     int *s_list = s_state + kMarchThreads;                                  // 256
@@ -530,10 +548,11 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     if (tid < staged) {
         const V3 om = to_model(reinterpret_cast<const float *>(s_xf4 + tid * 4), o);
         s_om[tid] = make_float4(om.x, om.y, om.z, 0.f);
+        s_prect[tid] = prects[s_prim[tid]];
     }
     __syncthreads();
-    const TileCands cands{entries, xf_g, s_prim, reinterpret_cast<const float *>(s_xf4), s_om,
-                          start, n, staged};
+    const TileCands cands{entries, xf_g, prects, s_prim, reinterpret_cast<const float *>(s_xf4),
+                          s_om, s_prect, start, n, staged};
 
     // phase 1: segment windows
     const int2 px = tile_pixel(tx, ty, tid);
@@ -544,7 +563,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
         V3 rd, d;
         generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
         const Window w{s_we, s_wx, s_wc, kMarchThreads, tid};
-        window_scan<CAP>(w, cands, cnt, more, o, d, true, 0.f, 0);
+        window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
     s_state[tid] = cnt | (more ? 256 : 0);
     if (valid && cnt == 0) write_pixel(od, (int64_t)px.y * cam.width + px.x, RayOut{});
@@ -574,7 +593,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
         const int st = s_state[r];
         const Window w{s_we, s_wx, s_wc, kMarchThreads, r};
-        ro = march_window<CAP>(cands, w, st & 255, (st & 256) != 0, o, d, jit, mp, payload, s_tab);
+        ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, payload, s_tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)p;
@@ -589,7 +608,8 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
 // kFallbackCap-entry window in global scratch (one window per thread of a fixed grid).
 template <bool kRays>
 __global__ void __launch_bounds__(kFallbackThreads)
-k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, const int4 *__restrict__ prects,
+                 int n_prim,
                  const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
                  const unsigned long long *__restrict__ entries, OutDev od, RaysDev rays,
                  DevCounters *ctr, const int *__restrict__ ovf_list, int ovf_cap,
@@ -612,16 +632,16 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, int n_
             d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
             if (rays.jitter) jit = rays.jitter[p];
             const AllCands cands{xf_g, n_prim};
-            ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
+            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(0, 0), jit, mp, payload, s_tab);
         } else {
             const int px = p % cam.width, py = p / cam.width;
             const int tile = (py / kTile) * cam.tiles_x + px / kTile;
             generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
             if (mp.jitter) jit = hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p));
             const uint32_t start = offsets[tile];
-            const TileCands cands{entries, xf_g, nullptr, nullptr, nullptr, start,
+            const TileCands cands{entries, xf_g, prects, nullptr, nullptr, nullptr, nullptr, start,
                                   (int)(offsets[tile + 1] - start), 0};
-            ro = march_ray<kFallbackCap>(cands, w, o, d, jit, mp, payload, s_tab);
+            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, payload, s_tab);
         }
         if (ro.overflow) {
             atomicAdd(&ctr->fallback_fail, 1);
@@ -659,7 +679,7 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
         const AllCands cands{xf_g, n_prim};
         const Window w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
-        ro = march_ray<CAP>(cands, w, o, d, jit, mp, payload, s_tab);
+        ro = march_ray<CAP>(cands, w, o, d, make_int2(0, 0), jit, mp, payload, s_tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)r;
@@ -690,10 +710,13 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 
 // ----------------------------------------------------------------------------------------
 // Host-side launchers (plain C++ signatures for vpb_api.cpp).
-constexpr int kWindowCap = 16;
+#ifndef VPB_WINDOW_CAP
+#define VPB_WINDOW_CAP 16
+#endif
+constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared memory)
 
 size_t march_tiles_smem() {
-    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 + kCandCap * 4 + 32 * 8 +
+    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 * 2 + kCandCap * 4 + 32 * 8 +
            kMarchThreads * 4 * 2 + 8 * 4 + (size_t)kWindowCap * kMarchThreads * 12;
 }
 
@@ -713,48 +736,61 @@ cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream
 }
 
 cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
-                           uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
+                           int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
                            uint32_t *cursor, unsigned long long *entries, int64_t capacity,
                            DevCounters *ctr, cudaStream_t st) {
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
-    if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, keys, tile_counts);
+    if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
     k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, ctr, capacity);
     if (n_prim > 0) k_emit<<<(n_prim + 127) / 128, 128, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
     k_tile_sort<<<n_tiles, 128, 0, st>>>(offsets, entries, ctr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                               const float4 *payload, const uint32_t *offsets,
-                               const unsigned long long *entries, const OutDev &od,
-                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
+template <int MT>
+static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                                  const int4 *prects, const float4 *payload, const uint32_t *offsets,
+                                  const unsigned long long *entries, const OutDev &od,
+                                  DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = march_tiles_smem();
     if (!attr_set) {
-        cudaFuncSetAttribute(k_march_tiles<kWindowCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_march_tiles<kWindowCap>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_march_tiles<kWindowCap, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_march_tiles<kWindowCap, MT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
-    const int n_tiles = cam.tiles_x * cam.tiles_y;
-    if (n_tiles == 0) return cudaSuccess;
-    k_march_tiles<kWindowCap><<<n_tiles, kMarchThreads, smem, st>>>(cam, mp, xf16, payload, offsets,
-                                                                  entries, od, ctr, ovf_list, ovf_cap);
+    k_march_tiles<kWindowCap, MT><<<cam.tiles_x * cam.tiles_y, kMarchThreads, smem, st>>>(
+        cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap);
     return cudaGetLastError();
 }
 
+cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                               const int4 *prects, const float4 *payload, const uint32_t *offsets,
+                               const unsigned long long *entries, const OutDev &od,
+                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
+    if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
+    switch (mp.m) {  // compile-time voxel counts for the common grids
+    case 4: return launch_tiles_m<4>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    case 8: return launch_tiles_m<8>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    case 16: return launch_tiles_m<16>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    case 32: return launch_tiles_m<32>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    default: return launch_tiles_m<0>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    }
+}
+
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
-                                  const float *xf16, int n_prim, const float4 *payload,
+                                  const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
                                   const uint32_t *offsets, const unsigned long long *entries,
                                   const OutDev &od, const RaysDev &rays, DevCounters *ctr,
                                   const int *ovf_list, int ovf_cap, float *se, float *sx,
                                   int *sc, cudaStream_t st) {
     if (rays_mode)
         k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-            cam, mp, xf16, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+            cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
     else
         k_march_fallback<false><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-            cam, mp, xf16, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+            cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
     return cudaGetLastError();
 }
 
