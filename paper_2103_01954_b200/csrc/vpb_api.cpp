@@ -71,7 +71,7 @@ struct vp_ctx {
     DBuf<float> xf16, xf15_tmp, planar_tmp;
     DBuf<float4> payload;
     DBuf<int4> rects, prects;
-    DBuf<uint32_t> keys, tile_counts, offsets, cursor;
+    DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
     DBuf<unsigned long long> entries;
     DBuf<float> out_rgb, out_alpha;
     DBuf<int> out_samples, ovf_list;
@@ -158,6 +158,7 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
     VP_CUDA(ctx, ctx->tile_counts.ensure(n_tiles));
     VP_CUDA(ctx, ctx->offsets.ensure(n_tiles + 1));
     VP_CUDA(ctx, ctx->cursor.ensure(n_tiles));
+    VP_CUDA(ctx, ctx->order.ensure(n_tiles));
     VP_CUDA(ctx, ctx->rects.ensure(size_t(std::max(ctx->n_prim, 1))));
     VP_CUDA(ctx, ctx->prects.ensure(size_t(std::max(ctx->n_prim, 1))));
     VP_CUDA(ctx, ctx->keys.ensure(size_t(std::max(ctx->n_prim, 1))));
@@ -175,12 +176,12 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
                    cudaStream_t st) {
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
     VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
-                                ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
+                                ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->order.p, ctx->entries.p,
                                 ctx->entries_cap, ctx->d_ctr, st));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
     VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->prects.p, ctx->payload.p, ctx->offsets.p,
-                                    ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
+                                    ctx->order.p, ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
     const RaysDev none{nullptr, nullptr, nullptr};
     VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->prects.p, ctx->n_prim, ctx->payload.p,
                                        ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
@@ -278,7 +279,7 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->payload.release();
     ctx->rects.release();
     ctx->prects.release();
-    for (auto *b : {&ctx->keys, &ctx->tile_counts, &ctx->offsets, &ctx->cursor}) b->release();
+    for (auto *b : {&ctx->keys, &ctx->tile_counts, &ctx->offsets, &ctx->cursor, &ctx->order}) b->release();
     ctx->entries.release();
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
     if (ctx->d_ctr) cudaFree(ctx->d_ctr);
@@ -615,7 +616,7 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
         VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
-                                    ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->entries.p,
+                                    ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->order.p, ctx->entries.p,
                                     ctx->entries_cap, ctx->d_ctr, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
         VP_CUDA(ctx, cudaStreamSynchronize(st));

@@ -176,13 +176,13 @@ __device__ __forceinline__ float clamp_unit(float v) {
 // payload (k, z, y, x, rgba), and window(). Each channel accumulates its 8 corners in the
 // reference order (z, y, x loops, x fastest; weight (wx*wy)*wz, starting from 0).
 //
-// MT > 0 makes the voxel count a compile-time constant: the stencil folds to constants and
+// pbase is the primitive's first voxel (payload + k * M^3). MT > 0 makes the voxel count a compile-time constant: the stencil folds to constants and
 // the eight corner loads become one address plus immediate offsets. Because
 // trilinearStencil clamps lo to [0, M-2], the upper corner is always lo+1 for M >= 2
 // (gatherChannel's min(lo+c, M-1) never bites); for M == 1 all corners are voxel 0.
 template <int MT>
-__device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payload, int m_rt,
-                                                 int k, const float *xf, V3 pw, float alpha,
+__device__ __forceinline__ void sample_primitive(const float4 *__restrict__ pbase, int m_rt,
+                                                 const float *xf, V3 pw, float alpha,
                                                  int beta, const unsigned long long *tab,
                                                  float &sigma, float &r, float &g, float &b) {
     const int m = MT > 0 ? MT : m_rt;
@@ -201,8 +201,7 @@ __device__ __forceinline__ void sample_primitive(const float4 *__restrict__ payl
         lo[a] = i0;
         fr[a] = m > 1 ? u - (float)i0 : 0.0f;
     }
-    const float4 *p = payload + (size_t)k * (unsigned)(m * m * m) +
-                      (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
+    const float4 *p = pbase + (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
     float4 c000, c001, c010, c011, c100, c101, c110, c111;
     if (MT >= 2) {  // immediate offsets
         c000 = __ldg(p);

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "vpb_device.cuh"
 #include "vpb_kernels.h"
@@ -125,11 +126,15 @@ __global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
 
 // K2: single-CTA exclusive scan over the tile counts (tiles <= a few 10^4). Writes the
 // bucket starts twice (offsets, and the emit cursors) and flags key-capacity overflow.
+// It also writes `order`: the tiles by descending candidate count (a proxy for their march
+// cost), so the raymarch hands the heaviest tiles out first and the tail stays short.
+constexpr int kOrderBuckets = 1024;
 __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
                        uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
-                       DevCounters *ctr, int64_t capacity) {
+                       uint32_t *__restrict__ order, DevCounters *ctr, int64_t capacity) {
     __shared__ unsigned long long warp_sums[32];
     __shared__ unsigned long long carry;
+    __shared__ unsigned hist[kOrderBuckets];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) carry = 0;
     __syncthreads();
@@ -169,6 +174,31 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
         ctr->keys = carry;
         ctr->key_overflow = (int64_t)carry > capacity ? 1 : 0;
     }
+    // counting sort of the tiles by min(count, 1023), descending
+    for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int t = tid; t < n_tiles; t += blockDim.x) atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u);
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan over buckets in descending order, 32 buckets per lane
+        unsigned local = 0;
+        for (int q = 0; q < kOrderBuckets / 32; ++q) local += hist[kOrderBuckets - 1 - (lane * 32 + q)];
+        unsigned incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        unsigned run = incl - local;
+        for (int q = 0; q < kOrderBuckets / 32; ++q) {
+            const int b = kOrderBuckets - 1 - (lane * 32 + q);
+            const unsigned h = hist[b];
+            hist[b] = run;
+            run += h;
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < n_tiles; t += blockDim.x)
+        order[atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u)] = (uint32_t)t;
 }
 
 // K3a: scatter keys into buckets. Order inside a bucket is arbitrary here; K3b makes it
@@ -226,58 +256,74 @@ __global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
 }
 
 // ----------------------------------------------------------------------------------------
-// Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205);
-// for a tile the camera centre is every ray's origin, so om = toModel(origin) is computed
-// once per staged candidate (same operations, same bits) instead of once per ray.
-struct TileCands {  // a tile's sorted bucket, first kCandCap staged in shared memory
+// Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
+//
+// TileCands<true>: every candidate of the tile is staged in shared memory (n <= kCandCap):
+// transform, toModel(camera centre) (every ray of a render starts there, so om is computed
+// once per candidate instead of once per ray, same operations, same bits), pixel rectangle
+// and payload base. TileCands<false>: the generic path reading the tile bucket from global
+// memory (tiles with more candidates, fallback re-march).
+template <bool STAGED>
+struct TileCands {
     const unsigned long long *entries;
     const float *xf_g;
     const int4 *prects_g;
+    const float4 *payload;
+    unsigned m3;
+    uint32_t start;
+    int n;
     const int *s_prim;
     const float *s_xf;
     const float4 *s_om;
     const int4 *s_prect;
-    uint32_t start;
-    int n, staged;
-    // the candidate's conservative pixel rectangle (k_cull) contains the pixel
-    __device__ __forceinline__ bool covers(int c, int2 px) const {
-        const int4 r = c < staged ? s_prect[c] : prects_g[prim(c)];
-        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
-    }
     __device__ __forceinline__ int prim(int c) const {
-        return c < staged ? s_prim[c] : (int)(uint32_t)(entries[start + c] & 0xffffffffull);
+        if (STAGED) return s_prim[c];
+        return (int)(uint32_t)(entries[start + c] & 0xffffffffull);
     }
     __device__ __forceinline__ const float *xf(int c) const {
-        return c < staged ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
+        return STAGED ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
+    }
+    __device__ __forceinline__ const float4 *base(int c) const {
+        return payload + (size_t)prim(c) * m3;
+    }
+    // the candidate's conservative pixel rectangle (k_cull) contains the pixel
+    __device__ __forceinline__ bool covers(int c, int2 px) const {
+        const int4 r = STAGED ? s_prect[c] : prects_g[prim(c)];
+        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
     }
     __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
-        if (c < staged) {
+        if (STAGED) {
             const float4 om = s_om[c];
-            return intersect_obb_om(s_xf + c * kXfStride, mk3(om.x, om.y, om.z), d, tE, tX);
+            return intersect_obb_om(xf(c), mk3(om.x, om.y, om.z), d, tE, tX);
         }
         return intersect_obb(xf(c), o, d, tE, tX);
     }
 };
 struct AllCands {  // every primitive (march over arbitrary rays)
     const float *xf_g;
+    const float4 *payload;
+    unsigned m3;
     int n;
     __device__ __forceinline__ int prim(int c) const { return c; }
     __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
     __device__ __forceinline__ bool covers(int, int2) const { return true; }
     __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
         return intersect_obb(xf(c), o, d, tE, tX);
     }
 };
 
-// Per-ray sorted segment window storage: slot j of ray `lane` lives at [j * stride + lane].
+// Per-ray sorted segment window: slot j of ray `lane` lives at [j * stride + lane]
+// (conflict-free across a warp). IdxT holds the candidate index (uint8_t for staged tiles).
+template <class IdxT>
 struct Window {
     float *e;
     float *x;
-    int *c;
+    IdxT *c;
     int stride, lane;
     __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
     __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
-    __device__ __forceinline__ int &C(int j) const { return c[j * stride + lane]; }
+    __device__ __forceinline__ IdxT &C(int j) const { return c[j * stride + lane]; }
 };
 
 struct RayOut {
@@ -293,8 +339,8 @@ __device__ __forceinline__ bool key_less(float ea, int pa, float eb, int pb) {
 
 // Inserts (tE, tX, c) into the sorted window [0, cnt) of capacity CAP, keeping the CAP
 // smallest (tEnter, prim) keys; `more` records that a hit fell outside the window.
-template <int CAP, class Cands>
-__device__ __forceinline__ void window_insert(const Window &w, const Cands &cands, int &cnt,
+template <int CAP, class Cands, class Win>
+__device__ __forceinline__ void window_insert(const Win &w, const Cands &cands, int &cnt,
                                               bool &more, float tE, float tX, int c, int prim) {
     if (cnt == CAP) {
         more = true;
@@ -318,8 +364,8 @@ __device__ __forceinline__ void window_insert(const Window &w, const Cands &cand
 
 // Fills the window with the smallest hits whose key exceeds (lastE, lastP) (or all hits
 // when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order).
-template <int CAP, class Cands>
-__device__ __forceinline__ void window_scan(const Window &w, const Cands &cands, int &cnt,
+template <int CAP, class Cands, class Win>
+__device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, int &cnt,
                                             bool &more, V3 o, V3 d, int2 px, bool first,
                                             float lastE, int lastP) {
     for (int c = 0; c < cands.n; ++c) {
@@ -338,23 +384,25 @@ __device__ __forceinline__ void window_scan(const Window &w, const Cands &cands,
 // segment is admitted and retired, where the empty-active-set branch breaks on the same step.
 //
 // The loop is flattened to one primitive-sample per iteration: a lane first finds its next
-// lattice step with a non-empty active set (admission, retirement, gap skip), then evaluates
-// one active primitive; the step's accumulation happens after its last active primitive. Lanes
-// whose steps have different numbers of active primitives therefore stay in lock-step on
-// primitive-samples instead of waiting for the widest step of the warp.
-template <int CAP, int MT, class Cands>
-__device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, bool more, V3 o,
+// lattice step with a non-empty active set, then evaluates one active primitive; the step's
+// accumulation happens after its last active primitive. Lanes whose steps have different
+// numbers of active primitives stay in lock-step on primitive-samples. Between events the
+// active set does not change: t_evt = min(next entry, earliest exit of a live entry), and
+// while ts < t_evt a step reuses the previous active set without touching the window.
+template <int CAP, int MT, class Cands, class Win>
+__device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
                                V3 d, int2 px, float jit, const MarchDev &mp,
-                               const float4 *__restrict__ payload, const unsigned long long *tab) {
+                               const unsigned long long *tab) {
     RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
     if (cnt == 0) return out;
     out.hit = 1;
     const float dt = mp.dt;
     const float t0 = w.E(0);
-    int nxt = 0, lo = 0, j = 0;
+    int nxt = 0, lo = 0, j = 0, jfirst = 0;
     long long i = 0;
     float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
     float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+    float t_evt = -3.402823466e+38f;
     V3 pw = o;
     bool sampling = false;
     for (;;) {
@@ -365,6 +413,10 @@ __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, boo
                     goto done;
                 }
                 ts = t0 + (__ll2float_rn(i) + jit) * dt;
+                if (ts < t_evt) {  // no admission, no retirement since the last step
+                    j = jfirst;
+                    break;
+                }
                 for (;;) {  // admission, refilling the window when it runs dry
                     while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
                     if (nxt < cnt || !more) break;
@@ -395,7 +447,15 @@ __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, boo
                 while (lo < nxt && w.X(lo) <= ts) ++lo;
                 j = lo;
                 while (j < nxt && !(w.X(j) > ts)) ++j;
-                if (j < nxt) break;
+                if (j < nxt) {
+                    jfirst = j;
+                    t_evt = nxt < cnt ? w.E(nxt) : 3.402823466e+38f;
+                    for (int q = j; q < nxt; ++q) {
+                        const float x = w.X(q);
+                        if (x > ts && x < t_evt) t_evt = x;
+                    }
+                    break;
+                }
                 if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:44
                 const float tNext = w.E(nxt);  // gap skip, march.cpp:45-49
                 const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
@@ -409,8 +469,8 @@ __device__ RayOut march_window(const Cands &cands, const Window &w, int cnt, boo
         {  // one primitive-sample (march.cpp:63-70)
             const int c = w.C(j);
             float sg, r, g, b;
-            sample_primitive<MT>(payload, mp.m, cands.prim(c), cands.xf(c), pw, mp.alpha, mp.beta,
-                             tab, sg, r, g, b);
+            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
+                                 g, b);
             sigmaSum += sg;
             rw += r * sg;
             gw += g * sg;
@@ -452,15 +512,14 @@ done:
     return out;
 }
 
-template <int CAP, class Cands>
-__device__ __forceinline__ RayOut march_ray(const Cands &cands, const Window &w, V3 o, V3 d,
+template <int CAP, class Cands, class Win>
+__device__ __forceinline__ RayOut march_ray(const Cands &cands, const Win &w, V3 o, V3 d,
                                             int2 px, float jit, const MarchDev &mp,
-                                            const float4 *__restrict__ payload,
                                             const unsigned long long *tab) {
     int cnt = 0;
     bool more = false;
     window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
-    return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, payload, tab);
+    return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
 }
 
 __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
@@ -502,98 +561,107 @@ __device__ __forceinline__ int2 tile_pixel(int tx, int ty, int tid) {
 }
 
 // ----------------------------------------------------------------------------------------
-// K5: one CTA per 16x16 tile.
-//   staging  the tile's candidates (transform + toModel(camera centre)) -> shared memory
-//   phase 1  every pixel: generateRay + exact segment window (all candidates)
+// K5: one CTA per 16x16 tile, heaviest tiles first (`order` from k_scan).
+//   staging  the tile's candidates -> shared memory (tiles with n <= kCandCap)
+//   phase 1  every pixel: generateRay + exact segment window over the candidates
 //   compact  rays with a non-empty window, in pixel order (misses write zeros and retire)
 //   phase 2  the first n_hit threads march the hit rays, so warps are full of live rays
-#ifndef VPB_MARCH_MINB
-#define VPB_MARCH_MINB 3
-#endif
-template <int CAP, int MT>
-__global__ void __launch_bounds__(kMarchThreads, VPB_MARCH_MINB)
-k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
-              const int4 *__restrict__ prects, const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
-              const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
-              int *__restrict__ ovf_list, int ovf_cap) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float4 *s_xf4 = reinterpret_cast<float4 *>(smem);                       // kCandCap * 4
-    float4 *s_om = s_xf4 + kCandCap * 4;                                    // kCandCap
-    int4 *s_prect = reinterpret_cast<int4 *>(s_om + kCandCap);             // kCandCap
-    int *s_prim = reinterpret_cast<int *>(s_prect + kCandCap);              // kCandCap
-    unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(s_prim + kCandCap);  // 32
-    int *s_state = reinterpret_cast<int *>(s_tab + 32);                     // 256: cnt | more<<8
-    int *s_list = s_state + kMarchThreads;                                  // 256
-    int *s_warp = s_list + kMarchThreads;                                   // 8
-    float *s_we = reinterpret_cast<float *>(s_warp + 8);                    // CAP * 256
-    float *s_wx = s_we + CAP * kMarchThreads;
-    int *s_wc = reinterpret_cast<int *>(s_wx + CAP * kMarchThreads);
+// Tiles with more than kCandCap candidates take the same path with TileCands<false>
+// (candidates read from global memory, 16-bit window indices); tiles beyond 65535
+// candidates send every pixel to the fallback re-march.
+struct TileSmem {
+    float4 *xf4;       // kCandCap * 4
+    float4 *om;        // kCandCap
+    int4 *prect;       // kCandCap
+    int *prim;         // kCandCap
+    unsigned long long *tab;  // 32
+    int *state;        // kMarchThreads: cnt | more << 8
+    int *list;         // kMarchThreads
+    int *warp;         // kMarchThreads / 32
+    float *we, *wx;    // CAP * kMarchThreads each
+    void *wc;          // CAP * kMarchThreads window indices (uint8 or uint16)
+};
 
-    if (ctr->key_overflow) return;
-    const int tile = blockIdx.x;
-    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-    const uint32_t start = offsets[tile];
-    const int n = (int)(offsets[tile + 1] - start);
-    const int staged = n < kCandCap ? n : kCandCap;
+template <int CAP, int MT, bool STAGED>
+__device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam, const MarchDev &mp,
+                                           const float *__restrict__ xf_g,
+                                           const int4 *__restrict__ prects,
+                                           const float4 *__restrict__ payload,
+                                           const unsigned long long *__restrict__ entries,
+                                           uint32_t start, int n, int tx, int ty, const OutDev &od,
+                                           DevCounters *ctr, int *__restrict__ ovf_list, int ovf_cap) {
+    using IdxT = typename std::conditional<STAGED, uint8_t, uint16_t>::type;
     const int tid = threadIdx.x;
+    const int m = MT > 0 ? MT : mp.m;
+    const unsigned m3 = (unsigned)(m * m * m);
     const V3 o = mk3(cam.center[0], cam.center[1], cam.center[2]);
-    if (tid < 32) s_tab[tid] = kExp2fTab[tid];
-    for (int i = tid; i < staged * 4; i += kMarchThreads) {
-        const int c = i >> 2, q = i & 3;
-        const int prim = (int)(uint32_t)(entries[start + c] & 0xffffffffull);
-        if (q == 0) s_prim[c] = prim;
-        s_xf4[i] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
+    if (STAGED) {
+        for (int i = tid; i < n * 4; i += kMarchThreads) {
+            const int c = i >> 2, q = i & 3;
+            const int prim = (int)(uint32_t)(entries[start + c] & 0xffffffffull);
+            if (q == 0) sm.prim[c] = prim;
+            sm.xf4[i] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
+        }
+        __syncthreads();
+        if (tid < n) {
+            const V3 om = to_model(reinterpret_cast<const float *>(sm.xf4 + tid * 4), o);
+            sm.om[tid] = make_float4(om.x, om.y, om.z, 0.f);
+            sm.prect[tid] = prects[sm.prim[tid]];
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    if (tid < staged) {
-        const V3 om = to_model(reinterpret_cast<const float *>(s_xf4 + tid * 4), o);
-        s_om[tid] = make_float4(om.x, om.y, om.z, 0.f);
-        s_prect[tid] = prects[s_prim[tid]];
-    }
-    __syncthreads();
-    const TileCands cands{entries, xf_g, prects, s_prim, reinterpret_cast<const float *>(s_xf4),
-                          s_om, s_prect, start, n, staged};
+    const TileCands<STAGED> cands{entries, xf_g, prects, payload, m3, start, n, sm.prim,
+                                  reinterpret_cast<const float *>(sm.xf4), sm.om, sm.prect};
+    IdxT *wc = reinterpret_cast<IdxT *>(sm.wc);
 
     // phase 1: segment windows
     const int2 px = tile_pixel(tx, ty, tid);
     const bool valid = px.x < cam.width && px.y < cam.height;
+    const int64_t pix = (int64_t)px.y * cam.width + px.x;
     int cnt = 0;
     bool more = false;
+    if (!STAGED && n > 65535) {  // window indices would not fit: re-march every pixel wide
+        if (valid) {
+            const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
+            if (slot < ovf_cap) ovf_list[slot] = (int)pix;
+        }
+        return;
+    }
     if (valid && n > 0) {
         V3 rd, d;
         generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
-        const Window w{s_we, s_wx, s_wc, kMarchThreads, tid};
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid};
         window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
-    s_state[tid] = cnt | (more ? 256 : 0);
-    if (valid && cnt == 0) write_pixel(od, (int64_t)px.y * cam.width + px.x, RayOut{});
+    sm.state[tid] = cnt | (more ? 256 : 0);
+    if (valid && cnt == 0) write_pixel(od, pix, RayOut{});
     // compaction of hit rays (block-wide exclusive scan of the hit flags)
     const bool hit = cnt > 0;
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
     const int wid = tid >> 5, lane = tid & 31;
-    if (lane == 0) s_warp[wid] = __popc(bal);
+    if (lane == 0) sm.warp[wid] = __popc(bal);
     __syncthreads();
     int base = 0, n_hit = 0;
     for (int q = 0; q < kMarchThreads / 32; ++q) {
-        base += q < wid ? s_warp[q] : 0;
-        n_hit += s_warp[q];
+        base += q < wid ? sm.warp[q] : 0;
+        n_hit += sm.warp[q];
     }
-    if (hit) s_list[base + __popc(bal & ((1u << lane) - 1))] = tid;
+    if (hit) sm.list[base + __popc(bal & ((1u << lane) - 1))] = tid;
     __syncthreads();
 
     // phase 2: march the hit rays
     RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
     const bool live = tid < n_hit;
     if (live) {
-        const int r = s_list[tid];
+        const int r = sm.list[tid];
         const int2 rp = tile_pixel(tx, ty, r);
         const int64_t p = (int64_t)rp.y * cam.width + rp.x;
         V3 rd, d;
         generate_ray(cam, (float)rp.x + 0.5f, (float)rp.y + 0.5f, rd, d);
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
-        const int st = s_state[r];
-        const Window w{s_we, s_wx, s_wc, kMarchThreads, r};
-        ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, payload, s_tab);
+        const int st = sm.state[r];
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r};
+        ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, sm.tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)p;
@@ -604,16 +672,54 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     add_counters(ctr, ro, live && !ro.overflow);
 }
 
+#ifndef VPB_MARCH_MINB
+#define VPB_MARCH_MINB 3
+#endif
+template <int CAP, int MT>
+__global__ void __launch_bounds__(kMarchThreads, VPB_MARCH_MINB)
+k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
+              const int4 *__restrict__ prects, const float4 *__restrict__ payload,
+              const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ order,
+              const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
+              int *__restrict__ ovf_list, int ovf_cap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    TileSmem sm;
+    sm.xf4 = reinterpret_cast<float4 *>(smem);
+    sm.om = sm.xf4 + kCandCap * 4;
+    sm.prect = reinterpret_cast<int4 *>(sm.om + kCandCap);
+    sm.prim = reinterpret_cast<int *>(sm.prect + kCandCap);
+    sm.tab = reinterpret_cast<unsigned long long *>(sm.prim + kCandCap);
+    sm.state = reinterpret_cast<int *>(sm.tab + 32);
+    sm.list = sm.state + kMarchThreads;
+    sm.warp = sm.list + kMarchThreads;
+    sm.we = reinterpret_cast<float *>(sm.warp + kMarchThreads / 32);
+    sm.wx = sm.we + CAP * kMarchThreads;
+    sm.wc = sm.wx + CAP * kMarchThreads;
+
+    if (ctr->key_overflow) return;
+    const int tile = (int)order[blockIdx.x];
+    const uint32_t start = offsets[tile];
+    const int n = (int)(offsets[tile + 1] - start);
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    if (threadIdx.x < 32) sm.tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    if (n <= kCandCap)
+        march_tile<CAP, MT, true>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
+                                  ovf_list, ovf_cap);
+    else
+        march_tile<CAP, MT, false>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
+                                   ovf_list, ovf_cap);
+}
+
 // K5b: rays whose live segments overflowed the shared-memory window are re-marched with a
 // kFallbackCap-entry window in global scratch (one window per thread of a fixed grid).
 template <bool kRays>
 __global__ void __launch_bounds__(kFallbackThreads)
-k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, const int4 *__restrict__ prects,
-                 int n_prim,
-                 const float4 *__restrict__ payload, const uint32_t *__restrict__ offsets,
-                 const unsigned long long *__restrict__ entries, OutDev od, RaysDev rays,
-                 DevCounters *ctr, const int *__restrict__ ovf_list, int ovf_cap,
-                 float *scratch_e, float *scratch_x, int *scratch_c) {
+k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
+                 const int4 *__restrict__ prects, int n_prim, const float4 *__restrict__ payload,
+                 const uint32_t *__restrict__ offsets, const unsigned long long *__restrict__ entries,
+                 OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ ovf_list,
+                 int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c) {
     __shared__ unsigned long long s_tab[32];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
@@ -621,7 +727,8 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, const 
     const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const Window w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const unsigned m3 = (unsigned)(mp.m * mp.m * mp.m);
     for (int q = gtid; q < n_ovf; q += nthreads) {
         const int p = ovf_list[q];
         V3 o, d;
@@ -631,17 +738,18 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g, const 
             o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
             d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
             if (rays.jitter) jit = rays.jitter[p];
-            const AllCands cands{xf_g, n_prim};
-            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(0, 0), jit, mp, payload, s_tab);
+            const AllCands cands{xf_g, payload, m3, n_prim};
+            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
         } else {
             const int px = p % cam.width, py = p / cam.width;
             const int tile = (py / kTile) * cam.tiles_x + px / kTile;
             generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
             if (mp.jitter) jit = hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p));
             const uint32_t start = offsets[tile];
-            const TileCands cands{entries, xf_g, prects, nullptr, nullptr, nullptr, nullptr, start,
-                                  (int)(offsets[tile + 1] - start), 0};
-            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, payload, s_tab);
+            const TileCands<false> cands{entries, xf_g, prects, payload, m3, start,
+                                         (int)(offsets[tile + 1] - start), nullptr, nullptr, nullptr,
+                                         nullptr};
+            ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, s_tab);
         }
         if (ro.overflow) {
             atomicAdd(&ctr->fallback_fail, 1);
@@ -677,9 +785,9 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const AllCands cands{xf_g, n_prim};
-        const Window w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
-        ro = march_ray<CAP>(cands, w, o, d, make_int2(0, 0), jit, mp, payload, s_tab);
+        const AllCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim};
+        const Window<int> w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
+        ro = march_ray<CAP>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
             if (slot < ovf_cap) ovf_list[slot] = (int)r;
@@ -689,8 +797,7 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     add_counters(ctr, ro, valid && !ro.overflow);
 }
 
-// Zero the outputs of tiles without candidates is implicit in k_march_tiles (n == 0 path);
-// composite() is elementwise.
+// composite() is elementwise (march.cpp:134-147).
 __global__ void k_composite(const float *__restrict__ rgb, const float *__restrict__ alpha,
                             const float *__restrict__ bg, float *__restrict__ out, int64_t n_px) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -717,7 +824,7 @@ constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared me
 
 size_t march_tiles_smem() {
     return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 * 2 + kCandCap * 4 + 32 * 8 +
-           kMarchThreads * 4 * 2 + 8 * 4 + (size_t)kWindowCap * kMarchThreads * 12;
+           kMarchThreads * 4 * 2 + (kMarchThreads / 32) * 4 + (size_t)kWindowCap * kMarchThreads * (8 + 2);
 }
 
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
@@ -737,12 +844,12 @@ cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream
 
 cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
                            int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
-                           uint32_t *cursor, unsigned long long *entries, int64_t capacity,
-                           DevCounters *ctr, cudaStream_t st) {
+                           uint32_t *cursor, uint32_t *order, unsigned long long *entries,
+                           int64_t capacity, DevCounters *ctr, cudaStream_t st) {
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
     if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
-    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, ctr, capacity);
+    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity);
     if (n_prim > 0) k_emit<<<(n_prim + 127) / 128, 128, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
     k_tile_sort<<<n_tiles, 128, 0, st>>>(offsets, entries, ctr);
     return cudaGetLastError();
@@ -751,40 +858,45 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
 template <int MT>
 static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const float *xf16,
                                   const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                                  const unsigned long long *entries, const OutDev &od,
-                                  DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
+                                  const uint32_t *order, const unsigned long long *entries,
+                                  const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                                  cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = march_tiles_smem();
+    auto kern = k_march_tiles<kWindowCap, MT>;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_march_tiles<kWindowCap, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_march_tiles<kWindowCap, MT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
-    k_march_tiles<kWindowCap, MT><<<cam.tiles_x * cam.tiles_y, kMarchThreads, smem, st>>>(
-        cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap);
+    kern<<<cam.tiles_x * cam.tiles_y, kMarchThreads, smem, st>>>(cam, mp, xf16, prects, payload, offsets,
+                                                                order, entries, od, ctr, ovf_list, ovf_cap);
     return cudaGetLastError();
 }
 
 cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
                                const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                               const unsigned long long *entries, const OutDev &od,
-                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st) {
+                               const uint32_t *order, const unsigned long long *entries,
+                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                               cudaStream_t st) {
     if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
+#define VPB_TILES(MT) launch_tiles_m<MT>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st)
     switch (mp.m) {  // compile-time voxel counts for the common grids
-    case 4: return launch_tiles_m<4>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
-    case 8: return launch_tiles_m<8>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
-    case 16: return launch_tiles_m<16>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
-    case 32: return launch_tiles_m<32>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
-    default: return launch_tiles_m<0>(cam, mp, xf16, prects, payload, offsets, entries, od, ctr, ovf_list, ovf_cap, st);
+    case 4: return VPB_TILES(4);
+    case 8: return VPB_TILES(8);
+    case 16: return VPB_TILES(16);
+    case 32: return VPB_TILES(32);
+    default: return VPB_TILES(0);
     }
+#undef VPB_TILES
 }
 
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
-                                  const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
-                                  const uint32_t *offsets, const unsigned long long *entries,
-                                  const OutDev &od, const RaysDev &rays, DevCounters *ctr,
-                                  const int *ovf_list, int ovf_cap, float *se, float *sx,
-                                  int *sc, cudaStream_t st) {
+                                  const float *xf16, const int4 *prects, int n_prim,
+                                  const float4 *payload, const uint32_t *offsets,
+                                  const unsigned long long *entries, const OutDev &od,
+                                  const RaysDev &rays, DevCounters *ctr, const int *ovf_list,
+                                  int ovf_cap, float *se, float *sx, int *sc, cudaStream_t st) {
     if (rays_mode)
         k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
             cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);

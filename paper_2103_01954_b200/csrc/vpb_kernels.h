@@ -53,12 +53,13 @@ cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, in
 cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream_t st);
 cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
                            int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
-                           uint32_t *cursor, unsigned long long *entries, int64_t capacity,
-                           DevCounters *ctr, cudaStream_t st);
+                           uint32_t *cursor, uint32_t *order, unsigned long long *entries,
+                           int64_t capacity, DevCounters *ctr, cudaStream_t st);
 cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
                                const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                               const unsigned long long *entries, const OutDev &od,
-                               DevCounters *ctr, int *ovf_list, int ovf_cap, cudaStream_t st);
+                               const uint32_t *order, const unsigned long long *entries,
+                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                               cudaStream_t st);
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
                                   const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
                                   const uint32_t *offsets, const unsigned long long *entries,
