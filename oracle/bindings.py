@@ -71,6 +71,8 @@ class Oracle:
                                  C.c_int32, C.c_uint64, C.c_uint64, f32p, f32p, i32p, C.c_int32]
         L.vpo_composite.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]
         L.vpo_cull.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, i32p, u32p]
+        L.vpo_cull_px.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, i32p, i32p,
+                                  u32p]
         L.vpo_tile_lists.restype = C.c_int64
         L.vpo_tile_lists.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32,
                                      i32p, i32p, C.c_int64]
@@ -144,6 +146,18 @@ class Oracle:
         self.lib.vpo_cull(k, _p(xf), _p(k9), _p(r9), _p(t3), int(cam.width), int(cam.height),
                           _p(rects, i32p), _p(keys, u32p))
         return rects[:k], keys[:k]
+
+    def cull_px(self, xf15, cam):
+        """(tile rects, pixel rects, depth keys)."""
+        xf = _f(xf15).reshape(-1, 15)
+        k = xf.shape[0]
+        k9, r9, t3 = cam_arrays(cam)
+        rects = np.zeros((max(k, 1), 4), np.int32)
+        prects = np.zeros((max(k, 1), 4), np.int32)
+        keys = np.zeros(max(k, 1), np.uint32)
+        self.lib.vpo_cull_px(k, _p(xf), _p(k9), _p(r9), _p(t3), int(cam.width), int(cam.height),
+                             _p(rects, i32p), _p(prects, i32p), _p(keys, u32p))
+        return rects[:k], prects[:k], keys[:k]
 
     def tile_lists(self, xf15, cam):
         xf = _f(xf15).reshape(-1, 15)

@@ -444,7 +444,7 @@ void vpo_composite(int32_t width, int32_t height, const float *rgb, const float 
  * Identical float operation sequence to k_cull in paper_2103_01954_b200/csrc/vpb_kernels.cu.
  */
 static void cull_one(const float *xf, const float *k9, const float *r9, const float *t3,
-                     int32_t width, int32_t height, int32_t *rect, uint32_t *key) {
+                     int32_t width, int32_t height, int32_t *rect, int32_t *prect, uint32_t *key) {
     const v3 s = ld3(xf + 12);
     const float r = sqrtf(dot3(s, s));
     const float rr = r * 1.001f + 1e-6f;
@@ -458,11 +458,14 @@ static void cull_one(const float *xf, const float *k9, const float *r9, const fl
     const int32_t tiles_x = (width + VPO_TILE - 1) / VPO_TILE;
     const int32_t tiles_y = (height + VPO_TILE - 1) / VPO_TILE;
     rect[0] = 0; rect[1] = 0; rect[2] = -1; rect[3] = -1;
+    prect[0] = 0; prect[1] = 0; prect[2] = -1; prect[3] = -1;
     if (width <= 0 || height <= 0) return;
     if (cc.z + rr < 0) return; /* entirely behind the camera plane */
     if (cc.z - rr <= 1e-3f * rr) { /* straddles or hugs the camera plane: every tile */
         rect[2] = tiles_x - 1;
         rect[3] = tiles_y - 1;
+        prect[2] = width - 1;
+        prect[3] = height - 1;
         return;
     }
     float umin = FLT_MAX, umax = -FLT_MAX, vmin = FLT_MAX, vmax = -FLT_MAX;
@@ -487,18 +490,31 @@ static void cull_one(const float *xf, const float *k9, const float *r9, const fl
     y0 = y0 > 0 ? y0 : 0;
     x1 = x1 < wl ? x1 : wl;
     y1 = y1 < hl ? y1 : hl;
-    rect[0] = (int32_t)x0 / VPO_TILE;
-    rect[1] = (int32_t)y0 / VPO_TILE;
-    rect[2] = (int32_t)x1 / VPO_TILE;
-    rect[3] = (int32_t)y1 / VPO_TILE;
+    prect[0] = (int32_t)x0;
+    prect[1] = (int32_t)y0;
+    prect[2] = (int32_t)x1;
+    prect[3] = (int32_t)y1;
+    rect[0] = prect[0] / VPO_TILE;
+    rect[1] = prect[1] / VPO_TILE;
+    rect[2] = prect[2] / VPO_TILE;
+    rect[3] = prect[3] / VPO_TILE;
 }
 
 void vpo_cull(int32_t n_prim, const float *xf15, const float *k9, const float *r9,
               const float *t3, int32_t width, int32_t height, int32_t *rect4,
               uint32_t *depth_key) {
-    for (int32_t k = 0; k < n_prim; ++k)
-        cull_one(xf15 + 15 * (size_t)k, k9, r9, t3, width, height, rect4 + 4 * (size_t)k,
+    vpo_cull_px(n_prim, xf15, k9, r9, t3, width, height, rect4, NULL, depth_key);
+}
+
+void vpo_cull_px(int32_t n_prim, const float *xf15, const float *k9, const float *r9,
+                 const float *t3, int32_t width, int32_t height, int32_t *rect4, int32_t *prect4,
+                 uint32_t *depth_key) {
+    for (int32_t k = 0; k < n_prim; ++k) {
+        int32_t pr[4];
+        cull_one(xf15 + 15 * (size_t)k, k9, r9, t3, width, height, rect4 + 4 * (size_t)k, pr,
                  depth_key + k);
+        if (prect4) memcpy(prect4 + 4 * (size_t)k, pr, sizeof pr);
+    }
 }
 
 static int cmp_u64(const void *a, const void *b) {

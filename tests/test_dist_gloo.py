@@ -1,0 +1,110 @@
+"""CPU, world_size 2 (gloo): the multi-GPU plumbing of paper_2103_01954_b200/dist.py —
+view sharding, the one-time scene broadcast and the per-view gather to rank 0 — with a fake
+renderer standing in for the device context."""
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2103_01954_b200.dist import ViewGather, broadcast_scene, view_shard
+
+
+def test_view_shard_partitions():
+    for n, world in ((64, 1), (64, 2), (64, 8), (10, 3), (3, 4)):
+        parts = [view_shard(n, world, r) for r in range(world)]
+        flat = [v for p in parts for v in p]
+        assert sorted(flat) == list(range(n))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    assert view_shard(64, 8, 3, per_rank=8) == list(range(24, 32))
+    assert view_shard(64, 1, 0, per_rank=8) == list(range(8))
+    with pytest.raises(ValueError):
+        view_shard(64, 2, 2)
+
+
+class FakeRenderer:
+    """Implements the Renderer methods broadcast_scene uses, on host memory."""
+
+    def __init__(self):
+        self.xf = None
+        self.payload = None
+        self.n_prim = self.m = None
+
+    def set_scene_composed(self, xf, slab, window):
+        self.xf = np.array(xf, np.float32)
+        self.n_prim, self.m = xf.shape[0], slab.voxels_per_axis
+        if slab.payload is not None:  # "repack": planar (k, c, v) -> interleaved (k, v, c)
+            k, m3 = self.n_prim, self.m ** 3
+            self.payload = np.ascontiguousarray(slab.payload.reshape(k, 4, m3).transpose(0, 2, 1)).reshape(-1)
+
+    def payload_floats(self):
+        return self.n_prim * self.m ** 3 * 4
+
+    def copy_payload_to(self, ptr):
+        ctypes.memmove(ptr, self.payload.ctypes.data, self.payload.nbytes)
+
+    def set_payload_interleaved(self, ptr):
+        n = self.payload_floats()
+        self.payload = np.ctypeslib.as_array((ctypes.c_float * n).from_address(ptr)).copy()
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_01954_b200.api import PrimitiveSlab, WindowParams
+        k, m = 5, 2
+        rng = np.random.default_rng(7)
+        xf = rng.uniform(-1, 1, (k, 15)).astype(np.float32)
+        planar = rng.uniform(0, 1, k * 4 * m ** 3).astype(np.float32)
+        r = FakeRenderer()
+        nbytes = broadcast_scene(r, xf if rank == 0 else None, PrimitiveSlab(k, m, planar) if rank == 0 else None,
+                                 WindowParams(), k, m, "cpu")
+        want = planar.reshape(k, 4, m ** 3).transpose(0, 2, 1).reshape(-1)
+        ok_bcast = bool(np.array_equal(r.payload, want) and np.array_equal(r.xf, xf) and nbytes == want.nbytes)
+
+        # per-view gather: each rank renders 3 "views" of 4x2 pixels
+        w, h, nv = 4, 2, 3
+        vg = ViewGather(nv, w, h, "cpu", world, rank)
+        rgb, alpha, samples = vg.views()
+        for j in range(nv):
+            rgb[j].fill_(rank * 10 + j)
+            alpha[j].fill_(0.5 + rank)
+            samples[j].fill_(100 * rank + j)
+            vg.gather_view(j)
+        vg.finish()
+        ok_gather = True
+        if rank == 0:
+            for j in range(nv):
+                rows = vg.gathered(j)
+                for src in range(world):
+                    c, a, s = ViewGather.unpack(rows[src], w, h)
+                    ok_gather &= bool(torch.all(c == src * 10 + j)) and bool(torch.all(a == 0.5 + src))
+                    ok_gather &= bool(torch.all(s == 100 * src + j))
+        q.put((rank, ok_bcast, ok_gather))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_broadcast_and_gather_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert res == [(0, True, True), (1, True, True)]
