@@ -378,6 +378,159 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
 }
 
 // The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
+// segment list (filled by window_scan). Entries [0, nxt) have been admitted; `act` is the
+// bitmask of admitted entries still live (tExit > ts). Iterating its set bits in ascending
+// order visits the reference's `active` list in its order (admission order = window order).
+// The reference's `ts >= tMax` break is implied: it only fires once every segment is
+// admitted and retired, where the empty-active-set branch breaks on the same step.
+//
+// Events are tracked in registers: nextE = tEnter of the next pending entry, minX = the
+// earliest exit among live entries. A step touches the window (shared memory) only when
+// ts reaches one of them, so most steps cost a compare.
+//
+// The loop is flattened to one primitive-sample per iteration: a lane first finds its next
+// lattice step with a non-empty active set, then evaluates one active primitive; the step's
+// accumulation happens after its last active primitive. Lanes whose steps have different
+// numbers of active primitives stay in lock-step on primitive-samples.
+template <int CAP, int MT, class Cands, class Win>
+__device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
+                               V3 d, int2 px, float jit, const MarchDev &mp,
+                               const unsigned long long *tab) {
+    static_assert(CAP <= 32, "the active set is a 32-bit mask");
+    const float kInf = __int_as_float(0x7f800000);
+    RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (cnt == 0) return out;
+    out.hit = 1;
+    const float dt = mp.dt;
+    const float t0 = w.E(0);
+    int nxt = 0, j = 0;
+    unsigned act = 0;
+    float nextE = t0, minX = kInf;
+    long long i = 0;
+    float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+    V3 pw = o;
+    bool sampling = false;
+    for (;;) {
+        if (!sampling) {
+            for (;;) {  // next lattice step with a non-empty active set
+                if (i > (1ll << 40)) {  // the reference would spin; report instead of hanging
+                    out.numeric = 1;
+                    goto done;
+                }
+                ts = t0 + (__ll2float_rn(i) + jit) * dt;
+                if (ts >= minX) {  // retirement (march.cpp:39-41)
+                    minX = kInf;
+                    for (unsigned m = act; m; m &= m - 1) {
+                        const int q = __ffs(m) - 1;
+                        const float x = w.X(q);
+                        if (x <= ts) act &= ~(1u << q);
+                        else minX = fminf(minX, x);
+                    }
+                }
+                if (nxt < cnt ? nextE <= ts : more) {  // admission (march.cpp:38), with refill
+                    for (;;) {
+                        while (nxt < cnt && nextE <= ts) {
+                            const float x = w.X(nxt);
+                            if (x > ts) {  // admitted and not retired in the same step
+                                act |= 1u << nxt;
+                                minX = fminf(minX, x);
+                            }
+                            ++nxt;
+                            nextE = nxt < cnt ? w.E(nxt) : kInf;
+                        }
+                        if (nxt < cnt || !more) break;
+                        // window exhausted while hits remain: keep the live entries (in
+                        // order), then fetch the next hits after the last key
+                        const float lastE = w.E(cnt - 1);
+                        const int lastP = cands.prim(w.C(cnt - 1));
+                        int live = 0;
+                        for (unsigned m = act; m; m &= m - 1, ++live) {
+                            const int q = __ffs(m) - 1;
+                            if (live != q) {
+                                w.E(live) = w.E(q);
+                                w.X(live) = w.X(q);
+                                w.C(live) = w.C(q);
+                            }
+                        }
+                        if (live == CAP) {
+                            out.overflow = 1;
+                            return out;
+                        }
+                        act = (1u << live) - 1u;
+                        cnt = live;
+                        nxt = live;
+                        more = false;
+                        ++out.refills;
+                        window_scan<CAP>(w, cands, cnt, more, o, d, px, false, lastE, lastP);
+                        nextE = nxt < cnt ? w.E(nxt) : kInf;
+                    }
+                }
+                if (act) {
+                    j = __ffs(act) - 1;
+                    break;
+                }
+                if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:43-44
+                // gap skip to the next entry (march.cpp:45-49)
+                const long long skipTo = (long long)ceil((double)((nextE - t0) / dt) - (double)jit);
+                i = skipTo > i + 1 ? skipTo : i + 1;
+            }
+            sampling = true;
+            sigmaSum = 0.f;
+            rw = gw = bw = 0.f;
+            pw = o + d * ts;
+        }
+        {  // one primitive-sample (march.cpp:63-70)
+            const int c = w.C(j);
+            float sg, r, g, b;
+            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
+                                 g, b);
+            sigmaSum += sg;
+            rw += r * sg;
+            gw += g * sg;
+            bw += b * sg;
+            ++out.prim_samples;
+        }
+        const unsigned rest = act & ~((2u << j) - 1u);
+        if (rest) {
+            j = __ffs(rest) - 1;
+            continue;
+        }
+        // step complete: march.cpp:71-88
+        sampling = false;
+        ++out.samples;
+        const float dT = sigmaSum * dt;
+        if (transmittance + dT >= 1.0f) {
+            const float frac = (1.0f - transmittance) / dT;
+            const float f = dt * frac;
+            cr += rw * f;
+            cg += gw * f;
+            cb += bw * f;
+            transmittance = 1.0f;
+            out.saturated = 1;
+            break;
+        }
+        cr += rw * dt;
+        cg += gw * dt;
+        cb += bw * dt;
+        transmittance += dT;
+        if (transmittance > 1.0f - mp.eps) {
+            out.early = 1;
+            break;
+        }
+        ++i;
+    }
+done:
+    out.r = cr;
+    out.g = cg;
+    out.b = cb;
+    out.alpha = transmittance;
+    return out;
+}
+
+// Generic variant for windows wider than 32 entries (the fallback re-march): the same
+// quadrature, with the live entries found by scanning the window instead of a bitmask.
+// The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
 // segment list (filled by window_scan). Entries [0, nxt) are admitted; an admitted entry is
 // live while tExit > ts, and the live ones in window order are exactly the reference's
 // `active` list. The reference's `ts >= tMax` break is implied: it only fires once every
@@ -390,7 +543,7 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
 // active set does not change: t_evt = min(next entry, earliest exit of a live entry), and
 // while ts < t_evt a step reuses the previous active set without touching the window.
 template <int CAP, int MT, class Cands, class Win>
-__device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
+__device__ RayOut march_window_generic(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
                                V3 d, int2 px, float jit, const MarchDev &mp,
                                const unsigned long long *tab) {
     RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -519,7 +672,10 @@ __device__ __forceinline__ RayOut march_ray(const Cands &cands, const Win &w, V3
     int cnt = 0;
     bool more = false;
     window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
-    return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
+    if constexpr (CAP <= 32)
+        return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
+    else
+        return march_window_generic<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
 }
 
 __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
@@ -818,7 +974,7 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 // ----------------------------------------------------------------------------------------
 // Host-side launchers (plain C++ signatures for vpb_api.cpp).
 #ifndef VPB_WINDOW_CAP
-#define VPB_WINDOW_CAP 16
+#define VPB_WINDOW_CAP 24
 #endif
 constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared memory)
 
