@@ -62,3 +62,18 @@ def test_module_level_render_and_composite():
     img = api.composite(out, bg)
     a = out.alpha
     assert np.allclose(img, a * out.color + (1 - a) * bg, atol=1e-7)
+
+
+def test_reference_dropin_adapter_is_bitwise_identical():
+    """oracle/_ref/dropin_check: the reference's volprim::render vs volprim::render_b200 (the
+    adapter of INTEGRATION.md over libvpb.so) on the same Scene, compared bitwise. The binary
+    is built where /root/reference exists (oracle/Makefile `dropin`) and travels prebuilt."""
+    import pathlib
+    import subprocess
+    exe = pathlib.Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "dropin_check"
+    if not exe.exists():
+        pytest.skip("dropin_check not built (needs /root/reference at build time)")
+    for args in (["64", "16", "256"], ["512", "8", "384"]):
+        r = subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "IDENTICAL" in r.stdout
