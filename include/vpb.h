@@ -136,6 +136,20 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                   const float *jitter01, const vp_march *cfg, float *rgb, float *alpha,
                   int32_t *samples);
 
+/* backwardRay (grad.cpp:34-195) for a batch of rays through the resident frame, given the
+ * output adjoints adj_rgb (n*3, dLoss/d rgb) and adj_alpha (n, dLoss/d alpha), exactly the
+ * values evalLoss passes (grad.cpp:240-248). transforms24 are the frame's PrimitiveTransform
+ * records (K*24): rBase and deltaR enter the rotation Jacobians; they must compose to the
+ * resident transforms. grads (host or device) holds K*4*M^3 + 9*K floats in the GradBuffer
+ * layout (params.h:12-27): the planar payload gradient, then deltaT[3] deltaR[3] deltaS[3]
+ * per primitive. accumulate != 0 adds into it, else it is overwritten. Per-sample terms
+ * match the reference bit for bit; the global sums use device atomics, so their summation
+ * order (and last bits) differ from the reference's sequential loop. Synchronous. */
+int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
+                     const float *jitter01, const float *adj_rgb, const float *adj_alpha,
+                     const vp_march *cfg, const float *transforms24, float *grads,
+                     int32_t accumulate);
+
 /* composite() (march.cpp:134-147): out = A*I + (1-A)*B, all H*W(*3) arrays. */
 int vp_composite(vp_ctx *ctx, int32_t width, int32_t height, const float *rgb,
                  const float *alpha, const float *background, float *out);

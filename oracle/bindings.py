@@ -76,6 +76,9 @@ class Oracle:
         L.vpo_tile_lists.restype = C.c_int64
         L.vpo_tile_lists.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32,
                                      i32p, i32p, C.c_int64]
+        L.vpo_backward_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, C.c_float, C.c_int32,
+                                        C.c_int64, f32p, f32p, f32p, f32p, f32p, C.c_float,
+                                        C.c_float, f32p]
         L.vpo_expf_port.restype = C.c_float
         L.vpo_expf_port.argtypes = [C.c_float]
         L.vpo_expf_mismatches.restype = C.c_int64
@@ -119,6 +122,24 @@ class Oracle:
                                 float(cfg.early_eps), int(cfg.accumulation_permutation), _p(rgb),
                                 _p(alpha), _p(samples, i32p))
         return rgb, alpha, samples
+
+    def backward_rays(self, tr24, m, payload, window, origins, dirs, adj_rgb, adj_alpha, cfg,
+                      jitter=None):
+        """backwardRay restatement; returns the GradBuffer values (payload planar | 9K)."""
+        tr = _f(tr24).reshape(-1, 24)
+        k = tr.shape[0]
+        rc, xf = self.compose(tr)
+        assert rc == 0
+        o = _f(origins).reshape(-1, 3)
+        d = _f(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        j = None if jitter is None else _f(jitter).reshape(n)
+        g = np.zeros(k * 4 * int(m) ** 3 + 9 * k, np.float32)
+        self.lib.vpo_backward_rays(k, int(m), _p(tr), _p(xf), _p(_f(payload)), float(window.alpha),
+                                   int(window.beta), n, _p(o), _p(d), _p(j), _p(_f(adj_rgb).reshape(n, 3)),
+                                   _p(_f(adj_alpha).reshape(n)), float(cfg.step_size), float(cfg.early_eps),
+                                   _p(g))
+        return g
 
     def generate_ray(self, cam, px, py):
         k9, r9, t3 = cam_arrays(cam)
@@ -216,6 +237,9 @@ class RefCore:
         L.vpref_march_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32,
                                        C.c_int64, f32p, f32p, f32p, C.c_float, C.c_float,
                                        C.c_uint64, f32p, f32p, i32p]
+        L.vpref_backward_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32,
+                                          C.c_int64, f32p, f32p, f32p, f32p, f32p, C.c_float,
+                                          C.c_float, f32p]
         L.vpref_window.restype = C.c_float
         L.vpref_window.argtypes = [C.c_float] * 4 + [C.c_int32]
 
@@ -295,3 +319,20 @@ class RefCore:
 
     def window(self, x, y, z, alpha=8.0, beta=8):
         return self.lib.vpref_window(x, y, z, alpha, beta)
+
+    def backward_rays(self, tr24, m, payload, window, origins, dirs, adj_rgb, adj_alpha, cfg,
+                      jitter=None):
+        tr = _f(tr24).reshape(-1, 24)
+        k = tr.shape[0]
+        o = _f(origins).reshape(-1, 3)
+        d = _f(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        j = None if jitter is None else _f(jitter).reshape(n)
+        g = np.zeros(k * 4 * int(m) ** 3 + 9 * k, np.float32)
+        rc = self.lib.vpref_backward_rays(k, int(m), _p(tr), _p(_f(payload)), float(window.alpha),
+                                          int(window.beta), n, _p(o), _p(d), _p(j),
+                                          _p(_f(adj_rgb).reshape(n, 3)), _p(_f(adj_alpha).reshape(n)),
+                                          float(cfg.step_size), float(cfg.early_eps), _p(g))
+        if rc != 0:
+            raise RuntimeError(f"reference backward failed ({rc}): {self.error()}")
+        return g

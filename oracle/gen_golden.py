@@ -171,6 +171,46 @@ def main():
     np.savez_compressed(OUT / "march_kats.npz",
                         **{f"{k}__{f}": v for k, d_ in kats.items() for f, v in d_.items()})
 
+    # -- backward pass: backwardRay (grad.cpp:34-195) with given output adjoints ---------------
+    bwd = {}
+
+    def bcase(name, trs, m, pay, win, cfg, o, d, jit, ar, aa):
+        g = ref.backward_rays(trs, m, pay, win, o, d, ar, aa, cfg, jit)
+        bwd[name] = dict(tr=np.asarray(trs, np.float32), m=np.int32(m), payload=np.asarray(pay, np.float32),
+                         window=np.array([win.alpha, win.beta], np.float32),
+                         cfg=np.array([cfg.step_size, cfg.early_eps], np.float32), o=o, d=d, jit=jit,
+                         adj_rgb=ar, adj_alpha=aa, grads=g)
+
+    nb, mb = 40, 4
+    trs = api.transform_records(rng.uniform(-0.5, 0.5, (nb, 3)), np.tile(np.eye(3), (nb, 1, 1)),
+                                0.05 + 0.2 * np.abs(rng.uniform(-1, 1, (nb, 3))),
+                                delta_t=rng.uniform(-0.02, 0.02, (nb, 3)), delta_r=rng.uniform(-1, 1, (nb, 3)))
+    pay = rng.uniform(0, 1, (nb, 4, mb, mb, mb)).astype(np.float32)
+    pay[:, 3] *= 8
+    nr = 512
+    o = (rng.uniform(-1, 1, (nr, 3)) * 0.25 + np.array([0, 0, -2])).astype(np.float32)
+    d = np.array([0, 0, 1]) + rng.normal(size=(nr, 3)) * 0.15
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    o[:16] = np.asarray(api.compose(trs)[:16, :3])  # origins inside boxes: no anchor chain
+    jit = rng.uniform(0, 1, nr).astype(np.float32)
+    ar = rng.normal(size=(nr, 3)).astype(np.float32)
+    aa = rng.normal(size=nr).astype(np.float32)
+    bcase("boxes_unsaturated", trs, mb, pay.reshape(-1), api.WindowParams(8, 8), api.MarchConfig(0.002, 0.01),
+          o, d, jit, ar, aa)
+    pay2 = pay.copy()
+    pay2[:, 3] *= 6
+    bcase("boxes_saturating", trs, mb, pay2.reshape(-1), api.WindowParams(8, 8), api.MarchConfig(0.002, 1e-7),
+          o, d, jit, ar, aa)
+    trs8, pays8 = synthetic.shell_arrays(64, 8)
+    camb = synthetic.shell_camera(-1, 0, 64)
+    from oracle.bindings import Oracle
+    orc = Oracle()
+    pix = rng.integers(0, 64, (nr, 2))
+    rays = np.array([np.concatenate(orc.generate_ray(camb, x + 0.5, y + 0.5)) for x, y in pix], np.float32)
+    bcase("shell64_m8_camera_rays", trs8, 8, pays8, api.WindowParams(8, 8), api.MarchConfig(0.001, 0.01),
+          rays[:, :3].copy(), rays[:, 3:].copy(), np.full(nr, 0.5, np.float32), ar, aa)
+    np.savez_compressed(OUT / "backward.npz", **{f"{k}__{f}": v for k, d_ in bwd.items() for f, v in d_.items()})
+
     # -- full renders (march.cpp:95-132) -------------------------------------------------------
     store, meta = {}, digests["meta"]
     tr, pay = synthetic.shell_arrays(64, 16)

@@ -13,6 +13,7 @@
 //   vpref_march_rays    -> intersect + march          (march.cpp:18-93)
 //   vpref_generate_ray  -> generateRay                (camera.cpp:14-23)
 //   vpref_window        -> window                     (primitive.cpp:25-28)
+//   vpref_backward_rays -> intersect + backwardRay    (grad.cpp:34-195) into a GradBuffer
 //
 // Flat layouts (shared with include/vpb.h):
 //   PrimitiveTransform = 24 floats: tBase[3] rBase[9] (column-major) sBase[3] deltaT[3]
@@ -27,6 +28,8 @@
 #include <vector>
 
 #include "volprim/errors.h"
+#include "volprim/grad.h"
+#include "volprim/params.h"
 #include "volprim/lbvh.h"
 #include "volprim/march.h"
 #include "volprim/primitive.h"
@@ -216,6 +219,38 @@ int vpref_march_rays(int32_t nPrim, int32_t m, const float *xf15, const float *p
             alpha[r] = mr.alpha;
             samples[r] = mr.samples;
         }
+    });
+}
+
+// backwardRay over explicit rays with given output adjoints; grads (K*4*M^3 + 9K floats,
+// the GradBuffer layout of params.h:12-27 with no vertices) are overwritten.
+int vpref_backward_rays(int32_t nPrim, int32_t m, const float *tr24, const float *payload,
+                        float wAlpha, int32_t wBeta, int64_t nRays, const float *origins,
+                        const float *dirs, const float *jitter01, const float *adjRgb,
+                        const float *adjAlpha, float stepSize, float earlyEps, float *grads) {
+    return guarded([&] {
+        Frame fr;
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        const std::vector<AffineXf> xfs = fr.composed();
+        std::vector<Aabb> boxes;
+        for (const auto &xf : xfs) boxes.push_back(primitiveAabb(xf));
+        const Lbvh bvh = buildLbvh(boxes);
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        const WindowParams w{wAlpha, wBeta};
+        GradBuffer gb(layoutOf(fr, 0));
+        for (int64_t r = 0; r < nRays; ++r) {
+            Ray ray;
+            ray.origin = v3(origins + 3 * r);
+            ray.direction = v3(dirs + 3 * r);
+            const RaySegmentList segs = intersect(bvh, xfs, ray);
+            backwardRay(ray, segs, fr, xfs, w, cfg, jitter01 ? jitter01[r] : real(0.5),
+                        v3(adjRgb + 3 * r), adjAlpha[r], gb);
+        }
+        std::memcpy(grads, gb.values.data(), gb.values.size() * sizeof(float));
     });
 }
 

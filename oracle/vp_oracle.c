@@ -278,9 +278,22 @@ typedef struct {
     uint64_t perm;
 } march_ctx;
 
+/* MarchResult replay bookkeeping (march.h:22-33) consumed by the backward pass. */
+typedef struct {
+    int64_t lastStep;
+    int saturated;
+    float satTPrev, satSigmaSum, satRgbWeighted[3];
+} march_rec;
+
 /* march.cpp:18-93 */
 static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSegs, int *active,
-                      float jitter01, float *rgb, float *alpha, int32_t *samples) {
+                      float jitter01, float *rgb, float *alpha, int32_t *samples, march_rec *rec) {
+    if (rec) {
+        rec->lastStep = -1;
+        rec->saturated = 0;
+        rec->satTPrev = rec->satSigmaSum = 0;
+        rec->satRgbWeighted[0] = rec->satRgbWeighted[1] = rec->satRgbWeighted[2] = 0;
+    }
     float color[3] = {0, 0, 0};
     float transmittance = 0;
     int nsamp = 0;
@@ -333,11 +346,18 @@ static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSe
                 rw[2] += r2 * sigma;
             }
             ++nsamp;
+            if (rec) rec->lastStep = i;
             const float dT = sigmaSum * dt;
             if (transmittance + dT >= 1) {
                 const float frac = (1 - transmittance) / dT;
                 const float f = dt * frac;
                 for (int ch = 0; ch < 3; ++ch) color[ch] += rw[ch] * f;
+                if (rec) {
+                    rec->satTPrev = transmittance;
+                    rec->satSigmaSum = sigmaSum;
+                    for (int ch = 0; ch < 3; ++ch) rec->satRgbWeighted[ch] = rw[ch];
+                    rec->saturated = 1;
+                }
                 transmittance = 1;
                 break;
             }
@@ -365,7 +385,7 @@ int vpo_march_rays(int32_t n_prim, int32_t m, const float *xf15, const float *pa
         const v3 o = ld3(origins + 3 * r), d = ld3(dirs + 3 * r);
         const int n = collect(n_prim, xf15, o, d, segs);
         march_one(&c, o, d, segs, n, active, jitter01 ? jitter01[r] : 0.5f, rgb + 3 * r,
-                  alpha + r, samples + r);
+                  alpha + r, samples + r, NULL);
     }
     free(segs);
     free(active);
@@ -395,7 +415,7 @@ static void *render_rows(void *arg) {
             const int n = collect(j->c->n_prim, j->c->xf15, ld3(o), ld3(d), segs);
             const float jit = j->jitter ? hash_to_unit(hash_combine(j->seed, (uint64_t)pixelId)) : 0.5f;
             march_one(j->c, ld3(o), ld3(d), segs, n, active, jit, j->rgb + 3 * (size_t)pixelId,
-                      j->alpha + pixelId, j->samples + pixelId);
+                      j->alpha + pixelId, j->samples + pixelId, NULL);
         }
     free(segs);
     free(active);
@@ -437,6 +457,319 @@ void vpo_composite(int32_t width, int32_t height, const float *rgb, const float 
         const float a = alpha[p];
         for (int ch = 0; ch < 3; ++ch) out[3 * p + ch] = a * rgb[3 * p + ch] + (1 - a) * bg[3 * p + ch];
     }
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Backward pass restatement: backwardRay (grad.cpp:34-195) over a batch of rays with given
+ * output adjoints. Gradients accumulate (+=) into the reference's GradBuffer layout
+ * (params.h:12-27): payload K*4*M^3 planar, then per primitive deltaT[3] deltaR[3] deltaS[3].
+ */
+static v3 cross3(v3 a, v3 b) {
+    return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+/* rotation.cpp:30-38 */
+static void rotation_derivative(v3 v, int i, float *out) {
+    const float t2 = dot3(v, v);
+    float e[3] = {0, 0, 0};
+    e[i] = 1;
+    float sk[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (t2 < 1e-14f) { /* skew(e) */
+        sk[3] = -e[2]; sk[6] = e[1]; sk[1] = e[2]; sk[7] = -e[0]; sk[2] = -e[1]; sk[5] = e[0];
+        memcpy(out, sk, sizeof sk);
+        return;
+    }
+    float r[9], imr[9], a[9], b[9], c[9];
+    static const float I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    rotation_from_axis_angle(v, r);
+    for (int q = 0; q < 9; ++q) imr[q] = I[q] - r[q];
+    const v3 w = cross3(v, matvec(imr, mk(e[0], e[1], e[2])));
+    const float vi = comp(v, i);
+    float skv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, skw[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    skv[3] = -v.z; skv[6] = v.y; skv[1] = v.z; skv[7] = -v.x; skv[2] = -v.y; skv[5] = v.x;
+    skw[3] = -w.z; skw[6] = w.y; skw[1] = w.z; skw[7] = -w.x; skw[2] = -w.y; skw[5] = w.x;
+    const float s = 1 / t2;
+    for (int q = 0; q < 9; ++q) a[q] = skv[q] * vi;
+    for (int q = 0; q < 9; ++q) b[q] = a[q] + skw[q];
+    for (int q = 0; q < 9; ++q) c[q] = b[q] * s;
+    matmul(c, r, out);
+}
+
+/* primitive.cpp:30-39 */
+static v3 window_gradient(v3 p, float alpha, int beta) {
+    if (alpha == 0) return mk(0, 0, 0);
+    const float wv = vpo_window(p.x, p.y, p.z, alpha, beta);
+    const float c = -alpha * (float)beta * wv;
+    return mk(c * (pow_even(p.x, beta - 2) * p.x), c * (pow_even(p.y, beta - 2) * p.y),
+              c * (pow_even(p.z, beta - 2) * p.z));
+}
+
+typedef struct { int lo[3]; float frac[3]; int clamped[3]; } stencil2_t;
+static stencil2_t trilinear_stencil2(int m, v3 p) { /* primitive.cpp:51-69 with clamped[] */
+    stencil2_t st;
+    for (int a = 0; a < 3; ++a) {
+        float u = (comp(p, a) + 1) * 0.5f * (float)m - 0.5f;
+        st.clamped[a] = 0;
+        if (u <= 0) { u = 0; st.clamped[a] = 1; }
+        else if (u >= (float)(m - 1)) { u = (float)(m - 1); st.clamped[a] = 1; }
+        int i0 = (int)floorf(u);
+        if (i0 > m - 2) i0 = (m - 2) > 0 ? (m - 2) : 0;
+        st.lo[a] = i0;
+        st.frac[a] = m > 1 ? u - (float)i0 : 0;
+    }
+    return st;
+}
+
+static size_t slab_index(int m, int k, int ch, int z, int y, int x) {
+    const size_t mm = (size_t)m;
+    return ((((size_t)k * 4 + ch) * mm + z) * mm + y) * mm + x;
+}
+
+/* primitive.cpp:101-127 */
+static v3 stencil_gradient(const float *payload, int m, int k, const stencil2_t *st, int ch) {
+    float g[3] = {0, 0, 0};
+    if (m == 1) return mk(0, 0, 0);
+    for (int cz = 0; cz < 2; ++cz)
+        for (int cy = 0; cy < 2; ++cy)
+            for (int cx = 0; cx < 2; ++cx) {
+                const int z = st->lo[2] + cz < m - 1 ? st->lo[2] + cz : m - 1;
+                const int y = st->lo[1] + cy < m - 1 ? st->lo[1] + cy : m - 1;
+                const int x = st->lo[0] + cx < m - 1 ? st->lo[0] + cx : m - 1;
+                const float v = payload[slab_index(m, k, ch, z, y, x)];
+                const float wx = cx ? st->frac[0] : 1 - st->frac[0];
+                const float wy = cy ? st->frac[1] : 1 - st->frac[1];
+                const float wz = cz ? st->frac[2] : 1 - st->frac[2];
+                const float dx = cx ? 1.0f : -1.0f, dy = cy ? 1.0f : -1.0f, dz = cz ? 1.0f : -1.0f;
+                g[0] += dx * wy * wz * v;
+                g[1] += wx * dy * wz * v;
+                g[2] += wx * wy * dz * v;
+            }
+    const float s = 0.5f * (float)m;
+    for (int a = 0; a < 3; ++a)
+        if (st->clamped[a]) g[a] = 0;
+    return mk(g[0] * s, g[1] * s, g[2] * s);
+}
+
+/* lbvh.cpp:177-205 with the entry face (entryAxis, entrySign, enterClamped) */
+static int intersect_obb_face(const float *xf, v3 o, v3 d, int *axis, int *sign, int *clamped) {
+    const v3 om = to_model(xf, o);
+    const v3 dm = cdiv3(matTvec(xf + 3, d), ld3(xf + 12));
+    float tEnter = -FLT_MAX, tExit = FLT_MAX;
+    *axis = -1;
+    *sign = 0;
+    for (int a = 0; a < 3; ++a) {
+        const float oa = comp(om, a), da = comp(dm, a);
+        if (da == 0) {
+            if (oa < -1 || oa > 1) return 0;
+            continue;
+        }
+        const float inv = 1 / da;
+        const float cNear = da > 0 ? -1.0f : 1.0f;
+        const float t1 = (cNear - oa) * inv;
+        const float t2 = (-cNear - oa) * inv;
+        if (t1 > tEnter) {
+            tEnter = t1;
+            *axis = a;
+            *sign = (int)cNear;
+        }
+        tExit = t2 < tExit ? t2 : tExit;
+    }
+    *clamped = tEnter < 0;
+    if (*clamped) tEnter = 0;
+    if (tEnter >= tExit || tExit <= 0) return 0;
+    return 1;
+}
+
+static void gadd3(float *g, v3 v) {
+    g[0] += v.x;
+    g[1] += v.y;
+    g[2] += v.z;
+}
+
+typedef struct {
+    int prim;
+    v3 pModel;
+    int cube[3];
+    stencil2_t st;
+    float sigmaRaw, win;
+    v3 rgb;
+} prim_sample_t;
+
+int vpo_backward_rays(int32_t n_prim, int32_t m, const float *tr24, const float *xf15,
+                      const float *payload, float w_alpha, int32_t w_beta, int64_t n_rays,
+                      const float *origins, const float *dirs, const float *jitter01,
+                      const float *adj_rgb, const float *adj_alpha, float step, float early_eps,
+                      float *grads) {
+    const march_ctx mc = {n_prim, m, xf15, payload, w_alpha, w_beta, step, early_eps, 0};
+    const size_t cap = (size_t)(n_prim > 0 ? n_prim : 1);
+    seg_t *segs = (seg_t *)malloc(sizeof(seg_t) * cap);
+    int *active = (int *)malloc(sizeof(int) * cap);
+    prim_sample_t *ps = (prim_sample_t *)malloc(sizeof(prim_sample_t) * cap);
+    float *rotd = (float *)malloc(sizeof(float) * 27 * cap);
+    int *rot_ready = (int *)calloc(cap, sizeof(int));
+    float *gdelta = grads + (size_t)n_prim * 4 * m * m * m;
+    for (int64_t r = 0; r < n_rays; ++r) {
+        const v3 o = ld3(origins + 3 * r), d = ld3(dirs + 3 * r);
+        const float jit = jitter01 ? jitter01[r] : 0.5f;
+        const v3 aRgb = ld3(adj_rgb + 3 * r);
+        const float aAlpha = adj_alpha[r];
+        const int nSegs = collect(n_prim, xf15, o, d, segs);
+        if (nSegs == 0) continue;
+        march_rec fwd;
+        float frgb[3], falpha;
+        int32_t fs;
+        march_one(&mc, o, d, segs, nSegs, active, jit, frgb, &falpha, &fs, &fwd);
+        if (fwd.lastStep < 0) continue;
+        /* rotDerivs cache is per backwardRay call (grad.cpp:46-54) */
+        memset(rot_ready, 0, sizeof(int) * cap);
+        const float dt = step;
+        const float t0 = segs[0].tEnter;
+        float tMax = 0;
+        for (int s = 0; s < nSegs; ++s) tMax = tMax < segs[s].tExit ? segs[s].tExit : tMax;
+        int nActive = 0, next = 0;
+        float gTmin = 0;
+        for (int64_t i = 0; i <= fwd.lastStep; ++i) {
+            const float ts = t0 + ((float)i + jit) * dt;
+            if (ts >= tMax) break;
+            while (next < nSegs && segs[next].tEnter <= ts) active[nActive++] = next++;
+            int w = 0;
+            for (int a = 0; a < nActive; ++a)
+                if (!(segs[active[a]].tExit <= ts)) active[w++] = active[a];
+            nActive = w;
+            if (nActive == 0) {
+                if (next >= nSegs) break;
+                const float tNext = segs[next].tEnter;
+                const int64_t skipTo = (int64_t)ceil((double)((tNext - t0) / dt) - (double)jit);
+                if (skipTo > i + 1) i = skipTo - 1;
+                continue;
+            }
+            const v3 pWorld = add3(o, scl3(d, ts));
+            float sigmaSum = 0;
+            v3 rgbW = mk(0, 0, 0);
+            for (int a = 0; a < nActive; ++a) {
+                prim_sample_t *p = &ps[a];
+                p->prim = segs[active[a]].prim;
+                const v3 raw = to_model(xf15 + 15 * (size_t)p->prim, pWorld);
+                for (int q = 0; q < 3; ++q) p->cube[q] = comp(raw, q) <= -1 || comp(raw, q) >= 1;
+                p->pModel = mk(clampc(raw.x), clampc(raw.y), clampc(raw.z));
+                p->st = trilinear_stencil2(m, p->pModel);
+                const stencil_t st1 = {{p->st.lo[0], p->st.lo[1], p->st.lo[2]},
+                                       {p->st.frac[0], p->st.frac[1], p->st.frac[2]}};
+                p->sigmaRaw = gather_channel(payload, m, p->prim, 3, &st1);
+                p->win = vpo_window(p->pModel.x, p->pModel.y, p->pModel.z, w_alpha, w_beta);
+                p->rgb = mk(gather_channel(payload, m, p->prim, 0, &st1),
+                            gather_channel(payload, m, p->prim, 1, &st1),
+                            gather_channel(payload, m, p->prim, 2, &st1));
+                sigmaSum += p->sigmaRaw * p->win;
+                rgbW = add3(rgbW, scl3(p->rgb, p->sigmaRaw * p->win));
+            }
+            (void)sigmaSum;
+            const int satStep = fwd.saturated && i == fwd.lastStep;
+            v3 gPWorldStep = mk(0, 0, 0);
+            for (int a = 0; a < nActive; ++a) {
+                const prim_sample_t *p = &ps[a];
+                const int k = p->prim;
+                const float sigmaW = p->sigmaRaw * p->win;
+                v3 gRgb;
+                float gSigmaW;
+                if (satStep) {
+                    const float budget = 1 - fwd.satTPrev;
+                    const float inv = 1 / fwd.satSigmaSum;
+                    gRgb = scl3(aRgb, sigmaW * budget * inv);
+                    gSigmaW = dot3(aRgb, sub3(scl3(p->rgb, fwd.satSigmaSum), rgbW)) * budget * inv * inv;
+                } else {
+                    gRgb = scl3(aRgb, sigmaW * dt);
+                    gSigmaW = dot3(aRgb, p->rgb) * dt;
+                    if (fwd.saturated)
+                        gSigmaW -= dot3(aRgb, ld3(fwd.satRgbWeighted)) / fwd.satSigmaSum * dt;
+                    else
+                        gSigmaW += aAlpha * dt;
+                }
+                for (int cz = 0; cz < 2; ++cz)
+                    for (int cy = 0; cy < 2; ++cy)
+                        for (int cx = 0; cx < 2; ++cx) {
+                            const float wx = cx ? p->st.frac[0] : 1 - p->st.frac[0];
+                            const float wy = cy ? p->st.frac[1] : 1 - p->st.frac[1];
+                            const float wz = cz ? p->st.frac[2] : 1 - p->st.frac[2];
+                            const float wgt = wx * wy * wz;
+                            if (wgt == 0) continue;
+                            const int z = p->st.lo[2] + cz < m - 1 ? p->st.lo[2] + cz : m - 1;
+                            const int y = p->st.lo[1] + cy < m - 1 ? p->st.lo[1] + cy : m - 1;
+                            const int x = p->st.lo[0] + cx < m - 1 ? p->st.lo[0] + cx : m - 1;
+                            for (int ch = 0; ch < 3; ++ch)
+                                grads[slab_index(m, k, ch, z, y, x)] += comp(gRgb, ch) * wgt;
+                            grads[slab_index(m, k, 3, z, y, x)] += gSigmaW * p->win * wgt;
+                        }
+                const v3 gradSigmaTri = stencil_gradient(payload, m, k, &p->st, 3);
+                const v3 gradW = window_gradient(p->pModel, w_alpha, w_beta);
+                v3 gP = scl3(add3(scl3(gradSigmaTri, p->win), scl3(gradW, p->sigmaRaw)), gSigmaW);
+                for (int ch = 0; ch < 3; ++ch)
+                    gP = add3(gP, scl3(stencil_gradient(payload, m, k, &p->st, ch), comp(gRgb, ch)));
+                if (p->cube[0]) gP.x = 0;
+                if (p->cube[1]) gP.y = 0;
+                if (p->cube[2]) gP.z = 0;
+                if (gP.x == 0 && gP.y == 0 && gP.z == 0) continue;
+                const float *xf = xf15 + 15 * (size_t)k;
+                const v3 gOverS = cdiv3(gP, ld3(xf + 12));
+                const v3 rotG = matvec(xf + 3, gOverS);
+                float *gk = gdelta + 9 * (size_t)k;
+                gadd3(gk + 0, mk(-rotG.x, -rotG.y, -rotG.z));
+                gadd3(gk + 6, mk(-gP.x * p->pModel.x / xf[12], -gP.y * p->pModel.y / xf[13],
+                                -gP.z * p->pModel.z / xf[14]));
+                const v3 u = sub3(pWorld, ld3(xf));
+                const v3 vv = matvec(tr24 + 24 * (size_t)k + 3, gOverS);
+                if (!rot_ready[k]) {
+                    for (int q = 0; q < 3; ++q)
+                        rotation_derivative(ld3(tr24 + 24 * (size_t)k + 18), q, rotd + 27 * (size_t)k + 9 * q);
+                    rot_ready[k] = 1;
+                }
+                const float *rd = rotd + 27 * (size_t)k;
+                gadd3(gk + 3, mk(dot3(matvec(rd, vv), u), dot3(matvec(rd + 9, vv), u),
+                                dot3(matvec(rd + 18, vv), u)));
+                gPWorldStep = add3(gPWorldStep, rotG);
+            }
+            gTmin += dot3(gPWorldStep, d);
+        }
+        if (gTmin != 0) { /* t_min anchor chain, grad.cpp:166-194 */
+            const int k0 = segs[0].prim;
+            const float *xf = xf15 + 15 * (size_t)k0;
+            int axis, sign, clamped;
+            if (intersect_obb_face(xf, o, d, &axis, &sign, &clamped) && !clamped) {
+                const int j = axis;
+                const float c = (float)sign;
+                const v3 q = mk(xf[3 + 3 * j], xf[4 + 3 * j], xf[5 + 3 * j]);
+                const float qd = dot3(q, d);
+                if (qd != 0) {
+                    const float tStar = t0;
+                    float *gk = gdelta + 9 * (size_t)k0;
+                    gadd3(gk + 0, scl3(q, gTmin / qd));
+                    float gS[3] = {0, 0, 0};
+                    gS[j] = gTmin * c / qd;
+                    gadd3(gk + 6, mk(gS[0], gS[1], gS[2]));
+                    const v3 toT = sub3(ld3(xf), o);
+                    const float *rb = tr24 + 24 * (size_t)k0 + 3;
+                    const v3 rj = mk(rb[3 * j], rb[3 * j + 1], rb[3 * j + 2]);
+                    if (!rot_ready[k0]) {
+                        for (int qq = 0; qq < 3; ++qq)
+                            rotation_derivative(ld3(tr24 + 24 * (size_t)k0 + 18), qq, rotd + 27 * (size_t)k0 + 9 * qq);
+                        rot_ready[k0] = 1;
+                    }
+                    float gR[3];
+                    for (int ii = 0; ii < 3; ++ii) {
+                        const v3 qp = matvec(rotd + 27 * (size_t)k0 + 9 * ii, rj);
+                        gR[ii] = gTmin * (dot3(qp, toT) - tStar * dot3(qp, d)) / qd;
+                    }
+                    gadd3(gk + 3, mk(gR[0], gR[1], gR[2]));
+                }
+            }
+        }
+    }
+    free(segs);
+    free(active);
+    free(ps);
+    free(rotd);
+    free(rot_ready);
+    return 0;
 }
 
 /* ---------------------------------------------------------------------------------------

@@ -61,6 +61,8 @@ SIGNATURES = {
     "vp_read_stats": (C.c_int, [C.c_void_p, C.POINTER(vp_stats)]),
     "vp_march_rays": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, f32p, C.POINTER(vp_march),
                                 f32p, f32p, i32p]),
+    "vp_backward_rays": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, f32p, f32p, f32p,
+                                   C.POINTER(vp_march), f32p, f32p, C.c_int32]),
     "vp_composite": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]),
     "vp_debug_tiles": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), i32p, u32p, i32p, i32p,
                                  C.c_int64, i64p]),

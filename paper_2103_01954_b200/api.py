@@ -313,6 +313,30 @@ class Renderer:
                self._ctx)
         return rgb, alpha, samples
 
+    def backward_rays(self, origins, dirs, adj_rgb, adj_alpha, cfg: MarchConfig, transforms,
+                      jitter01=None, grads: Optional[np.ndarray] = None) -> np.ndarray:
+        """backwardRay (grad.cpp:34-195) for each ray with the given output adjoints; returns
+        (or accumulates into `grads`) the GradBuffer values: K*4*M^3 planar payload entries,
+        then deltaT[3] deltaR[3] deltaS[3] per primitive (params.h:12-27)."""
+        o = _f32(origins).reshape(-1, 3)
+        d = _f32(dirs).reshape(-1, 3)
+        n = o.shape[0]
+        ar = _f32(adj_rgb).reshape(n, 3)
+        aa = _f32(adj_alpha).reshape(n)
+        j = None if jitter01 is None else _f32(jitter01).reshape(n)
+        tr = _f32(transforms).reshape(-1, 24)
+        k, m = int(self.n_prim or 0), int(self.m or 0)
+        size = k * 4 * m ** 3 + 9 * k
+        acc = grads is not None
+        out = grads if acc else np.zeros(size, np.float32)
+        if out.dtype != np.float32 or out.size != size or not out.flags.c_contiguous:
+            raise Error(ErrorCategory.USAGE, "gradient buffer must be contiguous float32 of the GradBuffer size")
+        mc = cfg.to_c()
+        _check(self._lib.vp_backward_rays(self._ctx, n, _fptr(o), _fptr(d), _fptr(j) if j is not None else None,
+                                          _fptr(ar), _fptr(aa), C.byref(mc), _fptr(tr), _fptr(out),
+                                          1 if acc else 0), self._ctx)
+        return out
+
     def debug_tiles(self, cam: Camera):
         """Cull rectangles, depth keys, tile offsets and per-tile sorted primitive lists."""
         k = self.n_prim or 0

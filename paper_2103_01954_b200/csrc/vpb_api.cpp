@@ -43,6 +43,7 @@ template <class T> struct DBuf {
         p = nullptr;
         n = 0;
     }
+    ~DBuf() { release(); }
 };
 
 bool is_device_ptr(const void *p) {
@@ -642,6 +643,80 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
         return VP_OK;
     }
     return fail(ctx, VP_ERR_DEVICE, "tile key buffer could not be sized");
+}
+
+int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
+                     const float *jitter01, const float *adj_rgb, const float *adj_alpha,
+                     const vp_march *cfg, const float *transforms24, float *grads,
+                     int32_t accumulate) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    if (n_rays < 0) return fail(ctx, VP_ERR_USAGE, "negative ray count");
+    const int k = ctx->n_prim, m = ctx->m;
+    const size_t n_pay = size_t(k) * 4 * m * m * m, n_grad = n_pay + 9 * size_t(k);
+    if (!grads) return fail(ctx, VP_ERR_USAGE, "null gradient buffer");
+    if (k > 0 && !transforms24) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    if (n_rays > 0 && (!origins || !dirs || !adj_rgb || !adj_alpha))
+        return fail(ctx, VP_ERR_USAGE, "null ray arrays");
+    cudaStream_t st = ctx->stream;
+    const bool d_grads = is_device_ptr(grads);
+    DBuf<float> g, pose, adj;
+    float *dg = grads;
+    if (!d_grads) {
+        VP_CUDA(ctx, g.ensure(n_grad));
+        dg = g.p;
+        if (accumulate) VP_CUDA(ctx, cudaMemcpyAsync(dg, grads, n_grad * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
+    if (k > 0 && n_rays > 0) {
+        // pose data on the host (exact reference code order): rBase, dR(deltaR)/dv_i
+        std::vector<float> p36(36 * size_t(k));
+        for (int i = 0; i < k; ++i) {
+            const float *tr = transforms24 + 24 * size_t(i);
+            std::memcpy(p36.data() + 36 * size_t(i), tr + 3, 9 * sizeof(float));
+            for (int q = 0; q < 3; ++q) {
+                const host::M3 r = host::rotation_derivative(host::load3(tr + 18), q);
+                std::memcpy(p36.data() + 36 * size_t(i) + 9 + 9 * q, r.m, 9 * sizeof(float));
+            }
+        }
+        VP_CUDA(ctx, pose.ensure(p36.size()));
+        VP_CUDA(ctx, cudaMemcpyAsync(pose.p, p36.data(), p36.size() * 4, cudaMemcpyHostToDevice, st));
+        const size_t n = size_t(n_rays);
+        RaysDev rays{origins, dirs, jitter01};
+        if (!is_device_ptr(origins)) {
+            VP_CUDA(ctx, ctx->ray_o.ensure(3 * n));
+            VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_o.p, origins, 12 * n, cudaMemcpyHostToDevice, st));
+            rays.origins = ctx->ray_o.p;
+        }
+        if (!is_device_ptr(dirs)) {
+            VP_CUDA(ctx, ctx->ray_d.ensure(3 * n));
+            VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_d.p, dirs, 12 * n, cudaMemcpyHostToDevice, st));
+            rays.dirs = ctx->ray_d.p;
+        }
+        if (jitter01 && !is_device_ptr(jitter01)) {
+            VP_CUDA(ctx, ctx->ray_j.ensure(n));
+            VP_CUDA(ctx, cudaMemcpyAsync(ctx->ray_j.p, jitter01, 4 * n, cudaMemcpyHostToDevice, st));
+            rays.jitter = ctx->ray_j.p;
+        }
+        const float *a_rgb = adj_rgb, *a_alpha = adj_alpha;
+        if (!is_device_ptr(adj_rgb) || !is_device_ptr(adj_alpha)) {
+            VP_CUDA(ctx, adj.ensure(4 * n));
+            VP_CUDA(ctx, cudaMemcpyAsync(adj.p, adj_rgb, 12 * n, cudaMemcpyDefault, st));
+            VP_CUDA(ctx, cudaMemcpyAsync(adj.p + 3 * n, adj_alpha, 4 * n, cudaMemcpyDefault, st));
+            a_rgb = adj.p;
+            a_alpha = adj.p + 3 * n;
+        }
+        if (int rc = ensure_fallback(ctx)) return rc;
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha};
+        VP_CUDA(ctx, launch_backward_rays(make_march(ctx, cfg), ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
+                                          bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+    }
+    if (!d_grads) VP_CUDA(ctx, cudaMemcpyAsync(grads, dg, n_grad * 4, cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    if (k > 0 && n_rays > 0) return check_counters(ctx, *ctx->h_ctr);
+    return VP_OK;
 }
 
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y) {

@@ -1,0 +1,448 @@
+// vpb_backward.cu — K6, the backward pass: backwardRay (grad.cpp:34-195) for a batch of rays.
+//
+// Per ray (one thread, grid-stride over the batch):
+//   1. the exact segment window (intersect over all primitives, lbvh.cpp:207-234);
+//   2. a bit-exact replay of march() recording the MarchResult bookkeeping the adjoints need
+//      (lastStep, saturated, satTPrev, satSigmaSum, satRgbWeighted; march.h:22-33);
+//   3. the adjoint walk over steps 0..lastStep (grad.cpp:66-164): per primitive-sample the
+//      colour/opacity adjoints, the payload scatter over 8 corners x 4 channels, the spatial
+//      gradient through the trilinear stencil and the fade window, and the pose Jacobians
+//      (deltaT, deltaS, deltaR via rotationDerivative);
+//   4. the t_min anchor chain onto the first-hit primitive (grad.cpp:166-194).
+// Every per-sample value is computed with the reference's operation order (same bits); the
+// global sums use device atomics (RED.ADD.F32), so only their summation order differs from
+// the reference's sequential loop. Pose gradients are first summed in registers over each
+// run of consecutive samples of the same primitive along the ray (a segment usually spans
+// tens of steps), cutting pose atomics by about an order of magnitude.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "vpb_device.cuh"
+#include "vpb_kernels.h"
+#include "vpb_march.cuh"
+
+namespace vpb {
+
+// Lattice walk shared by the replay and the adjoint pass (the stepping of march.cpp:27-58:
+// admission, retirement, gap skip, window refill). F::step_begin(i, ts, pw), F::prim(k, c),
+// F::step_end(i) -> bool stop. Returns 0, or 1 when the window overflowed, 2 on a runaway.
+template <int CAP, class Cands, class Win, class F>
+__device__ int walk_steps(const Cands &cands, const Win &w, int cnt, bool more, V3 o, V3 d,
+                          int2 px, float jit, float dt, long long i_end, F &f) {
+    if (cnt == 0) return 0;
+    const float t0 = w.E(0);
+    int nxt = 0, lo = 0;
+    for (long long i = 0; i <= i_end; ++i) {
+        if (i > (1ll << 40)) return 2;
+        const float ts = t0 + (__ll2float_rn(i) + jit) * dt;
+        for (;;) {
+            while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
+            if (nxt < cnt || !more) break;
+            const float lastE = w.E(cnt - 1);
+            const int lastP = cands.prim(w.C(cnt - 1));
+            int live = 0;
+            for (int q = 0; q < nxt; ++q) {
+                if (w.X(q) > ts) {
+                    if (live != q) {
+                        w.E(live) = w.E(q);
+                        w.X(live) = w.X(q);
+                        w.C(live) = w.C(q);
+                    }
+                    ++live;
+                }
+            }
+            if (live == CAP) return 1;
+            cnt = live;
+            nxt = live;
+            lo = 0;
+            more = false;
+            window_scan<CAP>(w, cands, cnt, more, o, d, px, false, lastE, lastP);
+        }
+        while (lo < nxt && w.X(lo) <= ts) ++lo;
+        bool any = false;
+        for (int j = lo; j < nxt; ++j)
+            if (w.X(j) > ts) {
+                any = true;
+                break;
+            }
+        if (!any) {
+            if (nxt >= cnt) break;
+            const float tNext = w.E(nxt);
+            const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
+            if (skipTo > i + 1) i = skipTo - 1;
+            continue;
+        }
+        f.step_begin(i, ts, o + d * ts);
+        for (int j = lo; j < nxt; ++j)
+            if (w.X(j) > ts) f.prim(cands.prim(w.C(j)), w.C(j));
+        if (f.step_end(i)) break;
+    }
+    return 0;
+}
+
+// Everything one primitive-sample exposes to the adjoints (PrimSample, grad.cpp:16-25).
+struct PrimEval {
+    V3 pm;
+    bool cube[3];
+    int lo[3];
+    float fr[3];
+    bool clamped[3];
+    float4 c[8];  // corners in (cz, cy, cx) order
+    float sigmaRaw, win;
+    V3 rgb;
+};
+
+__device__ __forceinline__ void eval_primitive(const float4 *__restrict__ pbase, int m,
+                                               const float *xf, V3 pw, float alpha, int beta,
+                                               const unsigned long long *tab, PrimEval &e) {
+    const V3 raw = to_model(xf, pw);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) e.cube[a] = comp(raw, a) <= -1.0f || comp(raw, a) >= 1.0f;
+    e.pm = mk3(clamp_unit(raw.x), clamp_unit(raw.y), clamp_unit(raw.z));
+    const float mf = (float)m;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float u = (comp(e.pm, a) + 1.0f) * 0.5f * mf - 0.5f;
+        e.clamped[a] = false;
+        if (u <= 0.0f) {
+            u = 0.0f;
+            e.clamped[a] = true;
+        } else if (u >= (float)(m - 1)) {
+            u = (float)(m - 1);
+            e.clamped[a] = true;
+        }
+        int i0 = (int)floorf(u);
+        if (i0 > m - 2) i0 = (m - 2) > 0 ? (m - 2) : 0;
+        e.lo[a] = i0;
+        e.fr[a] = m > 1 ? u - (float)i0 : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int z = min(e.lo[2] + (q >> 2), m - 1), y = min(e.lo[1] + ((q >> 1) & 1), m - 1),
+                  x = min(e.lo[0] + (q & 1), m - 1);
+        e.c[q] = __ldg(pbase + (z * m + y) * m + x);
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float wx = (q & 1) ? e.fr[0] : 1.0f - e.fr[0];
+        const float wy = ((q >> 1) & 1) ? e.fr[1] : 1.0f - e.fr[1];
+        const float wz = (q >> 2) ? e.fr[2] : 1.0f - e.fr[2];
+        const float wgt = wx * wy * wz;
+        acc[0] += wgt * e.c[q].x;
+        acc[1] += wgt * e.c[q].y;
+        acc[2] += wgt * e.c[q].z;
+        acc[3] += wgt * e.c[q].w;
+    }
+    e.rgb = mk3(acc[0], acc[1], acc[2]);
+    e.sigmaRaw = acc[3];
+    e.win = window_value(e.pm, alpha, beta, tab);
+}
+
+__device__ __forceinline__ float ch_of(float4 v, int ch) {
+    return ch == 0 ? v.x : (ch == 1 ? v.y : (ch == 2 ? v.z : v.w));
+}
+
+// stencilRgbGradient (primitive.cpp:101-127): d channel / d pModel, zero along clamped axes.
+__device__ __forceinline__ V3 stencil_gradient(const PrimEval &e, int m, int ch) {
+    if (m == 1) return mk3(0.f, 0.f, 0.f);
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
+        const float v = ch_of(e.c[q], ch);
+        const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
+        const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
+        const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
+        const float dx = cx ? 1.0f : -1.0f, dy = cy ? 1.0f : -1.0f, dz = cz ? 1.0f : -1.0f;
+        g0 += dx * wy * wz * v;
+        g1 += wx * dy * wz * v;
+        g2 += wx * wy * dz * v;
+    }
+    const float s = 0.5f * (float)m;
+    if (e.clamped[0]) g0 = 0.f;
+    if (e.clamped[1]) g1 = 0.f;
+    if (e.clamped[2]) g2 = 0.f;
+    return mk3(g0 * s, g1 * s, g2 * s);
+}
+
+// windowGradient (primitive.cpp:30-39)
+__device__ __forceinline__ V3 window_gradient(V3 p, float alpha, int beta, float wv) {
+    if (alpha == 0.0f) return mk3(0.f, 0.f, 0.f);
+    const float c = -alpha * (float)beta * wv;
+    return mk3(c * (pow_even(p.x, beta - 2) * p.x), c * (pow_even(p.y, beta - 2) * p.y),
+               c * (pow_even(p.z, beta - 2) * p.z));
+}
+
+// Step 2: bit-exact replay of march() keeping the backward bookkeeping.
+template <class Cands>
+struct FwdReplay {
+    const Cands &cands;
+    const MarchDev &mp;
+    const unsigned long long *tab;
+    float transmittance = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+    V3 pw;
+    long long lastStep = -1;
+    bool saturated = false;
+    float satTPrev = 0.f, satSigmaSum = 0.f, satR = 0.f, satG = 0.f, satB = 0.f;
+    __device__ FwdReplay(const Cands &c, const MarchDev &m, const unsigned long long *t)
+        : cands(c), mp(m), tab(t) {}
+    __device__ void step_begin(long long, float, V3 p) {
+        pw = p;
+        sigmaSum = rw = gw = bw = 0.f;
+    }
+    __device__ void prim(int k, int c) {
+        float sg, r, g, b;
+        sample_primitive<0>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r, g, b);
+        sigmaSum += sg;
+        rw += r * sg;
+        gw += g * sg;
+        bw += b * sg;
+    }
+    __device__ bool step_end(long long i) {
+        lastStep = i;
+        const float dT = sigmaSum * mp.dt;
+        if (transmittance + dT >= 1.0f) {
+            satTPrev = transmittance;
+            satSigmaSum = sigmaSum;
+            satR = rw;
+            satG = gw;
+            satB = bw;
+            transmittance = 1.0f;
+            saturated = true;
+            return true;
+        }
+        transmittance += dT;
+        return transmittance > 1.0f - mp.eps;
+    }
+};
+
+__device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }
+
+// Step 3: the adjoint walk.
+template <class Cands>
+struct BwdWalk {
+    const Cands &cands;
+    const MarchDev &mp;
+    const unsigned long long *tab;
+    const FwdReplay<Cands> &fwd;
+    const BwdDev &bd;
+    V3 d, aRgb;
+    float aAlpha;
+    float ts = 0.f;
+    V3 pw, gPWorldStep;
+    float gTmin = 0.f;
+    bool satStep = false;
+    int cur = -1;      // primitive whose pose gradients are being summed in registers
+    float acc[9];      // deltaT[3] deltaR[3] deltaS[3]
+    __device__ BwdWalk(const Cands &c, const MarchDev &m, const unsigned long long *t,
+                       const FwdReplay<Cands> &f, const BwdDev &b, V3 dir, V3 ar, float aa)
+        : cands(c), mp(m), tab(t), fwd(f), bd(b), d(dir), aRgb(ar), aAlpha(aa) {
+        for (float &v : acc) v = 0.f;
+    }
+    __device__ void flush() {
+        if (cur < 0) return;
+        float *g = bd.g_pose + 9 * (size_t)cur;
+        for (int q = 0; q < 9; ++q)
+            if (acc[q] != 0.f) red_add(g + q, acc[q]);
+        for (float &v : acc) v = 0.f;
+    }
+    __device__ void pose_add(int k, int off, V3 v) {
+        if (k != cur) {
+            flush();
+            cur = k;
+        }
+        acc[off] += v.x;
+        acc[off + 1] += v.y;
+        acc[off + 2] += v.z;
+    }
+    __device__ void step_begin(long long i, float t, V3 p) {
+        ts = t;
+        pw = p;
+        gPWorldStep = mk3(0.f, 0.f, 0.f);
+        satStep = fwd.saturated && i == fwd.lastStep;
+    }
+    __device__ void prim(int k, int c) {
+        const int m = mp.m;
+        const float *xf = cands.xf(c);
+        PrimEval e;
+        eval_primitive(cands.base(c), m, xf, pw, mp.alpha, mp.beta, tab, e);
+        const float dt = mp.dt;
+        const float sigmaW = e.sigmaRaw * e.win;
+        V3 gRgb;
+        float gSigmaW;
+        if (satStep) {  // grad.cpp:104-108 (rgbWeighted of this step == satRgbWeighted)
+            const float budget = 1.0f - fwd.satTPrev;
+            const float inv = 1.0f / fwd.satSigmaSum;
+            gRgb = aRgb * (sigmaW * budget * inv);
+            const V3 diff = e.rgb * fwd.satSigmaSum - mk3(fwd.satR, fwd.satG, fwd.satB);
+            gSigmaW = dot3(aRgb, diff) * budget * inv * inv;
+        } else {  // grad.cpp:109-118
+            gRgb = aRgb * (sigmaW * dt);
+            gSigmaW = dot3(aRgb, e.rgb) * dt;
+            if (fwd.saturated)
+                gSigmaW -= dot3(aRgb, mk3(fwd.satR, fwd.satG, fwd.satB)) / fwd.satSigmaSum * dt;
+            else
+                gSigmaW += aAlpha * dt;
+        }
+        // payload scatter (grad.cpp:121-134), planar GradBuffer indices
+        const size_t m3 = (size_t)m * m * m;
+        float *gk = bd.g_pay + (size_t)k * 4 * m3;
+        const float gsw = gSigmaW * e.win;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float wx = (q & 1) ? e.fr[0] : 1.0f - e.fr[0];
+            const float wy = ((q >> 1) & 1) ? e.fr[1] : 1.0f - e.fr[1];
+            const float wz = (q >> 2) ? e.fr[2] : 1.0f - e.fr[2];
+            const float wgt = wx * wy * wz;
+            if (wgt == 0.0f) continue;
+            const int z = min(e.lo[2] + (q >> 2), m - 1), y = min(e.lo[1] + ((q >> 1) & 1), m - 1),
+                      x = min(e.lo[0] + (q & 1), m - 1);
+            const size_t v = ((size_t)z * m + y) * m + x;
+            red_add(gk + v, gRgb.x * wgt);
+            red_add(gk + m3 + v, gRgb.y * wgt);
+            red_add(gk + 2 * m3 + v, gRgb.z * wgt);
+            red_add(gk + 3 * m3 + v, gsw * wgt);
+        }
+        // spatial gradient (grad.cpp:136-145)
+        const V3 gradSigmaTri = stencil_gradient(e, m, 3);
+        const V3 gradW = window_gradient(e.pm, mp.alpha, mp.beta, e.win);
+        V3 gP = (gradSigmaTri * e.win + gradW * e.sigmaRaw) * gSigmaW;
+        gP = gP + stencil_gradient(e, m, 0) * gRgb.x;
+        gP = gP + stencil_gradient(e, m, 1) * gRgb.y;
+        gP = gP + stencil_gradient(e, m, 2) * gRgb.z;
+        if (e.cube[0]) gP.x = 0.f;
+        if (e.cube[1]) gP.y = 0.f;
+        if (e.cube[2]) gP.z = 0.f;
+        if (gP.x == 0.f && gP.y == 0.f && gP.z == 0.f) return;
+        // pose Jacobians (grad.cpp:147-161)
+        const V3 gOverS = mk3(gP.x / xf[12], gP.y / xf[13], gP.z / xf[14]);
+        const V3 rotG = matvec(xf + 3, gOverS);
+        pose_add(k, 0, mk3(-rotG.x, -rotG.y, -rotG.z));
+        pose_add(k, 6, mk3(-gP.x * e.pm.x / xf[12], -gP.y * e.pm.y / xf[13], -gP.z * e.pm.z / xf[14]));
+        const V3 u = pw - mk3(xf[0], xf[1], xf[2]);
+        const float *pose = bd.pose36 + 36 * (size_t)k;  // rBase[9], dR/dv_i [3][9]
+        const V3 v = matvec(pose, gOverS);
+        pose_add(k, 3, mk3(dot3(matvec(pose + 9, v), u), dot3(matvec(pose + 18, v), u),
+                           dot3(matvec(pose + 27, v), u)));
+        gPWorldStep = gPWorldStep + rotG;
+    }
+    __device__ bool step_end(long long) {
+        gTmin += dot3(gPWorldStep, d);
+        return false;
+    }
+};
+
+// lbvh.cpp:177-205 keeping the entry face
+__device__ __forceinline__ bool intersect_face(const float *xf, V3 o, V3 d, int &axis, int &sign,
+                                               bool &clamped) {
+    const V3 om = to_model(xf, o);
+    const V3 q = matTvec(xf + 3, d);
+    const V3 dm = V3{q.x / xf[12], q.y / xf[13], q.z / xf[14]};
+    float tEnter = -3.402823466e+38f, tExit = 3.402823466e+38f;
+    axis = -1;
+    sign = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float oa = comp(om, a), da = comp(dm, a);
+        if (da == 0.0f) {
+            if (oa < -1.0f || oa > 1.0f) return false;
+            continue;
+        }
+        const float inv = 1.0f / da;
+        const float cNear = da > 0.0f ? -1.0f : 1.0f;
+        const float t1 = (cNear - oa) * inv;
+        const float t2 = (-cNear - oa) * inv;
+        if (t1 > tEnter) {
+            tEnter = t1;
+            axis = a;
+            sign = (int)cNear;
+        }
+        tExit = t2 < tExit ? t2 : tExit;
+    }
+    clamped = tEnter < 0.0f;
+    if (clamped) tEnter = 0.0f;
+    return !(tEnter >= tExit || tExit <= 0.0f);
+}
+
+__global__ void __launch_bounds__(kFallbackThreads)
+k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+                const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, BwdDev bd,
+                DevCounters *ctr, float *se, float *sx, int *sc) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const Window<int> w{se, sx, sc, nthreads, gtid};
+    const AllCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim};
+    for (int64_t r = gtid; r < n_rays; r += nthreads) {
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        const int2 px = make_int2(0, 0);
+        int cnt = 0;
+        bool more = false;
+        window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+        if (cnt == 0) continue;
+        const int k0 = cands.prim(w.C(0));
+        const float tMin = w.E(0);
+        FwdReplay<AllCands> fwd(cands, mp, s_tab);
+        int st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
+        if (st == 0 && fwd.lastStep >= 0) {
+            const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
+            BwdWalk<AllCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
+            cnt = 0;
+            more = false;
+            window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+            st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
+            if (st == 0 && bw.gTmin != 0.f) {  // t_min anchor chain (grad.cpp:166-194)
+                const float *xf = cands.xf(k0);
+                int axis, sign;
+                bool clamped;
+                if (intersect_face(xf, o, d, axis, sign, clamped) && !clamped) {
+                    const int j = axis;
+                    const float c = (float)sign;
+                    const V3 q = mk3(xf[3 + 3 * j], xf[4 + 3 * j], xf[5 + 3 * j]);
+                    const float qd = dot3(q, d);
+                    if (qd != 0.0f) {
+                        const float gT = bw.gTmin;
+                        bw.pose_add(k0, 0, q * (gT / qd));
+                        V3 gS = mk3(0.f, 0.f, 0.f);
+                        const float gsj = gT * c / qd;
+                        if (j == 0) gS.x = gsj;
+                        else if (j == 1) gS.y = gsj;
+                        else gS.z = gsj;
+                        bw.pose_add(k0, 6, gS);
+                        const V3 toT = mk3(xf[0], xf[1], xf[2]) - o;
+                        const float *pose = bd.pose36 + 36 * (size_t)k0;
+                        const V3 rj = mk3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2]);
+                        float gR[3];
+#pragma unroll
+                        for (int ii = 0; ii < 3; ++ii) {
+                            const V3 qp = matvec(pose + 9 + 9 * ii, rj);
+                            gR[ii] = gT * (dot3(qp, toT) - tMin * dot3(qp, d)) / qd;
+                        }
+                        bw.pose_add(k0, 3, mk3(gR[0], gR[1], gR[2]));
+                    }
+                }
+            }
+            bw.flush();
+        }
+        if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
+        if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
+    }
+}
+
+cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
+                                 const float4 *payload, const RaysDev &rays, int64_t n_rays,
+                                 const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
+                                 cudaStream_t st) {
+    if (n_rays == 0 || n_prim == 0) return cudaSuccess;
+    k_backward_rays<<<kFallbackBlocks, kFallbackThreads, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays,
+                                                                  bd, ctr, se, sx, sc);
+    return cudaGetLastError();
+}
+
+}  // namespace vpb

@@ -127,6 +127,31 @@ inline F3 axis_angle_from_matrix(const M3 &r) {
     return mul(axis, theta / s);
 }
 
+inline M3 skew(F3 v) {  // math.h:94-100
+    M3 r = zero3();
+    r(0, 1) = -v.z; r(0, 2) = v.y;
+    r(1, 0) = v.z;  r(1, 2) = -v.x;
+    r(2, 0) = -v.y; r(2, 1) = v.x;
+    return r;
+}
+
+// rotation.cpp:30-38 — d R(v) / d v_i
+inline M3 rotation_derivative(F3 v, int i) {
+    const float t2 = dot(v, v);
+    F3 e;
+    (i == 0 ? e.x : (i == 1 ? e.y : e.z)) = 1;
+    if (t2 < 1e-14f) return skew(e);
+    const M3 r = rotation_from_axis_angle(v);
+    M3 imr;
+    for (int q = 0; q < 9; ++q) imr.m[q] = M3{}.m[q] - r.m[q];
+    const F3 w = cross(v, mv(imr, e));
+    const M3 sv = skew(v), sw = skew(w);
+    const float vi = at(v, i), s = 1 / t2;
+    M3 c;
+    for (int q = 0; q < 9; ++q) c.m[q] = (sv.m[q] * vi + sw.m[q]) * s;
+    return mm(c, r);
+}
+
 inline F3 load3(const float *p) { return f3(p[0], p[1], p[2]); }
 inline M3 load9(const float *p) { M3 r; for (int i = 0; i < 9; ++i) r.m[i] = p[i]; return r; }
 

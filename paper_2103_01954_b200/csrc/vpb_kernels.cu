@@ -24,12 +24,10 @@
 
 #include "vpb_device.cuh"
 #include "vpb_kernels.h"
+#include "vpb_march.cuh"
 
 namespace vpb {
 
-constexpr int kTile = 16;
-constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
-constexpr int kCandCap = 64;        // candidates staged in shared memory per tile
 
 // ----------------------------------------------------------------------------------------
 // K0: planar -> interleaved. One thread per voxel; the four planar reads are coalesced
@@ -253,467 +251,6 @@ __global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
     }
     if (in_smem)
         for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = s[i];
-}
-
-// ----------------------------------------------------------------------------------------
-// Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
-//
-// TileCands<true>: every candidate of the tile is staged in shared memory (n <= kCandCap):
-// transform, toModel(camera centre) (every ray of a render starts there, so om is computed
-// once per candidate instead of once per ray, same operations, same bits), pixel rectangle
-// and payload base. TileCands<false>: the generic path reading the tile bucket from global
-// memory (tiles with more candidates, fallback re-march).
-template <bool STAGED>
-struct TileCands {
-    const unsigned long long *entries;
-    const float *xf_g;
-    const int4 *prects_g;
-    const float4 *payload;
-    unsigned m3;
-    uint32_t start;
-    int n;
-    const int *s_prim;
-    const float *s_xf;
-    const float4 *s_om;
-    const int4 *s_prect;
-    __device__ __forceinline__ int prim(int c) const {
-        if (STAGED) return s_prim[c];
-        return (int)(uint32_t)(entries[start + c] & 0xffffffffull);
-    }
-    __device__ __forceinline__ const float *xf(int c) const {
-        return STAGED ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
-    }
-    __device__ __forceinline__ const float4 *base(int c) const {
-        return payload + (size_t)prim(c) * m3;
-    }
-    // the candidate's conservative pixel rectangle (k_cull) contains the pixel
-    __device__ __forceinline__ bool covers(int c, int2 px) const {
-        const int4 r = STAGED ? s_prect[c] : prects_g[prim(c)];
-        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
-    }
-    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
-        if (STAGED) {
-            const float4 om = s_om[c];
-            return intersect_obb_om(xf(c), mk3(om.x, om.y, om.z), d, tE, tX);
-        }
-        return intersect_obb(xf(c), o, d, tE, tX);
-    }
-};
-struct AllCands {  // every primitive (march over arbitrary rays)
-    const float *xf_g;
-    const float4 *payload;
-    unsigned m3;
-    int n;
-    __device__ __forceinline__ int prim(int c) const { return c; }
-    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
-    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
-    __device__ __forceinline__ bool covers(int, int2) const { return true; }
-    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
-        return intersect_obb(xf(c), o, d, tE, tX);
-    }
-};
-
-// Per-ray sorted segment window: slot j of ray `lane` lives at [j * stride + lane]
-// (conflict-free across a warp). IdxT holds the candidate index (uint8_t for staged tiles).
-template <class IdxT>
-struct Window {
-    float *e;
-    float *x;
-    IdxT *c;
-    int stride, lane;
-    __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
-    __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
-    __device__ __forceinline__ IdxT &C(int j) const { return c[j * stride + lane]; }
-};
-
-struct RayOut {
-    float r, g, b, alpha;
-    int samples;
-    int prim_samples;
-    int hit, early, saturated, overflow, refills, numeric;
-};
-
-__device__ __forceinline__ bool key_less(float ea, int pa, float eb, int pb) {
-    return ea != eb ? ea < eb : pa < pb;
-}
-
-// Inserts (tE, tX, c) into the sorted window [0, cnt) of capacity CAP, keeping the CAP
-// smallest (tEnter, prim) keys; `more` records that a hit fell outside the window.
-template <int CAP, class Cands, class Win>
-__device__ __forceinline__ void window_insert(const Win &w, const Cands &cands, int &cnt,
-                                              bool &more, float tE, float tX, int c, int prim) {
-    if (cnt == CAP) {
-        more = true;
-        if (!key_less(tE, prim, w.E(CAP - 1), cands.prim(w.C(CAP - 1)))) return;
-        cnt = CAP - 1;
-    }
-    int j = cnt;
-    while (j > 0) {
-        const float e = w.E(j - 1);
-        if (e < tE || (e == tE && cands.prim(w.C(j - 1)) < prim)) break;
-        w.E(j) = e;
-        w.X(j) = w.X(j - 1);
-        w.C(j) = w.C(j - 1);
-        --j;
-    }
-    w.E(j) = tE;
-    w.X(j) = tX;
-    w.C(j) = c;
-    ++cnt;
-}
-
-// Fills the window with the smallest hits whose key exceeds (lastE, lastP) (or all hits
-// when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order).
-template <int CAP, class Cands, class Win>
-__device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, int &cnt,
-                                            bool &more, V3 o, V3 d, int2 px, bool first,
-                                            float lastE, int lastP) {
-    for (int c = 0; c < cands.n; ++c) {
-        float tE, tX;
-        if (!cands.covers(c, px) || !cands.hit(c, o, d, tE, tX)) continue;
-        const int prim = cands.prim(c);
-        if (!first && !key_less(lastE, lastP, tE, prim)) continue;
-        window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
-    }
-}
-
-// The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
-// segment list (filled by window_scan). Entries [0, nxt) have been admitted; `act` is the
-// bitmask of admitted entries still live (tExit > ts). Iterating its set bits in ascending
-// order visits the reference's `active` list in its order (admission order = window order).
-// The reference's `ts >= tMax` break is implied: it only fires once every segment is
-// admitted and retired, where the empty-active-set branch breaks on the same step.
-//
-// Events are tracked in registers: nextE = tEnter of the next pending entry, minX = the
-// earliest exit among live entries. A step touches the window (shared memory) only when
-// ts reaches one of them, so most steps cost a compare.
-//
-// The loop is flattened to one primitive-sample per iteration: a lane first finds its next
-// lattice step with a non-empty active set, then evaluates one active primitive; the step's
-// accumulation happens after its last active primitive. Lanes whose steps have different
-// numbers of active primitives stay in lock-step on primitive-samples.
-template <int CAP, int MT, class Cands, class Win>
-__device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
-                               V3 d, int2 px, float jit, const MarchDev &mp,
-                               const unsigned long long *tab) {
-    static_assert(CAP <= 32, "the active set is a 32-bit mask");
-    const float kInf = __int_as_float(0x7f800000);
-    RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (cnt == 0) return out;
-    out.hit = 1;
-    const float dt = mp.dt;
-    const float t0 = w.E(0);
-    int nxt = 0, j = 0;
-    unsigned act = 0;
-    float nextE = t0, minX = kInf;
-    long long i = 0;
-    float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
-    V3 pw = o;
-    bool sampling = false;
-    for (;;) {
-        if (!sampling) {
-            for (;;) {  // next lattice step with a non-empty active set
-                if (i > (1ll << 40)) {  // the reference would spin; report instead of hanging
-                    out.numeric = 1;
-                    goto done;
-                }
-                ts = t0 + (__ll2float_rn(i) + jit) * dt;
-                if (ts >= minX) {  // retirement (march.cpp:39-41)
-                    minX = kInf;
-                    for (unsigned m = act; m; m &= m - 1) {
-                        const int q = __ffs(m) - 1;
-                        const float x = w.X(q);
-                        if (x <= ts) act &= ~(1u << q);
-                        else minX = fminf(minX, x);
-                    }
-                }
-                if (nxt < cnt ? nextE <= ts : more) {  // admission (march.cpp:38), with refill
-                    for (;;) {
-                        while (nxt < cnt && nextE <= ts) {
-                            const float x = w.X(nxt);
-                            if (x > ts) {  // admitted and not retired in the same step
-                                act |= 1u << nxt;
-                                minX = fminf(minX, x);
-                            }
-                            ++nxt;
-                            nextE = nxt < cnt ? w.E(nxt) : kInf;
-                        }
-                        if (nxt < cnt || !more) break;
-                        // window exhausted while hits remain: keep the live entries (in
-                        // order), then fetch the next hits after the last key
-                        const float lastE = w.E(cnt - 1);
-                        const int lastP = cands.prim(w.C(cnt - 1));
-                        int live = 0;
-                        for (unsigned m = act; m; m &= m - 1, ++live) {
-                            const int q = __ffs(m) - 1;
-                            if (live != q) {
-                                w.E(live) = w.E(q);
-                                w.X(live) = w.X(q);
-                                w.C(live) = w.C(q);
-                            }
-                        }
-                        if (live == CAP) {
-                            out.overflow = 1;
-                            return out;
-                        }
-                        act = (1u << live) - 1u;
-                        cnt = live;
-                        nxt = live;
-                        more = false;
-                        ++out.refills;
-                        window_scan<CAP>(w, cands, cnt, more, o, d, px, false, lastE, lastP);
-                        nextE = nxt < cnt ? w.E(nxt) : kInf;
-                    }
-                }
-                if (act) {
-                    j = __ffs(act) - 1;
-                    break;
-                }
-                if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:43-44
-                // gap skip to the next entry (march.cpp:45-49)
-                const long long skipTo = (long long)ceil((double)((nextE - t0) / dt) - (double)jit);
-                i = skipTo > i + 1 ? skipTo : i + 1;
-            }
-            sampling = true;
-            sigmaSum = 0.f;
-            rw = gw = bw = 0.f;
-            pw = o + d * ts;
-        }
-        {  // one primitive-sample (march.cpp:63-70)
-            const int c = w.C(j);
-            float sg, r, g, b;
-            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
-                                 g, b);
-            sigmaSum += sg;
-            rw += r * sg;
-            gw += g * sg;
-            bw += b * sg;
-            ++out.prim_samples;
-        }
-        const unsigned rest = act & ~((2u << j) - 1u);
-        if (rest) {
-            j = __ffs(rest) - 1;
-            continue;
-        }
-        // step complete: march.cpp:71-88
-        sampling = false;
-        ++out.samples;
-        const float dT = sigmaSum * dt;
-        if (transmittance + dT >= 1.0f) {
-            const float frac = (1.0f - transmittance) / dT;
-            const float f = dt * frac;
-            cr += rw * f;
-            cg += gw * f;
-            cb += bw * f;
-            transmittance = 1.0f;
-            out.saturated = 1;
-            break;
-        }
-        cr += rw * dt;
-        cg += gw * dt;
-        cb += bw * dt;
-        transmittance += dT;
-        if (transmittance > 1.0f - mp.eps) {
-            out.early = 1;
-            break;
-        }
-        ++i;
-    }
-done:
-    out.r = cr;
-    out.g = cg;
-    out.b = cb;
-    out.alpha = transmittance;
-    return out;
-}
-
-// Generic variant for windows wider than 32 entries (the fallback re-march): the same
-// quadrature, with the live entries found by scanning the window instead of a bitmask.
-// The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted
-// segment list (filled by window_scan). Entries [0, nxt) are admitted; an admitted entry is
-// live while tExit > ts, and the live ones in window order are exactly the reference's
-// `active` list. The reference's `ts >= tMax` break is implied: it only fires once every
-// segment is admitted and retired, where the empty-active-set branch breaks on the same step.
-//
-// The loop is flattened to one primitive-sample per iteration: a lane first finds its next
-// lattice step with a non-empty active set, then evaluates one active primitive; the step's
-// accumulation happens after its last active primitive. Lanes whose steps have different
-// numbers of active primitives stay in lock-step on primitive-samples. Between events the
-// active set does not change: t_evt = min(next entry, earliest exit of a live entry), and
-// while ts < t_evt a step reuses the previous active set without touching the window.
-template <int CAP, int MT, class Cands, class Win>
-__device__ RayOut march_window_generic(const Cands &cands, const Win &w, int cnt, bool more, V3 o,
-                               V3 d, int2 px, float jit, const MarchDev &mp,
-                               const unsigned long long *tab) {
-    RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (cnt == 0) return out;
-    out.hit = 1;
-    const float dt = mp.dt;
-    const float t0 = w.E(0);
-    int nxt = 0, lo = 0, j = 0, jfirst = 0;
-    long long i = 0;
-    float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
-    float t_evt = -3.402823466e+38f;
-    V3 pw = o;
-    bool sampling = false;
-    for (;;) {
-        if (!sampling) {
-            for (;;) {  // next lattice step with a non-empty active set
-                if (i > (1ll << 40)) {  // the reference would spin; report instead of hanging
-                    out.numeric = 1;
-                    goto done;
-                }
-                ts = t0 + (__ll2float_rn(i) + jit) * dt;
-                if (ts < t_evt) {  // no admission, no retirement since the last step
-                    j = jfirst;
-                    break;
-                }
-                for (;;) {  // admission, refilling the window when it runs dry
-                    while (nxt < cnt && w.E(nxt) <= ts) ++nxt;
-                    if (nxt < cnt || !more) break;
-                    const float lastE = w.E(cnt - 1);
-                    const int lastP = cands.prim(w.C(cnt - 1));
-                    int live = 0;
-                    for (int q = 0; q < nxt; ++q) {
-                        if (w.X(q) > ts) {
-                            if (live != q) {
-                                w.E(live) = w.E(q);
-                                w.X(live) = w.X(q);
-                                w.C(live) = w.C(q);
-                            }
-                            ++live;
-                        }
-                    }
-                    if (live == CAP) {
-                        out.overflow = 1;
-                        return out;
-                    }
-                    cnt = live;
-                    nxt = live;
-                    lo = 0;
-                    more = false;
-                    ++out.refills;
-                    window_scan<CAP>(w, cands, cnt, more, o, d, px, false, lastE, lastP);
-                }
-                while (lo < nxt && w.X(lo) <= ts) ++lo;
-                j = lo;
-                while (j < nxt && !(w.X(j) > ts)) ++j;
-                if (j < nxt) {
-                    jfirst = j;
-                    t_evt = nxt < cnt ? w.E(nxt) : 3.402823466e+38f;
-                    for (int q = j; q < nxt; ++q) {
-                        const float x = w.X(q);
-                        if (x > ts && x < t_evt) t_evt = x;
-                    }
-                    break;
-                }
-                if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:44
-                const float tNext = w.E(nxt);  // gap skip, march.cpp:45-49
-                const long long skipTo = (long long)ceil((double)((tNext - t0) / dt) - (double)jit);
-                i = skipTo > i + 1 ? skipTo : i + 1;
-            }
-            sampling = true;
-            sigmaSum = 0.f;
-            rw = gw = bw = 0.f;
-            pw = o + d * ts;
-        }
-        {  // one primitive-sample (march.cpp:63-70)
-            const int c = w.C(j);
-            float sg, r, g, b;
-            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
-                                 g, b);
-            sigmaSum += sg;
-            rw += r * sg;
-            gw += g * sg;
-            bw += b * sg;
-            ++out.prim_samples;
-        }
-        ++j;
-        while (j < nxt && !(w.X(j) > ts)) ++j;
-        if (j < nxt) continue;
-        // step complete: march.cpp:71-88
-        sampling = false;
-        ++out.samples;
-        const float dT = sigmaSum * dt;
-        if (transmittance + dT >= 1.0f) {
-            const float frac = (1.0f - transmittance) / dT;
-            const float f = dt * frac;
-            cr += rw * f;
-            cg += gw * f;
-            cb += bw * f;
-            transmittance = 1.0f;
-            out.saturated = 1;
-            break;
-        }
-        cr += rw * dt;
-        cg += gw * dt;
-        cb += bw * dt;
-        transmittance += dT;
-        if (transmittance > 1.0f - mp.eps) {
-            out.early = 1;
-            break;
-        }
-        ++i;
-    }
-done:
-    out.r = cr;
-    out.g = cg;
-    out.b = cb;
-    out.alpha = transmittance;
-    return out;
-}
-
-template <int CAP, class Cands, class Win>
-__device__ __forceinline__ RayOut march_ray(const Cands &cands, const Win &w, V3 o, V3 d,
-                                            int2 px, float jit, const MarchDev &mp,
-                                            const unsigned long long *tab) {
-    int cnt = 0;
-    bool more = false;
-    window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
-    if constexpr (CAP <= 32)
-        return march_window<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
-    else
-        return march_window_generic<CAP, 0>(cands, w, cnt, more, o, d, px, jit, mp, tab);
-}
-
-__device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
-    od.rgb[3 * p + 0] = ro.r;
-    od.rgb[3 * p + 1] = ro.g;
-    od.rgb[3 * p + 2] = ro.b;
-    od.alpha[p] = ro.alpha;
-    if (od.samples) od.samples[p] = ro.samples;
-}
-
-// Warp-aggregated counter update: one atomic per warp per counter.
-__device__ __forceinline__ void add_counters(DevCounters *ctr, const RayOut &ro, bool valid) {
-    unsigned long long v[7] = {(unsigned long long)(valid ? ro.samples : 0),
-                               (unsigned long long)(valid ? ro.prim_samples : 0),
-                               (unsigned long long)(valid ? ro.hit : 0),
-                               (unsigned long long)(valid ? ro.early : 0),
-                               (unsigned long long)(valid ? ro.saturated : 0),
-                               (unsigned long long)(valid ? ro.refills : 0),
-                               (unsigned long long)(valid ? ro.numeric : 0)};
-#pragma unroll
-    for (int q = 0; q < 7; ++q)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
-    if ((threadIdx.x & 31) == 0) {
-        if (v[0]) atomicAdd(&ctr->ray_samples, v[0]);
-        if (v[1]) atomicAdd(&ctr->prim_samples, v[1]);
-        if (v[2]) atomicAdd(&ctr->hit_rays, v[2]);
-        if (v[3]) atomicAdd(&ctr->early_exits, v[3]);
-        if (v[4]) atomicAdd(&ctr->saturated, v[4]);
-        if (v[5]) atomicAdd(&ctr->refills, v[5]);
-        if (v[6]) atomicAdd(&ctr->numeric_fail, v[6]);
-    }
-}
-
-__device__ __forceinline__ int2 tile_pixel(int tx, int ty, int tid) {
-    // warps cover 8x4 pixel blocks (better ray coherence than 16x2 rows)
-    const int wid = tid >> 5, lane = tid & 31;
-    return make_int2(tx * kTile + (wid & 1) * 8 + (lane & 7), ty * kTile + (wid >> 1) * 4 + (lane >> 3));
 }
 
 // ----------------------------------------------------------------------------------------

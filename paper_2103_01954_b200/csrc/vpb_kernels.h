@@ -38,6 +38,17 @@ struct RaysDev {
     const float *jitter;
 };
 
+// Backward-pass buffers (K6): planar payload gradients + 9 pose gradients per primitive (the
+// GradBuffer layout of params.h:12-27), per-primitive pose data (rBase[9] and the three
+// rotationDerivative matrices [27]), and the per-ray output adjoints.
+struct BwdDev {
+    float *g_pay;
+    float *g_pose;
+    const float *pose36;
+    const float *adj_rgb;
+    const float *adj_alpha;
+};
+
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
@@ -70,6 +81,10 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const float4 *payload, const RaysDev &rays, int64_t n_rays,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st);
+cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
+                                 const float4 *payload, const RaysDev &rays, int64_t n_rays,
+                                 const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
+                                 cudaStream_t st);
 cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
 cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
                              int64_t n_px, cudaStream_t st);

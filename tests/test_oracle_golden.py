@@ -94,3 +94,14 @@ def test_expf_port_matches_libm(oracle):
     assert oracle.expf_port_mismatches(0x80000000, 0xC1C00000, 7) == 0
     assert oracle.expf_port_mismatches(0x80000000, 0xC2D00000, 4099) == 0
     assert oracle.expf_port_mismatches(0x00000000, 0x42B00000, 4099) == 0
+
+
+def test_backward_matches_reference(oracle):
+    """backwardRay restatement == the reference's GradBuffer, bit for bit (sequential order)."""
+    for name, g in load_groups("backward").items():
+        win = api.WindowParams(float(g["window"][0]), int(g["window"][1]))
+        cfg = api.MarchConfig(float(g["cfg"][0]), float(g["cfg"][1]))
+        got = oracle.backward_rays(g["tr"], int(g["m"]), g["payload"], win, g["o"], g["d"], g["adj_rgb"],
+                                   g["adj_alpha"], cfg, g["jit"])
+        assert np.array_equal(bits(got), bits(g["grads"])), name
+        assert np.count_nonzero(g["grads"]) > 1000, name
