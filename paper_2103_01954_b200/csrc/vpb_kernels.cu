@@ -511,7 +511,7 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 // ----------------------------------------------------------------------------------------
 // Host-side launchers (plain C++ signatures for vpb_api.cpp).
 #ifndef VPB_WINDOW_CAP
-#define VPB_WINDOW_CAP 24
+#define VPB_WINDOW_CAP 20
 #endif
 constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared memory)
 

@@ -13,7 +13,10 @@ namespace vpb {
 
 constexpr int kTile = 16;
 constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
-constexpr int kCandCap = 64;        // candidates staged in shared memory per tile
+#ifndef VPB_CAND_CAP
+#define VPB_CAND_CAP 192
+#endif
+constexpr int kCandCap = VPB_CAND_CAP;  // candidates staged in shared memory per tile (<= 255)
 
 // Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
 //

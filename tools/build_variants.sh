@@ -1,12 +1,15 @@
 #!/bin/bash
-# Builds libvpb variants (launch-bounds min blocks x window capacity) for tuning sweeps.
+# Builds libvpb variants for tuning sweeps: NAME = <min CTAs/SM>_<window cap>[_<staged candidates>].
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p build/variants
 for v in "$@"; do
-  b=${v%_*}; c=${v#*_}
+  IFS=_ read -r b c cc <<< "$v"
+  cc=${cc:-64}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-ffp-contract=off \
-    -DVPB_MARCH_MINB=$b -DVPB_WINDOW_CAP=$c -c paper_2103_01954_b200/csrc/vpb_kernels.cu -o build/variants/k_$v.o -Xptxas -v 2> build/variants/k_$v.log
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libvpb_$v.so build/variants/k_$v.o build/obj/vpb_backward.o build/obj/vpb_api.o build/obj/vpb_synth.o -cudart static
-  echo "$v: $(grep -A2 k_march_tiles build/variants/k_$v.log | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
+    -DVPB_MARCH_MINB=$b -DVPB_WINDOW_CAP=$c -DVPB_CAND_CAP=$cc -c paper_2103_01954_b200/csrc/vpb_kernels.cu \
+    -o build/variants/k_$v.o -Xptxas -v 2> build/variants/k_$v.log
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libvpb_$v.so build/variants/k_$v.o \
+    build/obj/vpb_backward.o build/obj/vpb_api.o build/obj/vpb_synth.o -cudart static
+  echo "$v: $(grep -A2 'k_march_tilesILi' build/variants/k_$v.log | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | head -2 | tr '\n' ' ')"
 done
