@@ -112,12 +112,8 @@ __constant__ unsigned long long kExp2fTab[32] = {
     0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
     0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
 
-__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
-    if (!(x == x)) return x + x;
-    if (x < -0x1.9fe368p6f) return 0.0f;
-    if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
-    if (x == -0x1.f8cbb2p+5f) return 0x1.f45326p-92f;
-    if (x == 0x1.04845ep+5f) return 0x1.f93e38p+46f;
+// The binary64 core, valid on [-0x1.9fe368p6, 0x1.62e42ep6] minus the two patched inputs.
+__device__ __forceinline__ float expf_core(float x, const unsigned long long *tab) {
     const double InvLn2N = 0x1.71547652b82fep+0 * 32, Shift = 0x1.8p+52;
     const double C0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32, C1 = 0x1.ebfce50fac4f3p-3 / 32 / 32,
                  C2 = 0x1.62e42ff0c52d6p-1 / 32;
@@ -133,6 +129,15 @@ __device__ __forceinline__ float expf_glibc(float x, const unsigned long long *t
     double y = __fma_rn(C2, r, 1.0);
     y = __fma_rn(zz, r2, y);
     return __double2float_rn(__dmul_rn(y, s));
+}
+
+__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
+    if (!(x == x)) return x + x;
+    if (x < -0x1.9fe368p6f) return 0.0f;
+    if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+    if (x == -0x1.f8cbb2p+5f) return 0x1.f45326p-92f;
+    if (x == 0x1.04845ep+5f) return 0x1.f93e38p+46f;
+    return expf_core(x, tab);
 }
 
 // primitive.cpp:12-22
@@ -162,7 +167,11 @@ __device__ __forceinline__ float window_value(V3 p, float alpha, int beta,
         s = (pow8(p.x) + pow8(p.y)) + pow8(p.z);
     else
         s = (pow_even(p.x, beta) + pow_even(p.y, beta)) + pow_even(p.z, beta);
-    return expf_glibc(-alpha * s, tab);
+    const float x = -alpha * s;
+    // |p| <= 1 makes s a finite value in [0, 3], so for 0 < alpha <= 34.6 the argument lies in
+    // [-103.8, 0]: no NaN, overflow or underflow cases; only the -63.1 patch can apply.
+    if (alpha > 0.0f && alpha <= 34.6f) return x == -0x1.f8cbb2p+5f ? 0x1.f45326p-92f : expf_core(x, tab);
+    return expf_glibc(x, tab);
 }
 
 // march.cpp:14-16 — cwiseMax(-1, cwiseMin(1, p)) with std::min/std::max semantics.
