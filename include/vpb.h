@@ -150,6 +150,41 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
                      const vp_march *cfg, const float *transforms24, float *grads,
                      int32_t accumulate);
 
+/* ---- training rows ------------------------------------------------------
+ * evalLoss's ray-batch part (grad.cpp:197-251): for each RaySample i (fit.cpp:85-113) the ray
+ * of camera cams[cam_index[i]] through pixel_xy[i] (generateRay, camera.cpp:14-23), evalLoss's
+ * jitter hash of (cam_index, pixel_id) (grad.cpp:222-225), march(), composite with
+ * background[i], L_pho = lambda * mean |composited - target|^2 (losses.cpp:12-25) into
+ * *loss_pho, the composited pixels (nullable), and, when grads != NULL, backwardRay of every
+ * ray with the photometric adjoints into grads (layout and accumulate as vp_backward_rays).
+ * VP_ERR_USAGE on an empty batch, a bad camera index or a pixel outside its image. */
+int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t n,
+                     const int32_t *cam_index, const float *pixel_xy, const int32_t *pixel_id,
+                     const float *target, const float *background, float lambda_pho,
+                     const vp_march *cfg, const float *transforms24, float *loss_pho,
+                     float *composited, float *grads, int32_t accumulate);
+
+/* lossVol + lossDel (losses.cpp:45-68) on the host; grad_pose (9 floats per primitive,
+ * nullable) accumulates +=. */
+int vp_loss_pose(int32_t n_prim, const float *transforms24, float lambda_vol, float lambda_del,
+                 float *loss_vol, float *loss_del, float *grad_pose);
+/* lossGeo (losses.cpp:27-43) on the host; offsets nullable; grad_verts (n*3) accumulates. */
+int vp_loss_geo(int32_t n_verts, const float *base, const float *offsets, const float *tracked,
+                float lambda, float *loss, float *grad_verts);
+
+/* AdamConfig (losses.h:34-44). */
+typedef struct vp_adam {
+    float lr, beta1, beta2, eps, lr_delta_scale, lr_vertex_scale;
+} vp_adam;
+/* adamStep (losses.cpp:70-104) on the resident frame over [payload | 9K deltas] (no guide-
+ * mesh vertices): grads (host or device, vp_backward_rays layout). The payload is updated and
+ * projected (>= 0) in place on the device; the deltas are updated in transforms24 (host,
+ * K*24, in/out), composed scales projected to >= 1e-4, and the frame recomposed and
+ * re-uploaded. Moments persist in the context (AdamState) until vp_adam_reset or a frame of
+ * a different size. VP_ERR_NUMERIC (and no update) on a non-finite gradient. */
+int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *transforms24);
+int vp_adam_reset(vp_ctx *ctx);
+
 /* composite() (march.cpp:134-147): out = A*I + (1-A)*B, all H*W(*3) arrays. */
 int vp_composite(vp_ctx *ctx, int32_t width, int32_t height, const float *rgb,
                  const float *alpha, const float *background, float *out);

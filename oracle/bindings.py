@@ -336,3 +336,47 @@ class RefCore:
         if rc != 0:
             raise RuntimeError(f"reference backward failed ({rc}): {self.error()}")
         return g
+
+
+def _cams23(cams):
+    out = np.zeros((len(cams), 23), np.float32)
+    for i, c in enumerate(cams):
+        k9, r9, t3 = cam_arrays(c)
+        out[i, :9], out[i, 9:18], out[i, 18:21] = k9, r9, t3
+        out[i, 21], out[i, 22] = c.width, c.height
+    return out
+
+
+def ref_eval_loss(ref, tr24, m, payload, window, cams, cam_index, pixel_xy, pixel_id, target,
+                  background, weights, cfg, with_grads=True):
+    """The reference evalLoss (no tracked vertices); returns (terms[4], grads or None)."""
+    L = ref.lib
+    L.vpref_eval_loss.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, C.c_int32,
+                                  f32p, C.c_int64, i32p, f32p, i32p, f32p, f32p, C.c_float, C.c_float,
+                                  C.c_float, C.c_float, C.c_float, C.c_int32, C.c_uint64, f32p, f32p]
+    tr = _f(tr24).reshape(-1, 24)
+    k = tr.shape[0]
+    n = len(cam_index)
+    terms = np.zeros(4, np.float32)
+    g = np.zeros(k * 4 * int(m) ** 3 + 9 * k, np.float32) if with_grads else None
+    rc = L.vpref_eval_loss(k, int(m), _p(tr), _p(_f(payload)), float(window.alpha), int(window.beta),
+                           len(cams), _p(_cams23(cams)), n, _p(np.ascontiguousarray(cam_index, np.int32), i32p),
+                           _p(_f(pixel_xy).reshape(n, 2)), _p(np.ascontiguousarray(pixel_id, np.int32), i32p),
+                           _p(_f(target).reshape(n, 3)), _p(_f(background).reshape(n, 3)), float(weights[0]),
+                           float(weights[1]), float(weights[2]), float(cfg.step_size), float(cfg.early_eps),
+                           int(bool(cfg.jitter)), int(cfg.seed), _p(terms), _p(g))
+    if rc != 0:
+        raise RuntimeError(f"reference evalLoss failed ({rc}): {ref.error()}")
+    return terms, g
+
+
+def ref_adam_run(ref, tr24, m, payload_planar, grads_seq, cfg6):
+    L = ref.lib
+    L.vpref_adam_run.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_int32, f32p, f32p]
+    tr = np.array(tr24, np.float32).reshape(-1, 24).copy()
+    pay = np.array(payload_planar, np.float32).copy()
+    gs = _f(grads_seq)
+    rc = L.vpref_adam_run(tr.shape[0], int(m), _p(tr), _p(pay), len(grads_seq), _p(gs), _p(_f(cfg6)))
+    if rc != 0:
+        raise RuntimeError(f"reference adamStep failed ({rc}): {ref.error()}")
+    return tr, pay

@@ -211,6 +211,39 @@ def main():
           rays[:, :3].copy(), rays[:, 3:].copy(), np.full(nr, 0.5, np.float32), ar, aa)
     np.savez_compressed(OUT / "backward.npz", **{f"{k}__{f}": v for k, d_ in bwd.items() for f, v in d_.items()})
 
+    # -- evalLoss (grad.cpp:197-251) and adamStep (losses.cpp:70-104) ---------------------------
+    from oracle.bindings import ref_adam_run, ref_eval_loss
+    cams = [synthetic.shell_camera(v, 16, 48) for v in (0, 5, 11)]
+    ns = 600
+    ci = rng.integers(0, 3, ns).astype(np.int32)
+    pid = rng.integers(0, 48 * 48, ns).astype(np.int32)
+    pxy = np.stack([(pid % 48) + 0.5, (pid // 48) + 0.5], 1).astype(np.float32)
+    tgt = rng.uniform(0, 1, (ns, 3)).astype(np.float32)
+    bgs = rng.uniform(0, 1, (ns, 3)).astype(np.float32)
+    trl = trs8.copy()
+    trl[:, 15:24] = rng.uniform(-0.01, 0.01, (64, 9)).astype(np.float32)
+    wts = np.array([1.0, 0.1, 0.01, 0.01], np.float32)
+    ecfg = api.MarchConfig(0.002, 0.01, True, 3)
+    terms, gl = ref_eval_loss(ref, trl, 8, pays8, api.WindowParams(8, 8), cams, ci, pxy, pid, tgt, bgs,
+                              [wts[0], wts[2], wts[3]], ecfg)
+    camarr = np.stack([np.concatenate([c.intrinsics.reshape(-1), c.rotation.reshape(-1), c.translation,
+                                       [c.width, c.height]]) for c in cams]).astype(np.float32)
+    adam_cfg = np.array([1e-3, 0.9, 0.999, 1e-8, 0.1, 1.0], np.float32)
+    na = nb * 4 * mb ** 3 + 9 * nb  # Adam on the 40-box scene (small fixture)
+    gseq = (rng.normal(size=(3, na)) * 0.05).astype(np.float32)
+    gseq[1, 5] = 0  # a zero-gradient parameter
+    pay_in = pay.reshape(-1).copy()
+    pay_in[:50] = 1e-5  # some payload entries pushed below zero by the step -> projected
+    tr_in = trs.copy()
+    tr_in[3, 21] = -tr_in[3, 12] + 2e-4  # composed scale near the 1e-4 floor -> projected
+    tr_out, pay_out = ref_adam_run(ref, tr_in, mb, pay_in, gseq, adam_cfg)
+    np.savez_compressed(OUT / "train.npz", tr=trl, m=np.int32(8), window=np.array([8, 8], np.float32),
+                        cams=camarr, cam_index=ci, pixel=pxy, pixel_id=pid, target=tgt, background=bgs,
+                        weights=wts, cfg=np.array([0.002, 0.01, 1, 3], np.float64), terms=terms, grads=gl,
+                        adam_cfg=adam_cfg, adam_m=np.int32(mb), adam_grads=gseq, adam_tr_in=tr_in,
+                        adam_pay_in=pay_in, adam_tr_out=tr_out, adam_pay_out=pay_out,
+                        payload_sha=np.array(sha(pays8)))
+
     # -- full renders (march.cpp:95-132) -------------------------------------------------------
     store, meta = {}, digests["meta"]
     tr, pay = synthetic.shell_arrays(64, 16)

@@ -254,6 +254,89 @@ int vpref_backward_rays(int32_t nPrim, int32_t m, const float *tr24, const float
     });
 }
 
+// evalLoss (grad.cpp:197-251) with no tracked vertices: cams23 = n_cams * {K[9] R[9] t[3] w h};
+// RaySamples given as arrays. terms4 = {pho, geo, vol, del}; grads (nullable) overwritten with
+// the GradBuffer (K*4*M^3 + 9K).
+int vpref_eval_loss(int32_t nPrim, int32_t m, const float *tr24, const float *payload,
+                    float wAlpha, int32_t wBeta, int32_t nCams, const float *cams23, int64_t n,
+                    const int32_t *camIndex, const float *pixelXY, const int32_t *pixelId,
+                    const float *target, const float *background, float lPho, float lVol,
+                    float lDel, float stepSize, float earlyEps, int32_t jitter, uint64_t seed,
+                    float *terms4, float *grads) {
+    return guarded([&] {
+        Scene scene;
+        scene.window = WindowParams{wAlpha, wBeta};
+        Frame fr;
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        scene.frames.push_back(fr);
+        std::vector<Camera> cams;
+        for (int c = 0; c < nCams; ++c) {
+            const float *q = cams23 + 23 * size_t(c);
+            cams.push_back(cameraFrom(q, q + 9, q + 18, int(q[21]), int(q[22])));
+        }
+        std::vector<RaySample> batch(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            RaySample &rs = batch[size_t(i)];
+            rs.cameraIndex = camIndex[i];
+            rs.pixel = Vec2(pixelXY[2 * i], pixelXY[2 * i + 1]);
+            rs.pixelId = pixelId[i];
+            rs.target = v3(target + 3 * i);
+            rs.background = v3(background + 3 * i);
+        }
+        LossWeights w;
+        w.pho = lPho;
+        w.vol = lVol;
+        w.del = lDel;
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        cfg.jitter = jitter != 0;
+        cfg.seed = seed;
+        GradBuffer gb(layoutOf(scene.frames[0], 0));
+        const LossTerms t = evalLoss(scene, 0, cams, batch, {}, w, cfg, grads ? &gb : nullptr);
+        terms4[0] = t.pho;
+        terms4[1] = t.geo;
+        terms4[2] = t.vol;
+        terms4[3] = t.del;
+        if (grads) std::memcpy(grads, gb.values.data(), gb.values.size() * sizeof(float));
+    });
+}
+
+// nSteps adamStep calls (losses.cpp:70-104) with the given gradient sequence
+// (nSteps * (K*4*M^3 + 9K)); tr24 and the planar payload are updated in place.
+int vpref_adam_run(int32_t nPrim, int32_t m, float *tr24, float *payload, int32_t nSteps,
+                   const float *grads, const float *cfg6) {
+    return guarded([&] {
+        Frame fr;
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        const ParamLayout layout = layoutOf(fr, 0);
+        AdamConfig c;
+        c.lr = cfg6[0];
+        c.beta1 = cfg6[1];
+        c.beta2 = cfg6[2];
+        c.eps = cfg6[3];
+        c.lrDeltaScale = cfg6[4];
+        c.lrVertexScale = cfg6[5];
+        AdamState state(layout.total(), c);
+        GradBuffer gb(layout);
+        for (int s = 0; s < nSteps; ++s) {
+            std::memcpy(gb.values.data(), grads + size_t(s) * layout.total(), layout.total() * sizeof(float));
+            adamStep(fr, layout, gb, state);
+        }
+        std::memcpy(payload, fr.slab.payload.data(), fr.slab.payload.size() * sizeof(float));
+        for (int k = 0; k < nPrim; ++k) {
+            float *o = tr24 + 24 * size_t(k);
+            put3(o + 15, fr.transforms[size_t(k)].deltaT);
+            put3(o + 18, fr.transforms[size_t(k)].deltaR);
+            put3(o + 21, fr.transforms[size_t(k)].deltaS);
+        }
+    });
+}
+
 float vpref_window(float x, float y, float z, float wAlpha, int32_t wBeta) {
     return window(Vec3(x, y, z), WindowParams{wAlpha, wBeta});
 }

@@ -29,6 +29,11 @@ class vp_march(C.Structure):
                 ("accumulation_permutation", C.c_uint64)]
 
 
+class vp_adam(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("lr_delta_scale", C.c_float), ("lr_vertex_scale", C.c_float)]
+
+
 class vp_stats(C.Structure):
     _fields_ = [("ray_samples", C.c_int64), ("prim_samples", C.c_int64),
                 ("hit_rays", C.c_int64), ("early_exits", C.c_int64),
@@ -63,6 +68,13 @@ SIGNATURES = {
                                 f32p, f32p, i32p]),
     "vp_backward_rays": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, f32p, f32p, f32p,
                                    C.POINTER(vp_march), f32p, f32p, C.c_int32]),
+    "vp_eval_loss_pho": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(vp_camera), C.c_int64, i32p, f32p,
+                                   i32p, f32p, f32p, C.c_float, C.POINTER(vp_march), f32p, f32p, f32p,
+                                   f32p, C.c_int32]),
+    "vp_loss_pose": (C.c_int, [C.c_int32, f32p, C.c_float, C.c_float, f32p, f32p, f32p]),
+    "vp_loss_geo": (C.c_int, [C.c_int32, f32p, f32p, f32p, C.c_float, f32p, f32p]),
+    "vp_adam_step": (C.c_int, [C.c_void_p, C.POINTER(vp_adam), f32p, f32p]),
+    "vp_adam_reset": (C.c_int, [C.c_void_p]),
     "vp_composite": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]),
     "vp_debug_tiles": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), i32p, u32p, i32p, i32p,
                                  C.c_int64, i64p]),

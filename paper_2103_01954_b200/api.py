@@ -372,6 +372,135 @@ class Renderer:
         return res
 
 
+# ----------------------------------------------------------------------------------------
+# Training rows: evalLoss (grad.cpp:197-251) and adamStep (losses.cpp:70-104)
+
+@dataclass
+class LossWeights:
+    """losses.h:10-15 (`del` is a Python keyword: del_)."""
+    pho: float = 1.0
+    geo: float = 0.1
+    vol: float = 0.01
+    del_: float = 0.01
+
+
+@dataclass
+class LossTerms:
+    """grad.h:28-31"""
+    pho: float = 0.0
+    geo: float = 0.0
+    vol: float = 0.0
+    del_: float = 0.0
+
+    def total(self) -> float:
+        return float(np.float32(np.float32(np.float32(self.pho) + np.float32(self.geo)) + np.float32(self.vol))
+                     + np.float32(self.del_))
+
+
+@dataclass
+class RaySamples:
+    """A batch of RaySample (grad.h:12-18) as arrays: camera_index (n,), pixel (n, 2) pixel
+    coordinates (x + 0.5, y + 0.5 for centres), pixel_id (n,), target and background (n, 3)."""
+    camera_index: np.ndarray
+    pixel: np.ndarray
+    pixel_id: np.ndarray
+    target: np.ndarray
+    background: np.ndarray
+
+
+@dataclass
+class AdamConfig:
+    """losses.h:34-44"""
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    lr_delta_scale: float = 1.0
+    lr_vertex_scale: float = 1.0
+
+
+def grad_size(n_prim: int, m: int, n_verts: int = 0) -> int:
+    """ParamLayout::total() (params.h:12-27)."""
+    return n_prim * 4 * m ** 3 + 9 * n_prim + 3 * n_verts
+
+
+def eval_loss(renderer: "Renderer", scene: Scene, frame: int, cams: List[Camera], batch: RaySamples,
+              weights: LossWeights, cfg: MarchConfig, grads: Optional[np.ndarray] = None,
+              tracked_verts: Optional[np.ndarray] = None, mesh_vertices: Optional[np.ndarray] = None,
+              vertex_offsets: Optional[np.ndarray] = None, upload: bool = True) -> LossTerms:
+    """evalLoss (grad.cpp:197-251): uploads the frame, runs the photometric term on the device
+    (rays, march, composite, L_pho and, with `grads`, backwardRay), adds L_vol / L_del (and
+    L_geo when tracked vertices are given) on the host. `grads` (GradBuffer layout, float32 of
+    grad_size(K, M, n_verts)) accumulates like the reference's GradBuffer."""
+    if frame < 0 or frame >= len(scene.frames):
+        raise Error(ErrorCategory.USAGE, "frame index out of range")
+    lib = _lib.load()
+    fr = scene.frames[frame]
+    if upload:  # else the renderer already holds this frame (e.g. after adam_step)
+        renderer.set_frame(scene, frame)
+    k, m = len(fr.transforms), fr.slab.voxels_per_axis
+    tr = _f32(fr.transforms).reshape(-1, 24)
+    n = int(np.asarray(batch.camera_index).size)
+    cams_c = (_lib.vp_camera * len(cams))(*[c.to_c() for c in cams])
+    ci = np.ascontiguousarray(batch.camera_index, np.int32)
+    pid = np.ascontiguousarray(batch.pixel_id, np.int32)
+    terms = LossTerms()
+    nv = 0 if tracked_verts is None else int(np.asarray(tracked_verts).size // 3)
+    if grads is not None and (grads.dtype != np.float32 or grads.size != grad_size(k, m, nv)):
+        raise Error(ErrorCategory.USAGE, "gradient buffer must be float32 of ParamLayout::total()")
+    n_kd = k * 4 * m ** 3 + 9 * k
+    g_dev = None if grads is None else np.ascontiguousarray(grads[:n_kd])
+    if nv:  # lossGeo (losses.cpp:27-43)
+        loss = C.c_float()
+        base = _f32(mesh_vertices).reshape(nv, 3)
+        off = None if vertex_offsets is None or np.asarray(vertex_offsets).size == 0 else _f32(vertex_offsets)
+        gv = None if grads is None else np.ascontiguousarray(grads[n_kd:])
+        _check(lib.vp_loss_geo(nv, _fptr(base), _fptr(off) if off is not None else None,
+                               _fptr(_f32(tracked_verts).reshape(nv, 3)), float(weights.geo), C.byref(loss),
+                               _fptr(gv) if gv is not None else None))
+        terms.geo = float(loss.value)
+        if gv is not None:
+            grads[n_kd:] = gv
+    lv, ld = C.c_float(), C.c_float()
+    gpose = None if g_dev is None else np.ascontiguousarray(g_dev[k * 4 * m ** 3:])
+    _check(lib.vp_loss_pose(k, _fptr(tr), float(weights.vol), float(weights.del_), C.byref(lv), C.byref(ld),
+                            _fptr(gpose) if gpose is not None else None))
+    terms.vol, terms.del_ = float(lv.value), float(ld.value)
+    if g_dev is not None:
+        g_dev[k * 4 * m ** 3:] = gpose
+    lp = C.c_float()
+    mc = cfg.to_c()
+    _check(lib.vp_eval_loss_pho(renderer.ctx, len(cams), cams_c, n, ci.ctypes.data_as(i32p),
+                                _fptr(_f32(batch.pixel).reshape(n, 2)), pid.ctypes.data_as(i32p),
+                                _fptr(_f32(batch.target).reshape(n, 3)), _fptr(_f32(batch.background).reshape(n, 3)),
+                                float(weights.pho), C.byref(mc), _fptr(tr), C.byref(lp),
+                                None, _fptr(g_dev) if g_dev is not None else None,
+                                1 if g_dev is not None else 0), renderer.ctx)
+    terms.pho = float(lp.value)
+    if grads is not None:
+        grads[:n_kd] = g_dev
+    return terms
+
+
+def adam_step(renderer: "Renderer", cfg: AdamConfig, grads: np.ndarray, transforms: np.ndarray) -> None:
+    """adamStep (losses.cpp:70-104) on the renderer's resident frame: the payload is updated
+    on the device, `transforms` (K x 24 float32) in place; the frame is recomposed."""
+    lib = _lib.load()
+    if transforms.dtype != np.float32 or not transforms.flags.c_contiguous:
+        raise Error(ErrorCategory.USAGE, "transforms must be a contiguous float32 K x 24 array")
+    ac = _lib.vp_adam(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.lr_delta_scale, cfg.lr_vertex_scale)
+    g = np.ascontiguousarray(grads, np.float32)
+    _check(lib.vp_adam_step(renderer.ctx, C.byref(ac), _fptr(g), _fptr(transforms)), renderer.ctx)
+
+
+def payload_planar(renderer: "Renderer") -> np.ndarray:
+    """The resident payload converted back to the reference's planar (k, c, z, y, x) layout."""
+    k, m = int(renderer.n_prim or 0), int(renderer.m or 0)
+    inter = np.zeros(k * m ** 3 * 4, np.float32)
+    renderer.copy_payload_to(inter.ctypes.data)
+    return np.ascontiguousarray(inter.reshape(k, m ** 3, 4).transpose(0, 2, 1)).reshape(-1)
+
+
 _default: dict = {}
 
 

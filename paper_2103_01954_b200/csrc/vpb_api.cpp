@@ -84,6 +84,8 @@ struct vp_ctx {
     int ovf_cap = 0;
     cudaEvent_t t_ev[2 * kTimingSlots] = {};
     int64_t t_count = 0;
+    DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
+    int64_t adam_step = 0;
 };
 
 namespace {
@@ -717,6 +719,169 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
     VP_CUDA(ctx, cudaStreamSynchronize(st));
     if (k > 0 && n_rays > 0) return check_counters(ctx, *ctx->h_ctr);
     return VP_OK;
+}
+
+int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t n,
+                     const int32_t *cam_index, const float *pixel_xy, const int32_t *pixel_id,
+                     const float *target, const float *background, float lambda_pho,
+                     const vp_march *cfg, const float *transforms24, float *loss_pho,
+                     float *composited, float *grads, int32_t accumulate) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    if (n <= 0) return fail(ctx, VP_ERR_USAGE, "empty pixel set");  // losses.cpp:14
+    if (n_cams <= 0 || !cams || !cam_index || !pixel_xy || !pixel_id || !target || !background)
+        return fail(ctx, VP_ERR_USAGE, "null ray-batch arrays");
+    if (grads && !transforms24) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    cudaStream_t st = ctx->stream;
+    const size_t nn = size_t(n);
+    std::vector<CamDev> cd(static_cast<size_t>(n_cams));
+    for (int32_t c = 0; c < n_cams; ++c) cd[size_t(c)] = make_cam(cams[c]);
+    // one device block: cams | cam_index | pixel_id | pixel_xy | target | bg | o | d | jit |
+    // rgb | alpha | composited | resid | adj_rgb | adj_alpha | bad flag
+    const size_t cam_f = (sizeof(CamDev) * cd.size() + 15) / 16 * 4;
+    DBuf<float> buf;
+    const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1) + 4;
+    VP_CUDA(ctx, buf.ensure(total));
+    float *p = buf.p;
+    CamDev *d_cams = reinterpret_cast<CamDev *>(p);
+    p += cam_f;
+    int *d_ci = reinterpret_cast<int *>(p); p += nn;
+    int *d_pid = reinterpret_cast<int *>(p); p += nn;
+    float *d_xy = p; p += 2 * nn;
+    float *d_tg = p; p += 3 * nn;
+    float *d_bg = p; p += 3 * nn;
+    float *d_o = p; p += 3 * nn;
+    float *d_d = p; p += 3 * nn;
+    float *d_j = p; p += nn;
+    float *d_rgb = p; p += 3 * nn;
+    float *d_a = p; p += nn;
+    float *d_comp = p; p += 3 * nn;
+    float *d_res = p; p += 3 * nn;
+    float *d_ar = p; p += 3 * nn;
+    float *d_aa = p; p += nn;
+    int *d_bad = reinterpret_cast<int *>(p);
+    VP_CUDA(ctx, cudaMemcpyAsync(d_cams, cd.data(), sizeof(CamDev) * cd.size(), cudaMemcpyHostToDevice, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_ci, cam_index, 4 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_pid, pixel_id, 4 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_xy, pixel_xy, 8 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_tg, target, 12 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_bg, background, 12 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, st));
+    VP_CUDA(ctx, launch_eval_rays(d_cams, n_cams, d_ci, d_xy, d_pid, n, cfg->jitter, cfg->seed, d_o, d_d, d_j,
+                                  d_bad, st));
+    int h_bad = 0;
+    VP_CUDA(ctx, cudaMemcpyAsync(&h_bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    if (h_bad == 1) return fail(ctx, VP_ERR_USAGE, "camera index out of range");
+    if (h_bad == 2) return fail(ctx, VP_ERR_USAGE, "pixel outside image bounds");  // camera.cpp:15-16
+    // forward march of the batch (evalLoss, grad.cpp:216-226)
+    const RaysDev rays{d_o, d_d, d_j};
+    const OutDev od{d_rgb, d_a, nullptr};
+    if (size_t(ctx->ovf_cap) < nn) {
+        VP_CUDA(ctx, ctx->ovf_list.ensure(nn));
+        ctx->ovf_cap = int(nn);
+    }
+    if (int rc = ensure_fallback(ctx)) return rc;
+    const MarchDev mp = make_march(ctx, cfg);
+    VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+    if (ctx->n_prim == 0) {
+        VP_CUDA(ctx, cudaMemsetAsync(d_rgb, 0, 12 * nn, st));
+        VP_CUDA(ctx, cudaMemsetAsync(d_a, 0, 4 * nn, st));
+    } else {
+        VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, rays, n, od, ctx->d_ctr,
+                                       ctx->ovf_list.p, ctx->ovf_cap, st));
+        const CamDev none{};
+        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, ctx->n_prim, ctx->payload.p,
+                                           nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
+                                           ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+    }
+    // lossPho (losses.cpp:12-25): residuals and adjoints on the device, the scalar sum on the
+    // host in the reference's sequential order
+    const float invN = 1.0f / float(nn);
+    const float scale = 2 * lambda_pho * invN;
+    VP_CUDA(ctx, launch_loss_adjoints(d_rgb, d_a, d_tg, d_bg, n, scale, d_comp, d_res, d_ar, d_aa, st));
+    std::vector<float> res(3 * nn);
+    VP_CUDA(ctx, cudaMemcpyAsync(res.data(), d_res, 12 * nn, cudaMemcpyDeviceToHost, st));
+    if (composited) VP_CUDA(ctx, cudaMemcpyAsync(composited, d_comp, 12 * nn, cudaMemcpyDefault, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    if (int rc = check_counters(ctx, *ctx->h_ctr)) return rc;
+    float acc = 0;
+    for (size_t i = 0; i < nn; ++i) {
+        const host::F3 e = host::f3(res[3 * i], res[3 * i + 1], res[3 * i + 2]);
+        acc += host::dot(e, e);
+    }
+    if (loss_pho) *loss_pho = lambda_pho * invN * acc;
+    if (!grads) return VP_OK;
+    // backwardRay for every ray with the photometric adjoints (grad.cpp:240-248)
+    return vp_backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate);
+}
+
+int vp_adam_reset(vp_ctx *ctx) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    ctx->adam_m1.release();
+    ctx->adam_m2.release();
+    ctx->adam_step = 0;
+    return VP_OK;
+}
+
+int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *transforms24) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (!cfg || !grads) return fail(ctx, VP_ERR_USAGE, "null arguments");
+    const int k = ctx->n_prim, m = ctx->m;
+    if (k > 0 && !transforms24) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    const size_t m3 = size_t(m) * m * m, n_pay = size_t(k) * 4 * m3, n = n_pay + 9 * size_t(k);
+    if (n == 0) return VP_OK;
+    cudaStream_t st = ctx->stream;
+    if (ctx->adam_m1.n != n || ctx->adam_step == 0) {  // AdamState(n): zero moments
+        VP_CUDA(ctx, ctx->adam_m1.ensure(n));
+        VP_CUDA(ctx, ctx->adam_m2.ensure(n));
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->adam_m1.p, 0, 4 * n, st));
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->adam_m2.p, 0, 4 * n, st));
+        ctx->adam_step = 0;
+    }
+    DBuf<float> tmp;  // [grads (if host) | deltas | bad flag]
+    VP_CUDA(ctx, tmp.ensure(n + 9 * size_t(k) + 1));
+    const float *dg = grads;
+    if (!is_device_ptr(grads)) {
+        VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, grads, 4 * n, cudaMemcpyHostToDevice, st));
+        dg = tmp.p;
+    }
+    float *d_delta = tmp.p + n;
+    int *d_bad = reinterpret_cast<int *>(tmp.p + n + 9 * size_t(k));
+    std::vector<float> deltas(9 * size_t(k));
+    for (int i = 0; i < k; ++i)
+        std::memcpy(deltas.data() + 9 * size_t(i), transforms24 + 24 * size_t(i) + 15, 9 * sizeof(float));
+    VP_CUDA(ctx, cudaMemcpyAsync(d_delta, deltas.data(), 4 * deltas.size(), cudaMemcpyHostToDevice, st));
+    VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, st));
+    AdamDev c{cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->lr_delta_scale, 0.f, 0.f};
+    VP_CUDA(ctx, launch_adam(dg, nullptr, nullptr, nullptr, nullptr, int64_t(n_pay), int64_t(n), unsigned(m3), c,
+                             d_bad, true, st));
+    int bad = 0;
+    VP_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    if (bad) return fail(ctx, VP_ERR_NUMERIC, "non-finite gradient");  // losses.cpp:74-75
+    ctx->adam_step += 1;
+    c.bc1 = 1 - std::pow(cfg->beta1, float(ctx->adam_step));  // losses.cpp:79-80
+    c.bc2 = 1 - std::pow(cfg->beta2, float(ctx->adam_step));
+    VP_CUDA(ctx, launch_adam(dg, ctx->adam_m1.p, ctx->adam_m2.p, ctx->payload.p, d_delta, int64_t(n_pay),
+                             int64_t(n), unsigned(m3), c, d_bad, false, st));
+    VP_CUDA(ctx, cudaMemcpyAsync(deltas.data(), d_delta, 4 * deltas.size(), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    // deltas back into the records, scale projection (losses.cpp:97-103), recompose + upload
+    constexpr float kMinScale = 1e-4f;  // losses.h:61
+    std::vector<float> xf(15 * size_t(k));
+    for (int i = 0; i < k; ++i) {
+        float *t = transforms24 + 24 * size_t(i);
+        std::memcpy(t + 15, deltas.data() + 9 * size_t(i), 9 * sizeof(float));
+        for (int a = 0; a < 3; ++a) {
+            const float composed = t[12 + a] + t[21 + a];
+            if (composed < kMinScale) t[21 + a] = kMinScale - t[12 + a];
+        }
+        if (!host::compose(t, xf.data() + 15 * size_t(i)))
+            return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+    }
+    return vp_set_transforms(ctx, k, xf.data());
 }
 
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y) {

@@ -49,6 +49,11 @@ struct BwdDev {
     const float *adj_alpha;
 };
 
+// Adam step constants (losses.cpp:70-104); bc1/bc2 = 1 - beta^step computed on the host.
+struct AdamDev {
+    float lr, beta1, beta2, eps, lr_delta_scale, bc1, bc2;
+};
+
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
@@ -85,6 +90,14 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
                                  cudaStream_t st);
+cudaError_t launch_eval_rays(const CamDev *cams, int n_cams, const int *cam_index, const float *pixel_xy,
+                             const int *pixel_id, int64_t n, int jitter, unsigned long long seed,
+                             float *origins, float *dirs, float *jit, int *bad, cudaStream_t st);
+cudaError_t launch_loss_adjoints(const float *rgb, const float *alpha, const float *target, const float *bg,
+                                 int64_t n, float scale, float *composited, float *resid, float *adj_rgb,
+                                 float *adj_alpha, cudaStream_t st);
+cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, float *deltas, int64_t n_pay,
+                        int64_t n, unsigned m3, const AdamDev &c, int *bad, bool check, cudaStream_t st);
 cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
 cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
                              int64_t n_px, cudaStream_t st);

@@ -1,0 +1,142 @@
+// vpb_train.cu — the training-side rows of SURVEY.md §8(f): the evalLoss ray-batch driver
+// (grad.cpp:197-251) and Adam with the feasibility projection (losses.cpp:70-104), both on
+// the resident frame so a fit iteration keeps the payload on the device.
+//
+//   k_eval_rays        RaySample -> Ray: generateRay per sample camera (camera.cpp:14-23) and
+//                      evalLoss's jitter hash (grad.cpp:222-225)
+//   k_loss_adjoints    composite with the sample background, the photometric residual and the
+//                      adjoints evalLoss hands to backwardRay (grad.cpp:228-247)
+//   k_adam_check /     adamStep: non-finite gradient check, then the bias-corrected update
+//   k_adam_update      over [payload | deltas] and the payload projection (>= 0); the
+//                      payload lives channel-interleaved on the device
+// Same arithmetic contract as the renderer (-fmad=false): element-wise results equal the
+// reference's bit for bit.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "vpb_device.cuh"
+#include "vpb_kernels.h"
+
+namespace vpb {
+
+__global__ void k_eval_rays(const CamDev *__restrict__ cams, int n_cams, const int *__restrict__ cam_index,
+                            const float *__restrict__ pixel_xy, const int *__restrict__ pixel_id,
+                            int64_t n, int jitter, unsigned long long seed, float *__restrict__ origins,
+                            float *__restrict__ dirs, float *__restrict__ jit, int *__restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int ci = cam_index[i];
+    if (ci < 0 || ci >= n_cams) {
+        atomicExch(bad, 1);
+        return;
+    }
+    const CamDev cam = cams[ci];
+    const float px = pixel_xy[2 * i], py = pixel_xy[2 * i + 1];
+    if (px < 0.0f || py < 0.0f || px > (float)cam.width || py > (float)cam.height) atomicExch(bad, 2);
+    V3 o, d;
+    generate_ray(cam, px, py, o, d);
+    origins[3 * i] = o.x;
+    origins[3 * i + 1] = o.y;
+    origins[3 * i + 2] = o.z;
+    dirs[3 * i] = d.x;
+    dirs[3 * i + 1] = d.y;
+    dirs[3 * i + 2] = d.z;
+    jit[i] = jitter ? hash_to_unit(hash_combine(seed, (uint64_t)(uint32_t)ci * 0x100000001b3ull +
+                                                          (uint64_t)(uint32_t)pixel_id[i]))
+                    : 0.5f;
+}
+
+// composited = rgb * a + bg * (1 - a); e = composited - target; aI = e * (2 lambda / n);
+// aRgb = aI * a; aAlpha = dot(aI, rgb - bg)   (grad.cpp:227-247, losses.cpp:12-25)
+__global__ void k_loss_adjoints(const float *__restrict__ rgb, const float *__restrict__ alpha,
+                                const float *__restrict__ target, const float *__restrict__ bg,
+                                int64_t n, float scale, float *__restrict__ composited,
+                                float *__restrict__ resid, float *__restrict__ adj_rgb,
+                                float *__restrict__ adj_alpha) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float a = alpha[i];
+    const V3 c = mk3(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+    const V3 b = mk3(bg[3 * i], bg[3 * i + 1], bg[3 * i + 2]);
+    const V3 comp = c * a + b * (1.0f - a);
+    const V3 e = comp - mk3(target[3 * i], target[3 * i + 1], target[3 * i + 2]);
+    const V3 aI = e * scale;
+    const V3 aRgb = aI * a;
+    composited[3 * i] = comp.x;
+    composited[3 * i + 1] = comp.y;
+    composited[3 * i + 2] = comp.z;
+    resid[3 * i] = e.x;
+    resid[3 * i + 1] = e.y;
+    resid[3 * i + 2] = e.z;
+    adj_rgb[3 * i] = aRgb.x;
+    adj_rgb[3 * i + 1] = aRgb.y;
+    adj_rgb[3 * i + 2] = aRgb.z;
+    adj_alpha[i] = dot3(aI, c - b);
+}
+
+__global__ void k_adam_check(const float *__restrict__ g, int64_t n, int *__restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(g[i])) atomicExch(bad, 1);
+}
+
+// One Adam step over [payload (planar GradBuffer order) | 9K deltas]; the payload parameter
+// with planar index (k, ch, v) lives at payload[k * m3 + v].ch (channel-interleaved).
+__global__ void k_adam_update(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
+                              float4 *__restrict__ payload, float *__restrict__ deltas, int64_t n_pay,
+                              int64_t n, unsigned m3, AdamDev c) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[i];
+        const float a = c.beta1 * m1[i] + (1.0f - c.beta1) * gi;
+        const float b = c.beta2 * m2[i] + (1.0f - c.beta2) * gi * gi;
+        m1[i] = a;
+        m2[i] = b;
+        const float mHat = a / c.bc1;
+        const float vHat = b / c.bc2;
+        const float lr = c.lr * (i < n_pay ? 1.0f : c.lr_delta_scale);
+        const float step = lr * mHat / (sqrtf(vHat) + c.eps);
+        if (i < n_pay) {
+            const int64_t k = i / (4 * (int64_t)m3), r = i - k * 4 * (int64_t)m3;
+            const int ch = (int)(r / m3);
+            const int64_t v = r - (int64_t)ch * m3;
+            float *p = reinterpret_cast<float *>(payload + k * m3 + v) + ch;
+            float nv = *p - step;
+            if (nv < 0.0f) nv = 0.0f;  // feasibility projection (losses.cpp:95-96)
+            *p = nv;
+        } else {
+            float *p = deltas + (i - n_pay);
+            *p = *p - step;
+        }
+    }
+}
+
+cudaError_t launch_eval_rays(const CamDev *cams, int n_cams, const int *cam_index, const float *pixel_xy,
+                             const int *pixel_id, int64_t n, int jitter, unsigned long long seed,
+                             float *origins, float *dirs, float *jit, int *bad, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_eval_rays<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(cams, n_cams, cam_index, pixel_xy, pixel_id, n,
+                                                             jitter, seed, origins, dirs, jit, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss_adjoints(const float *rgb, const float *alpha, const float *target, const float *bg,
+                                 int64_t n, float scale, float *composited, float *resid, float *adj_rgb,
+                                 float *adj_alpha, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_loss_adjoints<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(rgb, alpha, target, bg, n, scale, composited,
+                                                                 resid, adj_rgb, adj_alpha);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, float *deltas, int64_t n_pay,
+                        int64_t n, unsigned m3, const AdamDev &c, int *bad, bool check, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+    if (check)
+        k_adam_check<<<blocks, 256, 0, st>>>(g, n, bad);
+    else
+        k_adam_update<<<blocks, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c);
+    return cudaGetLastError();
+}
+
+}  // namespace vpb

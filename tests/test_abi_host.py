@@ -97,3 +97,17 @@ def test_march_config_and_errors_mirror_reference():
     w = api.WindowParams()
     assert (w.alpha, w.beta) == (8.0, 8)  # primitive.h:14-17
     assert [int(x) for x in api.ErrorCategory] == [2, 3, 4, 5, 6, 7]  # errors.h:11-17 + device
+
+
+def test_pose_regularisers_bit_exact():
+    """lossVol / lossDel (losses.cpp:45-68) terms equal the reference evalLoss's."""
+    import ctypes as C
+    z = np.load(GOLDEN / "train.npz")
+    lib = _lib.load()
+    tr = np.ascontiguousarray(z["tr"], np.float32)
+    lv, ld = C.c_float(), C.c_float()
+    g = np.zeros(9 * tr.shape[0], np.float32)
+    assert lib.vp_loss_pose(tr.shape[0], tr.ctypes.data_as(_lib.f32p), float(z["weights"][2]),
+                            float(z["weights"][3]), C.byref(lv), C.byref(ld), g.ctypes.data_as(_lib.f32p)) == 0
+    assert bits(np.float32(lv.value)) == bits(z["terms"][2]) and bits(np.float32(ld.value)) == bits(z["terms"][3])
+    assert np.any(g != 0)

@@ -1,0 +1,67 @@
+"""GPU: the training rows — evalLoss's ray-batch driver (vp_eval_loss_pho + the host
+regularisers) and adamStep on the device — against the reference's own evalLoss / adamStep
+(tests/golden/train.npz, written by oracle/gen_golden.py)."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from golden_cases import sha
+from paper_2103_01954_b200 import api, synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def _z():
+    return np.load(GOLDEN / "train.npz")
+
+
+def test_eval_loss_matches_reference(renderer):
+    z = _z()
+    tr, pay = synthetic.shell_arrays(64, 8)
+    assert sha(pay) == str(z["payload_sha"])
+    scene = api.Scene(api.WindowParams(8.0, 8), frames=[api.Frame(z["tr"], api.PrimitiveSlab(64, 8, pay))])
+    cams = [api.Camera(c[:9].reshape(3, 3), c[9:18].reshape(3, 3), c[18:21], int(c[21]), int(c[22]))
+            for c in z["cams"]]
+    batch = api.RaySamples(z["cam_index"], z["pixel"], z["pixel_id"], z["target"], z["background"])
+    w = z["weights"]
+    weights = api.LossWeights(float(w[0]), float(w[1]), float(w[2]), float(w[3]))
+    c = z["cfg"]
+    cfg = api.MarchConfig(float(np.float32(c[0])), float(np.float32(c[1])), bool(c[2]), int(c[3]))
+    grads = np.zeros(api.grad_size(64, 8), np.float32)
+    terms = api.eval_loss(renderer, scene, 0, cams, batch, weights, cfg, grads)
+    # the forward is bit-exact, so the photometric term (summed on the host in batch order) is too
+    got = np.array([terms.pho, terms.geo, terms.vol, terms.del_], np.float32)
+    assert np.array_equal(bits(got), bits(z["terms"])), (got, z["terms"])
+    want = z["grads"]
+    err = np.abs(grads.astype(np.float64) - want)
+    assert np.all(err <= 2e-5 * np.abs(want).max() + 1e-4 * np.abs(want)), err.max()
+    # no gradient: the loss alone
+    terms2 = api.eval_loss(renderer, scene, 0, cams, batch, weights, cfg)
+    assert terms2.pho == terms.pho
+
+
+def test_adam_step_matches_reference(renderer):
+    z = _z()
+    m = int(z["adam_m"])
+    tr = np.ascontiguousarray(z["adam_tr_in"], np.float32).copy()
+    k = tr.shape[0]
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, z["adam_pay_in"]), api.WindowParams())
+    a = z["adam_cfg"]
+    cfg = api.AdamConfig(*[float(x) for x in a])
+    renderer._lib.vp_adam_reset(renderer.ctx)
+    for g in z["adam_grads"]:
+        api.adam_step(renderer, cfg, g, tr)
+    assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))
+    assert np.array_equal(bits(api.payload_planar(renderer)), bits(z["adam_pay_out"]))
+    # the refreshed composed transforms are those of the updated records
+    rects, *_ = renderer.debug_tiles(synthetic.shell_camera(-1, 0, 32))
+    bad = z["adam_grads"][0].copy()
+    bad[7] = np.nan
+    with pytest.raises(api.Error) as e:
+        api.adam_step(renderer, cfg, bad, tr)
+    assert e.value.category == api.ErrorCategory.NUMERIC
+    assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))  # nothing updated
