@@ -38,6 +38,9 @@ extern "C" {
 enum {
     VP_OK = 0,
     VP_ERR_USAGE = 2,   /* ErrorCategory::Usage   (errors.h:12) */
+    VP_ERR_IO = 3,      /* ErrorCategory::Io      (errors.h:13) */
+    VP_ERR_FORMAT = 4,  /* ErrorCategory::Format  (errors.h:14) */
+    VP_ERR_VERSION = 5, /* ErrorCategory::Version (errors.h:15) */
     VP_ERR_NUMERIC = 6, /* ErrorCategory::Numeric (errors.h:16) */
     VP_ERR_DEVICE = 7   /* CUDA / device failure (no reference counterpart) */
 };
@@ -108,6 +111,15 @@ int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15);
  * e.g. after an NCCL broadcast of the repacked buffer. Keeps the current transforms. */
 int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m,
                                const float *payload_interleaved);
+/* loadSlab (scene_io.cpp:43-66; VPSL format, README.md:96-104) straight into the device
+ * layout: the file is streamed through double-buffered pinned chunks, copied and repacked
+ * (K0) chunk by chunk, so the planar slab never exists whole in host or device memory.
+ * xf15 are the frame's composed transforms (n_prim must equal the file's K). Errors as the
+ * reference: VP_ERR_IO (cannot open), VP_ERR_FORMAT (magic, truncation, implausible header:
+ * K = 0 or > 2^20, M = 0 or > 512), VP_ERR_VERSION (version != 1). */
+int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf15,
+                 float window_alpha, int32_t window_beta);
+
 /* Device pointer / float count of the resident interleaved payload (for broadcasts). */
 int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats);
 /* Copy the resident interleaved payload to dst (host or device, K*M^3*4 floats). */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "vp_set_scene": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32]),
     "vp_set_transforms": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
     "vp_set_payload_interleaved": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p]),
+    "vp_load_slab": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, f32p, C.c_float, C.c_int32]),
     "vp_payload_device": (C.c_int, [C.c_void_p, C.POINTER(f32p), i64p]),
     "vp_copy_payload": (C.c_int, [C.c_void_p, f32p]),
     "vp_kernel_times": (C.c_int, [C.c_void_p, C.c_int64, f32p, i64p]),

@@ -267,6 +267,17 @@ class Renderer:
         fr = scene.frames[frame]
         self.set_scene_composed(fr.composed(), fr.slab, scene.window)
 
+    def load_slab(self, path: str, xf15: np.ndarray, window: WindowParams):
+        """loadSlab (scene_io.cpp:43-66) streamed straight into the device layout; xf15 are the
+        frame's composed transforms. Raises Error(IO / FORMAT / VERSION) like the reference."""
+        xf = _f32(xf15).reshape(-1, 15)
+        _check(self._lib.vp_load_slab(self._ctx, str(path).encode(), xf.shape[0], _fptr(xf),
+                                      float(window.alpha), int(window.beta)), self._ctx)
+        self.n_prim = xf.shape[0]
+        with open(path, "rb") as f:
+            f.seek(12)
+            self.m = int(np.frombuffer(f.read(4), "<u4")[0])
+
     def set_transforms(self, xf15: np.ndarray):
         xf = _f32(xf15).reshape(-1, 15)
         _check(self._lib.vp_set_transforms(self._ctx, xf.shape[0], _fptr(xf)), self._ctx)

@@ -817,6 +817,67 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     return vp_backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate);
 }
 
+int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf15,
+                 float window_alpha, int32_t window_beta) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (!path) return fail(ctx, VP_ERR_USAGE, "null path");
+    std::FILE *f = std::fopen(path, "rb");
+    if (!f) return fail(ctx, VP_ERR_IO, std::string("cannot open slab: ") + path);  // scene_io.cpp:44
+    struct Closer {
+        std::FILE *f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "VPSL", 4) != 0)
+        return fail(ctx, VP_ERR_FORMAT, std::string("bad slab magic: ") + path);
+    uint32_t header[3];
+    if (std::fread(header, 4, 3, f) != 3)
+        return fail(ctx, VP_ERR_FORMAT, std::string("truncated slab header: ") + path);
+    if (header[0] != 1)
+        return fail(ctx, VP_ERR_VERSION, "unsupported slab version " + std::to_string(header[0]));
+    if (header[1] == 0 || header[2] == 0 || header[1] > (1u << 20) || header[2] > 512)
+        return fail(ctx, VP_ERR_FORMAT, std::string("implausible slab header: ") + path);
+    const int k = int(header[1]), m = int(header[2]);
+    if (n_prim != k) return fail(ctx, VP_ERR_USAGE, "slab primitive count does not match the transforms");
+    // transforms first (validates the scales), payload buffer allocated, filled below
+    if (int rc = vp_set_scene(ctx, k, m, xf15, nullptr, window_alpha, window_beta)) return rc;
+    ctx->has_scene = false;  // until the payload is complete
+    const size_t m3 = size_t(m) * m * m, per_prim = 4 * m3;
+    const size_t chunk_prims = std::max<size_t>(1, (size_t(64) << 20) / (per_prim * 4));
+    float *pinned[2] = {nullptr, nullptr};
+    DBuf<float> dev[2];
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    struct PinnedFree {
+        float **p;
+        cudaEvent_t *e;
+        ~PinnedFree() {
+            for (int i = 0; i < 2; ++i) {
+                if (e[i]) cudaEventSynchronize(e[i]), cudaEventDestroy(e[i]);
+                if (p[i]) cudaFreeHost(p[i]);
+            }
+        }
+    } pf{pinned, done};
+    for (int i = 0; i < 2; ++i) {
+        VP_CUDA(ctx, cudaMallocHost(&pinned[i], chunk_prims * per_prim * 4));
+        VP_CUDA(ctx, dev[i].ensure(chunk_prims * per_prim));
+        VP_CUDA(ctx, cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    // double-buffered: read chunk i+1 from the file while chunk i is copied and repacked
+    int slot = 0;
+    for (size_t k0 = 0; k0 < size_t(k); k0 += chunk_prims, slot ^= 1) {
+        const size_t nk = std::min(chunk_prims, size_t(k) - k0), nf = nk * per_prim;
+        VP_CUDA(ctx, cudaEventSynchronize(done[slot]));  // the slot's previous copy finished
+        if (std::fread(pinned[slot], 4, nf, f) != nf)
+            return fail(ctx, VP_ERR_FORMAT, std::string("truncated slab payload: ") + path);
+        VP_CUDA(ctx, cudaMemcpyAsync(dev[slot].p, pinned[slot], nf * 4, cudaMemcpyHostToDevice, ctx->stream));
+        VP_CUDA(ctx, launch_repack(dev[slot].p, ctx->payload.p + k0 * m3, int64_t(nk), int64_t(m3), ctx->stream));
+        VP_CUDA(ctx, cudaEventRecord(done[slot], ctx->stream));
+    }
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->has_scene = true;
+    return VP_OK;
+}
+
 int vp_adam_reset(vp_ctx *ctx) {
     if (int rc = check_ctx(ctx, false)) return rc;
     ctx->adam_m1.release();

@@ -65,3 +65,43 @@ def test_adam_step_matches_reference(renderer):
         api.adam_step(renderer, cfg, bad, tr)
     assert e.value.category == api.ErrorCategory.NUMERIC
     assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))  # nothing updated
+
+
+def _write_vpsl(path, k, m, payload, version=1, magic=b"VPSL", truncate=0):
+    """README.md:96-104: magic, u32 version, u32 K, u32 M, f32 payload (little-endian)."""
+    data = magic + np.array([version, k, m], "<u4").tobytes() + np.asarray(payload, "<f4").tobytes()
+    with open(path, "wb") as f:
+        f.write(data[:len(data) - truncate] if truncate else data)
+
+
+def test_vpsl_loader_streams_into_the_device_layout(renderer, tmp_path):
+    tr, pay = synthetic.shell_arrays(512, 8)
+    xf = api.compose(tr)
+    p = tmp_path / "shell.vpsl"
+    _write_vpsl(p, 512, 8, pay)
+    renderer.load_slab(str(p), xf, api.WindowParams())
+    assert np.array_equal(bits(api.payload_planar(renderer)), bits(pay))
+    cam = synthetic.shell_camera(5, 64, 128)
+    a = renderer.render(cam, api.MarchConfig())
+    renderer.set_scene_composed(xf, api.PrimitiveSlab(512, 8, pay), api.WindowParams())
+    b = renderer.render(cam, api.MarchConfig())
+    assert np.array_equal(bits(a.color), bits(b.color)) and np.array_equal(a.sample_counts, b.sample_counts)
+
+
+@pytest.mark.parametrize("kind,category", [("missing", 3), ("magic", 4), ("version", 5), ("truncated", 4),
+                                           ("implausible", 4)])
+def test_vpsl_loader_errors_mirror_the_reference(renderer, tmp_path, kind, category):
+    tr, pay = synthetic.shell_arrays(8, 4)
+    xf = api.compose(tr)
+    p = tmp_path / "bad.vpsl"
+    if kind == "magic":
+        _write_vpsl(p, 8, 4, pay, magic=b"VPSX")
+    elif kind == "version":
+        _write_vpsl(p, 8, 4, pay, version=2)
+    elif kind == "truncated":
+        _write_vpsl(p, 8, 4, pay, truncate=7)
+    elif kind == "implausible":
+        _write_vpsl(p, 8, 513, pay)
+    with pytest.raises(api.Error) as e:
+        renderer.load_slab(str(p), xf, api.WindowParams())
+    assert int(e.value.category) == category
