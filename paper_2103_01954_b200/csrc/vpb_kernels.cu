@@ -199,20 +199,23 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
         order[atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u)] = (uint32_t)t;
 }
 
-// K3a: scatter keys into buckets. Order inside a bucket is arbitrary here; K3b makes it
-// canonical.
+// K3a: scatter keys into buckets, one warp per primitive: the lanes claim the slots of the
+// primitive's tiles in parallel (a thread per primitive would chain its atomics' round trips).
+// Order inside a bucket is arbitrary here; K3b makes it canonical.
 __global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
                        int n_prim, int tiles_x, uint32_t *__restrict__ cursor,
                        unsigned long long *__restrict__ entries, const DevCounters *ctr) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (k >= n_prim || ctr->key_overflow) return;
     const int4 rc = rects[k];
+    const int w = rc.z - rc.x + 1, h = rc.w - rc.y + 1;
+    if (w <= 0 || h <= 0) return;
     const unsigned long long e = ((unsigned long long)keys[k] << 32) | (uint32_t)k;
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-        for (int tx = rc.x; tx <= rc.z; ++tx) {
-            const uint32_t pos = atomicAdd(&cursor[ty * tiles_x + tx], 1u);
-            entries[pos] = e;
-        }
+    for (int q = lane; q < w * h; q += 32) {
+        const int ty = rc.y + q / w, tx = rc.x + q % w;
+        entries[atomicAdd(&cursor[ty * tiles_x + tx], 1u)] = e;
+    }
 }
 
 // K3b: sort each bucket ascending by (depth bits, prim). All-ascending bitonic network
@@ -543,7 +546,7 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
     if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
     k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity);
-    if (n_prim > 0) k_emit<<<(n_prim + 127) / 128, 128, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
+    if (n_prim > 0) k_emit<<<(unsigned)((n_prim * 32ll + 255) / 256), 256, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
     k_tile_sort<<<n_tiles, 128, 0, st>>>(offsets, entries, ctr);
     return cudaGetLastError();
 }
