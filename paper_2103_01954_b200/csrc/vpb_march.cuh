@@ -168,7 +168,10 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
     int nxt = 0, j = 0;
     unsigned act = 0;
     float nextE = t0, minX = kInf;
-    long long i = 0;
+    // The lattice index is the reference's int64; a ray needing more than 2^30 steps (which
+    // the reference would take hours to walk) is reported as Numeric instead.
+    constexpr int kMaxStep = 1 << 30;
+    int i = 0;
     float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
     float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
     V3 pw = o;
@@ -176,11 +179,11 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
     for (;;) {
         if (!sampling) {
             for (;;) {  // next lattice step with a non-empty active set
-                if (i > (1ll << 40)) {  // the reference would spin; report instead of hanging
+                if (i > kMaxStep) {
                     out.numeric = 1;
                     goto done;
                 }
-                ts = t0 + (__ll2float_rn(i) + jit) * dt;
+                ts = t0 + (__int2float_rn(i) + jit) * dt;
                 if (ts >= minX) {  // retirement (march.cpp:39-41)
                     minX = kInf;
                     for (unsigned m = act; m; m &= m - 1) {
@@ -234,7 +237,8 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
                 }
                 if (nxt >= cnt) goto done;  // active set empty, nothing left: march.cpp:43-44
                 // gap skip to the next entry (march.cpp:45-49)
-                const long long skipTo = (long long)ceil((double)((nextE - t0) / dt) - (double)jit);
+                const double sk = ceil((double)((nextE - t0) / dt) - (double)jit);
+                const int skipTo = sk > (double)kMaxStep ? kMaxStep + 1 : (int)sk;
                 i = skipTo > i + 1 ? skipTo : i + 1;
             }
             sampling = true;

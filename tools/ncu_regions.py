@@ -19,18 +19,19 @@ MARKERS = [("vpb_device.cuh", r"^__device__ __forceinline__ V3 mk3", "vec/mat op
            ("vpb_device.cuh", r"^// glibc 2.39 expf", "expf (binary64 port)"),
            ("vpb_device.cuh", r"^// primitive.cpp:12-22", "window/pow8/clamp"),
            ("vpb_device.cuh", r"^// One primitive-sample", "sample_primitive (stencil+gather)"),
-           ("vpb_kernels.cu", r"^// Candidate sources", "candidate accessors"),
-           ("vpb_kernels.cu", r"^// Per-ray sorted segment window storage", "window accessors"),
-           ("vpb_kernels.cu", r"^__device__ __forceinline__ bool key_less", "window insert/scan"),
-           ("vpb_kernels.cu", r"^// The fused quadrature", "march loop control"),
-           ("vpb_kernels.cu", r"^__device__ __forceinline__ void write_pixel", "outputs/counters"),
+           ("vpb_march.cuh", r"^// Candidate sources", "candidate accessors"),
+           ("vpb_march.cuh", r"^// Per-ray sorted segment window", "window accessors"),
+           ("vpb_march.cuh", r"^__device__ __forceinline__ bool key_less", "window insert/scan"),
+           ("vpb_march.cuh", r"^// The fused quadrature", "march loop control"),
+           ("vpb_march.cuh", r"^// Generic variant for windows wider", "march loop (generic)"),
+           ("vpb_march.cuh", r"^__device__ __forceinline__ void write_pixel", "outputs/counters"),
            ("vpb_kernels.cu", r"^// K5: one CTA", "tile kernel body"),
            ("vpb_kernels.cu", r"^// K5b", "end")]
 
 
 def ranges():
     out = []
-    for f in ("vpb_device.cuh", "vpb_kernels.cu"):
+    for f in ("vpb_device.cuh", "vpb_march.cuh", "vpb_kernels.cu"):
         lines = open(SRC + f).read().splitlines()
         marks = []
         for ff, pat, name in MARKERS:
