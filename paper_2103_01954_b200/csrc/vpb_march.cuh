@@ -146,9 +146,11 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
 // The reference's `ts >= tMax` break is implied: it only fires once every segment is
 // admitted and retired, where the empty-active-set branch breaks on the same step.
 //
-// Events are tracked in registers: nextE = tEnter of the next pending entry, minX = the
-// earliest exit among live entries. A step touches the window (shared memory) only when
-// ts reaches one of them, so most steps cost a compare.
+// Retirement for step i+1 is decided while step i is sampled: each sampled entry's exit is
+// compared with ts(i+1) (the same expression step i+1 evaluates), so the check runs in the
+// converged sampling code instead of a divergent per-step scan. An entry admitted at step
+// i+1 is checked against ts(i+1) on admission. nextE caches tEnter of the next pending
+// entry; admission touches the window only when ts reaches it.
 //
 // The loop is flattened to one primitive-sample per iteration: a lane first finds its next
 // lattice step with a non-empty active set, then evaluates one active primitive; the step's
@@ -166,14 +168,14 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
     const float dt = mp.dt;
     const float t0 = w.E(0);
     int nxt = 0, j = 0;
-    unsigned act = 0;
-    float nextE = t0, minX = kInf;
+    unsigned act = 0, retire = 0;
+    float nextE = t0;
     // The lattice index is the reference's int64; a ray needing more than 2^30 steps (which
     // the reference would take hours to walk) is reported as Numeric instead.
     constexpr int kMaxStep = 1 << 30;
     int i = 0;
     float transmittance = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    float ts = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+    float ts = 0.f, tsNext = 0.f, sigmaSum = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
     V3 pw = o;
     bool sampling = false;
     for (;;) {
@@ -184,23 +186,10 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
                     goto done;
                 }
                 ts = t0 + (__int2float_rn(i) + jit) * dt;
-                if (ts >= minX) {  // retirement (march.cpp:39-41)
-                    minX = kInf;
-                    for (unsigned m = act; m; m &= m - 1) {
-                        const int q = __ffs(m) - 1;
-                        const float x = w.X(q);
-                        if (x <= ts) act &= ~(1u << q);
-                        else minX = fminf(minX, x);
-                    }
-                }
                 if (nxt < cnt ? nextE <= ts : more) {  // admission (march.cpp:38), with refill
                     for (;;) {
                         while (nxt < cnt && nextE <= ts) {
-                            const float x = w.X(nxt);
-                            if (x > ts) {  // admitted and not retired in the same step
-                                act |= 1u << nxt;
-                                minX = fminf(minX, x);
-                            }
+                            if (w.X(nxt) > ts) act |= 1u << nxt;  // else admitted and retired at once
                             ++nxt;
                             nextE = nxt < cnt ? w.E(nxt) : kInf;
                         }
@@ -244,6 +233,8 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
             sampling = true;
             sigmaSum = 0.f;
             rw = gw = bw = 0.f;
+            retire = 0;
+            tsNext = t0 + (__int2float_rn(i + 1) + jit) * dt;
             pw = o + d * ts;
         }
         {  // one primitive-sample (march.cpp:63-70)
@@ -256,6 +247,7 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
             gw += g * sg;
             bw += b * sg;
             ++out.prim_samples;
+            if (w.X(j) <= tsNext) retire |= 1u << j;  // retirement at step i+1 (march.cpp:39-41)
         }
         const unsigned rest = act & ~((2u << j) - 1u);
         if (rest) {
@@ -264,6 +256,7 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
         }
         // step complete: march.cpp:71-88
         sampling = false;
+        act &= ~retire;
         ++out.samples;
         const float dT = sigmaSum * dt;
         if (transmittance + dT >= 1.0f) {
