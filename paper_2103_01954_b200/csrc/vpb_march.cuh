@@ -146,11 +146,13 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
 // The reference's `ts >= tMax` break is implied: it only fires once every segment is
 // admitted and retired, where the empty-active-set branch breaks on the same step.
 //
-// Retirement for step i+1 is decided while step i is sampled: each sampled entry's exit is
-// compared with ts(i+1) (the same expression step i+1 evaluates), so the check runs in the
-// converged sampling code instead of a divergent per-step scan. An entry admitted at step
-// i+1 is checked against ts(i+1) on admission. nextE caches tEnter of the next pending
-// entry; admission touches the window only when ts reaches it.
+// Retirement and admission for step i+1 are decided while step i is sampled: each sampled
+// entry's exit is compared with ts(i+1) (the same expression step i+1 evaluates), and each
+// sample iteration admits at most one pending entry with tEnter <= ts(i+1) (checking its
+// exit against ts(i+1) as the reference's same-step removal does). This runs in the
+// converged sampling code instead of divergent per-step scans; the per-step admission loop
+// below only picks up what the folded admission left (and refills the window). nextE caches
+// tEnter of the next pending entry.
 //
 // The loop is flattened to one primitive-sample per iteration: a lane first finds its next
 // lattice step with a non-empty active set, then evaluates one active primitive; the step's
@@ -168,7 +170,7 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
     const float dt = mp.dt;
     const float t0 = w.E(0);
     int nxt = 0, j = 0;
-    unsigned act = 0, retire = 0;
+    unsigned act = 0, retire = 0, admit = 0;
     float nextE = t0;
     // The lattice index is the reference's int64; a ray needing more than 2^30 steps (which
     // the reference would take hours to walk) is reported as Numeric instead.
@@ -248,6 +250,11 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
             bw += b * sg;
             ++out.prim_samples;
             if (w.X(j) <= tsNext) retire |= 1u << j;  // retirement at step i+1 (march.cpp:39-41)
+            if (nxt < cnt && nextE <= tsNext) {  // admission at step i+1, one entry per sample
+                if (w.X(nxt) > tsNext) admit |= 1u << nxt;
+                ++nxt;
+                nextE = nxt < cnt ? w.E(nxt) : kInf;
+            }
         }
         const unsigned rest = act & ~((2u << j) - 1u);
         if (rest) {
@@ -256,7 +263,8 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
         }
         // step complete: march.cpp:71-88
         sampling = false;
-        act &= ~retire;
+        act = (act & ~retire) | admit;
+        admit = 0;
         ++out.samples;
         const float dT = sigmaSum * dt;
         if (transmittance + dT >= 1.0f) {
