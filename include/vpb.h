@@ -207,6 +207,12 @@ int vp_composite(vp_ctx *ctx, int32_t width, int32_t height, const float *rgb,
 int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *depth_key,
                    int32_t *tile_offsets, int32_t *tile_prims, int64_t cap, int64_t *n_keys);
 
+/* Profiling hook: renders the view with a per-CTA timeline of the raymarch kernel; out gets
+ * 4 uint64 per CTA in launch order: tile index, SM id, start and end (%globaltimer ns).
+ * *n_out receives the CTA count (= tiles). */
+int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, uint64_t *out,
+                        int64_t cap, int64_t *n_out);
+
 /* Test hook: evaluates the device port of glibc expf used by window() (primitive.cpp:27)
  * elementwise, so the port can be checked exhaustively against the host libm. */
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y);

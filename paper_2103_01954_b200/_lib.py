@@ -79,6 +79,8 @@ SIGNATURES = {
     "vp_composite": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]),
     "vp_debug_tiles": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), i32p, u32p, i32p, i32p,
                                  C.c_int64, i64p]),
+    "vp_debug_tile_times": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march),
+                                      C.POINTER(C.c_uint64), C.c_int64, i64p]),
     "vp_debug_expf": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p]),
     "vp_make_shell_scene": (C.c_int, [C.c_int32, C.c_int32, f32p, f32p]),
     "vp_look_at_camera": (C.c_int, [f32p, f32p, f32p, C.c_float, C.c_int32, C.c_int32,

@@ -817,6 +817,29 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     return vp_backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate);
 }
 
+int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, uint64_t *out,
+                        int64_t cap, int64_t *n_out) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_cam(ctx, cam)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    const CamDev cd = make_cam(*cam);
+    const size_t n_tiles = size_t(cd.tiles_x) * cd.tiles_y, n_px = size_t(cam->width) * cam->height;
+    if (n_out) *n_out = int64_t(n_tiles);
+    if (n_px == 0 || ctx->n_prim == 0) return VP_OK;
+    if (int rc = ensure_render_buffers(ctx, cd)) return rc;
+    VP_CUDA(ctx, ctx->out_rgb.ensure(3 * n_px));
+    VP_CUDA(ctx, ctx->out_alpha.ensure(n_px));
+    DBuf<unsigned long long> prof;
+    VP_CUDA(ctx, prof.ensure(4 * n_tiles));
+    OutDev od{ctx->out_rgb.p, ctx->out_alpha.p, nullptr};
+    od.prof = prof.p;
+    if (int rc = enqueue_render(ctx, cd, make_march(ctx, cfg), od, ctx->stream)) return rc;
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (out && cap > 0)
+        VP_CUDA(ctx, cudaMemcpy(out, prof.p, 8 * std::min<size_t>(size_t(cap), 4 * n_tiles), cudaMemcpyDeviceToHost));
+    return VP_OK;
+}
+
 int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf15,
                  float window_alpha, int32_t window_beta) {
     if (int rc = check_ctx(ctx, false)) return rc;

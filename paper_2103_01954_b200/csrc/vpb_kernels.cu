@@ -398,6 +398,8 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     const int n = (int)(offsets[tile + 1] - start);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     if (threadIdx.x < 32) sm.tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    unsigned long long t_start = 0;
+    if (od.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
     if (n <= kCandCap)
         march_tile<CAP, MT, true>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
@@ -405,6 +407,21 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     else
         march_tile<CAP, MT, false>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
                                    ovf_list, ovf_cap);
+    if (od.prof) {  // block-uniform: per-CTA timeline for load-balance analysis
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t_end, smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            unsigned s32;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
+            smid = s32;
+            unsigned long long *q = od.prof + 4 * (size_t)blockIdx.x;
+            q[0] = (unsigned long long)tile;
+            q[1] = smid;
+            q[2] = t_start;
+            q[3] = t_end;
+        }
+    }
 }
 
 // K5b: rays whose live segments overflowed the shared-memory window are re-marched with a

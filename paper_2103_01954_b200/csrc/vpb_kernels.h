@@ -30,6 +30,7 @@ struct OutDev {
     float *rgb;
     float *alpha;
     int *samples;
+    unsigned long long *prof = nullptr;  // per CTA: tile, SM id, start ns, end ns (debug)
 };
 
 struct RaysDev {
