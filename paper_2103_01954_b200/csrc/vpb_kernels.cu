@@ -371,7 +371,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
 #ifndef VPB_MARCH_MINB
 #define VPB_MARCH_MINB 3
 #endif
-template <int CAP, int MT>
+template <int CAP, int MT, bool PROF>
 __global__ void __launch_bounds__(kMarchThreads, VPB_MARCH_MINB)
 k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
               const int4 *__restrict__ prects, const float4 *__restrict__ payload,
@@ -399,7 +399,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     if (threadIdx.x < 32) sm.tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     unsigned long long t_start = 0;
-    if (od.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
     if (n <= kCandCap)
         march_tile<CAP, MT, true>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
@@ -407,7 +407,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     else
         march_tile<CAP, MT, false>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
                                    ovf_list, ovf_cap);
-    if (od.prof) {  // block-uniform: per-CTA timeline for load-balance analysis
+    if (PROF) {  // separate instantiation: per-CTA timeline for load-balance analysis
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned long long t_end, smid;
@@ -568,7 +568,7 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
     return cudaGetLastError();
 }
 
-template <int MT>
+template <int MT, bool PROF>
 static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const float *xf16,
                                   const int4 *prects, const float4 *payload, const uint32_t *offsets,
                                   const uint32_t *order, const unsigned long long *entries,
@@ -576,7 +576,7 @@ static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const f
                                   cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = march_tiles_smem();
-    auto kern = k_march_tiles<kWindowCap, MT>;
+    auto kern = k_march_tiles<kWindowCap, MT, PROF>;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -593,7 +593,8 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
                                const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                                cudaStream_t st) {
     if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
-#define VPB_TILES(MT) launch_tiles_m<MT>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st)
+#define VPB_TILES(MT) (od.prof ? launch_tiles_m<MT, true>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st) \
+                           : launch_tiles_m<MT, false>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st))
     switch (mp.m) {  // compile-time voxel counts for the common grids
     case 4: return VPB_TILES(4);
     case 8: return VPB_TILES(8);
