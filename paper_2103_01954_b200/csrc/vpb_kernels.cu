@@ -276,6 +276,7 @@ struct TileSmem {
     int *warp;         // kMarchThreads / 32
     float *we, *wx;    // CAP * kMarchThreads each
     void *wc;          // CAP * kMarchThreads window indices (uint8 or uint16)
+    unsigned *mask;    // kMaskWords * kMarchThreads per-ray candidate hit masks
 };
 
 template <int CAP, int MT, bool STAGED>
@@ -326,7 +327,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     if (valid && n > 0) {
         V3 rd, d;
         generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid};
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid, STAGED ? sm.mask : nullptr};
         window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
     sm.state[tid] = cnt | (more ? 256 : 0);
@@ -356,7 +357,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
         generate_ray(cam, (float)rp.x + 0.5f, (float)rp.y + 0.5f, rd, d);
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
         const int st = sm.state[r];
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r};
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r, STAGED ? sm.mask : nullptr};
         ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, sm.tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
@@ -391,6 +392,7 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     sm.we = reinterpret_cast<float *>(sm.warp + kMarchThreads / 32);
     sm.wx = sm.we + CAP * kMarchThreads;
     sm.wc = sm.wx + CAP * kMarchThreads;
+    sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + CAP * kMarchThreads);
 
     if (ctr->key_overflow) return;
     const int tile = (int)order[blockIdx.x];
@@ -537,7 +539,8 @@ constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared me
 
 size_t march_tiles_smem() {
     return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 * 2 + kCandCap * 4 + 32 * 8 +
-           kMarchThreads * 4 * 2 + (kMarchThreads / 32) * 4 + (size_t)kWindowCap * kMarchThreads * (8 + 2);
+           kMarchThreads * 4 * 2 + (kMarchThreads / 32) * 4 + (size_t)kWindowCap * kMarchThreads * (8 + 2) +
+           (size_t)kMaskWords * kMarchThreads * 4;
 }
 
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,

@@ -14,9 +14,10 @@ namespace vpb {
 constexpr int kTile = 16;
 constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
 #ifndef VPB_CAND_CAP
-#define VPB_CAND_CAP 192
+#define VPB_CAND_CAP 160
 #endif
 constexpr int kCandCap = VPB_CAND_CAP;  // candidates staged in shared memory per tile (<= 255)
+constexpr int kMaskWords = (kCandCap + 31) / 32;  // per-ray bitmask of the staged candidates hit
 
 // Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
 //
@@ -83,9 +84,11 @@ struct Window {
     float *x;
     IdxT *c;
     int stride, lane;
+    unsigned *m = nullptr;  // optional kMaskWords-word hit mask over the candidates
     __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
     __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
     __device__ __forceinline__ IdxT &C(int j) const { return c[j * stride + lane]; }
+    __device__ __forceinline__ unsigned &M(int word) const { return m[word * stride + lane]; }
 };
 
 struct RayOut {
@@ -125,14 +128,32 @@ __device__ __forceinline__ void window_insert(const Win &w, const Cands &cands, 
 }
 
 // Fills the window with the smallest hits whose key exceeds (lastE, lastP) (or all hits
-// when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order).
+// when first == true). The sorted list equals intersect()'s (lbvh.cpp:225-227 order); the
+// kept entries do not depend on the scan order. With a hit mask, the first scan records which
+// candidates hit and a refill re-tests only those (a refill is needed only by rays with more
+// hits than the window holds, which otherwise would re-test every candidate per refill).
 template <int CAP, class Cands, class Win>
 __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, int &cnt,
                                             bool &more, V3 o, V3 d, int2 px, bool first,
                                             float lastE, int lastP) {
+    if (!first && w.m) {
+        for (int word = 0; word < kMaskWords; ++word)
+            for (unsigned bits = w.M(word); bits; bits &= bits - 1) {
+                const int c = word * 32 + __ffs(bits) - 1;
+                float tE, tX;
+                cands.hit(c, o, d, tE, tX);  // hit before, same operations: hits again
+                const int prim = cands.prim(c);
+                if (!key_less(lastE, lastP, tE, prim)) continue;
+                window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
+            }
+        return;
+    }
+    if (first && w.m)
+        for (int word = 0; word < kMaskWords; ++word) w.M(word) = 0u;
     for (int c = 0; c < cands.n; ++c) {
         float tE, tX;
         if (!cands.covers(c, px) || !cands.hit(c, o, d, tE, tX)) continue;
+        if (first && w.m) w.M(c >> 5) |= 1u << (c & 31);
         const int prim = cands.prim(c);
         if (!first && !key_less(lastE, lastP, tE, prim)) continue;
         window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
