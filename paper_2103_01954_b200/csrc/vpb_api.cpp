@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -86,6 +87,10 @@ struct vp_ctx {
     int64_t t_count = 0;
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
     int64_t adam_step = 0;
+    // Raymarch configuration for the next render: the dense one (longer windows, 2 CTAs/SM)
+    // when the last render whose counters reached the host had long per-tile lists.
+    bool dense = false;
+    int tile_cfg = -1;  // VPB_TILE_CFG: -1 auto, 0 normal, 1 dense
 };
 
 namespace {
@@ -184,7 +189,8 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
     VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->prects.p, ctx->payload.p, ctx->offsets.p,
-                                    ctx->order.p, ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
+                                    ctx->order.p, ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
+                                    ctx->tile_cfg < 0 ? ctx->dense : ctx->tile_cfg == 1, st));
     const RaysDev none{nullptr, nullptr, nullptr};
     VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->prects.p, ctx->n_prim, ctx->payload.p,
                                        ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
@@ -193,6 +199,13 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
     ++ctx->t_count;
     return VP_OK;
+}
+
+// Mean candidates per non-empty tile above which the dense raymarch configuration is used.
+constexpr unsigned long long kDenseKeysPerTile = 40;
+
+void note_density(vp_ctx *ctx, const DevCounters &c) {
+    ctx->dense = c.nonempty_tiles > 0 && c.keys > kDenseKeysPerTile * c.nonempty_tiles;
 }
 
 void fill_stats(const DevCounters &c, float ms, vp_stats *s) {
@@ -252,6 +265,8 @@ int vp_create(int32_t device, vp_ctx **out) {
                                                 prop.name);
     vp_ctx *ctx = new vp_ctx();
     ctx->device = device;
+    if (const char *tc = std::getenv("VPB_TILE_CFG"))  // tuning override: normal | dense
+        ctx->tile_cfg = std::strcmp(tc, "dense") == 0 ? 1 : std::strcmp(tc, "normal") == 0 ? 0 : -1;
     int rc = VP_OK;
     if ((e = cudaSetDevice(device)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -446,6 +461,7 @@ int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
     if (int rc = check_ctx(ctx, false)) return rc;
     VP_CUDA(ctx, cudaMemcpy(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
     const DevCounters c = *ctx->h_ctr;
+    note_density(ctx, c);
     fill_stats(c, 0.f, stats);
     if (c.key_overflow) {
         ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
@@ -500,6 +516,7 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
         VP_CUDA(ctx, cudaStreamSynchronize(st));
         const DevCounters c = *ctx->h_ctr;
+        note_density(ctx, c);
         if (c.key_overflow) {  // grow the key buffer and run again
             ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
             continue;

@@ -175,7 +175,13 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
     // counting sort of the tiles by min(count, 1023), descending
     for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
     __syncthreads();
-    for (int t = tid; t < n_tiles; t += blockDim.x) atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u);
+    unsigned nonempty = 0;
+    for (int t = tid; t < n_tiles; t += blockDim.x) {
+        atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u);
+        nonempty += counts[t] > 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) nonempty += __shfl_down_sync(0xffffffffu, nonempty, o);
+    if (lane == 0 && nonempty) atomicAdd(&ctr->nonempty_tiles, (unsigned long long)nonempty);
     __syncthreads();
     if (wid == 0) {  // exclusive scan over buckets in descending order, 32 buckets per lane
         unsigned local = 0;
@@ -279,7 +285,7 @@ struct TileSmem {
     unsigned *mask;    // kMaskWords * kMarchThreads per-ray candidate hit masks
 };
 
-template <int CAP, int MT, bool STAGED>
+template <int CAP, int MT, bool STAGED, int CC>
 __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam, const MarchDev &mp,
                                            const float *__restrict__ xf_g,
                                            const int4 *__restrict__ prects,
@@ -327,7 +333,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     if (valid && n > 0) {
         V3 rd, d;
         generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid, STAGED ? sm.mask : nullptr};
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
         window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
     sm.state[tid] = cnt | (more ? 256 : 0);
@@ -357,7 +363,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
         generate_ray(cam, (float)rp.x + 0.5f, (float)rp.y + 0.5f, rd, d);
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
         const int st = sm.state[r];
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r, STAGED ? sm.mask : nullptr};
+        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
         ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, sm.tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
@@ -369,11 +375,8 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     add_counters(ctr, ro, live && !ro.overflow);
 }
 
-#ifndef VPB_MARCH_MINB
-#define VPB_MARCH_MINB 3
-#endif
-template <int CAP, int MT, bool PROF>
-__global__ void __launch_bounds__(kMarchThreads, VPB_MARCH_MINB)
+template <int CAP, int MT, bool PROF, int CC, int MINB>
+__global__ void __launch_bounds__(kMarchThreads, MINB)
 k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
               const int4 *__restrict__ prects, const float4 *__restrict__ payload,
               const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ order,
@@ -382,10 +385,10 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     extern __shared__ __align__(16) unsigned char smem[];
     TileSmem sm;
     sm.xf4 = reinterpret_cast<float4 *>(smem);
-    sm.om = sm.xf4 + kCandCap * 4;
-    sm.prect = reinterpret_cast<int4 *>(sm.om + kCandCap);
-    sm.prim = reinterpret_cast<int *>(sm.prect + kCandCap);
-    sm.tab = reinterpret_cast<unsigned long long *>(sm.prim + kCandCap);
+    sm.om = sm.xf4 + CC * 4;
+    sm.prect = reinterpret_cast<int4 *>(sm.om + CC);
+    sm.prim = reinterpret_cast<int *>(sm.prect + CC);
+    sm.tab = reinterpret_cast<unsigned long long *>(sm.prim + CC);
     sm.state = reinterpret_cast<int *>(sm.tab + 32);
     sm.list = sm.state + kMarchThreads;
     sm.warp = sm.list + kMarchThreads;
@@ -403,11 +406,11 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     unsigned long long t_start = 0;
     if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
-    if (n <= kCandCap)
-        march_tile<CAP, MT, true>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
+    if (n <= CC)
+        march_tile<CAP, MT, true, CC>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
                                   ovf_list, ovf_cap);
     else
-        march_tile<CAP, MT, false>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
+        march_tile<CAP, MT, false, CC>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
                                    ovf_list, ovf_cap);
     if (PROF) {  // separate instantiation: per-CTA timeline for load-balance analysis
         __syncthreads();
@@ -537,11 +540,25 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 #endif
 constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared memory)
 
-size_t march_tiles_smem() {
-    return (size_t)kCandCap * kXfStride * 4 + kCandCap * 16 * 2 + kCandCap * 4 + 32 * 8 +
-           kMarchThreads * 4 * 2 + (kMarchThreads / 32) * 4 + (size_t)kWindowCap * kMarchThreads * (8 + 2) +
-           (size_t)kMaskWords * kMarchThreads * 4;
+// Two raymarch configurations. Normal: 20-entry windows, 160 staged candidates, 3 CTAs/SM.
+// Dense (long per-tile lists, many segments per ray; chosen from the previous render's mean
+// candidates per non-empty tile): 28-entry windows, 192 staged candidates, 2 CTAs/SM. The
+// 28-entry windows avoid window refills, which sit on the critical path of the heaviest
+// tiles there.
+struct TileCfgNormal {
+    static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = 3;
+};
+struct TileCfgDense {
+    static constexpr int CAP = 28, CC = 192, MINB = 2;
+};
+
+template <int CAP, int CC>
+static size_t tiles_smem() {
+    return (size_t)CC * kXfStride * 4 + CC * 16 * 2 + CC * 4 + 32 * 8 + kMarchThreads * 4 * 2 +
+           (kMarchThreads / 32) * 4 + (size_t)CAP * kMarchThreads * (8 + 2) +
+           (size_t)((CC + 31) / 32) * kMarchThreads * 4;
 }
+size_t march_tiles_smem() { return tiles_smem<TileCfgNormal::CAP, TileCfgNormal::CC>(); }
 
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
                           cudaStream_t st) {
@@ -571,15 +588,15 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
     return cudaGetLastError();
 }
 
-template <int MT, bool PROF>
+template <class Cfg, int MT, bool PROF>
 static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const float *xf16,
                                   const int4 *prects, const float4 *payload, const uint32_t *offsets,
                                   const uint32_t *order, const unsigned long long *entries,
                                   const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                                   cudaStream_t st) {
     static bool attr_set = false;
-    const size_t smem = march_tiles_smem();
-    auto kern = k_march_tiles<kWindowCap, MT, PROF>;
+    const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC>();
+    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB>;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -590,14 +607,14 @@ static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const f
     return cudaGetLastError();
 }
 
-cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                               const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                               const uint32_t *order, const unsigned long long *entries,
-                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               cudaStream_t st) {
-    if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
-#define VPB_TILES(MT) (od.prof ? launch_tiles_m<MT, true>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st) \
-                           : launch_tiles_m<MT, false>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st))
+template <class Cfg>
+static cudaError_t launch_tiles_cfg(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                                    const int4 *prects, const float4 *payload, const uint32_t *offsets,
+                                    const uint32_t *order, const unsigned long long *entries,
+                                    const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                                    cudaStream_t st) {
+#define VPB_TILES(MT) (od.prof ? launch_tiles_m<Cfg, MT, true>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st) \
+                           : launch_tiles_m<Cfg, MT, false>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st))
     switch (mp.m) {  // compile-time voxel counts for the common grids
     case 4: return VPB_TILES(4);
     case 8: return VPB_TILES(8);
@@ -606,6 +623,19 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
     default: return VPB_TILES(0);
     }
 #undef VPB_TILES
+}
+
+cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
+                               const int4 *prects, const float4 *payload, const uint32_t *offsets,
+                               const uint32_t *order, const unsigned long long *entries,
+                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+                               bool dense, cudaStream_t st) {
+    if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
+    if (dense)
+        return launch_tiles_cfg<TileCfgDense>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
+                                              ovf_list, ovf_cap, st);
+    return launch_tiles_cfg<TileCfgNormal>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
+                                           ovf_list, ovf_cap, st);
 }
 
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,

@@ -13,7 +13,7 @@ namespace vpb {
 
 struct DevCounters {
     unsigned long long ray_samples, prim_samples, hit_rays, early_exits, saturated;
-    unsigned long long overflow_rays, refills, keys, numeric_fail;
+    unsigned long long overflow_rays, refills, keys, numeric_fail, nonempty_tiles;
     int key_overflow;
     int fallback_fail;
 };
@@ -76,7 +76,7 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
                                const int4 *prects, const float4 *payload, const uint32_t *offsets,
                                const uint32_t *order, const unsigned long long *entries,
                                const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               cudaStream_t st);
+                               bool dense, cudaStream_t st);
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
                                   const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
                                   const uint32_t *offsets, const unsigned long long *entries,

@@ -17,7 +17,6 @@ constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
 #define VPB_CAND_CAP 160
 #endif
 constexpr int kCandCap = VPB_CAND_CAP;  // candidates staged in shared memory per tile (<= 255)
-constexpr int kMaskWords = (kCandCap + 31) / 32;  // per-ray bitmask of the staged candidates hit
 
 // Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
 //
@@ -84,7 +83,8 @@ struct Window {
     float *x;
     IdxT *c;
     int stride, lane;
-    unsigned *m = nullptr;  // optional kMaskWords-word hit mask over the candidates
+    unsigned *m = nullptr;  // optional per-ray hit mask over the candidates (mw words)
+    int mw = 0;
     __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
     __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
     __device__ __forceinline__ IdxT &C(int j) const { return c[j * stride + lane]; }
@@ -137,7 +137,7 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
                                             bool &more, V3 o, V3 d, int2 px, bool first,
                                             float lastE, int lastP) {
     if (!first && w.m) {
-        for (int word = 0; word < kMaskWords; ++word)
+        for (int word = 0; word < w.mw; ++word)
             for (unsigned bits = w.M(word); bits; bits &= bits - 1) {
                 const int c = word * 32 + __ffs(bits) - 1;
                 float tE, tX;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
         return;
     }
     if (first && w.m)
-        for (int word = 0; word < kMaskWords; ++word) w.M(word) = 0u;
+        for (int word = 0; word < w.mw; ++word) w.M(word) = 0u;
     for (int c = 0; c < cands.n; ++c) {
         float tE, tX;
         if (!cands.covers(c, px) || !cands.hit(c, o, d, tE, tX)) continue;

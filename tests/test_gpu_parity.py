@@ -67,6 +67,27 @@ def test_full_size_render_digest(renderer, key):
     assert out.stats["ray_samples"] == d["total_samples"]
 
 
+@pytest.mark.parametrize("tile_cfg", ["normal", "dense"])
+@pytest.mark.parametrize("key", ["k32768_m8_1024_view-1", "k4096_m16_1024_view-1", "oracle_64x16_256_view-1"])
+def test_full_size_digest_under_each_tile_config(monkeypatch, key, tile_cfg):
+    """Both raymarch configurations (normal: 20-entry windows, 3 CTAs/SM; dense: 28-entry
+    windows, 192 staged candidates, 2 CTAs/SM) are bit-exact on every scene density."""
+    from paper_2103_01954_b200 import Renderer
+    monkeypatch.setenv("VPB_TILE_CFG", tile_cfg)
+    d = DIGESTS["renders"][key]
+    tr, pay = synthetic.shell_arrays(d["K"], d["M"])
+    r = Renderer(0)
+    try:
+        r.set_scene_composed(api.compose(tr), api.PrimitiveSlab(d["K"], d["M"], pay), api.WindowParams())
+        out = r.render(synthetic.shell_camera(d["view"], d["n_views"], d["W"]), api.MarchConfig())
+    finally:
+        r.close()
+    assert out.total_samples() == d["total_samples"]
+    assert sha(out.sample_counts) == d["samples"]
+    assert sha(out.alpha) == d["alpha"]
+    assert sha(out.color) == d["rgb"]
+
+
 def test_march_kats_match_reference(renderer):
     """test_march.cpp:50-194 scenarios plus random rays, through vp_march_rays."""
     for name, g in load_groups("march_kats").items():

@@ -6,7 +6,7 @@ import os
 import subprocess
 import sys
 
-CFGS = [[], ["--k", "32768", "--m", "8"], ["--k", "64", "--m", "16", "--width", "256"]]
+CFGS = [[], ["--k", "32768", "--m", "8"], ["--k", "512", "--m", "32"], ["--k", "64", "--m", "16", "--width", "256"]]
 libs = sys.argv[1:] or sorted(glob.glob("build/variants/libvpb_*.so"))
 for lib in libs:
     env = dict(os.environ, VPB_LIB=os.path.abspath(lib))
