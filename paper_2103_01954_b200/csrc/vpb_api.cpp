@@ -87,10 +87,10 @@ struct vp_ctx {
     int64_t t_count = 0;
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
     int64_t adam_step = 0;
-    // Raymarch configuration for the next render: the dense one (longer windows, 2 CTAs/SM)
-    // when the last render whose counters reached the host had long per-tile lists.
-    bool dense = false;
-    int tile_cfg = -1;  // VPB_TILE_CFG: -1 auto, 0 normal, 1 dense
+    // Raymarch configuration for the next render, from the mean candidates per non-empty tile
+    // of the last render whose counters reached the host (see note_density).
+    TileTier tier = TileTier::Normal;
+    int tile_cfg = -1;  // VPB_TILE_CFG override: -1 auto, else a TileTier
 };
 
 namespace {
@@ -190,7 +190,7 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
     VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->prects.p, ctx->payload.p, ctx->offsets.p,
                                     ctx->order.p, ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
-                                    ctx->tile_cfg < 0 ? ctx->dense : ctx->tile_cfg == 1, st));
+                                    ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     const RaysDev none{nullptr, nullptr, nullptr};
     VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->prects.p, ctx->n_prim, ctx->payload.p,
                                        ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
@@ -201,11 +201,15 @@ int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const Out
     return VP_OK;
 }
 
-// Mean candidates per non-empty tile above which the dense raymarch configuration is used.
-constexpr unsigned long long kDenseKeysPerTile = 40;
+// Mean candidates per non-empty tile: up to 14 -> Light, up to 40 -> Normal, else Dense
+// (thresholds between the BASELINE configs' 11, 22 and 66; vpb_kernels.cu TileCfg*).
+constexpr unsigned long long kLightKeysPerTile = 14, kDenseKeysPerTile = 40;
 
 void note_density(vp_ctx *ctx, const DevCounters &c) {
-    ctx->dense = c.nonempty_tiles > 0 && c.keys > kDenseKeysPerTile * c.nonempty_tiles;
+    if (c.nonempty_tiles == 0) return;
+    ctx->tier = c.keys > kDenseKeysPerTile * c.nonempty_tiles  ? TileTier::Dense
+                : c.keys > kLightKeysPerTile * c.nonempty_tiles ? TileTier::Normal
+                                                                : TileTier::Light;
 }
 
 void fill_stats(const DevCounters &c, float ms, vp_stats *s) {
@@ -265,8 +269,11 @@ int vp_create(int32_t device, vp_ctx **out) {
                                                 prop.name);
     vp_ctx *ctx = new vp_ctx();
     ctx->device = device;
-    if (const char *tc = std::getenv("VPB_TILE_CFG"))  // tuning override: normal | dense
-        ctx->tile_cfg = std::strcmp(tc, "dense") == 0 ? 1 : std::strcmp(tc, "normal") == 0 ? 0 : -1;
+    if (const char *tc = std::getenv("VPB_TILE_CFG"))  // tuning override: light | normal | dense
+        ctx->tile_cfg = std::strcmp(tc, "light") == 0    ? int(TileTier::Light)
+                        : std::strcmp(tc, "normal") == 0 ? int(TileTier::Normal)
+                        : std::strcmp(tc, "dense") == 0  ? int(TileTier::Dense)
+                                                         : -1;
     int rc = VP_OK;
     if ((e = cudaSetDevice(device)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||

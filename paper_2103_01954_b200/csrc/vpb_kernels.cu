@@ -264,25 +264,25 @@ __global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
 
 // ----------------------------------------------------------------------------------------
 // K5: one CTA per 16x16 tile, heaviest tiles first (`order` from k_scan).
-//   staging  the tile's candidates -> shared memory (tiles with n <= kCandCap)
+//   staging  the tile's candidates -> shared memory (tiles with n <= CC)
 //   phase 1  every pixel: generateRay + exact segment window over the candidates
 //   compact  rays with a non-empty window, in pixel order (misses write zeros and retire)
 //   phase 2  the first n_hit threads march the hit rays, so warps are full of live rays
-// Tiles with more than kCandCap candidates take the same path with TileCands<false>
+// Tiles with more than CC candidates take the same path with TileCands<false>
 // (candidates read from global memory, 16-bit window indices); tiles beyond 65535
 // candidates send every pixel to the fallback re-march.
 struct TileSmem {
-    float4 *xf4;       // kCandCap * 4
-    float4 *om;        // kCandCap
-    int4 *prect;       // kCandCap
-    int *prim;         // kCandCap
+    float4 *xf4;       // CC * 4
+    float4 *om;        // CC
+    int4 *prect;       // CC
+    int *prim;         // CC
     unsigned long long *tab;  // 32
     int *state;        // kMarchThreads: cnt | more << 8
     int *list;         // kMarchThreads
     int *warp;         // kMarchThreads / 32
     float *we, *wx;    // CAP * kMarchThreads each
     void *wc;          // CAP * kMarchThreads window indices (uint8 or uint16)
-    unsigned *mask;    // kMaskWords * kMarchThreads per-ray candidate hit masks
+    unsigned *mask;    // (CC + 31) / 32 words * kMarchThreads per-ray candidate hit masks
 };
 
 template <int CAP, int MT, bool STAGED, int CC>
@@ -536,20 +536,34 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 // ----------------------------------------------------------------------------------------
 // Host-side launchers (plain C++ signatures for vpb_api.cpp).
 #ifndef VPB_WINDOW_CAP
-#define VPB_WINDOW_CAP 20
+#define VPB_WINDOW_CAP 16
 #endif
-constexpr int kWindowCap = VPB_WINDOW_CAP;  // per-ray segment window (shared memory)
+constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp_march_rays)
 
-// Two raymarch configurations. Normal: 20-entry windows, 160 staged candidates, 3 CTAs/SM.
-// Dense (long per-tile lists, many segments per ray; chosen from the previous render's mean
-// candidates per non-empty tile): 28-entry windows, 192 staged candidates, 2 CTAs/SM. The
-// 28-entry windows avoid window refills, which sit on the critical path of the heaviest
-// tiles there.
+// Three raymarch configurations, chosen per render from the previous render's mean
+// candidates per non-empty tile (vpb_api.cpp). The kernel is bound by gather latency, so each
+// keeps its shared memory small enough that the rest of the SM's 256 KB stays L1 cache for the
+// payload (e.g. 3 x 52 KB -> 92 KB of L1 for Normal). Measured on the BASELINE configs
+// (profiles/r01_tile_configs.txt):
+//   Light  (<= 14 candidates/tile, K=512 M=32):   12-entry windows, 64 staged, 3 CTAs/SM
+//   Normal (<= 40, the K=4096 M=16 headline):      16-entry windows, 64 staged, 3 CTAs/SM
+//   Dense  (K=32768 M=8: long lists, many segments per ray, refills on the critical path of
+//          the heaviest tiles):                    24-entry windows, 192 staged, 2 CTAs/SM
+// VPB_WINDOW_CAP / VPB_CAND_CAP / VPB_MARCH_MINB override Normal for tuning builds.
+#ifndef VPB_MARCH_MINB
+#define VPB_MARCH_MINB 3
+#endif
+#ifndef VPB_CARVEOUT
+#define VPB_CARVEOUT -1  // shared-memory carveout hint in percent; -1: just enough for MINB CTAs
+#endif
+struct TileCfgLight {
+    static constexpr int CAP = 12, CC = 64, MINB = 3;
+};
 struct TileCfgNormal {
-    static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = 3;
+    static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = VPB_MARCH_MINB;
 };
 struct TileCfgDense {
-    static constexpr int CAP = 28, CC = 192, MINB = 2;
+    static constexpr int CAP = 24, CC = 192, MINB = 2;
 };
 
 template <int CAP, int CC>
@@ -599,7 +613,11 @@ static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const f
     auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB>;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        // Ask for just the shared memory MINB resident CTAs need (each also reserves 1 KB):
+        // the rest of the 256 KB unified array stays L1 cache for the payload gathers.
+        int carve = VPB_CARVEOUT;
+        if (carve < 0) carve = (int)((Cfg::MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
         attr_set = true;
     }
     kern<<<cam.tiles_x * cam.tiles_y, kMarchThreads, smem, st>>>(cam, mp, xf16, prects, payload, offsets,
@@ -629,13 +647,19 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
                                const int4 *prects, const float4 *payload, const uint32_t *offsets,
                                const uint32_t *order, const unsigned long long *entries,
                                const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               bool dense, cudaStream_t st) {
+                               TileTier tier, cudaStream_t st) {
     if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
-    if (dense)
+    switch (tier) {
+    case TileTier::Light:
+        return launch_tiles_cfg<TileCfgLight>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
+                                              ovf_list, ovf_cap, st);
+    case TileTier::Dense:
         return launch_tiles_cfg<TileCfgDense>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
                                               ovf_list, ovf_cap, st);
-    return launch_tiles_cfg<TileCfgNormal>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
-                                           ovf_list, ovf_cap, st);
+    default:
+        return launch_tiles_cfg<TileCfgNormal>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
+                                               ovf_list, ovf_cap, st);
+    }
 }
 
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
@@ -658,7 +682,7 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st) {
     if (n_rays == 0) return cudaSuccess;
-    k_march_rays<kWindowCap><<<(unsigned)((n_rays + kRayThreads - 1) / kRayThreads), kRayThreads, 0, st>>>(
+    k_march_rays<kRayWindowCap><<<(unsigned)((n_rays + kRayThreads - 1) / kRayThreads), kRayThreads, 0, st>>>(
         mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
     return cudaGetLastError();
 }

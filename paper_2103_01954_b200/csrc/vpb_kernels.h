@@ -18,6 +18,9 @@ struct DevCounters {
     int fallback_fail;
 };
 
+// Raymarch kernel configuration (window length, staged candidates, CTAs/SM): vpb_kernels.cu.
+enum class TileTier : int { Light = 0, Normal = 1, Dense = 2 };
+
 struct MarchDev {
     float dt, eps;
     int jitter, m;
@@ -76,7 +79,7 @@ cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const floa
                                const int4 *prects, const float4 *payload, const uint32_t *offsets,
                                const uint32_t *order, const unsigned long long *entries,
                                const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               bool dense, cudaStream_t st);
+                               TileTier tier, cudaStream_t st);
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
                                   const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
                                   const uint32_t *offsets, const unsigned long long *entries,

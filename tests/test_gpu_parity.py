@@ -67,11 +67,12 @@ def test_full_size_render_digest(renderer, key):
     assert out.stats["ray_samples"] == d["total_samples"]
 
 
-@pytest.mark.parametrize("tile_cfg", ["normal", "dense"])
+@pytest.mark.parametrize("tile_cfg", ["light", "normal", "dense"])
 @pytest.mark.parametrize("key", ["k32768_m8_1024_view-1", "k4096_m16_1024_view-1", "oracle_64x16_256_view-1"])
 def test_full_size_digest_under_each_tile_config(monkeypatch, key, tile_cfg):
-    """Both raymarch configurations (normal: 20-entry windows, 3 CTAs/SM; dense: 28-entry
-    windows, 192 staged candidates, 2 CTAs/SM) are bit-exact on every scene density."""
+    """Every raymarch configuration (light / normal / dense: 12 / 16 / 24-entry windows,
+    64 / 64 / 192 staged candidates) is bit-exact on every scene density, including the ones it
+    is not chosen for (window refills, unstaged tiles)."""
     from paper_2103_01954_b200 import Renderer
     monkeypatch.setenv("VPB_TILE_CFG", tile_cfg)
     d = DIGESTS["renders"][key]
