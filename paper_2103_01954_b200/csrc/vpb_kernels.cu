@@ -303,18 +303,19 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
             const int c = i >> 2, q = i & 3;
             const int prim = (int)(uint32_t)(entries[start + c] & 0xffffffffull);
             if (q == 0) sm.prim[c] = prim;
-            sm.xf4[i] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
+            sm.xf4[q * CC + c] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
         }
         __syncthreads();
         if (tid < n) {
-            const V3 om = to_model(reinterpret_cast<const float *>(sm.xf4 + tid * 4), o);
+            const Xf16 x = load_xf(sm.xf4 + tid, CC);
+            const V3 om = to_model(x.v, o);
             sm.om[tid] = make_float4(om.x, om.y, om.z, 0.f);
             sm.prect[tid] = prects[sm.prim[tid]];
         }
         __syncthreads();
     }
     const TileCands<STAGED> cands{entries, xf_g, prects, payload, m3, start, n, sm.prim,
-                                  reinterpret_cast<const float *>(sm.xf4), sm.om, sm.prect};
+                                  sm.xf4, sm.om, sm.prect, CC};
     IdxT *wc = reinterpret_cast<IdxT *>(sm.wc);
 
     // phase 1: segment windows

@@ -18,13 +18,45 @@ constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
 #endif
 constexpr int kCandCap = VPB_CAND_CAP;  // candidates staged in shared memory per tile (<= 255)
 
+// A primitive's 16-float transform record held in registers (four 16-byte loads).
+struct Xf16 {
+    float v[16];
+};
+__device__ __forceinline__ Xf16 load_xf(const float4 *src, int step) {
+    Xf16 r;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 t = src[q * step];
+        r.v[4 * q] = t.x;
+        r.v[4 * q + 1] = t.y;
+        r.v[4 * q + 2] = t.z;
+        r.v[4 * q + 3] = t.w;
+    }
+    return r;
+}
+__device__ __forceinline__ Xf16 ldg_xf(const float *xf) {
+    Xf16 r;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(xf) + q);
+        r.v[4 * q] = t.x;
+        r.v[4 * q + 1] = t.y;
+        r.v[4 * q + 2] = t.z;
+        r.v[4 * q + 3] = t.w;
+    }
+    return r;
+}
+
 // Candidate sources for the per-ray segment window. hit() is intersectObb (lbvh.cpp:177-205).
 //
 // TileCands<true>: every candidate of the tile is staged in shared memory (n <= kCandCap):
 // transform, toModel(camera centre) (every ray of a render starts there, so om is computed
 // once per candidate instead of once per ray, same operations, same bits), pixel rectangle
-// and payload base. TileCands<false>: the generic path reading the tile bucket from global
-// memory (tiles with more candidates, fallback re-march).
+// and payload base. The staged transforms are quad-major (quad q of candidate c at
+// s_xf4[q * xs + c]): lanes reading different candidates hit different banks (a 64-byte
+// record stride put every other candidate on the same banks). TileCands<false>: the generic
+// path reading the tile bucket from global memory (tiles with more candidates, fallback
+// re-march).
 template <bool STAGED>
 struct TileCands {
     const unsigned long long *entries;
@@ -35,15 +67,20 @@ struct TileCands {
     uint32_t start;
     int n;
     const int *s_prim;
-    const float *s_xf;
+    const float4 *s_xf4;
     const float4 *s_om;
     const int4 *s_prect;
+    int xs;  // quad stride of s_xf4 (the staging capacity)
     __device__ __forceinline__ int prim(int c) const {
         if (STAGED) return s_prim[c];
         return (int)(uint32_t)(entries[start + c] & 0xffffffffull);
     }
-    __device__ __forceinline__ const float *xf(int c) const {
-        return STAGED ? s_xf + c * kXfStride : xf_g + (size_t)prim(c) * kXfStride;
+    __device__ __forceinline__ const float *xf(int c) const {  // unstaged only
+        return xf_g + (size_t)prim(c) * kXfStride;
+    }
+    __device__ __forceinline__ Xf16 xfv(int c) const {
+        if (STAGED) return load_xf(s_xf4 + c, xs);
+        return ldg_xf(xf(c));
     }
     __device__ __forceinline__ const float4 *base(int c) const {
         return payload + (size_t)prim(c) * m3;
@@ -56,7 +93,8 @@ struct TileCands {
     __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
         if (STAGED) {
             const float4 om = s_om[c];
-            return intersect_obb_om(xf(c), mk3(om.x, om.y, om.z), d, tE, tX);
+            const Xf16 x = xfv(c);
+            return intersect_obb_om(x.v, mk3(om.x, om.y, om.z), d, tE, tX);
         }
         return intersect_obb(xf(c), o, d, tE, tX);
     }
@@ -68,6 +106,7 @@ struct AllCands {  // every primitive (march over arbitrary rays)
     int n;
     __device__ __forceinline__ int prim(int c) const { return c; }
     __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ Xf16 xfv(int c) const { return ldg_xf(xf(c)); }
     __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
     __device__ __forceinline__ bool covers(int, int2) const { return true; }
     __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
@@ -263,7 +302,8 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
         {  // one primitive-sample (march.cpp:63-70)
             const int c = w.C(j);
             float sg, r, g, b;
-            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
+            const Xf16 xr = cands.xfv(c);
+            sample_primitive<MT>(cands.base(c), mp.m, xr.v, pw, mp.alpha, mp.beta, tab, sg, r,
                                  g, b);
             sigmaSum += sg;
             rw += r * sg;
@@ -410,7 +450,8 @@ __device__ RayOut march_window_generic(const Cands &cands, const Win &w, int cnt
         {  // one primitive-sample (march.cpp:63-70)
             const int c = w.C(j);
             float sg, r, g, b;
-            sample_primitive<MT>(cands.base(c), mp.m, cands.xf(c), pw, mp.alpha, mp.beta, tab, sg, r,
+            const Xf16 xr = cands.xfv(c);
+            sample_primitive<MT>(cands.base(c), mp.m, xr.v, pw, mp.alpha, mp.beta, tab, sg, r,
                                  g, b);
             sigmaSum += sg;
             rw += r * sg;
