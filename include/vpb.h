@@ -102,11 +102,21 @@ int vp_compose(int32_t n_prim, const float *transforms24, float *xf15);
  * Uploads a frame: composed transforms and the planar slab, which kernel K0 repacks on the
  * device into channel-interleaved float4 voxels (k, z, y, x, rgba). window = WindowParams
  * (primitive.h:14-17). VP_ERR_USAGE on K < 0, M < 1 (when K > 0), odd or negative beta,
- * non-positive scale. */
+ * non-positive scale. xf15 may be NULL: the transforms then come from vp_set_frame (or
+ * vp_set_transforms) before the first render. */
 int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
                  const float *payload_planar, float window_alpha, int32_t window_beta);
 /* Replace only the transforms (same K), e.g. a new frame with the same payload. */
 int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15);
+/* Frame::composed() on the device (scene.h:19-24, primitive.cpp:41-49, rotation.cpp:8-27):
+ * takes the frame's PrimitiveTransform records (K*24 floats, host or device) and composes
+ * them into the resident transforms, bit-identical to vp_compose (the device restates glibc
+ * sinf/cosf). The records stay resident for vp_adam_step. Same K as the resident scene;
+ * vp_set_scene may be called with xf15 = NULL first. VP_ERR_USAGE on a non-positive
+ * composed scale. */
+int vp_set_frame(vp_ctx *ctx, int32_t n_prim, const float *transforms24);
+/* Copy the resident composed transforms out as K*15 floats (host or device). */
+int vp_get_transforms(vp_ctx *ctx, float *xf15);
 /* Adopt an already-interleaved payload (K*M^3 float4 = K*M^3*4 floats, host or device),
  * e.g. after an NCCL broadcast of the repacked buffer. Keeps the current transforms. */
 int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m,
@@ -216,6 +226,9 @@ int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, 
 /* Test hook: evaluates the device port of glibc expf used by window() (primitive.cpp:27)
  * elementwise, so the port can be checked exhaustively against the host libm. */
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y);
+/* Test hook: the device port of glibc sinf (which = 0) / cosf (which = 1) used by the
+ * device compose (rotationFromAxisAngle, rotation.cpp:19-22), elementwise. */
+int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t which);
 
 /* ---- synthetic benchmark inputs ("mvp_shell"), host only ------------------ */
 /* transforms24: K*24, payload_planar: K*4*M^3 (either may be NULL to skip). */

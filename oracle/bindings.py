@@ -85,6 +85,16 @@ class Oracle:
         L.vpo_expf_mismatches.argtypes = [C.c_uint32, C.c_uint32, f32p]
         L.vpo_expf_port_mismatches.restype = C.c_int64
         L.vpo_expf_port_mismatches.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+        L.vpo_sinf_port.restype = C.c_float
+        L.vpo_sinf_port.argtypes = [C.c_float]
+        L.vpo_cosf_port.restype = C.c_float
+        L.vpo_cosf_port.argtypes = [C.c_float]
+        L.vpo_sincos_port_mismatches.restype = C.c_int64
+        L.vpo_sincos_port_mismatches.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
+        L.vpo_sincos_mismatches.restype = C.c_int64
+        L.vpo_sincos_mismatches.argtypes = [C.c_uint32, C.c_uint32, f32p, C.c_int]
+        L.vpo_sincos_libm.restype = None
+        L.vpo_sincos_libm.argtypes = [C.c_int64, f32p, f32p, C.c_int]
 
     def compose(self, tr24):
         tr = _f(tr24).reshape(-1, 24)
@@ -205,6 +215,23 @@ class Oracle:
 
     def expf_port_mismatches(self, lo_bits: int, hi_bits: int, stride: int = 1) -> int:
         return int(self.lib.vpo_expf_port_mismatches(lo_bits, hi_bits, stride))
+
+    def sincos_port_mismatches(self, lo_bits: int, hi_bits: int, stride: int = 1, cos: bool = False) -> int:
+        """C port of glibc sinf/cosf vs this host's libm over float bit patterns."""
+        return int(self.lib.vpo_sincos_port_mismatches(lo_bits, hi_bits, stride, 1 if cos else 0))
+
+    def sincos_libm(self, x: np.ndarray, cos: bool = False) -> np.ndarray:
+        """This host's libm sinf/cosf over an array."""
+        xs = np.ascontiguousarray(x, np.float32)
+        y = np.empty_like(xs)
+        self.lib.vpo_sincos_libm(xs.size, _p(xs), _p(y), 1 if cos else 0)
+        return y
+
+    def sincos_mismatches(self, lo_bits: int, hi_bits: int, values: np.ndarray, cos: bool = False) -> int:
+        """values[i] (for bit pattern lo_bits + i) vs this host's libm sinf/cosf."""
+        v = np.ascontiguousarray(values, np.float32)
+        assert v.size == hi_bits - lo_bits + 1
+        return int(self.lib.vpo_sincos_mismatches(lo_bits, hi_bits, _p(v), 1 if cos else 0))
 
     def composite(self, rgb, alpha, bg):
         h, w = rgb.shape[:2]

@@ -961,3 +961,134 @@ int64_t vpo_expf_port_mismatches(uint32_t lo_bits, uint32_t hi_bits, uint32_t st
     }
     return bad;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * C port of glibc 2.39 sinf / cosf (sysdeps/ieee754/flt-32/s_sinf.c, s_cosf.c, sincosf.h:
+ * the ARM optimized-routines algorithm), as used by rotationFromAxisAngle
+ * (rotation.cpp:8-27) through std::sin / std::cos on float. Polynomials in binary64 with the
+ * multiply-adds fused, as in the FMA build glibc's ifunc selects on x86-64 hosts with FMA;
+ * one rounding to float at the end. The coefficient table is __sincosf_table (sign[4],
+ * hpi_inv = 2/pi * 2^24, hpi = pi/2, then c0 c1 s1 c2 s2 c3 s3 c4; the second row negates the
+ * cosine coefficients), the 4/pi bits are __inv_pio4. Ported to the device in
+ * paper_2103_01954_b200/csrc/vpb_device.cuh (device compose). */
+static const double kSinCosTab[2][8] = {
+    {0x1p0, -0x1.ffffffd0c621cp-2, -0x1.555545995a603p-3, 0x1.55553e1068f19p-5, 0x1.1107605230bc4p-7,
+     -0x1.6c087e89a359dp-10, -0x1.994eb3774cf24p-13, 0x1.99343027bf8c3p-16},
+    {-0x1p0, 0x1.ffffffd0c621cp-2, -0x1.555545995a603p-3, -0x1.55553e1068f19p-5, 0x1.1107605230bc4p-7,
+     0x1.6c087e89a359dp-10, -0x1.994eb3774cf24p-13, -0x1.99343027bf8c3p-16}};
+static const uint32_t kInvPio4[24] = {
+    0xa2,       0xa2f9,     0xa2f983,   0xa2f9836e, 0xf9836e4e, 0x836e4e44, 0x6e4e4415, 0x4e441529,
+    0x441529fc, 0x1529fc27, 0x29fc2757, 0xfc2757d1, 0x2757d1f5, 0x57d1f534, 0xd1f534dd, 0xf534ddc0,
+    0x34ddc0db, 0xddc0db62, 0xc0db6295, 0xdb629599, 0x6295993c, 0x95993c43, 0x993c4390, 0x3c439041};
+
+static uint32_t sc_abstop12(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    return (u >> 20) & 0x7ff;
+}
+
+/* sinf_poly: n even -> sine polynomial, odd -> cosine polynomial (c = kSinCosTab row) */
+static float sc_poly(double x, double x2, const double *c, int n) {
+    if ((n & 1) == 0) {
+        const double x3 = x * x2;
+        const double s1 = fma(x2, c[6], c[4]);
+        const double x7 = x3 * x2;
+        const double s = fma(x3, c[2], x);
+        return (float)fma(x7, s1, s);
+    }
+    const double x4 = x2 * x2;
+    const double c2 = fma(x2, c[7], c[5]);
+    const double c1 = fma(x2, c[1], c[0]);
+    const double x6 = x4 * x2;
+    const double cc = fma(x4, c[3], c1);
+    return (float)fma(x6, c2, cc);
+}
+
+static double sc_reduce_fast(double x, int *np) {
+    const double r = x * 0x1.45f306dc9c883p+23;
+    const int n = ((int32_t)r + 0x800000) >> 24;
+    *np = n;
+    return fma(-(double)n, 0x1.921fb54442d18p0, x);
+}
+
+static double sc_reduce_large(uint32_t xi, int *np) {
+    const uint32_t *arr = &kInvPio4[(xi >> 26) & 15];
+    const int shift = (xi >> 23) & 7;
+    xi = (xi & 0xffffff) | 0x800000;
+    xi <<= shift;
+    uint64_t res0 = (uint64_t)(uint32_t)(xi * arr[0]);
+    const uint64_t res1 = (uint64_t)xi * arr[4];
+    const uint64_t res2 = (uint64_t)xi * arr[8];
+    res0 = (res2 >> 32) | (res0 << 32);
+    res0 += res1;
+    const uint64_t n = (res0 + (1ULL << 61)) >> 62;
+    res0 -= n << 62;
+    *np = (int)n;
+    return (double)(int64_t)res0 * 0x1.921fb54442d18p-62;
+}
+
+static float sc_eval(float y, int want_cos) {
+    const double sign[4] = {1.0, -1.0, -1.0, 1.0};
+    double x = y;
+    int n = 0;
+    const double *c = kSinCosTab[0];
+    if (sc_abstop12(y) < sc_abstop12(0x1.921fb6p-1f)) {
+        const double x2 = x * x;
+        if (sc_abstop12(y) < sc_abstop12(0x1p-12f)) return want_cos ? 1.0f : y;
+        return sc_poly(x, x2, c, want_cos);
+    }
+    if (sc_abstop12(y) < sc_abstop12(120.0f)) {
+        x = sc_reduce_fast(x, &n);
+        const double s = sign[n & 3];
+        if (n & 2) c = kSinCosTab[1];
+        return sc_poly(x * s, x * x, c, want_cos ? n ^ 1 : n);
+    }
+    if (sc_abstop12(y) < sc_abstop12(INFINITY)) {
+        uint32_t xi;
+        memcpy(&xi, &y, 4);
+        const int sgn = (int)(xi >> 31);
+        x = sc_reduce_large(xi, &n);
+        const double s = sign[(n + sgn) & 3];
+        if ((n + sgn) & 2) c = kSinCosTab[1];
+        return sc_poly(x * s, x * x, c, want_cos ? n ^ 1 : n);
+    }
+    return (y - y) / (y - y);
+}
+
+float vpo_sinf_port(float x) { return sc_eval(x, 0); }
+float vpo_cosf_port(float x) { return sc_eval(x, 1); }
+
+/* Counts floats x = bits lo, lo+stride, ... <= hi where the ports differ from libm sinf/cosf
+ * (which: 0 sin, 1 cos). */
+int64_t vpo_sincos_port_mismatches(uint32_t lo_bits, uint32_t hi_bits, uint32_t stride, int which) {
+    int64_t bad = 0;
+    if (stride == 0) stride = 1;
+    for (uint64_t u = lo_bits; u <= hi_bits; u += stride) {
+        float x, a, b;
+        const uint32_t w = (uint32_t)u;
+        memcpy(&x, &w, 4);
+        a = which ? cosf(x) : sinf(x);
+        b = which ? vpo_cosf_port(x) : vpo_sinf_port(x);
+        if (memcmp(&a, &b, 4) != 0 && !(a != a && b != b)) ++bad;
+    }
+    return bad;
+}
+
+/* Counts inputs in [lo_bits, hi_bits] whose value in `values` differs bitwise from libm
+ * sinf/cosf (which: 0 sin, 1 cos). values[i] corresponds to lo_bits + i. */
+int64_t vpo_sincos_mismatches(uint32_t lo_bits, uint32_t hi_bits, const float *values, int which) {
+    int64_t bad = 0;
+    for (uint64_t u = lo_bits; u <= hi_bits; ++u) {
+        float x, e;
+        const uint32_t b = (uint32_t)u;
+        memcpy(&x, &b, 4);
+        e = which ? cosf(x) : sinf(x);
+        if (memcmp(&e, &values[u - lo_bits], 4) != 0 && !(e != e && values[u - lo_bits] != values[u - lo_bits])) ++bad;
+    }
+    return bad;
+}
+
+/* libm sinf / cosf (which: 0 sin, 1 cos) over an arbitrary array (test reference values). */
+void vpo_sincos_libm(int64_t n, const float *x, float *y, int which) {
+    for (int64_t i = 0; i < n; ++i) y[i] = which ? cosf(x[i]) : sinf(x[i]);
+}

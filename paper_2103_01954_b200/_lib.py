@@ -55,6 +55,8 @@ SIGNATURES = {
     "vp_compose": (C.c_int, [C.c_int32, f32p, f32p]),
     "vp_set_scene": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32]),
     "vp_set_transforms": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
+    "vp_set_frame": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
+    "vp_get_transforms": (C.c_int, [C.c_void_p, f32p]),
     "vp_set_payload_interleaved": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p]),
     "vp_load_slab": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, f32p, C.c_float, C.c_int32]),
     "vp_payload_device": (C.c_int, [C.c_void_p, C.POINTER(f32p), i64p]),
@@ -82,6 +84,7 @@ SIGNATURES = {
     "vp_debug_tile_times": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march),
                                       C.POINTER(C.c_uint64), C.c_int64, i64p]),
     "vp_debug_expf": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p]),
+    "vp_debug_sincos": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, C.c_int32]),
     "vp_make_shell_scene": (C.c_int, [C.c_int32, C.c_int32, f32p, f32p]),
     "vp_look_at_camera": (C.c_int, [f32p, f32p, f32p, C.c_float, C.c_int32, C.c_int32,
                                     C.POINTER(vp_camera), f32p]),

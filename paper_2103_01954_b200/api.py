@@ -262,10 +262,33 @@ class Renderer:
         return out[:n.value]
 
     def set_frame(self, scene: Scene, frame: int):
+        """Make scene.frames[frame] resident: the slab is repacked and the frame's
+        PrimitiveTransform records are composed on the device (Frame::composed())."""
         if frame < 0 or frame >= len(scene.frames):
             raise Error(ErrorCategory.USAGE, "frame index out of range")  # march.cpp:96-97
         fr = scene.frames[frame]
-        self.set_scene_composed(fr.composed(), fr.slab, scene.window)
+        self.set_scene_records(fr.transforms, fr.slab, scene.window)
+
+    def set_scene_records(self, transforms: np.ndarray, slab: PrimitiveSlab, window: WindowParams):
+        """Upload the planar slab and K x 24 PrimitiveTransform records; compose on the device."""
+        tr = _f32(transforms).reshape(-1, 24)
+        pay = None if slab.payload is None else _f32(slab.payload)
+        _check(self._lib.vp_set_scene(self._ctx, tr.shape[0], int(slab.voxels_per_axis), None,
+                                      _fptr(pay) if pay is not None else None,
+                                      float(window.alpha), int(window.beta)), self._ctx)
+        self.n_prim, self.m = tr.shape[0], int(slab.voxels_per_axis)
+        self.set_records(tr)
+
+    def set_records(self, transforms: np.ndarray):
+        """A new pose for the resident frame: K x 24 records composed on the device."""
+        tr = _f32(transforms).reshape(-1, 24)
+        _check(self._lib.vp_set_frame(self._ctx, tr.shape[0], _fptr(tr)), self._ctx)
+
+    def transforms(self) -> np.ndarray:
+        """The resident composed transforms (K x 15 AffineXf records)."""
+        out = np.zeros((int(self.n_prim or 0), 15), np.float32)
+        _check(self._lib.vp_get_transforms(self._ctx, _fptr(out)), self._ctx)
+        return out
 
     def load_slab(self, path: str, xf15: np.ndarray, window: WindowParams):
         """loadSlab (scene_io.cpp:43-66) streamed straight into the device layout; xf15 are the
@@ -365,6 +388,12 @@ class Renderer:
                                         prims.ctypes.data_as(i32p), prims.size, C.byref(n_keys)),
                self._ctx)
         return rects[:k], keys[:k], offs, prims[:n_keys.value]
+
+    def debug_sincos(self, x: np.ndarray, cos: bool = False) -> np.ndarray:
+        x = _f32(x).reshape(-1)
+        y = np.empty_like(x)
+        _check(self._lib.vp_debug_sincos(self._ctx, x.size, _fptr(x), _fptr(y), 1 if cos else 0), self._ctx)
+        return y
 
     def debug_expf(self, x: np.ndarray) -> np.ndarray:
         x = _f32(x).reshape(-1)

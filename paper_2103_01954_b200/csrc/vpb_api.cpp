@@ -71,6 +71,9 @@ struct vp_ctx {
     float w_alpha = 8;
     int32_t w_beta = 8;
     DBuf<float> xf16, xf15_tmp, planar_tmp;
+    DBuf<float> tr24;      // resident PrimitiveTransform records (vp_set_frame, vp_adam_step)
+    DBuf<int> flag;        // device error flag (compose)
+    bool has_xf = false;   // resident composed transforms are set
     DBuf<float4> payload;
     DBuf<int4> rects, prects;
     DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
@@ -234,9 +237,11 @@ int check_counters(vp_ctx *ctx, const DevCounters &c) {
     return VP_OK;
 }
 
-int check_ctx(vp_ctx *ctx, bool need_scene) {
+int check_ctx(vp_ctx *ctx, bool need_scene, bool need_xf = true) {
     if (!ctx) return fail(nullptr, VP_ERR_USAGE, "null context");
     if (need_scene && !ctx->has_scene) return fail(ctx, VP_ERR_USAGE, "no scene set");
+    if (need_scene && need_xf && ctx->n_prim > 0 && !ctx->has_xf)
+        return fail(ctx, VP_ERR_USAGE, "no transforms set (vp_set_frame / vp_set_transforms)");
     const cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
     return VP_OK;
@@ -298,6 +303,8 @@ int vp_destroy(vp_ctx *ctx) {
     if (!ctx) return VP_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ctx->tr24.release();
+    ctx->flag.release();
     for (auto *b : {&ctx->xf16, &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
                     &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
         b->release();
@@ -353,6 +360,41 @@ int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
     }
     VP_CUDA(ctx, launch_pad_xf(src, ctx->xf16.p, n_prim, ctx->stream));
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->has_xf = true;
+    return VP_OK;
+}
+
+int vp_set_frame(vp_ctx *ctx, int32_t n_prim, const float *tr24) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
+    if (n_prim == 0) return VP_OK;
+    if (!tr24) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    cudaStream_t st = ctx->stream;
+    VP_CUDA(ctx, ctx->tr24.ensure(size_t(n_prim) * 24));
+    VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
+    VP_CUDA(ctx, ctx->flag.ensure(1));
+    if ((const void *)tr24 != (const void *)ctx->tr24.p)
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->tr24.p, tr24, sizeof(float) * 24 * size_t(n_prim),
+                                     is_device_ptr(tr24) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    VP_CUDA(ctx, cudaMemsetAsync(ctx->flag.p, 0, sizeof(int), st));
+    VP_CUDA(ctx, launch_compose(ctx->tr24.p, nullptr, n_prim, ctx->xf16.p, ctx->flag.p, st));
+    int bad = 0;
+    VP_CUDA(ctx, cudaMemcpyAsync(&bad, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    ctx->has_xf = !bad;
+    if (bad) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+    return VP_OK;
+}
+
+int vp_get_transforms(vp_ctx *ctx, float *xf15) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (ctx->n_prim == 0) return VP_OK;
+    if (!xf15) return fail(ctx, VP_ERR_USAGE, "null destination");
+    VP_CUDA(ctx, cudaMemcpy2DAsync(xf15, 15 * sizeof(float), ctx->xf16.p, 16 * sizeof(float), 15 * sizeof(float),
+                                   size_t(ctx->n_prim),
+                                   is_device_ptr(xf15) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return VP_OK;
 }
 
@@ -361,7 +403,6 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     if (int rc = check_ctx(ctx, false)) return rc;
     if (n_prim < 0) return fail(ctx, VP_ERR_USAGE, "negative primitive count");
     if (n_prim > 0 && m < 1) return fail(ctx, VP_ERR_USAGE, "voxels per axis must be >= 1");
-    if (n_prim > 0 && !xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
     if (!std::isfinite(window_alpha)) return fail(ctx, VP_ERR_USAGE, "window alpha must be finite");
     ctx->has_scene = false;
     ctx->n_prim = n_prim;
@@ -369,10 +410,15 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     ctx->w_alpha = window_alpha;
     ctx->w_beta = window_beta;
     ctx->has_scene = true;
+    ctx->has_xf = false;
     if (n_prim == 0) return VP_OK;
-    if (int rc = vp_set_transforms(ctx, n_prim, xf15)) {
-        ctx->has_scene = false;
-        return rc;
+    if (xf15) {
+        if (int rc = vp_set_transforms(ctx, n_prim, xf15)) {
+            ctx->has_scene = false;
+            return rc;
+        }
+    } else {
+        VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
     }
     const int64_t m3 = int64_t(m) * m * m;
     const size_t nf = size_t(n_prim) * 4 * size_t(m3);
@@ -392,7 +438,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
 }
 
 int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *inter) {
-    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_ctx(ctx, true, false)) return rc;
     if (n_prim != ctx->n_prim || m != ctx->m) return fail(ctx, VP_ERR_USAGE, "payload shape mismatch");
     if (n_prim == 0) return VP_OK;
     if (!inter) return fail(ctx, VP_ERR_USAGE, "null payload");
@@ -407,14 +453,14 @@ int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const flo
 }
 
 int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats) {
-    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_ctx(ctx, true, false)) return rc;
     if (dev_ptr) *dev_ptr = reinterpret_cast<float *>(ctx->payload.p);
     if (n_floats) *n_floats = int64_t(ctx->n_prim) * ctx->m * ctx->m * ctx->m * 4;
     return VP_OK;
 }
 
 int vp_copy_payload(vp_ctx *ctx, float *dst) {
-    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_ctx(ctx, true, false)) return rc;
     const size_t n4 = size_t(ctx->n_prim) * size_t(ctx->m) * ctx->m * ctx->m;
     if (n4 == 0) return VP_OK;
     if (!dst) return fail(ctx, VP_ERR_USAGE, "null destination");
@@ -957,10 +1003,11 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
     }
     float *d_delta = tmp.p + n;
     int *d_bad = reinterpret_cast<int *>(tmp.p + n + 9 * size_t(k));
-    std::vector<float> deltas(9 * size_t(k));
-    for (int i = 0; i < k; ++i)
-        std::memcpy(deltas.data() + 9 * size_t(i), transforms24 + 24 * size_t(i) + 15, 9 * sizeof(float));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_delta, deltas.data(), 4 * deltas.size(), cudaMemcpyHostToDevice, st));
+    // the caller's records are authoritative: resident copy, then the deltas in Adam's order
+    VP_CUDA(ctx, ctx->tr24.ensure(24 * size_t(k)));
+    VP_CUDA(ctx, cudaMemcpyAsync(ctx->tr24.p, transforms24, 4 * 24 * size_t(k),
+                                 is_device_ptr(transforms24) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    VP_CUDA(ctx, launch_gather_deltas(ctx->tr24.p, k, d_delta, st));
     VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, st));
     AdamDev c{cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->lr_delta_scale, 0.f, 0.f};
     VP_CUDA(ctx, launch_adam(dg, nullptr, nullptr, nullptr, nullptr, int64_t(n_pay), int64_t(n), unsigned(m3), c,
@@ -974,22 +1021,32 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
     c.bc2 = 1 - std::pow(cfg->beta2, float(ctx->adam_step));
     VP_CUDA(ctx, launch_adam(dg, ctx->adam_m1.p, ctx->adam_m2.p, ctx->payload.p, d_delta, int64_t(n_pay),
                              int64_t(n), unsigned(m3), c, d_bad, false, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(deltas.data(), d_delta, 4 * deltas.size(), cudaMemcpyDeviceToHost, st));
+    // deltas back into the records with the scale projection (losses.cpp:97-103), then the
+    // frame is recomposed on the device (primitive.cpp:41-49)
+    VP_CUDA(ctx, ctx->xf16.ensure(16 * size_t(k)));
+    VP_CUDA(ctx, launch_compose(ctx->tr24.p, d_delta, k, ctx->xf16.p, d_bad, st));
+    if ((const void *)transforms24 != (const void *)ctx->tr24.p)
+        VP_CUDA(ctx, cudaMemcpyAsync(transforms24, ctx->tr24.p, 4 * 24 * size_t(k),
+                                     is_device_ptr(transforms24) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                     st));
+    VP_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
-    // deltas back into the records, scale projection (losses.cpp:97-103), recompose + upload
-    constexpr float kMinScale = 1e-4f;  // losses.h:61
-    std::vector<float> xf(15 * size_t(k));
-    for (int i = 0; i < k; ++i) {
-        float *t = transforms24 + 24 * size_t(i);
-        std::memcpy(t + 15, deltas.data() + 9 * size_t(i), 9 * sizeof(float));
-        for (int a = 0; a < 3; ++a) {
-            const float composed = t[12 + a] + t[21 + a];
-            if (composed < kMinScale) t[21 + a] = kMinScale - t[12 + a];
-        }
-        if (!host::compose(t, xf.data() + 15 * size_t(i)))
-            return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
-    }
-    return vp_set_transforms(ctx, k, xf.data());
+    ctx->has_xf = !bad;
+    if (bad) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+    return VP_OK;
+}
+
+int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t which) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (n < 0 || (n > 0 && (!x || !y)) || which < 0 || which > 1) return fail(ctx, VP_ERR_USAGE, "bad arguments");
+    if (n == 0) return VP_OK;
+    DBuf<float> tmp;
+    VP_CUDA(ctx, tmp.ensure(2 * size_t(n)));
+    VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, x, 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    VP_CUDA(ctx, launch_sincos(tmp.p, tmp.p + n, n, which == 1, ctx->stream));
+    VP_CUDA(ctx, cudaMemcpyAsync(y, tmp.p + n, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
 }
 
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y) {

@@ -103,6 +103,10 @@ cudaError_t launch_loss_adjoints(const float *rgb, const float *alpha, const flo
 cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, float *deltas, int64_t n_pay,
                         int64_t n, unsigned m3, const AdamDev &c, int *bad, bool check, cudaStream_t st);
 cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
+// vpb_compose.cu: Frame::composed() on the device (+ Adam's delta write-back and projection)
+cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st);
+cudaError_t launch_gather_deltas(const float *tr24, int n_prim, float *deltas, cudaStream_t st);
+cudaError_t launch_sincos(const float *x, float *y, int64_t n, bool want_cos, cudaStream_t st);
 cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
                              int64_t n_px, cudaStream_t st);
 

@@ -105,3 +105,61 @@ def test_vpsl_loader_errors_mirror_the_reference(renderer, tmp_path, kind, categ
     with pytest.raises(api.Error) as e:
         renderer.load_slab(str(p), xf, api.WindowParams())
     assert int(e.value.category) == category
+
+
+# -- device compose (Frame::composed() on the B200: vp_set_frame) ---------------------------
+def test_device_compose_matches_reference(renderer):
+    """vp_set_frame composes the reference's own fixtures (tests/golden/compose.npz, written by
+    the unmodified compose()) bit-for-bit; a non-positive scale is Usage, like the reference."""
+    z = np.load(GOLDEN / "compose.npz")
+    k = z["tr"].shape[0]
+    slab = api.PrimitiveSlab(k, 2, np.zeros(k * 4 * 8, np.float32))
+    renderer.set_scene_records(z["tr"], slab, api.WindowParams())
+    assert np.array_equal(bits(renderer.transforms()), bits(z["xf"]))
+    bad = z["bad"]
+    renderer.set_scene_records(z["tr"][:len(bad)], api.PrimitiveSlab(len(bad), 2, np.zeros(len(bad) * 32, np.float32)),
+                               api.WindowParams())
+    with pytest.raises(api.Error) as e:
+        renderer.set_records(bad)
+    assert e.value.category == api.ErrorCategory.USAGE
+
+
+def test_device_compose_equals_host_compose_on_large_angles(renderer):
+    """Random poses with rotation-vector magnitudes from 0 to 1e6 (both sinf/cosf reductions,
+    the small-angle series, the zero vector): device compose == host compose (vp_compose, the
+    reference's exact arithmetic)."""
+    rng = np.random.default_rng(7)
+    k = 4096
+    tr = np.zeros((k, 24), np.float32)
+    tr[:, 0:3] = rng.normal(size=(k, 3))
+    q = np.linalg.qr(rng.normal(size=(k, 3, 3)))[0]
+    tr[:, 3:12] = np.transpose(q, (0, 2, 1)).reshape(k, 9)
+    tr[:, 12:15] = rng.uniform(0.01, 0.1, size=(k, 3))
+    tr[:, 15:18] = rng.normal(scale=0.01, size=(k, 3))
+    axis = rng.normal(size=(k, 3))
+    axis /= np.linalg.norm(axis, axis=1, keepdims=True)
+    mag = 10.0 ** rng.uniform(-6, 6, size=k)
+    mag[:8] = [0, 1e-5, 9.99e-5, 1e-4, 0.7853982, 119.99, 120.0, 1e6]
+    tr[:, 18:21] = axis * mag[:, None]
+    tr[:, 21:24] = rng.normal(scale=1e-3, size=(k, 3))
+    slab = api.PrimitiveSlab(k, 2, np.zeros(k * 4 * 8, np.float32))
+    renderer.set_scene_records(tr, slab, api.WindowParams())
+    assert np.array_equal(bits(renderer.transforms()), bits(api.compose(tr)))
+
+
+@pytest.mark.parametrize("cos", [False, True])
+def test_device_sincos_is_glibc_exact(renderer, oracle, cos):
+    """The device port of glibc sinf/cosf used by compose: every float in [1e-4, 120) (the
+    rotation angles of any plausible pose; the fast-reduction path), strided beyond (the
+    large-argument reduction), against this host's libm."""
+    bad = 0
+    lo, hi, step = 0x38D1B717, 0x42F00000, 1 << 26
+    for start in range(lo, hi, step):
+        end = min(start + step - 1, hi - 1)
+        x = np.arange(start, end + 1, dtype=np.uint64).astype(np.uint32).view(np.float32)
+        bad += oracle.sincos_mismatches(start, end, renderer.debug_sincos(x, cos), cos)
+    big = np.arange(0x42F00000, 0x7F800000, 4099, dtype=np.uint64).astype(np.uint32)
+    x = np.concatenate([big, big | 0x80000000]).view(np.float32)
+    got, want = renderer.debug_sincos(x, cos), oracle.sincos_libm(x, cos)
+    bad += int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
+    assert bad == 0

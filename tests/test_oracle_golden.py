@@ -86,6 +86,19 @@ def test_window_known_answers(oracle):
     assert oracle.window(0.9, 0.9, 0.9, 0.0, 8) == 1.0
 
 
+@pytest.mark.parametrize("cos", [False, True])
+def test_sincos_port_matches_libm(oracle, cos):
+    """The binary64 sinf/cosf port (glibc 2.39's algorithm, ported to the device for compose)
+    equals this host's libm: strided walks over the polynomial-only range, the fast-reduction
+    range [0.75, 120) (where every axis-angle magnitude of a pose lives), the large-argument
+    reduction and negative inputs. Exhaustive runs (every float of [0, 120), stride 3 beyond)
+    were clean too; they take ~20 s."""
+    assert oracle.sincos_port_mismatches(0x00000000, 0x3F400000, 97, cos) == 0
+    assert oracle.sincos_port_mismatches(0x3F400000, 0x42F00000, 13, cos) == 0
+    assert oracle.sincos_port_mismatches(0x42F00000, 0x7F7FFFFF, 4099, cos) == 0
+    assert oracle.sincos_port_mismatches(0x80000000, 0xFF7FFFFF, 4099, cos) == 0
+
+
 def test_expf_port_matches_libm(oracle):
     """The binary64 expf port (the algorithm ported to the device) equals this host's glibc
     expf: a stride-7 walk over [-24, 0] (the window argument range at alpha = 8) and a
