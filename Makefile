@@ -24,7 +24,7 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
 
-$(PKG)/libvpb.so: $(OBJ)/vpb_kernels.o $(OBJ)/vpb_backward.o $(OBJ)/vpb_train.o $(OBJ)/vpb_compose.o $(OBJ)/vpb_api.o $(OBJ)/vpb_synth.o $(OBJ)/vpb_losses.o
+$(PKG)/libvpb.so: $(OBJ)/vpb_kernels.o $(OBJ)/vpb_backward.o $(OBJ)/vpb_train.o $(OBJ)/vpb_compose.o $(OBJ)/vpb_bvh.o $(OBJ)/vpb_api.o $(OBJ)/vpb_synth.o $(OBJ)/vpb_losses.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
 
 clean:

@@ -229,6 +229,10 @@ int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y);
 /* Test hook: the device port of glibc sinf (which = 0) / cosf (which = 1) used by the
  * device compose (rotationFromAxisAngle, rotation.cpp:19-22), elementwise. */
 int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t which);
+/* Test hook: backwardRay's per-primitive pose data (rBase[9], then rotationDerivative of
+ * deltaR for i = 0, 1, 2, rotation.cpp:30-38; 36 floats per primitive) from K*24 host records,
+ * computed by the device kernel (on_device = 1) or the host restatement (0). */
+int vp_debug_pose(vp_ctx *ctx, int32_t n_prim, const float *transforms24, float *out36, int32_t on_device);
 
 /* ---- synthetic benchmark inputs ("mvp_shell"), host only ------------------ */
 /* transforms24: K*24, payload_planar: K*4*M^3 (either may be NULL to skip). */

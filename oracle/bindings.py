@@ -397,6 +397,19 @@ def ref_eval_loss(ref, tr24, m, payload, window, cams, cam_index, pixel_xy, pixe
     return terms, g
 
 
+def ref_load_slab(ref, path):
+    """The reference loadSlab; returns (K, M, planar payload)."""
+    L = ref.lib
+    L.vpref_load_slab.argtypes = [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), f32p, C.c_int64]
+    k, m = C.c_int32(), C.c_int32()
+    if L.vpref_load_slab(str(path).encode(), C.byref(k), C.byref(m), None, 0) != 0:
+        raise RuntimeError(f"reference loadSlab failed: {ref.error()}")
+    pay = np.zeros(k.value * 4 * m.value ** 3, np.float32)
+    if L.vpref_load_slab(str(path).encode(), C.byref(k), C.byref(m), _p(pay), pay.size) != 0:
+        raise RuntimeError(f"reference loadSlab failed: {ref.error()}")
+    return k.value, m.value, pay
+
+
 def ref_adam_run(ref, tr24, m, payload_planar, grads_seq, cfg6):
     L = ref.lib
     L.vpref_adam_run.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_int32, f32p, f32p]

@@ -14,6 +14,7 @@
 //   vpref_generate_ray  -> generateRay                (camera.cpp:14-23)
 //   vpref_window        -> window                     (primitive.cpp:25-28)
 //   vpref_backward_rays -> intersect + backwardRay    (grad.cpp:34-195) into a GradBuffer
+//   vpref_load_slab     -> loadSlab                   (scene_io.cpp:43-66)
 //
 // Flat layouts (shared with include/vpb.h):
 //   PrimitiveTransform = 24 floats: tBase[3] rBase[9] (column-major) sBase[3] deltaT[3]
@@ -34,6 +35,7 @@
 #include "volprim/march.h"
 #include "volprim/primitive.h"
 #include "volprim/scene.h"
+#include "volprim/scene_io.h"
 #include "volprim/synthetic.h"
 
 using namespace volprim;
@@ -334,6 +336,18 @@ int vpref_adam_run(int32_t nPrim, int32_t m, float *tr24, float *payload, int32_
             put3(o + 18, fr.transforms[size_t(k)].deltaR);
             put3(o + 21, fr.transforms[size_t(k)].deltaS);
         }
+    });
+}
+
+// loadSlab into caller memory: *k, *m always; the planar payload when `payload` holds at
+// least `cap` floats >= K*4*M^3.
+int vpref_load_slab(const char *path, int32_t *k, int32_t *m, float *payload, int64_t cap) {
+    return guarded([&] {
+        const PrimitiveSlab slab = loadSlab(path);
+        *k = slab.numPrimitives;
+        *m = slab.voxelsPerAxis;
+        if (payload && int64_t(slab.payload.size()) <= cap)
+            std::memcpy(payload, slab.payload.data(), slab.payload.size() * sizeof(float));
     });
 }
 

@@ -85,6 +85,7 @@ SIGNATURES = {
                                       C.POINTER(C.c_uint64), C.c_int64, i64p]),
     "vp_debug_expf": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p]),
     "vp_debug_sincos": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, C.c_int32]),
+    "vp_debug_pose": (C.c_int, [C.c_void_p, C.c_int32, f32p, f32p, C.c_int32]),
     "vp_make_shell_scene": (C.c_int, [C.c_int32, C.c_int32, f32p, f32p]),
     "vp_look_at_camera": (C.c_int, [f32p, f32p, f32p, C.c_float, C.c_int32, C.c_int32,
                                     C.POINTER(vp_camera), f32p]),

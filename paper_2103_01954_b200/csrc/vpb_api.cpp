@@ -89,6 +89,12 @@ struct vp_ctx {
     cudaEvent_t t_ev[2 * kTimingSlots] = {};
     int64_t t_count = 0;
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
+    // per-entry-point scratch, kept across calls (a cudaMalloc per training call costs ms)
+    DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_adam;
+    // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
+    DBuf<BvhNode> bvh_nodes;
+    DBuf<unsigned char> bvh_scratch;
+    bool bvh_dirty = true;
     int64_t adam_step = 0;
     // Raymarch configuration for the next render, from the mean candidates per non-empty tile
     // of the last render whose counters reached the host (see note_density).
@@ -153,6 +159,20 @@ MarchDev make_march(const vp_ctx *ctx, const vp_march *cfg) {
     mp.alpha = ctx->w_alpha;
     mp.beta = ctx->w_beta;
     return mp;
+}
+
+// The BVH of the resident transforms (built on the ctx stream if the pose changed).
+int ensure_bvh(vp_ctx *ctx, MarchDev &mp) {
+    const int n = ctx->n_prim;
+    if (ctx->bvh_dirty && n > 1) {
+        VP_CUDA(ctx, ctx->bvh_nodes.ensure(size_t(n - 1)));
+        const size_t bytes = bvh_scratch_bytes(n);
+        VP_CUDA(ctx, ctx->bvh_scratch.ensure(bytes));
+        VP_CUDA(ctx, launch_bvh_build(ctx->xf16.p, n, ctx->bvh_nodes.p, ctx->bvh_scratch.p, bytes, ctx->stream));
+    }
+    ctx->bvh_dirty = false;
+    mp.bvh = BvhDev{ctx->bvh_nodes.p, n};
+    return VP_OK;
 }
 
 int ensure_fallback(vp_ctx *ctx) {
@@ -304,6 +324,7 @@ int vp_destroy(vp_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->tr24.release();
+    for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_adam}) b->release();
     ctx->flag.release();
     for (auto *b : {&ctx->xf16, &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
                     &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
@@ -361,6 +382,7 @@ int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
     VP_CUDA(ctx, launch_pad_xf(src, ctx->xf16.p, n_prim, ctx->stream));
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->has_xf = true;
+    ctx->bvh_dirty = true;
     return VP_OK;
 }
 
@@ -382,6 +404,7 @@ int vp_set_frame(vp_ctx *ctx, int32_t n_prim, const float *tr24) {
     VP_CUDA(ctx, cudaMemcpyAsync(&bad, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
     ctx->has_xf = !bad;
+    ctx->bvh_dirty = true;
     if (bad) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
     return VP_OK;
 }
@@ -624,7 +647,8 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         ctx->ovf_cap = int(n);
     }
     if (int rc = ensure_fallback(ctx)) return rc;
-    const MarchDev mp = make_march(ctx, cfg);
+    MarchDev mp = make_march(ctx, cfg);
+    if (int rc = ensure_bvh(ctx, mp)) return rc;
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
     if (ctx->n_prim == 0) {
         VP_CUDA(ctx, cudaMemsetAsync(od.rgb, 0, 12 * n, st));
@@ -732,7 +756,7 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
         return fail(ctx, VP_ERR_USAGE, "null ray arrays");
     cudaStream_t st = ctx->stream;
     const bool d_grads = is_device_ptr(grads);
-    DBuf<float> g, pose, adj;
+    DBuf<float> &g = ctx->s_bwd_g, &pose = ctx->s_bwd_pose, &adj = ctx->s_bwd_adj;
     float *dg = grads;
     if (!d_grads) {
         VP_CUDA(ctx, g.ensure(n_grad));
@@ -741,18 +765,16 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
     }
     if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
     if (k > 0 && n_rays > 0) {
-        // pose data on the host (exact reference code order): rBase, dR(deltaR)/dv_i
-        std::vector<float> p36(36 * size_t(k));
-        for (int i = 0; i < k; ++i) {
-            const float *tr = transforms24 + 24 * size_t(i);
-            std::memcpy(p36.data() + 36 * size_t(i), tr + 3, 9 * sizeof(float));
-            for (int q = 0; q < 3; ++q) {
-                const host::M3 r = host::rotation_derivative(host::load3(tr + 18), q);
-                std::memcpy(p36.data() + 36 * size_t(i) + 9 + 9 * q, r.m, 9 * sizeof(float));
-            }
+        // pose data on the device (k_pose36, the reference's operation order): rBase and
+        // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host]
+        VP_CUDA(ctx, pose.ensure(36 * size_t(k) + 24 * size_t(k)));
+        const float *d_tr = transforms24;
+        if (!is_device_ptr(transforms24)) {
+            VP_CUDA(ctx, cudaMemcpyAsync(pose.p + 36 * size_t(k), transforms24, 96 * size_t(k),
+                                         cudaMemcpyHostToDevice, st));
+            d_tr = pose.p + 36 * size_t(k);
         }
-        VP_CUDA(ctx, pose.ensure(p36.size()));
-        VP_CUDA(ctx, cudaMemcpyAsync(pose.p, p36.data(), p36.size() * 4, cudaMemcpyHostToDevice, st));
+        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, st));
         const size_t n = size_t(n_rays);
         RaysDev rays{origins, dirs, jitter01};
         if (!is_device_ptr(origins)) {
@@ -781,7 +803,9 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
         if (int rc = ensure_fallback(ctx)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
         const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha};
-        VP_CUDA(ctx, launch_backward_rays(make_march(ctx, cfg), ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
+        MarchDev mp = make_march(ctx, cfg);
+        if (int rc = ensure_bvh(ctx, mp)) return rc;
+        VP_CUDA(ctx, launch_backward_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
     }
@@ -809,7 +833,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     // one device block: cams | cam_index | pixel_id | pixel_xy | target | bg | o | d | jit |
     // rgb | alpha | composited | resid | adj_rgb | adj_alpha | bad flag
     const size_t cam_f = (sizeof(CamDev) * cd.size() + 15) / 16 * 4;
-    DBuf<float> buf;
+    DBuf<float> &buf = ctx->s_loss;
     const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1) + 4;
     VP_CUDA(ctx, buf.ensure(total));
     float *p = buf.p;
@@ -852,7 +876,8 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
         ctx->ovf_cap = int(nn);
     }
     if (int rc = ensure_fallback(ctx)) return rc;
-    const MarchDev mp = make_march(ctx, cfg);
+    MarchDev mp = make_march(ctx, cfg);
+    if (int rc = ensure_bvh(ctx, mp)) return rc;
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
     if (ctx->n_prim == 0) {
         VP_CUDA(ctx, cudaMemsetAsync(d_rgb, 0, 12 * nn, st));
@@ -994,7 +1019,7 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
         VP_CUDA(ctx, cudaMemsetAsync(ctx->adam_m2.p, 0, 4 * n, st));
         ctx->adam_step = 0;
     }
-    DBuf<float> tmp;  // [grads (if host) | deltas | bad flag]
+    DBuf<float> &tmp = ctx->s_adam;  // [grads (if host) | deltas | bad flag]
     VP_CUDA(ctx, tmp.ensure(n + 9 * size_t(k) + 1));
     const float *dg = grads;
     if (!is_device_ptr(grads)) {
@@ -1032,7 +1057,33 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
     VP_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
     ctx->has_xf = !bad;
+    ctx->bvh_dirty = true;
     if (bad) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+    return VP_OK;
+}
+
+int vp_debug_pose(vp_ctx *ctx, int32_t n_prim, const float *tr24, float *out36, int32_t on_device) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (n_prim < 0 || (n_prim > 0 && (!tr24 || !out36))) return fail(ctx, VP_ERR_USAGE, "bad arguments");
+    if (n_prim == 0) return VP_OK;
+    if (!on_device) {  // the host restatement (vpb_hostmath.hpp) the device kernel replaced
+        for (int i = 0; i < n_prim; ++i) {
+            const float *tr = tr24 + 24 * size_t(i);
+            std::memcpy(out36 + 36 * size_t(i), tr + 3, 9 * sizeof(float));
+            for (int q = 0; q < 3; ++q) {
+                const host::M3 r = host::rotation_derivative(host::load3(tr + 18), q);
+                std::memcpy(out36 + 36 * size_t(i) + 9 + 9 * q, r.m, 9 * sizeof(float));
+            }
+        }
+        return VP_OK;
+    }
+    DBuf<float> tmp;
+    VP_CUDA(ctx, tmp.ensure(60 * size_t(n_prim)));
+    VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, tr24, 96 * size_t(n_prim), cudaMemcpyHostToDevice, ctx->stream));
+    VP_CUDA(ctx, launch_pose36(tmp.p, n_prim, tmp.p + 24 * size_t(n_prim), ctx->stream));
+    VP_CUDA(ctx, cudaMemcpyAsync(out36, tmp.p + 24 * size_t(n_prim), 144 * size_t(n_prim), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return VP_OK;
 }
 

@@ -376,7 +376,7 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{se, sx, sc, nthreads, gtid};
-    const AllCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim};
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
     for (int64_t r = gtid; r < n_rays; r += nthreads) {
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
@@ -388,11 +388,11 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         if (cnt == 0) continue;
         const int k0 = cands.prim(w.C(0));
         const float tMin = w.E(0);
-        FwdReplay<AllCands> fwd(cands, mp, s_tab);
+        FwdReplay<BvhCands> fwd(cands, mp, s_tab);
         int st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
         if (st == 0 && fwd.lastStep >= 0) {
             const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
-            BwdWalk<AllCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
+            BwdWalk<BvhCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
             cnt = 0;
             more = false;
             window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);

@@ -1,0 +1,244 @@
+// vpb_bvh.cu — device build of the linear BVH used by arbitrary-ray marching (vpb_bvh.cuh).
+// Replaces the reference's host buildLbvh (lbvh.cpp:48-156) for march() / backwardRay /
+// evalLoss rays; camera renders use the tile lists instead (vpb_kernels.cu K1-K3).
+//
+//   k_bvh_boxes     padded world box per primitive (from the composed transform)
+//   k_bvh_bounds    one CTA: bounds of the box centres
+//   k_bvh_keys      (30-bit Morton code of the centre << 32) | primitive
+//   (sort)          CUB radix sort of the 62-bit keys
+//   k_bvh_internal  Karras (2012) hierarchy from the sorted keys: one thread per internal node
+//   k_bvh_refit     bottom-up child boxes (second arrival at a node computes it)
+//
+// The boxes only prune, so they are padded generously: a ray the exact model-space test
+// reports as a hit must never be pruned by float rounding in the world-space slab test.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cstdint>
+
+#include "vpb_bvh.cuh"
+#include "vpb_device.cuh"
+#include "vpb_kernels.h"
+
+namespace vpb {
+
+__global__ void k_bvh_boxes(const float *__restrict__ xf16, int n, float4 *__restrict__ lo,
+                            float4 *__restrict__ hi) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const float *x = xf16 + (size_t)k * kXfStride;
+    // half extent along world axis a: sum_j |R(a, j)| s_j (R column-major: R(a, j) = x[3 + 3j + a])
+    float h[3], c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        h[a] = fabsf(x[3 + a]) * x[12] + fabsf(x[6 + a]) * x[13] + fabsf(x[9 + a]) * x[14];
+        c[a] = x[a];
+        h[a] = h[a] * 1.001f + 1e-4f * (fabsf(c[a]) + h[a]) + 1e-7f;
+    }
+    lo[k] = make_float4(c[0] - h[0], c[1] - h[1], c[2] - h[2], 0.0f);
+    hi[k] = make_float4(c[0] + h[0], c[1] + h[1], c[2] + h[2], 0.0f);
+}
+
+__global__ void k_bvh_bounds(const float *__restrict__ xf16, int n, float *__restrict__ bounds) {
+    __shared__ float s[6][32];
+    float mn[3] = {3.402823466e+38f, 3.402823466e+38f, 3.402823466e+38f};
+    float mx[3] = {-3.402823466e+38f, -3.402823466e+38f, -3.402823466e+38f};
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float v = xf16[(size_t)k * kXfStride + a];
+            mn[a] = fminf(mn[a], v);
+            mx[a] = fmaxf(mx[a], v);
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s[a][wid] = mn[a];
+            s[3 + a][wid] = mx[a];
+        }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        float lo = 3.402823466e+38f, hi = -3.402823466e+38f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            lo = fminf(lo, s[a][w]);
+            hi = fmaxf(hi, s[3 + a][w]);
+        }
+        bounds[a] = lo;
+        bounds[3 + a] = hi;
+    }
+}
+
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {  // 10 bits -> every third bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_bvh_keys(const float *__restrict__ xf16, int n, const float *__restrict__ bounds,
+                           unsigned long long *__restrict__ keys) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint32_t q[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float ext = bounds[3 + a] - bounds[a];
+        const float u = ext > 0.0f ? (xf16[(size_t)k * kXfStride + a] - bounds[a]) / ext : 0.0f;
+        q[a] = (uint32_t)fminf(fmaxf(u * 1024.0f, 0.0f), 1023.0f);
+    }
+    const uint32_t morton = spread10(q[0]) | (spread10(q[1]) << 1) | (spread10(q[2]) << 2);
+    keys[k] = ((unsigned long long)morton << 32) | (uint32_t)k;
+}
+
+__device__ __forceinline__ int bvh_delta(const unsigned long long *keys, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    return __clzll(keys[i] ^ keys[j]);  // keys are distinct (primitive index in the low bits)
+}
+
+// Internal node i of n - 1. parent[] holds internal nodes at [0, n-1), leaves at n-1 + position.
+__global__ void k_bvh_internal(const unsigned long long *__restrict__ keys, int n, BvhNode *__restrict__ nodes,
+                               int *__restrict__ parent) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int d = bvh_delta(keys, n, i, i + 1) - bvh_delta(keys, n, i, i - 1) > 0 ? 1 : -1;
+    const int dmin = bvh_delta(keys, n, i, i - d);
+    int lmax = 2;
+    while (bvh_delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int t = lmax >> 1; t >= 1; t >>= 1)
+        if (bvh_delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+    const int j = i + l * d;
+    const int dnode = bvh_delta(keys, n, i, j);
+    int s = 0, t = l;
+    do {
+        t = (t + 1) >> 1;
+        if (bvh_delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    const int gamma = i + s * d + (d < 0 ? -1 : 0);
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    int left, right;
+    if (lo == gamma) {
+        left = -(int)(uint32_t)(keys[gamma] & 0xffffffffull) - 1;
+        parent[n - 1 + gamma] = i;
+    } else {
+        left = gamma;
+        parent[gamma] = i;
+    }
+    if (hi == gamma + 1) {
+        right = -(int)(uint32_t)(keys[gamma + 1] & 0xffffffffull) - 1;
+        parent[n - 1 + gamma + 1] = i;
+    } else {
+        right = gamma + 1;
+        parent[gamma + 1] = i;
+    }
+    nodes[i].d = make_int4(left, right, 0, 0);
+    if (i == 0) parent[0] = -1;
+}
+
+__global__ void k_bvh_refit(const unsigned long long *__restrict__ keys, int n, const float4 *__restrict__ lo,
+                            const float4 *__restrict__ hi, BvhNode *nodes, float4 *nlo, float4 *nhi,
+                            const int *__restrict__ parent, unsigned *flags) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int node = parent[n - 1 + p];
+    while (node >= 0) {
+        if (atomicAdd(&flags[node], 1u) == 0) return;  // the sibling subtree is not done yet
+        __threadfence();
+        const int4 ch = nodes[node].d;
+        float4 l0, h0, l1, h1;
+        if (ch.x < 0) {
+            l0 = lo[-ch.x - 1];
+            h0 = hi[-ch.x - 1];
+        } else {
+            l0 = __ldcg(nlo + ch.x);
+            h0 = __ldcg(nhi + ch.x);
+        }
+        if (ch.y < 0) {
+            l1 = lo[-ch.y - 1];
+            h1 = hi[-ch.y - 1];
+        } else {
+            l1 = __ldcg(nlo + ch.y);
+            h1 = __ldcg(nhi + ch.y);
+        }
+        nodes[node].a = make_float4(l0.x, l0.y, l0.z, h0.x);
+        nodes[node].b = make_float4(h0.y, h0.z, l1.x, l1.y);
+        nodes[node].c = make_float4(l1.z, h1.x, h1.y, h1.z);
+        nlo[node] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.0f);
+        nhi[node] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.0f);
+        __threadfence();
+        node = parent[node];
+    }
+}
+
+// Scratch carve-up, shared by the size query and the build.
+struct BvhScratch {
+    float4 *lo, *hi, *nlo, *nhi;
+    unsigned long long *k0, *k1;
+    int *parent;
+    unsigned *flags;
+    float *bounds;
+    void *cub_tmp;
+    size_t cub_bytes, total;
+};
+static BvhScratch bvh_layout(int n, void *base) {
+    BvhScratch s{};
+    unsigned char *p = static_cast<unsigned char *>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        void *q = p ? p + off : nullptr;
+        off += (bytes + 255) / 256 * 256;
+        return q;
+    };
+    s.lo = static_cast<float4 *>(take((size_t)n * 16));
+    s.hi = static_cast<float4 *>(take((size_t)n * 16));
+    s.nlo = static_cast<float4 *>(take((size_t)n * 16));
+    s.nhi = static_cast<float4 *>(take((size_t)n * 16));
+    s.k0 = static_cast<unsigned long long *>(take((size_t)n * 8));
+    s.k1 = static_cast<unsigned long long *>(take((size_t)n * 8));
+    s.parent = static_cast<int *>(take((size_t)(2 * n) * 4));
+    s.flags = static_cast<unsigned *>(take((size_t)n * 4));
+    s.bounds = static_cast<float *>(take(64));
+    cub::DeviceRadixSort::SortKeys(nullptr, s.cub_bytes, s.k0, s.k1, n, 0, 62);
+    s.cub_tmp = take(s.cub_bytes);
+    s.total = off;
+    return s;
+}
+
+size_t bvh_scratch_bytes(int n) { return n > 1 ? bvh_layout(n, nullptr).total : 0; }
+
+cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
+                             cudaStream_t st) {
+    if (n <= 1) return cudaSuccess;
+    const BvhScratch sc = bvh_layout(n, scratch);
+    if (sc.total > scratch_bytes) return cudaErrorInvalidValue;
+    float4 *lo = sc.lo, *hi = sc.hi, *nlo = sc.nlo, *nhi = sc.nhi;
+    unsigned long long *k0 = sc.k0, *k1 = sc.k1;
+    int *parent = sc.parent;
+    unsigned *flags = sc.flags;
+    float *bounds = sc.bounds;
+    void *cub_tmp = sc.cub_tmp;
+    size_t cub_bytes = sc.cub_bytes;
+    const int b = (n + 255) / 256;
+    k_bvh_boxes<<<b, 256, 0, st>>>(xf16, n, lo, hi);
+    k_bvh_bounds<<<1, 1024, 0, st>>>(xf16, n, bounds);
+    k_bvh_keys<<<b, 256, 0, st>>>(xf16, n, bounds, k0);
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, k0, k1, n, 0, 62, st);
+    if (e != cudaSuccess) return e;
+    k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(k1, n, nodes, parent);
+    cudaMemsetAsync(flags, 0, (size_t)n * 4, st);
+    k_bvh_refit<<<b, 256, 0, st>>>(k1, n, lo, hi, nodes, nlo, nhi, parent, flags);
+    return cudaGetLastError();
+}
+
+}  // namespace vpb

@@ -7,6 +7,7 @@
 //   k_compose        one thread per primitive; optionally first writes Adam's updated deltas
 //                    back into the records with the scale projection of losses.cpp:97-103
 //   k_gather_deltas  the 9 deltas per primitive, contiguous (Adam's GradBuffer order)
+//   k_pose36         backwardRay's pose data: rBase and rotationDerivative (rotation.cpp:30-38)
 //   k_sincos         test hook: the sinf / cosf port over an array
 #include <cuda_runtime.h>
 
@@ -124,6 +125,14 @@ __device__ __forceinline__ Mat3d mat_mul(const Mat3d &a, const Mat3d &o) {
     return r;
 }
 
+__device__ __forceinline__ Mat3d skew_dev(float x, float y, float z) {  // math.h:94-100
+    Mat3d k;
+    k.m[0] = 0.0f; k.m[1] = z;    k.m[2] = -y;
+    k.m[3] = -z;   k.m[4] = 0.0f; k.m[5] = x;
+    k.m[6] = y;    k.m[7] = -x;   k.m[8] = 0.0f;
+    return k;
+}
+
 // rotationFromAxisAngle (rotation.cpp:8-27): Rodrigues, I + K a + K^2 b
 __device__ __forceinline__ Mat3d rotation_from_axis_angle_dev(float vx, float vy, float vz) {
     Mat3d r;
@@ -140,14 +149,56 @@ __device__ __forceinline__ Mat3d rotation_from_axis_angle_dev(float vx, float vy
         a = __fdiv_rn(sincosf_glibc(theta, false), theta);
         b = __fdiv_rn(1.0f - sincosf_glibc(theta, true), t2);
     }
-    Mat3d k;  // skew(v), math.h:94-100
-    k.m[0] = 0.0f; k.m[1] = vz;   k.m[2] = -vy;
-    k.m[3] = -vz;  k.m[4] = 0.0f; k.m[5] = vx;
-    k.m[6] = vy;   k.m[7] = -vx;  k.m[8] = 0.0f;
+    const Mat3d k = skew_dev(vx, vy, vz);
     const Mat3d kk = mat_mul(k, k);
 #pragma unroll
     for (int i = 0; i < 9; ++i) r.m[i] = (r.m[i] + k.m[i] * a) + kk.m[i] * b;
     return r;
+}
+
+// rotationDerivative (rotation.cpp:30-38): dR(v)/dv_i, the vpb_hostmath.hpp operation order
+__device__ Mat3d rotation_derivative_dev(float vx, float vy, float vz, int i) {
+    const float t2 = (vx * vx + vy * vy) + vz * vz;
+    const float ex = i == 0 ? 1.0f : 0.0f, ey = i == 1 ? 1.0f : 0.0f, ez = i == 2 ? 1.0f : 0.0f;
+    if (t2 < 1e-14f) return skew_dev(ex, ey, ez);
+    const Mat3d r = rotation_from_axis_angle_dev(vx, vy, vz);
+    Mat3d imr;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) imr.m[q] = ((q % 4 == 0) ? 1.0f : 0.0f) - r.m[q];
+    // (I - R) e, math.h:122-124: (col0 * e.x + col1 * e.y) + col2 * e.z
+    const float ux = (imr.m[0] * ex + imr.m[3] * ey) + imr.m[6] * ez;
+    const float uy = (imr.m[1] * ex + imr.m[4] * ey) + imr.m[7] * ez;
+    const float uz = (imr.m[2] * ex + imr.m[5] * ey) + imr.m[8] * ez;
+    // cross(v, u), math.h:54-56
+    const float wx = vy * uz - vz * uy, wy = vz * ux - vx * uz, wz = vx * uy - vy * ux;
+    const Mat3d sv = skew_dev(vx, vy, vz), sw = skew_dev(wx, wy, wz);
+    const float vi = i == 0 ? vx : (i == 1 ? vy : vz);
+    const float s = __fdiv_rn(1.0f, t2);
+    Mat3d c;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) c.m[q] = (sv.m[q] * vi + sw.m[q]) * s;
+    return mat_mul(c, r);
+}
+
+// backwardRay's per-primitive pose data: rBase[9], then dR(deltaR)/dv_0..2 (27 floats).
+__global__ void k_pose36(const float *__restrict__ tr24, int n_prim, float *__restrict__ p36) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_prim) return;
+    const float *t = tr24 + (size_t)k * 24;
+    float *o = p36 + (size_t)k * 36;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) o[i] = t[3 + i];
+    for (int q = 0; q < 3; ++q) {
+        const Mat3d d = rotation_derivative_dev(t[18], t[19], t[20], q);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) o[9 + 9 * q + i] = d.m[i];
+    }
+}
+
+cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_t st) {
+    if (n_prim <= 0) return cudaSuccess;
+    k_pose36<<<(n_prim + 127) / 128, 128, 0, st>>>(tr24, n_prim, p36);
+    return cudaGetLastError();
 }
 
 // One primitive: [optional: deltas from Adam + the scale projection] then compose.

@@ -457,7 +457,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
             o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
             d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
             if (rays.jitter) jit = rays.jitter[p];
-            const AllCands cands{xf_g, payload, m3, n_prim};
+            const BvhCands cands{xf_g, payload, m3, n_prim, mp.bvh};
             ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
         } else {
             const int px = p % cam.width, py = p / cam.width;
@@ -504,7 +504,7 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const AllCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim};
+        const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
         const Window<int> w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
         ro = march_ray<CAP>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
         if (ro.overflow) {

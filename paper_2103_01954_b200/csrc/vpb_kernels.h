@@ -21,12 +21,27 @@ struct DevCounters {
 // Raymarch kernel configuration (window length, staged candidates, CTAs/SM): vpb_kernels.cu.
 enum class TileTier : int { Light = 0, Normal = 1, Dense = 2 };
 
+// Linear BVH over the primitives for arbitrary rays (vpb_bvh.cuh / vpb_bvh.cu). Internal
+// node: the boxes of both children and their indices (>= 0 internal node, < 0 leaf holding
+// primitive -(c + 1)). 64 bytes.
+struct BvhNode {
+    float4 a;  // left lo.xyz, left hi.x
+    float4 b;  // left hi.yz, right lo.xy
+    float4 c;  // right lo.z, right hi.xyz
+    int4 d;    // left, right, -, -
+};
+struct BvhDev {
+    const BvhNode *nodes;
+    int n_prim;  // 1 -> the root is primitive 0 itself
+};
+
 struct MarchDev {
     float dt, eps;
     int jitter, m;
     unsigned long long seed;
     float alpha;
     int beta;
+    BvhDev bvh;  // arbitrary-ray kernels only (vp_march_rays, backward, evalLoss)
 };
 
 struct OutDev {
@@ -106,6 +121,11 @@ cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
 // vpb_compose.cu: Frame::composed() on the device (+ Adam's delta write-back and projection)
 cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st);
 cudaError_t launch_gather_deltas(const float *tr24, int n_prim, float *deltas, cudaStream_t st);
+cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_t st);
+// vpb_bvh.cu: BVH build over the resident transforms (n - 1 nodes)
+size_t bvh_scratch_bytes(int n);
+cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
+                             cudaStream_t st);
 cudaError_t launch_sincos(const float *x, float *y, int64_t n, bool want_cos, cudaStream_t st);
 cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
                              int64_t n_px, cudaStream_t st);

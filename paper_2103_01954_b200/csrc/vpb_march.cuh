@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "vpb_bvh.cuh"
 #include "vpb_device.cuh"
 #include "vpb_kernels.h"
 
@@ -114,6 +115,26 @@ struct AllCands {  // every primitive (march over arbitrary rays)
     }
 };
 
+// Every primitive through the frame's BVH (arbitrary rays: march(), backwardRay, evalLoss).
+// The scan visits exactly the primitives whose padded box the ray crosses (window_scan
+// overload below); candidate ids are primitive ids.
+struct BvhCands {
+    const float *xf_g;
+    const float4 *payload;
+    unsigned m3;
+    int n;
+    BvhDev bvh;
+    __device__ __forceinline__ int id(int i) const { return i; }
+    __device__ __forceinline__ int prim(int c) const { return c; }
+    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ Xf16 xfv(int c) const { return ldg_xf(xf(c)); }
+    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
+    __device__ __forceinline__ bool covers(int, int2) const { return true; }
+    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
+        return intersect_obb(xf(c), o, d, tE, tX);
+    }
+};
+
 // Per-ray sorted segment window: slot j of ray `lane` lives at [j * stride + lane]
 // (conflict-free across a warp). IdxT holds the candidate index (uint8_t for staged tiles).
 template <class IdxT>
@@ -197,6 +218,19 @@ __device__ __forceinline__ void window_scan(const Win &w, const Cands &cands, in
         if (!first && !key_less(lastE, lastP, tE, prim)) continue;
         window_insert<CAP>(w, cands, cnt, more, tE, tX, c, prim);
     }
+}
+
+// window_scan over the BVH: the same predicate and insertion as the list scan, visiting the
+// primitives the BVH does not prune (no hit mask: refills traverse again).
+template <int CAP, class Win>
+__device__ __forceinline__ void window_scan(const Win &w, const BvhCands &cands, int &cnt, bool &more, V3 o,
+                                            V3 d, int2, bool first, float lastE, int lastP) {
+    bvh_for_each(cands.bvh, o, d, [&](int c) {
+        float tE, tX;
+        if (!cands.hit(c, o, d, tE, tX)) return;
+        if (!first && !key_less(lastE, lastP, tE, c)) return;
+        window_insert<CAP>(w, cands, cnt, more, tE, tX, c, c);
+    });
 }
 
 // The fused quadrature of march.cpp:18-93 over a sliding window of the ray's sorted

@@ -181,3 +181,35 @@ def test_composite_matches_reference_formula(renderer, oracle):
     with pytest.raises(api.Error) as e:
         renderer.composite(out, bg[:, :39])
     assert e.value.category == api.ErrorCategory.USAGE
+
+
+def test_arbitrary_rays_through_the_bvh_equal_brute_force(renderer, oracle):
+    """vp_march_rays prunes with the device BVH (vpb_bvh.cu); the result must equal the brute-
+    force restatement (oracle: every primitive tested) bit-for-bit, for rays from outside,
+    from far away, from inside the shell, axis-aligned and tangent to primitives."""
+    tr, pay = synthetic.shell_arrays(4096, 4)
+    xf = api.compose(tr)
+    renderer.set_scene_composed(xf, api.PrimitiveSlab(4096, 4, pay), api.WindowParams())
+    rng = np.random.default_rng(5)
+    n = 6000
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    dist = np.concatenate([rng.uniform(0.4, 2.0, n // 3), rng.uniform(20, 200, n // 3),
+                           rng.uniform(0.0, 0.3, n - 2 * (n // 3))])
+    o = (u * dist[:, None]).astype(np.float32)
+    target = rng.normal(scale=0.2, size=(n, 3))
+    d = target - o
+    d[: n // 10] = np.eye(3)[rng.integers(0, 3, n // 10)] * rng.choice([-1, 1], (n // 10, 1))
+    # tangent rays: aimed at a random primitive's corner
+    k = rng.integers(0, 4096, n // 10)
+    corner = xf[k, 0:3] + (xf[k, 3:12].reshape(-1, 3, 3).transpose(0, 2, 1) @
+                           (xf[k, 12:15] * rng.choice([-1, 1], (n // 10, 3)))[..., None])[..., 0]
+    d[n // 10: n // 5] = corner - o[n // 10: n // 5]
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    cfg = api.MarchConfig()
+    rgb, alpha, samples = renderer.march_rays(o, d, cfg)
+    orgb, oalpha, osamples = oracle.march_rays(xf, 4, pay, api.WindowParams(), o, d, cfg)
+    assert_bit_equal("rgb", rgb, orgb)
+    assert_bit_equal("alpha", alpha, oalpha)
+    assert_bit_equal("samples", samples, osamples)
+    assert (samples > 0).sum() > n // 4

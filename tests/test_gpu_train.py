@@ -147,6 +147,27 @@ def test_device_compose_equals_host_compose_on_large_angles(renderer):
     assert np.array_equal(bits(renderer.transforms()), bits(api.compose(tr)))
 
 
+def test_device_pose_data_equals_host_restatement(renderer):
+    """backwardRay's pose data (rBase + rotationDerivative, rotation.cpp:30-38) computed on the
+    device equals the host restatement bit-for-bit, across the small-angle, series and
+    large-angle branches."""
+    rng = np.random.default_rng(11)
+    k = 2048
+    tr = rng.normal(size=(k, 24)).astype(np.float32)
+    mag = 10.0 ** rng.uniform(-8, 4, size=k)
+    mag[:4] = [0, 1e-8, 1e-4, 200.0]
+    axis = rng.normal(size=(k, 3))
+    axis /= np.linalg.norm(axis, axis=1, keepdims=True)
+    tr[:, 18:21] = axis * mag[:, None]
+    lib, ctx = renderer._lib, renderer.ctx
+    from paper_2103_01954_b200._lib import f32p
+    a = np.zeros((k, 36), np.float32)
+    b = np.zeros((k, 36), np.float32)
+    assert lib.vp_debug_pose(ctx, k, tr.ctypes.data_as(f32p), a.ctypes.data_as(f32p), 1) == 0
+    assert lib.vp_debug_pose(ctx, k, tr.ctypes.data_as(f32p), b.ctypes.data_as(f32p), 0) == 0
+    assert np.array_equal(bits(a), bits(b))
+
+
 @pytest.mark.parametrize("cos", [False, True])
 def test_device_sincos_is_glibc_exact(renderer, oracle, cos):
     """The device port of glibc sinf/cosf used by compose: every float in [1e-4, 120) (the

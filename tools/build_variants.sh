@@ -12,6 +12,6 @@ for v in "$@"; do
     -DVPB_MARCH_MINB=$b -DVPB_WINDOW_CAP=$c -DVPB_CAND_CAP=$cc -DVPB_CARVEOUT=$co -c paper_2103_01954_b200/csrc/vpb_kernels.cu \
     -o build/variants/k_$v.o -Xptxas -v 2> build/variants/k_$v.log
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libvpb_$v.so build/variants/k_$v.o \
-    build/obj/vpb_backward.o build/obj/vpb_train.o build/obj/vpb_compose.o build/obj/vpb_api.o build/obj/vpb_synth.o build/obj/vpb_losses.o -cudart static
+    build/obj/vpb_backward.o build/obj/vpb_train.o build/obj/vpb_compose.o build/obj/vpb_bvh.o build/obj/vpb_api.o build/obj/vpb_synth.o build/obj/vpb_losses.o -cudart static
   echo "$v: $(grep -A2 'k_march_tilesILi' build/variants/k_$v.log | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | head -2 | tr '\n' ' ')"
 done
