@@ -486,8 +486,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
 }
 
 // march() over caller rays (one thread per ray, all primitives as candidates).
-constexpr int kRayThreads = 128;
-template <int CAP>
+template <int CAP, int kRayThreads>
 __global__ void __launch_bounds__(kRayThreads)
 k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
              const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, OutDev od,
@@ -683,8 +682,14 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st) {
     if (n_rays == 0) return cudaSuccess;
-    k_march_rays<kRayWindowCap><<<(unsigned)((n_rays + kRayThreads - 1) / kRayThreads), kRayThreads, 0, st>>>(
-        mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
+    // Each ray is a serial latency chain: small batches (evalLoss: 2048 rays) go out as
+    // one-warp CTAs so they spread over every SM instead of packing into a few.
+    if (n_rays < 148 * 128 * 2)
+        k_march_rays<kRayWindowCap, 32><<<(unsigned)((n_rays + 31) / 32), 32, 0, st>>>(
+            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
+    else
+        k_march_rays<kRayWindowCap, 128><<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(
+            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
     return cudaGetLastError();
 }
 
