@@ -141,11 +141,15 @@ int vp_copy_payload(vp_ctx *ctx, float *dst);
  * Synchronous. rgb: H*W*3, alpha: H*W, samples: H*W (nullable), stats nullable. */
 int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb,
               float *alpha, int32_t *samples, vp_stats *stats);
-/* Asynchronous variant: device output pointers only (samples nullable), enqueued on
- * `stream` (cudaStream_t; NULL = the context's stream). Counters can be read afterwards
- * with vp_read_stats (which synchronises that stream). */
-int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb_dev,
-                    float *alpha_dev, int32_t *samples_dev, void *stream);
+/* Asynchronous variant, enqueued on `stream` (cudaStream_t; NULL = the context's stream).
+ * Outputs are all device pointers (stream-ordered) or all host pointers (page-locked for
+ * overlap): then the view renders into one of two device slots and its device->host copy
+ * runs on an internal copy stream while the next view renders; call vp_sync before reading
+ * them. samples nullable. Counters can be read afterwards with vp_read_stats. */
+int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb,
+                    float *alpha, int32_t *samples, void *stream);
+/* Waits for every render and output copy the context has enqueued. */
+int vp_sync(vp_ctx *ctx);
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats);
 /* Device durations (CUDA events on the launching stream) of the raymarch kernels (K5 + K5b)
  * of the renders enqueued since the previous call, oldest first, at most the last 256.

@@ -93,6 +93,13 @@ struct vp_ctx {
     DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_adam;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
+    // vp_render_async into host memory: two device output slots; the device->host copy of
+    // one view (copy_stream) overlaps the rendering of the next
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_rendered[2] = {}, ev_copied[2] = {};
+    DBuf<float> ring_rgb[2], ring_alpha[2];
+    DBuf<int> ring_samples[2];
+    int ring_next = 0;
     DBuf<unsigned char> bvh_scratch;
     bool bvh_dirty = true;
     int64_t adam_step = 0;
@@ -303,6 +310,11 @@ int vp_create(int32_t device, vp_ctx **out) {
     if ((e = cudaSetDevice(device)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreate(&ctx->ev0)) != cudaSuccess || (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_rendered[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_rendered[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_copied[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_copied[1], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_ctr, sizeof(DevCounters))) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
@@ -323,6 +335,15 @@ int vp_destroy(vp_ctx *ctx) {
     if (!ctx) return VP_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    for (int q = 0; q < 2; ++q) {
+        ctx->ring_rgb[q].release();
+        ctx->ring_alpha[q].release();
+        ctx->ring_samples[q].release();
+        if (ctx->ev_rendered[q]) cudaEventDestroy(ctx->ev_rendered[q]);
+        if (ctx->ev_copied[q]) cudaEventDestroy(ctx->ev_copied[q]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     ctx->tr24.release();
     for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_adam}) b->release();
     ctx->flag.release();
@@ -529,8 +550,40 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
         return VP_OK;
     }
     if (int rc = ensure_render_buffers(ctx, cd)) return rc;
-    const OutDev od{rgb_dev, alpha_dev, samples_dev};
-    return enqueue_render(ctx, cd, make_march(ctx, cfg), od, st);
+    const bool host_out = !is_device_ptr(rgb_dev);
+    if (!host_out) {
+        if (!is_device_ptr(alpha_dev) || (samples_dev && !is_device_ptr(samples_dev)))
+            return fail(ctx, VP_ERR_USAGE, "outputs must be all device or all host pointers");
+        const OutDev od{rgb_dev, alpha_dev, samples_dev};
+        return enqueue_render(ctx, cd, make_march(ctx, cfg), od, st);
+    }
+    if (is_device_ptr(alpha_dev) || (samples_dev && is_device_ptr(samples_dev)))
+        return fail(ctx, VP_ERR_USAGE, "outputs must be all device or all host pointers");
+    // host outputs: render into a device slot, copy it out on copy_stream while the next view
+    // renders; the slot is reused only after its previous copy finished
+    const int q = ctx->ring_next;
+    ctx->ring_next ^= 1;
+    VP_CUDA(ctx, ctx->ring_rgb[q].ensure(3 * n_px));
+    VP_CUDA(ctx, ctx->ring_alpha[q].ensure(n_px));
+    if (samples_dev) VP_CUDA(ctx, ctx->ring_samples[q].ensure(n_px));
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copied[q], 0));
+    const OutDev od{ctx->ring_rgb[q].p, ctx->ring_alpha[q].p, samples_dev ? ctx->ring_samples[q].p : nullptr};
+    if (int rc = enqueue_render(ctx, cd, make_march(ctx, cfg), od, st)) return rc;
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_rendered[q], st));
+    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_rendered[q], 0));
+    VP_CUDA(ctx, cudaMemcpyAsync(rgb_dev, od.rgb, 12 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    VP_CUDA(ctx, cudaMemcpyAsync(alpha_dev, od.alpha, 4 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    if (samples_dev)
+        VP_CUDA(ctx, cudaMemcpyAsync(samples_dev, od.samples, 4 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[q], ctx->copy_stream));
+    return VP_OK;
+}
+
+int vp_sync(vp_ctx *ctx) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+    return VP_OK;
 }
 
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {

@@ -213,3 +213,31 @@ def test_arbitrary_rays_through_the_bvh_equal_brute_force(renderer, oracle):
     assert_bit_equal("alpha", alpha, oalpha)
     assert_bit_equal("samples", samples, osamples)
     assert (samples > 0).sum() > n // 4
+
+
+def test_async_render_into_host_memory_matches_sync(renderer):
+    """vp_render_async with page-locked host outputs (two device slots, the copy of one view
+    overlapping the next render) returns exactly what the synchronous vp_render returns."""
+    import ctypes as C
+
+    import torch
+    from paper_2103_01954_b200._lib import f32p, i32p
+    tr, pay = synthetic.shell_arrays(512, 8)
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(512, 8, pay), api.WindowParams())
+    w, views = 256, [0, 9, 17, 33, 50]
+    cams = [synthetic.shell_camera(v, 64, w) for v in views]
+    want = [renderer.render(c, api.MarchConfig()) for c in cams]
+    rgb = torch.empty((len(views), w * w * 3), dtype=torch.float32, pin_memory=True)
+    alpha = torch.empty((len(views), w * w), dtype=torch.float32, pin_memory=True)
+    samples = torch.empty((len(views), w * w), dtype=torch.int32, pin_memory=True)
+    lib, mc = renderer._lib, api.MarchConfig().to_c()
+    for j, c in enumerate(cams):
+        cc = c.to_c()
+        assert lib.vp_render_async(renderer.ctx, C.byref(cc), C.byref(mc), C.cast(rgb[j].data_ptr(), f32p),
+                                   C.cast(alpha[j].data_ptr(), f32p), C.cast(samples[j].data_ptr(), i32p),
+                                   None) == 0
+    assert lib.vp_sync(renderer.ctx) == 0
+    for j, o in enumerate(want):
+        assert_bit_equal("rgb", rgb[j].numpy().reshape(w, w, 3), o.color)
+        assert_bit_equal("alpha", alpha[j].numpy().reshape(w, w, 1), o.alpha)
+        assert_bit_equal("samples", samples[j].numpy(), o.sample_counts)
