@@ -183,7 +183,7 @@ int ensure_bvh(vp_ctx *ctx, MarchDev &mp) {
 }
 
 int ensure_fallback(vp_ctx *ctx) {
-    const size_t n = size_t(kFallbackBlocks) * kFallbackThreads * kFallbackCap;
+    const size_t n = size_t(kScratchThreads) * kFallbackCap;
     VP_CUDA(ctx, ctx->fb_e.ensure(n));
     VP_CUDA(ctx, ctx->fb_x.ensure(n));
     VP_CUDA(ctx, ctx->fb_c.ensure(n));

@@ -440,10 +440,11 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
                                  cudaStream_t st) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
-    // the scratch windows hold kFallbackBlocks * kFallbackThreads rays in flight; one-warp
-    // CTAs spread a small batch (evalLoss: 2048 rays) over every SM
-    k_backward_rays<<<kFallbackBlocks * (kFallbackThreads / 32), 32, 0, st>>>(mp, xf16, n_prim, payload, rays,
-                                                                              n_rays, bd, ctr, se, sx, sc);
+    // one-warp CTAs: a small batch (evalLoss: 2048 rays) spreads over every SM, a large one
+    // keeps kBackwardWarps * 32 rays in flight (one scratch window each)
+    const int64_t warps = (n_rays + 31) / 32;
+    k_backward_rays<<<(unsigned)(warps < kBackwardWarps ? warps : kBackwardWarps), 32, 0, st>>>(
+        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, se, sx, sc);
     return cudaGetLastError();
 }
 

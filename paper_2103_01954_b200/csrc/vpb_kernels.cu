@@ -224,42 +224,107 @@ __global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restric
     }
 }
 
-// K3b: sort each bucket ascending by (depth bits, prim). All-ascending bitonic network
-// (the "flip" formulation), so padding with +inf past n needs no special case.
-constexpr int kSortSmem = 2048;
-__global__ void k_tile_sort(const uint32_t *__restrict__ offsets,
-                            unsigned long long *__restrict__ entries, const DevCounters *ctr) {
-    __shared__ unsigned long long s[kSortSmem];
-    if (ctr->key_overflow) return;
-    const uint32_t start = offsets[blockIdx.x];
-    const int n = (int)(offsets[blockIdx.x + 1] - start);
-    if (n <= 1) return;
-    int p = 1;
-    while (p < n) p <<= 1;
-    unsigned long long *a = entries + start;
-    const bool in_smem = p <= kSortSmem;
-    if (in_smem) {
-        for (int i = threadIdx.x; i < p; i += blockDim.x) s[i] = i < n ? a[i] : ~0ull;
-        __syncthreads();
-    }
-    unsigned long long *v = in_smem ? s : a;
-    for (int k = 2; k <= p; k <<= 1) {
+// K3b: sort each bucket ascending by (depth bits, prim).
+// Buckets of up to 256 keys (all of them at the benchmark configs): one warp per bucket,
+// R = 2 or 8 keys per lane in registers, a bitonic network over 32R elements with shuffles
+// (no block barriers); the buckets past 256 keys are listed for k_tile_sort_big.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(unsigned long long (&v)[R], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < p; i += blockDim.x) {
-                const int partner = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
-                if (partner > i && (in_smem || partner < n)) {
-                    const unsigned long long x = v[i], y = v[partner];
-                    if (y < x) {
-                        v[i] = y;
-                        v[partner] = x;
+            if (j >= 32) {  // partner in another register of the same lane
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int pr = r ^ (j >> 5);
+                    if (pr > r) {
+                        const bool asc = ((lane + 32 * r) & k) == 0;
+                        const unsigned long long a = v[r], b = v[pr];
+                        if (asc ? b < a : a < b) {
+                            v[r] = b;
+                            v[pr] = a;
+                        }
                     }
                 }
+            } else {  // partner in lane ^ j
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int e = lane + 32 * r;
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool keep_min = ((e & j) == 0) == ((e & k) == 0);
+                    v[r] = keep_min ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+                }
             }
-            __syncthreads();
         }
     }
-    if (in_smem)
-        for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = s[i];
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_bucket(unsigned long long *a, int n, int lane) {
+    unsigned long long v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = lane + 32 * r < n ? a[lane + 32 * r] : ~0ull;
+    warp_bitonic<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (lane + 32 * r < n) a[lane + 32 * r] = v[r];
+}
+
+__global__ void __launch_bounds__(256)
+k_tile_sort_warp(const uint32_t *__restrict__ offsets, unsigned long long *__restrict__ entries,
+                 int n_tiles, uint32_t *__restrict__ big, DevCounters *ctr) {
+    if (ctr->key_overflow) return;
+    const int tile = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (tile >= n_tiles) return;
+    const uint32_t start = offsets[tile];
+    const int n = (int)(offsets[tile + 1] - start);
+    if (n <= 1) return;
+    if (n <= 64) warp_sort_bucket<2>(entries + start, n, lane);
+    else if (n <= 256) warp_sort_bucket<8>(entries + start, n, lane);
+    else if (lane == 0) big[atomicAdd(&ctr->big_buckets, 1u)] = (uint32_t)tile;
+}
+
+// Buckets past 256 keys: all-ascending bitonic network (the "flip" formulation), so padding
+// with +inf past n needs no special case; persistent CTAs over the list.
+constexpr int kSortSmem = 2048;
+__global__ void k_tile_sort_big(const uint32_t *__restrict__ offsets,
+                                unsigned long long *__restrict__ entries, const uint32_t *__restrict__ big,
+                                const DevCounters *ctr) {
+    __shared__ unsigned long long s[kSortSmem];
+    if (ctr->key_overflow) return;
+    for (unsigned q = blockIdx.x; q < ctr->big_buckets; q += gridDim.x) {
+        const uint32_t tile = big[q];
+        const uint32_t start = offsets[tile];
+        const int n = (int)(offsets[tile + 1] - start);
+        int p = 1;
+        while (p < n) p <<= 1;
+        unsigned long long *a = entries + start;
+        const bool in_smem = p <= kSortSmem;
+        if (in_smem) {
+            for (int i = threadIdx.x; i < p; i += blockDim.x) s[i] = i < n ? a[i] : ~0ull;
+            __syncthreads();
+        }
+        unsigned long long *v = in_smem ? s : a;
+        for (int k = 2; k <= p; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < p; i += blockDim.x) {
+                    const int partner = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
+                    if (partner > i && (in_smem || partner < n)) {
+                        const unsigned long long x = v[i], y = v[partner];
+                        if (y < x) {
+                            v[i] = y;
+                            v[partner] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (in_smem)
+            for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = s[i];
+        __syncthreads();
+    }
 }
 
 // ----------------------------------------------------------------------------------------
@@ -598,7 +663,8 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
     if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
     k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity);
     if (n_prim > 0) k_emit<<<(unsigned)((n_prim * 32ll + 255) / 256), 256, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
-    k_tile_sort<<<n_tiles, 128, 0, st>>>(offsets, entries, ctr);
+    k_tile_sort_warp<<<(n_tiles + 7) / 8, 256, 0, st>>>(offsets, entries, n_tiles, cursor, ctr);
+    k_tile_sort_big<<<148, 128, 0, st>>>(offsets, entries, cursor, ctr);
     return cudaGetLastError();
 }
 

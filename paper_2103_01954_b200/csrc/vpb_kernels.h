@@ -16,6 +16,8 @@ struct DevCounters {
     unsigned long long overflow_rays, refills, keys, numeric_fail, nonempty_tiles;
     int key_overflow;
     int fallback_fail;
+    unsigned big_buckets;  // K3b: tile buckets past 256 keys (sorted by k_tile_sort_big)
+    unsigned reserved;
 };
 
 // Raymarch kernel configuration (window length, staged candidates, CTAs/SM): vpb_kernels.cu.
@@ -76,6 +78,11 @@ struct AdamDev {
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
+// backwardRay: one-warp CTAs, as many as fit at its 232 registers (8 per SM); the scratch
+// windows (kFallbackCap entries each) are sized for the larger of the two grids
+constexpr int kBackwardWarps = 148 * 8;
+constexpr int kScratchThreads = kBackwardWarps * 32 > kFallbackBlocks * kFallbackThreads
+                                    ? kBackwardWarps * 32 : kFallbackBlocks * kFallbackThreads;
 
 size_t march_tiles_smem();
 
