@@ -366,7 +366,7 @@ __device__ __forceinline__ bool intersect_face(const float *xf, V3 o, V3 d, int 
     return !(tEnter >= tExit || tExit <= 0.0f);
 }
 
-__global__ void __launch_bounds__(kFallbackThreads)
+__global__ void __launch_bounds__(32, 12)
 k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                 const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, BwdDev bd,
                 DevCounters *ctr, float *se, float *sx, int *sc) {

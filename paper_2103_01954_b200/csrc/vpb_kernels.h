@@ -78,9 +78,9 @@ struct AdamDev {
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
-// backwardRay: one-warp CTAs, as many as fit at its 232 registers (8 per SM); the scratch
+// backwardRay: one-warp CTAs, 12 per SM (168 registers, no spills); the scratch
 // windows (kFallbackCap entries each) are sized for the larger of the two grids
-constexpr int kBackwardWarps = 148 * 8;
+constexpr int kBackwardWarps = 148 * 12;
 constexpr int kScratchThreads = kBackwardWarps * 32 > kFallbackBlocks * kFallbackThreads
                                     ? kBackwardWarps * 32 : kFallbackBlocks * kFallbackThreads;
 
