@@ -61,6 +61,16 @@ constexpr int kTimingSlots = 256;  // march-kernel event pairs kept for vp_kerne
 
 }  // namespace
 
+// Binning artefacts of one view (K1-K3 outputs + its counters). Two slots: the binning of the
+// next view runs on bin_stream while the current view marches (vpb_api.cpp enqueue_render).
+struct BinSlot {
+    DBuf<int4> rects, prects;
+    DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
+    DBuf<unsigned long long> entries;
+    DevCounters *d_ctr = nullptr;
+    cudaEvent_t ev_binned = nullptr, ev_marched = nullptr;
+};
+
 struct vp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -75,9 +85,10 @@ struct vp_ctx {
     DBuf<int> flag;        // device error flag (compose)
     bool has_xf = false;   // resident composed transforms are set
     DBuf<float4> payload;
-    DBuf<int4> rects, prects;
-    DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
-    DBuf<unsigned long long> entries;
+    BinSlot slot[2];
+    int cur = 0;  // slot of the latest render
+    BinSlot &bs() { return slot[cur]; }
+    cudaStream_t bin_stream = nullptr;
     DBuf<float> out_rgb, out_alpha;
     DBuf<int> out_samples, ovf_list;
     DBuf<float> fb_e, fb_x;
@@ -193,15 +204,17 @@ int ensure_fallback(vp_ctx *ctx) {
 int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
     const size_t n_tiles = size_t(cam.tiles_x) * cam.tiles_y;
     const size_t n_px = size_t(cam.width) * cam.height;
-    VP_CUDA(ctx, ctx->tile_counts.ensure(n_tiles));
-    VP_CUDA(ctx, ctx->offsets.ensure(n_tiles + 1));
-    VP_CUDA(ctx, ctx->cursor.ensure(n_tiles));
-    VP_CUDA(ctx, ctx->order.ensure(n_tiles));
-    VP_CUDA(ctx, ctx->rects.ensure(size_t(std::max(ctx->n_prim, 1))));
-    VP_CUDA(ctx, ctx->prects.ensure(size_t(std::max(ctx->n_prim, 1))));
-    VP_CUDA(ctx, ctx->keys.ensure(size_t(std::max(ctx->n_prim, 1))));
     if (ctx->entries_cap == 0) ctx->entries_cap = std::max<int64_t>(int64_t(1) << 20, int64_t(ctx->n_prim) * 16);
-    VP_CUDA(ctx, ctx->entries.ensure(size_t(ctx->entries_cap)));
+    for (BinSlot &b : ctx->slot) {
+        VP_CUDA(ctx, b.tile_counts.ensure(n_tiles));
+        VP_CUDA(ctx, b.offsets.ensure(n_tiles + 1));
+        VP_CUDA(ctx, b.cursor.ensure(n_tiles));
+        VP_CUDA(ctx, b.order.ensure(n_tiles));
+        VP_CUDA(ctx, b.rects.ensure(size_t(std::max(ctx->n_prim, 1))));
+        VP_CUDA(ctx, b.prects.ensure(size_t(std::max(ctx->n_prim, 1))));
+        VP_CUDA(ctx, b.keys.ensure(size_t(std::max(ctx->n_prim, 1))));
+        VP_CUDA(ctx, b.entries.ensure(size_t(ctx->entries_cap)));
+    }
     if (size_t(ctx->ovf_cap) < n_px) {
         VP_CUDA(ctx, ctx->ovf_list.ensure(n_px));
         ctx->ovf_cap = int(n_px);
@@ -209,24 +222,34 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
     return ensure_fallback(ctx);
 }
 
-// The device pipeline for one view (no host synchronisation).
+// The device pipeline for one view (no host synchronisation). Binning (K1-K3) goes to
+// bin_stream into the slot the previous view did not use, so it overlaps the previous view's
+// raymarch (whose tail leaves SMs idle); the raymarch waits for it on `st`. A slot is rebinned
+// only after the raymarch that read it (two views back) has finished.
 int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const OutDev &od,
                    cudaStream_t st) {
-    VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
-                                ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->order.p, ctx->entries.p,
-                                ctx->entries_cap, ctx->d_ctr, st));
+    ctx->cur ^= 1;
+    BinSlot &b = ctx->bs();
+    ctx->d_ctr = b.d_ctr;
+    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
+    VP_CUDA(ctx, cudaMemsetAsync(b.d_ctr, 0, sizeof(DevCounters), ctx->bin_stream));
+    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p, b.tile_counts.p,
+                                b.offsets.p, b.cursor.p, b.order.p, b.entries.p, ctx->entries_cap, b.d_ctr,
+                                ctx->bin_stream));
+    VP_CUDA(ctx, cudaEventRecord(b.ev_binned, ctx->bin_stream));
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, b.ev_binned, 0));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
-    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->prects.p, ctx->payload.p, ctx->offsets.p,
-                                    ctx->order.p, ctx->entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
+    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->bs().prects.p, ctx->payload.p, ctx->bs().offsets.p,
+                                    ctx->bs().order.p, ctx->bs().entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     const RaysDev none{nullptr, nullptr, nullptr};
-    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->prects.p, ctx->n_prim, ctx->payload.p,
-                                       ctx->offsets.p, ctx->entries.p, od, none, ctx->d_ctr,
+    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->bs().prects.p, ctx->n_prim, ctx->payload.p,
+                                       ctx->bs().offsets.p, ctx->bs().entries.p, od, none, ctx->d_ctr,
                                        ctx->ovf_list.p, ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p,
                                        ctx->fb_c.p, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
+    VP_CUDA(ctx, cudaEventRecord(b.ev_marched, st));
     ++ctx->t_count;
     return VP_OK;
 }
@@ -315,8 +338,16 @@ int vp_create(int32_t device, vp_ctx **out) {
         (e = cudaEventCreateWithFlags(&ctx->ev_rendered[1], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[1], cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_ctr, sizeof(DevCounters))) != cudaSuccess ||
-        (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
+        (e = cudaStreamCreateWithFlags(&ctx->bin_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->slot[0].d_ctr, sizeof(DevCounters))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->slot[1].d_ctr, sizeof(DevCounters))) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->slot[0].ev_binned, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->slot[1].ev_binned, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->slot[0].ev_marched, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->slot[1].ev_marched, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess ||
+        (e = cudaMemset(ctx->slot[0].d_ctr, 0, sizeof(DevCounters))) != cudaSuccess ||
+        (e = cudaMemset(ctx->slot[1].d_ctr, 0, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
         vp_destroy(ctx);
         return rc;
@@ -327,6 +358,7 @@ int vp_create(int32_t device, vp_ctx **out) {
         vp_destroy(ctx);
         return rc;
     }
+    ctx->d_ctr = ctx->slot[0].d_ctr;
     *out = ctx;
     return VP_OK;
 }
@@ -336,6 +368,7 @@ int vp_destroy(vp_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    if (ctx->bin_stream) cudaStreamSynchronize(ctx->bin_stream);
     for (int q = 0; q < 2; ++q) {
         ctx->ring_rgb[q].release();
         ctx->ring_alpha[q].release();
@@ -351,12 +384,17 @@ int vp_destroy(vp_ctx *ctx) {
                     &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
         b->release();
     ctx->payload.release();
-    ctx->rects.release();
-    ctx->prects.release();
-    for (auto *b : {&ctx->keys, &ctx->tile_counts, &ctx->offsets, &ctx->cursor, &ctx->order}) b->release();
-    ctx->entries.release();
+    for (BinSlot &b : ctx->slot) {
+        b.rects.release();
+        b.prects.release();
+        for (auto *u : {&b.keys, &b.tile_counts, &b.offsets, &b.cursor, &b.order}) u->release();
+        b.entries.release();
+        if (b.d_ctr) cudaFree(b.d_ctr);
+        if (b.ev_binned) cudaEventDestroy(b.ev_binned);
+        if (b.ev_marched) cudaEventDestroy(b.ev_marched);
+    }
+    if (ctx->bin_stream) cudaStreamDestroy(ctx->bin_stream);
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
-    if (ctx->d_ctr) cudaFree(ctx->d_ctr);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -765,8 +803,8 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->rects.p, ctx->prects.p, ctx->keys.p,
-                                    ctx->tile_counts.p, ctx->offsets.p, ctx->cursor.p, ctx->order.p, ctx->entries.p,
+        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->bs().rects.p, ctx->bs().prects.p, ctx->bs().keys.p,
+                                    ctx->bs().tile_counts.p, ctx->bs().offsets.p, ctx->bs().cursor.p, ctx->bs().order.p, ctx->bs().entries.p,
                                     ctx->entries_cap, ctx->d_ctr, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
         VP_CUDA(ctx, cudaStreamSynchronize(st));
@@ -778,15 +816,15 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
         const size_t nk = size_t(c.keys);
         if (n_keys) *n_keys = int64_t(nk);
         if (rect4 && ctx->n_prim > 0)
-            VP_CUDA(ctx, cudaMemcpy(rect4, ctx->rects.p, sizeof(int4) * ctx->n_prim, cudaMemcpyDeviceToHost));
+            VP_CUDA(ctx, cudaMemcpy(rect4, ctx->bs().rects.p, sizeof(int4) * ctx->n_prim, cudaMemcpyDeviceToHost));
         if (depth_key && ctx->n_prim > 0)
-            VP_CUDA(ctx, cudaMemcpy(depth_key, ctx->keys.p, sizeof(uint32_t) * ctx->n_prim, cudaMemcpyDeviceToHost));
+            VP_CUDA(ctx, cudaMemcpy(depth_key, ctx->bs().keys.p, sizeof(uint32_t) * ctx->n_prim, cudaMemcpyDeviceToHost));
         if (tile_offsets)
-            VP_CUDA(ctx, cudaMemcpy(tile_offsets, ctx->offsets.p, sizeof(uint32_t) * (n_tiles + 1),
+            VP_CUDA(ctx, cudaMemcpy(tile_offsets, ctx->bs().offsets.p, sizeof(uint32_t) * (n_tiles + 1),
                                     cudaMemcpyDeviceToHost));
         if (tile_prims && cap > 0 && nk > 0) {
             std::vector<unsigned long long> e(nk);
-            VP_CUDA(ctx, cudaMemcpy(e.data(), ctx->entries.p, nk * 8, cudaMemcpyDeviceToHost));
+            VP_CUDA(ctx, cudaMemcpy(e.data(), ctx->bs().entries.p, nk * 8, cudaMemcpyDeviceToHost));
             for (size_t i = 0; i < nk && int64_t(i) < cap; ++i) tile_prims[i] = int32_t(e[i] & 0xffffffffull);
         }
         return VP_OK;
