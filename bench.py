@@ -341,9 +341,9 @@ def main():
         st = vp_stats()
 
         def e2e_step():
-            # per step: the frame's transforms host->device, every view rendered into pinned
-            # host memory (each view's device->host copy overlaps the next view's render),
-            # then wait for all outputs
+            # per step: the frame's transforms host->device, then every view rendered into
+            # pinned host memory; each view's device->host copy overlaps the next render (also
+            # across steps); vp_sync after the last step waits for every copy
             if lib.vp_set_transforms(r.ctx, k, C.cast(xf_host.data_ptr(), f32p)):
                 raise RuntimeError(lib.vp_last_error(r.ctx).decode())
             for j, cam in enumerate(cams):
@@ -351,23 +351,27 @@ def main():
                                        C.cast(h_alpha[j].data_ptr(), f32p), C.cast(h_samp[j].data_ptr(), i32p),
                                        None):
                     raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+
+        def e2e_finish():
             if lib.vp_sync(r.ctx) or lib.vp_read_stats(r.ctx, C.byref(st)):
                 raise RuntimeError(lib.vp_last_error(r.ctx).decode())
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
+        e2e_finish()
         n_e2e = max(3, args.steps // 2)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()
+        e2e_finish()
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(all_ray / args.steps * n_e2e / float(te.item()) / 1e6, 3), "unit": METRIC,
                "h2d_bytes_per_step": 15 * 4 * k, "d2h_bytes_per_step": BYTES_PER_PIXEL * n_px * V,
-               "steps": n_e2e, "api": "vp_set_transforms + vp_render_async into pinned host outputs + vp_sync"}
+               "steps": n_e2e, "api": "vp_set_transforms + vp_render_async into pinned host outputs, vp_sync at the end"}
 
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
