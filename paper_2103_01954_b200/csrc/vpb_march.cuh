@@ -100,20 +100,6 @@ struct TileCands {
         return intersect_obb(xf(c), o, d, tE, tX);
     }
 };
-struct AllCands {  // every primitive (march over arbitrary rays)
-    const float *xf_g;
-    const float4 *payload;
-    unsigned m3;
-    int n;
-    __device__ __forceinline__ int prim(int c) const { return c; }
-    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
-    __device__ __forceinline__ Xf16 xfv(int c) const { return ldg_xf(xf(c)); }
-    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
-    __device__ __forceinline__ bool covers(int, int2) const { return true; }
-    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
-        return intersect_obb(xf(c), o, d, tE, tX);
-    }
-};
 
 // Every primitive through the frame's BVH (arbitrary rays: march(), backwardRay, evalLoss).
 // The scan visits exactly the primitives whose padded box the ray crosses (window_scan
