@@ -832,10 +832,14 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     return fail(ctx, VP_ERR_DEVICE, "tile key buffer could not be sized");
 }
 
-int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
-                     const float *jitter01, const float *adj_rgb, const float *adj_alpha,
-                     const vp_march *cfg, const float *transforms24, float *grads,
-                     int32_t accumulate) {
+}  // extern "C"
+
+namespace {
+// backwardRay over a batch; fwd_state (device, 8 floats per ray, written by the forward march
+// of the same rays) lets the kernel skip its replay of march().
+int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs, const float *jitter01,
+                  const float *adj_rgb, const float *adj_alpha, const vp_march *cfg, const float *transforms24,
+                  float *grads, int32_t accumulate, const float *fwd_state) {
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n_rays < 0) return fail(ctx, VP_ERR_USAGE, "negative ray count");
@@ -893,7 +897,7 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
         }
         if (int rc = ensure_fallback(ctx)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha};
+        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state};
         MarchDev mp = make_march(ctx, cfg);
         if (int rc = ensure_bvh(ctx, mp)) return rc;
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
@@ -905,6 +909,18 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
     if (k > 0 && n_rays > 0) return check_counters(ctx, *ctx->h_ctr);
     return VP_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
+                     const float *jitter01, const float *adj_rgb, const float *adj_alpha,
+                     const vp_march *cfg, const float *transforms24, float *grads,
+                     int32_t accumulate) {
+    return backward_rays(ctx, n_rays, origins, dirs, jitter01, adj_rgb, adj_alpha, cfg, transforms24, grads,
+                         accumulate, nullptr);
+}
+
 
 int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t n,
                      const int32_t *cam_index, const float *pixel_xy, const int32_t *pixel_id,
@@ -922,10 +938,10 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     std::vector<CamDev> cd(static_cast<size_t>(n_cams));
     for (int32_t c = 0; c < n_cams; ++c) cd[size_t(c)] = make_cam(cams[c]);
     // one device block: cams | cam_index | pixel_id | pixel_xy | target | bg | o | d | jit |
-    // rgb | alpha | composited | resid | adj_rgb | adj_alpha | bad flag
+    // rgb | alpha | composited | resid | adj_rgb | adj_alpha | forward state | bad flag
     const size_t cam_f = (sizeof(CamDev) * cd.size() + 15) / 16 * 4;
     DBuf<float> &buf = ctx->s_loss;
-    const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1) + 4;
+    const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1 + 8) + 4;
     VP_CUDA(ctx, buf.ensure(total));
     float *p = buf.p;
     CamDev *d_cams = reinterpret_cast<CamDev *>(p);
@@ -944,6 +960,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     float *d_res = p; p += 3 * nn;
     float *d_ar = p; p += 3 * nn;
     float *d_aa = p; p += nn;
+    float *d_state = p; p += 8 * nn;  // forward MarchResult bookkeeping for the backward
     int *d_bad = reinterpret_cast<int *>(p);
     VP_CUDA(ctx, cudaMemcpyAsync(d_cams, cd.data(), sizeof(CamDev) * cd.size(), cudaMemcpyHostToDevice, st));
     VP_CUDA(ctx, cudaMemcpyAsync(d_ci, cam_index, 4 * nn, cudaMemcpyDefault, st));
@@ -961,7 +978,8 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     if (h_bad == 2) return fail(ctx, VP_ERR_USAGE, "pixel outside image bounds");  // camera.cpp:15-16
     // forward march of the batch (evalLoss, grad.cpp:216-226)
     const RaysDev rays{d_o, d_d, d_j};
-    const OutDev od{d_rgb, d_a, nullptr};
+    OutDev od{d_rgb, d_a, nullptr};
+    od.state = d_state;
     if (size_t(ctx->ovf_cap) < nn) {
         VP_CUDA(ctx, ctx->ovf_list.ensure(nn));
         ctx->ovf_cap = int(nn);
@@ -1000,7 +1018,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     if (loss_pho) *loss_pho = lambda_pho * invN * acc;
     if (!grads) return VP_OK;
     // backwardRay for every ray with the photometric adjoints (grad.cpp:240-248)
-    return vp_backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate);
+    return backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate, d_state);
 }
 
 int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, uint64_t *out,

@@ -389,13 +389,28 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const int k0 = cands.prim(w.C(0));
         const float tMin = w.E(0);
         FwdReplay<BvhCands> fwd(cands, mp, s_tab);
-        int st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
+        int st = 0;
+        const bool have_fwd = bd.fwd_state != nullptr;
+        if (have_fwd) {  // the forward pass of this very ray recorded the replay's results
+            const float *s = bd.fwd_state + 8 * r;
+            fwd.lastStep = __float_as_int(s[0]);
+            fwd.saturated = __float_as_int(s[1]) != 0;
+            fwd.satTPrev = s[2];
+            fwd.satSigmaSum = s[3];
+            fwd.satR = s[4];
+            fwd.satG = s[5];
+            fwd.satB = s[6];
+        } else {
+            st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
+        }
         if (st == 0 && fwd.lastStep >= 0) {
             const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
             BwdWalk<BvhCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
-            cnt = 0;
-            more = false;
-            window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+            if (!have_fwd) {  // the replay consumed the window
+                cnt = 0;
+                more = false;
+                window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+            }
             st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
             if (st == 0 && bw.gTmin != 0.f) {  // t_min anchor chain (grad.cpp:166-194)
                 const float *xf = cands.xf(k0);

@@ -51,6 +51,7 @@ struct OutDev {
     float *alpha;
     int *samples;
     unsigned long long *prof = nullptr;  // per CTA: tile, SM id, start ns, end ns (debug)
+    float *state = nullptr;  // arbitrary rays: 8 floats per ray of MarchResult bookkeeping
 };
 
 struct RaysDev {
@@ -68,6 +69,7 @@ struct BwdDev {
     const float *pose36;
     const float *adj_rgb;
     const float *adj_alpha;
+    const float *fwd_state = nullptr;  // the forward's per-ray state (skips the replay), or null
 };
 
 // Adam step constants (losses.cpp:70-104); bc1/bc2 = 1 - beta^step computed on the host.

@@ -142,6 +142,9 @@ struct RayOut {
     int samples;
     int prim_samples;
     int hit, early, saturated, overflow, refills, numeric;
+    // MarchResult bookkeeping backwardRay needs (march.h:22-33); dead code unless stored
+    int last_step = -1;
+    float sat_tprev = 0.f, sat_sigma = 0.f, sat_r = 0.f, sat_g = 0.f, sat_b = 0.f;
 };
 
 __device__ __forceinline__ bool key_less(float ea, int pa, float eb, int pb) {
@@ -347,6 +350,7 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
         act = (act & ~retire) | admit;
         admit = 0;
         ++out.samples;
+        out.last_step = i;
         const float dT = sigmaSum * dt;
         if (transmittance + dT >= 1.0f) {
             const float frac = (1.0f - transmittance) / dT;
@@ -354,6 +358,11 @@ __device__ RayOut march_window(const Cands &cands, const Win &w, int cnt, bool m
             cr += rw * f;
             cg += gw * f;
             cb += bw * f;
+            out.sat_tprev = transmittance;
+            out.sat_sigma = sigmaSum;
+            out.sat_r = rw;
+            out.sat_g = gw;
+            out.sat_b = bw;
             transmittance = 1.0f;
             out.saturated = 1;
             break;
@@ -485,6 +494,7 @@ __device__ RayOut march_window_generic(const Cands &cands, const Win &w, int cnt
         // step complete: march.cpp:71-88
         sampling = false;
         ++out.samples;
+        out.last_step = (int)i;
         const float dT = sigmaSum * dt;
         if (transmittance + dT >= 1.0f) {
             const float frac = (1.0f - transmittance) / dT;
@@ -492,6 +502,11 @@ __device__ RayOut march_window_generic(const Cands &cands, const Win &w, int cnt
             cr += rw * f;
             cg += gw * f;
             cb += bw * f;
+            out.sat_tprev = transmittance;
+            out.sat_sigma = sigmaSum;
+            out.sat_r = rw;
+            out.sat_g = gw;
+            out.sat_b = bw;
             transmittance = 1.0f;
             out.saturated = 1;
             break;
@@ -533,6 +548,16 @@ __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const R
     od.rgb[3 * p + 2] = ro.b;
     od.alpha[p] = ro.alpha;
     if (od.samples) od.samples[p] = ro.samples;
+    if (od.state) {  // per-ray forward state for a following backward pass (evalLoss)
+        float *s = od.state + 8 * p;
+        s[0] = __int_as_float(ro.last_step);
+        s[1] = __int_as_float(ro.saturated);
+        s[2] = ro.sat_tprev;
+        s[3] = ro.sat_sigma;
+        s[4] = ro.sat_r;
+        s[5] = ro.sat_g;
+        s[6] = ro.sat_b;
+    }
 }
 
 // Warp-aggregated counter update: one atomic per warp per counter.
