@@ -80,32 +80,43 @@ __global__ void k_adam_check(const float *__restrict__ g, int64_t n, int *__rest
         if (!isfinite(g[i])) atomicExch(bad, 1);
 }
 
-// One Adam step over [payload (planar GradBuffer order) | 9K deltas]; the payload parameter
-// with planar index (k, ch, v) lives at payload[k * m3 + v].ch (channel-interleaved).
+// One Adam step over [payload (planar GradBuffer order) | 9K deltas] (losses.cpp:81-92). The
+// payload parameter with planar index (k, ch, v) lives at payload[k * m3 + v].ch
+// (channel-interleaved), so a thread takes one voxel: its float4 is read and written once,
+// and the four channels' gradient and moments are coalesced across the warp (consecutive v).
+__device__ __forceinline__ float adam_one(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
+                                          int64_t i, float lr, const AdamDev &c) {
+    const float gi = g[i];
+    const float a = c.beta1 * m1[i] + (1.0f - c.beta1) * gi;
+    const float b = c.beta2 * m2[i] + (1.0f - c.beta2) * gi * gi;
+    m1[i] = a;
+    m2[i] = b;
+    const float mHat = a / c.bc1;
+    const float vHat = b / c.bc2;
+    return lr * mHat / (sqrtf(vHat) + c.eps);
+}
+
 __global__ void k_adam_update(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
                               float4 *__restrict__ payload, float *__restrict__ deltas, int64_t n_pay,
                               int64_t n, unsigned m3, AdamDev c) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float gi = g[i];
-        const float a = c.beta1 * m1[i] + (1.0f - c.beta1) * gi;
-        const float b = c.beta2 * m2[i] + (1.0f - c.beta2) * gi * gi;
-        m1[i] = a;
-        m2[i] = b;
-        const float mHat = a / c.bc1;
-        const float vHat = b / c.bc2;
-        const float lr = c.lr * (i < n_pay ? 1.0f : c.lr_delta_scale);
-        const float step = lr * mHat / (sqrtf(vHat) + c.eps);
-        if (i < n_pay) {
-            const int64_t k = i / (4 * (int64_t)m3), r = i - k * 4 * (int64_t)m3;
-            const int ch = (int)(r / m3);
-            const int64_t v = r - (int64_t)ch * m3;
-            float *p = reinterpret_cast<float *>(payload + k * m3 + v) + ch;
-            float nv = *p - step;
-            if (nv < 0.0f) nv = 0.0f;  // feasibility projection (losses.cpp:95-96)
-            *p = nv;
+    const int64_t n_vox = n_pay / 4, total = n_vox + (n - n_pay);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        if (q < n_vox) {
+            const int64_t k = q / m3, v = q - k * m3;
+            float4 pv = payload[q];
+            float *pf = &pv.x;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                const float step = adam_one(g, m1, m2, (k * 4 + ch) * (int64_t)m3 + v, c.lr * 1.0f, c);
+                float nv = pf[ch] - step;
+                if (nv < 0.0f) nv = 0.0f;  // feasibility projection (losses.cpp:95-96)
+                pf[ch] = nv;
+            }
+            payload[q] = pv;
         } else {
+            const int64_t i = n_pay + (q - n_vox);
             float *p = deltas + (i - n_pay);
-            *p = *p - step;
+            *p = *p - adam_one(g, m1, m2, i, c.lr * c.lr_delta_scale, c);
         }
     }
 }
