@@ -580,6 +580,51 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     add_counters(ctr, ro, valid && !ro.overflow);
 }
 
+// march() over caller rays, one warp per ray (small batches): lane 0 collects the ray's whole
+// sorted segment list through the BVH into the warp's shared-memory list, then the warp walks
+// it 32 lattice steps at a time (march_warp). Rays with more than kWarpList segments go to the
+// wide-window fallback like window overflows.
+constexpr int kWarpList = 96;
+__global__ void __launch_bounds__(128)
+k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+                  RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
+                  int ovf_cap) {
+    __shared__ unsigned long long s_tab[32];
+    __shared__ float s_e[4][kWarpList], s_x[4][kWarpList];
+    __shared__ int s_c[4][kWarpList];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
+    for (int64_t r = blockIdx.x * 4 + wid; r < n_rays; r += (int64_t)gridDim.x * 4) {
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        int cnt = 0;
+        bool more = false;
+        if (lane == 0) {
+            const Window<int> w{s_e[wid], s_x[wid], s_c[wid], 1, 0};
+            window_scan<kWarpList>(w, cands, cnt, more, o, d, make_int2(0, 0), true, 0.f, 0);
+        }
+        cnt = __shfl_sync(0xffffffffu, cnt, 0);
+        more = __shfl_sync(0xffffffffu, more ? 1 : 0, 0) != 0;
+        __syncwarp();
+        RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (more) {
+            ro.overflow = 1;
+            if (lane == 0) {
+                const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
+                if (slot < ovf_cap) ovf_list[slot] = (int)r;
+            }
+        } else {
+            ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane);
+            if (lane == 0) write_pixel(od, r, ro);
+        }
+        add_counters(ctr, ro, lane == 0 && !ro.overflow);
+        __syncwarp();
+    }
+}
+
 // composite() is elementwise (march.cpp:134-147).
 __global__ void k_composite(const float *__restrict__ rgb, const float *__restrict__ alpha,
                             const float *__restrict__ bg, float *__restrict__ out, int64_t n_px) {
@@ -748,8 +793,14 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st) {
     if (n_rays == 0) return cudaSuccess;
-    // Each ray is a serial latency chain: small batches (evalLoss: 2048 rays) go out as
-    // one-warp CTAs so they spread over every SM instead of packing into a few.
+    // Each ray is a serial latency chain: small batches (evalLoss: 2048 rays) are marched a
+    // warp per ray, 32 lattice steps at a time; mid-size ones go out as one-warp CTAs so they
+    // spread over every SM instead of packing into a few.
+    if (n_rays <= kWarpRayBatch) {
+        k_march_rays_warp<<<(unsigned)((n_rays + 3) / 4), 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays,
+                                                                        od, ctr, ovf_list, ovf_cap);
+        return cudaGetLastError();
+    }
     if (n_rays < 148 * 128 * 2)
         k_march_rays<kRayWindowCap, 32><<<(unsigned)((n_rays + 31) / 32), 32, 0, st>>>(
             mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);

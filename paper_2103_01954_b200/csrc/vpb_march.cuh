@@ -529,6 +529,115 @@ done:
     return out;
 }
 
+// Step-parallel march of ONE ray by a warp (small ray batches, e.g. evalLoss's 2048 rays,
+// where one thread per ray leaves the GPU idle while the longest rays walk hundreds of steps).
+// E/X/P hold the ray's complete sorted segment list (cnt entries, no refill). Lane L takes
+// lattice step base + L: its active set {j : E_j <= ts < X_j} in list order is exactly the
+// reference's incremental `active` list at that step (admission in list order, retirement at
+// X <= ts), so each lane forms the step's sums with the same operations as march_window.
+// The visited sequence is then replayed in order: consecutive steps while the active set is
+// non-empty, and at the first empty one the reference's gap skip (march.cpp:43-49) picks the
+// next chunk's base. Transmittance and colour are accumulated serially over the chunk's
+// steps (every lane computes the same values from shuffles), so the result is bit-identical.
+template <class Cands>
+__device__ RayOut march_warp(const Cands &cands, const float *E, const float *X, const int *P, int cnt, V3 o,
+                             V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane) {
+    RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (cnt == 0) return out;
+    out.hit = 1;
+    const float dt = mp.dt, t0 = E[0];
+    constexpr int kMaxStep = 1 << 30;
+    float T = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    int base = 0;
+    bool done = false;
+    while (!done) {
+        if (base > kMaxStep) {
+            out.numeric = 1;
+            break;
+        }
+        const int i = base + lane;
+        const bool in_range = i <= kMaxStep;
+        const float ts = t0 + (__int2float_rn(i) + jit) * dt;
+        const V3 pw = o + d * ts;
+        float sig = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
+        int na = 0, nadm = 0;
+        for (int j = 0; j < cnt && in_range; ++j) {
+            if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
+            nadm = j + 1;
+            if (X[j] > ts) {
+                const int c = P[j];
+                float sg, r, g, b;
+                const Xf16 xr = cands.xfv(c);
+                sample_primitive<0>(cands.base(c), mp.m, xr.v, pw, mp.alpha, mp.beta, tab, sg, r, g, b);
+                sig += sg;
+                rw += r * sg;
+                gw += g * sg;
+                bw += b * sg;
+                ++na;
+            }
+        }
+        const unsigned empty = __ballot_sync(0xffffffffu, !(in_range && na > 0));
+        const int L = empty ? __ffs(empty) - 1 : 32;
+        for (int s = 0; s < L; ++s) {  // the chunk's visited steps, in order (march.cpp:71-88)
+            const float s_sig = __shfl_sync(0xffffffffu, sig, s);
+            const float s_rw = __shfl_sync(0xffffffffu, rw, s);
+            const float s_gw = __shfl_sync(0xffffffffu, gw, s);
+            const float s_bw = __shfl_sync(0xffffffffu, bw, s);
+            const int s_na = __shfl_sync(0xffffffffu, na, s);
+            if (done) continue;
+            ++out.samples;
+            out.prim_samples += s_na;
+            out.last_step = base + s;
+            const float dT = s_sig * dt;
+            if (T + dT >= 1.0f) {
+                const float frac = (1.0f - T) / dT;
+                const float f = dt * frac;
+                cr += s_rw * f;
+                cg += s_gw * f;
+                cb += s_bw * f;
+                out.sat_tprev = T;
+                out.sat_sigma = s_sig;
+                out.sat_r = s_rw;
+                out.sat_g = s_gw;
+                out.sat_b = s_bw;
+                T = 1.0f;
+                out.saturated = 1;
+                done = true;
+                continue;
+            }
+            cr += s_rw * dt;
+            cg += s_gw * dt;
+            cb += s_bw * dt;
+            T += dT;
+            if (T > 1.0f - mp.eps) {
+                out.early = 1;
+                done = true;
+            }
+        }
+        if (done) break;
+        if (L == 32) {
+            base += 32;
+            continue;
+        }
+        const int iL = base + L;  // visited with an empty active set
+        if (iL > kMaxStep) {
+            out.numeric = 1;
+            break;
+        }
+        const int nadmL = __shfl_sync(0xffffffffu, nadm, L);
+        if (nadmL >= cnt) break;  // nothing left to admit: march.cpp:43-44
+        const float nextE = E[nadmL];
+        const double sk = ceil((double)((nextE - t0) / dt) - (double)jit);  // gap skip, march.cpp:45-49
+        const int skipTo = sk > (double)kMaxStep ? kMaxStep + 1 : (int)sk;
+        base = skipTo > iL + 1 ? skipTo : iL + 1;
+    }
+    out.r = cr;
+    out.g = cg;
+    out.b = cb;
+    out.alpha = T;
+    return out;
+}
+
 template <int CAP, class Cands, class Win>
 __device__ __forceinline__ RayOut march_ray(const Cands &cands, const Win &w, V3 o, V3 d,
                                             int2 px, float jit, const MarchDev &mp,
