@@ -366,6 +366,85 @@ __device__ __forceinline__ bool intersect_face(const float *xf, V3 o, V3 d, int 
     return !(tEnter >= tExit || tExit <= 0.0f);
 }
 
+// The t_min anchor chain (grad.cpp:166-194): the first hit's entry depends on the pose of the
+// first primitive (k0) through its entry face.
+template <class Cands>
+__device__ void anchor_chain(BwdWalk<Cands> &bw, const Cands &cands, const BwdDev &bd, int k0, float tMin,
+                             float gTmin, V3 o, V3 d) {
+    if (gTmin == 0.f) return;
+    const float *xf = cands.xf(k0);
+    int axis, sign;
+    bool clamped;
+    if (!intersect_face(xf, o, d, axis, sign, clamped) || clamped) return;
+    const int j = axis;
+    const float c = (float)sign;
+    const V3 q = mk3(xf[3 + 3 * j], xf[4 + 3 * j], xf[5 + 3 * j]);
+    const float qd = dot3(q, d);
+    if (qd == 0.0f) return;
+    const float gT = gTmin;
+    bw.pose_add(k0, 0, q * (gT / qd));
+    V3 gS = mk3(0.f, 0.f, 0.f);
+    const float gsj = gT * c / qd;
+    if (j == 0) gS.x = gsj;
+    else if (j == 1) gS.y = gsj;
+    else gS.z = gsj;
+    bw.pose_add(k0, 6, gS);
+    const V3 toT = mk3(xf[0], xf[1], xf[2]) - o;
+    const float *pose = bd.pose36 + 36 * (size_t)k0;
+    const V3 rj = mk3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2]);
+    float gR[3];
+#pragma unroll
+    for (int ii = 0; ii < 3; ++ii) {
+        const V3 qp = matvec(pose + 9 + 9 * ii, rj);
+        gR[ii] = gT * (dot3(qp, toT) - tMin * dot3(qp, d)) / qd;
+    }
+    bw.pose_add(k0, 3, mk3(gR[0], gR[1], gR[2]));
+}
+
+__device__ __forceinline__ void load_fwd_state(FwdReplay<BvhCands> &fwd, const float *s) {
+    fwd.lastStep = __float_as_int(s[0]);
+    fwd.saturated = __float_as_int(s[1]) != 0;
+    fwd.satTPrev = s[2];
+    fwd.satSigmaSum = s[3];
+    fwd.satR = s[4];
+    fwd.satG = s[5];
+    fwd.satB = s[6];
+}
+
+// backwardRay of one ray by one thread with a kFallbackCap-entry window; returns 0, or 1 / 2
+// (window overflow / runaway walk).
+template <class Win>
+__device__ int backward_one_ray(const BvhCands &cands, const Win &w, const MarchDev &mp,
+                                const unsigned long long *tab, const BwdDev &bd, V3 o, V3 d, float jit,
+                                int64_t r) {
+    const int2 px = make_int2(0, 0);
+    int cnt = 0;
+    bool more = false;
+    window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+    if (cnt == 0) return 0;
+    const int k0 = cands.prim(w.C(0));
+    const float tMin = w.E(0);
+    FwdReplay<BvhCands> fwd(cands, mp, tab);
+    int st = 0;
+    const bool have_fwd = bd.fwd_state != nullptr;
+    if (have_fwd)  // the forward pass of this very ray recorded the replay's results
+        load_fwd_state(fwd, bd.fwd_state + 8 * r);
+    else
+        st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
+    if (st != 0 || fwd.lastStep < 0) return st;
+    const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
+    BwdWalk<BvhCands> bw(cands, mp, tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
+    if (!have_fwd) {  // the replay consumed the window
+        cnt = 0;
+        more = false;
+        window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+    }
+    st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
+    if (st == 0) anchor_chain(bw, cands, bd, k0, tMin, bw.gTmin, o, d);
+    bw.flush();
+    return st;
+}
+
 __global__ void __launch_bounds__(32, 12)
 k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                 const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, BwdDev bd,
@@ -381,72 +460,102 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const int2 px = make_int2(0, 0);
-        int cnt = 0;
-        bool more = false;
-        window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
-        if (cnt == 0) continue;
-        const int k0 = cands.prim(w.C(0));
-        const float tMin = w.E(0);
-        FwdReplay<BvhCands> fwd(cands, mp, s_tab);
-        int st = 0;
-        const bool have_fwd = bd.fwd_state != nullptr;
-        if (have_fwd) {  // the forward pass of this very ray recorded the replay's results
-            const float *s = bd.fwd_state + 8 * r;
-            fwd.lastStep = __float_as_int(s[0]);
-            fwd.saturated = __float_as_int(s[1]) != 0;
-            fwd.satTPrev = s[2];
-            fwd.satSigmaSum = s[3];
-            fwd.satR = s[4];
-            fwd.satG = s[5];
-            fwd.satB = s[6];
-        } else {
-            st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
-        }
-        if (st == 0 && fwd.lastStep >= 0) {
-            const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
-            BwdWalk<BvhCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
-            if (!have_fwd) {  // the replay consumed the window
-                cnt = 0;
-                more = false;
-                window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
-            }
-            st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
-            if (st == 0 && bw.gTmin != 0.f) {  // t_min anchor chain (grad.cpp:166-194)
-                const float *xf = cands.xf(k0);
-                int axis, sign;
-                bool clamped;
-                if (intersect_face(xf, o, d, axis, sign, clamped) && !clamped) {
-                    const int j = axis;
-                    const float c = (float)sign;
-                    const V3 q = mk3(xf[3 + 3 * j], xf[4 + 3 * j], xf[5 + 3 * j]);
-                    const float qd = dot3(q, d);
-                    if (qd != 0.0f) {
-                        const float gT = bw.gTmin;
-                        bw.pose_add(k0, 0, q * (gT / qd));
-                        V3 gS = mk3(0.f, 0.f, 0.f);
-                        const float gsj = gT * c / qd;
-                        if (j == 0) gS.x = gsj;
-                        else if (j == 1) gS.y = gsj;
-                        else gS.z = gsj;
-                        bw.pose_add(k0, 6, gS);
-                        const V3 toT = mk3(xf[0], xf[1], xf[2]) - o;
-                        const float *pose = bd.pose36 + 36 * (size_t)k0;
-                        const V3 rj = mk3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2]);
-                        float gR[3];
-#pragma unroll
-                        for (int ii = 0; ii < 3; ++ii) {
-                            const V3 qp = matvec(pose + 9 + 9 * ii, rj);
-                            gR[ii] = gT * (dot3(qp, toT) - tMin * dot3(qp, d)) / qd;
-                        }
-                        bw.pose_add(k0, 3, mk3(gR[0], gR[1], gR[2]));
-                    }
-                }
-            }
-            bw.flush();
-        }
+        const int st = backward_one_ray(cands, w, mp, s_tab, bd, o, d, jit, r);
         if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
         if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
+    }
+}
+
+// backwardRay for small batches with the forward's per-ray state (evalLoss): one warp per ray,
+// 32 lattice steps at a time. Lane 0 collects the ray's sorted segment list; each lane takes
+// one step of the visited sequence (the march_warp replay of the lattice walk) and runs the
+// adjoint of its active primitives (the payload scatter and pose sums are atomics, as in the
+// per-thread walk); gTmin, the only sequential sum, is accumulated over the chunk's steps in
+// step order. Rays with more than kWarpListBwd segments take the per-thread path.
+constexpr int kWarpListBwd = 96;
+__global__ void __launch_bounds__(128)
+k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+                     RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, float *se, float *sx, int *sc) {
+    __shared__ unsigned long long s_tab[32];
+    __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
+    __shared__ int s_c[4][kWarpListBwd];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * 4, gw = blockIdx.x * 4 + wid;
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
+    const float dt = mp.dt;
+    for (int64_t r = gw; r < n_rays; r += nwarps) {
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        int cnt = 0;
+        bool more = false;
+        if (lane == 0) {
+            const Window<int> w{s_e[wid], s_x[wid], s_c[wid], 1, 0};
+            window_scan<kWarpListBwd>(w, cands, cnt, more, o, d, make_int2(0, 0), true, 0.f, 0);
+        }
+        cnt = __shfl_sync(0xffffffffu, cnt, 0);
+        more = __shfl_sync(0xffffffffu, more ? 1 : 0, 0) != 0;
+        __syncwarp();
+        if (more) {  // a long segment list: the per-thread walk with a global window
+            if (lane == 0) {
+                const Window<int> w{se, sx, sc, nwarps, gw};
+                const int st = backward_one_ray(cands, w, mp, s_tab, bd, o, d, jit, r);
+                if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
+                if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
+            }
+            __syncwarp();
+            continue;
+        }
+        if (cnt == 0) continue;
+        const float *E = s_e[wid], *X = s_x[wid];
+        const int *P = s_c[wid];
+        FwdReplay<BvhCands> fwd(cands, mp, s_tab);
+        load_fwd_state(fwd, bd.fwd_state + 8 * r);
+        const int lastStep = (int)fwd.lastStep;
+        if (lastStep < 0) continue;
+        const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
+        BwdWalk<BvhCands> bw(cands, mp, s_tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
+        const float t0 = E[0];
+        float gTmin = 0.f;
+        int base = 0;
+        for (;;) {
+            const int i = base + lane;
+            const bool valid = i <= lastStep;
+            const float ts = t0 + (__int2float_rn(i) + jit) * dt;
+            int na = 0, nadm = 0;
+            for (int j = 0; j < cnt && valid; ++j) {
+                if (!(E[j] <= ts)) break;
+                nadm = j + 1;
+                na += X[j] > ts;
+            }
+            const unsigned empty = __ballot_sync(0xffffffffu, !(valid && na > 0));
+            const int L = empty ? __ffs(empty) - 1 : 32;
+            float contrib = 0.f;
+            if (lane < L) {  // a visited step with samples (grad.cpp:66-164)
+                bw.step_begin(i, ts, o + d * ts);
+                for (int j = 0; j < nadm; ++j)
+                    if (X[j] > ts) bw.prim(P[j], P[j]);
+                contrib = dot3(bw.gPWorldStep, d);
+            }
+            for (int s = 0; s < L; ++s) gTmin += __shfl_sync(0xffffffffu, contrib, s);  // step order
+            if (base + L - 1 >= lastStep) break;
+            if (L == 32) {
+                base += 32;
+                continue;
+            }
+            const int iL = base + L;
+            const int nadmL = __shfl_sync(0xffffffffu, nadm, L);
+            if (nadmL >= cnt) break;
+            const float nextE = E[nadmL];
+            const double sk = ceil((double)((nextE - t0) / dt) - (double)jit);  // gap skip, march.cpp:45-49
+            const int skipTo = sk > (double)(1 << 30) ? (1 << 30) + 1 : (int)sk;
+            base = skipTo > iL + 1 ? skipTo : iL + 1;
+        }
+        if (lane == 0) anchor_chain(bw, cands, bd, P[0], t0, gTmin, o, d);
+        bw.flush();
+        __syncwarp();
     }
 }
 
@@ -455,8 +564,13 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
                                  cudaStream_t st) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
-    // one-warp CTAs: a small batch (evalLoss: 2048 rays) spreads over every SM, a large one
-    // keeps kBackwardWarps * 32 rays in flight (one scratch window each)
+    if (bd.fwd_state && n_rays <= kWarpRayBatch) {  // small batch with the forward's state
+        k_backward_rays_warp<<<(unsigned)((n_rays + 3) / 4), 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays,
+                                                                           bd, ctr, se, sx, sc);
+        return cudaGetLastError();
+    }
+    // one-warp CTAs: a small batch spreads over every SM, a large one keeps
+    // kBackwardWarps * 32 rays in flight (one scratch window each)
     const int64_t warps = (n_rays + 31) / 32;
     k_backward_rays<<<(unsigned)(warps < kBackwardWarps ? warps : kBackwardWarps), 32, 0, st>>>(
         mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, se, sx, sc);
