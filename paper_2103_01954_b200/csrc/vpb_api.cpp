@@ -101,7 +101,7 @@ struct vp_ctx {
     int64_t t_count = 0;
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
     // per-entry-point scratch, kept across calls (a cudaMalloc per training call costs ms)
-    DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_adam;
+    DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_bwd_fwd, s_adam;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
     // vp_render_async into host memory: two device output slots; the device->host copy of
@@ -378,7 +378,8 @@ int vp_destroy(vp_ctx *ctx) {
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     ctx->tr24.release();
-    for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_adam}) b->release();
+    for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_bwd_fwd, &ctx->s_adam})
+        b->release();
     ctx->flag.release();
     for (auto *b : {&ctx->xf16, &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
                     &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
@@ -897,9 +898,27 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         if (int rc = ensure_fallback(ctx)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state};
         MarchDev mp = make_march(ctx, cfg);
         if (int rc = ensure_bvh(ctx, mp)) return rc;
+        if (!fwd_state) {
+            // forward march of the same rays first, recording the MarchResult bookkeeping, so
+            // the backward kernel does not replay march() itself
+            VP_CUDA(ctx, ctx->s_bwd_fwd.ensure(12 * n));
+            OutDev od{ctx->s_bwd_fwd.p, ctx->s_bwd_fwd.p + 3 * n, nullptr};
+            od.state = ctx->s_bwd_fwd.p + 4 * n;
+            if (size_t(ctx->ovf_cap) < n) {
+                VP_CUDA(ctx, ctx->ovf_list.ensure(n));
+                ctx->ovf_cap = int(n);
+            }
+            VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays, od, ctx->d_ctr,
+                                           ctx->ovf_list.p, ctx->ovf_cap, st));
+            const CamDev none{};
+            VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, k, ctx->payload.p, nullptr,
+                                               nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
+                                               ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+            fwd_state = od.state;
+        }
+        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state};
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
