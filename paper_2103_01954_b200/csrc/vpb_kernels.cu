@@ -539,7 +539,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
             atomicAdd(&ctr->fallback_fail, 1);
             continue;
         }
-        write_pixel(od, p, ro);
+        write_ray(od, p, ro);  // (od.state is null for camera renders)
         atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);  // rare path: plain atomics
         atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
         atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
@@ -576,7 +576,7 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
             if (slot < ovf_cap) ovf_list[slot] = (int)r;
         }
     }
-    if (valid && !ro.overflow) write_pixel(od, r, ro);
+    if (valid && !ro.overflow) write_ray(od, r, ro);
     add_counters(ctr, ro, valid && !ro.overflow);
 }
 
@@ -618,7 +618,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
             }
         } else {
             ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane);
-            if (lane == 0) write_pixel(od, r, ro);
+            if (lane == 0) write_ray(od, r, ro);
         }
         add_counters(ctr, ro, lane == 0 && !ro.overflow);
         __syncwarp();

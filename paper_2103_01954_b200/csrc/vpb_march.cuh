@@ -657,7 +657,13 @@ __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const R
     od.rgb[3 * p + 2] = ro.b;
     od.alpha[p] = ro.alpha;
     if (od.samples) od.samples[p] = ro.samples;
-    if (od.state) {  // per-ray forward state for a following backward pass (evalLoss)
+}
+
+// Arbitrary-ray kernels only (the tile kernel keeps the bookkeeping dead): the per-ray
+// forward state for a following backward pass.
+__device__ __forceinline__ void write_ray(const OutDev &od, int64_t p, const RayOut &ro) {
+    write_pixel(od, p, ro);
+    if (od.state) {
         float *s = od.state + 8 * p;
         s[0] = __int_as_float(ro.last_step);
         s[1] = __int_as_float(ro.saturated);
