@@ -796,9 +796,13 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
     // Each ray is a serial latency chain: small batches (evalLoss: 2048 rays) are marched a
     // warp per ray, 32 lattice steps at a time; mid-size ones go out as one-warp CTAs so they
     // spread over every SM instead of packing into a few.
-    if (n_rays <= kWarpRayBatch) {
-        k_march_rays_warp<<<(unsigned)((n_rays + 3) / 4), 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays,
-                                                                        od, ctr, ovf_list, ovf_cap);
+#ifndef VPB_FWD_WARP_MAX
+#define VPB_FWD_WARP_MAX kWarpRayBatch
+#endif
+    if (n_rays <= (int64_t)VPB_FWD_WARP_MAX) {
+        const int64_t blocks = (n_rays + 3) / 4;
+        k_march_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
+            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
         return cudaGetLastError();
     }
     if (n_rays < 148 * 128 * 2)
