@@ -467,18 +467,22 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 }
 
 // backwardRay for small batches with the forward's per-ray state (evalLoss): one warp per ray,
-// 32 lattice steps at a time. Lane 0 collects the ray's sorted segment list; each lane takes
+// 32 lattice steps at a time. The warp builds the ray's sorted segment list
+// (warp_segment_list); each lane takes
 // one step of the visited sequence (the march_warp replay of the lattice walk) and runs the
 // adjoint of its active primitives (the payload scatter and pose sums are atomics, as in the
 // per-thread walk); gTmin, the only sequential sum, is accumulated over the chunk's steps in
 // step order. Rays with more than kWarpListBwd segments take the per-thread path.
 constexpr int kWarpListBwd = 96;
+constexpr int kWarpCandBwd = 256;
 __global__ void __launch_bounds__(128)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, float *se, float *sx, int *sc) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];
+    __shared__ int s_cand[4][kWarpCandBwd];
+    __shared__ float s_ce[4][kWarpCandBwd], s_cx[4][kWarpCandBwd];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -489,16 +493,10 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        int cnt = 0;
-        bool more = false;
-        if (lane == 0) {
-            const Window<int> w{s_e[wid], s_x[wid], s_c[wid], 1, 0};
-            window_scan<kWarpListBwd>(w, cands, cnt, more, o, d, make_int2(0, 0), true, 0.f, 0);
-        }
-        cnt = __shfl_sync(0xffffffffu, cnt, 0);
-        more = __shfl_sync(0xffffffffu, more ? 1 : 0, 0) != 0;
-        __syncwarp();
-        if (more) {  // a long segment list: the per-thread walk with a global window
+        const int nh = warp_segment_list(cands, o, d, lane, s_cand[wid], s_ce[wid], s_cx[wid], kWarpCandBwd,
+                                         s_e[wid], s_x[wid], s_c[wid], kWarpListBwd);
+        const int cnt = nh < 0 ? 0 : nh;
+        if (nh < 0) {  // a long segment list: the per-thread walk with a global window
             if (lane == 0) {
                 const Window<int> w{se, sx, sc, nwarps, gw};
                 const int st = backward_one_ray(cands, w, mp, s_tab, bd, o, d, jit, r);

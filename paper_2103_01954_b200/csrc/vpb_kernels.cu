@@ -580,11 +580,12 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     add_counters(ctr, ro, valid && !ro.overflow);
 }
 
-// march() over caller rays, one warp per ray (small batches): lane 0 collects the ray's whole
-// sorted segment list through the BVH into the warp's shared-memory list, then the warp walks
+// march() over caller rays, one warp per ray (small batches): the warp builds the ray's whole
+// sorted segment list through the BVH (warp_segment_list) in shared memory, then walks
 // it 32 lattice steps at a time (march_warp). Rays with more than kWarpList segments go to the
 // wide-window fallback like window overflows.
-constexpr int kWarpList = 96;
+constexpr int kWarpList = 96;   // segments per ray held by the warp
+constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp path gives up
 __global__ void __launch_bounds__(128)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
@@ -592,6 +593,8 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpList], s_x[4][kWarpList];
     __shared__ int s_c[4][kWarpList];
+    __shared__ int s_cand[4][kWarpCand];
+    __shared__ float s_ce[4][kWarpCand], s_cx[4][kWarpCand];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -600,15 +603,10 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        int cnt = 0;
-        bool more = false;
-        if (lane == 0) {
-            const Window<int> w{s_e[wid], s_x[wid], s_c[wid], 1, 0};
-            window_scan<kWarpList>(w, cands, cnt, more, o, d, make_int2(0, 0), true, 0.f, 0);
-        }
-        cnt = __shfl_sync(0xffffffffu, cnt, 0);
-        more = __shfl_sync(0xffffffffu, more ? 1 : 0, 0) != 0;
-        __syncwarp();
+        const int nh = warp_segment_list(cands, o, d, lane, s_cand[wid], s_ce[wid], s_cx[wid], kWarpCand, s_e[wid],
+                                         s_x[wid], s_c[wid], kWarpList);
+        const bool more = nh < 0;
+        const int cnt = more ? 0 : nh;
         RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
         if (more) {
             ro.overflow = 1;

@@ -529,6 +529,51 @@ done:
     return out;
 }
 
+// The complete sorted segment list of one ray, built by a warp: lane 0 walks the BVH and
+// lists the primitives whose box the ray crosses (cheap box tests); the exact intersectObb
+// tests run on all lanes; the hits are placed by rank of their (tEnter, prim) key (keys are
+// distinct), which is the order window_scan produces. Returns the hit count, or -1 when the
+// ray crosses more than `cap_cand` boxes or has more than `cap` hits (caller falls back).
+__device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3 d, int lane, int *cand,
+                                                 float *ce, float *cx, int cap_cand, float *E, float *X, int *P,
+                                                 int cap) {
+    int nc = 0;
+    if (lane == 0) {
+        bvh_for_each(cands.bvh, o, d, [&](int c) {
+            if (nc < cap_cand) cand[nc] = c;
+            ++nc;
+        });
+    }
+    nc = __shfl_sync(0xffffffffu, nc, 0);
+    __syncwarp();
+    if (nc > cap_cand) return -1;
+    for (int q = lane; q < nc; q += 32) {
+        float tE, tX;
+        const bool hit = cands.hit(cand[q], o, d, tE, tX);
+        ce[q] = hit ? tE : __int_as_float(0x7f800000);
+        cx[q] = tX;
+    }
+    __syncwarp();
+    int nh = 0;
+    for (int q = 0; q < nc; ++q) nh += ce[q] != __int_as_float(0x7f800000);
+    if (nh > cap) return -1;
+    for (int q = lane; q < nc; q += 32) {
+        const float e = ce[q];
+        if (e == __int_as_float(0x7f800000)) continue;
+        const int pq = cand[q];
+        int rank = 0;
+        for (int u = 0; u < nc; ++u) {
+            const float eu = ce[u];
+            rank += eu != __int_as_float(0x7f800000) && key_less(eu, cand[u], e, pq);
+        }
+        E[rank] = e;
+        X[rank] = cx[q];
+        P[rank] = pq;
+    }
+    __syncwarp();
+    return nh;
+}
+
 // Step-parallel march of ONE ray by a warp (small ray batches, e.g. evalLoss's 2048 rays,
 // where one thread per ray leaves the GPU idle while the longest rays walk hundreds of steps).
 // E/X/P hold the ray's complete sorted segment list (cnt entries, no refill). Lane L takes
