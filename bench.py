@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--width", type=int, default=1024)
     p.add_argument("--views-per-gpu", type=int, default=8)
     p.add_argument("--no-gather", action="store_true")
+    p.add_argument("--per-view", action="store_true",
+                   help="one raymarch launch per view instead of one per step (vp_render_batch_async)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -247,15 +249,29 @@ def main():
 
     rgb, alpha, samples = vg.views()
 
+    batch = not args.per_view and V <= 16
+    cams_arr = (vp_camera * V)(*cams)
+    rgb_ptrs = (f32p * V)(*[C.cast(rgb[j].data_ptr(), f32p) for j in range(V)])
+    alpha_ptrs = (f32p * V)(*[C.cast(alpha[j].data_ptr(), f32p) for j in range(V)])
+    samp_ptrs = (i32p * V)(*[C.cast(samples[j].data_ptr(), i32p) for j in range(V)])
+
     def step(i):
-        for j, cam in enumerate(cams):
-            rc = lib.vp_render_async(r.ctx, C.byref(cam), C.byref(mc), C.cast(rgb[j].data_ptr(), f32p),
-                                     C.cast(alpha[j].data_ptr(), f32p), C.cast(samples[j].data_ptr(), i32p),
-                                     C.c_void_p(sh))
-            if rc:
+        if batch:  # every view of the step in one raymarch launch
+            if lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), rgb_ptrs, alpha_ptrs, samp_ptrs,
+                                         C.c_void_p(sh)):
                 raise RuntimeError(lib.vp_last_error(r.ctx).decode())
             if gather:
-                vg.gather_view(j)
+                for j in range(V):
+                    vg.gather_view(j)
+        else:
+            for j, cam in enumerate(cams):
+                rc = lib.vp_render_async(r.ctx, C.byref(cam), C.byref(mc), C.cast(rgb[j].data_ptr(), f32p),
+                                         C.cast(alpha[j].data_ptr(), f32p), C.cast(samples[j].data_ptr(), i32p),
+                                         C.c_void_p(sh))
+                if rc:
+                    raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+                if gather:
+                    vg.gather_view(j)
         if gather:
             vg.finish()
 
@@ -300,24 +316,26 @@ def main():
     # roofline of the dominant kernel (raymarch K5 + fallback K5b), per launch
     pk, pk_kind = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
-    alg_bytes_per_launch = (BYTES_PER_PRIM_SAMPLE * prim_samples + BYTES_PER_PIXEL * w * w * V) / V
+    views_per_launch = V if batch else 1
+    alg_bytes_per_launch = (BYTES_PER_PRIM_SAMPLE * prim_samples + BYTES_PER_PIXEL * w * w * V) / V * views_per_launch
     march_avg_s = float(np.mean(march_ms)) / 1e3 if len(march_ms) else float("nan")
     achieved = alg_bytes_per_launch / march_avg_s / 1e9
     frame_s = t_local / (V * args.steps)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": None,
-                "kernel": "k_march_tiles (+k_march_fallback)", "peak_kind": pk_kind,
+                "kernel": "k_march_tiles (+k_march_fallback_views)", "peak_kind": pk_kind,
+                "views_per_launch": views_per_launch,
                 "alg_bytes_per_launch": int(alg_bytes_per_launch), "avg_launch_ms": round(march_avg_s * 1e3, 4),
-                "march_share_of_step": round(march_avg_s * V * args.steps / max(t_local, 1e-12), 4),
+                "march_share_of_step": round(march_avg_s * V / views_per_launch * args.steps / max(t_local, 1e-12), 4),
                 "frame_ms": round(frame_s * 1e3, 4),
-                "frame_frac": round(alg_bytes_per_launch / frame_s / 1e9 / hbm, 4)}
+                "frame_frac": round(alg_bytes_per_launch / views_per_launch / frame_s / 1e9 / hbm, 4)}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
             tr_ = json.loads(prof.read_text())
             key = f"K{k}_M{m}_W{w}"
             if key in tr_:
-                roofline["traffic"] = tr_[key]["dram_bytes_per_launch"]
+                roofline["traffic"] = tr_[key]["dram_bytes_per_view"] * views_per_launch
                 roofline["traffic_source"] = tr_[key]["source"]
         except Exception:
             pass

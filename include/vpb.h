@@ -148,6 +148,12 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
  * them. samples nullable. Counters can be read afterwards with vp_read_stats. */
 int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb,
                     float *alpha, int32_t *samples, void *stream);
+/* A batch of 1..16 views of the resident frame in ONE raymarch launch (the tiles of all views
+ * heaviest first, so the batch pays the launch's tail once; e.g. the 64-view ring in 4..8
+ * calls). Outputs are arrays of device pointers (samples may be NULL), enqueued on `stream`.
+ * vp_read_stats afterwards reports the last view. */
+int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,
+                          float *const *rgb, float *const *alpha, int32_t *const *samples, void *stream);
 /* Waits for every render and output copy the context has enqueued. */
 int vp_sync(vp_ctx *ctx);
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats);

@@ -61,12 +61,15 @@ constexpr int kTimingSlots = 256;  // march-kernel event pairs kept for vp_kerne
 
 }  // namespace
 
-// Binning artefacts of one view (K1-K3 outputs + its counters). Two slots: the binning of the
-// next view runs on bin_stream while the current view marches (vpb_api.cpp enqueue_render).
+// Binning artefacts of one view (K1-K3 outputs), its counters and its overflow list. Two
+// groups of kMaxViews slots: a launch's views are binned on bin_stream into one group while
+// the previous launch marches from the other (enqueue_views).
 struct BinSlot {
     DBuf<int4> rects, prects;
     DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
     DBuf<unsigned long long> entries;
+    DBuf<int> ovf;
+    int ovf_cap = 0;
     DevCounters *d_ctr = nullptr;
     cudaEvent_t ev_binned = nullptr, ev_marched = nullptr;
 };
@@ -85,10 +88,12 @@ struct vp_ctx {
     DBuf<int> flag;        // device error flag (compose)
     bool has_xf = false;   // resident composed transforms are set
     DBuf<float4> payload;
-    BinSlot slot[2];
-    int cur = 0;  // slot of the latest render
+    BinSlot slot[2 * kMaxViews];
+    int cur = 0;    // slot of the latest render's last view
+    int group = 0;  // slot group of the latest launch
     BinSlot &bs() { return slot[cur]; }
     cudaStream_t bin_stream = nullptr;
+    DBuf<uint32_t> batch_order[2];  // per group: heaviest-first (view, tile) order of a batch
     DBuf<float> out_rgb, out_alpha;
     DBuf<int> out_samples, ovf_list;
     DBuf<float> fb_e, fb_x;
@@ -201,57 +206,97 @@ int ensure_fallback(vp_ctx *ctx) {
     return VP_OK;
 }
 
-int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
+int ensure_slot(vp_ctx *ctx, BinSlot &b) {
+    if (b.d_ctr) return VP_OK;
+    VP_CUDA(ctx, cudaMalloc(&b.d_ctr, sizeof(DevCounters)));
+    VP_CUDA(ctx, cudaMemset(b.d_ctr, 0, sizeof(DevCounters)));
+    VP_CUDA(ctx, cudaEventCreateWithFlags(&b.ev_binned, cudaEventDisableTiming));
+    VP_CUDA(ctx, cudaEventCreateWithFlags(&b.ev_marched, cudaEventDisableTiming));
+    return VP_OK;
+}
+
+// Buffers of one slot for a view of camera `cam`.
+int ensure_slot_buffers(vp_ctx *ctx, BinSlot &b, const CamDev &cam) {
     const size_t n_tiles = size_t(cam.tiles_x) * cam.tiles_y;
     const size_t n_px = size_t(cam.width) * cam.height;
+    if (n_tiles >= (size_t(1) << 20)) return fail(ctx, VP_ERR_USAGE, "image too large (2^20 tiles)");
     if (ctx->entries_cap == 0) ctx->entries_cap = std::max<int64_t>(int64_t(1) << 20, int64_t(ctx->n_prim) * 16);
-    for (BinSlot &b : ctx->slot) {
-        VP_CUDA(ctx, b.tile_counts.ensure(n_tiles));
-        VP_CUDA(ctx, b.offsets.ensure(n_tiles + 1));
-        VP_CUDA(ctx, b.cursor.ensure(n_tiles));
-        VP_CUDA(ctx, b.order.ensure(n_tiles));
-        VP_CUDA(ctx, b.rects.ensure(size_t(std::max(ctx->n_prim, 1))));
-        VP_CUDA(ctx, b.prects.ensure(size_t(std::max(ctx->n_prim, 1))));
-        VP_CUDA(ctx, b.keys.ensure(size_t(std::max(ctx->n_prim, 1))));
-        VP_CUDA(ctx, b.entries.ensure(size_t(ctx->entries_cap)));
-    }
-    if (size_t(ctx->ovf_cap) < n_px) {
-        VP_CUDA(ctx, ctx->ovf_list.ensure(n_px));
-        ctx->ovf_cap = int(n_px);
+    if (int rc = ensure_slot(ctx, b)) return rc;
+    VP_CUDA(ctx, b.tile_counts.ensure(n_tiles));
+    VP_CUDA(ctx, b.offsets.ensure(n_tiles + 1));
+    VP_CUDA(ctx, b.cursor.ensure(n_tiles));
+    VP_CUDA(ctx, b.order.ensure(n_tiles));
+    VP_CUDA(ctx, b.rects.ensure(size_t(std::max(ctx->n_prim, 1))));
+    VP_CUDA(ctx, b.prects.ensure(size_t(std::max(ctx->n_prim, 1))));
+    VP_CUDA(ctx, b.keys.ensure(size_t(std::max(ctx->n_prim, 1))));
+    VP_CUDA(ctx, b.entries.ensure(size_t(ctx->entries_cap)));
+    if (size_t(b.ovf_cap) < n_px) {
+        VP_CUDA(ctx, b.ovf.ensure(n_px));
+        b.ovf_cap = int(n_px);
     }
     return ensure_fallback(ctx);
 }
 
-// The device pipeline for one view (no host synchronisation). Binning (K1-K3) goes to
-// bin_stream into the slot the previous view did not use, so it overlaps the previous view's
-// raymarch (whose tail leaves SMs idle); the raymarch waits for it on `st`. A slot is rebinned
-// only after the raymarch that read it (two views back) has finished.
-int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const OutDev &od,
-                   cudaStream_t st) {
-    ctx->cur ^= 1;
-    BinSlot &b = ctx->bs();
-    ctx->d_ctr = b.d_ctr;
-    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
-    VP_CUDA(ctx, cudaMemsetAsync(b.d_ctr, 0, sizeof(DevCounters), ctx->bin_stream));
-    VP_CUDA(ctx, launch_binning(cam, ctx->xf16.p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p, b.tile_counts.p,
-                                b.offsets.p, b.cursor.p, b.order.p, b.entries.p, ctx->entries_cap, b.d_ctr,
-                                ctx->bin_stream));
-    VP_CUDA(ctx, cudaEventRecord(b.ev_binned, ctx->bin_stream));
-    VP_CUDA(ctx, cudaStreamWaitEvent(st, b.ev_binned, 0));
+// Buffers for a single-view render (both slots it may land in).
+int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
+    for (int g = 0; g < 2; ++g)
+        if (int rc = ensure_slot_buffers(ctx, ctx->slot[g * kMaxViews], cam)) return rc;
+    return VP_OK;
+}
+
+// The device pipeline for `n` views (no host synchronisation). Binning (K1-K3) of each view
+// goes to bin_stream into the slot group the previous launch did not use, so it overlaps the
+// previous launch's raymarch (whose tail leaves SMs idle); a slot is rebinned only after the
+// raymarch that read it has finished. Then ONE raymarch launch covers the tiles of all the
+// views, heaviest first across views (a batch pays the tail of a launch once), and one
+// fallback launch their overflow rays.
+int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, const OutDev *ods, cudaStream_t st) {
+    if (n < 1 || n > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per launch");
+    ctx->group ^= 1;
+    BinSlot *grp = ctx->slot + ctx->group * kMaxViews;
+    for (int v = 0; v < n; ++v)
+        if (int rc = ensure_slot_buffers(ctx, grp[v], cams[v])) return rc;
+    ViewBatch vb{};
+    vb.n = n;
+    const uint32_t *counts[kMaxViews];
+    int n_tiles[kMaxViews];
+    int total = 0;
+    for (int v = 0; v < n; ++v) {
+        BinSlot &b = grp[v];
+        VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
+        VP_CUDA(ctx, cudaMemsetAsync(b.d_ctr, 0, sizeof(DevCounters), ctx->bin_stream));
+        VP_CUDA(ctx, launch_binning(cams[v], ctx->xf16.p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p,
+                                    b.tile_counts.p, b.offsets.p, b.cursor.p, b.order.p, b.entries.p,
+                                    ctx->entries_cap, b.d_ctr, ctx->bin_stream));
+        vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap};
+        counts[v] = b.tile_counts.p;
+        n_tiles[v] = cams[v].tiles_x * cams[v].tiles_y;
+        total += n_tiles[v];
+    }
+    const uint32_t *order = grp[0].order.p;
+    if (n > 1) {
+        VP_CUDA(ctx, ctx->batch_order[ctx->group].ensure(size_t(std::max(total, 1))));
+        VP_CUDA(ctx, launch_batch_order(counts, n_tiles, n, ctx->batch_order[ctx->group].p, ctx->bin_stream));
+        order = ctx->batch_order[ctx->group].p;
+    }
+    VP_CUDA(ctx, cudaEventRecord(grp[0].ev_binned, ctx->bin_stream));
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, grp[0].ev_binned, 0));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
-    VP_CUDA(ctx, launch_march_tiles(cam, mp, ctx->xf16.p, ctx->bs().prects.p, ctx->payload.p, ctx->bs().offsets.p,
-                                    ctx->bs().order.p, ctx->bs().entries.p, od, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
+    VP_CUDA(ctx, launch_march_tiles(mp, ctx->xf16.p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
-    const RaysDev none{nullptr, nullptr, nullptr};
-    VP_CUDA(ctx, launch_march_fallback(false, cam, mp, ctx->xf16.p, ctx->bs().prects.p, ctx->n_prim, ctx->payload.p,
-                                       ctx->bs().offsets.p, ctx->bs().entries.p, od, none, ctx->d_ctr,
-                                       ctx->ovf_list.p, ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p,
-                                       ctx->fb_c.p, st));
+    VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
+                                             ctx->fb_x.p, ctx->fb_c.p, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
-    VP_CUDA(ctx, cudaEventRecord(b.ev_marched, st));
+    for (int v = 0; v < n; ++v) VP_CUDA(ctx, cudaEventRecord(grp[v].ev_marched, st));
     ++ctx->t_count;
+    ctx->cur = ctx->group * kMaxViews + n - 1;
+    ctx->d_ctr = grp[n - 1].d_ctr;
     return VP_OK;
+}
+
+int enqueue_render(vp_ctx *ctx, const CamDev &cam, const MarchDev &mp, const OutDev &od, cudaStream_t st) {
+    return enqueue_views(ctx, 1, &cam, mp, &od, st);
 }
 
 // Mean candidates per non-empty tile: up to 14 -> Light, up to 40 -> Normal, else Dense
@@ -339,15 +384,8 @@ int vp_create(int32_t device, vp_ctx **out) {
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[1], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->bin_stream, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->slot[0].d_ctr, sizeof(DevCounters))) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->slot[1].d_ctr, sizeof(DevCounters))) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->slot[0].ev_binned, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->slot[1].ev_binned, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->slot[0].ev_marched, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->slot[1].ev_marched, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess ||
-        (e = cudaMemset(ctx->slot[0].d_ctr, 0, sizeof(DevCounters))) != cudaSuccess ||
-        (e = cudaMemset(ctx->slot[1].d_ctr, 0, sizeof(DevCounters))) != cudaSuccess) {
+
+        (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
         vp_destroy(ctx);
         return rc;
@@ -355,6 +393,11 @@ int vp_create(int32_t device, vp_ctx **out) {
     for (cudaEvent_t &ev : ctx->t_ev)
         if ((e = cudaEventCreate(&ev)) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
+        vp_destroy(ctx);
+        return rc;
+    }
+    if ((rc = ensure_slot(ctx, ctx->slot[0])) != VP_OK) {
+        g_err = ctx->err;
         vp_destroy(ctx);
         return rc;
     }
@@ -390,11 +433,14 @@ int vp_destroy(vp_ctx *ctx) {
         b.prects.release();
         for (auto *u : {&b.keys, &b.tile_counts, &b.offsets, &b.cursor, &b.order}) u->release();
         b.entries.release();
+        b.ovf.release();
         if (b.d_ctr) cudaFree(b.d_ctr);
         if (b.ev_binned) cudaEventDestroy(b.ev_binned);
         if (b.ev_marched) cudaEventDestroy(b.ev_marched);
     }
     if (ctx->bin_stream) cudaStreamDestroy(ctx->bin_stream);
+    ctx->batch_order[0].release();
+    ctx->batch_order[1].release();
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -618,6 +664,34 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
     return VP_OK;
 }
 
+int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,
+                          float *const *rgb, float *const *alpha, int32_t *const *samples, void *stream) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    if (n_views < 1 || n_views > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per batch");
+    if (!cams || !rgb || !alpha) return fail(ctx, VP_ERR_USAGE, "null arguments");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    CamDev cds[kMaxViews];
+    OutDev ods[kMaxViews];
+    for (int v = 0; v < n_views; ++v) {
+        if (int rc = check_cam(ctx, &cams[v])) return rc;
+        if (size_t(cams[v].width) * cams[v].height == 0) return fail(ctx, VP_ERR_USAGE, "empty view in a batch");
+        int32_t *sp = samples ? samples[v] : nullptr;
+        if (!rgb[v] || !alpha[v] || !is_device_ptr(rgb[v]) || !is_device_ptr(alpha[v]) || (sp && !is_device_ptr(sp)))
+            return fail(ctx, VP_ERR_USAGE, "batch outputs must be device pointers");
+        cds[v] = make_cam(cams[v]);
+        ods[v] = OutDev{rgb[v], alpha[v], sp};
+        if (ctx->n_prim == 0) {
+            const size_t n_px = size_t(cams[v].width) * cams[v].height;
+            VP_CUDA(ctx, cudaMemsetAsync(rgb[v], 0, 12 * n_px, st));
+            VP_CUDA(ctx, cudaMemsetAsync(alpha[v], 0, 4 * n_px, st));
+            if (sp) VP_CUDA(ctx, cudaMemsetAsync(sp, 0, 4 * n_px, st));
+        }
+    }
+    if (ctx->n_prim == 0) return VP_OK;
+    return enqueue_views(ctx, n_views, cds, make_march(ctx, cfg), ods, st);
+}
+
 int vp_sync(vp_ctx *ctx) {
     if (int rc = check_ctx(ctx, false)) return rc;
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -801,6 +875,9 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     const CamDev cd = make_cam(*cam);
     const size_t n_tiles = size_t(cd.tiles_x) * cd.tiles_y;
     cudaStream_t st = ctx->stream;
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->bin_stream));
+    ctx->cur = 0;  // slot 0, synchronously on the context stream
+    ctx->d_ctr = ctx->slot[0].d_ctr;
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));

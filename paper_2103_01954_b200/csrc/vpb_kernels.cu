@@ -443,11 +443,8 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
 
 template <int CAP, int MT, bool PROF, int CC, int MINB>
 __global__ void __launch_bounds__(kMarchThreads, MINB)
-k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
-              const int4 *__restrict__ prects, const float4 *__restrict__ payload,
-              const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ order,
-              const unsigned long long *__restrict__ entries, OutDev od, DevCounters *ctr,
-              int *__restrict__ ovf_list, int ovf_cap) {
+k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restrict__ payload, ViewBatch views,
+              const uint32_t *__restrict__ order) {
     extern __shared__ __align__(16) unsigned char smem[];
     TileSmem sm;
     sm.xf4 = reinterpret_cast<float4 *>(smem);
@@ -463,21 +460,26 @@ k_march_tiles(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     sm.wc = sm.wx + CAP * kMarchThreads;
     sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + CAP * kMarchThreads);
 
+    const uint32_t oe = order[blockIdx.x];
+    const ViewDev &vd = views.v[oe >> 20];
+    const CamDev &cam = vd.cam;
+    const OutDev &od = vd.od;
+    DevCounters *ctr = vd.ctr;
     if (ctr->key_overflow) return;
-    const int tile = (int)order[blockIdx.x];
-    const uint32_t start = offsets[tile];
-    const int n = (int)(offsets[tile + 1] - start);
+    const int tile = (int)(oe & 0xfffffu);
+    const uint32_t start = vd.offsets[tile];
+    const int n = (int)(vd.offsets[tile + 1] - start);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     if (threadIdx.x < 32) sm.tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     unsigned long long t_start = 0;
     if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
     if (n <= CC)
-        march_tile<CAP, MT, true, CC>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
-                                  ovf_list, ovf_cap);
+        march_tile<CAP, MT, true, CC>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+                                      vd.ovf_list, vd.ovf_cap);
     else
-        march_tile<CAP, MT, false, CC>(sm, cam, mp, xf_g, prects, payload, entries, start, n, tx, ty, od, ctr,
-                                   ovf_list, ovf_cap);
+        march_tile<CAP, MT, false, CC>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+                                       vd.ovf_list, vd.ovf_cap);
     if (PROF) {  // separate instantiation: per-CTA timeline for load-balance analysis
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -712,11 +714,8 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
 }
 
 template <class Cfg, int MT, bool PROF>
-static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                                  const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                                  const uint32_t *order, const unsigned long long *entries,
-                                  const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                                  cudaStream_t st) {
+static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const float4 *payload,
+                                  const ViewBatch &views, const uint32_t *order, int n_ctas, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC>();
     auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB>;
@@ -729,19 +728,16 @@ static cudaError_t launch_tiles_m(const CamDev &cam, const MarchDev &mp, const f
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
         attr_set = true;
     }
-    kern<<<cam.tiles_x * cam.tiles_y, kMarchThreads, smem, st>>>(cam, mp, xf16, prects, payload, offsets,
-                                                                order, entries, od, ctr, ovf_list, ovf_cap);
+    kern<<<n_ctas, kMarchThreads, smem, st>>>(mp, xf16, payload, views, order);
     return cudaGetLastError();
 }
 
 template <class Cfg>
-static cudaError_t launch_tiles_cfg(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                                    const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                                    const uint32_t *order, const unsigned long long *entries,
-                                    const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
+static cudaError_t launch_tiles_cfg(const MarchDev &mp, const float *xf16, const float4 *payload,
+                                    const ViewBatch &views, const uint32_t *order, int n_ctas, bool prof,
                                     cudaStream_t st) {
-#define VPB_TILES(MT) (od.prof ? launch_tiles_m<Cfg, MT, true>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st) \
-                           : launch_tiles_m<Cfg, MT, false>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr, ovf_list, ovf_cap, st))
+#define VPB_TILES(MT) (prof ? launch_tiles_m<Cfg, MT, true>(mp, xf16, payload, views, order, n_ctas, st) \
+                            : launch_tiles_m<Cfg, MT, false>(mp, xf16, payload, views, order, n_ctas, st))
     switch (mp.m) {  // compile-time voxel counts for the common grids
     case 4: return VPB_TILES(4);
     case 8: return VPB_TILES(8);
@@ -752,23 +748,121 @@ static cudaError_t launch_tiles_cfg(const CamDev &cam, const MarchDev &mp, const
 #undef VPB_TILES
 }
 
-cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                               const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                               const uint32_t *order, const unsigned long long *entries,
-                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               TileTier tier, cudaStream_t st) {
-    if (cam.tiles_x * cam.tiles_y == 0) return cudaSuccess;
+cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const ViewBatch &views,
+                               const uint32_t *order, int n_ctas, bool prof, TileTier tier, cudaStream_t st) {
+    if (n_ctas == 0) return cudaSuccess;
     switch (tier) {
     case TileTier::Light:
-        return launch_tiles_cfg<TileCfgLight>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
-                                              ovf_list, ovf_cap, st);
+        return launch_tiles_cfg<TileCfgLight>(mp, xf16, payload, views, order, n_ctas, prof, st);
     case TileTier::Dense:
-        return launch_tiles_cfg<TileCfgDense>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
-                                              ovf_list, ovf_cap, st);
+        return launch_tiles_cfg<TileCfgDense>(mp, xf16, payload, views, order, n_ctas, prof, st);
     default:
-        return launch_tiles_cfg<TileCfgNormal>(cam, mp, xf16, prects, payload, offsets, order, entries, od, ctr,
-                                               ovf_list, ovf_cap, st);
+        return launch_tiles_cfg<TileCfgNormal>(mp, xf16, payload, views, order, n_ctas, prof, st);
     }
+}
+
+// K5b over every view of a launch: each view's overflow rays (key-overflowed views skipped).
+__global__ void __launch_bounds__(kFallbackThreads)
+k_march_fallback_views(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+                       ViewBatch views, float *scratch_e, float *scratch_x, int *scratch_c) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __syncthreads();
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const unsigned m3 = (unsigned)(mp.m * mp.m * mp.m);
+    for (int v = 0; v < views.n; ++v) {
+        const ViewDev &vd = views.v[v];
+        DevCounters *ctr = vd.ctr;
+        if (ctr->key_overflow) continue;
+        const int n_ovf = (int)min((unsigned long long)vd.ovf_cap, ctr->overflow_rays);
+        const CamDev &cam = vd.cam;
+        for (int q = gtid; q < n_ovf; q += nthreads) {
+            const int p = vd.ovf_list[q];
+            const int px = p % cam.width, py = p / cam.width;
+            const int tile = (py / kTile) * cam.tiles_x + px / kTile;
+            V3 o, d;
+            generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+            const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p)) : 0.5f;
+            const uint32_t start = vd.offsets[tile];
+            const TileCands<false> cands{vd.entries, xf_g, vd.prects, payload, m3, start,
+                                         (int)(vd.offsets[tile + 1] - start), nullptr, nullptr, nullptr,
+                                         nullptr};
+            const RayOut ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, s_tab);
+            if (ro.overflow) {
+                atomicAdd(&ctr->fallback_fail, 1);
+                continue;
+            }
+            write_pixel(vd.od, p, ro);
+            atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);  // rare path: plain atomics
+            atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
+            atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
+            atomicAdd(&ctr->early_exits, (unsigned long long)ro.early);
+            atomicAdd(&ctr->saturated, (unsigned long long)ro.saturated);
+            atomicAdd(&ctr->refills, (unsigned long long)ro.refills);
+            if (ro.numeric) atomicAdd(&ctr->numeric_fail, 1ull);
+        }
+    }
+}
+
+cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                        const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st) {
+    k_march_fallback_views<<<kFallbackBlocks, kFallbackThreads, 0, st>>>(mp, xf16, n_prim, payload, views, se, sx,
+                                                                         sc);
+    return cudaGetLastError();
+}
+
+// Heaviest-first order over several views' tiles: one CTA, counting sort of min(count, 1023)
+// descending; entries are (view << 20 | tile).
+struct BatchCounts {
+    const uint32_t *counts[kMaxViews];
+    int n_tiles[kMaxViews];
+    int n;
+};
+__global__ void k_batch_order(BatchCounts bc, uint32_t *__restrict__ order) {
+    __shared__ unsigned hist[kOrderBuckets];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int v = 0; v < bc.n; ++v)
+        for (int t = tid; t < bc.n_tiles[v]; t += blockDim.x)
+            atomicAdd(&hist[min(bc.counts[v][t], (uint32_t)kOrderBuckets - 1)], 1u);
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan over buckets in descending order, 32 buckets per lane
+        unsigned local = 0;
+        for (int q = 0; q < kOrderBuckets / 32; ++q) local += hist[kOrderBuckets - 1 - (lane * 32 + q)];
+        unsigned incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        unsigned run = incl - local;
+        for (int q = 0; q < kOrderBuckets / 32; ++q) {
+            const int b = kOrderBuckets - 1 - (lane * 32 + q);
+            const unsigned h = hist[b];
+            hist[b] = run;
+            run += h;
+        }
+    }
+    __syncthreads();
+    for (int v = 0; v < bc.n; ++v)
+        for (int t = tid; t < bc.n_tiles[v]; t += blockDim.x)
+            order[atomicAdd(&hist[min(bc.counts[v][t], (uint32_t)kOrderBuckets - 1)], 1u)] =
+                ((uint32_t)v << 20) | (uint32_t)t;
+}
+
+cudaError_t launch_batch_order(const uint32_t *const *tile_counts, const int *n_tiles, int n_views, uint32_t *order,
+                               cudaStream_t st) {
+    BatchCounts bc{};
+    bc.n = n_views;
+    for (int v = 0; v < n_views; ++v) {
+        bc.counts[v] = tile_counts[v];
+        bc.n_tiles[v] = n_tiles[v];
+    }
+    k_batch_order<<<1, 1024, 0, st>>>(bc, order);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,

@@ -54,6 +54,25 @@ struct OutDev {
     float *state = nullptr;  // arbitrary rays: 8 floats per ray of MarchResult bookkeeping
 };
 
+// One camera view of a raymarch launch: its camera, outputs and binning artefacts (K1-K3 of
+// that view), its counters and its overflow list. A launch marches the tiles of up to
+// kMaxViews views (vp_render_batch_async), passed by value as a kernel parameter.
+struct ViewDev {
+    CamDev cam;
+    OutDev od;
+    const int4 *prects;
+    const uint32_t *offsets;
+    const unsigned long long *entries;
+    DevCounters *ctr;
+    int *ovf_list;
+    int ovf_cap;
+};
+constexpr int kMaxViews = 16;
+struct ViewBatch {
+    ViewDev v[kMaxViews];
+    int n;
+};
+
 struct RaysDev {
     const float *origins;
     const float *dirs;
@@ -100,11 +119,15 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
                            int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
                            uint32_t *cursor, uint32_t *order, unsigned long long *entries,
                            int64_t capacity, DevCounters *ctr, cudaStream_t st);
-cudaError_t launch_march_tiles(const CamDev &cam, const MarchDev &mp, const float *xf16,
-                               const int4 *prects, const float4 *payload, const uint32_t *offsets,
-                               const uint32_t *order, const unsigned long long *entries,
-                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
-                               TileTier tier, cudaStream_t st);
+// K5 over the tiles of every view in `views`; `order` lists (view << 20 | tile), heaviest first.
+cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const ViewBatch &views,
+                               const uint32_t *order, int n_ctas, bool prof, TileTier tier, cudaStream_t st);
+// K5b for the views' overflow rays (one launch for all views).
+cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                        const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st);
+// Heaviest-first order over the tiles of several views (counting sort of their candidate counts).
+cudaError_t launch_batch_order(const uint32_t *const *tile_counts, const int *n_tiles, int n_views, uint32_t *order,
+                               cudaStream_t st);
 cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const MarchDev &mp,
                                   const float *xf16, const int4 *prects, int n_prim, const float4 *payload,
                                   const uint32_t *offsets, const unsigned long long *entries,

@@ -264,3 +264,33 @@ def test_tile_path_equals_ray_path_at_large_sizes(renderer, oracle, k, m, w):
     assert_bit_equal("rgb", rgb, out.color.reshape(-1, 3)[pix])
     assert_bit_equal("alpha", alpha, out.alpha.reshape(-1)[pix])
     assert_bit_equal("samples", samples, out.sample_counts[pix])
+
+
+def test_batch_render_equals_single_views(renderer):
+    """vp_render_batch_async marches the tiles of several views (different sizes) in one launch,
+    heaviest first across views; every view must equal its own vp_render bit-for-bit."""
+    import ctypes as C
+
+    import torch
+    from paper_2103_01954_b200._lib import f32p, i32p, vp_camera
+    tr, pay = synthetic.shell_arrays(4096, 8)
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(4096, 8, pay), api.WindowParams())
+    specs = [(0, 256), (11, 200), (23, 333), (40, 128), (-1, 300)]
+    cams = [synthetic.shell_camera(v, 64, w) if v >= 0 else synthetic.shell_camera(-1, 0, w) for v, w in specs]
+    want = [renderer.render(c, api.MarchConfig()) for c in cams]
+    outs = [(torch.empty(c.width * c.height * 3, device="cuda"), torch.empty(c.width * c.height, device="cuda"),
+             torch.empty(c.width * c.height, dtype=torch.int32, device="cuda")) for c in cams]
+    n = len(cams)
+    cams_c = (vp_camera * n)(*[c.to_c() for c in cams])
+    rgbp = (f32p * n)(*[C.cast(o[0].data_ptr(), f32p) for o in outs])
+    ap = (f32p * n)(*[C.cast(o[1].data_ptr(), f32p) for o in outs])
+    sp = (i32p * n)(*[C.cast(o[2].data_ptr(), i32p) for o in outs])
+    mc = api.MarchConfig().to_c()
+    lib = renderer._lib
+    for _ in range(2):  # twice: both slot groups
+        assert lib.vp_render_batch_async(renderer.ctx, n, cams_c, C.byref(mc), rgbp, ap, sp, None) == 0
+        assert lib.vp_sync(renderer.ctx) == 0
+        for o, ww, c in zip(outs, want, cams):
+            assert_bit_equal("rgb", o[0].cpu().numpy().reshape(c.height, c.width, 3), ww.color)
+            assert_bit_equal("alpha", o[1].cpu().numpy().reshape(c.height, c.width, 1), ww.alpha)
+            assert_bit_equal("samples", o[2].cpu().numpy(), ww.sample_counts)
