@@ -347,6 +347,9 @@ def main():
         h_rgb = torch.empty((V, n_px * 3), dtype=torch.float32, pin_memory=True)
         h_alpha = torch.empty((V, n_px), dtype=torch.float32, pin_memory=True)
         h_samp = torch.empty((V, n_px), dtype=torch.int32, pin_memory=True)
+        h_rgb_p = (f32p * V)(*[C.cast(h_rgb[j].data_ptr(), f32p) for j in range(V)])
+        h_alpha_p = (f32p * V)(*[C.cast(h_alpha[j].data_ptr(), f32p) for j in range(V)])
+        h_samp_p = (i32p * V)(*[C.cast(h_samp[j].data_ptr(), i32p) for j in range(V)])
         if world > 1:
             xf_host = torch.empty((k, 15), dtype=torch.float32)
             xf_dev = torch.empty((k, 15), dtype=torch.float32, device=device)
@@ -362,8 +365,14 @@ def main():
             # per step: the frame's transforms host->device, then every view rendered into
             # pinned host memory; each view's device->host copy overlaps the next render (also
             # across steps); vp_sync after the last step waits for every copy
-            if lib.vp_set_transforms(r.ctx, k, C.cast(xf_host.data_ptr(), f32p)):
+            set_xf = lib.vp_set_transforms_async if batch else lib.vp_set_transforms
+            if (set_xf(r.ctx, k, C.cast(xf_host.data_ptr(), f32p), None) if batch
+                    else set_xf(r.ctx, k, C.cast(xf_host.data_ptr(), f32p))):
                 raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+            if batch:  # one launch for the step's views; their copies overlap the next step
+                if lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), h_rgb_p, h_alpha_p, h_samp_p, None):
+                    raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+                return
             for j, cam in enumerate(cams):
                 if lib.vp_render_async(r.ctx, C.byref(cam), C.byref(mc), C.cast(h_rgb[j].data_ptr(), f32p),
                                        C.cast(h_alpha[j].data_ptr(), f32p), C.cast(h_samp[j].data_ptr(), i32p),
@@ -389,7 +398,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(all_ray / args.steps * n_e2e / float(te.item()) / 1e6, 3), "unit": METRIC,
                "h2d_bytes_per_step": 15 * 4 * k, "d2h_bytes_per_step": BYTES_PER_PIXEL * n_px * V,
-               "steps": n_e2e, "api": "vp_set_transforms + vp_render_async into pinned host outputs, vp_sync at the end"}
+               "steps": n_e2e, "api": ("vp_set_transforms_async + vp_render_batch_async" if batch else "vp_set_transforms + vp_render_async")
+                      + " into pinned host outputs, vp_sync at the end"}
 
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):

@@ -108,6 +108,12 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
                  const float *payload_planar, float window_alpha, int32_t window_beta);
 /* Replace only the transforms (same K), e.g. a new frame with the same payload. */
 int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15);
+/* Stream-ordered variant (cudaStream_t `stream`, NULL = the context's): the upload waits for
+ * the binning and raymarch of the previous render (they read the old transforms), and later
+ * renders wait for it. xf15 host (page-locked for
+ * overlap) or device; it must stay valid until the copy has run. Unlike vp_set_transforms
+ * it does not re-check the scales (the caller's records were composed by vp_compose). */
+int vp_set_transforms_async(vp_ctx *ctx, int32_t n_prim, const float *xf15, void *stream);
 /* Frame::composed() on the device (scene.h:19-24, primitive.cpp:41-49, rotation.cpp:8-27):
  * takes the frame's PrimitiveTransform records (K*24 floats, host or device) and composes
  * them into the resident transforms, bit-identical to vp_compose (the device restates glibc
@@ -150,8 +156,9 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
                     float *alpha, int32_t *samples, void *stream);
 /* A batch of 1..16 views of the resident frame in ONE raymarch launch (the tiles of all views
  * heaviest first, so the batch pays the launch's tail once; e.g. the 64-view ring in 4..8
- * calls). Outputs are arrays of device pointers (samples may be NULL), enqueued on `stream`.
- * vp_read_stats afterwards reports the last view. */
+ * calls), enqueued on `stream`. Outputs are arrays of all device or all host pointers (samples
+ * may be NULL); host outputs (page-locked for overlap) are copied out while the next batch
+ * renders: call vp_sync before reading them. vp_read_stats afterwards reports the last view. */
 int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,
                           float *const *rgb, float *const *alpha, int32_t *const *samples, void *stream);
 /* Waits for every render and output copy the context has enqueued. */

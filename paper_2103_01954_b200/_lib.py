@@ -55,6 +55,7 @@ SIGNATURES = {
     "vp_compose": (C.c_int, [C.c_int32, f32p, f32p]),
     "vp_set_scene": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32]),
     "vp_set_transforms": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
+    "vp_set_transforms_async": (C.c_int, [C.c_void_p, C.c_int32, f32p, C.c_void_p]),
     "vp_set_frame": (C.c_int, [C.c_void_p, C.c_int32, f32p]),
     "vp_get_transforms": (C.c_int, [C.c_void_p, f32p]),
     "vp_set_payload_interleaved": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f32p]),

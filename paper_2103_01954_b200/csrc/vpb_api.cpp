@@ -83,7 +83,12 @@ struct vp_ctx {
     int32_t n_prim = 0, m = 0;
     float w_alpha = 8;
     int32_t w_beta = 8;
-    DBuf<float> xf16, xf15_tmp, planar_tmp;
+    // composed transforms, 16 floats per primitive: double-buffered so vp_set_transforms_async
+    // can upload the next frame while the current one is still binned / marched
+    DBuf<float> xfb[2];
+    int xfi = 0;
+    cudaEvent_t ev_xf_binned[2] = {}, ev_xf_marched[2] = {};
+    DBuf<float> xf15_tmp, planar_tmp;
     DBuf<float> tr24;      // resident PrimitiveTransform records (vp_set_frame, vp_adam_step)
     DBuf<int> flag;        // device error flag (compose)
     bool has_xf = false;   // resident composed transforms are set
@@ -94,6 +99,14 @@ struct vp_ctx {
     BinSlot &bs() { return slot[cur]; }
     cudaStream_t bin_stream = nullptr;
     DBuf<uint32_t> batch_order[2];  // per group: heaviest-first (view, tile) order of a batch
+    // vp_render_batch_async into host memory: per slot group, device outputs of every view;
+    // the group's device->host copies (copy_stream) overlap the other group's raymarch
+    DBuf<float> bring_rgb[2], bring_alpha[2];
+    DBuf<int> bring_samples[2];
+    cudaEvent_t ev_brendered[2] = {}, ev_bcopied[2] = {};
+    // vp_set_transforms_async: the upload waits for binning still reading the old transforms
+    // (ev_last_binned) and the next binning waits for the upload (ev_xf)
+    cudaEvent_t ev_xf = nullptr, ev_last_binned = nullptr, ev_last_marched = nullptr;
     DBuf<float> out_rgb, out_alpha;
     DBuf<int> out_samples, ovf_list;
     DBuf<float> fb_e, fb_x;
@@ -191,7 +204,7 @@ int ensure_bvh(vp_ctx *ctx, MarchDev &mp) {
         VP_CUDA(ctx, ctx->bvh_nodes.ensure(size_t(n - 1)));
         const size_t bytes = bvh_scratch_bytes(n);
         VP_CUDA(ctx, ctx->bvh_scratch.ensure(bytes));
-        VP_CUDA(ctx, launch_bvh_build(ctx->xf16.p, n, ctx->bvh_nodes.p, ctx->bvh_scratch.p, bytes, ctx->stream));
+        VP_CUDA(ctx, launch_bvh_build(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_scratch.p, bytes, ctx->stream));
     }
     ctx->bvh_dirty = false;
     mp.bvh = BvhDev{ctx->bvh_nodes.p, n};
@@ -258,6 +271,7 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
         if (int rc = ensure_slot_buffers(ctx, grp[v], cams[v])) return rc;
     ViewBatch vb{};
     vb.n = n;
+    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, ctx->ev_xf, 0));  // vp_set_transforms_async
     const uint32_t *counts[kMaxViews];
     int n_tiles[kMaxViews];
     int total = 0;
@@ -265,7 +279,7 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
         BinSlot &b = grp[v];
         VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
         VP_CUDA(ctx, cudaMemsetAsync(b.d_ctr, 0, sizeof(DevCounters), ctx->bin_stream));
-        VP_CUDA(ctx, launch_binning(cams[v], ctx->xf16.p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p,
+        VP_CUDA(ctx, launch_binning(cams[v], ctx->xfb[ctx->xfi].p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p,
                                     b.tile_counts.p, b.offsets.p, b.cursor.p, b.order.p, b.entries.p,
                                     ctx->entries_cap, b.d_ctr, ctx->bin_stream));
         vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap};
@@ -280,15 +294,19 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
         order = ctx->batch_order[ctx->group].p;
     }
     VP_CUDA(ctx, cudaEventRecord(grp[0].ev_binned, ctx->bin_stream));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_last_binned, ctx->bin_stream));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf_binned[ctx->xfi], ctx->bin_stream));
     VP_CUDA(ctx, cudaStreamWaitEvent(st, grp[0].ev_binned, 0));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
-    VP_CUDA(ctx, launch_march_tiles(mp, ctx->xf16.p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
+    VP_CUDA(ctx, launch_march_tiles(mp, ctx->xfb[ctx->xfi].p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
-    VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
+    VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
                                              ctx->fb_x.p, ctx->fb_c.p, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
     for (int v = 0; v < n; ++v) VP_CUDA(ctx, cudaEventRecord(grp[v].ev_marched, st));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_last_marched, st));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf_marched[ctx->xfi], st));
     ++ctx->t_count;
     ctx->cur = ctx->group * kMaxViews + n - 1;
     ctx->d_ctr = grp[n - 1].d_ctr;
@@ -342,6 +360,15 @@ int check_ctx(vp_ctx *ctx, bool need_scene, bool need_xf = true) {
     return VP_OK;
 }
 
+// Before a synchronous entry point rewrites the resident transforms or payload: wait for the
+// asynchronous renders that may still read them (binning stream, last raymarch, own stream).
+int quiesce(vp_ctx *ctx) {
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->bin_stream));
+    VP_CUDA(ctx, cudaEventSynchronize(ctx->ev_last_marched));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
+}
+
 int check_cam(vp_ctx *ctx, const vp_camera *cam) {
     if (!cam) return fail(ctx, VP_ERR_USAGE, "null camera");
     if (cam->width < 0 || cam->height < 0) return fail(ctx, VP_ERR_USAGE, "negative image size");
@@ -384,6 +411,17 @@ int vp_create(int32_t device, vp_ctx **out) {
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_copied[1], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->bin_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_brendered[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_brendered[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_bcopied[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_bcopied[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_xf, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_last_binned, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_last_marched, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_xf_binned[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_xf_binned[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[1], cudaEventDisableTiming)) != cudaSuccess ||
 
         (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
@@ -424,7 +462,7 @@ int vp_destroy(vp_ctx *ctx) {
     for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_bwd_fwd, &ctx->s_adam})
         b->release();
     ctx->flag.release();
-    for (auto *b : {&ctx->xf16, &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
+    for (auto *b : {&ctx->xfb[0], &ctx->xfb[1], &ctx->xf15_tmp, &ctx->planar_tmp, &ctx->out_rgb, &ctx->out_alpha,
                     &ctx->fb_e, &ctx->fb_x, &ctx->ray_o, &ctx->ray_d, &ctx->ray_j})
         b->release();
     ctx->payload.release();
@@ -439,8 +477,21 @@ int vp_destroy(vp_ctx *ctx) {
         if (b.ev_marched) cudaEventDestroy(b.ev_marched);
     }
     if (ctx->bin_stream) cudaStreamDestroy(ctx->bin_stream);
-    ctx->batch_order[0].release();
-    ctx->batch_order[1].release();
+    if (ctx->ev_xf) cudaEventDestroy(ctx->ev_xf);
+    if (ctx->ev_last_binned) cudaEventDestroy(ctx->ev_last_binned);
+    if (ctx->ev_last_marched) cudaEventDestroy(ctx->ev_last_marched);
+    for (int q = 0; q < 2; ++q) {
+        if (ctx->ev_xf_binned[q]) cudaEventDestroy(ctx->ev_xf_binned[q]);
+        if (ctx->ev_xf_marched[q]) cudaEventDestroy(ctx->ev_xf_marched[q]);
+    }
+    for (int g = 0; g < 2; ++g) {
+        ctx->batch_order[g].release();
+        ctx->bring_rgb[g].release();
+        ctx->bring_alpha[g].release();
+        ctx->bring_samples[g].release();
+        if (ctx->ev_brendered[g]) cudaEventDestroy(ctx->ev_brendered[g]);
+        if (ctx->ev_bcopied[g]) cudaEventDestroy(ctx->ev_bcopied[g]);
+    }
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -466,6 +517,7 @@ int vp_compose(int32_t n_prim, const float *tr24, float *xf15) {
 
 int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
     if (int rc = check_ctx(ctx, false)) return rc;
+    if (int rc = quiesce(ctx)) return rc;
     if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
     if (n_prim == 0) return VP_OK;
     if (!xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
@@ -477,7 +529,7 @@ int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
                 return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
         }
     }
-    VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
+    VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(size_t(n_prim) * 16));
     const float *src = xf15;
     if (!dev) {
         VP_CUDA(ctx, ctx->xf15_tmp.ensure(size_t(n_prim) * 15));
@@ -485,27 +537,50 @@ int vp_set_transforms(vp_ctx *ctx, int32_t n_prim, const float *xf15) {
                                      cudaMemcpyHostToDevice, ctx->stream));
         src = ctx->xf15_tmp.p;
     }
-    VP_CUDA(ctx, launch_pad_xf(src, ctx->xf16.p, n_prim, ctx->stream));
+    VP_CUDA(ctx, launch_pad_xf(src, ctx->xfb[ctx->xfi].p, n_prim, ctx->stream));
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->has_xf = true;
     ctx->bvh_dirty = true;
     return VP_OK;
 }
 
+int vp_set_transforms_async(vp_ctx *ctx, int32_t n_prim, const float *xf15, void *stream) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
+    if (n_prim == 0) return VP_OK;
+    if (!xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
+    if (!ctx->has_xf) return fail(ctx, VP_ERR_USAGE, "set the frame's transforms synchronously first");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    // upload into the other buffer, once the binning and raymarch that last read it are done
+    const int j = ctx->xfi ^ 1;
+    VP_CUDA(ctx, ctx->xfb[j].ensure(size_t(n_prim) * 16));
+    VP_CUDA(ctx, ctx->xf15_tmp.ensure(size_t(n_prim) * 15));
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_xf_binned[j], 0));
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_xf_marched[j], 0));
+    VP_CUDA(ctx, cudaMemcpyAsync(ctx->xf15_tmp.p, xf15, sizeof(float) * 15 * size_t(n_prim), cudaMemcpyDefault, st));
+    VP_CUDA(ctx, launch_pad_xf(ctx->xf15_tmp.p, ctx->xfb[j].p, n_prim, st));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf, st));
+    if (st != ctx->stream) VP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_xf, 0));
+    ctx->xfi = j;
+    ctx->bvh_dirty = true;
+    return VP_OK;
+}
+
 int vp_set_frame(vp_ctx *ctx, int32_t n_prim, const float *tr24) {
     if (int rc = check_ctx(ctx, false)) return rc;
+    if (int rc = quiesce(ctx)) return rc;
     if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
     if (n_prim == 0) return VP_OK;
     if (!tr24) return fail(ctx, VP_ERR_USAGE, "null transforms");
     cudaStream_t st = ctx->stream;
     VP_CUDA(ctx, ctx->tr24.ensure(size_t(n_prim) * 24));
-    VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
+    VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(size_t(n_prim) * 16));
     VP_CUDA(ctx, ctx->flag.ensure(1));
     if ((const void *)tr24 != (const void *)ctx->tr24.p)
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->tr24.p, tr24, sizeof(float) * 24 * size_t(n_prim),
                                      is_device_ptr(tr24) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     VP_CUDA(ctx, cudaMemsetAsync(ctx->flag.p, 0, sizeof(int), st));
-    VP_CUDA(ctx, launch_compose(ctx->tr24.p, nullptr, n_prim, ctx->xf16.p, ctx->flag.p, st));
+    VP_CUDA(ctx, launch_compose(ctx->tr24.p, nullptr, n_prim, ctx->xfb[ctx->xfi].p, ctx->flag.p, st));
     int bad = 0;
     VP_CUDA(ctx, cudaMemcpyAsync(&bad, ctx->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
@@ -519,7 +594,7 @@ int vp_get_transforms(vp_ctx *ctx, float *xf15) {
     if (int rc = check_ctx(ctx, true)) return rc;
     if (ctx->n_prim == 0) return VP_OK;
     if (!xf15) return fail(ctx, VP_ERR_USAGE, "null destination");
-    VP_CUDA(ctx, cudaMemcpy2DAsync(xf15, 15 * sizeof(float), ctx->xf16.p, 16 * sizeof(float), 15 * sizeof(float),
+    VP_CUDA(ctx, cudaMemcpy2DAsync(xf15, 15 * sizeof(float), ctx->xfb[ctx->xfi].p, 16 * sizeof(float), 15 * sizeof(float),
                                    size_t(ctx->n_prim),
                                    is_device_ptr(xf15) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                    ctx->stream));
@@ -530,6 +605,7 @@ int vp_get_transforms(vp_ctx *ctx, float *xf15) {
 int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
                  const float *payload, float window_alpha, int32_t window_beta) {
     if (int rc = check_ctx(ctx, false)) return rc;
+    if (int rc = quiesce(ctx)) return rc;
     if (n_prim < 0) return fail(ctx, VP_ERR_USAGE, "negative primitive count");
     if (n_prim > 0 && m < 1) return fail(ctx, VP_ERR_USAGE, "voxels per axis must be >= 1");
     if (!std::isfinite(window_alpha)) return fail(ctx, VP_ERR_USAGE, "window alpha must be finite");
@@ -547,7 +623,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
             return rc;
         }
     } else {
-        VP_CUDA(ctx, ctx->xf16.ensure(size_t(n_prim) * 16));
+        VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(size_t(n_prim) * 16));
     }
     const int64_t m3 = int64_t(m) * m * m;
     const size_t nf = size_t(n_prim) * 4 * size_t(m3);
@@ -568,6 +644,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
 
 int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *inter) {
     if (int rc = check_ctx(ctx, true, false)) return rc;
+    if (int rc = quiesce(ctx)) return rc;
     if (n_prim != ctx->n_prim || m != ctx->m) return fail(ctx, VP_ERR_USAGE, "payload shape mismatch");
     if (n_prim == 0) return VP_OK;
     if (!inter) return fail(ctx, VP_ERR_USAGE, "null payload");
@@ -669,27 +746,58 @@ int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, c
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n_views < 1 || n_views > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per batch");
-    if (!cams || !rgb || !alpha) return fail(ctx, VP_ERR_USAGE, "null arguments");
+    if (!cams || !rgb || !alpha || !rgb[0]) return fail(ctx, VP_ERR_USAGE, "null arguments");
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    const bool host_out = !is_device_ptr(rgb[0]);
     CamDev cds[kMaxViews];
     OutDev ods[kMaxViews];
+    size_t px_off[kMaxViews + 1] = {0};
     for (int v = 0; v < n_views; ++v) {
         if (int rc = check_cam(ctx, &cams[v])) return rc;
-        if (size_t(cams[v].width) * cams[v].height == 0) return fail(ctx, VP_ERR_USAGE, "empty view in a batch");
+        const size_t n_px = size_t(cams[v].width) * cams[v].height;
+        if (n_px == 0) return fail(ctx, VP_ERR_USAGE, "empty view in a batch");
         int32_t *sp = samples ? samples[v] : nullptr;
-        if (!rgb[v] || !alpha[v] || !is_device_ptr(rgb[v]) || !is_device_ptr(alpha[v]) || (sp && !is_device_ptr(sp)))
-            return fail(ctx, VP_ERR_USAGE, "batch outputs must be device pointers");
+        if (!rgb[v] || !alpha[v] || is_device_ptr(rgb[v]) != !host_out || is_device_ptr(alpha[v]) != !host_out ||
+            (sp && is_device_ptr(sp) != !host_out))
+            return fail(ctx, VP_ERR_USAGE, "batch outputs must be all device or all host pointers");
         cds[v] = make_cam(cams[v]);
         ods[v] = OutDev{rgb[v], alpha[v], sp};
-        if (ctx->n_prim == 0) {
-            const size_t n_px = size_t(cams[v].width) * cams[v].height;
-            VP_CUDA(ctx, cudaMemsetAsync(rgb[v], 0, 12 * n_px, st));
-            VP_CUDA(ctx, cudaMemsetAsync(alpha[v], 0, 4 * n_px, st));
-            if (sp) VP_CUDA(ctx, cudaMemsetAsync(sp, 0, 4 * n_px, st));
-        }
+        px_off[v + 1] = px_off[v] + n_px;
     }
-    if (ctx->n_prim == 0) return VP_OK;
-    return enqueue_views(ctx, n_views, cds, make_march(ctx, cfg), ods, st);
+    const int g = ctx->group ^ 1;  // the slot group enqueue_views is about to use
+    if (host_out) {  // render into the group's device outputs; copied out on copy_stream
+        VP_CUDA(ctx, ctx->bring_rgb[g].ensure(3 * px_off[n_views]));
+        VP_CUDA(ctx, ctx->bring_alpha[g].ensure(px_off[n_views]));
+        if (samples) VP_CUDA(ctx, ctx->bring_samples[g].ensure(px_off[n_views]));
+        VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_bcopied[g], 0));
+        for (int v = 0; v < n_views; ++v)
+            ods[v] = OutDev{ctx->bring_rgb[g].p + 3 * px_off[v], ctx->bring_alpha[g].p + px_off[v],
+                            samples && samples[v] ? ctx->bring_samples[g].p + px_off[v] : nullptr};
+    }
+    if (ctx->n_prim == 0) {
+        for (int v = 0; v < n_views; ++v) {
+            const size_t n_px = px_off[v + 1] - px_off[v];
+            VP_CUDA(ctx, cudaMemsetAsync(ods[v].rgb, 0, 12 * n_px, st));
+            VP_CUDA(ctx, cudaMemsetAsync(ods[v].alpha, 0, 4 * n_px, st));
+            if (ods[v].samples) VP_CUDA(ctx, cudaMemsetAsync(ods[v].samples, 0, 4 * n_px, st));
+        }
+        ctx->group = g;
+    } else if (int rc = enqueue_views(ctx, n_views, cds, make_march(ctx, cfg), ods, st)) {
+        return rc;
+    }
+    if (!host_out) return VP_OK;
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_brendered[g], st));
+    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_brendered[g], 0));
+    for (int v = 0; v < n_views; ++v) {
+        const size_t n_px = px_off[v + 1] - px_off[v];
+        VP_CUDA(ctx, cudaMemcpyAsync(rgb[v], ods[v].rgb, 12 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        VP_CUDA(ctx, cudaMemcpyAsync(alpha[v], ods[v].alpha, 4 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        if (ods[v].samples)
+            VP_CUDA(ctx, cudaMemcpyAsync(samples[v], ods[v].samples, 4 * n_px, cudaMemcpyDeviceToHost,
+                                         ctx->copy_stream));
+    }
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_bcopied[g], ctx->copy_stream));
+    return VP_OK;
 }
 
 int vp_sync(vp_ctx *ctx) {
@@ -821,10 +929,10 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         VP_CUDA(ctx, cudaMemsetAsync(od.alpha, 0, 4 * n, st));
         if (od.samples) VP_CUDA(ctx, cudaMemsetAsync(od.samples, 0, 4 * n, st));
     } else {
-        VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, rays, n_rays, od,
+        VP_CUDA(ctx, launch_march_rays(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, rays, n_rays, od,
                                        ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap, st));
         const CamDev none{};
-        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, ctx->n_prim, ctx->payload.p,
+        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, ctx->n_prim, ctx->payload.p,
                                            nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p,
                                            ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
     }
@@ -881,7 +989,7 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
-        VP_CUDA(ctx, launch_binning(cd, ctx->xf16.p, ctx->n_prim, ctx->bs().rects.p, ctx->bs().prects.p, ctx->bs().keys.p,
+        VP_CUDA(ctx, launch_binning(cd, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->bs().rects.p, ctx->bs().prects.p, ctx->bs().keys.p,
                                     ctx->bs().tile_counts.p, ctx->bs().offsets.p, ctx->bs().cursor.p, ctx->bs().order.p, ctx->bs().entries.p,
                                     ctx->entries_cap, ctx->d_ctr, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
@@ -987,16 +1095,16 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                 VP_CUDA(ctx, ctx->ovf_list.ensure(n));
                 ctx->ovf_cap = int(n);
             }
-            VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays, od, ctx->d_ctr,
+            VP_CUDA(ctx, launch_march_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays, od, ctx->d_ctr,
                                            ctx->ovf_list.p, ctx->ovf_cap, st));
             const CamDev none{};
-            VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, k, ctx->payload.p, nullptr,
+            VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, k, ctx->payload.p, nullptr,
                                                nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
                                                ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
             fwd_state = od.state;
         }
         const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state};
-        VP_CUDA(ctx, launch_backward_rays(mp, ctx->xf16.p, k, ctx->payload.p, rays, n_rays,
+        VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
     }
@@ -1088,10 +1196,10 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
         VP_CUDA(ctx, cudaMemsetAsync(d_rgb, 0, 12 * nn, st));
         VP_CUDA(ctx, cudaMemsetAsync(d_a, 0, 4 * nn, st));
     } else {
-        VP_CUDA(ctx, launch_march_rays(mp, ctx->xf16.p, ctx->n_prim, ctx->payload.p, rays, n, od, ctx->d_ctr,
+        VP_CUDA(ctx, launch_march_rays(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, rays, n, od, ctx->d_ctr,
                                        ctx->ovf_list.p, ctx->ovf_cap, st));
         const CamDev none{};
-        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xf16.p, nullptr, ctx->n_prim, ctx->payload.p,
+        VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, ctx->n_prim, ctx->payload.p,
                                            nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
                                            ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
     }
@@ -1211,6 +1319,7 @@ int vp_adam_reset(vp_ctx *ctx) {
 
 int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *transforms24) {
     if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = quiesce(ctx)) return rc;
     if (!cfg || !grads) return fail(ctx, VP_ERR_USAGE, "null arguments");
     const int k = ctx->n_prim, m = ctx->m;
     if (k > 0 && !transforms24) return fail(ctx, VP_ERR_USAGE, "null transforms");
@@ -1253,8 +1362,8 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
                              int64_t(n), unsigned(m3), c, d_bad, false, st));
     // deltas back into the records with the scale projection (losses.cpp:97-103), then the
     // frame is recomposed on the device (primitive.cpp:41-49)
-    VP_CUDA(ctx, ctx->xf16.ensure(16 * size_t(k)));
-    VP_CUDA(ctx, launch_compose(ctx->tr24.p, d_delta, k, ctx->xf16.p, d_bad, st));
+    VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(16 * size_t(k)));
+    VP_CUDA(ctx, launch_compose(ctx->tr24.p, d_delta, k, ctx->xfb[ctx->xfi].p, d_bad, st));
     if ((const void *)transforms24 != (const void *)ctx->tr24.p)
         VP_CUDA(ctx, cudaMemcpyAsync(transforms24, ctx->tr24.p, 4 * 24 * size_t(k),
                                      is_device_ptr(transforms24) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,

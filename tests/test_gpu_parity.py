@@ -294,3 +294,55 @@ def test_batch_render_equals_single_views(renderer):
             assert_bit_equal("rgb", o[0].cpu().numpy().reshape(c.height, c.width, 3), ww.color)
             assert_bit_equal("alpha", o[1].cpu().numpy().reshape(c.height, c.width, 1), ww.alpha)
             assert_bit_equal("samples", o[2].cpu().numpy(), ww.sample_counts)
+    # host outputs (page-locked): copied out while the next batch renders
+    hosts = [(torch.empty(c.width * c.height * 3, pin_memory=True), torch.empty(c.width * c.height, pin_memory=True),
+              torch.empty(c.width * c.height, dtype=torch.int32, pin_memory=True)) for c in cams]
+    hrgb = (f32p * n)(*[C.cast(o[0].data_ptr(), f32p) for o in hosts])
+    ha = (f32p * n)(*[C.cast(o[1].data_ptr(), f32p) for o in hosts])
+    hs = (i32p * n)(*[C.cast(o[2].data_ptr(), i32p) for o in hosts])
+    for _ in range(3):
+        assert lib.vp_render_batch_async(renderer.ctx, n, cams_c, C.byref(mc), hrgb, ha, hs, None) == 0
+    assert lib.vp_sync(renderer.ctx) == 0
+    for o, ww, c in zip(hosts, want, cams):
+        assert_bit_equal("rgb", o[0].numpy().reshape(c.height, c.width, 3), ww.color)
+        assert_bit_equal("alpha", o[1].numpy().reshape(c.height, c.width, 1), ww.alpha)
+        assert_bit_equal("samples", o[2].numpy(), ww.sample_counts)
+
+
+def test_async_transform_updates_between_batches(renderer):
+    """vp_set_transforms_async between batches (new poses every batch, no host sync): each
+    batch sees exactly its own transforms (compared with synchronous renders)."""
+    import ctypes as C
+
+    import torch
+    from paper_2103_01954_b200._lib import f32p, i32p, vp_camera
+    tr, pay = synthetic.shell_arrays(512, 8)
+    poses = []
+    for q in range(3):
+        t = tr.copy()
+        t[:, 15:18] += np.float32(0.01 * q)
+        poses.append(api.compose(t))
+    renderer.set_scene_composed(poses[0], api.PrimitiveSlab(512, 8, pay), api.WindowParams())
+    cams = [synthetic.shell_camera(v, 64, 160) for v in (3, 30)]
+    want = []
+    for xf in poses:
+        renderer.set_transforms(xf)
+        want.append([renderer.render(c, api.MarchConfig()) for c in cams])
+    renderer.set_transforms(poses[0])
+    lib, mc = renderer._lib, api.MarchConfig().to_c()
+    n = len(cams)
+    cams_c = (vp_camera * n)(*[c.to_c() for c in cams])
+    pinned = [torch.from_numpy(np.ascontiguousarray(xf)).pin_memory() for xf in poses]
+    outs = [[(torch.empty(160 * 160 * 3, pin_memory=True), torch.empty(160 * 160, pin_memory=True),
+              torch.empty(160 * 160, dtype=torch.int32, pin_memory=True)) for _ in cams] for _ in poses]
+    for q, xf in enumerate(pinned):
+        assert lib.vp_set_transforms_async(renderer.ctx, 512, C.cast(xf.data_ptr(), f32p), None) == 0
+        rgbp = (f32p * n)(*[C.cast(o[0].data_ptr(), f32p) for o in outs[q]])
+        ap = (f32p * n)(*[C.cast(o[1].data_ptr(), f32p) for o in outs[q]])
+        sp = (i32p * n)(*[C.cast(o[2].data_ptr(), i32p) for o in outs[q]])
+        assert lib.vp_render_batch_async(renderer.ctx, n, cams_c, C.byref(mc), rgbp, ap, sp, None) == 0
+    assert lib.vp_sync(renderer.ctx) == 0
+    for q in range(3):
+        for o, ww in zip(outs[q], want[q]):
+            assert_bit_equal("rgb", o[0].numpy().reshape(160, 160, 3), ww.color)
+            assert_bit_equal("samples", o[2].numpy(), ww.sample_counts)
