@@ -419,7 +419,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": 6 * V * args.steps,
                 "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
-                "stats_last_view": rc_stats.as_dict()}
+                "stats_last_launch": rc_stats.as_dict()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

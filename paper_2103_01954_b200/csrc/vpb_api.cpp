@@ -113,6 +113,8 @@ struct vp_ctx {
     DBuf<int> fb_c;
     DBuf<float> ray_o, ray_d, ray_j;
     DevCounters *d_ctr = nullptr, *h_ctr = nullptr;
+    DevCounters *last_ctr[kMaxViews] = {};  // the counters of the latest render launch's views
+    int last_n = 1;                          // 1: ctx->d_ctr alone (single view / ray calls)
     int64_t entries_cap = 0;
     int ovf_cap = 0;
     cudaEvent_t t_ev[2 * kTimingSlots] = {};
@@ -310,6 +312,8 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     ++ctx->t_count;
     ctx->cur = ctx->group * kMaxViews + n - 1;
     ctx->d_ctr = grp[n - 1].d_ctr;
+    for (int v = 0; v < n; ++v) ctx->last_ctr[v] = grp[v].d_ctr;
+    ctx->last_n = n;
     return VP_OK;
 }
 
@@ -706,6 +710,7 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
     if (!rgb_dev || !alpha_dev) return fail(ctx, VP_ERR_USAGE, "null output");
     if (ctx->n_prim == 0) {
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
         VP_CUDA(ctx, cudaMemsetAsync(rgb_dev, 0, n_px * 3 * sizeof(float), st));
         VP_CUDA(ctx, cudaMemsetAsync(alpha_dev, 0, n_px * sizeof(float), st));
         if (samples_dev) VP_CUDA(ctx, cudaMemsetAsync(samples_dev, 0, n_px * sizeof(int32_t), st));
@@ -809,12 +814,33 @@ int vp_sync(vp_ctx *ctx) {
 
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
     if (int rc = check_ctx(ctx, false)) return rc;
-    VP_CUDA(ctx, cudaMemcpy(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
-    const DevCounters c = *ctx->h_ctr;
+    // the latest launch may still run on a caller's stream
+    VP_CUDA(ctx, cudaEventSynchronize(ctx->ev_last_marched));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    DevCounters c{};
+    unsigned long long max_keys = 0;  // the key capacity a single view needs
+    for (int v = 0; v < (ctx->last_n > 1 ? ctx->last_n : 1); ++v) {  // a batch: summed over its views
+        VP_CUDA(ctx, cudaMemcpy(ctx->h_ctr, ctx->last_n > 1 ? ctx->last_ctr[v] : ctx->d_ctr, sizeof(DevCounters),
+                                cudaMemcpyDeviceToHost));
+        const DevCounters &q = *ctx->h_ctr;
+        c.ray_samples += q.ray_samples;
+        c.prim_samples += q.prim_samples;
+        c.hit_rays += q.hit_rays;
+        c.early_exits += q.early_exits;
+        c.saturated += q.saturated;
+        c.overflow_rays += q.overflow_rays;
+        c.refills += q.refills;
+        c.keys += q.keys;
+        max_keys = std::max(max_keys, q.keys);
+        c.numeric_fail += q.numeric_fail;
+        c.nonempty_tiles += q.nonempty_tiles;
+        c.key_overflow |= q.key_overflow;
+        c.fallback_fail |= q.fallback_fail;
+    }
     note_density(ctx, c);
     fill_stats(c, 0.f, stats);
     if (c.key_overflow) {
-        ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
+        ctx->entries_cap = int64_t(max_keys) + int64_t(max_keys) / 4 + 1024;
         return fail(ctx, VP_ERR_DEVICE, "tile key buffer was too small; capacity grown, render again");
     }
     return check_counters(ctx, c);
@@ -924,6 +950,7 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     MarchDev mp = make_march(ctx, cfg);
     if (int rc = ensure_bvh(ctx, mp)) return rc;
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
     if (ctx->n_prim == 0) {
         VP_CUDA(ctx, cudaMemsetAsync(od.rgb, 0, 12 * n, st));
         VP_CUDA(ctx, cudaMemsetAsync(od.alpha, 0, 4 * n, st));
@@ -989,6 +1016,7 @@ int vp_debug_tiles(vp_ctx *ctx, const vp_camera *cam, int32_t *rect4, uint32_t *
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
         VP_CUDA(ctx, launch_binning(cd, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->bs().rects.p, ctx->bs().prects.p, ctx->bs().keys.p,
                                     ctx->bs().tile_counts.p, ctx->bs().offsets.p, ctx->bs().cursor.p, ctx->bs().order.p, ctx->bs().entries.p,
                                     ctx->entries_cap, ctx->d_ctr, st));
@@ -1083,6 +1111,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         if (int rc = ensure_fallback(ctx)) return rc;
         VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
         MarchDev mp = make_march(ctx, cfg);
         if (int rc = ensure_bvh(ctx, mp)) return rc;
         if (!fwd_state) {
@@ -1192,6 +1221,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     MarchDev mp = make_march(ctx, cfg);
     if (int rc = ensure_bvh(ctx, mp)) return rc;
     VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
     if (ctx->n_prim == 0) {
         VP_CUDA(ctx, cudaMemsetAsync(d_rgb, 0, 12 * nn, st));
         VP_CUDA(ctx, cudaMemsetAsync(d_a, 0, 4 * nn, st));

@@ -287,9 +287,13 @@ def test_batch_render_equals_single_views(renderer):
     sp = (i32p * n)(*[C.cast(o[2].data_ptr(), i32p) for o in outs])
     mc = api.MarchConfig().to_c()
     lib = renderer._lib
+    from paper_2103_01954_b200._lib import vp_stats
     for _ in range(2):  # twice: both slot groups
         assert lib.vp_render_batch_async(renderer.ctx, n, cams_c, C.byref(mc), rgbp, ap, sp, None) == 0
-        assert lib.vp_sync(renderer.ctx) == 0
+        st = vp_stats()
+        assert lib.vp_read_stats(renderer.ctx, C.byref(st)) == 0  # summed over the batch's views
+        assert st.ray_samples == sum(ww.stats["ray_samples"] for ww in want)
+        assert st.prim_samples == sum(ww.stats["prim_samples"] for ww in want)
         for o, ww, c in zip(outs, want, cams):
             assert_bit_equal("rgb", o[0].cpu().numpy().reshape(c.height, c.width, 3), ww.color)
             assert_bit_equal("alpha", o[1].cpu().numpy().reshape(c.height, c.width, 1), ww.alpha)
