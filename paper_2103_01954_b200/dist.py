@@ -58,44 +58,60 @@ def broadcast_scene(renderer, xf15: Optional[np.ndarray], slab, window, n_prim: 
 
 
 class ViewGather:
-    """Per-step output buffer ([views, H*W*5] float32 rows: rgb, alpha, samples as int32
-    bits) and the per-view asynchronous gather to rank `dst`, so the transfer of view j
-    overlaps the rendering of view j+1 (NCCL runs on its own stream after the view's
-    kernels, which are enqueued on torch's current stream)."""
+    """Per-step output buffers ([views, H*W*5] float32 rows: rgb, alpha, samples as int32
+    bits) and the per-view asynchronous gather to rank `dst`.
+
+    There are `slots` output buffers (default 2): step s renders into slot s % slots, and its
+    gathers run on NCCL's stream while step s+1 renders into the other slot. Before a slot is
+    rendered into again, `wait_slot` makes the current stream wait for the gathers that read
+    it, so at most one step of transfers is in flight and it overlaps the next step's raymarch
+    instead of serialising behind it."""
 
     def __init__(self, n_local: int, width: int, height: int, device, world: int, rank: int,
-                 dst: int = 0):
+                 dst: int = 0, slots: int = 2):
         import torch
         self.hw = width * height
-        self.buf = torch.zeros((n_local, 5 * self.hw), dtype=torch.float32, device=device)
+        self.slots = max(1, slots)
+        self.bufs = [torch.zeros((n_local, 5 * self.hw), dtype=torch.float32, device=device)
+                     for _ in range(self.slots)]
+        self.buf = self.bufs[0]
         self.world, self.rank, self.dst = world, rank, dst
-        self.recv = ([[torch.empty(5 * self.hw, dtype=torch.float32, device=device) for _ in range(world)]
-                      for _ in range(n_local)] if rank == dst else None)
-        self.works = []
+        self.recvs = ([[[torch.empty(5 * self.hw, dtype=torch.float32, device=device) for _ in range(world)]
+                        for _ in range(n_local)] for _ in range(self.slots)] if rank == dst else None)
+        self.recv = self.recvs[0] if self.recvs is not None else None
+        self.works = [[] for _ in range(self.slots)]
 
-    def views(self):
-        """(rgb, alpha, samples) row views, one row per local view."""
+    def views(self, slot: int = 0):
+        """(rgb, alpha, samples) row views of one slot, one row per local view."""
         import torch
-        hw = self.hw
-        return self.buf[:, :3 * hw], self.buf[:, 3 * hw:4 * hw], self.buf[:, 4 * hw:].view(torch.int32)
+        hw, buf = self.hw, self.bufs[slot % self.slots]
+        return buf[:, :3 * hw], buf[:, 3 * hw:4 * hw], buf[:, 4 * hw:].view(torch.int32)
 
-    def gather_view(self, j: int, async_op: bool = True):
+    def gather_view(self, j: int, async_op: bool = True, slot: int = 0):
         import torch.distributed as dist
         if self.world == 1:
             return
-        w = dist.gather(self.buf[j], self.recv[j] if self.rank == self.dst else None,
+        s = slot % self.slots
+        w = dist.gather(self.bufs[s][j], self.recvs[s][j] if self.rank == self.dst else None,
                         dst=self.dst, async_op=async_op)
         if async_op:
-            self.works.append(w)
+            self.works[s].append(w)
+
+    def wait_slot(self, slot: int):
+        """The current stream waits for the in-flight gathers that read `slot` (call before
+        rendering into it again)."""
+        s = slot % self.slots
+        for w in self.works[s]:
+            w.wait()
+        self.works[s].clear()
 
     def finish(self):
-        for w in self.works:
-            w.wait()
-        self.works.clear()
+        for s in range(self.slots):
+            self.wait_slot(s)
 
-    def gathered(self, j: int):
-        """On rank dst: per-rank [5*H*W] rows of local view j."""
-        return self.recv[j]
+    def gathered(self, j: int, slot: int = 0):
+        """On rank dst: per-rank [5*H*W] rows of local view j of one slot."""
+        return self.recvs[slot % self.slots][j]
 
     @staticmethod
     def unpack(row, width: int, height: int):

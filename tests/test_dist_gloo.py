@@ -68,23 +68,30 @@ def _worker(rank, world, port, q):
         ok_bcast = bool(np.array_equal(r.payload, want) and np.array_equal(r.xf, xf) and nbytes == want.nbytes)
 
         # per-view gather: each rank renders 3 "views" of 4x2 pixels
+        # in two steps, into the two output slots (as bench.py's step i uses slot i % 2)
         w, h, nv = 4, 2, 3
         vg = ViewGather(nv, w, h, "cpu", world, rank)
-        rgb, alpha, samples = vg.views()
-        for j in range(nv):
-            rgb[j].fill_(rank * 10 + j)
-            alpha[j].fill_(0.5 + rank)
-            samples[j].fill_(100 * rank + j)
-            vg.gather_view(j)
+        assert vg.slots == 2
+        for step in range(3):
+            slot = step % vg.slots
+            vg.wait_slot(slot)
+            rgb, alpha, samples = vg.views(slot)
+            for j in range(nv):
+                rgb[j].fill_(rank * 10 + j + 1000 * step)
+                alpha[j].fill_(0.5 + rank + step)
+                samples[j].fill_(100 * rank + j + 1000 * step)
+                vg.gather_view(j, slot=slot)
         vg.finish()
         ok_gather = True
         if rank == 0:
-            for j in range(nv):
-                rows = vg.gathered(j)
-                for src in range(world):
-                    c, a, s = ViewGather.unpack(rows[src], w, h)
-                    ok_gather &= bool(torch.all(c == src * 10 + j)) and bool(torch.all(a == 0.5 + src))
-                    ok_gather &= bool(torch.all(s == 100 * src + j))
+            for step, slot in ((1, 1), (2, 0)):  # the latest step in each slot
+                for j in range(nv):
+                    rows = vg.gathered(j, slot)
+                    for src in range(world):
+                        c, a, s = ViewGather.unpack(rows[src], w, h)
+                        ok_gather &= bool(torch.all(c == src * 10 + j + 1000 * step))
+                        ok_gather &= bool(torch.all(a == 0.5 + src + step))
+                        ok_gather &= bool(torch.all(s == 100 * src + j + 1000 * step))
         q.put((rank, ok_bcast, ok_gather))
     finally:
         dist.destroy_process_group()
