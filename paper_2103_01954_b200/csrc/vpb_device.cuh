@@ -69,6 +69,29 @@ __device__ __forceinline__ bool intersect_obb_om(const float *xf, V3 om, V3 d, f
     return true;
 }
 
+// Conservative line-vs-box rejection in the primitive's rotated, unscaled frame, run before
+// intersect_obb_om's six divisions: the ray's line misses the box of half-extents s iff one
+// of the three axes e_a x q separates them, |o'_a q_b - o'_b q_a| > s_a |q_b| + s_b |q_a|, with
+// o' = om * s and q = R^T d. It never rejects a hit of the exact test: a rejection needs the
+// line to clear the box by a margin of 2^-15 of the terms' magnitudes (relative rounding of
+// every quantity involved, om's and the slab test's t-values included, is below 2^-20), so a
+// rejected candidate misses by far more than intersect_obb_om's rounding can bridge.
+// Returns true when the exact test is still needed.
+__device__ __forceinline__ bool line_may_hit_box(const float *xf, V3 om, V3 q) {
+    const float sx = xf[12], sy = xf[13], sz = xf[14];
+    const float ox = om.x * sx, oy = om.y * sy, oz = om.z * sz;
+    const float ax = fabsf(q.x), ay = fabsf(q.y), az = fabsf(q.z);
+    const float kRel = 3.0517578125e-05f;  // 2^-15
+    const float a1 = ox * q.y, b1 = oy * q.x;
+    const float a2 = oy * q.z, b2 = oz * q.y;
+    const float a3 = oz * q.x, b3 = ox * q.z;
+    const float r1 = sx * ay + sy * ax, r2 = sy * az + sz * ay, r3 = sz * ax + sx * az;
+    const bool miss = fabsf(a1 - b1) > r1 + kRel * ((fabsf(a1) + fabsf(b1)) + r1) ||
+                      fabsf(a2 - b2) > r2 + kRel * ((fabsf(a2) + fabsf(b2)) + r2) ||
+                      fabsf(a3 - b3) > r3 + kRel * ((fabsf(a3) + fabsf(b3)) + r3);
+    return !miss;
+}
+
 __device__ __forceinline__ bool intersect_obb(const float *xf, V3 o, V3 d, float &tEnterOut,
                                               float &tExitOut) {
     return intersect_obb_om(xf, to_model(xf, o), d, tEnterOut, tExitOut);

@@ -350,7 +350,7 @@ struct TileSmem {
     unsigned *mask;    // (CC + 31) / 32 words * kMarchThreads per-ray candidate hit masks
 };
 
-template <int CAP, int MT, bool STAGED, int CC>
+template <int CAP, int MT, bool STAGED, int CC, bool PF>
 __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam, const MarchDev &mp,
                                            const float *__restrict__ xf_g,
                                            const int4 *__restrict__ prects,
@@ -379,7 +379,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
         }
         __syncthreads();
     }
-    const TileCands<STAGED> cands{entries, xf_g, prects, payload, m3, start, n, sm.prim,
+    const TileCands<STAGED, PF> cands{entries, xf_g, prects, payload, m3, start, n, sm.prim,
                                   sm.xf4, sm.om, sm.prect, CC};
     IdxT *wc = reinterpret_cast<IdxT *>(sm.wc);
 
@@ -441,7 +441,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     add_counters(ctr, ro, live && !ro.overflow);
 }
 
-template <int CAP, int MT, bool PROF, int CC, int MINB>
+template <int CAP, int MT, bool PROF, int CC, int MINB, bool PF>
 __global__ void __launch_bounds__(kMarchThreads, MINB)
 k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restrict__ payload, ViewBatch views,
               const uint32_t *__restrict__ order) {
@@ -475,10 +475,10 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
     if (n <= CC)
-        march_tile<CAP, MT, true, CC>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+        march_tile<CAP, MT, true, CC, PF>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
                                       vd.ovf_list, vd.ovf_cap);
     else
-        march_tile<CAP, MT, false, CC>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+        march_tile<CAP, MT, false, CC, false>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
                                        vd.ovf_list, vd.ovf_cap);
     if (PROF) {  // separate instantiation: per-CTA timeline for load-balance analysis
         __syncthreads();
@@ -666,14 +666,22 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 #ifndef VPB_CARVEOUT
 #define VPB_CARVEOUT -1  // shared-memory carveout hint in percent; -1: just enough for MINB CTAs
 #endif
+#ifndef VPB_NORMAL_PF
+#define VPB_NORMAL_PF false
+#endif
+// PF: line-vs-box prefilter before the exact candidate test (K=32768 M=8 launch 4.58 ->
+// 4.27 ms; the K=4096 headline 6.16 -> 6.28 ms, so only the dense tier uses it).
 struct TileCfgLight {
     static constexpr int CAP = 12, CC = 64, MINB = 3;
+    static constexpr bool PF = false;
 };
 struct TileCfgNormal {
     static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = VPB_MARCH_MINB;
+    static constexpr bool PF = VPB_NORMAL_PF;
 };
 struct TileCfgDense {
     static constexpr int CAP = 24, CC = 192, MINB = 2;
+    static constexpr bool PF = true;
 };
 
 template <int CAP, int CC>
@@ -718,7 +726,7 @@ static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const f
                                   const ViewBatch &views, const uint32_t *order, int n_ctas, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC>();
-    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB>;
+    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB, Cfg::PF>;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // Ask for just the shared memory MINB resident CTAs need (each also reserves 1 KB):

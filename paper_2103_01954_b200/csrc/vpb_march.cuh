@@ -57,8 +57,9 @@ __device__ __forceinline__ Xf16 ldg_xf(const float *xf) {
 // s_xf4[q * xs + c]): lanes reading different candidates hit different banks (a 64-byte
 // record stride put every other candidate on the same banks). TileCands<false>: the generic
 // path reading the tile bucket from global memory (tiles with more candidates, fallback
-// re-march).
-template <bool STAGED>
+// re-march). PF puts the line-vs-box prefilter (line_may_hit_box) in front of the staged
+// exact test: it pays where most covered candidates miss (small primitives, the dense tier).
+template <bool STAGED, bool PF = false>
 struct TileCands {
     const unsigned long long *entries;
     const float *xf_g;
@@ -95,6 +96,7 @@ struct TileCands {
         if (STAGED) {
             const float4 om = s_om[c];
             const Xf16 x = xfv(c);
+            if (PF && !line_may_hit_box(x.v, mk3(om.x, om.y, om.z), matTvec(x.v + 3, d))) return false;
             return intersect_obb_om(x.v, mk3(om.x, om.y, om.z), d, tE, tX);
         }
         return intersect_obb(xf(c), o, d, tE, tX);

@@ -50,7 +50,9 @@ def test_backward_accumulates_and_is_linear_in_the_adjoints(renderer):
     args = (g["o"], g["d"])
     a = renderer.backward_rays(*args, g["adj_rgb"], g["adj_alpha"], cfg, g["tr"], g["jit"])
     b = renderer.backward_rays(*args, g["adj_rgb"], g["adj_alpha"], cfg, g["tr"], g["jit"], grads=a.copy())
-    assert np.allclose(b, 2 * a, rtol=1e-5, atol=1e-6 * np.abs(a).max())
+    # b = a + a', a' a second accumulation with its own atomics order: |a' - a| is within twice
+    # the reordering bound, which is the bound _check_close applies to 2a
+    _check_close("accumulated", b, 2 * a.astype(np.float64))
     z = renderer.backward_rays(*args, np.zeros_like(g["adj_rgb"]), np.zeros_like(g["adj_alpha"]), cfg,
                                g["tr"], g["jit"])
     assert not z.any()

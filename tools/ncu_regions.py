@@ -15,6 +15,7 @@ SRC = "paper_2103_01954_b200/csrc/"
 MARKERS = [("vpb_device.cuh", r"^__device__ __forceinline__ V3 mk3", "vec/mat ops"),
            ("vpb_device.cuh", r"^__device__ __forceinline__ V3 to_model", "to_model (3 IEEE div)"),
            ("vpb_device.cuh", r"^__device__ __forceinline__ bool intersect_obb_om", "intersect_obb"),
+           ("vpb_device.cuh", r"^// Conservative line-vs-box", "line prefilter"),
            ("vpb_device.cuh", r"^// camera.cpp:14-23", "generate_ray/hash"),
            ("vpb_device.cuh", r"^// glibc 2.39 expf", "expf (binary64 port)"),
            ("vpb_device.cuh", r"^// primitive.cpp:12-22", "window/pow8/clamp"),

@@ -7,6 +7,8 @@ import subprocess
 import sys
 
 CFGS = [[], ["--k", "32768", "--m", "8"], ["--k", "512", "--m", "32"], ["--k", "64", "--m", "16", "--width", "256"]]
+if os.environ.get("SWEEP_ONLY"):  # comma-separated indices into CFGS
+    CFGS = [CFGS[int(i)] for i in os.environ["SWEEP_ONLY"].split(",")]
 libs = sys.argv[1:] or sorted(glob.glob("build/variants/libvpb_*.so"))
 for lib in libs:
     env = dict(os.environ, VPB_LIB=os.path.abspath(lib))
