@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--quick", action="store_true", help="profiling mode: no baseline / e2e")
+    p.add_argument("--tile-shard", action="store_true",
+                   help="single-view mode: each step renders ONE view (the headline camera), rank r "
+                        "marching the tiles t %% N == r (vp_render_shard_async), gathered to rank 0")
     return p.parse_args()
 
 
@@ -185,6 +188,102 @@ def workload_config(args, world, gather):
             "l2": "flushed (256 MiB write) before every timed step; payload 268 MB > 126 MB L2"}
 
 
+def run_tile_shard(args, rank, world, local, device):
+    """--tile-shard: one view per step split by tile over the ranks (single-view
+    configs). Step = this rank's shard render + the gather of every shard to rank 0 + rank 0
+    placing the tiles into the image. value = the view's ray-samples / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_01954_b200 import Renderer, api, synthetic
+    from paper_2103_01954_b200.dist import TileShardGather, broadcast_scene
+
+    k, m, w = args.k, args.m, args.width
+    r = Renderer(local)
+    xf = slab = None
+    if rank == 0:
+        tr, pay = synthetic.shell_arrays(k, m)
+        xf = api.compose(tr)
+        slab = api.PrimitiveSlab(k, m, pay)
+    win = api.WindowParams()
+    if world > 1:
+        broadcast_scene(r, xf, slab, win, k, m, device)
+    else:
+        r.set_scene_composed(xf, slab, win)
+    cam = synthetic.shell_camera(-1, 0, w)
+    cfg = api.MarchConfig()
+    g = TileShardGather(w, w, device, world, rank)
+    rgb, alpha, samp = g.outputs()
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
+
+    def step():
+        r.render_shard_device(cam, cfg, rank, world, rgb.data_ptr(), alpha.data_ptr(), samp.data_ptr(),
+                              stream.cuda_stream)
+        if world > 1:
+            g.gather()
+            g.wait()
+        if rank == 0:
+            g.assemble()
+
+    step()
+    torch.cuda.synchronize()
+    mine = r.read_stats()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    r.kernel_times()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_local = sum(a.elapsed_time(b) for a, b in evs) / 1e3
+    march_ms = r.kernel_times(4096)
+    t = torch.tensor([t_local], dtype=torch.float64, device=device)
+    tot = torch.tensor([mine["ray_samples"], mine["prim_samples"]], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot)
+    t_max = float(t.item())
+    ray_view, prim_view = (float(x) for x in tot.tolist())
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    alg = BYTES_PER_PRIM_SAMPLE * mine["prim_samples"] + BYTES_PER_PIXEL * 256 * api.shard_tiles(w, w, rank, world)
+    march_s = float(np.mean(march_ms)) / 1e3 if len(march_ms) else float("nan")
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(ray_view * args.steps / t_max / 1e6, 3), "unit": METRIC,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(1e3 * t_max / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"mvp_shell K={k} M={m}, ONE {w}x{w} view per step split by tile over "
+                                       f"{world} GPU(s) (BASELINE config {3 if k == 4096 else 'n/a'}, tile-sharded)",
+                           "K": k, "M": m, "width": w, "height": w, "parallelism": f"tile-shard x{world}",
+                           "gather_to_rank0": world > 1,
+                           "l2": "flushed (256 MiB write) before every timed step"},
+                "frames_per_s": round(args.steps / t_max, 2),
+                "prim_samples_per_s": round(prim_view * args.steps / t_max / 1e6, 3),
+                "roofline": {"bound": "hbm", "achieved": round(alg / march_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                             "frac": round(alg / march_s / 1e9 / hbm, 4), "traffic": None,
+                             "kernel": "k_march_tiles (+k_march_fallback_views), rank 0's shard",
+                             "peak_kind": pk_kind, "avg_launch_ms": round(march_s * 1e3, 4)},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": 6 * args.steps, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    r.close()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -206,6 +305,11 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    if args.tile_shard:
+        run_tile_shard(args, rank, world, local, device)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     gather = world > 1 and not args.no_gather
     k, m, w = args.k, args.m, args.width
     V = args.views_per_gpu

@@ -161,6 +161,19 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
  * renders: call vp_sync before reading them. vp_read_stats afterwards reports the last view. */
 int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,
                           float *const *rgb, float *const *alpha, int32_t *const *samples, void *stream);
+/* One shard of a view split over n_shards renders (tile sharding across GPUs, SURVEY.md §8e;
+ * the reference renders a view in one call, march.cpp:95-132, and parallelises over rows,
+ * threads.h:16-36). The shard owns the 16x16 tiles t (row-major tile index, tiles_x =
+ * ceil(W/16)) with t % n_shards == shard: it culls every primitive, but bins and marches only
+ * its tiles, heaviest first. Outputs are DEVICE pointers in a tile-major layout of
+ * vp_shard_tiles() slots of 256 pixels: pixel (x, y) of owned tile t is at slot t / n_shards,
+ * offset (y % 16) * 16 + x % 16 (rgb 3 floats, alpha 1 float, samples 1 int32 per pixel);
+ * pixels of partial edge tiles outside the image are not written. Every pixel value is
+ * bitwise the one vp_render_async produces. Enqueued on `stream` (NULL: the context's). */
+int vp_render_shard_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, int32_t shard,
+                          int32_t n_shards, float *rgb, float *alpha, int32_t *samples, void *stream);
+/* Number of tile slots of shard `shard` of n_shards for a width x height view. */
+int64_t vp_shard_tiles(int32_t width, int32_t height, int32_t shard, int32_t n_shards);
 /* Waits for every render and output copy the context has enqueued. */
 int vp_sync(vp_ctx *ctx);
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats);

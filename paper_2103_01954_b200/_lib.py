@@ -69,6 +69,9 @@ SIGNATURES = {
                                   f32p, i32p, C.c_void_p]),
     "vp_render_batch_async": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(vp_camera), C.POINTER(vp_march),
                                         C.POINTER(f32p), C.POINTER(f32p), C.POINTER(i32p), C.c_void_p]),
+    "vp_render_shard_async": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march), C.c_int32,
+                                        C.c_int32, f32p, f32p, i32p, C.c_void_p]),
+    "vp_shard_tiles": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "vp_sync": (C.c_int, [C.c_void_p]),
     "vp_read_stats": (C.c_int, [C.c_void_p, C.POINTER(vp_stats)]),
     "vp_march_rays": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, f32p, C.POINTER(vp_march),

@@ -327,6 +327,17 @@ class Renderer:
                                          C.cast(C.c_void_p(samples_ptr), i32p) if samples_ptr else None,
                                          C.c_void_p(stream) if stream else None), self._ctx)
 
+    def render_shard_device(self, cam: Camera, cfg: MarchConfig, shard: int, n_shards: int, rgb_ptr: int,
+                            alpha_ptr: int, samples_ptr: int = 0, stream: int = 0):
+        """Enqueue shard `shard` of `n_shards` of a view (vp_render_shard_async) into device
+        buffers in the tile-major layout (shard_tiles(...) slots of 256 pixels)."""
+        cc, mc = cam.to_c(), cfg.to_c()
+        _check(self._lib.vp_render_shard_async(self._ctx, C.byref(cc), C.byref(mc), int(shard), int(n_shards),
+                                               C.cast(C.c_void_p(rgb_ptr), f32p),
+                                               C.cast(C.c_void_p(alpha_ptr), f32p),
+                                               C.cast(C.c_void_p(samples_ptr), i32p) if samples_ptr else None,
+                                               C.c_void_p(stream) if stream else None), self._ctx)
+
     def read_stats(self) -> dict:
         st = vp_stats()
         _check(self._lib.vp_read_stats(self._ctx, C.byref(st)), self._ctx)
@@ -560,3 +571,10 @@ def render(scene: Scene, frame: int, cam: Camera, cfg: MarchConfig, device: int 
 def composite(out: RenderOutput, background: np.ndarray, device: int = 0) -> np.ndarray:
     """volprim::composite (march.h:62)."""
     return _renderer(device).composite(out, background)
+
+
+def shard_tiles(width: int, height: int, shard: int, n_shards: int) -> int:
+    """Tile slots of shard `shard` of `n_shards` (vp_shard_tiles): the tiles t with
+    t % n_shards == shard, t the row-major index of the ceil(W/16) x ceil(H/16) tile grid."""
+    from ._lib import load
+    return int(load().vp_shard_tiles(int(width), int(height), int(shard), int(n_shards)))

@@ -265,7 +265,9 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
 // raymarch that read it has finished. Then ONE raymarch launch covers the tiles of all the
 // views, heaviest first across views (a batch pays the tail of a launch once), and one
 // fallback launch their overflow rays.
-int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, const OutDev *ods, cudaStream_t st) {
+// n_ctas_single: a shard render's owned tile count (its order lists them first), else -1.
+int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, const OutDev *ods, cudaStream_t st,
+                  int n_ctas_single = -1) {
     if (n < 1 || n > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per launch");
     ctx->group ^= 1;
     BinSlot *grp = ctx->slot + ctx->group * kMaxViews;
@@ -301,6 +303,7 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     VP_CUDA(ctx, cudaStreamWaitEvent(st, grp[0].ev_binned, 0));
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
+    if (n == 1 && n_ctas_single >= 0) total = n_ctas_single;
     VP_CUDA(ctx, launch_march_tiles(mp, ctx->xfb[ctx->xfi].p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
@@ -744,6 +747,44 @@ int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, floa
         VP_CUDA(ctx, cudaMemcpyAsync(samples_dev, od.samples, 4 * n_px, cudaMemcpyDeviceToHost, ctx->copy_stream));
     VP_CUDA(ctx, cudaEventRecord(ctx->ev_copied[q], ctx->copy_stream));
     return VP_OK;
+}
+
+int64_t vp_shard_tiles(int32_t width, int32_t height, int32_t shard, int32_t n_shards) {
+    if (width <= 0 || height <= 0 || n_shards < 1 || shard < 0 || shard >= n_shards) return 0;
+    const int64_t n_tiles = int64_t((width + 15) / 16) * ((height + 15) / 16);
+    return n_tiles > shard ? (n_tiles - shard + n_shards - 1) / n_shards : 0;
+}
+
+int vp_render_shard_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, int32_t shard,
+                          int32_t n_shards, float *rgb, float *alpha, int32_t *samples, void *stream) {
+    if (int rc = check_ctx(ctx, true)) return rc;
+    if (int rc = check_cam(ctx, cam)) return rc;
+    if (int rc = check_march(ctx, cfg)) return rc;
+    if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(ctx, VP_ERR_USAGE, "bad shard index");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    const int64_t slots = vp_shard_tiles(cam->width, cam->height, shard, n_shards);
+    if (slots == 0) return VP_OK;
+    if (!rgb || !alpha) return fail(ctx, VP_ERR_USAGE, "null output");
+    if (!is_device_ptr(rgb) || !is_device_ptr(alpha) || (samples && !is_device_ptr(samples)))
+        return fail(ctx, VP_ERR_USAGE, "shard outputs must be device pointers");
+    const size_t n_px = size_t(slots) * 256;
+    if (ctx->n_prim == 0) {
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), st));
+        ctx->last_n = 1;
+        VP_CUDA(ctx, cudaMemsetAsync(rgb, 0, n_px * 3 * sizeof(float), st));
+        VP_CUDA(ctx, cudaMemsetAsync(alpha, 0, n_px * sizeof(float), st));
+        if (samples) VP_CUDA(ctx, cudaMemsetAsync(samples, 0, n_px * sizeof(int32_t), st));
+        return VP_OK;
+    }
+    CamDev cd = make_cam(*cam);
+    cd.n_shards = n_shards;
+    cd.shard = shard;
+    if (int rc = ensure_render_buffers(ctx, cd)) return rc;
+    OutDev od{rgb, alpha, samples};
+    od.shard_n = n_shards;
+    od.width = cd.width;
+    od.tiles_x = cd.tiles_x;
+    return enqueue_views(ctx, 1, &cd, make_march(ctx, cfg), &od, st, int(slots));
 }
 
 int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,

@@ -14,6 +14,15 @@ struct CamDev {
     float t[3];
     float center[3];
     int32_t width, height, tiles_x, tiles_y;
+    // Tile sharding of one view over n_shards renders (vp_render_shard_async): this render
+    // owns the tiles t (row-major tile index) with t % n_shards == shard. 1/0 = every tile.
+    int32_t n_shards, shard;
 };
+
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__ bool tile_owned(const CamDev &c, int t) {
+    return c.n_shards <= 1 || t % c.n_shards == c.shard;
+}
+#endif
 
 }  // namespace vpb

@@ -119,17 +119,23 @@ __global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
     prects[k] = prc;
     keys[k] = key;
     for (int ty = rc.y; ty <= rc.w; ++ty)
-        for (int tx = rc.x; tx <= rc.z; ++tx) atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1u);
+        for (int tx = rc.x; tx <= rc.z; ++tx)
+            if (tile_owned(cam, ty * cam.tiles_x + tx)) atomicAdd(&tile_counts[ty * cam.tiles_x + tx], 1u);
 }
 
 // K2: single-CTA exclusive scan over the tile counts (tiles <= a few 10^4). Writes the
 // bucket starts twice (offsets, and the emit cursors) and flags key-capacity overflow.
 // It also writes `order`: the tiles by descending candidate count (a proxy for their march
-// cost), so the raymarch hands the heaviest tiles out first and the tail stays short.
+// cost), so the raymarch hands the heaviest tiles out first and the tail stays short. In a
+// shard render the tiles the shard does not own go last (bucket 0), after its empty tiles.
 constexpr int kOrderBuckets = 1024;
 __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
                        uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
-                       uint32_t *__restrict__ order, DevCounters *ctr, int64_t capacity) {
+                       uint32_t *__restrict__ order, DevCounters *ctr, int64_t capacity, int n_shards,
+                       int shard) {
+    const auto bucket = [&](int t) {
+        return n_shards > 1 && t % n_shards != shard ? 0u : min(counts[t], (uint32_t)kOrderBuckets - 2) + 1u;
+    };
     __shared__ unsigned long long warp_sums[32];
     __shared__ unsigned long long carry;
     __shared__ unsigned hist[kOrderBuckets];
@@ -172,12 +178,12 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
         ctr->keys = carry;
         ctr->key_overflow = (int64_t)carry > capacity ? 1 : 0;
     }
-    // counting sort of the tiles by min(count, 1023), descending
+    // counting sort of the tiles by bucket(t) (1 + min(count, 1022), 0 if not owned), descending
     for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     unsigned nonempty = 0;
     for (int t = tid; t < n_tiles; t += blockDim.x) {
-        atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u);
+        atomicAdd(&hist[bucket(t)], 1u);
         nonempty += counts[t] > 0;
     }
     for (int o = 16; o > 0; o >>= 1) nonempty += __shfl_down_sync(0xffffffffu, nonempty, o);
@@ -202,7 +208,7 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
     }
     __syncthreads();
     for (int t = tid; t < n_tiles; t += blockDim.x)
-        order[atomicAdd(&hist[min(counts[t], (uint32_t)kOrderBuckets - 1)], 1u)] = (uint32_t)t;
+        order[atomicAdd(&hist[bucket(t)], 1u)] = (uint32_t)t;
 }
 
 // K3a: scatter keys into buckets, one warp per primitive: the lanes claim the slots of the
@@ -210,7 +216,8 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
 // Order inside a bucket is arbitrary here; K3b makes it canonical.
 __global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
                        int n_prim, int tiles_x, uint32_t *__restrict__ cursor,
-                       unsigned long long *__restrict__ entries, const DevCounters *ctr) {
+                       unsigned long long *__restrict__ entries, const DevCounters *ctr, int n_shards,
+                       int shard) {
     const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (k >= n_prim || ctr->key_overflow) return;
@@ -219,8 +226,8 @@ __global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restric
     if (w <= 0 || h <= 0) return;
     const unsigned long long e = ((unsigned long long)keys[k] << 32) | (uint32_t)k;
     for (int q = lane; q < w * h; q += 32) {
-        const int ty = rc.y + q / w, tx = rc.x + q % w;
-        entries[atomicAdd(&cursor[ty * tiles_x + tx], 1u)] = e;
+        const int t = (rc.y + q / w) * tiles_x + rc.x + q % w;
+        if (n_shards <= 1 || t % n_shards == shard) entries[atomicAdd(&cursor[t], 1u)] = e;
     }
 }
 
@@ -714,8 +721,11 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
     const int n_tiles = cam.tiles_x * cam.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
     if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
-    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity);
-    if (n_prim > 0) k_emit<<<(unsigned)((n_prim * 32ll + 255) / 256), 256, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor, entries, ctr);
+    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity, cam.n_shards,
+                               cam.shard);
+    if (n_prim > 0)
+        k_emit<<<(unsigned)((n_prim * 32ll + 255) / 256), 256, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor,
+                                                                         entries, ctr, cam.n_shards, cam.shard);
     k_tile_sort_warp<<<(n_tiles + 7) / 8, 256, 0, st>>>(offsets, entries, n_tiles, cursor, ctr);
     k_tile_sort_big<<<148, 128, 0, st>>>(offsets, entries, cursor, ctr);
     return cudaGetLastError();

@@ -52,6 +52,9 @@ struct OutDev {
     int *samples;
     unsigned long long *prof = nullptr;  // per CTA: tile, SM id, start ns, end ns (debug)
     float *state = nullptr;  // arbitrary rays: 8 floats per ray of MarchResult bookkeeping
+    // Tile-major shard outputs (vp_render_shard_async): pixel (x, y) of owned tile t is
+    // written at (t / shard_n) * 256 + (y % 16) * 16 + x % 16. 0 = the image layout.
+    int shard_n = 0, width = 0, tiles_x = 0;
 };
 
 // One camera view of a raymarch launch: its camera, outputs and binning artefacts (K1-K3 of

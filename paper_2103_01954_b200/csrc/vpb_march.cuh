@@ -699,6 +699,11 @@ __device__ __forceinline__ RayOut march_ray(const Cands &cands, const Win &w, V3
 }
 
 __device__ __forceinline__ void write_pixel(const OutDev &od, int64_t p, const RayOut &ro) {
+    if (od.shard_n) {  // image pixel index -> slot in the shard's tile-major buffer
+        const int px = (int)(p % od.width), py = (int)(p / od.width);
+        const int t = (py >> 4) * od.tiles_x + (px >> 4);
+        p = (int64_t)(t / od.shard_n) * 256 + (py & 15) * 16 + (px & 15);
+    }
     od.rgb[3 * p + 0] = ro.r;
     od.rgb[3 * p + 1] = ro.g;
     od.rgb[3 * p + 2] = ro.b;

@@ -1,7 +1,9 @@
 """Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL over NVLink/NVSwitch).
 
 The raymarcher shards by view: rays are independent and the scene is
-read-only, so each rank renders its own views with no data-path collective. The only
+read-only, so each rank renders its own views with no data-path collective. A single view
+shards by tile (`TileShardGather`): rank r renders the tiles t % world == r
+(vp_render_shard_async, tile-major outputs) and rank 0 gathers and places them. The only
 communication is
   * a one-time broadcast of the repacked, channel-interleaved payload (K*M^3*16 bytes) and the
     composed transforms from rank 0 (`broadcast_scene`), and
@@ -120,3 +122,72 @@ class ViewGather:
         hw = width * height
         return (row[:3 * hw].reshape(height, width, 3), row[3 * hw:4 * hw].reshape(height, width, 1),
                 row[4 * hw:].view(torch.int32))
+
+
+def assemble_tile_shards(parts, width: int, height: int, channels: int):
+    """The [H, W, channels] image from the tile-major shard outputs parts[r] ([slots_r (or
+    more), 256, channels], numpy or torch): slot s of shard r is tile t = s * n + r (row-major
+    over the ceil(W/16) x ceil(H/16) grid), pixel (y % 16) * 16 + x % 16 of it."""
+    n = len(parts)
+    tx, ty = (width + 15) // 16, (height + 15) // 16
+    n_tiles = tx * ty
+    p0 = parts[0]
+    if hasattr(p0, "new_empty"):  # torch
+        tiles = p0.new_zeros((n_tiles, 256, channels))
+    else:
+        tiles = np.zeros((n_tiles, 256, channels), p0.dtype)
+    for r, part in enumerate(parts):
+        k = len(range(r, n_tiles, n))
+        tiles[r::n] = part.reshape(-1, 256, channels)[:k]
+    img = tiles.reshape(ty, tx, 16, 16, channels)
+    img = img.permute(0, 2, 1, 3, 4) if hasattr(img, "permute") else img.transpose(0, 2, 1, 3, 4)
+    return img.reshape(ty * 16, tx * 16, channels)[:height, :width]
+
+
+class TileShardGather:
+    """Single-view tile sharding: this rank's tile-major outputs (rgb, alpha, samples as int32
+    bits in one float32 buffer of slots_max * 256 * 5 values, slots_max = the largest shard's
+    tile count, so every rank sends the same size) and their gather to rank `dst`, which
+    places the tiles into the [H, W] image (assemble)."""
+
+    def __init__(self, width: int, height: int, device, world: int, rank: int, dst: int = 0):
+        import torch
+        from .api import shard_tiles
+        self.width, self.height, self.world, self.rank, self.dst = width, height, world, rank, dst
+        self.slots = [shard_tiles(width, height, r, world) for r in range(world)]
+        self.slots_max = max(max(self.slots), 1)
+        n = self.slots_max * 256
+        self.n = n
+        self.buf = torch.zeros(5 * n, dtype=torch.float32, device=device)
+        self.recv = ([torch.empty(5 * n, dtype=torch.float32, device=device) for _ in range(world)]
+                     if rank == dst else None)
+        self.work = None
+
+    def outputs(self):
+        """(rgb, alpha, samples) device views of this rank's shard buffer."""
+        import torch
+        n = self.n
+        return self.buf[:3 * n], self.buf[3 * n:4 * n], self.buf[4 * n:].view(torch.int32)
+
+    def gather(self, async_op: bool = True):
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        self.work = dist.gather(self.buf, self.recv if self.rank == self.dst else None, dst=self.dst,
+                                async_op=async_op)
+
+    def wait(self):
+        if self.work is not None:
+            self.work.wait()
+            self.work = None
+
+    def assemble(self):
+        """On rank dst: (rgb [H,W,3], alpha [H,W,1], samples [H,W] int32) of the whole view."""
+        import torch
+        rows = self.recv if self.world > 1 else [self.buf]
+        n = self.n
+        rgb = assemble_tile_shards([r[:3 * n].view(-1, 256, 3) for r in rows], self.width, self.height, 3)
+        alpha = assemble_tile_shards([r[3 * n:4 * n].view(-1, 256, 1) for r in rows], self.width, self.height, 1)
+        samp = assemble_tile_shards([r[4 * n:].view(torch.int32).view(-1, 256, 1) for r in rows],
+                                    self.width, self.height, 1)
+        return rgb, alpha, samp[..., 0]

@@ -115,3 +115,68 @@ def test_broadcast_and_gather_world2():
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
     assert res == [(0, True, True), (1, True, True)]
+
+
+def _split_tile_shard(img, shard, n):
+    """Inverse of assemble_tile_shards for one shard: [slots, 256, C] (zeros outside the image)."""
+    h, w, c = img.shape
+    tx, ty = (w + 15) // 16, (h + 15) // 16
+    pad = np.zeros((ty * 16, tx * 16, c), img.dtype)
+    pad[:h, :w] = img
+    tiles = pad.reshape(ty, 16, tx, 16, c).transpose(0, 2, 1, 3, 4).reshape(tx * ty, 256, c)
+    return tiles[shard::n]
+
+
+@pytest.mark.parametrize("w,h,n", [(64, 64, 1), (64, 48, 2), (100, 37, 3), (1024, 1024, 8), (17, 16, 5)])
+def test_assemble_tile_shards_inverts_the_shard_layout(w, h, n):
+    from paper_2103_01954_b200.api import shard_tiles
+    from paper_2103_01954_b200.dist import assemble_tile_shards
+    img = np.random.default_rng(w * h + n).standard_normal((h, w, 3)).astype(np.float32)
+    parts = [_split_tile_shard(img, r, n) for r in range(n)]
+    assert [len(p) for p in parts] == [shard_tiles(w, h, r, n) for r in range(n)]
+    assert sum(len(p) for p in parts) == ((w + 15) // 16) * ((h + 15) // 16)
+    assert np.array_equal(assemble_tile_shards(parts, w, h, 3), img)
+    tparts = [torch.from_numpy(p.copy()) for p in parts]
+    assert np.array_equal(assemble_tile_shards(tparts, w, h, 3).numpy(), img)
+    assert shard_tiles(w, h, n, n) == 0 and shard_tiles(w, h, -1, n) == 0 and shard_tiles(0, h, 0, n) == 0
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_01954_b200.dist import TileShardGather
+        w, h = 70, 45
+        rng = np.random.default_rng(3)
+        rgb = rng.standard_normal((h, w, 3)).astype(np.float32)
+        alpha = rng.uniform(0, 1, (h, w, 1)).astype(np.float32)
+        samp = rng.integers(0, 500, (h, w, 1)).astype(np.int32)
+        g = TileShardGather(w, h, "cpu", world, rank)
+        o_rgb, o_alpha, o_samp = g.outputs()
+        for out, img, c in ((o_rgb, rgb, 3), (o_alpha, alpha, 1), (o_samp, samp, 1)):
+            part = _split_tile_shard(img, rank, world)
+            out[:part.size] = torch.from_numpy(np.ascontiguousarray(part).reshape(-1))
+        g.gather()
+        g.wait()
+        ok = True
+        if rank == 0:
+            a_rgb, a_alpha, a_samp = g.assemble()
+            ok = (np.array_equal(a_rgb.numpy(), rgb) and np.array_equal(a_alpha.numpy(), alpha)
+                  and np.array_equal(a_samp.numpy(), samp[..., 0]))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tile_shard_gather_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert res == [(0, True), (1, True)]
