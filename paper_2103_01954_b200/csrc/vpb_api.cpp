@@ -279,18 +279,22 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     const uint32_t *counts[kMaxViews];
     int n_tiles[kMaxViews];
     int total = 0;
+    BinBatch bb{};  // K1-K3 of every view: one launch per stage (vpb_kernels.cu k_bin_zero ...)
+    bb.n = n;
+    bb.xf16 = ctx->xfb[ctx->xfi].p;
+    bb.n_prim = ctx->n_prim;
+    bb.capacity = ctx->entries_cap;
     for (int v = 0; v < n; ++v) {
         BinSlot &b = grp[v];
         VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
-        VP_CUDA(ctx, cudaMemsetAsync(b.d_ctr, 0, sizeof(DevCounters), ctx->bin_stream));
-        VP_CUDA(ctx, launch_binning(cams[v], ctx->xfb[ctx->xfi].p, ctx->n_prim, b.rects.p, b.prects.p, b.keys.p,
-                                    b.tile_counts.p, b.offsets.p, b.cursor.p, b.order.p, b.entries.p,
-                                    ctx->entries_cap, b.d_ctr, ctx->bin_stream));
+        bb.v[v] = BinView{cams[v], b.rects.p, b.prects.p, b.keys.p, b.tile_counts.p, b.offsets.p, b.cursor.p,
+                          b.order.p, b.entries.p, b.d_ctr};
         vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap};
         counts[v] = b.tile_counts.p;
         n_tiles[v] = cams[v].tiles_x * cams[v].tiles_y;
         total += n_tiles[v];
     }
+    VP_CUDA(ctx, launch_binning_batch(bb, ctx->bin_stream));
     const uint32_t *order = grp[0].order.p;
     if (n > 1) {
         VP_CUDA(ctx, ctx->batch_order[ctx->group].ensure(size_t(std::max(total, 1))));
@@ -557,8 +561,11 @@ int vp_set_transforms_async(vp_ctx *ctx, int32_t n_prim, const float *xf15, void
     if (n_prim == 0) return VP_OK;
     if (!xf15) return fail(ctx, VP_ERR_USAGE, "null transforms");
     if (!ctx->has_xf) return fail(ctx, VP_ERR_USAGE, "set the frame's transforms synchronously first");
-    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
-    // upload into the other buffer, once the binning and raymarch that last read it are done
+    // Upload into the other buffer, once the binning and raymarch that last read it are done.
+    // Without a caller stream the upload goes on the binning stream: enqueued on the render
+    // stream it would wait for the raymarch in flight, and the next views' binning (which
+    // waits for the upload) could not overlap that raymarch.
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->bin_stream;
     const int j = ctx->xfi ^ 1;
     VP_CUDA(ctx, ctx->xfb[j].ensure(size_t(n_prim) * 16));
     VP_CUDA(ctx, ctx->xf15_tmp.ensure(size_t(n_prim) * 15));

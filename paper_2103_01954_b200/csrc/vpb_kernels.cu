@@ -104,7 +104,7 @@ __device__ __forceinline__ void cull_rect(const float *xf, const CamDev &cam, in
     rect = make_int4(prect.x / kTile, prect.y / kTile, prect.z / kTile, prect.w / kTile);
 }
 
-__global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
+__device__ __forceinline__ void cull_body(const float *__restrict__ xf16, int n_prim, const CamDev &cam,
                        int4 *__restrict__ rects, int4 *__restrict__ prects,
                        uint32_t *__restrict__ keys, uint32_t *__restrict__ tile_counts) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,7 +129,7 @@ __global__ void k_cull(const float *__restrict__ xf16, int n_prim, CamDev cam,
 // cost), so the raymarch hands the heaviest tiles out first and the tail stays short. In a
 // shard render the tiles the shard does not own go last (bucket 0), after its empty tiles.
 constexpr int kOrderBuckets = 1024;
-__global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
+__device__ __forceinline__ void scan_body(const uint32_t *__restrict__ counts, int n_tiles,
                        uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
                        uint32_t *__restrict__ order, DevCounters *ctr, int64_t capacity, int n_shards,
                        int shard) {
@@ -214,7 +214,7 @@ __global__ void k_scan(const uint32_t *__restrict__ counts, int n_tiles,
 // K3a: scatter keys into buckets, one warp per primitive: the lanes claim the slots of the
 // primitive's tiles in parallel (a thread per primitive would chain its atomics' round trips).
 // Order inside a bucket is arbitrary here; K3b makes it canonical.
-__global__ void k_emit(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
+__device__ __forceinline__ void emit_body(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
                        int n_prim, int tiles_x, uint32_t *__restrict__ cursor,
                        unsigned long long *__restrict__ entries, const DevCounters *ctr, int n_shards,
                        int shard) {
@@ -278,8 +278,7 @@ __device__ __forceinline__ void warp_sort_bucket(unsigned long long *a, int n, i
         if (lane + 32 * r < n) a[lane + 32 * r] = v[r];
 }
 
-__global__ void __launch_bounds__(256)
-k_tile_sort_warp(const uint32_t *__restrict__ offsets, unsigned long long *__restrict__ entries,
+__device__ __forceinline__ void tile_sort_warp_body(const uint32_t *__restrict__ offsets, unsigned long long *__restrict__ entries,
                  int n_tiles, uint32_t *__restrict__ big, DevCounters *ctr) {
     if (ctr->key_overflow) return;
     const int tile = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -295,7 +294,7 @@ k_tile_sort_warp(const uint32_t *__restrict__ offsets, unsigned long long *__res
 // Buckets past 256 keys: all-ascending bitonic network (the "flip" formulation), so padding
 // with +inf past n needs no special case; persistent CTAs over the list.
 constexpr int kSortSmem = 2048;
-__global__ void k_tile_sort_big(const uint32_t *__restrict__ offsets,
+__device__ __forceinline__ void tile_sort_big_body(const uint32_t *__restrict__ offsets,
                                 unsigned long long *__restrict__ entries, const uint32_t *__restrict__ big,
                                 const DevCounters *ctr) {
     __shared__ unsigned long long s[kSortSmem];
@@ -332,6 +331,41 @@ __global__ void k_tile_sort_big(const uint32_t *__restrict__ offsets,
             for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = s[i];
         __syncthreads();
     }
+}
+
+// Binning of a batch of views in one launch per stage: blockIdx.y is the view (BinBatch), so a
+// batch of 8 views costs 6 launches instead of 48 and the views' single-CTA scans run side by
+// side (one launch of each small kernel is latency, not work).
+__global__ void k_bin_zero(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    const int n_tiles = v.cam.tiles_x * v.cam.tiles_y;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x)
+        v.tile_counts[t] = 0u;
+    if (blockIdx.x == 0) {
+        unsigned *c = reinterpret_cast<unsigned *>(v.ctr);
+        for (int i = threadIdx.x; i < (int)(sizeof(DevCounters) / 4); i += blockDim.x) c[i] = 0u;
+    }
+}
+__global__ void k_cull(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    cull_body(bb.xf16, bb.n_prim, v.cam, v.rects, v.prects, v.keys, v.tile_counts);
+}
+__global__ void k_scan(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    scan_body(v.tile_counts, v.cam.tiles_x * v.cam.tiles_y, v.offsets, v.cursor, v.order, v.ctr, bb.capacity,
+              v.cam.n_shards, v.cam.shard);
+}
+__global__ void k_emit(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    emit_body(v.rects, v.keys, bb.n_prim, v.cam.tiles_x, v.cursor, v.entries, v.ctr, v.cam.n_shards, v.cam.shard);
+}
+__global__ void __launch_bounds__(256) k_tile_sort_warp(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    tile_sort_warp_body(v.offsets, v.entries, v.cam.tiles_x * v.cam.tiles_y, v.cursor, v.ctr);
+}
+__global__ void k_tile_sort_big(const __grid_constant__ BinBatch bb) {
+    const BinView &v = bb.v[blockIdx.y];
+    tile_sort_big_body(v.offsets, v.entries, v.cursor, v.ctr);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -714,21 +748,30 @@ cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream
     return cudaGetLastError();
 }
 
+cudaError_t launch_binning_batch(const BinBatch &bb, cudaStream_t st) {
+    int max_tiles = 0;
+    for (int v = 0; v < bb.n; ++v) max_tiles = max(max_tiles, bb.v[v].cam.tiles_x * bb.v[v].cam.tiles_y);
+    const unsigned nv = (unsigned)bb.n;
+    k_bin_zero<<<dim3((unsigned)((max_tiles + 1023) / 1024), nv), 1024, 0, st>>>(bb);
+    if (bb.n_prim > 0) k_cull<<<dim3((unsigned)((bb.n_prim + 127) / 128), nv), 128, 0, st>>>(bb);
+    k_scan<<<dim3(1, nv), 1024, 0, st>>>(bb);
+    if (bb.n_prim > 0) k_emit<<<dim3((unsigned)((bb.n_prim * 32ll + 255) / 256), nv), 256, 0, st>>>(bb);
+    k_tile_sort_warp<<<dim3((unsigned)((max_tiles + 7) / 8), nv), 256, 0, st>>>(bb);
+    k_tile_sort_big<<<dim3((unsigned)(148 / bb.n > 16 ? 148 / bb.n : 16), nv), 128, 0, st>>>(bb);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
                            int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
                            uint32_t *cursor, uint32_t *order, unsigned long long *entries,
                            int64_t capacity, DevCounters *ctr, cudaStream_t st) {
-    const int n_tiles = cam.tiles_x * cam.tiles_y;
-    cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
-    if (n_prim > 0) k_cull<<<(n_prim + 127) / 128, 128, 0, st>>>(xf16, n_prim, cam, rects, prects, keys, tile_counts);
-    k_scan<<<1, 1024, 0, st>>>(tile_counts, n_tiles, offsets, cursor, order, ctr, capacity, cam.n_shards,
-                               cam.shard);
-    if (n_prim > 0)
-        k_emit<<<(unsigned)((n_prim * 32ll + 255) / 256), 256, 0, st>>>(rects, keys, n_prim, cam.tiles_x, cursor,
-                                                                         entries, ctr, cam.n_shards, cam.shard);
-    k_tile_sort_warp<<<(n_tiles + 7) / 8, 256, 0, st>>>(offsets, entries, n_tiles, cursor, ctr);
-    k_tile_sort_big<<<148, 128, 0, st>>>(offsets, entries, cursor, ctr);
-    return cudaGetLastError();
+    BinBatch bb{};
+    bb.n = 1;
+    bb.xf16 = xf16;
+    bb.n_prim = n_prim;
+    bb.capacity = capacity;
+    bb.v[0] = BinView{cam, rects, prects, keys, tile_counts, offsets, cursor, order, entries, ctr};
+    return launch_binning_batch(bb, st);
 }
 
 template <class Cfg, int MT, bool PROF>

@@ -76,6 +76,22 @@ struct ViewBatch {
     int n;
 };
 
+// Binning (K1-K3) of up to kMaxViews views in one launch per stage (blockIdx.y = view).
+struct BinView {
+    CamDev cam;
+    int4 *rects, *prects;
+    uint32_t *keys, *tile_counts, *offsets, *cursor, *order;
+    unsigned long long *entries;
+    DevCounters *ctr;  // zeroed by the batch's first kernel
+};
+struct BinBatch {
+    BinView v[kMaxViews];
+    int n;
+    const float *xf16;
+    int n_prim;
+    int64_t capacity;
+};
+
 struct RaysDev {
     const float *origins;
     const float *dirs;
@@ -118,6 +134,8 @@ namespace vpb {
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
                           cudaStream_t st);
 cudaError_t launch_pad_xf(const float *xf15, float *xf16, int n_prim, cudaStream_t st);
+cudaError_t launch_binning_batch(const BinBatch &bb, cudaStream_t st);
+// one view; also zeroes its counters
 cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int4 *rects,
                            int4 *prects, uint32_t *keys, uint32_t *tile_counts, uint32_t *offsets,
                            uint32_t *cursor, uint32_t *order, unsigned long long *entries,

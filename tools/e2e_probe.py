@@ -32,3 +32,37 @@ run("batch host", lambda: lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(
 run("xf sync + batch host", lambda: (lib.vp_set_transforms(r.ctx, k, C.cast(xh.data_ptr(), f32p)), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), hr, ha, hs, None)))
 run("xf async + batch device", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), dr, da, ds, None)))
 run("xf async + batch host", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), hr, ha, hs, None)))
+
+
+def kt(name, fn, n=30):
+    fn(); lib.vp_sync(r.ctx); torch.cuda.synchronize(); r.kernel_times()
+    t0 = time.perf_counter()
+    for _ in range(n): fn()
+    lib.vp_sync(r.ctx); torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / n
+    ks = r.kernel_times(4096)
+    print(f"{name:40s} {dt*1e3:8.2f} ms/step wall, march kernel mean {ks.mean():.3f} ms (n={len(ks)})", flush=True)
+
+
+kt("xf async + batch device (30)", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), dr, da, ds, None)))
+kt("xf async + batch host (30)", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), hr, ha, hs, None)))
+kt("xf async + batch device (30)", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), dr, da, ds, None)))
+kt("xf async + batch host (30)", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), hr, ha, hs, None)))
+
+
+def enq(name, fn, n=30):
+    fn(); lib.vp_sync(r.ctx); torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ts = []
+    for _ in range(n):
+        a = time.perf_counter(); fn(); ts.append(time.perf_counter() - a)
+    t1 = time.perf_counter()
+    lib.vp_sync(r.ctx); torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    ts = np.array(ts) * 1e3
+    print(f"{name:30s} enqueue {1e3*(t1-t0)/n:6.2f} ms/step (call max {ts.max():.2f}, median {np.median(ts):.3f}), "
+          f"total {1e3*(t2-t0)/n:6.2f} ms/step", flush=True)
+
+
+enq("host outputs", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), hr, ha, hs, None)))
+enq("device outputs", lambda: (lib.vp_set_transforms_async(r.ctx, k, C.cast(xh.data_ptr(), f32p), None), lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), dr, da, ds, None)))
