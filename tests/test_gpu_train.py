@@ -67,6 +67,42 @@ def test_adam_step_matches_reference(renderer):
     assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))  # nothing updated
 
 
+@pytest.mark.parametrize("m", [3, 4, 5, 8])
+def test_adam_payload_update_both_access_widths(renderer, m):
+    """The payload part of adamStep (losses.cpp:81-96) against a float32 numpy restatement (each
+    operation rounded to binary32, no contraction), three steps, for even M (16-byte kernel,
+    k_adam_update4) and odd M (scalar kernel)."""
+    k = 7
+    rng = np.random.default_rng(m)
+    tr, _ = synthetic.shell_arrays(k, 2)
+    tr = np.ascontiguousarray(tr, np.float32)
+    pay = rng.uniform(0.0, 1.0, k * 4 * m ** 3).astype(np.float32)
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, pay), api.WindowParams())
+    renderer._lib.vp_adam_reset(renderer.ctx)
+    cfg = api.AdamConfig(lr=3e-2, beta1=0.9, beta2=0.999, eps=1e-8, lr_delta_scale=0.0)
+    f = np.float32
+    n_pay = pay.size
+    m1 = np.zeros(n_pay, f)
+    m2 = np.zeros(n_pay, f)
+    want = pay.copy()
+    b1, b2, lr, eps = f(cfg.beta1), f(cfg.beta2), f(cfg.lr), f(cfg.eps)
+    for step in range(1, 4):
+        g = rng.standard_normal(api.grad_size(k, m)).astype(np.float32)
+        api.adam_step(renderer, cfg, g, tr)
+        gp = g[:n_pay]
+        m1 = b1 * m1 + (f(1) - b1) * gp
+        m2 = b2 * m2 + (f(1) - b2) * gp * gp
+        bc1 = f(1) - f(np.power(b1, f(step), dtype=np.float32))
+        bc2 = f(1) - f(np.power(b2, f(step), dtype=np.float32))
+        want = want - (lr * (m1 / bc1)) / (np.sqrt(m2 / bc2) + eps)
+        want = np.where(want < 0, f(0), want).astype(np.float32)
+    got = api.payload_planar(renderer)
+    # bc = 1 - pow(beta, step) comes from the host's std::pow; numpy's may differ by an ulp, so
+    # allow 2 ulp of the update instead of demanding bits here (the reference fixture above is
+    # the bit-exact check)
+    assert np.allclose(got, want, rtol=5e-7, atol=1e-7), np.abs(got - want).max()
+
+
 def _write_vpsl(path, k, m, payload, version=1, magic=b"VPSL", truncate=0):
     """README.md:96-104: magic, u32 version, u32 K, u32 M, f32 payload (little-endian)."""
     data = magic + np.array([version, k, m], "<u4").tobytes() + np.asarray(payload, "<f4").tobytes()
