@@ -69,6 +69,10 @@ class Oracle:
         L.vpo_render.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, f32p,
                                  f32p, f32p, C.c_int32, C.c_int32, C.c_float, C.c_float,
                                  C.c_int32, C.c_uint64, C.c_uint64, f32p, f32p, i32p, C.c_int32]
+        L.vpo_render_counted.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, f32p,
+                                         f32p, f32p, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                         C.c_int32, C.c_uint64, C.c_uint64, f32p, f32p, i32p, i32p,
+                                         C.c_int32]
         L.vpo_composite.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]
         L.vpo_cull.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, i32p, u32p]
         L.vpo_cull_px.argtypes = [C.c_int32, f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, i32p, i32p,
@@ -117,6 +121,24 @@ class Oracle:
                                  _p(samples, i32p), int(nt))
         assert rc == 0
         return rgb, alpha, samples
+
+    def render_counted(self, xf15, m, payload, window, cam, cfg, n_threads=None):
+        """render() plus the per-pixel prim-sample counts (int32, H*W)."""
+        xf = _f(xf15).reshape(-1, 15)
+        k9, r9, t3 = cam_arrays(cam)
+        w, h = int(cam.width), int(cam.height)
+        rgb = np.zeros((h, w, 3), np.float32)
+        alpha = np.zeros((h, w, 1), np.float32)
+        samples = np.zeros(h * w, np.int32)
+        prim = np.zeros(h * w, np.int32)
+        nt = n_threads if n_threads else (os.cpu_count() or 1)
+        rc = self.lib.vpo_render_counted(xf.shape[0], int(m), _p(xf), _p(_f(payload)), float(window.alpha),
+                                         int(window.beta), _p(k9), _p(r9), _p(t3), w, h,
+                                         float(cfg.step_size), float(cfg.early_eps), int(bool(cfg.jitter)),
+                                         int(cfg.seed), int(cfg.accumulation_permutation), _p(rgb), _p(alpha),
+                                         _p(samples, i32p), _p(prim, i32p), int(nt))
+        assert rc == 0
+        return rgb, alpha, samples, prim
 
     def march_rays(self, xf15, m, payload, window, origins, dirs, cfg, jitter=None):
         xf = _f(xf15).reshape(-1, 15)
@@ -261,6 +283,9 @@ class RefCore:
                                          C.c_float, f32p, f32p]
         L.vpref_intersect.argtypes = [C.c_int32, f32p, f32p, f32p, C.c_int32, i32p, i32p, f32p,
                                       f32p, f32p, f32p]
+        L.vpref_render_prim_counts.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32, f32p,
+                                               f32p, f32p, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                               C.c_int32, C.c_uint64, i32p]
         L.vpref_march_rays.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32,
                                        C.c_int64, f32p, f32p, f32p, C.c_float, C.c_float,
                                        C.c_uint64, f32p, f32p, i32p]
@@ -325,6 +350,20 @@ class RefCore:
         self.lib.vpref_intersect(k, _p(xf), _p(_f(origin, 3)), _p(_f(direction, 3)), k, C.byref(n),
                                  _p(prims, i32p), _p(te), _p(tx), C.byref(tmin), C.byref(tmax))
         return prims[:n.value], te[:n.value], tx[:n.value]
+
+    def render_prim_counts(self, tr24, m, payload, window, cam, cfg):
+        """Per-pixel prim-sample counts of the reference's render() (vpref_render_prim_counts)."""
+        tr = _f(tr24).reshape(-1, 24)
+        k9, r9, t3 = cam_arrays(cam)
+        w, h = int(cam.width), int(cam.height)
+        prim = np.zeros(h * w, np.int32)
+        rc = self.lib.vpref_render_prim_counts(tr.shape[0], int(m), _p(tr), _p(_f(payload)), float(window.alpha),
+                                               int(window.beta), _p(k9), _p(r9), _p(t3), w, h,
+                                               float(cfg.step_size), float(cfg.early_eps), int(bool(cfg.jitter)),
+                                               int(cfg.seed), _p(prim, i32p))
+        if rc != 0:
+            raise RuntimeError(self.error())
+        return prim
 
     def march_rays(self, xf15, m, payload, window, origins, dirs, cfg, jitter=None):
         xf = _f(xf15).reshape(-1, 15)

@@ -23,6 +23,7 @@
 //   Camera             = K[9] (column-major), R[9] (column-major), t[3], width, height
 // Return codes: 0 ok, volprim::ErrorCategory value on volprim::Error, 1 on other exceptions.
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -186,6 +187,65 @@ int vpref_intersect(int32_t nPrim, const float *xf15, const float *origin, const
         }
         *tMin = segs.tMin;
         *tMax = segs.tMax;
+    });
+}
+
+// Per-pixel prim-sample counts of render(): the reference's own generateRay,
+// intersect and march per pixel (march.cpp:112-126); march() reports where it stopped
+// (MarchResult::lastStep), and the step loop of march.cpp:34-49 is replayed on the reference's
+// segment list up to that step, adding the size of the active set at every visited step
+// (the executions of march.cpp:63-70). Single-threaded; composes the frame like render().
+int vpref_render_prim_counts(int32_t nPrim, int32_t m, const float *tr24, const float *payload, float wAlpha,
+                             int32_t wBeta, const float *k9, const float *r9, const float *t3, int32_t width,
+                             int32_t height, float stepSize, float earlyEps, int32_t jitter, uint64_t seed,
+                             int32_t *prim) {
+    return guarded([&] {
+        Frame fr;
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        const std::vector<AffineXf> xfs = fr.composed();
+        std::vector<Aabb> boxes;
+        for (const auto &xf : xfs) boxes.push_back(primitiveAabb(xf));
+        const Lbvh bvh = buildLbvh(boxes);
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        const WindowParams w{wAlpha, wBeta};
+        const Camera cam = cameraFrom(k9, r9, t3, width, height);
+        for (int y = 0; y < height; ++y)
+            for (int x = 0; x < width; ++x) {
+                const int pixelId = y * width + x;
+                const Ray ray = generateRay(cam, Vec2(real(x) + real(0.5), real(y) + real(0.5)));
+                const RaySegmentList segs = intersect(bvh, xfs, ray);
+                real jitter01 = real(0.5);
+                if (jitter) jitter01 = hashToUnit(hashCombine(seed, uint64_t(pixelId)));
+                const MarchResult mr = march(ray, segs, fr.slab, xfs, w, cfg, jitter01);
+                int64_t count = 0;
+                if (!segs.segments.empty() && mr.lastStep >= 0) {
+                    const real dt = cfg.stepSize, t0 = segs.tMin;
+                    const int nSegs = int(segs.segments.size());
+                    std::vector<int> active;
+                    int next = 0;
+                    for (int64_t i = 0; i <= mr.lastStep; ++i) {
+                        const real ts = t0 + (real(i) + jitter01) * dt;
+                        if (ts >= segs.tMax) break;
+                        while (next < nSegs && segs.segments[next].tEnter <= ts) active.push_back(next++);
+                        active.erase(std::remove_if(active.begin(), active.end(),
+                                                    [&](int q) { return segs.segments[q].tExit <= ts; }),
+                                     active.end());
+                        if (active.empty()) {
+                            if (next >= nSegs) break;
+                            const real tNext = segs.segments[next].tEnter;
+                            const int64_t skipTo = int64_t(std::ceil((tNext - t0) / dt - double(jitter01)));
+                            if (skipTo > i + 1) i = skipTo - 1;
+                            continue;
+                        }
+                        count += int64_t(active.size());
+                    }
+                }
+                prim[pixelId] = int32_t(count);
+            }
     });
 }
 

@@ -286,8 +286,12 @@ typedef struct {
 } march_rec;
 
 /* march.cpp:18-93 */
-static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSegs, int *active,
-                      float jitter01, float *rgb, float *alpha, int32_t *samples, march_rec *rec) {
+/* prim (nullable) receives the number of primitive evaluations, the executions of the body of
+ * march.cpp:63-70 (SURVEY.md §8d "prim-samples"). */
+static void march_one_counted(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSegs, int *active,
+                              float jitter01, float *rgb, float *alpha, int32_t *samples, march_rec *rec,
+                              int32_t *prim) {
+    int32_t nprim = 0;
     if (rec) {
         rec->lastStep = -1;
         rec->saturated = 0;
@@ -346,6 +350,7 @@ static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSe
                 rw[2] += r2 * sigma;
             }
             ++nsamp;
+            nprim += nActive;
             if (rec) rec->lastStep = i;
             const float dT = sigmaSum * dt;
             if (transmittance + dT >= 1) {
@@ -371,6 +376,12 @@ static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSe
     rgb[2] = color[2];
     *alpha = transmittance;
     *samples = nsamp;
+    if (prim) *prim = nprim;
+}
+
+static void march_one(const march_ctx *c, v3 o, v3 d, const seg_t *segs, int nSegs, int *active,
+                      float jitter01, float *rgb, float *alpha, int32_t *samples, march_rec *rec) {
+    march_one_counted(c, o, d, segs, nSegs, active, jitter01, rgb, alpha, samples, rec, NULL);
 }
 
 int vpo_march_rays(int32_t n_prim, int32_t m, const float *xf15, const float *payload,
@@ -399,7 +410,7 @@ typedef struct {
     uint64_t seed;
     int64_t y0, y1;
     float *rgb, *alpha;
-    int32_t *samples;
+    int32_t *samples, *prim;
 } render_job;
 
 static void *render_rows(void *arg) {
@@ -414,22 +425,26 @@ static void *render_rows(void *arg) {
             vpo_generate_ray(j->k9, j->r9, j->t3, (float)x + 0.5f, (float)y + 0.5f, o, d);
             const int n = collect(j->c->n_prim, j->c->xf15, ld3(o), ld3(d), segs);
             const float jit = j->jitter ? hash_to_unit(hash_combine(j->seed, (uint64_t)pixelId)) : 0.5f;
-            march_one(j->c, ld3(o), ld3(d), segs, n, active, jit, j->rgb + 3 * (size_t)pixelId,
-                      j->alpha + pixelId, j->samples + pixelId, NULL);
+            march_one_counted(j->c, ld3(o), ld3(d), segs, n, active, jit, j->rgb + 3 * (size_t)pixelId,
+                              j->alpha + pixelId, j->samples + pixelId, NULL,
+                              j->prim ? j->prim + pixelId : NULL);
         }
     free(segs);
     free(active);
     return NULL;
 }
 
-int vpo_render(int32_t n_prim, int32_t m, const float *xf15, const float *payload, float w_alpha,
-               int32_t w_beta, const float *k9, const float *r9, const float *t3, int32_t width,
-               int32_t height, float step, float early_eps, int32_t jitter, uint64_t seed,
-               uint64_t perm, float *rgb, float *alpha, int32_t *samples, int32_t n_threads) {
+/* vpo_render plus the per-pixel prim-sample counts (nullable). */
+int vpo_render_counted(int32_t n_prim, int32_t m, const float *xf15, const float *payload, float w_alpha,
+                       int32_t w_beta, const float *k9, const float *r9, const float *t3, int32_t width,
+                       int32_t height, float step, float early_eps, int32_t jitter, uint64_t seed,
+                       uint64_t perm, float *rgb, float *alpha, int32_t *samples, int32_t *prim,
+                       int32_t n_threads) {
     const size_t np = (size_t)width * (size_t)height;
     memset(rgb, 0, np * 3 * sizeof(float));
     memset(alpha, 0, np * sizeof(float));
     memset(samples, 0, np * sizeof(int32_t));
+    if (prim) memset(prim, 0, np * sizeof(int32_t));
     if (n_prim == 0 || np == 0) return 0; /* march.cpp:108 */
     const march_ctx c = {n_prim, m, xf15, payload, w_alpha, w_beta, step, early_eps, perm};
     if (n_threads <= 1) n_threads = 1;
@@ -441,7 +456,7 @@ int vpo_render(int32_t n_prim, int32_t m, const float *xf15, const float *payloa
     int started = 0;
     for (int w = 0; w < n_threads; ++w) {
         render_job j = {&c, k9, r9, t3, width, height, jitter, seed, w * chunk,
-                        (w + 1) * chunk < height ? (w + 1) * chunk : height, rgb, alpha, samples};
+                        (w + 1) * chunk < height ? (w + 1) * chunk : height, rgb, alpha, samples, prim};
         if (j.y0 >= j.y1) break;
         jobs[w] = j;
         pthread_create(&th[w], NULL, render_rows, &jobs[w]);
@@ -449,6 +464,14 @@ int vpo_render(int32_t n_prim, int32_t m, const float *xf15, const float *payloa
     }
     for (int w = 0; w < started; ++w) pthread_join(th[w], NULL);
     return 0;
+}
+
+int vpo_render(int32_t n_prim, int32_t m, const float *xf15, const float *payload, float w_alpha,
+               int32_t w_beta, const float *k9, const float *r9, const float *t3, int32_t width,
+               int32_t height, float step, float early_eps, int32_t jitter, uint64_t seed,
+               uint64_t perm, float *rgb, float *alpha, int32_t *samples, int32_t n_threads) {
+    return vpo_render_counted(n_prim, m, xf15, payload, w_alpha, w_beta, k9, r9, t3, width, height, step,
+                              early_eps, jitter, seed, perm, rgb, alpha, samples, NULL, n_threads);
 }
 
 void vpo_composite(int32_t width, int32_t height, const float *rgb, const float *alpha,

@@ -44,6 +44,9 @@ def test_render_matches_reference(renderer, case):
     assert_bit_equal(f"{case}.samples", out.sample_counts, c["samples"])
     if out.stats is not None and len(c["tr"]):
         assert out.stats["ray_samples"] == int(c["samples"].sum())
+        # the K5 prim-sample counter (the roofline's algorithmic bytes) vs the reference's count
+        prim = np.load(GOLDEN / "prim_counts.npz")[f"case_{case}"]
+        assert out.stats["prim_samples"] == int(prim.astype(np.int64).sum())
 
 
 DIGESTS = json.loads((GOLDEN / "digests.json").read_text())
@@ -65,6 +68,9 @@ def test_full_size_render_digest(renderer, key):
     assert sha(out.alpha) == d["alpha"]
     assert sha(out.color) == d["rgb"]
     assert out.stats["ray_samples"] == d["total_samples"]
+    # 128 B per prim-sample is the roofline's numerator: the device counter equals the
+    # reference's own count (oracle/gen_prim_counts.py)
+    assert out.stats["prim_samples"] == d["prim_samples"]
 
 
 @pytest.mark.parametrize("tile_cfg", ["light", "normal", "dense"])

@@ -60,20 +60,25 @@ def test_march_kats_match_reference(oracle):
 def test_render_matches_reference(oracle, case):
     c = render_cases()[case]
     xf = api.compose(c["tr"]) if len(c["tr"]) else np.zeros((0, 15), np.float32)
-    rgb, alpha, samples = oracle.render(xf, c["m"], c["payload"], c["window"], c["cam"], c["cfg"])
+    rgb, alpha, samples, prim = oracle.render_counted(xf, c["m"], c["payload"], c["window"], c["cam"], c["cfg"])
     assert np.array_equal(bits(rgb), bits(c["rgb"]))
     assert np.array_equal(bits(alpha), bits(c["alpha"]))
     assert np.array_equal(samples, c["samples"])
+    # per-pixel prim-samples (executions of march.cpp:63-70), counted by the reference itself
+    assert np.array_equal(prim, np.load(GOLDEN / "prim_counts.npz")[f"case_{case}"])
 
 
 def test_oracle_config1_full_size_digest(oracle):
-    """BASELINE config 1 (64 x 16^3 at 256^2, the reference's CPU oracle run), bit-exact."""
+    """BASELINE config 1 (64 x 16^3 at 256^2, the reference's CPU oracle run), bit-exact, with
+    the reference's per-pixel prim-sample counts."""
     d = json.loads((GOLDEN / "digests.json").read_text())["renders"]["oracle_64x16_256_view-1"]
     tr, pay = synthetic.shell_arrays(64, 16)
-    rgb, alpha, samples = oracle.render(api.compose(tr), 16, pay, api.WindowParams(),
-                                        synthetic.shell_camera(-1, 64, 256), api.MarchConfig())
+    rgb, alpha, samples, prim = oracle.render_counted(api.compose(tr), 16, pay, api.WindowParams(),
+                                                      synthetic.shell_camera(-1, 64, 256), api.MarchConfig())
     assert int(samples.sum()) == d["total_samples"]
     assert sha(samples) == d["samples"] and sha(alpha) == d["alpha"] and sha(rgb) == d["rgb"]
+    assert np.array_equal(prim, np.load(GOLDEN / "prim_counts.npz")["full_oracle_64x16_256_view-1"])
+    assert int(prim.astype(np.int64).sum()) == d["prim_samples"]
 
 
 def test_window_known_answers(oracle):
