@@ -777,17 +777,20 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
 template <class Cfg, int MT, bool PROF>
 static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const float4 *payload,
                                   const ViewBatch &views, const uint32_t *order, int n_ctas, cudaStream_t st) {
-    static bool attr_set = false;
+    // function attributes are per device: set them once on each device this process uses
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
     const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC>();
     auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB, Cfg::PF>;
-    if (!attr_set) {
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // Ask for just the shared memory MINB resident CTAs need (each also reserves 1 KB):
         // the rest of the 256 KB unified array stays L1 cache for the payload gathers.
         int carve = VPB_CARVEOUT;
         if (carve < 0) carve = (int)((Cfg::MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
-        attr_set = true;
+        if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
     kern<<<n_ctas, kMarchThreads, smem, st>>>(mp, xf16, payload, views, order);
     return cudaGetLastError();
