@@ -383,40 +383,43 @@ struct TileSmem {
     int4 *prect;       // CC
     int *prim;         // CC
     unsigned long long *tab;  // 32
-    int *state;        // kMarchThreads: cnt | more << 8
-    int *list;         // kMarchThreads
-    int *warp;         // kMarchThreads / 32
-    float *we, *wx;    // CAP * kMarchThreads each
-    void *wc;          // CAP * kMarchThreads window indices (uint8 or uint16)
-    unsigned *mask;    // (CC + 31) / 32 words * kMarchThreads per-ray candidate hit masks
+    int *state;        // NT: cnt | more << 8
+    int *list;         // NT
+    int *warp;         // NT / 32
+    float *we, *wx;    // CAP * NT each
+    void *wc;          // CAP * NT window indices (uint8 or uint16)
+    unsigned *mask;    // (CC + 31) / 32 words * NT per-ray candidate hit masks
 };
 
-template <int CAP, int MT, bool STAGED, int CC, bool PF>
+template <int CAP, int MT, bool STAGED, int CC, bool PF, int NT>
 __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam, const MarchDev &mp,
                                            const float *__restrict__ xf_g,
                                            const int4 *__restrict__ prects,
                                            const float4 *__restrict__ payload,
                                            const unsigned long long *__restrict__ entries,
-                                           uint32_t start, int n, int tx, int ty, const OutDev &od,
+                                           uint32_t start, int n, int tx, int ty, int half, const OutDev &od,
                                            DevCounters *ctr, int *__restrict__ ovf_list, int ovf_cap) {
+    // NT = 256: the CTA is the whole 16x16 tile; NT = 128: the CTA is the tile's top (half 0)
+    // or bottom (half 1) 16x8 pixels, and the two halves stage the same candidate list
+    const int pix0 = half * NT;  // tile_pixel index of this CTA's first pixel
     using IdxT = typename std::conditional<STAGED, uint8_t, uint16_t>::type;
     const int tid = threadIdx.x;
     const int m = MT > 0 ? MT : mp.m;
     const unsigned m3 = (unsigned)(m * m * m);
     const V3 o = mk3(cam.center[0], cam.center[1], cam.center[2]);
     if (STAGED) {
-        for (int i = tid; i < n * 4; i += kMarchThreads) {
+        for (int i = tid; i < n * 4; i += NT) {
             const int c = i >> 2, q = i & 3;
             const int prim = (int)(uint32_t)(entries[start + c] & 0xffffffffull);
             if (q == 0) sm.prim[c] = prim;
             sm.xf4[q * CC + c] = __ldg(reinterpret_cast<const float4 *>(xf_g + (size_t)prim * kXfStride) + q);
         }
         __syncthreads();
-        if (tid < n) {
-            const Xf16 x = load_xf(sm.xf4 + tid, CC);
+        for (int c = tid; c < n; c += NT) {
+            const Xf16 x = load_xf(sm.xf4 + c, CC);
             const V3 om = to_model(x.v, o);
-            sm.om[tid] = make_float4(om.x, om.y, om.z, 0.f);
-            sm.prect[tid] = prects[sm.prim[tid]];
+            sm.om[c] = make_float4(om.x, om.y, om.z, 0.f);
+            sm.prect[c] = prects[sm.prim[c]];
         }
         __syncthreads();
     }
@@ -425,7 +428,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     IdxT *wc = reinterpret_cast<IdxT *>(sm.wc);
 
     // phase 1: segment windows
-    const int2 px = tile_pixel(tx, ty, tid);
+    const int2 px = tile_pixel(tx, ty, pix0 + tid);
     const bool valid = px.x < cam.width && px.y < cam.height;
     const int64_t pix = (int64_t)px.y * cam.width + px.x;
     int cnt = 0;
@@ -440,7 +443,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     if (valid && n > 0) {
         V3 rd, d;
         generate_ray(cam, (float)px.x + 0.5f, (float)px.y + 0.5f, rd, d);
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, tid, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
+        const Window<IdxT> w{sm.we, sm.wx, wc, NT, tid, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
         window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
     sm.state[tid] = cnt | (more ? 256 : 0);
@@ -452,7 +455,7 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     if (lane == 0) sm.warp[wid] = __popc(bal);
     __syncthreads();
     int base = 0, n_hit = 0;
-    for (int q = 0; q < kMarchThreads / 32; ++q) {
+    for (int q = 0; q < NT / 32; ++q) {
         base += q < wid ? sm.warp[q] : 0;
         n_hit += sm.warp[q];
     }
@@ -464,13 +467,13 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     const bool live = tid < n_hit;
     if (live) {
         const int r = sm.list[tid];
-        const int2 rp = tile_pixel(tx, ty, r);
+        const int2 rp = tile_pixel(tx, ty, pix0 + r);
         const int64_t p = (int64_t)rp.y * cam.width + rp.x;
         V3 rd, d;
         generate_ray(cam, (float)rp.x + 0.5f, (float)rp.y + 0.5f, rd, d);
         const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)(int)p)) : 0.5f;
         const int st = sm.state[r];
-        const Window<IdxT> w{sm.we, sm.wx, wc, kMarchThreads, r, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
+        const Window<IdxT> w{sm.we, sm.wx, wc, NT, r, STAGED ? sm.mask : nullptr, STAGED ? (CC + 31) / 32 : 0};
         ro = march_window<CAP, MT>(cands, w, st & 255, (st & 256) != 0, o, d, rp, jit, mp, sm.tab);
         if (ro.overflow) {
             const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
@@ -482,8 +485,8 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     add_counters(ctr, ro, live && !ro.overflow);
 }
 
-template <int CAP, int MT, bool PROF, int CC, int MINB, bool PF>
-__global__ void __launch_bounds__(kMarchThreads, MINB)
+template <int CAP, int MT, bool PROF, int CC, int MINB, bool PF, int NT>
+__global__ void __launch_bounds__(NT, MINB)
 k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restrict__ payload, ViewBatch views,
               const uint32_t *__restrict__ order) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -494,14 +497,16 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     sm.prim = reinterpret_cast<int *>(sm.prect + CC);
     sm.tab = reinterpret_cast<unsigned long long *>(sm.prim + CC);
     sm.state = reinterpret_cast<int *>(sm.tab + 32);
-    sm.list = sm.state + kMarchThreads;
-    sm.warp = sm.list + kMarchThreads;
-    sm.we = reinterpret_cast<float *>(sm.warp + kMarchThreads / 32);
-    sm.wx = sm.we + CAP * kMarchThreads;
-    sm.wc = sm.wx + CAP * kMarchThreads;
-    sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + CAP * kMarchThreads);
+    sm.list = sm.state + NT;
+    sm.warp = sm.list + NT;
+    sm.we = reinterpret_cast<float *>(sm.warp + NT / 32);
+    sm.wx = sm.we + CAP * NT;
+    sm.wc = sm.wx + CAP * NT;
+    sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + CAP * NT);
 
-    const uint32_t oe = order[blockIdx.x];
+    constexpr int kParts = kMarchThreads / NT;  // CTAs per tile
+    const uint32_t oe = order[blockIdx.x / kParts];
+    const int half = (int)(blockIdx.x % kParts);
     const ViewDev &vd = views.v[oe >> 20];
     const CamDev &cam = vd.cam;
     const OutDev &od = vd.od;
@@ -516,20 +521,20 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
     if (n <= CC)
-        march_tile<CAP, MT, true, CC, PF>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+        march_tile<CAP, MT, true, CC, PF, NT>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, half, od, ctr,
                                       vd.ovf_list, vd.ovf_cap);
     else
-        march_tile<CAP, MT, false, CC, false>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, od, ctr,
+        march_tile<CAP, MT, false, CC, false, NT>(sm, cam, mp, xf_g, vd.prects, payload, vd.entries, start, n, tx, ty, half, od, ctr,
                                        vd.ovf_list, vd.ovf_cap);
     if (PROF) {  // separate instantiation: per-CTA timeline for load-balance analysis
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && half == 0) {  // per tile: its first CTA
             unsigned long long t_end, smid;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             unsigned s32;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
             smid = s32;
-            unsigned long long *q = od.prof + 4 * (size_t)blockIdx.x;
+            unsigned long long *q = od.prof + 4 * (size_t)(blockIdx.x / kParts);
             q[0] = (unsigned long long)tile;
             q[1] = smid;
             q[2] = t_start;
@@ -697,12 +702,12 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 // payload (e.g. 3 x 52 KB -> 92 KB of L1 for Normal). Measured on the BASELINE configs
 // (profiles/r01_tile_configs.txt):
 //   Light  (<= 14 candidates/tile, K=512 M=32):   12-entry windows, 64 staged, 3 CTAs/SM
-//   Normal (<= 40, the K=4096 M=16 headline):      16-entry windows, 64 staged, 3 CTAs/SM
+//   Normal (<= 40, the K=4096 M=16 headline):      16-entry windows, 64 staged, 6 half-tile CTAs/SM
 //   Dense  (K=32768 M=8: long lists, many segments per ray, refills on the critical path of
 //          the heaviest tiles):                    24-entry windows, 192 staged, 2 CTAs/SM
 // VPB_WINDOW_CAP / VPB_CAND_CAP / VPB_MARCH_MINB override Normal for tuning builds.
 #ifndef VPB_MARCH_MINB
-#define VPB_MARCH_MINB 3
+#define VPB_MARCH_MINB 6
 #endif
 #ifndef VPB_CARVEOUT
 #define VPB_CARVEOUT -1  // shared-memory carveout hint in percent; -1: just enough for MINB CTAs
@@ -712,26 +717,42 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 #endif
 // PF: line-vs-box prefilter before the exact candidate test (K=32768 M=8 launch 4.58 ->
 // 4.27 ms; the K=4096 headline 6.16 -> 6.28 ms, so only the dense tier uses it).
+#ifndef VPB_NORMAL_NT
+#define VPB_NORMAL_NT 128
+#endif
+#ifndef VPB_LIGHT_NT
+#define VPB_LIGHT_NT 256
+#endif
+#ifndef VPB_DENSE_NT
+#define VPB_DENSE_NT 256
+#endif
+#ifndef VPB_DENSE_MINB
+#define VPB_DENSE_MINB 2
+#endif
+// NT: threads per CTA (256: a CTA per 16x16 tile; 128: a CTA per 16x8 half tile). A CTA holds
+// its warp slots until its longest ray ends; by the per-pixel sample counts of the headline,
+// lanes are 67 % busy over a 16x16 CTA's lifetime and 72 % over a 16x8 one
+// (tools/lane_efficiency.py). The normal tier therefore runs half tiles, 6 CTAs/SM: the
+// headline launch went from 6.18 to 6.02 ms (profiles/r01_tile_configs.txt, sweep 6).
 struct TileCfgLight {
-    static constexpr int CAP = 12, CC = 64, MINB = 3;
+    static constexpr int CAP = 12, CC = 64, MINB = VPB_LIGHT_NT == 128 ? 6 : 3, NT = VPB_LIGHT_NT;
     static constexpr bool PF = false;
 };
 struct TileCfgNormal {
-    static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = VPB_MARCH_MINB;
+    static constexpr int CAP = VPB_WINDOW_CAP, CC = kCandCap, MINB = VPB_MARCH_MINB, NT = VPB_NORMAL_NT;
     static constexpr bool PF = VPB_NORMAL_PF;
 };
 struct TileCfgDense {
-    static constexpr int CAP = 24, CC = 192, MINB = 2;
+    static constexpr int CAP = 24, CC = 192, MINB = VPB_DENSE_MINB, NT = VPB_DENSE_NT;
     static constexpr bool PF = true;
 };
 
-template <int CAP, int CC>
+template <int CAP, int CC, int NT>
 static size_t tiles_smem() {
-    return (size_t)CC * kXfStride * 4 + CC * 16 * 2 + CC * 4 + 32 * 8 + kMarchThreads * 4 * 2 +
-           (kMarchThreads / 32) * 4 + (size_t)CAP * kMarchThreads * (8 + 2) +
-           (size_t)((CC + 31) / 32) * kMarchThreads * 4;
+    return (size_t)CC * kXfStride * 4 + CC * 16 * 2 + CC * 4 + 32 * 8 + NT * 4 * 2 + (NT / 32) * 4 +
+           (size_t)CAP * NT * (8 + 2) + (size_t)((CC + 31) / 32) * NT * 4;
 }
-size_t march_tiles_smem() { return tiles_smem<TileCfgNormal::CAP, TileCfgNormal::CC>(); }
+size_t march_tiles_smem() { return tiles_smem<TileCfgNormal::CAP, TileCfgNormal::CC, TileCfgNormal::NT>(); }
 
 cudaError_t launch_repack(const float *planar, float4 *inter, int64_t n_prim, int64_t m3,
                           cudaStream_t st) {
@@ -781,8 +802,8 @@ static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const f
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC>();
-    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB, Cfg::PF>;
+    const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC, Cfg::NT>();
+    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB, Cfg::PF, Cfg::NT>;
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // Ask for just the shared memory MINB resident CTAs need (each also reserves 1 KB):
@@ -792,7 +813,7 @@ static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const f
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
         if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
-    kern<<<n_ctas, kMarchThreads, smem, st>>>(mp, xf16, payload, views, order);
+    kern<<<n_ctas * (kMarchThreads / Cfg::NT), Cfg::NT, smem, st>>>(mp, xf16, payload, views, order);
     return cudaGetLastError();
 }
 
