@@ -279,7 +279,9 @@ def run_tile_shard(args, rank, world, local, device):
                              "frac": round(alg / march_s / 1e9 / hbm, 4), "traffic": None,
                              "kernel": "k_march_tiles (+k_march_fallback_views), rank 0's shard",
                              "peak_kind": pk_kind, "avg_launch_ms": round(march_s * 1e3, 4)},
-                "cpu_baseline": None, "e2e": None, "gpu_launches": 6 * args.steps, "clocks": clk}
+                "cpu_baseline": None, "e2e": None,
+                # per step: 6 binning stages, the raymarch and its fallback (one view)
+                "gpu_launches": 8 * args.steps, "clocks": clk}
         print(json.dumps(line), flush=True)
     r.close()
 
@@ -529,7 +531,9 @@ def main():
                 "prim_samples_per_s": round(all_prim / t_max / 1e6, 3),
                 "ray_samples_per_view": ray_samples // V, "prim_samples_per_view": prim_samples // V,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": 6 * V * args.steps,
+                # per step, batched: 6 binning stages for all views, the cross-view tile order, one
+                # raymarch and one fallback launch; per view: 6 + 2 launches for each view
+                "gpu_launches": (9 if batch else 8 * V) * args.steps,
                 "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
                 "stats_last_launch": rc_stats.as_dict()}
         print(json.dumps(line), flush=True)
