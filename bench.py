@@ -500,7 +500,7 @@ def main():
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
         e2e_finish()
-        n_e2e = max(3, args.steps // 2)
+        n_e2e = max(3, args.steps)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
