@@ -702,7 +702,7 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 // payload (e.g. 3 x 52 KB -> 92 KB of L1 for Normal). Measured on the BASELINE configs
 // (profiles/r01_tile_configs.txt):
 //   Light  (<= 14 candidates/tile, K=512 M=32):   12-entry windows, 64 staged, 3 CTAs/SM
-//   Normal (<= 40, the K=4096 M=16 headline):      14-entry windows, 64 staged, 6 half-tile CTAs/SM
+//   Normal (<= 40, the K=4096 M=16 headline):      14-entry windows, 56 staged, 6 half-tile CTAs/SM
 //   Dense  (K=32768 M=8: long lists, many segments per ray, refills on the critical path of
 //          the heaviest tiles):                    24-entry windows, 192 staged, 2 CTAs/SM
 // VPB_WINDOW_CAP / VPB_CAND_CAP / VPB_MARCH_MINB override Normal for tuning builds.
@@ -734,7 +734,9 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 // lanes are 67 % busy over a 16x16 CTA's lifetime and 72 % over a 16x8 one
 // (tools/lane_efficiency.py). The normal tier therefore runs half tiles, 6 CTAs/SM: the
 // headline launch went from 6.18 to 5.99 ms (profiles/r01_tile_configs.txt, sweeps 6-7);
-// 16x4 quarter tiles at 10-12 CTAs/SM lose again (6.07-6.42 ms).
+// 16x4 quarter tiles at 10-12 CTAs/SM lose again (6.07-6.42 ms). Staging 56 candidates
+// instead of 64 keeps 6 CTAs' shared memory under the 164 KB carveout, so L1 keeps 92 KB
+// instead of 60: 5.92 ms (sweep 8).
 struct TileCfgLight {
     static constexpr int CAP = 12, CC = 64, MINB = VPB_LIGHT_NT == 128 ? 6 : 3, NT = VPB_LIGHT_NT;
     static constexpr bool PF = false;

@@ -15,7 +15,7 @@ namespace vpb {
 constexpr int kTile = 16;
 constexpr int kMarchThreads = 256;  // one thread per pixel of a 16x16 tile
 #ifndef VPB_CAND_CAP
-#define VPB_CAND_CAP 64
+#define VPB_CAND_CAP 56
 #endif
 constexpr int kCandCap = VPB_CAND_CAP;  // candidates staged in shared memory per tile (<= 255)
 
