@@ -701,7 +701,7 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 // keeps its shared memory small enough that the rest of the SM's 256 KB stays L1 cache for the
 // payload (e.g. 3 x 52 KB -> 92 KB of L1 for Normal). Measured on the BASELINE configs
 // (profiles/r01_tile_configs.txt):
-//   Light  (<= 14 candidates/tile, K=512 M=32):   12-entry windows, 64 staged, 3 CTAs/SM
+//   Light  (<= 14 candidates/tile, K=512 M=32):   10-entry windows, 48 staged, 6 half-tile CTAs/SM
 //   Normal (<= 40, the K=4096 M=16 headline):      14-entry windows, 56 staged, 6 half-tile CTAs/SM
 //   Dense  (K=32768 M=8: long lists, many segments per ray, refills on the critical path of
 //          the heaviest tiles):                    24-entry windows, 192 staged, 2 CTAs/SM
@@ -721,13 +721,25 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 #define VPB_NORMAL_NT 128
 #endif
 #ifndef VPB_LIGHT_NT
-#define VPB_LIGHT_NT 256
+#define VPB_LIGHT_NT 128
 #endif
 #ifndef VPB_DENSE_NT
 #define VPB_DENSE_NT 256
 #endif
 #ifndef VPB_DENSE_MINB
 #define VPB_DENSE_MINB 2
+#endif
+#ifndef VPB_DENSE_CAP
+#define VPB_DENSE_CAP 24
+#endif
+#ifndef VPB_DENSE_CC
+#define VPB_DENSE_CC 192
+#endif
+#ifndef VPB_LIGHT_CAP
+#define VPB_LIGHT_CAP 10
+#endif
+#ifndef VPB_LIGHT_CC
+#define VPB_LIGHT_CC 48
 #endif
 // NT: threads per CTA (256: a CTA per 16x16 tile; 128: a CTA per 16x8 half tile). A CTA holds
 // its warp slots until its longest ray ends; by the per-pixel sample counts of the headline,
@@ -736,9 +748,11 @@ constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp
 // headline launch went from 6.18 to 5.99 ms (profiles/r01_tile_configs.txt, sweeps 6-7);
 // 16x4 quarter tiles at 10-12 CTAs/SM lose again (6.07-6.42 ms). Staging 56 candidates
 // instead of 64 keeps 6 CTAs' shared memory under the 164 KB carveout, so L1 keeps 92 KB
-// instead of 60: 5.92 ms (sweep 8).
+// instead of 60: 5.92 ms (sweep 8). The light tier as half tiles with 10-entry windows and 48
+// staged: K=512 M=32 12.61 -> 12.24 ms, K=64 M=16 at 256^2 2.63 -> 2.50 ms (sweep 10).
 struct TileCfgLight {
-    static constexpr int CAP = 12, CC = 64, MINB = VPB_LIGHT_NT == 128 ? 6 : 3, NT = VPB_LIGHT_NT;
+    static constexpr int CAP = VPB_LIGHT_CAP, CC = VPB_LIGHT_CC, MINB = VPB_LIGHT_NT == 128 ? 6 : 3,
+                         NT = VPB_LIGHT_NT;
     static constexpr bool PF = false;
 };
 struct TileCfgNormal {
@@ -746,7 +760,7 @@ struct TileCfgNormal {
     static constexpr bool PF = VPB_NORMAL_PF;
 };
 struct TileCfgDense {
-    static constexpr int CAP = 24, CC = 192, MINB = VPB_DENSE_MINB, NT = VPB_DENSE_NT;
+    static constexpr int CAP = VPB_DENSE_CAP, CC = VPB_DENSE_CC, MINB = VPB_DENSE_MINB, NT = VPB_DENSE_NT;
     static constexpr bool PF = true;
 };
 
