@@ -324,11 +324,13 @@ def main():
         xf = api.compose(tr)
         slab = api.PrimitiveSlab(k, m, pay)
     win = api.WindowParams()
+    t_up = time.perf_counter()
     if world > 1:
         bcast_bytes = broadcast_scene(r, xf, slab, win, k, m, device)
     else:
         r.set_scene_composed(xf, slab, win)
         bcast_bytes = 0
+    scene_upload_ms = (time.perf_counter() - t_up) * 1e3  # one-time: H2D, K0 repack (+ broadcast)
     views = view_shard(N_RING, world, rank, per_rank=V)
     cams = [synthetic.shell_camera(v, N_RING, w).to_c() for v in views]
     cfg = api.MarchConfig()
@@ -341,6 +343,26 @@ def main():
         per_view.append(out.stats)
     ray_samples = sum(s["ray_samples"] for s in per_view)
     prim_samples = sum(s["prim_samples"] for s in per_view)
+
+    # one view per launch (SURVEY.md §8d's per-view timing): K1-K5 of ONE view per raymarch
+    # launch (vp_render_async into device buffers, renders back to back, so a view's binning
+    # overlaps the previous view's raymarch), CUDA events on the launching stream, median of 20
+    # after 5 warm-ups; outside the timed region, which marches 8 views per launch
+    sv_stream = torch.cuda.Stream(device)
+    sv_out = [torch.empty(w * w * 3, device=device), torch.empty(w * w, device=device),
+              torch.empty(w * w, dtype=torch.int32, device=device)]
+    sv_ms = []
+    cam0 = api.Camera.from_c(cams[0])
+    for i in range(25):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sv_stream)
+        r.render_device(cam0, cfg, sv_out[0].data_ptr(), sv_out[1].data_ptr(), sv_out[2].data_ptr(),
+                        sv_stream.cuda_stream)
+        e1.record(sv_stream)
+        sv_ms.append((e0, e1))
+    torch.cuda.synchronize()
+    single_view_ms = float(np.median([a.elapsed_time(b) for a, b in sv_ms[5:]]))
+    del sv_out
     r.kernel_times()
 
     vg = ViewGather(V, w, w, device, world, rank)
@@ -535,6 +557,10 @@ def main():
                 # raymarch and one fallback launch; per view: 6 + 2 launches for each view
                 "gpu_launches": (9 if batch else 8 * V) * args.steps,
                 "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
+                "single_view": {"ms": round(single_view_ms, 4), "frames_per_s": round(1e3 / single_view_ms, 1),
+                                "what": "one view per raymarch launch (vp_render_async, back to back), "
+                                        f"median of 20, view {views[0]} of the ring"},
+                "scene_upload_ms": round(scene_upload_ms, 2),
                 "stats_last_launch": rc_stats.as_dict()}
         print(json.dumps(line), flush=True)
     if world > 1:
