@@ -475,7 +475,12 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 // step order. Rays with more than kWarpListBwd segments take the per-thread path.
 constexpr int kWarpListBwd = 96;
 constexpr int kWarpCandBwd = 256;
-__global__ void __launch_bounds__(128)
+// 3 CTAs/SM (168 registers, 16 B of spills) against 2 at the unbounded 230: the 65,536-ray
+// backward row 3.08 -> 2.78 ms (gpurun_out sweep, K6)
+#ifndef VPB_BWD_WARP_MINB
+#define VPB_BWD_WARP_MINB 3
+#endif
+__global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, float *se, float *sx, int *sc) {
     __shared__ unsigned long long s_tab[32];

@@ -987,11 +987,13 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st) {
     if (n_rays == 0) return cudaSuccess;
-    // Each ray is a serial latency chain: small batches (evalLoss: 2048 rays) are marched a
-    // warp per ray, 32 lattice steps at a time; mid-size ones go out as one-warp CTAs so they
-    // spread over every SM instead of packing into a few.
+    // Each ray is a serial latency chain, so rays are marched a warp per ray, 32 lattice steps
+    // at a time. Since the warp walks the BVH cooperatively (warp_bvh_leaves) this wins at
+    // every batch size measured (65,536 rays: 1.05 -> 0.7 ms against one thread per ray).
+    // VPB_FWD_WARP_MAX (tuning builds) sends larger batches to the thread-per-ray kernel:
+    // one-warp CTAs for mid-size batches so they spread over every SM, 128-thread CTAs beyond.
 #ifndef VPB_FWD_WARP_MAX
-#define VPB_FWD_WARP_MAX kWarpRayBatch
+#define VPB_FWD_WARP_MAX INT64_MAX
 #endif
     if (n_rays <= (int64_t)VPB_FWD_WARP_MAX) {
         const int64_t blocks = (n_rays + 3) / 4;

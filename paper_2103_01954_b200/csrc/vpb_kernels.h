@@ -118,7 +118,6 @@ struct AdamDev {
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
-constexpr int64_t kWarpRayBatch = 16384;  // vp_march_rays batches up to this go warp-per-ray
 // backwardRay: one-warp CTAs, 12 per SM (168 registers, no spills); the scratch
 // windows (kFallbackCap entries each) are sized for the larger of the two grids
 constexpr int kBackwardWarps = 148 * 12;

@@ -531,8 +531,59 @@ done:
     return out;
 }
 
-// The complete sorted segment list of one ray, built by a warp: lane 0 walks the BVH and
-// lists the primitives whose box the ray crosses (cheap box tests); the exact intersectObb
+// The BVH leaves whose padded box a ray crosses, found by a whole warp (n_prim >= 2). The
+// warp keeps a frontier of pending nodes in shared memory (`fr`, `cap_fr` entries) and each
+// round takes up to 32 of them off the top, one per lane; a lane tests both children's boxes
+// and the hits are appended with ballots: internal children back onto the frontier, leaves
+// onto `cand` (the first `cap_cand` of them are stored; `nc` counts all). The leaf set equals
+// bvh_for_each's; only the order differs, and warp_segment_list orders its hits by key.
+// Returns 0, or -1 when the frontier or the leaf list overflows (caller falls back).
+__device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, int lane, int *cand, int cap_cand,
+                                               int *fr, int cap_fr, int &nc) {
+    const V3 inv = mk3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+    const unsigned below = (1u << lane) - 1u;
+    if (lane == 0) fr[0] = 0;
+    __syncwarp();
+    int sp = 1;
+    nc = 0;
+    while (sp > 0) {
+        const int take = sp < 32 ? sp : 32, b = sp - take;
+        const bool act = lane < take;
+        const int node = act ? fr[b + lane] : 0;
+        __syncwarp();
+        bool hl = false, hr = false;
+        int l = 0, r = 0;
+        if (act) {
+            const BvhNode n = bvh.nodes[node];
+            hl = ray_box(o, d, inv, n.a.x, n.a.y, n.a.z, n.a.w, n.b.x, n.b.y);
+            hr = ray_box(o, d, inv, n.b.z, n.b.w, n.c.x, n.c.y, n.c.z, n.c.w);
+            l = n.d.x;
+            r = n.d.y;
+        }
+        const unsigned pl = __ballot_sync(0xffffffffu, hl && l >= 0), pr = __ballot_sync(0xffffffffu, hr && r >= 0);
+        const unsigned ll = __ballot_sync(0xffffffffu, hl && l < 0), lr = __ballot_sync(0xffffffffu, hr && r < 0);
+        const int npl = __popc(pl), np = npl + __popc(pr), nll = __popc(ll);
+        if (b + np > cap_fr) return -1;
+        if (hl && l >= 0) fr[b + __popc(pl & below)] = l;
+        if (hr && r >= 0) fr[b + npl + __popc(pr & below)] = r;
+        if (hl && l < 0) {
+            const int q = nc + __popc(ll & below);
+            if (q < cap_cand) cand[q] = -l - 1;
+        }
+        if (hr && r < 0) {
+            const int q = nc + nll + __popc(lr & below);
+            if (q < cap_cand) cand[q] = -r - 1;
+        }
+        nc += nll + __popc(lr);
+        if (nc > cap_cand) return -1;
+        sp = b + np;
+        __syncwarp();
+    }
+    return 0;
+}
+
+// The complete sorted segment list of one ray, built by a warp: the warp walks the BVH
+// (warp_bvh_leaves) and lists the primitives whose box the ray crosses (cheap box tests); the exact intersectObb
 // tests run on all lanes; the hits are placed by rank of their (tEnter, prim) key (keys are
 // distinct), which is the order window_scan produces. Returns the hit count, or -1 when the
 // ray crosses more than `cap_cand` boxes or has more than `cap` hits (caller falls back).
@@ -540,13 +591,17 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
                                                  float *ce, float *cx, int cap_cand, float *E, float *X, int *P,
                                                  int cap) {
     int nc = 0;
-    if (lane == 0) {
-        bvh_for_each(cands.bvh, o, d, [&](int c) {
-            if (nc < cap_cand) cand[nc] = c;
-            ++nc;
-        });
+    if (cands.bvh.n_prim <= 1) {
+        if (lane == 0)
+            bvh_for_each(cands.bvh, o, d, [&](int c) {
+                if (nc < cap_cand) cand[nc] = c;
+                ++nc;
+            });
+        nc = __shfl_sync(0xffffffffu, nc, 0);
+    } else if (warp_bvh_leaves(cands.bvh, o, d, lane, cand, cap_cand, reinterpret_cast<int *>(ce), cap_cand,
+                               nc) < 0) {
+        return -1;
     }
-    nc = __shfl_sync(0xffffffffu, nc, 0);
     __syncwarp();
     if (nc > cap_cand) return -1;
     for (int q = lane; q < nc; q += 32) {
