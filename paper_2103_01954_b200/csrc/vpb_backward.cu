@@ -477,6 +477,9 @@ constexpr int kWarpListBwd = 96;
 constexpr int kWarpCandBwd = 256;
 // 3 CTAs/SM (168 registers, 16 B of spills) against 2 at the unbounded 230: the 65,536-ray
 // backward row 3.08 -> 2.78 ms (gpurun_out sweep, K6)
+#ifndef VPB_BWD_PAIRS
+#define VPB_BWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
+#endif
 #ifndef VPB_BWD_WARP_MINB
 #define VPB_BWD_WARP_MINB 3
 #endif
@@ -536,12 +539,72 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
             const unsigned empty = __ballot_sync(0xffffffffu, !(valid && na > 0));
             const int L = empty ? __ffs(empty) - 1 : 32;
             float contrib = 0.f;
+#if VPB_BWD_PAIRS
+            // The chunk's primitive-samples (step s < L, k-th active entry of s), step-major,
+            // are dealt out one per lane, 32 at a time. Each step's sum of rotG is then folded
+            // in list order, starting from the carry of the previous batch, exactly as
+            // gPWorldStep accumulates in the per-step walk (grad.cpp:66-164).
+            const int myna = lane < L ? na : 0;
+            int incl = myna;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            const int excl = incl - myna;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            V3 acc = mk3(0.f, 0.f, 0.f);  // gPWorldStep of this lane's step
+            for (int p0 = 0; p0 < total; p0 += 32) {
+                const int p = p0 + lane;
+                const bool has = p < total;
+                int s = 0;  // the pair's step: the number of lanes with incl <= p
+#pragma unroll
+                for (int h = 16; h > 0; h >>= 1)
+                    if (__shfl_sync(0xffffffffu, incl, s + h - 1) <= p) s += h;
+                const int k = p - __shfl_sync(0xffffffffu, excl, s);
+                const int incl_s = __shfl_sync(0xffffffffu, incl, s);
+                const float tsp = __shfl_sync(0xffffffffu, ts, s);
+                V3 rg = mk3(0.f, 0.f, 0.f);
+                if (has) {
+                    int j = 0;
+                    for (int left = k;; ++j)
+                        if (X[j] > tsp) {
+                            if (left == 0) break;
+                            --left;
+                        }
+                    bw.step_begin(base + s, tsp, o + d * tsp);
+                    bw.prim(P[j], P[j]);
+                    rg = bw.gPWorldStep;
+                }
+                const bool lead = has && (lane == 0 || k == 0);
+                const int run = lead ? min(incl_s - p, 32 - lane) : 0;
+                // a run leader starts from its step's carry (the sum over earlier batches)
+                V3 c = mk3(__shfl_sync(0xffffffffu, acc.x, s), __shfl_sync(0xffffffffu, acc.y, s),
+                           __shfl_sync(0xffffffffu, acc.z, s));
+                c = c + rg;
+                const int maxrun = __reduce_max_sync(0xffffffffu, run);
+                for (int t = 1; t < maxrun; ++t) {
+                    const V3 v = mk3(__shfl_down_sync(0xffffffffu, rg.x, t), __shfl_down_sync(0xffffffffu, rg.y, t),
+                                     __shfl_down_sync(0xffffffffu, rg.z, t));
+                    if (t < run) c = c + v;
+                }
+                // lane s < L takes its step's fold from the lane holding the step's first pair here
+                const int f = excl > p0 ? excl - p0 : 0;
+                const bool mine = lane < L && excl < p0 + 32 && incl > p0;
+                const int fl = f < 32 ? f : 31;
+                const V3 nv = mk3(__shfl_sync(0xffffffffu, c.x, fl), __shfl_sync(0xffffffffu, c.y, fl),
+                                  __shfl_sync(0xffffffffu, c.z, fl));
+                if (mine) acc = nv;
+            }
+            if (lane < L) contrib = dot3(acc, d);
+#else
             if (lane < L) {  // a visited step with samples (grad.cpp:66-164)
                 bw.step_begin(i, ts, o + d * ts);
                 for (int j = 0; j < nadm; ++j)
                     if (X[j] > ts) bw.prim(P[j], P[j]);
                 contrib = dot3(bw.gPWorldStep, d);
             }
+#endif
             for (int s = 0; s < L; ++s) gTmin += __shfl_sync(0xffffffffu, contrib, s);  // step order
             if (base + L - 1 >= lastStep) break;
             if (L == 32) {
