@@ -641,6 +641,9 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
 // non-empty, and at the first empty one the reference's gap skip (march.cpp:43-49) picks the
 // next chunk's base. Transmittance and colour are accumulated serially over the chunk's
 // steps (every lane computes the same values from shuffles), so the result is bit-identical.
+#ifndef VPB_FWD_PAIRS
+#define VPB_FWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
+#endif
 template <class Cands>
 __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X, const int *P, int cnt, V3 o,
                              V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane) {
@@ -660,9 +663,87 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         const int i = base + lane;
         const bool in_range = i <= kMaxStep;
         const float ts = t0 + (__int2float_rn(i) + jit) * dt;
-        const V3 pw = o + d * ts;
         float sig = 0.f, rw = 0.f, gw = 0.f, bw = 0.f;
         int na = 0, nadm = 0;
+#if VPB_FWD_PAIRS
+        for (int j = 0; j < cnt && in_range; ++j) {
+            if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
+            nadm = j + 1;
+            na += X[j] > ts;
+        }
+        const unsigned empty = __ballot_sync(0xffffffffu, !(in_range && na > 0));
+        const int L = empty ? __ffs(empty) - 1 : 32;
+        // The primitive-samples of the visited steps s < L (k-th active entry of step s),
+        // step-major, are dealt out one per lane, 32 at a time; each step's four sums are then
+        // folded in list order from the carry of the previous batch, which is exactly the
+        // per-step accumulation below (march.cpp:60-70).
+        const int myna = lane < L ? na : 0;
+        int incl = myna;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int excl = incl - myna;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int p0 = 0; p0 < total; p0 += 32) {
+            const int p = p0 + lane;
+            const bool has = p < total;
+            int s = 0;  // the pair's step: the number of lanes with incl <= p
+#pragma unroll
+            for (int h = 16; h > 0; h >>= 1)
+                if (__shfl_sync(0xffffffffu, incl, s + h - 1) <= p) s += h;
+            const int k = p - __shfl_sync(0xffffffffu, excl, s);
+            const int incl_s = __shfl_sync(0xffffffffu, incl, s);
+            const float tsp = __shfl_sync(0xffffffffu, ts, s);
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+            if (has) {
+                int j = 0;
+                for (int left = k;; ++j)
+                    if (X[j] > tsp) {
+                        if (left == 0) break;
+                        --left;
+                    }
+                const int c = P[j];
+                float sg, r, g, b;
+                const Xf16 xr = cands.xfv(c);
+                sample_primitive<0>(cands.base(c), mp.m, xr.v, o + d * tsp, mp.alpha, mp.beta, tab, sg, r, g, b);
+                a[0] = sg;
+                a[1] = r * sg;
+                a[2] = g * sg;
+                a[3] = b * sg;
+            }
+            const bool lead = has && (lane == 0 || k == 0);
+            const int run = lead ? min(incl_s - p, 32 - lane) : 0;
+            float c[4] = {__shfl_sync(0xffffffffu, sig, s), __shfl_sync(0xffffffffu, rw, s),
+                          __shfl_sync(0xffffffffu, gw, s), __shfl_sync(0xffffffffu, bw, s)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] += a[q];
+            const int maxrun = __reduce_max_sync(0xffffffffu, run);
+            for (int t = 1; t < maxrun; ++t) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = __shfl_down_sync(0xffffffffu, a[q], t);
+                if (t < run)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) c[q] += v[q];
+            }
+            // lane s < L takes its step's fold from the lane holding the step's first pair here
+            const int f = excl > p0 ? excl - p0 : 0;
+            const int fl = f < 32 ? f : 31;
+            const bool mine = lane < L && excl < p0 + 32 && incl > p0;
+            float nv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nv[q] = __shfl_sync(0xffffffffu, c[q], fl);
+            if (mine) {
+                sig = nv[0];
+                rw = nv[1];
+                gw = nv[2];
+                bw = nv[3];
+            }
+        }
+#else
+        const V3 pw = o + d * ts;
         for (int j = 0; j < cnt && in_range; ++j) {
             if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
             nadm = j + 1;
@@ -680,6 +761,7 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         }
         const unsigned empty = __ballot_sync(0xffffffffu, !(in_range && na > 0));
         const int L = empty ? __ffs(empty) - 1 : 32;
+#endif
         for (int s = 0; s < L; ++s) {  // the chunk's visited steps, in order (march.cpp:71-88)
             const float s_sig = __shfl_sync(0xffffffffu, sig, s);
             const float s_rw = __shfl_sync(0xffffffffu, rw, s);
