@@ -1101,7 +1101,7 @@ namespace {
 // of the same rays) lets the kernel skip its replay of march().
 int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs, const float *jitter01,
                   const float *adj_rgb, const float *adj_alpha, const vp_march *cfg, const float *transforms24,
-                  float *grads, int32_t accumulate, const float *fwd_state) {
+                  float *grads, int32_t accumulate, const float *fwd_state, const float *fwd_segs) {
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n_rays < 0) return fail(ctx, VP_ERR_USAGE, "negative ray count");
@@ -1165,9 +1165,10 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         if (!fwd_state) {
             // forward march of the same rays first, recording the MarchResult bookkeeping, so
             // the backward kernel does not replay march() itself
-            VP_CUDA(ctx, ctx->s_bwd_fwd.ensure(12 * n));
+            VP_CUDA(ctx, ctx->s_bwd_fwd.ensure((12 + 3 * kRaySegs) * n));
             OutDev od{ctx->s_bwd_fwd.p, ctx->s_bwd_fwd.p + 3 * n, nullptr};
             od.state = ctx->s_bwd_fwd.p + 4 * n;
+            od.segs = ctx->s_bwd_fwd.p + 12 * n;
             if (size_t(ctx->ovf_cap) < n) {
                 VP_CUDA(ctx, ctx->ovf_list.ensure(n));
                 ctx->ovf_cap = int(n);
@@ -1179,8 +1180,9 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                                                nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
                                                ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
             fwd_state = od.state;
+            fwd_segs = od.segs;
         }
-        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state};
+        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
@@ -1199,7 +1201,7 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
                      const vp_march *cfg, const float *transforms24, float *grads,
                      int32_t accumulate) {
     return backward_rays(ctx, n_rays, origins, dirs, jitter01, adj_rgb, adj_alpha, cfg, transforms24, grads,
-                         accumulate, nullptr);
+                         accumulate, nullptr, nullptr);
 }
 
 
@@ -1219,10 +1221,11 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     std::vector<CamDev> cd(static_cast<size_t>(n_cams));
     for (int32_t c = 0; c < n_cams; ++c) cd[size_t(c)] = make_cam(cams[c]);
     // one device block: cams | cam_index | pixel_id | pixel_xy | target | bg | o | d | jit |
-    // rgb | alpha | composited | resid | adj_rgb | adj_alpha | forward state | bad flag
+    // rgb | alpha | composited | resid | adj_rgb | adj_alpha | forward state | segment lists | bad flag
     const size_t cam_f = (sizeof(CamDev) * cd.size() + 15) / 16 * 4;
     DBuf<float> &buf = ctx->s_loss;
-    const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1 + 8) + 4;
+    const size_t n_seg = grads ? size_t(3 * kRaySegs) : 0;  // segment lists kept for the backward
+    const size_t total = cam_f + nn * (1 + 1 + 2 + 3 + 3 + 3 + 3 + 1 + 3 + 1 + 3 + 3 + 3 + 1 + 8 + n_seg) + 4;
     VP_CUDA(ctx, buf.ensure(total));
     float *p = buf.p;
     CamDev *d_cams = reinterpret_cast<CamDev *>(p);
@@ -1242,6 +1245,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     float *d_ar = p; p += 3 * nn;
     float *d_aa = p; p += nn;
     float *d_state = p; p += 8 * nn;  // forward MarchResult bookkeeping for the backward
+    float *d_segs = n_seg ? p : nullptr; p += n_seg * nn;
     int *d_bad = reinterpret_cast<int *>(p);
     VP_CUDA(ctx, cudaMemcpyAsync(d_cams, cd.data(), sizeof(CamDev) * cd.size(), cudaMemcpyHostToDevice, st));
     VP_CUDA(ctx, cudaMemcpyAsync(d_ci, cam_index, 4 * nn, cudaMemcpyDefault, st));
@@ -1261,6 +1265,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     const RaysDev rays{d_o, d_d, d_j};
     OutDev od{d_rgb, d_a, nullptr};
     od.state = d_state;
+    od.segs = d_segs;
     if (size_t(ctx->ovf_cap) < nn) {
         VP_CUDA(ctx, ctx->ovf_list.ensure(nn));
         ctx->ovf_cap = int(nn);
@@ -1300,7 +1305,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     if (loss_pho) *loss_pho = lambda_pho * invN * acc;
     if (!grads) return VP_OK;
     // backwardRay for every ray with the photometric adjoints (grad.cpp:240-248)
-    return backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate, d_state);
+    return backward_rays(ctx, n, d_o, d_d, d_j, d_ar, d_aa, cfg, transforms24, grads, accumulate, d_state, d_segs);
 }
 
 int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, uint64_t *out,

@@ -473,7 +473,7 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 // adjoint of its active primitives (the payload scatter and pose sums are atomics, as in the
 // per-thread walk); gTmin, the only sequential sum, is accumulated over the chunk's steps in
 // step order. Rays with more than kWarpListBwd segments take the per-thread path.
-constexpr int kWarpListBwd = 96;
+constexpr int kWarpListBwd = kRaySegs;
 constexpr int kWarpCandBwd = 256;
 // 3 CTAs/SM (168 registers, 16 B of spills) against 2 at the unbounded 230: the 65,536-ray
 // backward row 3.08 -> 2.78 ms (gpurun_out sweep, K6)
@@ -501,8 +501,20 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const int nh = warp_segment_list(cands, o, d, lane, s_cand[wid], s_ce[wid], s_cx[wid], kWarpCandBwd,
-                                         s_e[wid], s_x[wid], s_c[wid], kWarpListBwd);
+        // the forward of these rays may have kept the ray's segment list (count >= 0)
+        int nh = bd.fwd_segs ? __float_as_int(bd.fwd_state[8 * r + 7]) : -1;
+        if (nh >= 0) {
+            const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
+            for (int j = lane; j < nh; j += 32) {
+                s_e[wid][j] = sg[j];
+                s_x[wid][j] = sg[kRaySegs + j];
+                s_c[wid][j] = __float_as_int(sg[2 * kRaySegs + j]);
+            }
+            __syncwarp();
+        } else {
+            nh = warp_segment_list(cands, o, d, lane, s_cand[wid], s_ce[wid], s_cx[wid], kWarpCandBwd, s_e[wid],
+                                   s_x[wid], s_c[wid], kWarpListBwd);
+        }
         const int cnt = nh < 0 ? 0 : nh;
         if (nh < 0) {  // a long segment list: the per-thread walk with a global window
             if (lane == 0) {

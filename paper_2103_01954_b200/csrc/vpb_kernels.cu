@@ -632,7 +632,7 @@ k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 // sorted segment list through the BVH (warp_segment_list) in shared memory, then walks
 // it 32 lattice steps at a time (march_warp). Rays with more than kWarpList segments go to the
 // wide-window fallback like window overflows.
-constexpr int kWarpList = 96;   // segments per ray held by the warp
+constexpr int kWarpList = kRaySegs;  // segments per ray held by the warp
 constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp path gives up
 __global__ void __launch_bounds__(128)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
@@ -665,6 +665,15 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
         } else {
             ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane);
             if (lane == 0) write_ray(od, r, ro);
+            if (od.segs) {  // keep the list for the backward pass of the same rays
+                float *sg = od.segs + (size_t)r * (3 * kRaySegs);
+                for (int j = lane; j < cnt; j += 32) {
+                    sg[j] = s_e[wid][j];
+                    sg[kRaySegs + j] = s_x[wid][j];
+                    sg[2 * kRaySegs + j] = __int_as_float(s_c[wid][j]);
+                }
+                if (lane == 0) od.state[8 * r + 7] = __int_as_float(cnt);
+            }
         }
         add_counters(ctr, ro, lane == 0 && !ro.overflow);
         __syncwarp();

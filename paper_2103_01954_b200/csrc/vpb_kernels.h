@@ -52,6 +52,9 @@ struct OutDev {
     int *samples;
     unsigned long long *prof = nullptr;  // per CTA: tile, SM id, start ns, end ns (debug)
     float *state = nullptr;  // arbitrary rays: 8 floats per ray of MarchResult bookkeeping
+    // arbitrary rays, warp kernel: the ray's sorted segment list for a following backward,
+    // kRaySegs (E) | kRaySegs (X) | kRaySegs (primitive) per ray; count in state[7] (-1: none)
+    float *segs = nullptr;
     // Tile-major shard outputs (vp_render_shard_async): pixel (x, y) of owned tile t is
     // written at (t / shard_n) * 256 + (y % 16) * 16 + x % 16. 0 = the image layout.
     int shard_n = 0, width = 0, tiles_x = 0;
@@ -108,6 +111,7 @@ struct BwdDev {
     const float *adj_rgb;
     const float *adj_alpha;
     const float *fwd_state = nullptr;  // the forward's per-ray state (skips the replay), or null
+    const float *fwd_segs = nullptr;   // the forward's segment lists (OutDev::segs), or null
 };
 
 // Adam step constants (losses.cpp:70-104); bc1/bc2 = 1 - beta^step computed on the host.
@@ -116,6 +120,7 @@ struct AdamDev {
 };
 
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
+constexpr int kRaySegs = 96;  // segments per ray held by the warp-per-ray kernels
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
 // backwardRay: one-warp CTAs, 12 per SM (168 registers, no spills); the scratch

@@ -861,6 +861,7 @@ __device__ __forceinline__ void write_ray(const OutDev &od, int64_t p, const Ray
         s[4] = ro.sat_r;
         s[5] = ro.sat_g;
         s[6] = ro.sat_b;
+        s[7] = __int_as_float(-1);  // no stored segment list (the warp kernel overwrites it)
     }
 }
 
