@@ -56,3 +56,41 @@ def test_backward_accumulates_and_is_linear_in_the_adjoints(renderer):
     z = renderer.backward_rays(*args, np.zeros_like(g["adj_rgb"]), np.zeros_like(g["adj_alpha"]), cfg,
                                g["tr"], g["jit"])
     assert not z.any()
+
+
+def test_long_rays_take_the_overflow_paths(renderer, oracle):
+    """A column of 320 primitives along z. Rays near the axis cross every box: more than 256
+    BVH leaves (the warp walk's frontier / candidate cap) and more than 96 segments (the warp
+    kernels' list cap), so the forward re-marches them with global windows and the backward
+    takes the per-thread walk; tilted rays leave the column after a few to a few hundred
+    boxes and stay on the warp paths. Forward bit-exact, gradients within the reordering bound."""
+    k, m = 320, 4
+    rng = np.random.default_rng(7)
+    tr = np.zeros((k, 24), np.float32)
+    tr[:, 2] = 0.05 * np.arange(k)
+    tr[:, 3:12] = np.eye(3, dtype=np.float32).reshape(9)
+    tr[:, 12:15] = 0.03
+    pay = rng.uniform(0.0, 0.05, size=k * 4 * m ** 3).astype(np.float32)
+    win, cfg = api.WindowParams(), api.MarchConfig()
+    xf = api.compose(tr)
+    renderer.set_scene_composed(xf, api.PrimitiveSlab(k, m, pay), win)
+    n = 48
+    o = np.zeros((n, 3), np.float32)
+    o[:, :2] = rng.uniform(-0.02, 0.02, size=(n, 2))
+    o[:, 2] = -1.0
+    slope = np.where(np.arange(n) < 16, 0.0, rng.uniform(0.002, 0.05, size=n)).astype(np.float32)
+    d = np.stack([slope, np.zeros(n, np.float32), np.ones(n, np.float32)], 1)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rgb, alpha, samples = renderer.march_rays(o, d, cfg)
+    assert renderer.read_stats()["overflow_rays"] >= 16  # the axis rays took the fallback
+    rgb_o, alpha_o, samples_o = oracle.march_rays(xf, m, pay, win, o, d, cfg)
+    assert np.array_equal(samples, samples_o)
+    assert np.array_equal(rgb.view(np.uint32), rgb_o.view(np.uint32))
+    assert np.array_equal(alpha.view(np.uint32), alpha_o.view(np.uint32))
+    ar = rng.normal(size=(n, 3)).astype(np.float32)
+    aa = rng.normal(size=n).astype(np.float32)
+    got = renderer.backward_rays(o, d, ar, aa, cfg, tr)
+    want = oracle.backward_rays(tr, m, pay, win, o, d, ar, aa, cfg)
+    n_pay = k * 4 * m ** 3
+    _check_close("long.payload", got[:n_pay], want[:n_pay])
+    _check_close("long.pose", got[n_pay:], want[n_pay:])
