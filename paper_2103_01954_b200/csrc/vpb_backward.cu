@@ -220,6 +220,10 @@ struct FwdReplay {
 
 __device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }
 
+#ifndef VPB_BWD_WARP_AGG
+#define VPB_BWD_WARP_AGG 1  // warp-aggregated pose atomics at the end of each ray
+#endif
+
 // Step 3: the adjoint walk.
 template <class Cands>
 struct BwdWalk {
@@ -240,6 +244,38 @@ struct BwdWalk {
                        const FwdReplay<Cands> &f, const BwdDev &b, V3 dir, V3 ar, float aa)
         : cands(c), mp(m), tab(t), fwd(f), bd(b), d(dir), aRgb(ar), aAlpha(aa) {
         for (float &v : acc) v = 0.f;
+    }
+    // End of a warp-per-ray walk (all 32 lanes converged): lanes summing the same primitive
+    // are reduced with a masked butterfly, one group at a time, and the group's lowest lane
+    // issues the 9 pose atomics (warp-aggregated atomics).
+    __device__ void flush_warp(int lane) {
+#if VPB_BWD_WARP_AGG
+        unsigned left = __ballot_sync(0xffffffffu, cur >= 0);
+        while (left) {
+            const int lead = __ffs(left) - 1;
+            const int k = __shfl_sync(0xffffffffu, cur, lead);
+            const unsigned grp = __ballot_sync(0xffffffffu, cur == k);
+            const bool in = (grp >> lane) & 1u;
+            float v[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) v[q] = in ? acc[q] : 0.f;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int q = 0; q < 9; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+            if (lane == lead) {
+                float *g = bd.g_pose + 9 * (size_t)k;
+                for (int q = 0; q < 9; ++q)
+                    if (v[q] != 0.f) red_add(g + q, v[q]);
+            }
+            left &= ~grp;
+        }
+        cur = -1;
+        for (float &x : acc) x = 0.f;
+#else
+        (void)lane;
+        flush();
+#endif
     }
     __device__ void flush() {
         if (cur < 0) return;
@@ -632,7 +668,8 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
             base = skipTo > iL + 1 ? skipTo : iL + 1;
         }
         if (lane == 0) anchor_chain(bw, cands, bd, P[0], t0, gTmin, o, d);
-        bw.flush();
+        __syncwarp();
+        bw.flush_warp(lane);
         __syncwarp();
     }
 }
