@@ -80,6 +80,32 @@ __global__ void k_adam_check(const float *__restrict__ g, int64_t n, int *__rest
         if (!isfinite(g[i])) atomicExch(bad, 1);
 }
 
+// lr * (a / bc1) / (sqrt(b / bc2) + eps) (losses.cpp:88-90). Most parameters of a fit step
+// have zero moments (voxels no ray touched), and a zero dividend sends the IEEE division down
+// its slow path (FCHK flags it; ncu put half of the update's instructions there). A zero over a positive divisor is that zero with its sign, and sqrt(+-0) is
+// +-0, so returning the operand itself gives the same bits; NaN, infinite and non-positive
+// divisors still divide.
+// An opaque copy: the compiler may not replace it by an operand it knows to be discarded.
+__device__ __forceinline__ float opaque(float x) {
+    float y;
+    asm("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float adam_quot(float a, float b, float lr, const AdamDev &c) {
+    // The division runs speculatively under a select, so a zero operand is replaced by 1 (a
+    // fast-path division whose result is discarded) through an opaque copy.
+    const bool za = a == 0.0f && c.bc1 > 0.0f, zb = b == 0.0f && c.bc2 > 0.0f;
+    const float qa = opaque(za ? 1.0f : a) / c.bc1, qb = opaque(zb ? 1.0f : b) / c.bc2;
+    const float mHat = za ? a : qa, vHat = zb ? b : qb;
+    const bool zv = vHat == 0.0f;
+    const float rv = sqrtf(opaque(zv ? 1.0f : vHat));
+    const float root = zv ? vHat : rv;
+    const float num = lr * mHat, den = root + c.eps;
+    const bool zn = num == 0.0f && den > 0.0f;
+    const float q = opaque(zn ? 1.0f : num) / den;
+    return zn ? num : q;
+}
+
 // One Adam step over [payload (planar GradBuffer order) | 9K deltas] (losses.cpp:81-92). The
 // payload parameter with planar index (k, ch, v) lives at payload[k * m3 + v].ch
 // (channel-interleaved), so a thread takes one voxel: its float4 is read and written once,
@@ -91,9 +117,7 @@ __device__ __forceinline__ float adam_one(const float *__restrict__ g, float *__
     const float b = c.beta2 * m2[i] + (1.0f - c.beta2) * gi * gi;
     m1[i] = a;
     m2[i] = b;
-    const float mHat = a / c.bc1;
-    const float vHat = b / c.bc2;
-    return lr * mHat / (sqrtf(vHat) + c.eps);
+    return adam_quot(a, b, lr, c);
 }
 
 __global__ void k_adam_update(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
@@ -132,9 +156,7 @@ __device__ __forceinline__ float adam_elem(float gi, float &m1, float &m2, float
     const float b = c.beta2 * m2 + (1.0f - c.beta2) * gi * gi;
     m1 = a;
     m2 = b;
-    const float mHat = a / c.bc1;
-    const float vHat = b / c.bc2;
-    return lr * mHat / (sqrtf(vHat) + c.eps);
+    return adam_quot(a, b, lr, c);
 }
 
 __global__ void __launch_bounds__(256)
