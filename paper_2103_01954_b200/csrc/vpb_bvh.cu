@@ -209,7 +209,7 @@ static BvhScratch bvh_layout(int n, void *base) {
     s.parent = static_cast<int *>(take((size_t)(2 * n) * 4));
     s.flags = static_cast<unsigned *>(take((size_t)n * 4));
     s.bounds = static_cast<float *>(take(64));
-    cub::DeviceRadixSort::SortKeys(nullptr, s.cub_bytes, s.k0, s.k1, n, 0, 62);
+    cub::DeviceRadixSort::SortKeys(nullptr, s.cub_bytes, s.k0, s.k1, n, 32, 62);
     s.cub_tmp = take(s.cub_bytes);
     s.total = off;
     return s;
@@ -233,7 +233,10 @@ cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scr
     k_bvh_boxes<<<b, 256, 0, st>>>(xf16, n, lo, hi);
     k_bvh_bounds<<<1, 1024, 0, st>>>(xf16, n, bounds);
     k_bvh_keys<<<b, 256, 0, st>>>(xf16, n, bounds, k0);
-    cudaError_t e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, k0, k1, n, 0, 62, st);
+    // Only the 30 Morton bits are sorted: the keys start in primitive order and the radix sort
+    // is stable, so equal codes stay in index order, which is the full 62-bit key order
+    // (4 digit passes instead of 8).
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, k0, k1, n, 32, 62, st);
     if (e != cudaSuccess) return e;
     k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(k1, n, nodes, parent);
     cudaMemsetAsync(flags, 0, (size_t)n * 4, st);
