@@ -11,3 +11,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ma
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bw_launches.csv python bench_rows.py --rows backward --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bw_launches.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_backward_rays_warp -s 1 -c 1 -o gpurun_out/bw_full python bench_rows.py --rows backward --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bw_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_march_rays_warp -s 1 -c 1 -o gpurun_out/fw_full python bench_rows.py --rows backward --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/fw_full.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fit_launches.csv python bench_rows.py --rows fit --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/fit_launches.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_adam_update4 -s 1 -c 1 -o gpurun_out/adam_full python bench_rows.py --rows fit --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/adam_full.log 2>&1
