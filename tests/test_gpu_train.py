@@ -103,6 +103,45 @@ def test_adam_payload_update_both_access_widths(renderer, m):
     assert np.allclose(got, want, rtol=5e-7, atol=1e-7), np.abs(got - want).max()
 
 
+@pytest.mark.parametrize("m", [3, 4])
+def test_adam_sparse_gradients_are_bit_exact(renderer, m):
+    """Sparse gradients as a fit step produces them (most voxels untouched: zero moments), with
+    signed zeros and subnormals: the update divides zeros off the IEEE slow path and must still
+    give the bits of the plain division. beta1 = 0.5 and beta2 = 0.75 make 1 - beta^step exact,
+    so the float32 numpy restatement (one rounding per operation) is compared bit for bit."""
+    k = 5
+    rng = np.random.default_rng(100 + m)
+    tr, _ = synthetic.shell_arrays(k, 2)
+    tr = np.ascontiguousarray(tr, np.float32)
+    pay = rng.uniform(0.0, 1.0, k * 4 * m ** 3).astype(np.float32)
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, pay), api.WindowParams())
+    renderer._lib.vp_adam_reset(renderer.ctx)
+    cfg = api.AdamConfig(lr=3e-2, beta1=0.5, beta2=0.75, eps=1e-8, lr_delta_scale=0.0)
+    f = np.float32
+    n_pay = pay.size
+    m1 = np.zeros(n_pay, f)
+    m2 = np.zeros(n_pay, f)
+    want = pay.copy()
+    b1, b2, lr, eps = f(cfg.beta1), f(cfg.beta2), f(cfg.lr), f(cfg.eps)
+    for step in range(1, 4):
+        g = np.zeros(api.grad_size(k, m), np.float32)
+        u = rng.uniform(size=n_pay)
+        g[:n_pay] = np.where(u < 0.1, rng.standard_normal(n_pay).astype(f), g[:n_pay])
+        g[:n_pay] = np.where((u >= 0.1) & (u < 0.15), f(-0.0), g[:n_pay])
+        g[:n_pay] = np.where((u >= 0.15) & (u < 0.2), f(1e-40) * np.sign(rng.standard_normal(n_pay)).astype(f),
+                             g[:n_pay])
+        api.adam_step(renderer, cfg, g, tr)
+        gp = g[:n_pay]
+        with np.errstate(under="ignore"):
+            m1 = b1 * m1 + (f(1) - b1) * gp
+            m2 = b2 * m2 + (f(1) - b2) * gp * gp
+            bc1 = f(1) - b1 ** step
+            bc2 = f(1) - b2 ** step
+            want = want - (lr * (m1 / bc1)) / (np.sqrt(m2 / bc2) + eps)
+        want = np.where(want < 0, f(0), want).astype(np.float32)
+    assert np.array_equal(bits(api.payload_planar(renderer)), bits(want))
+
+
 def _write_vpsl(path, k, m, payload, version=1, magic=b"VPSL", truncate=0):
     """README.md:96-104: magic, u32 version, u32 K, u32 M, f32 payload (little-endian)."""
     data = magic + np.array([version, k, m], "<u4").tobytes() + np.asarray(payload, "<f4").tobytes()
