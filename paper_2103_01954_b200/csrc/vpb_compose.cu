@@ -204,9 +204,10 @@ cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_
 // One primitive: [optional: deltas from Adam + the scale projection] then compose.
 // tr24: tBase[3] rBase[9] sBase[3] deltaT[3] deltaR[3] deltaS[3].
 __global__ void k_compose(float *__restrict__ tr24, const float *__restrict__ deltas, int n_prim,
-                          float *__restrict__ xf16, int *__restrict__ bad) {
+                          float *__restrict__ xf16, int *__restrict__ bad, const int *__restrict__ skip) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_prim) return;
+    if (skip && *skip) return;  // adamStep found a non-finite gradient: nothing is touched
     float t[24];
 #pragma unroll
     for (int i = 0; i < 24; ++i) t[i] = tr24[(size_t)k * 24 + i];
@@ -252,9 +253,10 @@ __global__ void k_sincos(const float *__restrict__ x, float *__restrict__ y, int
         y[i] = sincosf_glibc(x[i], want_cos != 0);
 }
 
-cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st) {
+cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st,
+                           const int *skip) {
     if (n_prim <= 0) return cudaSuccess;
-    k_compose<<<(n_prim + 127) / 128, 128, 0, st>>>(tr24, deltas, n_prim, xf16, bad);
+    k_compose<<<(n_prim + 127) / 128, 128, 0, st>>>(tr24, deltas, n_prim, xf16, bad, skip);
     return cudaGetLastError();
 }
 

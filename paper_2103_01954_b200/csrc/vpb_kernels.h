@@ -175,9 +175,13 @@ cudaError_t launch_loss_adjoints(const float *rgb, const float *alpha, const flo
                                  float *adj_alpha, cudaStream_t st);
 cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, float *deltas, int64_t n_pay,
                         int64_t n, unsigned m3, const AdamDev &c, int *bad, bool check, cudaStream_t st);
+// check: k_adam_check sets *bad on a non-finite gradient. Otherwise the update, which reads *bad
+// (non-null) first and returns without writing when it is set.
 cudaError_t launch_expf(const float *x, float *y, int64_t n, cudaStream_t st);
 // vpb_compose.cu: Frame::composed() on the device (+ Adam's delta write-back and projection)
-cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st);
+// skip (nullable, device): when *skip != 0 the kernel returns without touching anything
+cudaError_t launch_compose(float *tr24, const float *deltas, int n_prim, float *xf16, int *bad, cudaStream_t st,
+                           const int *skip = nullptr);
 cudaError_t launch_gather_deltas(const float *tr24, int n_prim, float *deltas, cudaStream_t st);
 cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_t st);
 // vpb_bvh.cu: BVH build over the resident transforms (n - 1 nodes)

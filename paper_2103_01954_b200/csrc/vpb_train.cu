@@ -122,7 +122,8 @@ __device__ __forceinline__ float adam_one(const float *__restrict__ g, float *__
 
 __global__ void k_adam_update(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
                               float4 *__restrict__ payload, float *__restrict__ deltas, int64_t n_pay,
-                              int64_t n, unsigned m3, AdamDev c) {
+                              int64_t n, unsigned m3, AdamDev c, const int *__restrict__ skip) {
+    if (*skip) return;  // the check pass found a non-finite gradient (losses.cpp:74-75)
     const int64_t n_vox = n_pay / 4, total = n_vox + (n - n_pay);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         if (q < n_vox) {
@@ -162,7 +163,8 @@ __device__ __forceinline__ float adam_elem(float gi, float &m1, float &m2, float
 __global__ void __launch_bounds__(256)
 k_adam_update4(const float *__restrict__ g, float *__restrict__ m1, float *__restrict__ m2,
                float4 *__restrict__ payload, float *__restrict__ deltas, int64_t n_pay, int64_t n, unsigned m3,
-               AdamDev c) {
+               AdamDev c, const int *__restrict__ skip) {
+    if (*skip) return;  // the check pass found a non-finite gradient (losses.cpp:74-75)
     const int64_t q4 = m3 / 4, n_quads = n_pay / 16, total = n_quads + (n - n_pay);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         if (q < n_quads) {
@@ -224,9 +226,9 @@ cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, f
     } else if (m3 % 4 == 0) {
         const int64_t items = n_pay / 16 + (n - n_pay);
         const unsigned b4 = (unsigned)((items + 255) / 256 < 148 * 8 ? (items + 255) / 256 : 148 * 8);
-        k_adam_update4<<<b4, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c);
+        k_adam_update4<<<b4, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c, bad);
     } else {
-        k_adam_update<<<blocks, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c);
+        k_adam_update<<<blocks, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c, bad);
     }
     return cudaGetLastError();
 }
