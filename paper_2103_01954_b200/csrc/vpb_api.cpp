@@ -1220,6 +1220,19 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     const size_t nn = size_t(n);
     std::vector<CamDev> cd(static_cast<size_t>(n_cams));
     for (int32_t c = 0; c < n_cams; ++c) cd[size_t(c)] = make_cam(cams[c]);
+    // Host-resident pixel sets are range-checked here (the comparisons k_eval_rays makes), so
+    // the device flag needs no round trip before the march; device-resident ones are checked
+    // by k_eval_rays and read back below.
+    const bool host_check = !is_device_ptr(cam_index) && !is_device_ptr(pixel_xy);
+    if (host_check) {
+        for (size_t i = 0; i < nn; ++i) {
+            const int ci = cam_index[i];
+            if (ci < 0 || ci >= n_cams) return fail(ctx, VP_ERR_USAGE, "camera index out of range");
+            const float px = pixel_xy[2 * i], py = pixel_xy[2 * i + 1];
+            if (px < 0.0f || py < 0.0f || px > float(cd[size_t(ci)].width) || py > float(cd[size_t(ci)].height))
+                return fail(ctx, VP_ERR_USAGE, "pixel outside image bounds");  // camera.cpp:15-16
+        }
+    }
     // one device block: cams | cam_index | pixel_id | pixel_xy | target | bg | o | d | jit |
     // rgb | alpha | composited | resid | adj_rgb | adj_alpha | forward state | segment lists | bad flag
     const size_t cam_f = (sizeof(CamDev) * cd.size() + 15) / 16 * 4;
@@ -1257,8 +1270,10 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     VP_CUDA(ctx, launch_eval_rays(d_cams, n_cams, d_ci, d_xy, d_pid, n, cfg->jitter, cfg->seed, d_o, d_d, d_j,
                                   d_bad, st));
     int h_bad = 0;
-    VP_CUDA(ctx, cudaMemcpyAsync(&h_bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
-    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    if (!host_check) {
+        VP_CUDA(ctx, cudaMemcpyAsync(&h_bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+        VP_CUDA(ctx, cudaStreamSynchronize(st));
+    }
     if (h_bad == 1) return fail(ctx, VP_ERR_USAGE, "camera index out of range");
     if (h_bad == 2) return fail(ctx, VP_ERR_USAGE, "pixel outside image bounds");  // camera.cpp:15-16
     // forward march of the batch (evalLoss, grad.cpp:216-226)
@@ -1416,46 +1431,48 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
         VP_CUDA(ctx, cudaMemsetAsync(ctx->adam_m2.p, 0, 4 * n, st));
         ctx->adam_step = 0;
     }
-    DBuf<float> &tmp = ctx->s_adam;  // [grads (if host) | deltas | bad flag]
-    VP_CUDA(ctx, tmp.ensure(n + 9 * size_t(k) + 1));
+    DBuf<float> &tmp = ctx->s_adam;  // [grads (if host) | deltas | flags: non-finite gradient, bad scale]
+    VP_CUDA(ctx, tmp.ensure(n + 9 * size_t(k) + 2));
     const float *dg = grads;
     if (!is_device_ptr(grads)) {
         VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, grads, 4 * n, cudaMemcpyHostToDevice, st));
         dg = tmp.p;
     }
     float *d_delta = tmp.p + n;
-    int *d_bad = reinterpret_cast<int *>(tmp.p + n + 9 * size_t(k));
+    int *d_bad = reinterpret_cast<int *>(tmp.p + n + 9 * size_t(k));  // [0] gradient, [1] scale
     // the caller's records are authoritative: resident copy, then the deltas in Adam's order
     VP_CUDA(ctx, ctx->tr24.ensure(24 * size_t(k)));
     VP_CUDA(ctx, cudaMemcpyAsync(ctx->tr24.p, transforms24, 4 * 24 * size_t(k),
                                  is_device_ptr(transforms24) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     VP_CUDA(ctx, launch_gather_deltas(ctx->tr24.p, k, d_delta, st));
-    VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, st));
+    VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 8, st));
     AdamDev c{cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->lr_delta_scale, 0.f, 0.f};
     VP_CUDA(ctx, launch_adam(dg, nullptr, nullptr, nullptr, nullptr, int64_t(n_pay), int64_t(n), unsigned(m3), c,
                              d_bad, true, st));
-    int bad = 0;
-    VP_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
-    VP_CUDA(ctx, cudaStreamSynchronize(st));
-    if (bad) return fail(ctx, VP_ERR_NUMERIC, "non-finite gradient");  // losses.cpp:74-75
-    ctx->adam_step += 1;
-    c.bc1 = 1 - std::pow(cfg->beta1, float(ctx->adam_step));  // losses.cpp:79-80
-    c.bc2 = 1 - std::pow(cfg->beta2, float(ctx->adam_step));
+    // No host round trip between the check and the update: the update and the compose read the
+    // check's flag on the device and touch nothing when it is set, so a non-finite gradient
+    // still leaves every parameter, moment and the step count as they were (losses.cpp:74-75).
+    const int step = ctx->adam_step + 1;
+    c.bc1 = 1 - std::pow(cfg->beta1, float(step));  // losses.cpp:79-80
+    c.bc2 = 1 - std::pow(cfg->beta2, float(step));
     VP_CUDA(ctx, launch_adam(dg, ctx->adam_m1.p, ctx->adam_m2.p, ctx->payload.p, d_delta, int64_t(n_pay),
                              int64_t(n), unsigned(m3), c, d_bad, false, st));
     // deltas back into the records with the scale projection (losses.cpp:97-103), then the
     // frame is recomposed on the device (primitive.cpp:41-49)
     VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(16 * size_t(k)));
-    VP_CUDA(ctx, launch_compose(ctx->tr24.p, d_delta, k, ctx->xfb[ctx->xfi].p, d_bad, st));
+    VP_CUDA(ctx, launch_compose(ctx->tr24.p, d_delta, k, ctx->xfb[ctx->xfi].p, d_bad + 1, st, d_bad));
     if ((const void *)transforms24 != (const void *)ctx->tr24.p)
         VP_CUDA(ctx, cudaMemcpyAsync(transforms24, ctx->tr24.p, 4 * 24 * size_t(k),
                                      is_device_ptr(transforms24) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                      st));
-    VP_CUDA(ctx, cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+    int bad[2] = {0, 0};
+    VP_CUDA(ctx, cudaMemcpyAsync(bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
-    ctx->has_xf = !bad;
+    if (bad[0]) return fail(ctx, VP_ERR_NUMERIC, "non-finite gradient");  // losses.cpp:74-75
+    ctx->adam_step = step;
+    ctx->has_xf = !bad[1];
     ctx->bvh_dirty = true;
-    if (bad) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
+    if (bad[1]) return fail(ctx, VP_ERR_USAGE, "non-positive composed primitive scale");
     return VP_OK;
 }
 

@@ -65,6 +65,25 @@ def test_adam_step_matches_reference(renderer):
         api.adam_step(renderer, cfg, bad, tr)
     assert e.value.category == api.ErrorCategory.NUMERIC
     assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))  # nothing updated
+    assert np.array_equal(bits(api.payload_planar(renderer)), bits(z["adam_pay_out"]))
+    bad_delta = z["adam_grads"][1].copy()
+    bad_delta[-3] = np.inf  # a pose-delta gradient (the tail of [payload | deltas])
+    with pytest.raises(api.Error) as e:
+        api.adam_step(renderer, cfg, bad_delta, tr)
+    assert e.value.category == api.ErrorCategory.NUMERIC
+    assert np.array_equal(bits(tr), bits(z["adam_tr_out"]))
+    assert np.array_equal(bits(api.payload_planar(renderer)), bits(z["adam_pay_out"]))
+    # moments and the step count survived the rejected steps: one more step lands where the
+    # same step does after an uninterrupted run
+    api.adam_step(renderer, cfg, z["adam_grads"][0], tr)
+    got_tr, got_pay = bits(tr).copy(), bits(api.payload_planar(renderer)).copy()
+    tr2 = np.ascontiguousarray(z["adam_tr_in"], np.float32).copy()
+    renderer.set_scene_composed(api.compose(tr2), api.PrimitiveSlab(k, m, z["adam_pay_in"]), api.WindowParams())
+    renderer._lib.vp_adam_reset(renderer.ctx)
+    for g in list(z["adam_grads"]) + [z["adam_grads"][0]]:
+        api.adam_step(renderer, cfg, g, tr2)
+    assert np.array_equal(got_tr, bits(tr2))
+    assert np.array_equal(got_pay, bits(api.payload_planar(renderer)))
 
 
 @pytest.mark.parametrize("m", [3, 4, 5, 8])
@@ -259,3 +278,56 @@ def test_device_sincos_is_glibc_exact(renderer, oracle, cos):
     got, want = renderer.debug_sincos(x, cos), oracle.sincos_libm(x, cos)
     bad += int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
     assert bad == 0
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+@pytest.mark.parametrize("kind", ["pixel", "camera"])
+def test_eval_loss_pixel_set_errors(renderer, on_device, kind):
+    """evalLoss's pixel-set errors (camera.cpp:15-16, a camera index outside the list) are
+    Usage errors whether the pixel set is host-resident (checked on the host before any launch)
+    or device-resident (checked by k_eval_rays and read back before the march)."""
+    import ctypes as C
+    import torch
+    from paper_2103_01954_b200 import _lib
+
+    z = _z()
+    tr, pay = synthetic.shell_arrays(64, 8)
+    scene = api.Scene(api.WindowParams(8.0, 8), frames=[api.Frame(z["tr"], api.PrimitiveSlab(64, 8, pay))])
+    renderer.set_frame(scene, 0)
+    cams = [api.Camera(c[:9].reshape(3, 3), c[9:18].reshape(3, 3), c[18:21], int(c[21]), int(c[22]))
+            for c in z["cams"]]
+    n = int(z["cam_index"].size)
+    ci = np.ascontiguousarray(z["cam_index"], np.int32).copy()
+    xy = np.ascontiguousarray(z["pixel"], np.float32).reshape(n, 2).copy()
+    if kind == "pixel":
+        xy[n // 2, 0] = float(cams[int(ci[n // 2])].width) + 0.5
+    else:
+        ci[n // 3] = len(cams)
+    pid = np.ascontiguousarray(z["pixel_id"], np.int32)
+    tg = np.ascontiguousarray(z["target"], np.float32)
+    bg = np.ascontiguousarray(z["background"], np.float32)
+    arrays = [ci, xy, pid, tg, bg]
+    if on_device:
+        keep = [torch.from_numpy(a).cuda() for a in arrays]
+        ptrs = [C.c_void_p(t.data_ptr()) for t in keep]
+    else:
+        ptrs = [a.ctypes.data_as(C.c_void_p) for a in arrays]
+    lib = _lib.load()
+    cams_c = (_lib.vp_camera * len(cams))(*[c.to_c() for c in cams])
+    c = z["cfg"]
+    cfg = api.MarchConfig(float(np.float32(c[0])), float(np.float32(c[1])), bool(c[2]), int(c[3]))
+    mc = cfg.to_c()
+    lp = C.c_float()
+    trf = np.ascontiguousarray(z["tr"], np.float32).reshape(-1, 24)
+    rc = lib.vp_eval_loss_pho(renderer.ctx, len(cams), cams_c, n, C.cast(ptrs[0], C.POINTER(C.c_int32)),
+                              C.cast(ptrs[1], C.POINTER(C.c_float)), C.cast(ptrs[2], C.POINTER(C.c_int32)),
+                              C.cast(ptrs[3], C.POINTER(C.c_float)), C.cast(ptrs[4], C.POINTER(C.c_float)),
+                              1.0, C.byref(mc), trf.ctypes.data_as(C.POINTER(C.c_float)), C.byref(lp),
+                              None, None, 0)
+    assert rc == int(api.ErrorCategory.USAGE)
+    # the context is still usable: the valid set goes through
+    good = api.RaySamples(z["cam_index"], z["pixel"], z["pixel_id"], z["target"], z["background"])
+    w = z["weights"]
+    terms = api.eval_loss(renderer, scene, 0, cams, good,
+                          api.LossWeights(float(w[0]), float(w[1]), float(w[2]), float(w[3])), cfg)
+    assert np.float32(terms.pho) == np.float32(z["terms"][0])
