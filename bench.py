@@ -58,7 +58,12 @@ def parse():
                    help="one raymarch launch per view instead of one per step (vp_render_batch_async)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-one-core", type=int, default=1, help="also time one view pinned to one core")
+    p.add_argument("--ref-budget", type=float, default=200.0,
+                   help="--impl reference: cap on the timed steps' seconds (steps actually run are reported)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sweep", action="store_true", help="skip configs 1, 2, 4 (the 'sweep' key)")
+    p.add_argument("--sweep-steps", type=int, default=10)
     p.add_argument("--quick", action="store_true", help="profiling mode: no baseline / e2e")
     p.add_argument("--tile-shard", action="store_true",
                    help="single-view mode: each step renders ONE view (the headline camera), rank r "
@@ -117,27 +122,43 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class CpuReference:
     """The unmodified reference volprim::render (oracle/_ref/libvolprim_ref.so) on this host's
-    cores (std::thread x hardware_concurrency, threads.h:16-36); the C restatement when the
-    reference core was not built ("port")."""
+    cores (std::thread x hardware_concurrency, threads.h:16-36), on a resident reference Scene
+    built once by the reference-side generator (vpref_scene_new_shell): each render() call times
+    volprim::render (march.cpp:95-132) alone. Nothing from the product package (libvpb.so) is
+    loaded."""
 
     def __init__(self, k, m, width):
-        from oracle.bindings import Oracle, RefCore
-        from paper_2103_01954_b200 import api, synthetic
+        from oracle import bindings as B
         self.k, self.m, self.width = k, m, width
-        self.tr, self.pay = synthetic.shell_arrays(k, m)
-        self.win, self.cfg = api.WindowParams(), api.MarchConfig()
-        self.synthetic = synthetic
-        if RefCore.available():
-            self.core, self.kind, self.xf = RefCore(), "reference", self.tr
-        else:
-            self.core, self.kind, self.xf = Oracle(), "port", api.compose(self.tr)
-        self.cores = os.cpu_count() or 1
+        self.cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        if B.RefCore.available():
+            self.kind = "reference"
+            self.core = B.RefCore()
+            self.scene = B.RefScene(self.core, k, m)
+            self.cam = lambda v: B.ref_shell_camera(self.core, v, N_RING, width)
+        else:  # the reference core is built in this container and travels with the snapshot
+            raise RuntimeError("oracle/_ref/libvolprim_ref.so missing: build it with make -C oracle ref")
 
     def render(self, view):
-        cam = self.synthetic.shell_camera(view, N_RING, self.width)
-        return int(self.core.render(self.xf, self.m, self.pay, self.win, cam, self.cfg)[2].sum())
+        k9, r9, t3 = self.cam(view)
+        return int(self.scene.render(k9, r9, t3, self.width, self.width))
 
     def sample(self, views, budget_s):
         """(ray-samples, seconds, n_views) for views rendered until budget_s is spent."""
@@ -149,33 +170,149 @@ class CpuReference:
                 break
         return total, time.perf_counter() - t0, n
 
+    def sample_one_core(self, view):
+        """One view with the process pinned to one core (the survey's `taskset -c 0` run): the
+        reference's worker threads inherit the calling thread's affinity."""
+        if not hasattr(os, "sched_setaffinity"):
+            return None
+        old = os.sched_getaffinity(0)
+        core = min(old)
+        os.sched_setaffinity(0, {core})
+        try:
+            t0 = time.perf_counter()
+            s = self.render(view)
+            return s, time.perf_counter() - t0, core
+        finally:
+            os.sched_setaffinity(0, old)
 
-def run_reference(args, rank):
-    """--impl reference: the reference's own CPU renderer, rank 0 only."""
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU renderer on rank 0 (other ranks exit). A step
+    renders the same number of views as one GPU of our arm (--views-per-gpu, default 8) at the
+    same K, M and image size; at N = 1 those are the very views our arm renders (0..7 of the
+    ring), at N > 1 the steps walk through the views of all N ranks in turn (a bounded sample of
+    the whole job). The run is capped at --ref-budget seconds of timed steps."""
     if rank != 0:
         return
-    views = [i % N_RING for i in range(args.warmup + args.steps)]
-    step_s, step_samples = [], []
     ref = CpuReference(args.k, args.m, args.width)
-    kind, cores = ref.kind, ref.cores
-    for i, v in enumerate(views):
-        s, dt, _ = ref.sample([v], 1e9)
-        if i >= args.warmup:
-            step_s.append(dt)
-            step_samples.append(s)
+    V = args.views_per_gpu
+    all_views = [v % N_RING for v in range(V * max(world, 1))]
+    ring = [all_views[i % len(all_views)] for i in range(V * (args.warmup + args.steps))]
+    steps = [ring[i * V:(i + 1) * V] for i in range(args.warmup + args.steps)]
+    for vs in steps[:args.warmup]:
+        for v in vs:
+            ref.render(v)
+    step_s, step_samples = [], []
+    t_start = time.perf_counter()
+    for vs in steps[args.warmup:]:
+        t0 = time.perf_counter()
+        n = sum(ref.render(v) for v in vs)
+        step_s.append(time.perf_counter() - t0)
+        step_samples.append(n)
+        if time.perf_counter() - t_start > args.ref_budget:
+            break
     t = sum(step_s)
+    done = len(step_s)
     value = sum(step_samples) / t / 1e6
+    views_timed = sorted({v for vs in steps[args.warmup:args.warmup + done] for v in vs})
+    sample = (f"{done} steps x {V} views ({'views ' + str(views_timed[0]) + '..' + str(views_timed[-1])}"
+              f" of the 64-view ring), full {args.width}x{args.width} frames, resident reference Scene, "
+              f"volprim::render with std::thread x hardware_concurrency on {cpu_model()}")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": METRIC,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+            "n_gpus": world, "steps": done, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t / done, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(args, 1, False) | {"views_per_step": 1},
-            "frames_per_s": round(args.steps / t, 4),
-            "cpu_baseline": {"value": round(value, 3), "unit": METRIC, "cores": cores, "kind": kind,
-                             "sample": f"1 view of the 64-view ring per step, {args.steps} steps "
-                                       f"(reference volprim::render, std::thread x hardware_concurrency)"},
+            "config": workload_config(args, world, world > 1),
+            "frames_per_s": round(done * V / t, 4),
+            "cpu_baseline": {"value": round(value, 3), "unit": METRIC, "cores": ref.cores, "kind": ref.kind,
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": round(value, 3), "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if done < args.steps:
+        line["steps_requested"] = args.steps
     print(json.dumps(line), flush=True)
+
+
+SWEEP_CONFIGS = {"oracle_64x16_256": (1, 64, 16, 256), "k512_m32_1024": (2, 512, 32, 1024),
+                 "k32768_m8_1024": (4, 32768, 8, 1024)}
+
+
+def run_sweep(r, args, device, flush, hbm):
+    """BASELINE.json's "K x voxel^3 sweep": configs 1, 2 and 4 measured in the same run as the
+    headline (config 3), on the same box. Per config: ring views 0..7 in ONE raymarch launch
+    (vp_render_batch_async into device buffers), bit-checked against the reference digests of
+    those views (tests/golden/digests.json "ring_configs", oracle/gen_ring_digests.py), then
+    `sweep_steps` timed launches after 3 warm-ups, L2 flushed before each (CUDA events on the
+    launching stream for the step; the library's own events for the raymarch kernel)."""
+    import hashlib
+    import torch
+    import ctypes as C
+    from paper_2103_01954_b200 import api, synthetic
+    from paper_2103_01954_b200._lib import f32p, i32p, vp_camera
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+    golden = json.loads((ROOT / "tests" / "golden" / "digests.json").read_text()).get("ring_configs", {})
+    lib = r._lib
+    stream = torch.cuda.current_stream(device)
+    out = {}
+    for name, (cfg_no, k, m, w) in SWEEP_CONFIGS.items():
+        tr, pay = synthetic.shell_arrays(k, m)
+        r.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, pay), api.WindowParams())
+        del pay
+        cams = [synthetic.shell_camera(v, N_RING, w) for v in range(8)]
+        mc = api.MarchConfig()
+        host = r.render_batch(cams, mc)  # also sets the raymarch tier for this density
+        g = golden.get(name, {}).get("views", {})
+        digest_ok = bool(g) and all(
+            sha(o.color) == g[str(v)]["rgb"] and sha(o.alpha) == g[str(v)]["alpha"]
+            and sha(o.sample_counts) == g[str(v)]["samples"] for v, o in enumerate(host))
+        ray_samples = sum(o.total_samples() for o in host)
+        prim = 0
+        for c in cams:  # per-view device counters (deterministic)
+            prim += r.render(c, mc).stats["prim_samples"]
+        n_px = w * w
+        bufs = [(torch.empty(n_px * 3, device=device), torch.empty(n_px, device=device),
+                 torch.empty(n_px, dtype=torch.int32, device=device)) for _ in range(8)]
+        cc = (vp_camera * 8)(*[c.to_c() for c in cams])
+        mcc = mc.to_c()
+        rgb = (f32p * 8)(*[C.cast(b[0].data_ptr(), f32p) for b in bufs])
+        alp = (f32p * 8)(*[C.cast(b[1].data_ptr(), f32p) for b in bufs])
+        smp = (i32p * 8)(*[C.cast(b[2].data_ptr(), i32p) for b in bufs])
+
+        def launch():
+            if lib.vp_render_batch_async(r.ctx, 8, cc, C.byref(mcc), rgb, alp, smp, C.c_void_p(stream.cuda_stream)):
+                raise RuntimeError(lib.vp_last_error(r.ctx).decode())
+
+        for _ in range(3):
+            launch()
+        torch.cuda.synchronize()
+        r.kernel_times()
+        evs = []
+        for i in range(args.sweep_steps):
+            flush.fill_(i & 0xff)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launch()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        kms = r.kernel_times(4096)
+        step_s = sum(a.elapsed_time(b) for a, b in evs) / 1e3
+        kernel_s = float(np.mean(kms)) / 1e3
+        alg = BYTES_PER_PRIM_SAMPLE * prim + BYTES_PER_PIXEL * n_px * 8
+        out[name] = {"baseline_config": cfg_no, "K": k, "M": m, "width": w, "views_per_launch": 8,
+                     "views": "ring 0..7", "value": round(ray_samples * args.sweep_steps / step_s / 1e6, 3),
+                     "unit": METRIC, "frames_per_s": round(8 * args.sweep_steps / step_s, 2),
+                     "ms_per_launch_step": round(1e3 * step_s / args.sweep_steps, 4),
+                     "kernel_ms_per_launch": round(kernel_s * 1e3, 4),
+                     "prim_samples_per_launch": int(prim), "ray_samples_per_launch": int(ray_samples),
+                     "roofline_frac": round(alg / kernel_s / 1e9 / hbm, 4),
+                     "achieved_gbs": round(alg / kernel_s / 1e9, 1),
+                     "digest_ok": digest_ok, "steps": args.sweep_steps}
+        del bufs
+        torch.cuda.synchronize()
+    return out
 
 
 def workload_config(args, world, gather):
@@ -292,7 +429,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
 
     import torch
@@ -338,9 +475,14 @@ def main():
 
     # deterministic per-view counts (bit-exact renders), measured once outside the timed region
     per_view = []
-    for cam in cams:
+    ring_golden = json.loads((ROOT / "tests" / "golden" / "digests.json").read_text()).get("ring", {})
+    digest_ok = (ring_golden.get("K"), ring_golden.get("M"), ring_golden.get("W")) == (k, m, w)
+    for v, cam in zip(views, cams):
         out = r.render(api.Camera.from_c(cam), cfg)
         per_view.append(out.stats)
+        g = ring_golden.get("views", {}).get(str(v)) if digest_ok else None
+        digest_ok = bool(g) and digest_ok and all(
+            _sha(a) == g[key] for a, key in ((out.color, "rgb"), (out.alpha, "alpha"), (out.sample_counts, "samples")))
     ray_samples = sum(s["ray_samples"] for s in per_view)
     prim_samples = sum(s["prim_samples"] for s in per_view)
 
@@ -537,12 +679,23 @@ def main():
                "steps": n_e2e, "api": ("vp_set_transforms_async + vp_render_batch_async" if batch else "vp_set_transforms + vp_render_async")
                       + " into pinned host outputs, vp_sync at the end"}
 
+    sweep = None
+    if world == 1 and not (args.no_sweep or args.quick):
+        sweep = run_sweep(r, args, device, flush, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
         ref = CpuReference(k, m, w)
         s, dt, nv = ref.sample(views, args.cpu_seconds)
         cpu = {"value": round(s / dt / 1e6, 3), "unit": METRIC, "cores": ref.cores, "kind": ref.kind,
-               "sample": f"{nv} view(s) of this rank's views, full {w}x{w} frames, {dt:.1f} s"}
+               "cpu_model": cpu_model(),
+               "sample": f"{nv} view(s) of this rank's views, full {w}x{w} frames, {dt:.1f} s, resident "
+                         f"reference Scene (volprim::render only)"}
+        one = ref.sample_one_core(views[0]) if args.cpu_one_core else None
+        if one:
+            cpu["one_core"] = {"value": round(one[0] / one[1] / 1e6, 3), "unit": METRIC, "cores": 1,
+                               "core_id": one[2], "seconds": round(one[1], 2),
+                               "sample": f"view {views[0]}, process pinned to one core (taskset -c equivalent)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": METRIC, "n_gpus": world,
@@ -551,8 +704,9 @@ def main():
                 "data": "synthetic", "config": workload_config(args, world, gather),
                 "frames_per_s": round(all_views / t_max, 2),
                 "prim_samples_per_s": round(all_prim / t_max / 1e6, 3),
+                "digest_ok": digest_ok,  # every timed view bit-equal to the reference's digest
                 "ray_samples_per_view": ray_samples // V, "prim_samples_per_view": prim_samples // V,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sweep": sweep,
                 # per step, batched: 6 binning stages for all views, the cross-view tile order, one
                 # raymarch and one fallback launch; per view: 6 + 2 launches for each view
                 "gpu_launches": (9 if batch else 8 * V) * args.steps,

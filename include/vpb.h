@@ -174,6 +174,12 @@ int vp_render_shard_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg
                           int32_t n_shards, float *rgb, float *alpha, int32_t *samples, void *stream);
 /* Number of tile slots of shard `shard` of n_shards for a width x height view. */
 int64_t vp_shard_tiles(int32_t width, int32_t height, int32_t shard, int32_t n_shards);
+/* Capacity (keys) of each view's tile-key buffer (K3's (tile, depth) entries); 0 restores the
+ * default max(2^20, 16 K). A view whose keys do not all fit still renders exactly: the tiles
+ * whose buckets overflow are marched by the fallback kernel from all K primitives' pixel
+ * rectangles (slower). With grow != 0 the capacity then follows the largest key count seen
+ * (without waiting on the device); grow == 0 keeps it fixed (memory-bounded callers, tests). */
+int vp_set_key_capacity(vp_ctx *ctx, int64_t keys, int32_t grow);
 /* Waits for every render and output copy the context has enqueued. */
 int vp_sync(vp_ctx *ctx);
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats);

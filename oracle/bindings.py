@@ -459,3 +459,79 @@ def ref_adam_run(ref, tr24, m, payload_planar, grads_seq, cfg6):
     if rc != 0:
         raise RuntimeError(f"reference adamStep failed ({rc}): {ref.error()}")
     return tr, pay
+
+
+# Default MarchConfig / WindowParams of the §8d workload (march.h:11-20, primitive.h:14-17);
+# restated here so the reference arm of bench.py needs nothing from the product package.
+REF_STEP, REF_EPS, REF_WALPHA, REF_WBETA = 0.001, 0.01, 8.0, 8
+
+
+def ref_shell_arrays(ref: RefCore, k: int, m: int):
+    """The §8d "mvp_shell" inputs built by the reference-side generator (vpref_shell_scene):
+    (K x 24 PrimitiveTransform records, planar K*4*M^3 payload)."""
+    L = ref.lib
+    L.vpref_shell_scene.argtypes = [C.c_int32, C.c_int32, f32p, f32p]
+    tr = np.zeros((k, 24), np.float32)
+    pay = np.zeros(k * 4 * m ** 3, np.float32)
+    if L.vpref_shell_scene(int(k), int(m), _p(tr), _p(pay)) != 0:
+        raise RuntimeError(f"reference shell scene failed: {ref.error()}")
+    return tr, pay
+
+
+def ref_shell_camera(ref: RefCore, view: int, n_views: int, width: int):
+    """(K9, R9, t3) column-major of the §8d camera: view < 0 headline, else ring view."""
+    L = ref.lib
+    L.vpref_shell_camera.argtypes = [C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p]
+    k9, r9, t3 = np.zeros(9, np.float32), np.zeros(9, np.float32), np.zeros(3, np.float32)
+    if L.vpref_shell_camera(int(view), int(n_views), int(width), _p(k9), _p(r9), _p(t3)) != 0:
+        raise RuntimeError(f"reference shell camera failed: {ref.error()}")
+    return k9, r9, t3
+
+
+class RefScene:
+    """A resident reference Scene (vpref_scene_*): built once, then every render() call runs
+    volprim::render (march.cpp:95-132) on it. Outputs are copied only when asked for."""
+
+    def __init__(self, ref: RefCore, k: int, m: int, tr24=None, payload=None,
+                 w_alpha: float = REF_WALPHA, w_beta: int = REF_WBETA):
+        L = ref.lib
+        L.vpref_scene_new.restype = C.c_void_p
+        L.vpref_scene_new.argtypes = [C.c_int32, C.c_int32, f32p, f32p, C.c_float, C.c_int32]
+        L.vpref_scene_new_shell.restype = C.c_void_p
+        L.vpref_scene_new_shell.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_int32]
+        L.vpref_scene_free.argtypes = [C.c_void_p]
+        L.vpref_scene_render.argtypes = [C.c_void_p, f32p, f32p, f32p, C.c_int32, C.c_int32, C.c_float,
+                                         C.c_float, C.c_int32, C.c_uint64, f32p, f32p, i32p,
+                                         C.POINTER(C.c_int64)]
+        self.ref, self.lib = ref, L
+        if tr24 is None:  # the §8d shell scene, generated in place
+            self.h = L.vpref_scene_new_shell(int(k), int(m), float(w_alpha), int(w_beta))
+        else:
+            tr = _f(tr24).reshape(-1, 24)
+            self.h = L.vpref_scene_new(tr.shape[0], int(m), _p(tr), _p(_f(payload)), float(w_alpha), int(w_beta))
+        if not self.h:
+            raise RuntimeError(f"reference scene failed: {ref.error()}")
+
+    def render(self, k9, r9, t3, width, height, step=REF_STEP, eps=REF_EPS, jitter=False, seed=0,
+               outputs: bool = False):
+        """Returns total ray-samples, or (total, rgb, alpha, samples) when outputs=True."""
+        tot = C.c_int64()
+        rgb = alpha = samples = None
+        if outputs:
+            rgb = np.zeros((height, width, 3), np.float32)
+            alpha = np.zeros((height, width, 1), np.float32)
+            samples = np.zeros(height * width, np.int32)
+        rc = self.lib.vpref_scene_render(self.h, _p(_f(k9)), _p(_f(r9)), _p(_f(t3)), int(width), int(height),
+                                         float(step), float(eps), int(bool(jitter)), int(seed), _p(rgb),
+                                         _p(alpha), _p(samples, i32p), C.byref(tot))
+        if rc != 0:
+            raise RuntimeError(f"reference render failed ({rc}): {self.ref.error()}")
+        return (tot.value, rgb, alpha, samples) if outputs else tot.value
+
+    def close(self):
+        if self.h:
+            self.lib.vpref_scene_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

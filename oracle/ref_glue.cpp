@@ -15,6 +15,11 @@
 //   vpref_window        -> window                     (primitive.cpp:25-28)
 //   vpref_backward_rays -> intersect + backwardRay    (grad.cpp:34-195) into a GradBuffer
 //   vpref_load_slab     -> loadSlab                   (scene_io.cpp:43-66)
+//   vpref_shell_scene   -> the §8d "mvp_shell" bench inputs, built with the reference's own
+//                          compose() / AffineXf::toWorld (primitive.cpp:41-49, primitive.h:60)
+//   vpref_shell_camera  -> lookAtCamera on the §8d headline view / 64-view ring
+//   vpref_scene_*       -> a resident Scene (built once), so the reference arm of bench.py times
+//                          volprim::render (march.cpp:95-132) and nothing else per call
 //
 // Flat layouts (shared with include/vpb.h):
 //   PrimitiveTransform = 24 floats: tBase[3] rBase[9] (column-major) sBase[3] deltaT[3]
@@ -24,8 +29,11 @@
 // Return codes: 0 ok, volprim::ErrorCategory value on volprim::Error, 1 on other exceptions.
 #include <cstdint>
 #include <algorithm>
+#include <cmath>
+#include <random>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -408,6 +416,150 @@ int vpref_load_slab(const char *path, int32_t *k, int32_t *m, float *payload, in
         *m = slab.voxelsPerAxis;
         if (payload && int64_t(slab.payload.size()) <= cap)
             std::memcpy(payload, slab.payload.data(), slab.payload.size() * sizeof(float));
+    });
+}
+
+// The §8d synthetic scene ("mvp_shell"), restated on the reference's own types so the reference
+// arm never loads the product library. K primitives on a Fibonacci sphere (R = 0.35 m,
+// h = R*sqrt(4*pi/K)), frame R_hat = [t b n], pose deltas from mt19937_64(1234) drawn six at a
+// time in a fixed order, analytic RGB/sigma fields sampled at voxel-centre world points of the
+// composed frame. tests/test_oracle_golden.py pins its output to digests.json["generator"].
+int vpref_shell_scene(int32_t nPrim, int32_t m, float *tr24, float *payload) {
+    return guarded([&] {
+        if (nPrim < 0 || m < 1) throw Error(ErrorCategory::Usage, "shell scene: bad K or M");
+        constexpr double pi = 3.14159265358979323846;
+        const double radius = 0.35;
+        const double h = nPrim > 0 ? radius * std::sqrt(4.0 * pi / nPrim) : 0.0;
+        const double sigma0 = nPrim > 0 ? 1.5 / (0.7 * h) : 0.0;
+        const double goldenAngle = pi * (3.0 - std::sqrt(5.0));
+        std::mt19937_64 gen(1234);
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        const size_t vox = size_t(m) * m * m;
+        for (int32_t k = 0; k < nPrim; ++k) {
+            const double nz = 1.0 - (2.0 * k + 1.0) / nPrim;
+            const double rr = std::sqrt(std::max(0.0, 1.0 - nz * nz));
+            const double ph = k * goldenAngle;
+            const double nx = rr * std::cos(ph), ny = rr * std::sin(ph);
+            // tangent = normalize(e_z x n) (fallback e_y), bitangent = n x tangent
+            double tx = -ny, ty = nx, tz = 0.0;
+            const double len = std::sqrt(tx * tx + ty * ty + tz * tz);
+            if (len < 1e-12) {
+                tx = 0.0; ty = 1.0; tz = 0.0;
+            } else {
+                tx /= len; ty /= len; tz /= len;
+            }
+            const double bx = ny * tz - nz * ty, by = nz * tx - nx * tz, bz = nx * ty - ny * tx;
+            double d[6];
+            for (double &v : d) v = u(gen);
+            PrimitiveTransform pt;
+            pt.tBase = Vec3(float(radius * nx), float(radius * ny), float(radius * nz));
+            const float cols[9] = {float(tx), float(ty), float(tz), float(bx), float(by), float(bz),
+                                   float(nx), float(ny), float(nz)};
+            pt.rBase = m3(cols);
+            pt.sBase = Vec3(float(0.6 * h), float(0.6 * h), float(0.35 * h));
+            pt.deltaT = Vec3(float(0.05 * h * d[3]), float(0.05 * h * d[4]), float(0.05 * h * d[5]));
+            pt.deltaR = Vec3(float(0.1 * d[0]), float(0.1 * d[1]), float(0.1 * d[2]));
+            pt.deltaS = Vec3(0, 0, 0);
+            if (tr24) {
+                float *o = tr24 + 24 * size_t(k);
+                put3(o + 0, pt.tBase);
+                put9(o + 3, pt.rBase);
+                put3(o + 12, pt.sBase);
+                put3(o + 15, pt.deltaT);
+                put3(o + 18, pt.deltaR);
+                put3(o + 21, pt.deltaS);
+            }
+            if (!payload) continue;
+            const AffineXf xf = compose(pt);
+            float *dst = payload + size_t(k) * 4 * vox;
+            for (int zi = 0; zi < m; ++zi)
+                for (int yi = 0; yi < m; ++yi)
+                    for (int xi = 0; xi < m; ++xi) {
+                        const Vec3 pm(-1 + float(2 * xi + 1) / m, -1 + float(2 * yi + 1) / m,
+                                      -1 + float(2 * zi + 1) / m);
+                        const Vec3 pw = xf.toWorld(pm);
+                        const double x = pw.x, y = pw.y, z = pw.z;
+                        const size_t at = (size_t(zi) * m + yi) * m + xi;
+                        for (int c = 0; c < 3; ++c)
+                            dst[c * vox + at] = float(0.5 + 0.45 * std::sin(9 * x + 7 * y * (c + 1) + 5 * z));
+                        dst[3 * vox + at] = float(sigma0 * (0.5 + 0.5 * std::sin(11 * x + 13 * y + 3 * z)));
+                    }
+        }
+    });
+}
+
+// lookAtCamera (synthetic.cpp:15-38) at the §8d positions: view < 0 is the headline camera at
+// (0.25, 0.15, -1.1); otherwise view v of an n-view ring (az = 2*pi*v/n, el = 0.35*sin(3*az),
+// radius 1.1). Target the origin, up +y, f = 1.2*W, square W x W image.
+int vpref_shell_camera(int32_t view, int32_t nViews, int32_t width, float *k9, float *r9, float *t3) {
+    return guarded([&] {
+        if (width <= 0 || (view >= 0 && (nViews <= 0 || view >= nViews)))
+            throw Error(ErrorCategory::Usage, "shell camera: bad view");
+        Vec3 pos(0.25f, 0.15f, -1.1f);
+        if (view >= 0) {
+            constexpr double pi = 3.14159265358979323846;
+            const double az = 2.0 * pi * view / nViews;
+            const double el = 0.35 * std::sin(3.0 * az);
+            pos = Vec3(float(1.1 * std::cos(el) * std::sin(az)), float(1.1 * std::sin(el)),
+                       float(-1.1 * std::cos(el) * std::cos(az)));
+        }
+        const Camera cam = lookAtCamera(pos, Vec3(0, 0, 0), Vec3(0, 1, 0), float(1.2 * width), width, width);
+        put9(k9, cam.intrinsics);
+        put9(r9, cam.rotation.matrix);
+        put3(t3, cam.translation);
+    });
+}
+
+// A resident one-frame Scene. The handle owns a volprim::Scene built once; vpref_scene_render
+// then runs volprim::render on it and nothing else is inside the call except the optional
+// copies into caller arrays (null pointers skip them) and the sum of the sample counts.
+struct RefScene {
+    Scene scene;
+};
+
+void *vpref_scene_new(int32_t nPrim, int32_t m, const float *tr24, const float *payload, float wAlpha,
+                      int32_t wBeta) {
+    RefScene *rs = nullptr;
+    const int rc = guarded([&] {
+        auto owned = std::make_unique<RefScene>();
+        owned->scene.window = WindowParams{wAlpha, wBeta};
+        Frame fr;
+        fr.transforms.reserve(size_t(nPrim));
+        for (int k = 0; k < nPrim; ++k) fr.transforms.push_back(transformFrom24(tr24 + 24 * size_t(k)));
+        fr.slab.resize(nPrim, m);
+        std::memcpy(fr.slab.payload.data(), payload, fr.slab.payload.size() * sizeof(float));
+        owned->scene.frames.push_back(std::move(fr));
+        rs = owned.release();
+    });
+    return rc == 0 ? rs : nullptr;
+}
+
+// The shell scene generated straight into a resident Scene (no 268 MB round trip through Python).
+void *vpref_scene_new_shell(int32_t nPrim, int32_t m, float wAlpha, int32_t wBeta) {
+    std::vector<float> tr(size_t(nPrim) * 24), pay(size_t(nPrim) * 4 * size_t(m) * m * m);
+    if (vpref_shell_scene(nPrim, m, tr.data(), pay.data()) != 0) return nullptr;
+    return vpref_scene_new(nPrim, m, tr.data(), pay.data(), wAlpha, wBeta);
+}
+
+void vpref_scene_free(void *h) { delete static_cast<RefScene *>(h); }
+
+int vpref_scene_render(void *h, const float *k9, const float *r9, const float *t3, int32_t width,
+                       int32_t height, float stepSize, float earlyEps, int32_t jitter, uint64_t seed,
+                       float *rgb, float *alpha, int32_t *samples, int64_t *totalSamples) {
+    return guarded([&] {
+        if (!h) throw Error(ErrorCategory::Usage, "null scene");
+        MarchConfig cfg;
+        cfg.stepSize = stepSize;
+        cfg.earlyEps = earlyEps;
+        cfg.jitter = jitter != 0;
+        cfg.seed = seed;
+        const Camera cam = cameraFrom(k9, r9, t3, width, height);
+        const RenderOutput out = render(static_cast<RefScene *>(h)->scene, 0, cam, cfg);
+        if (totalSamples) *totalSamples = int64_t(out.totalSamples());
+        if (rgb) std::memcpy(rgb, out.color.data.data(), out.color.data.size() * sizeof(float));
+        if (alpha) std::memcpy(alpha, out.alpha.data.data(), out.alpha.data.size() * sizeof(float));
+        if (samples)
+            for (size_t i = 0; i < out.sampleCounts.size(); ++i) samples[i] = out.sampleCounts[i];
     });
 }
 

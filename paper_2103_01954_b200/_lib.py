@@ -73,6 +73,7 @@ SIGNATURES = {
                                         C.c_int32, f32p, f32p, i32p, C.c_void_p]),
     "vp_shard_tiles": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "vp_sync": (C.c_int, [C.c_void_p]),
+    "vp_set_key_capacity": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32]),
     "vp_read_stats": (C.c_int, [C.c_void_p, C.POINTER(vp_stats)]),
     "vp_march_rays": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, f32p, C.POINTER(vp_march),
                                 f32p, f32p, i32p]),

@@ -317,6 +317,24 @@ class Renderer:
                                    samples.ctypes.data_as(i32p), C.byref(st)), self._ctx)
         return RenderOutput(color, alpha, samples, st.as_dict() if with_stats else None)
 
+    def render_batch(self, cams: List[Camera], cfg: MarchConfig) -> List[RenderOutput]:
+        """Up to 16 views of the resident frame in one raymarch launch (vp_render_batch_async)
+        into host arrays; waits for the copies (vp_sync). Stats are not per view here."""
+        n = len(cams)
+        if n == 0:
+            return []
+        outs = [RenderOutput(np.zeros((int(c.height), int(c.width), 3), np.float32),
+                             np.zeros((int(c.height), int(c.width), 1), np.float32),
+                             np.zeros(int(c.height) * int(c.width), np.int32), None) for c in cams]
+        cc = (vp_camera * n)(*[c.to_c() for c in cams])
+        mc = cfg.to_c()
+        rgb = (f32p * n)(*[_fptr(o.color) for o in outs])
+        alpha = (f32p * n)(*[_fptr(o.alpha) for o in outs])
+        samp = (i32p * n)(*[o.sample_counts.ctypes.data_as(i32p) for o in outs])
+        _check(self._lib.vp_render_batch_async(self._ctx, n, cc, C.byref(mc), rgb, alpha, samp, None), self._ctx)
+        _check(self._lib.vp_sync(self._ctx), self._ctx)
+        return outs
+
     def render_device(self, cam: Camera, cfg: MarchConfig, rgb_ptr: int, alpha_ptr: int,
                       samples_ptr: int = 0, stream: int = 0):
         """Enqueue a render into device buffers (e.g. torch CUDA tensors' data_ptr())."""
@@ -337,6 +355,11 @@ class Renderer:
                                                C.cast(C.c_void_p(alpha_ptr), f32p),
                                                C.cast(C.c_void_p(samples_ptr), i32p) if samples_ptr else None,
                                                C.c_void_p(stream) if stream else None), self._ctx)
+
+    def set_key_capacity(self, keys: int, grow: bool = True):
+        """vp_set_key_capacity: tile-key buffer capacity per view (0 = default). Renders stay
+        exact when it is too small (overflowed tiles go to the fallback kernel)."""
+        _check(self._lib.vp_set_key_capacity(self._ctx, int(keys), int(bool(grow))), self._ctx)
 
     def read_stats(self) -> dict:
         st = vp_stats()

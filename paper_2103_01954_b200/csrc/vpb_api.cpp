@@ -116,7 +116,14 @@ struct vp_ctx {
     DevCounters *last_ctr[kMaxViews] = {};  // the counters of the latest render launch's views
     int last_n = 1;                          // 1: ctx->d_ctr alone (single view / ray calls)
     int64_t entries_cap = 0;
+    bool key_cap_fixed = false;  // vp_set_key_capacity(..., grow = 0)
     int ovf_cap = 0;
+    // K5b's per-CTA candidate lists for key-overflowed tiles (kOvfTileBlocks x n_prim ids)
+    DBuf<uint32_t> ovf_tile_lists;
+    // per slot: the key count K2 found, copied to pinned memory after each binning so the next
+    // launch can grow entries_cap without waiting (h_keys_ready: that copy's event)
+    unsigned long long *h_keys = nullptr;
+    cudaEvent_t ev_keys[2] = {};
     cudaEvent_t t_ev[2 * kTimingSlots] = {};
     int64_t t_count = 0;
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
@@ -245,6 +252,7 @@ int ensure_slot_buffers(vp_ctx *ctx, BinSlot &b, const CamDev &cam) {
     VP_CUDA(ctx, b.prects.ensure(size_t(std::max(ctx->n_prim, 1))));
     VP_CUDA(ctx, b.keys.ensure(size_t(std::max(ctx->n_prim, 1))));
     VP_CUDA(ctx, b.entries.ensure(size_t(ctx->entries_cap)));
+    VP_CUDA(ctx, ctx->ovf_tile_lists.ensure(size_t(kOvfTileBlocks) * size_t(std::max(ctx->n_prim, 1))));
     if (size_t(b.ovf_cap) < n_px) {
         VP_CUDA(ctx, b.ovf.ensure(n_px));
         b.ovf_cap = int(n_px);
@@ -259,6 +267,24 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
     return VP_OK;
 }
 
+// Key capacity for the next binning. A view whose tile buckets do not fit the entries buffer
+// still renders exactly (its overflowed tiles are marched by K5b from all K pixel rectangles),
+// but slower, so the capacity follows the largest key count seen: from the pinned copies of
+// launches whose binning has completed (never waits) and from vp_render / vp_read_stats.
+void note_keys(vp_ctx *ctx, unsigned long long keys) {
+    if (!ctx->key_cap_fixed && int64_t(keys) > ctx->entries_cap) ctx->entries_cap = int64_t(keys) + int64_t(keys) / 4 + 1024;
+}
+
+void grow_key_capacity(vp_ctx *ctx) {
+    for (int g = 0; g < 2; ++g) {
+        if (!ctx->ev_keys[g] || cudaEventQuery(ctx->ev_keys[g]) != cudaSuccess) {
+            cudaGetLastError();  // cudaErrorNotReady is not an error here
+            continue;
+        }
+        for (int v = 0; v < kMaxViews; ++v) note_keys(ctx, ctx->h_keys[g * kMaxViews + v]);
+    }
+}
+
 // The device pipeline for `n` views (no host synchronisation). Binning (K1-K3) of each view
 // goes to bin_stream into the slot group the previous launch did not use, so it overlaps the
 // previous launch's raymarch (whose tail leaves SMs idle); a slot is rebinned only after the
@@ -269,6 +295,7 @@ int ensure_render_buffers(vp_ctx *ctx, const CamDev &cam) {
 int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, const OutDev *ods, cudaStream_t st,
                   int n_ctas_single = -1) {
     if (n < 1 || n > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per launch");
+    grow_key_capacity(ctx);
     ctx->group ^= 1;
     BinSlot *grp = ctx->slot + ctx->group * kMaxViews;
     for (int v = 0; v < n; ++v)
@@ -295,6 +322,11 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
         total += n_tiles[v];
     }
     VP_CUDA(ctx, launch_binning_batch(bb, ctx->bin_stream));
+    for (int v = 0; v < n; ++v)  // the views' key counts, for grow_key_capacity at a later launch
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_keys + ctx->group * kMaxViews + v, &grp[v].d_ctr->keys,
+                                     sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->bin_stream));
+    for (int v = n; v < kMaxViews; ++v) ctx->h_keys[ctx->group * kMaxViews + v] = 0;
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_keys[ctx->group], ctx->bin_stream));
     const uint32_t *order = grp[0].order.p;
     if (n > 1) {
         VP_CUDA(ctx, ctx->batch_order[ctx->group].ensure(size_t(std::max(total, 1))));
@@ -311,7 +343,7 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     VP_CUDA(ctx, launch_march_tiles(mp, ctx->xfb[ctx->xfi].p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
-                                             ctx->fb_x.p, ctx->fb_c.p, st));
+                                             ctx->fb_x.p, ctx->fb_c.p, ctx->ovf_tile_lists.p, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
     for (int v = 0; v < n; ++v) VP_CUDA(ctx, cudaEventRecord(grp[v].ev_marched, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->ev_last_marched, st));
@@ -434,11 +466,15 @@ int vp_create(int32_t device, vp_ctx **out) {
         (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[1], cudaEventDisableTiming)) != cudaSuccess ||
 
+        (e = cudaEventCreateWithFlags(&ctx->ev_keys[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_keys[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaMallocHost(&ctx->h_keys, sizeof(unsigned long long) * 2 * kMaxViews)) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
         vp_destroy(ctx);
         return rc;
     }
+    std::memset(ctx->h_keys, 0, sizeof(unsigned long long) * 2 * kMaxViews);
     for (cudaEvent_t &ev : ctx->t_ev)
         if ((e = cudaEventCreate(&ev)) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
@@ -505,6 +541,10 @@ int vp_destroy(vp_ctx *ctx) {
     }
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    if (ctx->h_keys) cudaFreeHost(ctx->h_keys);
+    for (cudaEvent_t ev : ctx->ev_keys)
+        if (ev) cudaEventDestroy(ev);
+    ctx->ovf_tile_lists.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t ev : ctx->t_ev)
@@ -860,6 +900,14 @@ int vp_sync(vp_ctx *ctx) {
     return VP_OK;
 }
 
+int vp_set_key_capacity(vp_ctx *ctx, int64_t keys, int32_t grow) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (keys < 0 || keys > int64_t(0xfffffffe)) return fail(ctx, VP_ERR_USAGE, "key capacity out of range");
+    ctx->entries_cap = keys;  // 0: the default, max(2^20, 16 K), at the next render
+    ctx->key_cap_fixed = keys > 0 && grow == 0;
+    return VP_OK;
+}
+
 int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
     if (int rc = check_ctx(ctx, false)) return rc;
     // the latest launch may still run on a caller's stream
@@ -887,10 +935,7 @@ int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
     }
     note_density(ctx, c);
     fill_stats(c, 0.f, stats);
-    if (c.key_overflow) {
-        ctx->entries_cap = int64_t(max_keys) + int64_t(max_keys) / 4 + 1024;
-        return fail(ctx, VP_ERR_DEVICE, "tile key buffer was too small; capacity grown, render again");
-    }
+    note_keys(ctx, max_keys);  // key-overflowed tiles were rendered by K5b; grow for the next render
     return check_counters(ctx, c);
 }
 
@@ -932,7 +977,7 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
         VP_CUDA(ctx, ctx->out_samples.ensure(n_px));
         od.samples = ctx->out_samples.p;
     }
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    {
         if (int rc = ensure_render_buffers(ctx, cd)) return rc;
         VP_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
         if (int rc = enqueue_render(ctx, cd, mp, od, st)) return rc;
@@ -941,10 +986,7 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
         VP_CUDA(ctx, cudaStreamSynchronize(st));
         const DevCounters c = *ctx->h_ctr;
         note_density(ctx, c);
-        if (c.key_overflow) {  // grow the key buffer and run again
-            ctx->entries_cap = int64_t(c.keys) + int64_t(c.keys) / 4 + 1024;
-            continue;
-        }
+        note_keys(ctx, c.keys);  // overflowed tiles were marched by K5b; size for the next render
         if (!d_rgb) VP_CUDA(ctx, cudaMemcpyAsync(rgb, od.rgb, n_px * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
         if (!d_alpha) VP_CUDA(ctx, cudaMemcpyAsync(alpha, od.alpha, n_px * sizeof(float), cudaMemcpyDeviceToHost, st));
         if (samples && !d_samp)
@@ -955,7 +997,6 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
         fill_stats(c, ms, stats);
         return check_counters(ctx, c);
     }
-    return fail(ctx, VP_ERR_DEVICE, "tile key buffer could not be sized");
 }
 
 int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,

@@ -165,18 +165,20 @@ __device__ __forceinline__ void scan_body(const uint32_t *__restrict__ counts, i
         }
         __syncthreads();
         const unsigned long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + incl - v;
-        if (i < n_tiles) {
-            offsets[i] = (uint32_t)excl;
-            cursor[i] = (uint32_t)excl;
+        if (i < n_tiles) {  // saturated: a bucket past 2^32 - 1 keys cannot wrap (tile_key_overflowed)
+            const uint32_t e32 = excl < 0xffffffffull ? (uint32_t)excl : 0xffffffffu;
+            offsets[i] = e32;
+            cursor[i] = e32;
         }
         __syncthreads();
         if (tid == blockDim.x - 1) carry = excl + v;
         __syncthreads();
     }
     if (tid == 0) {
-        offsets[n_tiles] = (uint32_t)carry;
+        offsets[n_tiles] = carry < 0xffffffffull ? (uint32_t)carry : 0xffffffffu;
         ctr->keys = carry;
         ctr->key_overflow = (int64_t)carry > capacity ? 1 : 0;
+        ctr->key_cap = (uint32_t)min(capacity, (int64_t)0xfffffffe);
     }
     // counting sort of the tiles by bucket(t) (1 + min(count, 1022), 0 if not owned), descending
     for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
@@ -215,18 +217,21 @@ __device__ __forceinline__ void scan_body(const uint32_t *__restrict__ counts, i
 // primitive's tiles in parallel (a thread per primitive would chain its atomics' round trips).
 // Order inside a bucket is arbitrary here; K3b makes it canonical.
 __device__ __forceinline__ void emit_body(const int4 *__restrict__ rects, const uint32_t *__restrict__ keys,
-                       int n_prim, int tiles_x, uint32_t *__restrict__ cursor,
+                       int n_prim, int tiles_x, const uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
                        unsigned long long *__restrict__ entries, const DevCounters *ctr, int n_shards,
                        int shard) {
     const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (k >= n_prim || ctr->key_overflow) return;
+    if (k >= n_prim) return;
     const int4 rc = rects[k];
     const int w = rc.z - rc.x + 1, h = rc.w - rc.y + 1;
     if (w <= 0 || h <= 0) return;
     const unsigned long long e = ((unsigned long long)keys[k] << 32) | (uint32_t)k;
+    const bool ovf = ctr->key_overflow != 0;
+    const unsigned cap = ctr->key_cap;
     for (int q = lane; q < w * h; q += 32) {
         const int t = (rc.y + q / w) * tiles_x + rc.x + q % w;
+        if (ovf && tile_key_overflowed(offsets, t, cap)) continue;  // the fallback rebuilds its list
         if (n_shards <= 1 || t % n_shards == shard) entries[atomicAdd(&cursor[t], 1u)] = e;
     }
 }
@@ -280,9 +285,9 @@ __device__ __forceinline__ void warp_sort_bucket(unsigned long long *a, int n, i
 
 __device__ __forceinline__ void tile_sort_warp_body(const uint32_t *__restrict__ offsets, unsigned long long *__restrict__ entries,
                  int n_tiles, uint32_t *__restrict__ big, DevCounters *ctr) {
-    if (ctr->key_overflow) return;
     const int tile = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (tile >= n_tiles) return;
+    if (ctr->key_overflow && tile_key_overflowed(offsets, tile, ctr->key_cap)) return;
     const uint32_t start = offsets[tile];
     const int n = (int)(offsets[tile + 1] - start);
     if (n <= 1) return;
@@ -298,7 +303,6 @@ __device__ __forceinline__ void tile_sort_big_body(const uint32_t *__restrict__ 
                                 unsigned long long *__restrict__ entries, const uint32_t *__restrict__ big,
                                 const DevCounters *ctr) {
     __shared__ unsigned long long s[kSortSmem];
-    if (ctr->key_overflow) return;
     for (unsigned q = blockIdx.x; q < ctr->big_buckets; q += gridDim.x) {
         const uint32_t tile = big[q];
         const uint32_t start = offsets[tile];
@@ -357,7 +361,8 @@ __global__ void k_scan(const __grid_constant__ BinBatch bb) {
 }
 __global__ void k_emit(const __grid_constant__ BinBatch bb) {
     const BinView &v = bb.v[blockIdx.y];
-    emit_body(v.rects, v.keys, bb.n_prim, v.cam.tiles_x, v.cursor, v.entries, v.ctr, v.cam.n_shards, v.cam.shard);
+    emit_body(v.rects, v.keys, bb.n_prim, v.cam.tiles_x, v.offsets, v.cursor, v.entries, v.ctr, v.cam.n_shards,
+              v.cam.shard);
 }
 __global__ void __launch_bounds__(256) k_tile_sort_warp(const __grid_constant__ BinBatch bb) {
     const BinView &v = bb.v[blockIdx.y];
@@ -511,8 +516,8 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     const CamDev &cam = vd.cam;
     const OutDev &od = vd.od;
     DevCounters *ctr = vd.ctr;
-    if (ctr->key_overflow) return;
     const int tile = (int)(oe & 0xfffffu);
+    if (ctr->key_overflow && tile_key_overflowed(vd.offsets, tile, ctr->key_cap)) return;  // K5b marches it
     const uint32_t start = vd.offsets[tile];
     const int n = (int)(vd.offsets[tile + 1] - start);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -872,40 +877,131 @@ cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const floa
     }
 }
 
-// K5b over every view of a launch: each view's overflow rays (key-overflowed views skipped).
+// Candidates of a key-overflowed tile rebuilt from all K pixel rectangles (prim ids, any
+// order: the window keeps the smallest (tEnter, prim) keys whatever the scan order). Same
+// predicate and exact test as TileCands<false>, so the rays get the very same segment lists.
+struct ListCands {
+    const uint32_t *list;
+    const float *xf_g;
+    const int4 *prects_g;
+    const float4 *payload;
+    unsigned m3;
+    int n;
+    __device__ __forceinline__ int prim(int c) const { return (int)list[c]; }
+    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)prim(c) * kXfStride; }
+    __device__ __forceinline__ Xf16 xfv(int c) const { return ldg_xf(xf(c)); }
+    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)prim(c) * m3; }
+    __device__ __forceinline__ bool covers(int c, int2 px) const {
+        const int4 r = prects_g[prim(c)];
+        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
+    }
+    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
+        return intersect_obb(xf(c), o, d, tE, tX);
+    }
+};
+
+__device__ __forceinline__ void fallback_pixel(const ViewDev &vd, const MarchDev &mp, int p, RayOut &ro,
+                                               bool &ok, const ListCands *lc, const float *xf_g,
+                                               const float4 *payload, unsigned m3, const Window<int> &w,
+                                               const unsigned long long *tab) {
+    const CamDev &cam = vd.cam;
+    const int px = p % cam.width, py = p / cam.width;
+    V3 o, d;
+    generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+    const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p)) : 0.5f;
+    if (lc) {
+        ro = march_ray<kFallbackCap>(*lc, w, o, d, make_int2(px, py), jit, mp, tab);
+    } else {
+        const int tile = (py / kTile) * cam.tiles_x + px / kTile;
+        const uint32_t start = vd.offsets[tile];
+        const TileCands<false> cands{vd.entries, xf_g, vd.prects, payload, m3, start,
+                                     (int)(vd.offsets[tile + 1] - start), nullptr, nullptr, nullptr,
+                                     nullptr};
+        ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, tab);
+    }
+    ok = !ro.overflow;
+    if (!ok) {
+        atomicAdd(&vd.ctr->fallback_fail, 1);
+        return;
+    }
+    write_pixel(vd.od, p, ro);
+}
+
+// K5b over every view of a launch.
+//  (1) Key-overflowed tiles (their bucket did not fit the entries buffer; K3 and K5 skipped
+//      them): each CTA takes such tiles in turn, rebuilds the tile's candidate list from all K
+//      pixel rectangles (the tile-rectangle test K1/K3 use) into its slice of `tile_scratch`,
+//      and marches the tile's pixels with kFallbackCap-entry windows. Nothing is skipped, so an
+//      async render is exact whatever the key capacity.
+//  (2) The rays whose live segments overflowed K5's window, re-marched wide.
 __global__ void __launch_bounds__(kFallbackThreads)
 k_march_fallback_views(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
-                       ViewBatch views, float *scratch_e, float *scratch_x, int *scratch_c) {
+                       ViewBatch views, float *scratch_e, float *scratch_x, int *scratch_c,
+                       uint32_t *__restrict__ tile_scratch) {
     __shared__ unsigned long long s_tab[32];
+    __shared__ int s_warp[kFallbackThreads / 32];
+    __shared__ int s_n;
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
     const unsigned m3 = (unsigned)(mp.m * mp.m * mp.m);
     for (int v = 0; v < views.n; ++v) {
         const ViewDev &vd = views.v[v];
         DevCounters *ctr = vd.ctr;
-        if (ctr->key_overflow) continue;
-        const int n_ovf = (int)min((unsigned long long)vd.ovf_cap, ctr->overflow_rays);
+        if (!ctr->key_overflow) continue;
         const CamDev &cam = vd.cam;
-        for (int q = gtid; q < n_ovf; q += nthreads) {
-            const int p = vd.ovf_list[q];
-            const int px = p % cam.width, py = p / cam.width;
-            const int tile = (py / kTile) * cam.tiles_x + px / kTile;
-            V3 o, d;
-            generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
-            const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p)) : 0.5f;
-            const uint32_t start = vd.offsets[tile];
-            const TileCands<false> cands{vd.entries, xf_g, vd.prects, payload, m3, start,
-                                         (int)(vd.offsets[tile + 1] - start), nullptr, nullptr, nullptr,
-                                         nullptr};
-            const RayOut ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, s_tab);
-            if (ro.overflow) {
-                atomicAdd(&ctr->fallback_fail, 1);
-                continue;
+        const unsigned cap = ctr->key_cap;
+        const int n_tiles = cam.tiles_x * cam.tiles_y;
+        uint32_t *list = tile_scratch + (size_t)blockIdx.x * n_prim;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            if (!tile_key_overflowed(vd.offsets, t, cap)) continue;  // uniform over the CTA
+            const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
+            if (tid == 0) s_n = 0;
+            __syncthreads();
+            for (int base = 0; base < n_prim; base += kFallbackThreads) {  // compaction in prim order
+                const int k = base + tid;
+                bool in = false;
+                if (k < n_prim) {
+                    const int4 r = vd.prects[k];
+                    in = r.z >= r.x && r.w >= r.y && tx >= r.x / kTile && tx <= r.z / kTile &&
+                         ty >= r.y / kTile && ty <= r.w / kTile;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                if (lane == 0) s_warp[wid] = __popc(bal);
+                __syncthreads();
+                int off = s_n;
+                for (int q = 0; q < wid; ++q) off += s_warp[q];
+                if (in) list[off + __popc(bal & ((1u << lane) - 1))] = (uint32_t)k;
+                __syncthreads();
+                if (tid == 0)
+                    for (int q = 0; q < kFallbackThreads / 32; ++q) s_n += s_warp[q];
+                __syncthreads();
             }
-            write_pixel(vd.od, p, ro);
+            __threadfence_block();
+            const ListCands lc{list, xf_g, vd.prects, payload, m3, s_n};
+            for (int q = tid; q < kTile * kTile; q += kFallbackThreads) {
+                const int2 pp = make_int2(tx * kTile + (q & 15), ty * kTile + (q >> 4));
+                RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
+                bool ok = false;
+                if (pp.x < cam.width && pp.y < cam.height)
+                    fallback_pixel(vd, mp, pp.y * cam.width + pp.x, ro, ok, &lc, xf_g, payload, m3, w, s_tab);
+                add_counters(ctr, ro, ok);
+            }
+            __syncthreads();  // the list slice is reused by the CTA's next tile
+        }
+    }
+    for (int v = 0; v < views.n; ++v) {
+        const ViewDev &vd = views.v[v];
+        DevCounters *ctr = vd.ctr;
+        const int n_ovf = (int)min((unsigned long long)vd.ovf_cap, ctr->overflow_rays);
+        for (int q = gtid; q < n_ovf; q += nthreads) {
+            RayOut ro;
+            bool ok;
+            fallback_pixel(vd, mp, vd.ovf_list[q], ro, ok, nullptr, xf_g, payload, m3, w, s_tab);
+            if (!ok) continue;
             atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);  // rare path: plain atomics
             atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
             atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
@@ -918,9 +1014,10 @@ k_march_fallback_views(MarchDev mp, const float *__restrict__ xf_g, int n_prim, 
 }
 
 cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
-                                        const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st) {
-    k_march_fallback_views<<<kFallbackBlocks, kFallbackThreads, 0, st>>>(mp, xf16, n_prim, payload, views, se, sx,
-                                                                         sc);
+                                        const ViewBatch &views, float *se, float *sx, int *sc,
+                                        uint32_t *tile_scratch, cudaStream_t st) {
+    k_march_fallback_views<<<kOvfTileBlocks, kFallbackThreads, 0, st>>>(mp, xf16, n_prim, payload, views, se, sx,
+                                                                        sc, tile_scratch);
     return cudaGetLastError();
 }
 

@@ -17,8 +17,18 @@ struct DevCounters {
     int key_overflow;
     int fallback_fail;
     unsigned big_buckets;  // K3b: tile buckets past 256 keys (sorted by k_tile_sort_big)
-    unsigned reserved;
+    // key capacity of this view's entries buffer (set by K2): a tile whose bucket ends past it
+    // is "key-overflowed" (tile_key_overflowed) and is marched by the fallback from all K
+    // primitives' pixel rectangles instead of its (unwritten) bucket
+    unsigned key_cap;
 };
+
+// A tile whose bucket [offsets[t], offsets[t+1]) does not fit the entries buffer. K2 saturates
+// the offsets at 0xffffffff, so they never wrap; an empty tile past the capacity is not one.
+__host__ __device__ __forceinline__ bool tile_key_overflowed(const uint32_t *offsets, int t, unsigned cap) {
+    const uint32_t end = offsets[t + 1];
+    return end > cap && (end > offsets[t] || end == 0xffffffffu);
+}
 
 // Raymarch kernel configuration (window length, staged candidates, CTAs/SM): vpb_kernels.cu.
 enum class TileTier : int { Light = 0, Normal = 1, Dense = 2 };
@@ -123,6 +133,9 @@ constexpr int kFallbackCap = 256;      // segment window of the fallback re-marc
 constexpr int kRaySegs = 96;  // segments per ray held by the warp-per-ray kernels
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
 constexpr int kFallbackThreads = 128;
+// key-overflowed tiles (tile_key_overflowed): a fallback CTA rebuilds such a tile's candidate
+// list from all K pixel rectangles into its own slice of K entries of global scratch
+constexpr int kOvfTileBlocks = kFallbackBlocks;
 // backwardRay: one-warp CTAs, 12 per SM (168 registers, no spills); the scratch
 // windows (kFallbackCap entries each) are sized for the larger of the two grids
 constexpr int kBackwardWarps = 148 * 12;
@@ -148,8 +161,10 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
 cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const ViewBatch &views,
                                const uint32_t *order, int n_ctas, bool prof, TileTier tier, cudaStream_t st);
 // K5b for the views' overflow rays (one launch for all views).
+// Key-overflowed tiles are marched here too: tile_scratch holds kOvfTileBlocks * n_prim prim ids.
 cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
-                                        const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st);
+                                        const ViewBatch &views, float *se, float *sx, int *sc,
+                                        uint32_t *tile_scratch, cudaStream_t st);
 // Heaviest-first order over the tiles of several views (counting sort of their candidate counts).
 cudaError_t launch_batch_order(const uint32_t *const *tile_counts, const int *n_tiles, int n_views, uint32_t *order,
                                cudaStream_t st);

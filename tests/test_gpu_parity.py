@@ -356,3 +356,23 @@ def test_async_transform_updates_between_batches(renderer):
         for o, ww in zip(outs[q], want[q]):
             assert_bit_equal("rgb", o[0].numpy().reshape(160, 160, 3), ww.color)
             assert_bit_equal("samples", o[2].numpy(), ww.sample_counts)
+
+
+@pytest.mark.parametrize("group", range(8))
+def test_ring_views_batched_match_reference(renderer, group):
+    """All 64 views of BASELINE config 5 (the bench's timed views included), 8 per raymarch launch
+    through vp_render_batch_async, against the reference's per-view digests
+    (oracle/gen_ring_digests.py)."""
+    ring = DIGESTS["ring"]
+    k, m, w, n = ring["K"], ring["M"], ring["W"], ring["n_views"]
+    if renderer.n_prim != k or renderer.m != m:
+        tr, pay = synthetic.shell_arrays(k, m)
+        renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, pay), api.WindowParams())
+    views = list(range(8 * group, 8 * group + 8))
+    outs = renderer.render_batch([synthetic.shell_camera(v, n, w) for v in views], api.MarchConfig())
+    for v, out in zip(views, outs):
+        d = ring["views"][str(v)]
+        assert out.total_samples() == d["total_samples"], f"view {v}"
+        assert sha(out.sample_counts) == d["samples"], f"view {v} samples"
+        assert sha(out.alpha) == d["alpha"], f"view {v} alpha"
+        assert sha(out.color) == d["rgb"], f"view {v} rgb"

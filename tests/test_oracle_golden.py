@@ -123,3 +123,49 @@ def test_backward_matches_reference(oracle):
                                    g["adj_alpha"], cfg, g["jit"])
         assert np.array_equal(bits(got), bits(g["grads"])), name
         assert np.count_nonzero(g["grads"]) > 1000, name
+
+
+REF = pytest.mark.skipif(not (GOLDEN.parent.parent / "oracle" / "_ref" / "libvolprim_ref.so").exists(),
+                         reason="reference core not built (make -C oracle ref)")
+
+
+@REF
+@pytest.mark.parametrize("km", ["64x16", "512x32"])
+def test_reference_side_generator_matches_digests(km):
+    """The reference arm's own scene generator (ref_glue vpref_shell_scene, built on the
+    reference's compose/toWorld) reproduces the pinned generator digests, so bench.py's
+    reference arm renders exactly the inputs our arm renders without loading libvpb.so."""
+    from oracle.bindings import RefCore, ref_shell_arrays
+    k, m = map(int, km.split("x"))
+    tr, pay = ref_shell_arrays(RefCore(), k, m)
+    gen = json.loads((GOLDEN / "digests.json").read_text())["generator"][km]
+    assert sha(tr) == gen["tr"] and sha(pay) == gen["payload"]
+
+
+@REF
+def test_reference_side_cameras_match_product_cameras():
+    """vpref_shell_camera (reference lookAtCamera) == the product's vp_shell_camera, bit for bit,
+    on the headline view and all 64 ring views."""
+    from oracle.bindings import RefCore, ref_shell_camera
+    ref = RefCore()
+    for v in [-1] + list(range(64)):
+        k9, r9, t3 = ref_shell_camera(ref, v, 64, 1024)
+        cam = synthetic.shell_camera(v, 64, 1024)
+        assert np.array_equal(k9.view(np.uint32), np.asarray(cam.intrinsics, np.float32).T.reshape(-1).view(np.uint32))
+        assert np.array_equal(r9.view(np.uint32), np.asarray(cam.rotation, np.float32).T.reshape(-1).view(np.uint32))
+        assert np.array_equal(t3.view(np.uint32), np.asarray(cam.translation, np.float32).reshape(-1).view(np.uint32))
+
+
+@REF
+def test_reference_resident_scene_render_matches_digest():
+    """The resident-Scene entry the reference arm times (vpref_scene_render) gives the config-1
+    reference digest."""
+    from oracle.bindings import RefCore, RefScene, ref_shell_camera
+    d = json.loads((GOLDEN / "digests.json").read_text())["renders"]["oracle_64x16_256_view-1"]
+    ref = RefCore()
+    sc = RefScene(ref, 64, 16)
+    k9, r9, t3 = ref_shell_camera(ref, -1, 0, 256)
+    tot, rgb, alpha, samples = sc.render(k9, r9, t3, 256, 256, outputs=True)
+    sc.close()
+    assert tot == d["total_samples"]
+    assert sha(samples) == d["samples"] and sha(alpha) == d["alpha"] and sha(rgb) == d["rgb"]
