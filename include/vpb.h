@@ -239,7 +239,14 @@ typedef struct vp_adam {
  * projected (>= 0) in place on the device; the deltas are updated in transforms24 (host,
  * K*24, in/out), composed scales projected to >= 1e-4, and the frame recomposed and
  * re-uploaded. Moments persist in the context (AdamState) until vp_adam_reset or a frame of
- * a different size. VP_ERR_NUMERIC (and no update) on a non-finite gradient. */
+ * a different size. VP_ERR_NUMERIC (and no update) on a non-finite gradient: the payload,
+ * moments, step count and transforms24 are untouched, and the resident records are the
+ * caller's (the resident composition is unchanged). VP_ERR_USAGE when a composed scale is
+ * still non-positive after the projection (the reference's Frame::composed() would throw at the
+ * next use, primitive.cpp:44-45): the step IS committed (payload, moments, step count and the
+ * deltas in transforms24), but the frame is not recomposed and renders fail until valid
+ * transforms are set. grads: device pointers need no alignment (16-byte aligned ones take the
+ * vectorised update). */
 int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *transforms24);
 int vp_adam_reset(vp_ctx *ctx);
 

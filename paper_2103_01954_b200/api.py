@@ -564,6 +564,11 @@ def adam_step(renderer: "Renderer", cfg: AdamConfig, grads: np.ndarray, transfor
         raise Error(ErrorCategory.USAGE, "transforms must be a contiguous float32 K x 24 array")
     ac = _lib.vp_adam(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.lr_delta_scale, cfg.lr_vertex_scale)
     g = np.ascontiguousarray(grads, np.float32)
+    k, m = int(renderer.n_prim or 0), int(renderer.m or 0)
+    if g.size < k * 4 * m ** 3 + 9 * k:  # vp_adam_step reads that many floats
+        raise Error(ErrorCategory.USAGE, f"grads hold {g.size} floats; the frame needs {k * 4 * m ** 3 + 9 * k}")
+    if transforms.size < 24 * k:
+        raise Error(ErrorCategory.USAGE, "transforms must hold K x 24 records")
     _check(lib.vp_adam_step(renderer.ctx, C.byref(ac), _fptr(g), _fptr(transforms)), renderer.ctx)
 
 

@@ -122,7 +122,7 @@ struct vp_ctx {
     DBuf<uint32_t> ovf_tile_lists;
     // per slot: the key count K2 found, copied to pinned memory after each binning so the next
     // launch can grow entries_cap without waiting (h_keys_ready: that copy's event)
-    unsigned long long *h_keys = nullptr;
+    unsigned long long *h_keys = nullptr, *d_keys = nullptr;  // mapped pinned: host / device view
     cudaEvent_t ev_keys[2] = {};
     cudaEvent_t t_ev[2 * kTimingSlots] = {};
     int64_t t_count = 0;
@@ -281,7 +281,8 @@ void grow_key_capacity(vp_ctx *ctx) {
             cudaGetLastError();  // cudaErrorNotReady is not an error here
             continue;
         }
-        for (int v = 0; v < kMaxViews; ++v) note_keys(ctx, ctx->h_keys[g * kMaxViews + v]);
+        for (int v = 0; v < kMaxViews; ++v)
+            note_keys(ctx, reinterpret_cast<volatile unsigned long long *>(ctx->h_keys)[g * kMaxViews + v]);
     }
 }
 
@@ -314,19 +315,16 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     for (int v = 0; v < n; ++v) {
         BinSlot &b = grp[v];
         VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, b.ev_marched, 0));
+        unsigned long long *kh = ctx->h_keys + ctx->group * kMaxViews + v;  // grow_key_capacity reads it
         bb.v[v] = BinView{cams[v], b.rects.p, b.prects.p, b.keys.p, b.tile_counts.p, b.offsets.p, b.cursor.p,
-                          b.order.p, b.entries.p, b.d_ctr};
+                          b.order.p, b.entries.p, b.d_ctr, ctx->d_keys + (kh - ctx->h_keys)};
         vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap};
         counts[v] = b.tile_counts.p;
         n_tiles[v] = cams[v].tiles_x * cams[v].tiles_y;
         total += n_tiles[v];
     }
     VP_CUDA(ctx, launch_binning_batch(bb, ctx->bin_stream));
-    for (int v = 0; v < n; ++v)  // the views' key counts, for grow_key_capacity at a later launch
-        VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_keys + ctx->group * kMaxViews + v, &grp[v].d_ctr->keys,
-                                     sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->bin_stream));
-    for (int v = n; v < kMaxViews; ++v) ctx->h_keys[ctx->group * kMaxViews + v] = 0;
-    VP_CUDA(ctx, cudaEventRecord(ctx->ev_keys[ctx->group], ctx->bin_stream));
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_keys[ctx->group], ctx->bin_stream));  // K2 stored the key counts
     const uint32_t *order = grp[0].order.p;
     if (n > 1) {
         VP_CUDA(ctx, ctx->batch_order[ctx->group].ensure(size_t(std::max(total, 1))));
@@ -468,7 +466,9 @@ int vp_create(int32_t device, vp_ctx **out) {
 
         (e = cudaEventCreateWithFlags(&ctx->ev_keys[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_keys[1], cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaMallocHost(&ctx->h_keys, sizeof(unsigned long long) * 2 * kMaxViews)) != cudaSuccess ||
+        (e = cudaHostAlloc(&ctx->h_keys, sizeof(unsigned long long) * 2 * kMaxViews, cudaHostAllocMapped)) !=
+            cudaSuccess ||
+        (e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->d_keys), ctx->h_keys, 0)) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_ctr, sizeof(DevCounters))) != cudaSuccess) {
         rc = cuda_fail(nullptr, e, "vp_create");
         vp_destroy(ctx);
@@ -611,6 +611,9 @@ int vp_set_transforms_async(vp_ctx *ctx, int32_t n_prim, const float *xf15, void
     VP_CUDA(ctx, ctx->xf15_tmp.ensure(size_t(n_prim) * 15));
     VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_xf_binned[j], 0));
     VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_xf_marched[j], 0));
+    // xf15_tmp is shared by every upload: the previous one (possibly on another stream) must
+    // have finished reading it
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_xf, 0));
     VP_CUDA(ctx, cudaMemcpyAsync(ctx->xf15_tmp.p, xf15, sizeof(float) * 15 * size_t(n_prim), cudaMemcpyDefault, st));
     VP_CUDA(ctx, launch_pad_xf(ctx->xf15_tmp.p, ctx->xfb[j].p, n_prim, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf, st));
@@ -1472,15 +1475,19 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
         VP_CUDA(ctx, cudaMemsetAsync(ctx->adam_m2.p, 0, 4 * n, st));
         ctx->adam_step = 0;
     }
-    DBuf<float> &tmp = ctx->s_adam;  // [grads (if host) | deltas | flags: non-finite gradient, bad scale]
-    VP_CUDA(ctx, tmp.ensure(n + 9 * size_t(k) + 2));
+    // scratch: [deltas | flags: non-finite gradient, bad scale | pad to 16 B | host grads]; the
+    // gradient slot exists only for host gradients (device ones are read in place)
+    DBuf<float> &tmp = ctx->s_adam;
+    const bool host_grads = !is_device_ptr(grads);
+    const size_t g_off = (9 * size_t(k) + 2 + 3) & ~size_t(3);
+    VP_CUDA(ctx, tmp.ensure(g_off + (host_grads ? n : 0)));
     const float *dg = grads;
-    if (!is_device_ptr(grads)) {
-        VP_CUDA(ctx, cudaMemcpyAsync(tmp.p, grads, 4 * n, cudaMemcpyHostToDevice, st));
-        dg = tmp.p;
+    if (host_grads) {
+        VP_CUDA(ctx, cudaMemcpyAsync(tmp.p + g_off, grads, 4 * n, cudaMemcpyHostToDevice, st));
+        dg = tmp.p + g_off;
     }
-    float *d_delta = tmp.p + n;
-    int *d_bad = reinterpret_cast<int *>(tmp.p + n + 9 * size_t(k));  // [0] gradient, [1] scale
+    float *d_delta = tmp.p;
+    int *d_bad = reinterpret_cast<int *>(tmp.p + 9 * size_t(k));  // [0] gradient, [1] scale
     // the caller's records are authoritative: resident copy, then the deltas in Adam's order
     VP_CUDA(ctx, ctx->tr24.ensure(24 * size_t(k)));
     VP_CUDA(ctx, cudaMemcpyAsync(ctx->tr24.p, transforms24, 4 * 24 * size_t(k),

@@ -132,7 +132,7 @@ constexpr int kOrderBuckets = 1024;
 __device__ __forceinline__ void scan_body(const uint32_t *__restrict__ counts, int n_tiles,
                        uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor,
                        uint32_t *__restrict__ order, DevCounters *ctr, int64_t capacity, int n_shards,
-                       int shard) {
+                       int shard, unsigned long long *keys_host = nullptr) {
     const auto bucket = [&](int t) {
         return n_shards > 1 && t % n_shards != shard ? 0u : min(counts[t], (uint32_t)kOrderBuckets - 2) + 1u;
     };
@@ -179,6 +179,7 @@ __device__ __forceinline__ void scan_body(const uint32_t *__restrict__ counts, i
         ctr->keys = carry;
         ctr->key_overflow = (int64_t)carry > capacity ? 1 : 0;
         ctr->key_cap = (uint32_t)min(capacity, (int64_t)0xfffffffe);
+        if (keys_host) *(volatile unsigned long long *)keys_host = carry;
     }
     // counting sort of the tiles by bucket(t) (1 + min(count, 1022), 0 if not owned), descending
     for (int b = tid; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
@@ -357,7 +358,7 @@ __global__ void k_cull(const __grid_constant__ BinBatch bb) {
 __global__ void k_scan(const __grid_constant__ BinBatch bb) {
     const BinView &v = bb.v[blockIdx.y];
     scan_body(v.tile_counts, v.cam.tiles_x * v.cam.tiles_y, v.offsets, v.cursor, v.order, v.ctr, bb.capacity,
-              v.cam.n_shards, v.cam.shard);
+              v.cam.n_shards, v.cam.shard, v.keys_host);
 }
 __global__ void k_emit(const __grid_constant__ BinBatch bb) {
     const BinView &v = bb.v[blockIdx.y];

@@ -96,6 +96,9 @@ struct BinView {
     uint32_t *keys, *tile_counts, *offsets, *cursor, *order;
     unsigned long long *entries;
     DevCounters *ctr;  // zeroed by the batch's first kernel
+    // nullable: K2 also stores the key count here (mapped pinned host memory: a store over
+    // the bus, so no copy-engine transfer queues behind the caller's output copies)
+    unsigned long long *keys_host;
 };
 struct BinBatch {
     BinView v[kMaxViews];

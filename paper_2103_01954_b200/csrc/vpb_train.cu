@@ -223,7 +223,9 @@ cudaError_t launch_adam(const float *g, float *m1, float *m2, float4 *payload, f
     const unsigned blocks = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
     if (check) {
         k_adam_check<<<blocks, 256, 0, st>>>(g, n, bad);
-    } else if (m3 % 4 == 0) {
+    } else if (m3 % 4 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+        // 16-byte gradient loads: only for an aligned caller pointer (a view at an offset into a
+        // flat buffer may be 4-byte aligned; a misaligned LDG.128 would kill the context)
         const int64_t items = n_pay / 16 + (n - n_pay);
         const unsigned b4 = (unsigned)((items + 255) / 256 < 148 * 8 ? (items + 255) / 256 : 148 * 8);
         k_adam_update4<<<b4, 256, 0, st>>>(g, m1, m2, payload, deltas, n_pay, n, m3, c, bad);

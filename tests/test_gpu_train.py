@@ -1,12 +1,14 @@
 """GPU: the training rows — evalLoss's ray-batch driver (vp_eval_loss_pho + the host
 regularisers) and adamStep on the device — against the reference's own evalLoss / adamStep
 (tests/golden/train.npz, written by oracle/gen_golden.py)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
 from conftest import GOLDEN
 from golden_cases import sha
-from paper_2103_01954_b200 import api, synthetic
+from paper_2103_01954_b200 import _lib, api, synthetic
 
 pytestmark = pytest.mark.gpu
 
@@ -331,3 +333,48 @@ def test_eval_loss_pixel_set_errors(renderer, on_device, kind):
     terms = api.eval_loss(renderer, scene, 0, cams, good,
                           api.LossWeights(float(w[0]), float(w[1]), float(w[2]), float(w[3])), cfg)
     assert np.float32(terms.pho) == np.float32(z["terms"][0])
+
+
+def test_adam_step_device_gradient_at_unaligned_offset(renderer):
+    """a device gradient pointer that is only 4-byte aligned (a view one float into a
+    flat buffer) must not take the 16-byte update path; the result equals the host-gradient
+    step bit for bit."""
+    import torch
+    z = _z()
+    m = int(z["adam_m"])
+    k = z["adam_tr_in"].shape[0]
+    a = z["adam_cfg"]
+    cfg = api.AdamConfig(*[float(x) for x in a])
+    g = np.ascontiguousarray(z["adam_grads"][0], np.float32)
+    outs = []
+    for on_device in (False, True):
+        tr = np.ascontiguousarray(z["adam_tr_in"], np.float32).copy()
+        renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, z["adam_pay_in"]), api.WindowParams())
+        renderer._lib.vp_adam_reset(renderer.ctx)
+        if on_device:
+            flat = torch.zeros(g.size + 1, dtype=torch.float32, device="cuda")
+            flat[1:] = torch.from_numpy(g).cuda()
+            torch.cuda.synchronize()
+            ac = _lib.vp_adam(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.lr_delta_scale, cfg.lr_vertex_scale)
+            ptr = flat.data_ptr() + 4
+            assert ptr % 16 != 0
+            rc = renderer._lib.vp_adam_step(renderer.ctx, C.byref(ac), C.cast(C.c_void_p(ptr), _lib.f32p),
+                                            tr.ctypes.data_as(_lib.f32p))
+            assert rc == 0, renderer._lib.vp_last_error(renderer.ctx)
+        else:
+            api.adam_step(renderer, cfg, g, tr)
+        outs.append((bits(tr).copy(), bits(api.payload_planar(renderer)).copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_adam_step_rejects_short_gradient(renderer):
+    z = _z()
+    m = int(z["adam_m"])
+    tr = np.ascontiguousarray(z["adam_tr_in"], np.float32).copy()
+    k = tr.shape[0]
+    renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(k, m, z["adam_pay_in"]), api.WindowParams())
+    cfg = api.AdamConfig(*[float(x) for x in z["adam_cfg"]])
+    with pytest.raises(api.Error) as e:
+        api.adam_step(renderer, cfg, np.zeros(k * 4 * m ** 3, np.float32), tr)  # payload part only
+    assert e.value.category == api.ErrorCategory.USAGE
