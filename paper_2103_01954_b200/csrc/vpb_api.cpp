@@ -129,6 +129,13 @@ struct vp_ctx {
     DBuf<float> adam_m1, adam_m2;  // Adam moments over [payload | deltas] (GradBuffer order)
     // per-entry-point scratch, kept across calls (a cudaMalloc per training call costs ms)
     DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_bwd_fwd, s_adam;
+    // backward payload gradient, channel-interleaved (zero between calls) + touched flags
+    DBuf<float> g_pay4;
+    DBuf<unsigned> g_touched;
+    DBuf<int> bwd_list;  // K6: rays whose segment lists the forward did not keep
+    // off by default: the kernel runs 14 % faster with vector reductions, but the transpose
+    // into the planar GradBuffer costs more than that (K6); VPB_BWD_LAYOUT=v4 enables it
+    bool bwd_v4 = false;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
     // vp_render_async into host memory: two device output slots; the device->host copy of
@@ -437,6 +444,8 @@ int vp_create(int32_t device, vp_ctx **out) {
                                                 prop.name);
     vp_ctx *ctx = new vp_ctx();
     ctx->device = device;
+    if (const char *bl = std::getenv("VPB_BWD_LAYOUT"))  // A/B: "v4" = interleaved + vector reductions
+        ctx->bwd_v4 = std::strcmp(bl, "v4") == 0;
     if (const char *tc = std::getenv("VPB_TILE_CFG"))  // tuning override: light | normal | dense
         ctx->tile_cfg = std::strcmp(tc, "light") == 0    ? int(TileTier::Light)
                         : std::strcmp(tc, "normal") == 0 ? int(TileTier::Normal)
@@ -545,6 +554,9 @@ int vp_destroy(vp_ctx *ctx) {
     for (cudaEvent_t ev : ctx->ev_keys)
         if (ev) cudaEventDestroy(ev);
     ctx->ovf_tile_lists.release();
+    ctx->g_pay4.release();
+    ctx->g_touched.release();
+    ctx->bwd_list.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t ev : ctx->t_ev)
@@ -1164,7 +1176,20 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         dg = g.p;
         if (accumulate) VP_CUDA(ctx, cudaMemcpyAsync(dg, grads, n_grad * 4, cudaMemcpyHostToDevice, st));
     }
-    if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
+    // v4: the payload gradient is scattered channel-interleaved (one 16-byte reduction per
+    // corner) into ctx->g_pay4, kept zeroed between calls, then transposed into dg
+    const bool v4 = ctx->bwd_v4 && k > 0 && n_rays > 0;
+    if (v4) {
+        if (ctx->g_pay4.n < n_pay) {
+            VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
+            VP_CUDA(ctx, cudaMemsetAsync(ctx->g_pay4.p, 0, n_pay * 4, st));
+        }
+        VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
+        VP_CUDA(ctx, cudaMemsetAsync(ctx->g_touched.p, 0, 4 * size_t(k), st));
+        if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg + n_pay, 0, (n_grad - n_pay) * 4, st));
+    } else if (!accumulate) {
+        VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
+    }
     if (k > 0 && n_rays > 0) {
         // pose data on the device (k_pose36, the reference's operation order): rBase and
         // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host]
@@ -1226,9 +1251,18 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             fwd_state = od.state;
             fwd_segs = od.segs;
         }
-        const BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
+        BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
+        if (v4) {
+            bd.g_pay4 = ctx->g_pay4.p;
+            bd.touched = ctx->g_touched.p;
+        }
+        VP_CUDA(ctx, ctx->bwd_list.ensure(n));
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
-                                          bd, ctx->d_ctr, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+                                          bd, ctx->d_ctr, ctx->bwd_list.p, int(n), ctx->fb_e.p, ctx->fb_x.p,
+                                          ctx->fb_c.p, st));
+        if (v4)
+            VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(ctx->g_pay4.p), dg, ctx->g_touched.p, k,
+                                               unsigned(size_t(m) * m * m), accumulate != 0, st));
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
     }
     if (!d_grads) VP_CUDA(ctx, cudaMemcpyAsync(grads, dg, n_grad * 4, cudaMemcpyDeviceToHost, st));

@@ -88,11 +88,18 @@ struct PrimEval {
     int lo[3];
     float fr[3];
     bool clamped[3];
-    float4 c[8];  // corners in (cz, cy, cx) order
     float sigmaRaw, win;
     V3 rgb;
+    // stencilRgbGradient sums (primitive.cpp:101-127) per channel (rgb, sigma) before the
+    // 0.5*M scale and the clamped-axis zeroing
+    float sgx[4], sgy[4], sgz[4];
 };
 
+// The sample's trilinear stencil (primitive.cpp:51-99) and, in the same pass over the 8
+// corners, the four channels' stencil-gradient sums: a corner's value is used as soon as it
+// arrives and no corner stays live in registers. Each sum runs over the corners in the
+// reference's order with the reference's products ((wx*wy)*wz, ((dx*wy)*wz)*v), so the bits
+// are the reference's.
 __device__ __forceinline__ void eval_primitive(const float4 *__restrict__ pbase, int m,
                                                const float *xf, V3 pw, float alpha, int beta,
                                                const unsigned long long *tab, PrimEval &e) {
@@ -117,55 +124,38 @@ __device__ __forceinline__ void eval_primitive(const float4 *__restrict__ pbase,
         e.lo[a] = i0;
         e.fr[a] = m > 1 ? u - (float)i0 : 0.0f;
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int z = min(e.lo[2] + (q >> 2), m - 1), y = min(e.lo[1] + ((q >> 1) & 1), m - 1),
-                  x = min(e.lo[0] + (q & 1), m - 1);
-        e.c[q] = __ldg(pbase + (z * m + y) * m + x);
-    }
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
+    for (int ch = 0; ch < 4; ++ch) e.sgx[ch] = e.sgy[ch] = e.sgz[ch] = 0.f;
+#pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const float wx = (q & 1) ? e.fr[0] : 1.0f - e.fr[0];
-        const float wy = ((q >> 1) & 1) ? e.fr[1] : 1.0f - e.fr[1];
-        const float wz = (q >> 2) ? e.fr[2] : 1.0f - e.fr[2];
+        const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
+        const int z = min(e.lo[2] + cz, m - 1), y = min(e.lo[1] + cy, m - 1), x = min(e.lo[0] + cx, m - 1);
+        const float4 c = __ldg(pbase + (z * m + y) * m + x);
+        const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
+        const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
+        const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
         const float wgt = wx * wy * wz;
-        acc[0] += wgt * e.c[q].x;
-        acc[1] += wgt * e.c[q].y;
-        acc[2] += wgt * e.c[q].z;
-        acc[3] += wgt * e.c[q].w;
+        acc[0] += wgt * c.x;
+        acc[1] += wgt * c.y;
+        acc[2] += wgt * c.z;
+        acc[3] += wgt * c.w;
+        const float a0 = (cx ? 1.0f : -1.0f) * wy * wz;
+        const float a1 = wx * (cy ? 1.0f : -1.0f) * wz;
+        const float a2 = wx * wy * (cz ? 1.0f : -1.0f);
+        const float v[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            e.sgx[ch] += a0 * v[ch];
+            e.sgy[ch] += a1 * v[ch];
+            e.sgz[ch] += a2 * v[ch];
+        }
     }
     e.rgb = mk3(acc[0], acc[1], acc[2]);
     e.sigmaRaw = acc[3];
     e.win = window_value(e.pm, alpha, beta, tab);
 }
 
-__device__ __forceinline__ float ch_of(float4 v, int ch) {
-    return ch == 0 ? v.x : (ch == 1 ? v.y : (ch == 2 ? v.z : v.w));
-}
-
-// stencilRgbGradient (primitive.cpp:101-127): d channel / d pModel, zero along clamped axes.
-__device__ __forceinline__ V3 stencil_gradient(const PrimEval &e, int m, int ch) {
-    if (m == 1) return mk3(0.f, 0.f, 0.f);
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
-        const float v = ch_of(e.c[q], ch);
-        const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
-        const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
-        const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
-        const float dx = cx ? 1.0f : -1.0f, dy = cy ? 1.0f : -1.0f, dz = cz ? 1.0f : -1.0f;
-        g0 += dx * wy * wz * v;
-        g1 += wx * dy * wz * v;
-        g2 += wx * wy * dz * v;
-    }
-    const float s = 0.5f * (float)m;
-    if (e.clamped[0]) g0 = 0.f;
-    if (e.clamped[1]) g1 = 0.f;
-    if (e.clamped[2]) g2 = 0.f;
-    return mk3(g0 * s, g1 * s, g2 * s);
-}
 
 // windowGradient (primitive.cpp:30-39)
 __device__ __forceinline__ V3 window_gradient(V3 p, float alpha, int beta, float wv) {
@@ -220,6 +210,26 @@ struct FwdReplay {
 
 __device__ __forceinline__ void red_add(float *p, float v) { atomicAdd(p, v); }
 
+// One corner's payload gradient (rgb, sigma) of primitive k at voxel v. Planar GradBuffer
+// (params.h:12-27): four scalar reductions, one per channel plane. With VPB_BWD_V4 the device
+// gradient is channel-interleaved like the payload (k, z, y, x, c) and the corner is ONE
+// 16-byte vector reduction (red.global.add.v4.f32); vp_backward_rays transposes it to the
+// planar layout at the C-ABI.
+__device__ __forceinline__ void scatter_payload(const BwdDev &bd, int k, size_t m3, size_t v, float r, float g,
+                                                float b, float s) {
+    if (bd.g_pay4) {
+        float *p = bd.g_pay4 + 4 * ((size_t)k * m3 + v);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(r), "f"(g), "f"(b), "f"(s)
+                     : "memory");
+        return;
+    }
+    float *gk = bd.g_pay + (size_t)k * 4 * m3;
+    red_add(gk + v, r);
+    red_add(gk + m3 + v, g);
+    red_add(gk + 2 * m3 + v, b);
+    red_add(gk + 3 * m3 + v, s);
+}
+
 #ifndef VPB_BWD_WARP_AGG
 #define VPB_BWD_WARP_AGG 1  // warp-aggregated pose atomics at the end of each ray
 #endif
@@ -239,6 +249,7 @@ struct BwdWalk {
     float gTmin = 0.f;
     bool satStep = false;
     int cur = -1;      // primitive whose pose gradients are being summed in registers
+    int last_touched = -1;
     float acc[9];      // deltaT[3] deltaR[3] deltaS[3]
     __device__ BwdWalk(const Cands &c, const MarchDev &m, const unsigned long long *t,
                        const FwdReplay<Cands> &f, const BwdDev &b, V3 dir, V3 ar, float aa)
@@ -302,6 +313,10 @@ struct BwdWalk {
     __device__ void prim(int k, int c) {
         const int m = mp.m;
         const float *xf = cands.xf(c);
+        if (bd.touched && k != last_touched) {  // primitives with gradient entries (the transpose's set)
+            bd.touched[k] = 1u;
+            last_touched = k;
+        }
         PrimEval e;
         eval_primitive(cands.base(c), m, xf, pw, mp.alpha, mp.beta, tab, e);
         const float dt = mp.dt;
@@ -322,32 +337,34 @@ struct BwdWalk {
             else
                 gSigmaW += aAlpha * dt;
         }
-        // payload scatter (grad.cpp:121-134), planar GradBuffer indices
+        // payload scatter (grad.cpp:121-134): corner weights in the reference's product order
         const size_t m3 = (size_t)m * m * m;
-        float *gk = bd.g_pay + (size_t)k * 4 * m3;
         const float gsw = gSigmaW * e.win;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const float wx = (q & 1) ? e.fr[0] : 1.0f - e.fr[0];
-            const float wy = ((q >> 1) & 1) ? e.fr[1] : 1.0f - e.fr[1];
-            const float wz = (q >> 2) ? e.fr[2] : 1.0f - e.fr[2];
+            const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
+            const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
+            const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
+            const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
             const float wgt = wx * wy * wz;
             if (wgt == 0.0f) continue;
-            const int z = min(e.lo[2] + (q >> 2), m - 1), y = min(e.lo[1] + ((q >> 1) & 1), m - 1),
-                      x = min(e.lo[0] + (q & 1), m - 1);
-            const size_t v = ((size_t)z * m + y) * m + x;
-            red_add(gk + v, gRgb.x * wgt);
-            red_add(gk + m3 + v, gRgb.y * wgt);
-            red_add(gk + 2 * m3 + v, gRgb.z * wgt);
-            red_add(gk + 3 * m3 + v, gsw * wgt);
+            const int z = min(e.lo[2] + cz, m - 1), y = min(e.lo[1] + cy, m - 1), x = min(e.lo[0] + cx, m - 1);
+            scatter_payload(bd, k, m3, ((size_t)z * m + y) * m + x, gRgb.x * wgt, gRgb.y * wgt, gRgb.z * wgt,
+                            gsw * wgt);
         }
+        V3 sgrad[4];
+        const float sh = 0.5f * (float)m;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+            sgrad[ch] = m == 1 ? mk3(0.f, 0.f, 0.f)
+                               : mk3(e.clamped[0] ? 0.f : e.sgx[ch] * sh, e.clamped[1] ? 0.f : e.sgy[ch] * sh,
+                                     e.clamped[2] ? 0.f : e.sgz[ch] * sh);
         // spatial gradient (grad.cpp:136-145)
-        const V3 gradSigmaTri = stencil_gradient(e, m, 3);
         const V3 gradW = window_gradient(e.pm, mp.alpha, mp.beta, e.win);
-        V3 gP = (gradSigmaTri * e.win + gradW * e.sigmaRaw) * gSigmaW;
-        gP = gP + stencil_gradient(e, m, 0) * gRgb.x;
-        gP = gP + stencil_gradient(e, m, 1) * gRgb.y;
-        gP = gP + stencil_gradient(e, m, 2) * gRgb.z;
+        V3 gP = (sgrad[3] * e.win + gradW * e.sigmaRaw) * gSigmaW;
+        gP = gP + sgrad[0] * gRgb.x;
+        gP = gP + sgrad[1] * gRgb.y;
+        gP = gP + sgrad[2] * gRgb.z;
         if (e.cube[0]) gP.x = 0.f;
         if (e.cube[1]) gP.y = 0.f;
         if (e.cube[2]) gP.z = 0.f;
@@ -481,10 +498,13 @@ __device__ int backward_one_ray(const BvhCands &cands, const Win &w, const March
     return st;
 }
 
+// The rays whose segment list the forward could not keep (more than kRaySegs segments; none
+// at the benchmark configs): one thread per ray with a kFallbackCap-entry global window,
+// rebuilding the list through the BVH. The warp kernel lists them (ray_list, ctr->bwd_long).
 __global__ void __launch_bounds__(32, 12)
-k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
-                const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, BwdDev bd,
-                DevCounters *ctr, float *se, float *sx, int *sc) {
+k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+                     const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
+                     const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
     __shared__ unsigned long long s_tab[32];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
@@ -492,7 +512,9 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{se, sx, sc, nthreads, gtid};
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
-    for (int64_t r = gtid; r < n_rays; r += nthreads) {
+    const int n = (int)min((unsigned)list_cap, ctr->bwd_long);
+    for (int q = gtid; q < n; q += nthreads) {
+        const int64_t r = ray_list[q];
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
@@ -511,8 +533,9 @@ k_backward_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 // step order. Rays with more than kWarpListBwd segments take the per-thread path.
 constexpr int kWarpListBwd = kRaySegs;
 constexpr int kWarpCandBwd = 256;
-// 3 CTAs/SM (168 registers, 16 B of spills) against 2 at the unbounded 230: the 65,536-ray
-// backward row 3.08 -> 2.78 ms (gpurun_out sweep, K6)
+// 3 CTAs/SM (162 registers, no spills). 4 CTAs (128 registers, 28 B of spills) and 5 (96,
+// 180 B) measured 2.05 and 2.14 ms for the 65,536-ray row against 2.03: more resident warps
+// do not help this walk (K6, tools/bwd_sweep.sh)
 #ifndef VPB_BWD_PAIRS
 #define VPB_BWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
 #endif
@@ -521,12 +544,11 @@ constexpr int kWarpCandBwd = 256;
 #endif
 __global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
-                     RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, float *se, float *sx, int *sc) {
+                     RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, int *__restrict__ ray_list,
+                     int list_cap) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];
-    __shared__ int s_cand[4][kWarpCandBwd];
-    __shared__ float s_ce[4][kWarpCandBwd], s_cx[4][kWarpCandBwd];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -537,9 +559,17 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        // the forward of these rays may have kept the ray's segment list (count >= 0)
-        int nh = bd.fwd_segs ? __float_as_int(bd.fwd_state[8 * r + 7]) : -1;
-        if (nh >= 0) {
+        // the forward of these rays kept the ray's segment list (count >= 0), or marked it as
+        // too long (-1): those rays go to k_backward_rays_list
+        const int nh = __float_as_int(bd.fwd_state[8 * r + 7]);
+        if (nh < 0) {
+            if (lane == 0) {
+                const unsigned slot = atomicAdd(&ctr->bwd_long, 1u);
+                if ((int)slot < list_cap) ray_list[slot] = (int)r;
+            }
+            continue;
+        }
+        {
             const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
             for (int j = lane; j < nh; j += 32) {
                 s_e[wid][j] = sg[j];
@@ -547,21 +577,8 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
                 s_c[wid][j] = __float_as_int(sg[2 * kRaySegs + j]);
             }
             __syncwarp();
-        } else {
-            nh = warp_segment_list(cands, o, d, lane, s_cand[wid], s_ce[wid], s_cx[wid], kWarpCandBwd, s_e[wid],
-                                   s_x[wid], s_c[wid], kWarpListBwd);
         }
-        const int cnt = nh < 0 ? 0 : nh;
-        if (nh < 0) {  // a long segment list: the per-thread walk with a global window
-            if (lane == 0) {
-                const Window<int> w{se, sx, sc, nwarps, gw};
-                const int st = backward_one_ray(cands, w, mp, s_tab, bd, o, d, jit, r);
-                if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
-                if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
-            }
-            __syncwarp();
-            continue;
-        }
+        const int cnt = nh;
         if (cnt == 0) continue;
         const float *E = s_e[wid], *X = s_x[wid];
         const int *P = s_c[wid];
@@ -674,25 +691,75 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
     }
 }
 
+// The channel-interleaved payload gradient (VPB_BWD_V4 layout) into the caller's planar
+// GradBuffer (params.h:12-27): primitives the walk touched are transposed (assigned, or added
+// when accumulating) and their interleaved slots cleared for the next call; untouched ones get
+// zeros (or keep the caller's values when accumulating). One thread per voxel.
+__global__ void __launch_bounds__(256) k_grad_transpose(float4 *__restrict__ g4, float *__restrict__ planar,
+                                                        const unsigned *__restrict__ touched, int n_prim,
+                                                        unsigned m3, int accumulate) {
+    for (int k = blockIdx.x; k < n_prim; k += gridDim.x) {  // one primitive per CTA iteration
+        float *dst = planar + (size_t)k * 4 * m3;
+        float4 *src = g4 + (size_t)k * m3;
+        if (!touched[k]) {
+            if (!accumulate)
+                for (unsigned i = threadIdx.x; i < 4 * m3; i += blockDim.x) dst[i] = 0.f;
+            continue;
+        }
+        // four voxels per thread per round, all loads issued before the stores (one load in
+        // flight per thread left the kernel latency-bound at 12 % of DRAM bandwidth)
+        constexpr int U = 4;
+        for (unsigned v0 = threadIdx.x; v0 < m3; v0 += U * blockDim.x) {
+            float4 g[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned v = v0 + u * blockDim.x;
+                g[u] = v < m3 ? src[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned v = v0 + u * blockDim.x;
+                if (v >= m3) break;
+                src[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (accumulate) {
+                    dst[v] += g[u].x;
+                    dst[m3 + v] += g[u].y;
+                    dst[2 * m3 + v] += g[u].z;
+                    dst[3 * m3 + v] += g[u].w;
+                } else {
+                    dst[v] = g[u].x;
+                    dst[m3 + v] = g[u].y;
+                    dst[2 * m3 + v] = g[u].z;
+                    dst[3 * m3 + v] = g[u].w;
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
+                                  bool accumulate, cudaStream_t st) {
+    if (n_prim == 0 || m3 == 0) return cudaSuccess;
+    const int blocks = n_prim < 148 * 8 ? n_prim : 148 * 8;
+    k_grad_transpose<<<blocks, 256, 0, st>>>(g4, planar, touched, n_prim, m3, accumulate ? 1 : 0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
-                                 const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
-                                 cudaStream_t st) {
+                                 const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
+                                 float *sx, int *sc, cudaStream_t st) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
-    // With the forward's state the adjoint walk goes warp-per-ray for every batch size: one
-    // ray per thread leaves 27 % of the lanes busy (the rays' walks diverge), the step-parallel
-    // walk is 6 % faster even at 65,536 rays and far faster for small batches.
-    if (bd.fwd_state) {
-        const int64_t blocks = (n_rays + 3) / 4;
-        k_backward_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
-            mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, se, sx, sc);
-        return cudaGetLastError();
-    }
-    // one-warp CTAs: a small batch spreads over every SM, a large one keeps
-    // kBackwardWarps * 32 rays in flight (one scratch window each)
-    const int64_t warps = (n_rays + 31) / 32;
-    k_backward_rays<<<(unsigned)(warps < kBackwardWarps ? warps : kBackwardWarps), 32, 0, st>>>(
-        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, se, sx, sc);
+    // The adjoint walk goes warp-per-ray for every batch size (the forward's state and segment
+    // lists are required): one ray per thread leaves 27 % of the lanes busy (the rays' walks
+    // diverge); then the rays with lists too long for the forward to keep, one per thread.
+    if (!bd.fwd_state || !bd.fwd_segs) return cudaErrorInvalidValue;
+    const int64_t blocks = (n_rays + 3) / 4;
+    k_backward_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
+        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap);
+    if (cudaError_t e = cudaGetLastError()) return e;
+    k_backward_rays_list<<<kBackwardWarps, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, ray_list,
+                                                         list_cap, se, sx, sc);
     return cudaGetLastError();
 }
 

@@ -21,6 +21,8 @@ struct DevCounters {
     // is "key-overflowed" (tile_key_overflowed) and is marched by the fallback from all K
     // primitives' pixel rectangles instead of its (unwritten) bucket
     unsigned key_cap;
+    unsigned bwd_long;  // K6: rays whose segment list the forward did not keep (k_backward_rays_list)
+    unsigned pad_;
 };
 
 // A tile whose bucket [offsets[t], offsets[t+1]) does not fit the entries buffer. K2 saturates
@@ -125,6 +127,8 @@ struct BwdDev {
     const float *adj_alpha;
     const float *fwd_state = nullptr;  // the forward's per-ray state (skips the replay), or null
     const float *fwd_segs = nullptr;   // the forward's segment lists (OutDev::segs), or null
+    float *g_pay4 = nullptr;  // non-null: channel-interleaved payload gradient (k, z, y, x, c)
+    unsigned *touched = nullptr;  // with g_pay4: per primitive, set when the walk scatters into it
 };
 
 // Adam step constants (losses.cpp:70-104); bc1/bc2 = 1 - beta^step computed on the host.
@@ -181,10 +185,15 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const float4 *payload, const RaysDev &rays, int64_t n_rays,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
                               cudaStream_t st);
+// K6: needs bd.fwd_state and bd.fwd_segs (the forward of the same rays, k_march_rays_warp);
+// ray_list (list_cap entries) collects the rays whose lists the forward could not keep.
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
-                                 const BwdDev &bd, DevCounters *ctr, float *se, float *sx, int *sc,
-                                 cudaStream_t st);
+                                 const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
+                                 float *sx, int *sc, cudaStream_t st);
+// vpb_backward.cu: interleaved payload gradient -> planar GradBuffer (touched primitives)
+cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
+                                  bool accumulate, cudaStream_t st);
 cudaError_t launch_eval_rays(const CamDev *cams, int n_cams, const int *cam_index, const float *pixel_xy,
                              const int *pixel_id, int64_t n, int jitter, unsigned long long seed,
                              float *origins, float *dirs, float *jit, int *bad, cudaStream_t st);
