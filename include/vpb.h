@@ -269,6 +269,9 @@ int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, 
 /* Test hook: evaluates the device port of glibc expf used by window() (primitive.cpp:27)
  * elementwise, so the port can be checked exhaustively against the host libm. */
 int vp_debug_expf(vp_ctx *ctx, int64_t n, const float *x, float *y);
+/* Test hook: the device LBVH's stable radix sort (vpb_bvh.cu) of n 64-bit keys on bits [32, 62),
+ * host arrays (the replacement of buildLbvh's std::sort, lbvh.cpp:81-100). */
+int vp_debug_radix_sort(vp_ctx *ctx, int64_t n, const uint64_t *keys_in, uint64_t *keys_out);
 /* Test hook: the device port of glibc sinf (which = 0) / cosf (which = 1) used by the
  * device compose (rotationFromAxisAngle, rotation.cpp:19-22), elementwise. */
 int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t which);

@@ -92,6 +92,7 @@ SIGNATURES = {
     "vp_debug_tile_times": (C.c_int, [C.c_void_p, C.POINTER(vp_camera), C.POINTER(vp_march),
                                       C.POINTER(C.c_uint64), C.c_int64, i64p]),
     "vp_debug_expf": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p]),
+    "vp_debug_radix_sort": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vp_debug_sincos": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, C.c_int32]),
     "vp_debug_pose": (C.c_int, [C.c_void_p, C.c_int32, f32p, f32p, C.c_int32]),
     "vp_make_shell_scene": (C.c_int, [C.c_int32, C.c_int32, f32p, f32p]),

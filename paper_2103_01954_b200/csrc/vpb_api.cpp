@@ -1583,6 +1583,22 @@ int vp_debug_pose(vp_ctx *ctx, int32_t n_prim, const float *tr24, float *out36, 
     return VP_OK;
 }
 
+int vp_debug_radix_sort(vp_ctx *ctx, int64_t n, const uint64_t *keys_in, uint64_t *keys_out) {
+    if (int rc = check_ctx(ctx, false)) return rc;
+    if (n < 0 || n > (int64_t(1) << 26) || (n > 0 && (!keys_in || !keys_out)))
+        return fail(ctx, VP_ERR_USAGE, "bad arguments");
+    if (n == 0) return VP_OK;
+    DBuf<unsigned long long> k;
+    DBuf<unsigned> h;
+    VP_CUDA(ctx, k.ensure(2 * size_t(n)));
+    VP_CUDA(ctx, h.ensure(256 * size_t((n + 2047) / 2048)));
+    VP_CUDA(ctx, cudaMemcpyAsync(k.p, keys_in, 8 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    VP_CUDA(ctx, launch_radix_sort30(k.p, k.p + n, h.p, int(n), ctx->stream));
+    VP_CUDA(ctx, cudaMemcpyAsync(keys_out, k.p, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return VP_OK;
+}
+
 int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t which) {
     if (int rc = check_ctx(ctx, false)) return rc;
     if (n < 0 || (n > 0 && (!x || !y)) || which < 0 || which > 1) return fail(ctx, VP_ERR_USAGE, "bad arguments");

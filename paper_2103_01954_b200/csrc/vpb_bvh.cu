@@ -5,7 +5,8 @@
 //   k_bvh_boxes     padded world box per primitive (from the composed transform)
 //   k_bvh_bounds    one CTA: bounds of the box centres
 //   k_bvh_keys      (30-bit Morton code of the centre << 32) | primitive
-//   (sort)          CUB radix sort of the 62-bit keys
+//   k_radix_*       stable LSD radix sort of the keys on their 30 Morton bits (in-house: four
+//                   8-bit digit passes of tile histogram -> digit-major scan -> stable scatter)
 //   k_bvh_internal  Karras (2012) hierarchy from the sorted keys: one thread per internal node
 //   k_bvh_refit     bottom-up child boxes (second arrival at a node computes it)
 //
@@ -13,7 +14,6 @@
 // reports as a hit must never be pruned by float rounding in the world-space slab test.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cstdint>
 
 #include "vpb_bvh.cuh"
@@ -181,6 +181,111 @@ __global__ void k_bvh_refit(const unsigned long long *__restrict__ keys, int n, 
     }
 }
 
+// ---- stable LSD radix sort of 64-bit keys on bits [32, 62) ------------------------------------
+// A pass sorts on one 8-bit digit (the last one on 6 bits): (1) k_radix_hist counts the digits of
+// each tile of kRadixTile keys into hist[digit * n_tiles + tile]; (2) k_radix_scan, one CTA,
+// turns that digit-major table into exclusive offsets (digit-major order = the stable order);
+// (3) k_radix_scatter ranks each key inside its tile, in tile order, and writes it to
+// offset[digit][tile] + rank. The keys start in primitive order, so equal Morton codes keep
+// that order: the result is the order of the full 62-bit keys, as buildLbvh sorts them
+// (lbvh.cpp:81-100).
+constexpr int kRadixThreads = 256, kRadixItems = 8, kRadixTile = kRadixThreads * kRadixItems;
+constexpr int kRadixBins = 256;
+
+__device__ __forceinline__ unsigned radix_digit(unsigned long long key, int shift) {
+    return (unsigned)(key >> shift) & (kRadixBins - 1);
+}
+
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const unsigned long long *__restrict__ keys, int n,
+                                                              int shift, unsigned *__restrict__ hist, int n_tiles) {
+    __shared__ unsigned h[kRadixBins];
+    for (int b = threadIdx.x; b < kRadixBins; b += kRadixThreads) h[b] = 0u;
+    __syncthreads();
+    const int base = blockIdx.x * kRadixTile;
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const int i = base + r * kRadixThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[radix_digit(keys[i], shift)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kRadixBins; b += kRadixThreads) hist[b * n_tiles + blockIdx.x] = h[b];
+}
+
+// One CTA: exclusive scan of the m = 256 * n_tiles counts in place.
+__global__ void __launch_bounds__(1024) k_radix_scan(unsigned *__restrict__ hist, int m) {
+    __shared__ unsigned warp_sums[32];
+    __shared__ unsigned carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < m; base += 1024) {
+        const int i = base + tid;
+        const unsigned v = i < m ? hist[i] : 0u;
+        unsigned incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) warp_sums[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned ws = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += u;
+            }
+            warp_sums[lane] = ws;
+        }
+        __syncthreads();
+        const unsigned excl = carry + (wid ? warp_sums[wid - 1] : 0u) + incl - v;
+        if (i < m) hist[i] = excl;
+        __syncthreads();
+        if (tid == 1023) carry = excl + v;
+        __syncthreads();
+    }
+}
+
+// Stable scatter of one tile: kRadixItems rounds of kRadixThreads keys in index order. Inside a
+// round a key's rank among equal digits = its rank in its warp (__match_any_sync) + the counts of
+// the earlier warps + the keys of earlier rounds.
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const unsigned long long *__restrict__ in,
+                                                                 unsigned long long *__restrict__ out, int n,
+                                                                 int shift, const unsigned *__restrict__ offs,
+                                                                 int n_tiles) {
+    constexpr int kWarps = kRadixThreads / 32;
+    __shared__ unsigned run[kRadixBins];           // offset of the next key of each digit
+    __shared__ unsigned wcnt[kWarps][kRadixBins];  // per warp: its count, then its exclusive prefix
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int b = tid; b < kRadixBins; b += kRadixThreads) run[b] = offs[b * n_tiles + blockIdx.x];
+    const int base = blockIdx.x * kRadixTile;
+    for (int r = 0; r < kRadixItems; ++r) {
+        for (int b = tid; b < kWarps * kRadixBins; b += kRadixThreads) (&wcnt[0][0])[b] = 0u;
+        __syncthreads();
+        const int i = base + r * kRadixThreads + tid;
+        const bool valid = i < n;
+        const unsigned long long key = valid ? in[i] : 0ull;
+        const unsigned dg = valid ? radix_digit(key, shift) : kRadixBins;  // kRadixBins: no key
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        const unsigned below = __popc(peers & ((1u << lane) - 1u));
+        if (valid && below == 0) wcnt[wid][dg] = __popc(peers);  // the group's lowest lane
+        __syncthreads();
+        for (int b = tid; b < kRadixBins; b += kRadixThreads) {  // exclusive prefix over warps
+            unsigned acc = run[b];
+            for (int w = 0; w < kWarps; ++w) {
+                const unsigned c = wcnt[w][b];
+                wcnt[w][b] = acc;
+                acc += c;
+            }
+            run[b] = acc;
+        }
+        __syncthreads();
+        if (valid) out[wcnt[wid][dg] + below] = key;
+        __syncthreads();
+    }
+}
+
 // Scratch carve-up, shared by the size query and the build.
 struct BvhScratch {
     float4 *lo, *hi, *nlo, *nhi;
@@ -188,8 +293,9 @@ struct BvhScratch {
     int *parent;
     unsigned *flags;
     float *bounds;
-    void *cub_tmp;
-    size_t cub_bytes, total;
+    unsigned *hist;  // radix sort: 256 digits x tiles
+    int n_tiles;
+    size_t total;
 };
 static BvhScratch bvh_layout(int n, void *base) {
     BvhScratch s{};
@@ -209,13 +315,30 @@ static BvhScratch bvh_layout(int n, void *base) {
     s.parent = static_cast<int *>(take((size_t)(2 * n) * 4));
     s.flags = static_cast<unsigned *>(take((size_t)n * 4));
     s.bounds = static_cast<float *>(take(64));
-    cub::DeviceRadixSort::SortKeys(nullptr, s.cub_bytes, s.k0, s.k1, n, 32, 62);
-    s.cub_tmp = take(s.cub_bytes);
+    s.n_tiles = (n + kRadixTile - 1) / kRadixTile;
+    s.hist = static_cast<unsigned *>(take((size_t)kRadixBins * s.n_tiles * 4));
     s.total = off;
     return s;
 }
 
 size_t bvh_scratch_bytes(int n) { return n > 1 ? bvh_layout(n, nullptr).total : 0; }
+
+// The BVH's key sort alone (testing): sorts n keys on bits [32, 62), stable; keys/tmp device.
+cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n,
+                                cudaStream_t st) {
+    if (n <= 1) return cudaSuccess;
+    const int nt = (n + kRadixTile - 1) / kRadixTile;
+    unsigned long long *src = keys, *dst = tmp;
+    for (int shift = 32; shift < 62; shift += 8) {
+        k_radix_hist<<<nt, kRadixThreads, 0, st>>>(src, n, shift, hist, nt);
+        k_radix_scan<<<1, 1024, 0, st>>>(hist, kRadixBins * nt);
+        k_radix_scatter<<<nt, kRadixThreads, 0, st>>>(src, dst, n, shift, hist, nt);
+        unsigned long long *t = src;
+        src = dst;
+        dst = t;
+    }
+    return cudaGetLastError();  // an even number of passes: the result is back in keys
+}
 
 cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
                              cudaStream_t st) {
@@ -223,24 +346,30 @@ cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scr
     const BvhScratch sc = bvh_layout(n, scratch);
     if (sc.total > scratch_bytes) return cudaErrorInvalidValue;
     float4 *lo = sc.lo, *hi = sc.hi, *nlo = sc.nlo, *nhi = sc.nhi;
-    unsigned long long *k0 = sc.k0, *k1 = sc.k1;
+    unsigned long long *k0 = sc.k0, *k1 = sc.k1;  // radix ping-pong buffers
     int *parent = sc.parent;
     unsigned *flags = sc.flags;
     float *bounds = sc.bounds;
-    void *cub_tmp = sc.cub_tmp;
-    size_t cub_bytes = sc.cub_bytes;
     const int b = (n + 255) / 256;
     k_bvh_boxes<<<b, 256, 0, st>>>(xf16, n, lo, hi);
     k_bvh_bounds<<<1, 1024, 0, st>>>(xf16, n, bounds);
     k_bvh_keys<<<b, 256, 0, st>>>(xf16, n, bounds, k0);
-    // Only the 30 Morton bits are sorted: the keys start in primitive order and the radix sort
-    // is stable, so equal codes stay in index order, which is the full 62-bit key order
-    // (4 digit passes instead of 8).
-    cudaError_t e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, k0, k1, n, 32, 62, st);
-    if (e != cudaSuccess) return e;
-    k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(k1, n, nodes, parent);
+    // Only the 30 Morton bits are sorted (digits at bits 32, 40, 48, 56): the keys start in
+    // primitive order and the sort is stable, so equal codes stay in index order, which is the
+    // full 62-bit key order. Four passes ping-pong k0 -> k1 -> k0 -> k1 -> k0.
+    const int nt = sc.n_tiles;
+    unsigned long long *src = k0, *dst = k1;
+    for (int shift = 32; shift < 62; shift += 8) {
+        k_radix_hist<<<nt, kRadixThreads, 0, st>>>(src, n, shift, sc.hist, nt);
+        k_radix_scan<<<1, 1024, 0, st>>>(sc.hist, kRadixBins * nt);
+        k_radix_scatter<<<nt, kRadixThreads, 0, st>>>(src, dst, n, shift, sc.hist, nt);
+        unsigned long long *t = src;
+        src = dst;
+        dst = t;
+    }
+    k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(src, n, nodes, parent);
     cudaMemsetAsync(flags, 0, (size_t)n * 4, st);
-    k_bvh_refit<<<b, 256, 0, st>>>(k1, n, lo, hi, nodes, nlo, nhi, parent, flags);
+    k_bvh_refit<<<b, 256, 0, st>>>(src, n, lo, hi, nodes, nlo, nhi, parent, flags);
     return cudaGetLastError();
 }
 

@@ -215,6 +215,9 @@ cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_
 size_t bvh_scratch_bytes(int n);
 cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
                              cudaStream_t st);
+// the BVH's stable radix sort on key bits [32, 62) (testing); hist: 256 * ceil(n / 2048) words
+cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n,
+                                cudaStream_t st);
 cudaError_t launch_sincos(const float *x, float *y, int64_t n, bool want_cos, cudaStream_t st);
 cudaError_t launch_composite(const float *rgb, const float *alpha, const float *bg, float *out,
                              int64_t n_px, cudaStream_t st);

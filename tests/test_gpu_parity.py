@@ -376,3 +376,22 @@ def test_ring_views_batched_match_reference(renderer, group):
         assert sha(out.sample_counts) == d["samples"], f"view {v} samples"
         assert sha(out.alpha) == d["alpha"], f"view {v} alpha"
         assert sha(out.color) == d["rgb"], f"view {v} rgb"
+
+
+@pytest.mark.parametrize("n", [1, 2, 2047, 2048, 2049, 4096, 32768, 262144, 1 << 20])
+def test_bvh_radix_sort_is_stable_and_sorted(renderer, n):
+    """The in-house LSD radix sort that orders the device LBVH's (Morton << 32 | prim) keys
+    (vpb_bvh.cu, replacing buildLbvh's sort, lbvh.cpp:81-100): sorted on bits [32, 62) and stable,
+    i.e. the order of the full 62-bit keys, with many duplicate codes."""
+    import ctypes as C
+    rng = np.random.default_rng(n)
+    codes = rng.integers(0, 1 << 30, n, dtype=np.uint64)
+    codes[: n // 3] = codes[0]  # a run of equal codes (stability)
+    codes[n // 3: n // 2] &= np.uint64(0xff)  # only the low digit differs
+    rng.shuffle(codes)
+    keys = (codes << np.uint64(32)) | np.arange(n, dtype=np.uint64)
+    out = np.zeros(n, np.uint64)
+    p64 = C.POINTER(C.c_uint64)
+    rc = renderer._lib.vp_debug_radix_sort(renderer.ctx, n, keys.ctypes.data_as(p64), out.ctypes.data_as(p64))
+    assert rc == 0
+    assert np.array_equal(out, np.sort(keys))

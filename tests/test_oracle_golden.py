@@ -169,3 +169,30 @@ def test_reference_resident_scene_render_matches_digest():
     sc.close()
     assert tot == d["total_samples"]
     assert sha(samples) == d["samples"] and sha(alpha) == d["alpha"] and sha(rgb) == d["rgb"]
+
+
+@REF
+def test_gradcheck_fixture_pinned_to_reference():
+    """tests/golden/gradcheck.npz (oracle/gen_gradcheck.py): the reference's f32 evalLoss gradient
+    on the fixture scene reproduces the stored values bit for bit, and the f64 finite differences
+    agree with it within the generator's reported bound."""
+    from oracle.bindings import RefCore, ref_eval_loss
+    z = np.load(GOLDEN / "gradcheck.npz")
+
+    class Cam:
+        def __init__(self, c):
+            self.intrinsics, self.rotation = c[:9].reshape(3, 3).T, c[9:18].reshape(3, 3).T
+            self.translation, self.width, self.height = c[18:21], int(c[21]), int(c[22])
+
+    class MC:
+        step_size, early_eps, jitter, seed = float(z["cfg"][0]), float(z["cfg"][1]), False, 0
+
+    class W:
+        alpha, beta = 8.0, 8
+    w = z["weights"]
+    _, g = ref_eval_loss(RefCore(), z["tr"], int(z["m"]), z["payload"], W, [Cam(c) for c in z["cams"]],
+                         z["cam_index"], z["pixel"], z["pixel_id"], z["target"], z["background"], [w[0], w[2], w[3]], MC)
+    assert np.array_equal(g[z["index"]].view(np.uint32), z["ref_f32_analytic"].view(np.uint32))
+    fd = z["finite_diff"]
+    rel = np.abs(g[z["index"]] - fd) / np.maximum(np.abs(g[z["index"]]) + np.abs(fd), 1e-4)
+    assert rel.max() <= 1e-3
