@@ -14,10 +14,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vpb.h"
+#include "vpb_hostcopy.hpp"
 #include "vpb_hostmath.hpp"
 #include "vpb_kernels.h"
 
@@ -58,6 +61,7 @@ bool is_device_ptr(const void *p) {
 }
 
 constexpr int kTimingSlots = 256;  // march-kernel event pairs kept for vp_kernel_times
+constexpr size_t kStageBytes = size_t(8) << 20;  // host slab upload chunk (upload_planar_host)
 
 }  // namespace
 
@@ -133,6 +137,17 @@ struct vp_ctx {
     DBuf<float> g_pay4;
     DBuf<unsigned> g_touched;
     DBuf<int> bwd_list;  // K6: rays whose segment lists the forward did not keep
+    // host slab uploads (upload_planar_host): page-locked + device staging chunks, their
+    // transfer events, and the host copy threads
+    static constexpr int kStageSlots = 4;
+    float *stage_h[kStageSlots] = {};
+    size_t stage_h_floats[kStageSlots] = {};
+    DBuf<float> stage_d[kStageSlots];
+    cudaEvent_t ev_stage[kStageSlots] = {};
+    std::unique_ptr<CopyPool> copy_pool;
+    void *out_stage = nullptr;  // copy_out_host: page-locked staging of pageable outputs
+    size_t out_stage_bytes = 0;
+    cudaEvent_t ev_out[3] = {};
     // off by default: the kernel runs 14 % faster with vector reductions, but the transpose
     // into the planar GradBuffer costs more than that (K6); VPB_BWD_LAYOUT=v4 enables it
     bool bwd_v4 = false;
@@ -473,6 +488,13 @@ int vp_create(int32_t device, vp_ctx **out) {
         (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_xf_marched[1], cudaEventDisableTiming)) != cudaSuccess ||
 
+        (e = cudaEventCreateWithFlags(&ctx->ev_out[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_out[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_out[2], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_stage[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_stage[1], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_stage[2], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_stage[3], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_keys[0], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_keys[1], cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaHostAlloc(&ctx->h_keys, sizeof(unsigned long long) * 2 * kMaxViews, cudaHostAllocMapped)) !=
@@ -557,6 +579,15 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->g_pay4.release();
     ctx->g_touched.release();
     ctx->bwd_list.release();
+    for (int i = 0; i < vp_ctx::kStageSlots; ++i) {
+        if (ctx->stage_h[i]) cudaFreeHost(ctx->stage_h[i]);
+        ctx->stage_d[i].release();
+        if (ctx->ev_stage[i]) cudaEventDestroy(ctx->ev_stage[i]);
+    }
+    ctx->copy_pool.reset();
+    if (ctx->out_stage) cudaFreeHost(ctx->out_stage);
+    for (cudaEvent_t ev : ctx->ev_out)
+        if (ev) cudaEventDestroy(ev);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t ev : ctx->t_ev)
@@ -671,6 +702,100 @@ int vp_get_transforms(vp_ctx *ctx, float *xf15) {
     return VP_OK;
 }
 
+// A host planar slab (pageable, e.g. the reference Scene's std::vector) into the resident
+// interleaved payload: chunks of whole primitives go pageable -> page-locked staging (the copy
+// pool's threads) -> device staging (copy engine) -> K0 repack, double-buffered, so the host
+// copies of the next chunks overlap the transfer and repack of chunk i (four slots: the host
+// copy outruns PCIe, so the copy engine never waits). Page-locked callers skip the
+// host copy. The staging buffers persist in the context.
+static int upload_planar_host(vp_ctx *ctx, const float *payload, int64_t n_prim, int64_t m3) {
+    cudaStream_t st = ctx->stream;
+    const size_t per_prim = 4 * size_t(m3);  // floats
+    const size_t chunk_prims = std::max<size_t>(1, kStageBytes / (per_prim * 4));
+    const size_t chunk_floats = chunk_prims * per_prim;
+    cudaPointerAttributes attr{};
+    const bool pinned =
+        cudaPointerGetAttributes(&attr, payload) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    for (int i = 0; i < vp_ctx::kStageSlots; ++i) {
+        VP_CUDA(ctx, ctx->stage_d[i].ensure(chunk_floats));
+        if (!pinned && ctx->stage_h_floats[i] < chunk_floats) {
+            if (ctx->stage_h[i]) cudaFreeHost(ctx->stage_h[i]);
+            ctx->stage_h[i] = nullptr;
+            ctx->stage_h_floats[i] = 0;
+            VP_CUDA(ctx, cudaMallocHost(&ctx->stage_h[i], chunk_floats * sizeof(float)));
+            ctx->stage_h_floats[i] = chunk_floats;
+        }
+    }
+    if (!pinned && !ctx->copy_pool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->copy_pool = std::make_unique<CopyPool>(int(std::min(7u, hw > 1 ? hw - 1 : 0u)));
+    }
+    int slot = 0;
+    for (size_t k0 = 0; k0 < size_t(n_prim); k0 += chunk_prims, slot = (slot + 1) % vp_ctx::kStageSlots) {
+        const size_t nk = std::min(chunk_prims, size_t(n_prim) - k0), nfl = nk * per_prim;
+        const float *src = payload + k0 * per_prim;
+        if (!pinned) {  // the staging slot is free once its previous transfer has run
+            VP_CUDA(ctx, cudaEventSynchronize(ctx->ev_stage[slot]));
+            ctx->copy_pool->copy(ctx->stage_h[slot], src, nfl * sizeof(float));
+            src = ctx->stage_h[slot];
+        }
+        VP_CUDA(ctx, cudaMemcpyAsync(ctx->stage_d[slot].p, src, nfl * sizeof(float), cudaMemcpyHostToDevice, st));
+        VP_CUDA(ctx, cudaEventRecord(ctx->ev_stage[slot], st));
+        VP_CUDA(ctx, launch_repack(ctx->stage_d[slot].p, ctx->payload.p + k0 * size_t(m3), int64_t(nk), m3, st));
+    }
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    return VP_OK;
+}
+
+// Device results into caller host memory. Page-locked destinations take a direct copy;
+// pageable ones (e.g. the reference's RenderOutput vectors) are staged through one page-locked
+// buffer, each array copied out by the copy pool as soon as its own transfer has landed.
+struct HostOut {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+static int copy_out_host(vp_ctx *ctx, const HostOut *outs, int n, cudaStream_t st) {
+    size_t staged = 0;
+    bool pageable[3] = {};
+    for (int i = 0; i < n; ++i) {
+        cudaPointerAttributes attr{};
+        pageable[i] = !(cudaPointerGetAttributes(&attr, outs[i].dst) == cudaSuccess &&
+                        attr.type == cudaMemoryTypeHost);
+        cudaGetLastError();
+        if (pageable[i]) staged += (outs[i].bytes + 255) & ~size_t(255);
+    }
+    if (staged > ctx->out_stage_bytes) {
+        if (ctx->out_stage) cudaFreeHost(ctx->out_stage);
+        ctx->out_stage = nullptr;
+        ctx->out_stage_bytes = 0;
+        VP_CUDA(ctx, cudaMallocHost(&ctx->out_stage, staged));
+        ctx->out_stage_bytes = staged;
+    }
+    if (staged && !ctx->copy_pool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->copy_pool = std::make_unique<CopyPool>(int(std::min(7u, hw > 1 ? hw - 1 : 0u)));
+    }
+    size_t off = 0;
+    unsigned char *stage = static_cast<unsigned char *>(ctx->out_stage);
+    for (int i = 0; i < n; ++i) {
+        void *dst = pageable[i] ? stage + off : outs[i].dst;
+        VP_CUDA(ctx, cudaMemcpyAsync(dst, outs[i].src, outs[i].bytes, cudaMemcpyDeviceToHost, st));
+        VP_CUDA(ctx, cudaEventRecord(ctx->ev_out[i], st));
+        if (pageable[i]) off += (outs[i].bytes + 255) & ~size_t(255);
+    }
+    off = 0;
+    for (int i = 0; i < n; ++i) {
+        VP_CUDA(ctx, cudaEventSynchronize(ctx->ev_out[i]));
+        if (!pageable[i]) continue;
+        ctx->copy_pool->copy(outs[i].dst, stage + off, outs[i].bytes);
+        off += (outs[i].bytes + 255) & ~size_t(255);
+    }
+    VP_CUDA(ctx, cudaStreamSynchronize(st));
+    return VP_OK;
+}
+
 int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
                  const float *payload, float window_alpha, int32_t window_beta) {
     if (int rc = check_ctx(ctx, false)) return rc;
@@ -698,16 +823,10 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     const size_t nf = size_t(n_prim) * 4 * size_t(m3);
     VP_CUDA(ctx, ctx->payload.ensure(size_t(n_prim) * size_t(m3)));
     if (!payload) return VP_OK;  // filled later by vp_set_payload_interleaved
-    const float *src = payload;
-    if (!is_device_ptr(payload)) {
-        VP_CUDA(ctx, ctx->planar_tmp.ensure(nf));
-        VP_CUDA(ctx, cudaMemcpyAsync(ctx->planar_tmp.p, payload, nf * sizeof(float),
-                                     cudaMemcpyHostToDevice, ctx->stream));
-        src = ctx->planar_tmp.p;
-    }
-    VP_CUDA(ctx, launch_repack(src, ctx->payload.p, n_prim, m3, ctx->stream));
+    if (!is_device_ptr(payload)) return upload_planar_host(ctx, payload, n_prim, m3);
+    VP_CUDA(ctx, launch_repack(payload, ctx->payload.p, n_prim, m3, ctx->stream));
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    ctx->planar_tmp.release();
+    (void)nf;
     return VP_OK;
 }
 
@@ -1002,11 +1121,12 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
         const DevCounters c = *ctx->h_ctr;
         note_density(ctx, c);
         note_keys(ctx, c.keys);  // overflowed tiles were marched by K5b; size for the next render
-        if (!d_rgb) VP_CUDA(ctx, cudaMemcpyAsync(rgb, od.rgb, n_px * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
-        if (!d_alpha) VP_CUDA(ctx, cudaMemcpyAsync(alpha, od.alpha, n_px * sizeof(float), cudaMemcpyDeviceToHost, st));
-        if (samples && !d_samp)
-            VP_CUDA(ctx, cudaMemcpyAsync(samples, od.samples, n_px * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        VP_CUDA(ctx, cudaStreamSynchronize(st));
+        HostOut outs[3];
+        int n_out = 0;
+        if (!d_rgb) outs[n_out++] = HostOut{rgb, od.rgb, n_px * 3 * sizeof(float)};
+        if (!d_alpha) outs[n_out++] = HostOut{alpha, od.alpha, n_px * sizeof(float)};
+        if (samples && !d_samp) outs[n_out++] = HostOut{samples, od.samples, n_px * sizeof(int32_t)};
+        if (int rc = copy_out_host(ctx, outs, n_out, st)) return rc;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         fill_stats(c, ms, stats);

@@ -604,36 +604,6 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
     }
 }
 
-// march() over caller rays (one thread per ray, all primitives as candidates).
-template <int CAP, int kRayThreads>
-__global__ void __launch_bounds__(kRayThreads)
-k_march_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
-             const float4 *__restrict__ payload, RaysDev rays, int64_t n_rays, OutDev od,
-             DevCounters *ctr, int *__restrict__ ovf_list, int ovf_cap) {
-    __shared__ unsigned long long s_tab[32];
-    __shared__ float s_we[CAP * kRayThreads], s_wx[CAP * kRayThreads];
-    __shared__ int s_wc[CAP * kRayThreads];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
-    __syncthreads();
-    const int64_t r = blockIdx.x * (int64_t)kRayThreads + threadIdx.x;
-    const bool valid = r < n_rays;
-    RayOut ro{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (valid) {
-        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
-        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
-        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
-        const Window<int> w{s_we, s_wx, s_wc, kRayThreads, (int)threadIdx.x};
-        ro = march_ray<CAP>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
-        if (ro.overflow) {
-            const int slot = (int)atomicAdd(&ctr->overflow_rays, 1ull);
-            if (slot < ovf_cap) ovf_list[slot] = (int)r;
-        }
-    }
-    if (valid && !ro.overflow) write_ray(od, r, ro);
-    add_counters(ctr, ro, valid && !ro.overflow);
-}
-
 // march() over caller rays, one warp per ray (small batches): the warp builds the ray's whole
 // sorted segment list through the BVH (warp_segment_list) in shared memory, then walks
 // it 32 lattice steps at a time (march_warp). Rays with more than kWarpList segments go to the
@@ -709,7 +679,6 @@ __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64
 #ifndef VPB_WINDOW_CAP
 #define VPB_WINDOW_CAP 14
 #endif
-constexpr int kRayWindowCap = 20;  // per-ray segment window of k_march_rays (vp_march_rays)
 
 // Three raymarch configurations, chosen per render from the previous render's mean
 // candidates per non-empty tile (vpb_api.cpp). The kernel is bound by gather latency, so each
@@ -835,13 +804,15 @@ static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const f
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t smem = tiles_smem<Cfg::CAP, Cfg::CC, Cfg::NT>();
-    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, Cfg::MINB, Cfg::PF, Cfg::NT>;
+    // a runtime voxel count needs a few more registers: one CTA fewer per SM instead of spills
+    constexpr int MINB = MT == 0 && Cfg::MINB > 2 ? Cfg::MINB - 1 : Cfg::MINB;
+    auto kern = k_march_tiles<Cfg::CAP, MT, PROF, Cfg::CC, MINB, Cfg::PF, Cfg::NT>;
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // Ask for just the shared memory MINB resident CTAs need (each also reserves 1 KB):
         // the rest of the 256 KB unified array stays L1 cache for the payload gathers.
         int carve = VPB_CARVEOUT;
-        if (carve < 0) carve = (int)((Cfg::MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+        if (carve < 0) carve = (int)((MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve > 100 ? 100 : carve);
         if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
@@ -856,6 +827,8 @@ static cudaError_t launch_tiles_cfg(const MarchDev &mp, const float *xf16, const
 #define VPB_TILES(MT) (prof ? launch_tiles_m<Cfg, MT, true>(mp, xf16, payload, views, order, n_ctas, st) \
                             : launch_tiles_m<Cfg, MT, false>(mp, xf16, payload, views, order, n_ctas, st))
     switch (mp.m) {  // compile-time voxel counts for the common grids
+    case 1: return VPB_TILES(1);
+    case 2: return VPB_TILES(2);
     case 4: return VPB_TILES(4);
     case 8: return VPB_TILES(8);
     case 16: return VPB_TILES(16);
@@ -1080,12 +1053,10 @@ cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const March
                                   const unsigned long long *entries, const OutDev &od,
                                   const RaysDev &rays, DevCounters *ctr, const int *ovf_list,
                                   int ovf_cap, float *se, float *sx, int *sc, cudaStream_t st) {
-    if (rays_mode)
-        k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-            cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
-    else
-        k_march_fallback<false><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-            cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+    // camera renders re-march their overflow rays in k_march_fallback_views
+    if (!rays_mode) return cudaErrorInvalidValue;
+    k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
+        cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
     return cudaGetLastError();
 }
 
@@ -1096,24 +1067,11 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
     if (n_rays == 0) return cudaSuccess;
     // Each ray is a serial latency chain, so rays are marched a warp per ray, 32 lattice steps
     // at a time. Since the warp walks the BVH cooperatively (warp_bvh_leaves) this wins at
-    // every batch size measured (65,536 rays: 1.05 -> 0.7 ms against one thread per ray).
-    // VPB_FWD_WARP_MAX (tuning builds) sends larger batches to the thread-per-ray kernel:
-    // one-warp CTAs for mid-size batches so they spread over every SM, 128-thread CTAs beyond.
-#ifndef VPB_FWD_WARP_MAX
-#define VPB_FWD_WARP_MAX INT64_MAX
-#endif
-    if (n_rays <= (int64_t)VPB_FWD_WARP_MAX) {
-        const int64_t blocks = (n_rays + 3) / 4;
-        k_march_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
-            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
-        return cudaGetLastError();
-    }
-    if (n_rays < 148 * 128 * 2)
-        k_march_rays<kRayWindowCap, 32><<<(unsigned)((n_rays + 31) / 32), 32, 0, st>>>(
-            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
-    else
-        k_march_rays<kRayWindowCap, 128><<<(unsigned)((n_rays + 127) / 128), 128, 0, st>>>(
-            mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
+    // every batch size measured (65,536 rays: 1.05 -> 0.7 ms against one thread per ray, a
+    // kernel since removed).
+    const int64_t blocks = (n_rays + 3) / 4;
+    k_march_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
+        mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
     return cudaGetLastError();
 }
 
