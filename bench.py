@@ -54,6 +54,11 @@ def parse():
     p.add_argument("--width", type=int, default=1024)
     p.add_argument("--views-per-gpu", type=int, default=8)
     p.add_argument("--no-gather", action="store_true")
+    p.add_argument("--torch-comm", action="store_true",
+                   help="N > 1: gather / broadcast with torch.distributed NCCL instead of libvpb's vp_comm_*")
+    p.add_argument("--nccl-max-ctas", type=int, default=8, help="libvpb NCCL communicator's CTA cap")
+    p.add_argument("--comm-at-1", action="store_true",
+                   help="N = 1: run the N > 1 data plane anyway (a 1-rank communicator; testing)")
     p.add_argument("--per-view", action="store_true",
                    help="one raymarch launch per view instead of one per step (vp_render_batch_async)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
@@ -437,19 +442,26 @@ def main():
 
     from paper_2103_01954_b200 import Renderer, api, synthetic
     from paper_2103_01954_b200._lib import f32p, i32p, vp_camera, vp_march, vp_stats
-    from paper_2103_01954_b200.dist import ViewGather, broadcast_scene, view_shard
+    from paper_2103_01954_b200.dist import NativeComm, NativeViewGather, ViewGather, broadcast_scene, view_shard
     import ctypes as C
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    # data plane: libvpb's own NCCL (vp_comm_*), so torch.distributed is only the control plane
+    # (rendezvous, the NCCL id, barriers, the max-over-ranks timing): gloo on CPU tensors.
+    # --torch-comm (and the tile-shard mode) move the data plane to torch.distributed NCCL.
+    native = (world > 1 or args.comm_at_1) and not (args.torch_comm or args.tile_shard)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if native:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     if args.tile_shard:
         run_tile_shard(args, rank, world, local, device)
         if world > 1:
             dist.destroy_process_group()
         return
-    gather = world > 1 and not args.no_gather
+    gather = (world > 1 or native) and not args.no_gather
     k, m, w = args.k, args.m, args.width
     V = args.views_per_gpu
     r = Renderer(local)
@@ -462,7 +474,11 @@ def main():
         slab = api.PrimitiveSlab(k, m, pay)
     win = api.WindowParams()
     t_up = time.perf_counter()
-    if world > 1:
+    comm = None
+    if native:
+        comm = NativeComm(r, world, rank, max_ctas=args.nccl_max_ctas)
+        bcast_bytes = comm.broadcast_scene(xf, slab, win, k, m)
+    elif world > 1:
         bcast_bytes = broadcast_scene(r, xf, slab, win, k, m, device)
     else:
         r.set_scene_composed(xf, slab, win)
@@ -507,7 +523,7 @@ def main():
     del sv_out
     r.kernel_times()
 
-    vg = ViewGather(V, w, w, device, world, rank)
+    vg = NativeViewGather(comm, V, w, w, device) if native else ViewGather(V, w, w, device, world, rank)
     # a dedicated (non-default) stream: the renders, the timing events and the NCCL gathers'
     # dependencies all hang off it
     stream = torch.cuda.Stream(device)
@@ -531,13 +547,18 @@ def main():
         # stream under step i+1's raymarch (which renders into the other slot)
         slot = i % vg.slots
         if gather:
-            vg.wait_slot(slot)
+            if native:  # the render stream waits for the gathers still reading this slot
+                vg.wait_slot(slot, sh)
+            else:
+                vg.wait_slot(slot)
         rgb_ptrs, alpha_ptrs, samp_ptrs = slot_ptrs[slot]
         if batch:  # every view of the step in one raymarch launch
             if lib.vp_render_batch_async(r.ctx, V, cams_arr, C.byref(mc), rgb_ptrs, alpha_ptrs, samp_ptrs,
                                          C.c_void_p(sh)):
                 raise RuntimeError(lib.vp_last_error(r.ctx).decode())
-            if gather:
+            if gather and native:  # every view of the step in ONE grouped NCCL call
+                vg.gather(slot)
+            elif gather:
                 for j in range(V):
                     vg.gather_view(j, slot=slot)
         else:
@@ -546,8 +567,10 @@ def main():
                                          samp_ptrs[j], C.c_void_p(sh))
                 if rc:
                     raise RuntimeError(lib.vp_last_error(r.ctx).decode())
-                if gather:
+                if gather and not native:
                     vg.gather_view(j, slot=slot)
+            if gather and native:
+                vg.gather(slot)
 
     for i in range(args.warmup):
         step(i)
@@ -580,12 +603,13 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_local = sum(step_ms) / 1e3
     march_ms = r.kernel_times(4096)
-    t = torch.tensor([t_local], dtype=torch.float64, device=device)
+    cdev = "cpu" if native else device  # gloo reduces CPU tensors
+    t = torch.tensor([t_local], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     totals = torch.tensor([ray_samples * args.steps, prim_samples * args.steps, V * args.steps],
-                          dtype=torch.float64, device=device)
+                          dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(totals)
     all_ray, all_prim, all_views = (float(x) for x in totals.tolist())
@@ -628,13 +652,8 @@ def main():
         h_rgb_p = (f32p * V)(*[C.cast(h_rgb[j].data_ptr(), f32p) for j in range(V)])
         h_alpha_p = (f32p * V)(*[C.cast(h_alpha[j].data_ptr(), f32p) for j in range(V)])
         h_samp_p = (i32p * V)(*[C.cast(h_samp[j].data_ptr(), i32p) for j in range(V)])
-        if world > 1:
-            xf_host = torch.empty((k, 15), dtype=torch.float32)
-            xf_dev = torch.empty((k, 15), dtype=torch.float32, device=device)
-            if rank == 0:
-                xf_dev.copy_(torch.from_numpy(xf))
-            dist.broadcast(xf_dev, 0)
-            xf_host = xf_dev.cpu().pin_memory()
+        if world > 1:  # every rank holds the broadcast transforms
+            xf_host = torch.from_numpy(np.ascontiguousarray(r.transforms())).pin_memory()
         else:
             xf_host = torch.from_numpy(xf).pin_memory()
         st = vp_stats()
@@ -671,7 +690,7 @@ def main():
         for _ in range(n_e2e):
             e2e_step()
         e2e_finish()
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(all_ray / args.steps * n_e2e / float(te.item()) / 1e6, 3), "unit": METRIC,
@@ -711,12 +730,17 @@ def main():
                 # raymarch and one fallback launch; per view: 6 + 2 launches for each view
                 "gpu_launches": (9 if batch else 8 * V) * args.steps,
                 "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
+                "data_plane": ("libvpb vp_comm_* (NCCL: vp_broadcast_scene once, one grouped vp_gather_views per "
+                               f"step, maxCTAs {args.nccl_max_ctas}; torch.distributed gloo for control only)"
+                               if native else ("torch.distributed NCCL" if world > 1 else "none (1 GPU)")),
                 "single_view": {"ms": round(single_view_ms, 4), "frames_per_s": round(1e3 / single_view_ms, 1),
                                 "what": "one view per raymarch launch (vp_render_async, back to back), "
                                         f"median of 20, view {views[0]} of the ring"},
                 "scene_upload_ms": round(scene_upload_ms, 2),
                 "stats_last_launch": rc_stats.as_dict()}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     r.close()

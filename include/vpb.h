@@ -280,6 +280,49 @@ int vp_debug_sincos(vp_ctx *ctx, int64_t n, const float *x, float *y, int32_t wh
  * computed by the device kernel (on_device = 1) or the host restatement (0). */
 int vp_debug_pose(vp_ctx *ctx, int32_t n_prim, const float *transforms24, float *out36, int32_t on_device);
 
+/* ---- multi-GPU: NCCL over NVLink / NVSwitch inside libvpb -----------------
+ * The path shards by view or image tile with no data-path collective; the only traffic is one
+ * broadcast of the scene and the gather of outputs to a root. The reference parallelises over
+ * rows inside one process (threads.h:16-36, used at march.cpp:112); these calls are its
+ * multi-GPU counterpart, for C++ callers of the drop-in (no torch needed). A vp_comm belongs
+ * to one context (its device); collectives run on the communicator's own stream. */
+#define VP_COMM_ID_BYTES 128
+typedef struct vp_comm vp_comm;
+/* A fresh NCCL unique id (VP_COMM_ID_BYTES); rank 0 creates it and shares it out of band. */
+int vp_comm_unique_id(uint8_t *id);
+/* One process per GPU: joins the n_ranks communicator as `rank` on ctx's device. max_ctas > 0
+ * caps NCCL's CTAs (ncclConfig_t.maxCTAs) so a gather overlapping the next raymarch takes few
+ * SMs; 0 = NCCL's default. */
+int vp_comm_init(vp_ctx *ctx, const uint8_t *id, int32_t n_ranks, int32_t rank, int32_t max_ctas,
+                 vp_comm **out);
+/* One process driving n GPUs: ctxs[i] (created on devices[i]) becomes rank i of one
+ * communicator (the ncclCommInitAll pattern); out receives n communicators. Collectives of this
+ * mode are issued for every rank between vp_group_start and vp_group_end. */
+int vp_comm_init_all(int32_t n, vp_ctx *const *ctxs, const int32_t *devices, int32_t max_ctas, vp_comm **out);
+int vp_comm_destroy(vp_comm *comm);
+int vp_group_start(void);
+int vp_group_end(void);
+/* Every rank first calls vp_set_scene with the same K and M: the root with its transforms and
+ * payload, the others with NULL for both (shape only). Then the root's composed transforms and
+ * repacked interleaved payload are broadcast, so only the root runs K0. Stream-ordered: the
+ * other ranks' next renders wait for the broadcast. */
+int vp_broadcast_scene(vp_comm *comm, int32_t root);
+/* Gathers n_views rendered views of every rank to the root in one NCCL group, after the
+ * context's renders so far. rgb/alpha/samples: this rank's n_views DEVICE outputs of n_px
+ * pixels (samples NULL on every rank or on none). dst_*: on the root, n_ranks * n_views device
+ * pointers (rank r's view j at r * n_views + j; the root's own views are copied on the device),
+ * NULL on the other ranks. Asynchronous: see vp_comm_wait / vp_comm_sync. */
+int vp_gather_views(vp_comm *comm, int32_t root, int32_t n_views, int64_t n_px, float *const *rgb,
+                    float *const *alpha, int32_t *const *samples, float *const *dst_rgb, float *const *dst_alpha,
+                    int32_t *const *dst_samples);
+/* `stream` (NULL: the context's) waits for the communicator's work so far (e.g. before a render
+ * overwrites outputs a gather is still sending). */
+int vp_comm_wait(vp_comm *comm, void *stream);
+/* Blocks until the communicator's work so far has completed. */
+int vp_comm_sync(vp_comm *comm);
+/* Message of the last failing vp_comm_* / vp_group_* call made without a context. */
+const char *vp_comm_last_error(void);
+
 /* ---- synthetic benchmark inputs ("mvp_shell"), host only ------------------ */
 /* transforms24: K*24, payload_planar: K*4*M^3 (either may be NULL to skip). */
 int vp_make_shell_scene(int32_t n_prim, int32_t m, float *transforms24, float *payload_planar);

@@ -95,6 +95,19 @@ SIGNATURES = {
     "vp_debug_radix_sort": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "vp_debug_sincos": (C.c_int, [C.c_void_p, C.c_int64, f32p, f32p, C.c_int32]),
     "vp_debug_pose": (C.c_int, [C.c_void_p, C.c_int32, f32p, f32p, C.c_int32]),
+    "vp_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "vp_comm_init": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
+                               C.POINTER(C.c_void_p)]),
+    "vp_comm_init_all": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), i32p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "vp_comm_destroy": (C.c_int, [C.c_void_p]),
+    "vp_group_start": (C.c_int, []),
+    "vp_group_end": (C.c_int, []),
+    "vp_broadcast_scene": (C.c_int, [C.c_void_p, C.c_int32]),
+    "vp_gather_views": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.POINTER(f32p), C.POINTER(f32p),
+                                  C.POINTER(i32p), C.POINTER(f32p), C.POINTER(f32p), C.POINTER(i32p)]),
+    "vp_comm_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "vp_comm_sync": (C.c_int, [C.c_void_p]),
+    "vp_comm_last_error": (C.c_char_p, []),
     "vp_make_shell_scene": (C.c_int, [C.c_int32, C.c_int32, f32p, f32p]),
     "vp_look_at_camera": (C.c_int, [f32p, f32p, f32p, C.c_float, C.c_int32, C.c_int32,
                                     C.POINTER(vp_camera), f32p]),

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/vpb.h"
+#include "vpb_ctx_internal.h"
 #include "vpb_hostcopy.hpp"
 #include "vpb_hostmath.hpp"
 #include "vpb_kernels.h"
@@ -97,6 +98,10 @@ struct vp_ctx {
     DBuf<int> flag;        // device error flag (compose)
     bool has_xf = false;   // resident composed transforms are set
     DBuf<float4> payload;
+    // derived x-pair layout of the payload for the raymarch's 256-bit gathers (march_uses_pairs);
+    // rebuilt before the next raymarch whenever the payload may have changed
+    DBuf<float4> pairs;
+    bool pairs_dirty = true;
     BinSlot slot[2 * kMaxViews];
     int cur = 0;    // slot of the latest render's last view
     int group = 0;  // slot group of the latest launch
@@ -360,7 +365,13 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     const int slot = int(ctx->t_count % kTimingSlots);
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot], st));
     if (n == 1 && n_ctas_single >= 0) total = n_ctas_single;
-    VP_CUDA(ctx, launch_march_tiles(mp, ctx->xfb[ctx->xfi].p, ctx->payload.p, vb, order, total, ods[0].prof != nullptr,
+    if (march_uses_pairs(ctx->m) && ctx->pairs_dirty) {  // the raymarch's x-pair layout, after a payload change
+        VP_CUDA(ctx, ctx->pairs.ensure(2 * size_t(ctx->n_prim) * ctx->m * ctx->m * (ctx->m - 1)));
+        VP_CUDA(ctx, launch_build_pairs(ctx->payload.p, ctx->pairs.p, ctx->n_prim, ctx->m, st));
+        ctx->pairs_dirty = false;
+    }
+    VP_CUDA(ctx, launch_march_tiles(mp, ctx->xfb[ctx->xfi].p, ctx->payload.p, ctx->pairs.p, vb, order, total,
+                                    ods[0].prof != nullptr,
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
                                              ctx->fb_x.p, ctx->fb_c.p, ctx->ovf_tile_lists.p, st));
@@ -439,6 +450,38 @@ int check_cam(vp_ctx *ctx, const vp_camera *cam) {
 }
 
 }  // namespace
+
+namespace vpb {
+
+int ctx_scene(vp_ctx *ctx, CtxScene *out) {
+    if (!ctx) return fail(nullptr, VP_ERR_USAGE, "null context");
+    if (!ctx->has_scene) return fail(ctx, VP_ERR_USAGE, "no scene set (vp_set_scene first)");
+    const size_t k = size_t(ctx->n_prim);
+    if (k > 0) {  // a receiving context may hold only the shape (vp_set_scene with NULL data)
+        VP_CUDA(ctx, ctx->xfb[ctx->xfi].ensure(16 * k));
+        VP_CUDA(ctx, ctx->payload.ensure(k * size_t(ctx->m) * ctx->m * ctx->m));
+    }
+    *out = CtxScene{ctx->xfb[ctx->xfi].p, ctx->payload.p, ctx->n_prim, ctx->m, ctx->device, ctx->stream};
+    return VP_OK;
+}
+
+int ctx_scene_written(vp_ctx *ctx, cudaStream_t st) {
+    ctx->has_xf = true;
+    ctx->bvh_dirty = true;
+    ctx->pairs_dirty = true;
+    VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf, st));  // enqueue_views' binning waits for ev_xf
+    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_xf, 0));
+    return VP_OK;
+}
+
+int ctx_wait_renders(vp_ctx *ctx, cudaStream_t st) {
+    VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_last_marched, 0));
+    return VP_OK;
+}
+
+int ctx_fail(vp_ctx *ctx, int code, const std::string &msg) { return fail(ctx, code, msg); }
+
+}  // namespace vpb
 
 extern "C" {
 
@@ -822,6 +865,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     const int64_t m3 = int64_t(m) * m * m;
     const size_t nf = size_t(n_prim) * 4 * size_t(m3);
     VP_CUDA(ctx, ctx->payload.ensure(size_t(n_prim) * size_t(m3)));
+    ctx->pairs_dirty = true;
     if (!payload) return VP_OK;  // filled later by vp_set_payload_interleaved
     if (!is_device_ptr(payload)) return upload_planar_host(ctx, payload, n_prim, m3);
     VP_CUDA(ctx, launch_repack(payload, ctx->payload.p, n_prim, m3, ctx->stream));
@@ -838,6 +882,7 @@ int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const flo
     if (!inter) return fail(ctx, VP_ERR_USAGE, "null payload");
     const size_t n4 = size_t(n_prim) * size_t(m) * m * m;
     VP_CUDA(ctx, ctx->payload.ensure(n4));
+    ctx->pairs_dirty = true;
     if ((const void *)inter != (const void *)ctx->payload.p)
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->payload.p, inter, n4 * sizeof(float4),
                                      is_device_ptr(inter) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -848,6 +893,7 @@ int vp_set_payload_interleaved(vp_ctx *ctx, int32_t n_prim, int32_t m, const flo
 
 int vp_payload_device(vp_ctx *ctx, float **dev_ptr, int64_t *n_floats) {
     if (int rc = check_ctx(ctx, true, false)) return rc;
+    ctx->pairs_dirty = true;  // the caller may write through the pointer (a broadcast's destination)
     if (dev_ptr) *dev_ptr = reinterpret_cast<float *>(ctx->payload.p);
     if (n_floats) *n_floats = int64_t(ctx->n_prim) * ctx->m * ctx->m * ctx->m * 4;
     return VP_OK;
@@ -1598,6 +1644,7 @@ int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf1
             return fail(ctx, VP_ERR_FORMAT, std::string("truncated slab payload: ") + path);
         VP_CUDA(ctx, cudaMemcpyAsync(dev[slot].p, pinned[slot], nf * 4, cudaMemcpyHostToDevice, ctx->stream));
         VP_CUDA(ctx, launch_repack(dev[slot].p, ctx->payload.p + k0 * m3, int64_t(nk), int64_t(m3), ctx->stream));
+        ctx->pairs_dirty = true;
         VP_CUDA(ctx, cudaEventRecord(done[slot], ctx->stream));
     }
     VP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1657,6 +1704,7 @@ int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *tra
     const int step = ctx->adam_step + 1;
     c.bc1 = 1 - std::pow(cfg->beta1, float(step));  // losses.cpp:79-80
     c.bc2 = 1 - std::pow(cfg->beta2, float(step));
+    ctx->pairs_dirty = true;
     VP_CUDA(ctx, launch_adam(dg, ctx->adam_m1.p, ctx->adam_m2.p, ctx->payload.p, d_delta, int64_t(n_pay),
                              int64_t(n), unsigned(m3), c, d_bad, false, st));
     // deltas back into the records with the scale projection (losses.cpp:97-103), then the

@@ -212,6 +212,19 @@ __device__ __forceinline__ float clamp_unit(float v) {
 // the eight corner loads become one address plus immediate offsets. Because
 // trilinearStencil clamps lo to [0, M-2], the upper corner is always lo+1 for M >= 2
 // (gatherChannel's min(lo+c, M-1) never bites); for M == 1 all corners are voxel 0.
+#ifndef VPB_PAIRS
+#define VPB_PAIRS 0
+#endif
+// Compile-time voxel counts (MT >= 2) gather from the x-pair payload layout (vpb_kernels.cu
+// k_build_pairs): 4 x 256-bit loads per sample instead of 8 x 128-bit.
+constexpr bool kPairGathers = VPB_PAIRS != 0;
+
+__device__ __forceinline__ void ldg_pair(const float4 *p, float4 &a, float4 &b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
+
 template <int MT>
 __device__ __forceinline__ void sample_primitive(const float4 *__restrict__ pbase, int m_rt,
                                                  const float *xf, V3 pw, float alpha,
@@ -233,9 +246,18 @@ __device__ __forceinline__ void sample_primitive(const float4 *__restrict__ pbas
         lo[a] = i0;
         fr[a] = m > 1 ? u - (float)i0 : 0.0f;
     }
-    const float4 *p = pbase + (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
     float4 c000, c001, c010, c011, c100, c101, c110, c111;
-    if (MT >= 2) {  // immediate offsets
+    if (kPairGathers && MT >= 2) {
+        // x-pair layout (build_pairs): entry (z, y, x) of the primitive holds voxels x and x+1,
+        // 32 B aligned, so each (z, y) row of the stencil is ONE 256-bit load (LDG.256)
+        constexpr int R = 2 * (MT - 1);  // float4s per row of pairs
+        const float4 *p = pbase + (unsigned)(2 * ((lo[2] * MT + lo[1]) * (MT - 1) + lo[0]));
+        ldg_pair(p, c000, c001);
+        ldg_pair(p + R, c010, c011);
+        ldg_pair(p + MT * R, c100, c101);
+        ldg_pair(p + MT * R + R, c110, c111);
+    } else if (MT >= 2) {  // immediate offsets
+        const float4 *p = pbase + (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
         c000 = __ldg(p);
         c001 = __ldg(p + 1);
         c010 = __ldg(p + MT);
@@ -245,6 +267,7 @@ __device__ __forceinline__ void sample_primitive(const float4 *__restrict__ pbas
         c110 = __ldg(p + MT * MT + MT);
         c111 = __ldg(p + MT * MT + MT + 1);
     } else {
+        const float4 *p = pbase + (unsigned)((lo[2] * m + lo[1]) * m + lo[0]);
         const int dx = m > 1 ? 1 : 0, dy = m > 1 ? m : 0, dz = m > 1 ? m * m : 0;
         c000 = __ldg(p);
         c001 = __ldg(p + dx);

@@ -411,7 +411,8 @@ __device__ __forceinline__ void march_tile(const TileSmem &sm, const CamDev &cam
     using IdxT = typename std::conditional<STAGED, uint8_t, uint16_t>::type;
     const int tid = threadIdx.x;
     const int m = MT > 0 ? MT : mp.m;
-    const unsigned m3 = (unsigned)(m * m * m);
+    // per-primitive stride of `payload` in float4s: the x-pair layout for compile-time M
+    const unsigned m3 = kPairGathers && MT >= 2 ? (unsigned)(2 * MT * MT * (MT - 1)) : (unsigned)(m * m * m);
     const V3 o = mk3(cam.center[0], cam.center[1], cam.center[2]);
     if (STAGED) {
         for (int i = tid; i < n * 4; i += NT) {
@@ -797,8 +798,10 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
 }
 
 template <class Cfg, int MT, bool PROF>
-static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const float4 *payload,
-                                  const ViewBatch &views, const uint32_t *order, int n_ctas, cudaStream_t st) {
+static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const float4 *payload_canon,
+                                  const float4 *pairs, const ViewBatch &views, const uint32_t *order, int n_ctas,
+                                  cudaStream_t st) {
+    const float4 *payload = kPairGathers && MT >= 2 ? pairs : payload_canon;
     // function attributes are per device: set them once on each device this process uses
     static bool attr_set[64] = {};
     int dev = 0;
@@ -822,10 +825,11 @@ static cudaError_t launch_tiles_m(const MarchDev &mp, const float *xf16, const f
 
 template <class Cfg>
 static cudaError_t launch_tiles_cfg(const MarchDev &mp, const float *xf16, const float4 *payload,
-                                    const ViewBatch &views, const uint32_t *order, int n_ctas, bool prof,
-                                    cudaStream_t st) {
-#define VPB_TILES(MT) (prof ? launch_tiles_m<Cfg, MT, true>(mp, xf16, payload, views, order, n_ctas, st) \
-                            : launch_tiles_m<Cfg, MT, false>(mp, xf16, payload, views, order, n_ctas, st))
+                                    const float4 *pairs, const ViewBatch &views, const uint32_t *order, int n_ctas,
+                                    bool prof, cudaStream_t st) {
+#define VPB_TILES(MT)                                                                                  \
+    (prof ? launch_tiles_m<Cfg, MT, true>(mp, xf16, payload, pairs, views, order, n_ctas, st)      \
+          : launch_tiles_m<Cfg, MT, false>(mp, xf16, payload, pairs, views, order, n_ctas, st))
     switch (mp.m) {  // compile-time voxel counts for the common grids
     case 1: return VPB_TILES(1);
     case 2: return VPB_TILES(2);
@@ -838,17 +842,44 @@ static cudaError_t launch_tiles_cfg(const MarchDev &mp, const float *xf16, const
 #undef VPB_TILES
 }
 
-cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const ViewBatch &views,
-                               const uint32_t *order, int n_ctas, bool prof, TileTier tier, cudaStream_t st) {
+cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const float4 *pairs,
+                               const ViewBatch &views, const uint32_t *order, int n_ctas, bool prof, TileTier tier,
+                               cudaStream_t st) {
     if (n_ctas == 0) return cudaSuccess;
     switch (tier) {
     case TileTier::Light:
-        return launch_tiles_cfg<TileCfgLight>(mp, xf16, payload, views, order, n_ctas, prof, st);
+        return launch_tiles_cfg<TileCfgLight>(mp, xf16, payload, pairs, views, order, n_ctas, prof, st);
     case TileTier::Dense:
-        return launch_tiles_cfg<TileCfgDense>(mp, xf16, payload, views, order, n_ctas, prof, st);
+        return launch_tiles_cfg<TileCfgDense>(mp, xf16, payload, pairs, views, order, n_ctas, prof, st);
     default:
-        return launch_tiles_cfg<TileCfgNormal>(mp, xf16, payload, views, order, n_ctas, prof, st);
+        return launch_tiles_cfg<TileCfgNormal>(mp, xf16, payload, pairs, views, order, n_ctas, prof, st);
     }
+}
+
+bool march_uses_pairs(int m) { return kPairGathers && (m == 2 || m == 4 || m == 8 || m == 16 || m == 32); }
+
+// The x-pair payload layout the raymarch gathers from (kPairGathers): for primitive k and row
+// (z, y), entry x in [0, M-1) holds the interleaved voxels x and x+1 (32 B, aligned), so a
+// trilinear stencil reads 4 aligned 32-byte rows. Derived from the canonical interleaved payload
+// after every change of it.
+__global__ void k_build_pairs(const float4 *__restrict__ payload, float4 *__restrict__ pairs, int64_t n_prim,
+                              int m) {
+    const int64_t rows = n_prim * m * m, per = m - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * per;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / per, x = i - row * per;
+        const float4 *src = payload + row * m + x;
+        pairs[2 * i] = src[0];
+        pairs[2 * i + 1] = src[1];
+    }
+}
+
+cudaError_t launch_build_pairs(const float4 *payload, float4 *pairs, int64_t n_prim, int m, cudaStream_t st) {
+    const int64_t n = n_prim * m * m * (m - 1);
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    k_build_pairs<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(payload, pairs, n_prim, m);
+    return cudaGetLastError();
 }
 
 // Candidates of a key-overflowed tile rebuilt from all K pixel rectangles (prim ids, any

@@ -165,8 +165,13 @@ cudaError_t launch_binning(const CamDev &cam, const float *xf16, int n_prim, int
                            uint32_t *cursor, uint32_t *order, unsigned long long *entries,
                            int64_t capacity, DevCounters *ctr, cudaStream_t st);
 // K5 over the tiles of every view in `views`; `order` lists (view << 20 | tile), heaviest first.
-cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const ViewBatch &views,
-                               const uint32_t *order, int n_ctas, bool prof, TileTier tier, cudaStream_t st);
+// pairs: the x-pair layout (launch_build_pairs), read instead of payload when march_uses_pairs(M)
+cudaError_t launch_march_tiles(const MarchDev &mp, const float *xf16, const float4 *payload, const float4 *pairs,
+                               const ViewBatch &views, const uint32_t *order, int n_ctas, bool prof, TileTier tier,
+                               cudaStream_t st);
+bool march_uses_pairs(int m);
+// x-pair layout: n_prim * M * M * (M - 1) entries of 2 float4s
+cudaError_t launch_build_pairs(const float4 *payload, float4 *pairs, int64_t n_prim, int m, cudaStream_t st);
 // K5b for the views' overflow rays (one launch for all views).
 // Key-overflowed tiles are marched here too: tile_scratch holds kOvfTileBlocks * n_prim prim ids.
 cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,

@@ -1,4 +1,7 @@
-"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL over NVLink/NVSwitch).
+"""Multi-GPU plumbing: one process per GPU. Two data planes: the library's own NCCL
+(`NativeComm` / `NativeViewGather` over include/vpb.h vp_comm_*, what bench.py uses and what a
+C++ caller uses) and torch.distributed collectives (`broadcast_scene`, `ViewGather`,
+`TileShardGather`, also runnable with gloo on CPU tensors).
 
 The raymarcher shards by view: rays are independent and the scene is
 read-only, so each rank renders its own views with no data-path collective. A single view
@@ -191,3 +194,126 @@ class TileShardGather:
         samp = assemble_tile_shards([r[4 * n:].view(torch.int32).view(-1, 256, 1) for r in rows],
                                     self.width, self.height, 1)
         return rgb, alpha, samp[..., 0]
+
+
+class NativeComm:
+    """The multi-GPU C-ABI of libvpb (include/vpb.h vp_comm_*: NCCL inside the library, no torch
+    on the data path). torch.distributed (any backend, gloo included) is used only to hand the
+    128-byte NCCL id from rank 0 to the others. One communicator per Renderer (its device)."""
+
+    def __init__(self, renderer, world: int, rank: int, max_ctas: int = 8, comm_id: Optional[bytes] = None):
+        import ctypes as C
+        from . import _lib
+        from .api import _check
+        self.lib, self.r, self.world, self.rank = renderer._lib, renderer, world, rank
+        self.C = C
+        if comm_id is None:
+            comm_id = self.share_id(world, rank)
+        idb = (C.c_uint8 * 128).from_buffer_copy(comm_id)
+        h = C.c_void_p()
+        rc = self.lib.vp_comm_init(renderer.ctx, idb, world, rank, max_ctas, C.byref(h))
+        if rc:
+            raise RuntimeError(f"vp_comm_init failed ({rc}): {self.lib.vp_last_error(renderer.ctx).decode()}")
+        self.h = h
+        self._check = _check
+        self._lib = _lib
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from . import _lib
+        lib = _lib.load()
+        buf = (C.c_uint8 * 128)()
+        if lib.vp_comm_unique_id(buf):
+            raise RuntimeError(f"vp_comm_unique_id: {lib.vp_comm_last_error().decode()}")
+        return bytes(buf)
+
+    @staticmethod
+    def share_id(world: int, rank: int) -> bytes:
+        """Rank 0's NCCL id, broadcast over torch.distributed (world 1: a local id)."""
+        if world == 1:
+            return NativeComm.unique_id()
+        import torch.distributed as dist
+        obj = [NativeComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def broadcast_scene(self, xf15, slab, window, n_prim: int, m: int, root: int = 0) -> int:
+        """vp_set_scene on every rank (the root with its data, the others shape only), then
+        vp_broadcast_scene: the root's composed transforms and repacked payload, once."""
+        if self.rank == root:
+            self.r.set_scene_composed(xf15, slab, window)
+        else:
+            self._check(self.lib.vp_set_scene(self.r.ctx, int(n_prim), int(m), None, None, float(window.alpha),
+                                              int(window.beta)), self.r.ctx)
+            self.r.n_prim, self.r.m = int(n_prim), int(m)
+        self._check(self.lib.vp_broadcast_scene(self.h, root), self.r.ctx)
+        self._check(self.lib.vp_comm_sync(self.h), self.r.ctx)
+        return int(n_prim) * (16 + 4 * int(m) ** 3) * 4
+
+    def gather_views(self, n_views: int, n_px: int, rgb, alpha, samples, dst=None, root: int = 0):
+        """vp_gather_views: this rank's n_views device outputs (pointer lists) to the root;
+        dst = (rgb, alpha, samples) pointer lists of n_ranks * n_views entries on the root."""
+        C = self.C
+        f32p, i32p = self._lib.f32p, self._lib.i32p
+        P = lambda ptrs, t: (t * len(ptrs))(*[C.cast(C.c_void_p(p), t) for p in ptrs])  # noqa: E731
+        src = (P(rgb, f32p), P(alpha, f32p), P(samples, i32p) if samples is not None else None)
+        d = (None, None, None)
+        if dst is not None:
+            d = (P(dst[0], f32p), P(dst[1], f32p), P(dst[2], i32p) if dst[2] is not None else None)
+        self._check(self.lib.vp_gather_views(self.h, root, n_views, n_px, src[0], src[1], src[2], d[0], d[1], d[2]),
+                    self.r.ctx)
+
+    def wait(self, stream: int = 0):
+        """`stream` (0: the context's) waits for the communicator's work so far."""
+        self._check(self.lib.vp_comm_wait(self.h, self.C.c_void_p(stream) if stream else None), self.r.ctx)
+
+    def sync(self):
+        self._check(self.lib.vp_comm_sync(self.h), self.r.ctx)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vp_comm_destroy(self.h)
+            self.h = None
+
+
+class NativeViewGather:
+    """ViewGather over the native communicator: per slot, every local view's rgb / alpha /
+    samples device buffers; each step's gather of all its views is ONE vp_gather_views call (one
+    NCCL group) on the communicator's stream, overlapping the next step's raymarch, which
+    renders into the other slot. wait_slot makes the render stream wait for the gathers so far
+    before a slot is rendered into again."""
+
+    def __init__(self, comm: NativeComm, n_local: int, width: int, height: int, device, dst: int = 0,
+                 slots: int = 2):
+        import torch
+        self.comm, self.n, self.hw, self.dst, self.slots = comm, n_local, width * height, dst, max(1, slots)
+        hw = self.hw
+        self.bufs = [(torch.zeros((n_local, 3 * hw), dtype=torch.float32, device=device),
+                      torch.zeros((n_local, hw), dtype=torch.float32, device=device),
+                      torch.zeros((n_local, hw), dtype=torch.int32, device=device)) for _ in range(self.slots)]
+        world = comm.world
+        self.recv = None
+        if comm.rank == dst:  # [slot] -> (rgb, alpha, samples) of world * n_local views
+            self.recv = [(torch.empty((world * n_local, 3 * hw), dtype=torch.float32, device=device),
+                          torch.empty((world * n_local, hw), dtype=torch.float32, device=device),
+                          torch.empty((world * n_local, hw), dtype=torch.int32, device=device))
+                         for _ in range(self.slots)]
+
+    def views(self, slot: int = 0):
+        return self.bufs[slot % self.slots]
+
+    def gather(self, slot: int, stream: int = 0):
+        s = slot % self.slots
+        rgb, alpha, samp = self.bufs[s]
+        ptr = lambda t: [t[j].data_ptr() for j in range(t.shape[0])]  # noqa: E731
+        dst = None
+        if self.recv is not None:
+            dst = tuple(ptr(t) for t in self.recv[s])
+        self.comm.gather_views(self.n, self.hw, ptr(rgb), ptr(alpha), ptr(samp), dst, self.dst)
+
+    def wait_slot(self, slot: int, stream: int = 0):
+        self.comm.wait(stream)
+
+    def finish(self):
+        self.comm.sync()

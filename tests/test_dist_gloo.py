@@ -180,3 +180,29 @@ def test_tile_shard_gather_world2():
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
     assert res == [(0, True), (1, True)]
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_01954_b200.dist import NativeComm
+        q.put((rank, NativeComm.share_id(world, rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_native_comm_id_exchange_world2():
+    """bench.py's N > 1 control plane (gloo) hands rank 0's NCCL id (vp_comm_unique_id, 128 bytes)
+    to every rank before vp_comm_init; the data plane itself needs GPUs (tests/test_gpu_comm.py)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert len(res[0][1]) == 128 and res[0][1] == res[1][1]
