@@ -20,6 +20,8 @@
 #include <vector>
 
 #include "../../include/vpb.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "vpb_ctx_internal.h"
 #include "vpb_hostcopy.hpp"
 #include "vpb_hostmath.hpp"
@@ -62,6 +64,13 @@ bool is_device_ptr(const void *p) {
 }
 
 constexpr int kTimingSlots = 256;  // march-kernel event pairs kept for vp_kernel_times
+
+// NVTX range over a C-ABI call (header-only NVTX v3: free unless a profiler is attached), so a
+// timeline shows each entry point around the kernels it launches.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 constexpr size_t kStageBytes = size_t(8) << 20;  // host slab upload chunk (upload_planar_host)
 
 }  // namespace
@@ -171,6 +180,7 @@ struct vp_ctx {
     // Raymarch configuration for the next render, from the mean candidates per non-empty tile
     // of the last render whose counters reached the host (see note_density).
     TileTier tier = TileTier::Normal;
+    bool tier_known = false;  // false after a scene change: the next render measures the density first
     int tile_cfg = -1;  // VPB_TILE_CFG override: -1 auto, else a TileTier
 };
 
@@ -320,6 +330,8 @@ void grow_key_capacity(vp_ctx *ctx) {
 // views, heaviest first across views (a batch pays the tail of a launch once), and one
 // fallback launch their overflow rays.
 // n_ctas_single: a shard render's owned tile count (its order lists them first), else -1.
+void note_density(vp_ctx *ctx, const DevCounters &c);
+
 int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, const OutDev *ods, cudaStream_t st,
                   int n_ctas_single = -1) {
     if (n < 1 || n > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per launch");
@@ -352,6 +364,19 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
     }
     VP_CUDA(ctx, launch_binning_batch(bb, ctx->bin_stream));
     VP_CUDA(ctx, cudaEventRecord(ctx->ev_keys[ctx->group], ctx->bin_stream));  // K2 stored the key counts
+    if (!ctx->tier_known && ctx->tile_cfg < 0) {
+        // first render of a scene: wait for its binning (tens of µs, once) and pick the raymarch
+        // tier from this scene's density instead of the previous scene's
+        VP_CUDA(ctx, cudaStreamSynchronize(ctx->bin_stream));
+        DevCounters sum{};
+        for (int v = 0; v < n; ++v) {
+            VP_CUDA(ctx, cudaMemcpy(ctx->h_ctr, grp[v].d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+            sum.keys += ctx->h_ctr->keys;
+            sum.nonempty_tiles += ctx->h_ctr->nonempty_tiles;
+        }
+        note_density(ctx, sum);
+        ctx->tier_known = true;
+    }
     const uint32_t *order = grp[0].order.p;
     if (n > 1) {
         VP_CUDA(ctx, ctx->batch_order[ctx->group].ensure(size_t(std::max(total, 1))));
@@ -397,6 +422,7 @@ constexpr unsigned long long kLightKeysPerTile = 14, kDenseKeysPerTile = 40;
 
 void note_density(vp_ctx *ctx, const DevCounters &c) {
     if (c.nonempty_tiles == 0) return;
+    ctx->tier_known = true;
     ctx->tier = c.keys > kDenseKeysPerTile * c.nonempty_tiles  ? TileTier::Dense
                 : c.keys > kLightKeysPerTile * c.nonempty_tiles ? TileTier::Normal
                                                                 : TileTier::Light;
@@ -710,6 +736,7 @@ int vp_set_transforms_async(vp_ctx *ctx, int32_t n_prim, const float *xf15, void
 }
 
 int vp_set_frame(vp_ctx *ctx, int32_t n_prim, const float *tr24) {
+    NvtxRange nvtx_("vp_set_frame");
     if (int rc = check_ctx(ctx, false)) return rc;
     if (int rc = quiesce(ctx)) return rc;
     if (!ctx->has_scene || n_prim != ctx->n_prim) return fail(ctx, VP_ERR_USAGE, "primitive count mismatch");
@@ -841,6 +868,7 @@ static int copy_out_host(vp_ctx *ctx, const HostOut *outs, int n, cudaStream_t s
 
 int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
                  const float *payload, float window_alpha, int32_t window_beta) {
+    NvtxRange nvtx_("vp_set_scene");
     if (int rc = check_ctx(ctx, false)) return rc;
     if (int rc = quiesce(ctx)) return rc;
     if (n_prim < 0) return fail(ctx, VP_ERR_USAGE, "negative primitive count");
@@ -930,6 +958,7 @@ int vp_kernel_times(vp_ctx *ctx, int64_t max, float *march_ms, int64_t *n) {
 
 int vp_render_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb_dev,
                     float *alpha_dev, int32_t *samples_dev, void *stream) {
+    NvtxRange nvtx_("vp_render_async");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_cam(ctx, cam)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
@@ -984,6 +1013,7 @@ int64_t vp_shard_tiles(int32_t width, int32_t height, int32_t shard, int32_t n_s
 
 int vp_render_shard_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, int32_t shard,
                           int32_t n_shards, float *rgb, float *alpha, int32_t *samples, void *stream) {
+    NvtxRange nvtx_("vp_render_shard_async");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_cam(ctx, cam)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
@@ -1016,6 +1046,7 @@ int vp_render_shard_async(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg
 
 int vp_render_batch_async(vp_ctx *ctx, int32_t n_views, const vp_camera *cams, const vp_march *cfg,
                           float *const *rgb, float *const *alpha, int32_t *const *samples, void *stream) {
+    NvtxRange nvtx_("vp_render_batch_async");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n_views < 1 || n_views > kMaxViews) return fail(ctx, VP_ERR_USAGE, "1 to 16 views per batch");
@@ -1121,6 +1152,7 @@ int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
 
 int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb, float *alpha,
               int32_t *samples, vp_stats *stats) {
+    NvtxRange nvtx_("vp_render");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_cam(ctx, cam)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
@@ -1183,6 +1215,7 @@ int vp_render(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, float *rgb
 int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float *dirs,
                   const float *jitter01, const vp_march *cfg, float *rgb, float *alpha,
                   int32_t *samples) {
+    NvtxRange nvtx_("vp_march_rays");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n_rays < 0) return fail(ctx, VP_ERR_USAGE, "negative ray count");
@@ -1444,6 +1477,7 @@ int vp_backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const fl
                      const float *jitter01, const float *adj_rgb, const float *adj_alpha,
                      const vp_march *cfg, const float *transforms24, float *grads,
                      int32_t accumulate) {
+    NvtxRange nvtx_("vp_backward_rays");
     return backward_rays(ctx, n_rays, origins, dirs, jitter01, adj_rgb, adj_alpha, cfg, transforms24, grads,
                          accumulate, nullptr, nullptr);
 }
@@ -1454,6 +1488,7 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
                      const float *target, const float *background, float lambda_pho,
                      const vp_march *cfg, const float *transforms24, float *loss_pho,
                      float *composited, float *grads, int32_t accumulate) {
+    NvtxRange nvtx_("vp_eval_loss_pho");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = check_march(ctx, cfg)) return rc;
     if (n <= 0) return fail(ctx, VP_ERR_USAGE, "empty pixel set");  // losses.cpp:14
@@ -1592,6 +1627,7 @@ int vp_debug_tile_times(vp_ctx *ctx, const vp_camera *cam, const vp_march *cfg, 
 
 int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf15,
                  float window_alpha, int32_t window_beta) {
+    NvtxRange nvtx_("vp_load_slab");
     if (int rc = check_ctx(ctx, false)) return rc;
     if (!path) return fail(ctx, VP_ERR_USAGE, "null path");
     std::FILE *f = std::fopen(path, "rb");
@@ -1661,6 +1697,7 @@ int vp_adam_reset(vp_ctx *ctx) {
 }
 
 int vp_adam_step(vp_ctx *ctx, const vp_adam *cfg, const float *grads, float *transforms24) {
+    NvtxRange nvtx_("vp_adam_step");
     if (int rc = check_ctx(ctx, true)) return rc;
     if (int rc = quiesce(ctx)) return rc;
     if (!cfg || !grads) return fail(ctx, VP_ERR_USAGE, "null arguments");

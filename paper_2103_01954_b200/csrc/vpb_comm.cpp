@@ -16,6 +16,7 @@
 // gather that overlaps the next raymarch takes few SMs from it.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstring>
 #include <string>
@@ -187,6 +188,8 @@ int vp_group_end(void) {
 // transforms and payload: shape only). Then the root's composed transforms (K x 16 floats) and
 // repacked interleaved payload (K M^3 float4) go to every rank in two broadcasts.
 int vp_broadcast_scene(vp_comm *comm, int32_t root) {
+    nvtxRangePushA("vp_broadcast_scene");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
     if (!comm || root < 0 || root >= comm->n_ranks) {
         g_comm_err = "vp_broadcast_scene: bad arguments";
         return VP_ERR_USAGE;
@@ -218,6 +221,8 @@ int vp_broadcast_scene(vp_comm *comm, int32_t root) {
 int vp_gather_views(vp_comm *comm, int32_t root, int32_t n_views, int64_t n_px, float *const *rgb,
                     float *const *alpha, int32_t *const *samples, float *const *dst_rgb, float *const *dst_alpha,
                     int32_t *const *dst_samples) {
+    nvtxRangePushA("vp_gather_views");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
     if (!comm || root < 0 || root >= comm->n_ranks || n_views < 0 || n_px < 0 || (n_views > 0 && (!rgb || !alpha))) {
         g_comm_err = "vp_gather_views: bad arguments";
         return VP_ERR_USAGE;
