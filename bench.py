@@ -227,7 +227,7 @@ def run_reference(args, rank, world):
             "n_gpus": world, "steps": done, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t / done, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(args, world, world > 1),
+            "config": workload_config(args, world, world > 1) | {"l2": "n/a: host CPU run"},
             "frames_per_s": round(done * V / t, 4),
             "cpu_baseline": {"value": round(value, 3), "unit": METRIC, "cores": ref.cores, "kind": ref.kind,
                              "cpu_model": cpu_model(), "sample": sample},
