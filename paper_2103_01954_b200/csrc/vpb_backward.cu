@@ -506,7 +506,7 @@ k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                      const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
                      const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
     __shared__ unsigned long long s_tab[32];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -549,7 +549,7 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = gridDim.x * 4, gw = blockIdx.x * 4 + wid;

@@ -125,6 +125,9 @@ __device__ __forceinline__ float hash_to_unit(uint64_t h) {
 // builds agree on every float in [-104, 88] (checked exhaustively on the host), as does
 // this port except at the two inputs patched below. The table lives in shared memory
 // (lanes index it divergently).
+#ifndef VPB_EXPTAB_SPLIT
+#define VPB_EXPTAB_SPLIT 1
+#endif
 __constant__ unsigned long long kExp2fTab[32] = {
     0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
     0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
@@ -145,13 +148,36 @@ __device__ __forceinline__ float expf_core(float x, const unsigned long long *ta
     const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
     kd = __dsub_rn(kd, Shift);
     const double r = __dsub_rn(z, kd);
+    // the table is staged as two 32-bit halves (load_exp_tab): two conflict-free LDS.32 instead
+    // of an LDS.64 whose entries i and i + 16 share banks
+#if VPB_EXPTAB_SPLIT
+    const unsigned *tw = reinterpret_cast<const unsigned *>(tab);
+    const unsigned j = (unsigned)(ki & 31);
+    const unsigned long long t = (((unsigned long long)tw[32 + j] << 32) | tw[j]) + (ki << 47);
+#else
     const unsigned long long t = tab[ki & 31] + (ki << 47);
+#endif
     const double s = __longlong_as_double((long long)t);
     const double zz = __fma_rn(C0, r, C1);
     const double r2 = __dmul_rn(r, r);
     double y = __fma_rn(C2, r, 1.0);
     y = __fma_rn(zz, r2, y);
     return __double2float_rn(__dmul_rn(y, s));
+}
+
+// Stages kExp2fTab into 32 shared u64 slots (64 words) as lo[32] then hi[32]; threads 0..31 of
+// the block write it (a __syncthreads must follow before expf_core reads it).
+__device__ __forceinline__ void load_exp_tab(unsigned long long *s_tab) {
+    if (threadIdx.x < 32) {
+        const unsigned long long v = kExp2fTab[threadIdx.x];
+#if VPB_EXPTAB_SPLIT
+        unsigned *w = reinterpret_cast<unsigned *>(s_tab);
+        w[threadIdx.x] = (unsigned)v;
+        w[32 + threadIdx.x] = (unsigned)(v >> 32);
+#else
+        s_tab[threadIdx.x] = v;
+#endif
+    }
 }
 
 __device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {

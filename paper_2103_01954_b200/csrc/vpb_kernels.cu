@@ -383,6 +383,11 @@ __global__ void k_tile_sort_big(const __grid_constant__ BinBatch bb) {
 // Tiles with more than CC candidates take the same path with TileCands<false>
 // (candidates read from global memory, 16-bit window indices); tiles beyond 65535
 // candidates send every pixel to the fallback re-march.
+// window index slots per thread (16-bit units): Window::C word-interleaves the indices, so
+// the region is rounded up to whole words of every width
+template <int CAP>
+constexpr size_t kWcSlots = (size_t)((CAP + 3) / 4 * 4);
+
 struct TileSmem {
     float4 *xf4;       // CC * 4
     float4 *om;        // CC
@@ -509,7 +514,7 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     sm.we = reinterpret_cast<float *>(sm.warp + NT / 32);
     sm.wx = sm.we + CAP * NT;
     sm.wc = sm.wx + CAP * NT;
-    sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + CAP * NT);
+    sm.mask = reinterpret_cast<unsigned *>(reinterpret_cast<uint16_t *>(sm.wc) + kWcSlots<CAP> * NT);
 
     constexpr int kParts = kMarchThreads / NT;  // CTAs per tile
     const uint32_t oe = order[blockIdx.x / kParts];
@@ -523,7 +528,7 @@ k_march_tiles(MarchDev mp, const float *__restrict__ xf_g, const float4 *__restr
     const uint32_t start = vd.offsets[tile];
     const int n = (int)(vd.offsets[tile + 1] - start);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-    if (threadIdx.x < 32) sm.tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(sm.tab);
     unsigned long long t_start = 0;
     if (PROF && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
@@ -560,7 +565,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
                  OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ ovf_list,
                  int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c) {
     __shared__ unsigned long long s_tab[32];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     if (!kRays && ctr->key_overflow) return;
     const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
@@ -620,7 +625,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
     __shared__ int s_c[4][kWarpList];
     __shared__ int s_cand[4][kWarpCand];
     __shared__ float s_ce[4][kWarpCand], s_cx[4][kWarpCand];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
@@ -669,7 +674,7 @@ __global__ void k_composite(const float *__restrict__ rgb, const float *__restri
 
 __global__ void k_expf(const float *__restrict__ x, float *__restrict__ y, int64_t n) {
     __shared__ unsigned long long s_tab[32];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = expf_glibc(x[i], s_tab);
@@ -752,7 +757,7 @@ struct TileCfgDense {
 template <int CAP, int CC, int NT>
 static size_t tiles_smem() {
     return (size_t)CC * kXfStride * 4 + CC * 16 * 2 + CC * 4 + 32 * 8 + NT * 4 * 2 + (NT / 32) * 4 +
-           (size_t)CAP * NT * (8 + 2) + (size_t)((CC + 31) / 32) * NT * 4;
+           (size_t)CAP * NT * 8 + kWcSlots<CAP> * NT * 2 + (size_t)((CC + 31) / 32) * NT * 4;
 }
 size_t march_tiles_smem() { return tiles_smem<TileCfgNormal::CAP, TileCfgNormal::CC, TileCfgNormal::NT>(); }
 
@@ -946,7 +951,7 @@ k_march_fallback_views(MarchDev mp, const float *__restrict__ xf_g, int n_prim, 
     __shared__ unsigned long long s_tab[32];
     __shared__ int s_warp[kFallbackThreads / 32];
     __shared__ int s_n;
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    load_exp_tab(s_tab);
     __syncthreads();
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;

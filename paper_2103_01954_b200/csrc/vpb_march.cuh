@@ -125,6 +125,9 @@ struct BvhCands {
 
 // Per-ray sorted segment window: slot j of ray `lane` lives at [j * stride + lane]
 // (conflict-free across a warp). IdxT holds the candidate index (uint8_t for staged tiles).
+#ifndef VPB_WC_INTERLEAVE
+#define VPB_WC_INTERLEAVE 0
+#endif
 template <class IdxT>
 struct Window {
     float *e;
@@ -135,7 +138,15 @@ struct Window {
     int mw = 0;
     __device__ __forceinline__ float &E(int j) const { return e[j * stride + lane]; }
     __device__ __forceinline__ float &X(int j) const { return x[j * stride + lane]; }
-    __device__ __forceinline__ IdxT &C(int j) const { return c[j * stride + lane]; }
+    // VPB_WC_INTERLEAVE=1 word-interleaves indices narrower than a word (a lane's entries
+    // j..j+3 share one 32-bit word in the lane's own bank, so lanes at different j never
+    // conflict; with c[j * stride + lane] four lanes share a bank). It removes 13 M excessive
+    // shared wavefronts per headline launch but measured 0.4 % slower (more address math): off
+    __device__ __forceinline__ IdxT &C(int j) const {
+        constexpr int P = VPB_WC_INTERLEAVE && sizeof(IdxT) < 4 ? 4 / (int)sizeof(IdxT) : 1;
+        if (P == 1) return c[j * stride + lane];
+        return c[((j / P) * stride + lane) * P + (j % P)];
+    }
     __device__ __forceinline__ unsigned &M(int word) const { return m[word * stride + lane]; }
 };
 
