@@ -120,3 +120,20 @@ def test_shard_argument_errors(renderer):
     with pytest.raises(api.Error) as e:  # tile-major shard outputs are device-only
         renderer.render_shard_device(cam, api.MarchConfig(), 0, 2, host.ctypes.data, host.ctypes.data)
     assert e.value.category == api.ErrorCategory.USAGE
+
+
+@pytest.mark.parametrize("n", [1, 3])
+def test_shards_with_key_overflow(n):
+    """Tile shards whose owned tiles overflow a forced key capacity (K5b rebuilds those tiles'
+    lists from all primitives and writes the shard's tile-major slots) still assemble to the
+    unsharded render."""
+    tr, pay = synthetic.shell_arrays(4096, 8)
+    with Renderer(0) as r:
+        r.set_scene_composed(api.compose(tr), api.PrimitiveSlab(4096, 8, pay), api.WindowParams())
+        cam = synthetic.shell_camera(5, 64, 256)
+        cfg = api.MarchConfig()
+        full = r.render(cam, cfg)
+        r.set_key_capacity(500, grow=False)
+        got = _render_shards(r, cam, cfg, n)
+        assert all(s["keys"] > 500 for s in got[3]) or n > 1
+    _check(full, got)
