@@ -180,7 +180,8 @@ struct vp_ctx {
     // Raymarch configuration for the next render, from the mean candidates per non-empty tile
     // of the last render whose counters reached the host (see note_density).
     TileTier tier = TileTier::Normal;
-    bool tier_known = false;  // false after a scene change: the next render measures the density first
+    bool tier_known = false;
+    cudaStream_t scene_writer = nullptr;  // another agent's stream that wrote the scene (broadcast)  // false after a scene change: the next render measures the density first
     int tile_cfg = -1;  // VPB_TILE_CFG override: -1 auto, else a TileTier
 };
 
@@ -452,6 +453,12 @@ int check_counters(vp_ctx *ctx, const DevCounters &c) {
 
 int check_ctx(vp_ctx *ctx, bool need_scene, bool need_xf = true) {
     if (!ctx) return fail(nullptr, VP_ERR_USAGE, "null context");
+    if (ctx->scene_writer) {  // ctx_scene_written: everything from now on waits for the writer
+        VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf, ctx->scene_writer));  // the binning waits for ev_xf
+        VP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_xf, 0));
+        VP_CUDA(ctx, cudaStreamWaitEvent(ctx->bin_stream, ctx->ev_xf, 0));
+        ctx->scene_writer = nullptr;
+    }
     if (need_scene && !ctx->has_scene) return fail(ctx, VP_ERR_USAGE, "no scene set");
     if (need_scene && need_xf && ctx->n_prim > 0 && !ctx->has_xf)
         return fail(ctx, VP_ERR_USAGE, "no transforms set (vp_set_frame / vp_set_transforms)");
@@ -495,9 +502,15 @@ int ctx_scene_written(vp_ctx *ctx, cudaStream_t st) {
     ctx->has_xf = true;
     ctx->bvh_dirty = true;
     ctx->pairs_dirty = true;
-    VP_CUDA(ctx, cudaEventRecord(ctx->ev_xf, st));  // enqueue_views' binning waits for ev_xf
-    VP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_xf, 0));
+    // The writer's work may not be enqueued yet (a broadcast inside a caller's NCCL group is
+    // launched at vp_group_end), so the context waits for `st` when it next uses the scene
+    // (check_ctx), not now.
+    ctx->scene_writer = st;
     return VP_OK;
+}
+
+void ctx_drop_writer(vp_ctx *ctx, cudaStream_t st) {  // the writer's stream is being destroyed (synced)
+    if (ctx && ctx->scene_writer == st) ctx->scene_writer = nullptr;
 }
 
 int ctx_wait_renders(vp_ctx *ctx, cudaStream_t st) {

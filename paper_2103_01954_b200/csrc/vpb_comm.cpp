@@ -81,6 +81,7 @@ void free_comm(vp_comm *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    vpb::ctx_drop_writer(c->ctx, c->stream);
     if (c->nc) ncclCommDestroy(c->nc);
     if (c->ev) cudaEventDestroy(c->ev);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -22,10 +22,13 @@ struct CtxScene {
 };
 // VP_ERR_USAGE when the context holds no scene (vp_set_scene first).
 int ctx_scene(vp_ctx *ctx, CtxScene *out);
-// The scene's transforms and payload were written on `st` by another agent (a broadcast): the
+// The scene's transforms and payload are written on `st` by another agent (a broadcast): the
 // context's derived state (BVH, the raymarch's pair layout) is stale, the transforms count as
-// set, and the next binning waits for `st`'s work so far.
+// set, and the context's next call that uses the scene makes its streams wait for `st`'s work
+// enqueued by then (so a broadcast launched only at a caller's vp_group_end is covered).
 int ctx_scene_written(vp_ctx *ctx, cudaStream_t st);
+// `st` (a former scene writer) is about to be destroyed after a synchronize: forget it.
+void ctx_drop_writer(vp_ctx *ctx, cudaStream_t st);
 // Make `st` wait for the context's renders enqueued so far (their device outputs complete).
 int ctx_wait_renders(vp_ctx *ctx, cudaStream_t st);
 // Error reporting shared with vpb_api.cpp (vp_last_error).
