@@ -24,10 +24,11 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
 
-# NCCL (multi-GPU C-ABI, vpb_comm.cpp) is linked dynamically by soname: in a process that has
-# already loaded torch's bundled libnccl.so.2 that one is shared, else the system one.
+# NCCL (multi-GPU C-ABI, vpb_comm.cpp) is not linked: vpb_comm.cpp binds libnccl.so.2 with
+# dlopen at the first vp_comm_* call (torch's copy when torch is loaded), so rendering never
+# loads NCCL and cannot shadow torch's newer one.
 $(PKG)/libvpb.so: $(OBJ)/vpb_kernels.o $(OBJ)/vpb_backward.o $(OBJ)/vpb_train.o $(OBJ)/vpb_compose.o $(OBJ)/vpb_bvh.o $(OBJ)/vpb_api.o $(OBJ)/vpb_synth.o $(OBJ)/vpb_losses.o $(OBJ)/vpb_comm.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -ldl
 
 clean:
 	rm -rf build $(PKG)/libvpb.so

@@ -124,6 +124,13 @@ def load() -> C.CDLL:
         if not LIB_PATH.exists():
             raise OSError(f"libvpb.so not built at {LIB_PATH}; run `make lib` or "
                           "__graft_entry__.build() — there is no CPU fallback")
+        # torch (when installed) first: libvpb binds libnccl.so.2 lazily for vp_comm_*, and it
+        # must find torch's (newer) copy already loaded rather than bring in the system one,
+        # which would then shadow torch's and break a later `import torch`
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)

@@ -15,10 +15,12 @@
 // on (stream-ordered, no host wait). NCCL's CTA count is capped (ncclConfig_t.maxCTAs) so a
 // gather that overlaps the next raymarch takes few SMs from it.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -37,8 +39,56 @@ namespace {
 
 thread_local std::string g_comm_err;
 
+// NCCL is bound at the first vp_comm_* call (dlopen by soname, dlsym), not linked: rendering
+// never needs it, and a process that imports torch AFTER loading libvpb must get torch's own
+// (newer) libnccl.so.2 — a linked system NCCL would already own that soname and break torch.
+// When torch is loaded first, dlopen returns torch's library.
+struct Nccl {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+const Nccl &nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // already in the process (torch)?
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            n.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return;
+        }
+        bool all = true;
+        auto sym = [&](auto &fn, const char *name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            all = all && fn != nullptr;
+        };
+        sym(n.GetUniqueId, "ncclGetUniqueId");
+        sym(n.CommInitRankConfig, "ncclCommInitRankConfig");
+        sym(n.CommDestroy, "ncclCommDestroy");
+        sym(n.GroupStart, "ncclGroupStart");
+        sym(n.GroupEnd, "ncclGroupEnd");
+        sym(n.Broadcast, "ncclBroadcast");
+        sym(n.Send, "ncclSend");
+        sym(n.Recv, "ncclRecv");
+        sym(n.GetErrorString, "ncclGetErrorString");
+        n.ok = all;
+        if (!all) n.why = "libnccl.so.2 lacks an entry point libvpb needs";
+    });
+    return n;
+}
+
 int nccl_fail(vp_ctx *ctx, ncclResult_t r, const char *where) {
-    const std::string msg = std::string(where) + ": " + ncclGetErrorString(r);
+    const std::string msg = std::string(where) + ": " + nccl().GetErrorString(r);
     if (ctx) return vpb::ctx_fail(ctx, VP_ERR_DEVICE, msg);
     g_comm_err = msg;
     return VP_ERR_DEVICE;
@@ -53,6 +103,14 @@ int cuda_fail(vp_ctx *ctx, cudaError_t e, const char *where) {
     do {                                                             \
         const ncclResult_t r_ = (call);                              \
         if (r_ != ncclSuccess) return nccl_fail((ctx), r_, #call);   \
+    } while (0)
+#define VP_NEED_NCCL(ctx)                                            \
+    do {                                                             \
+        if (!nccl().ok) {                                            \
+            if (ctx) return vpb::ctx_fail((ctx), VP_ERR_DEVICE, nccl().why); \
+            g_comm_err = nccl().why;                                 \
+            return VP_ERR_DEVICE;                                    \
+        }                                                            \
     } while (0)
 #define VP_CU(ctx, call)                                             \
     do {                                                             \
@@ -82,7 +140,7 @@ void free_comm(vp_comm *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     vpb::ctx_drop_writer(c->ctx, c->stream);
-    if (c->nc) ncclCommDestroy(c->nc);
+    if (c->nc) nccl().CommDestroy(c->nc);
     if (c->ev) cudaEventDestroy(c->ev);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -96,9 +154,10 @@ const char *vp_comm_last_error(void) { return g_comm_err.c_str(); }
 
 int vp_comm_unique_id(uint8_t *id) {
     if (!id) return VP_ERR_USAGE;
+    VP_NEED_NCCL(nullptr);
     static_assert(sizeof(ncclUniqueId) == VP_COMM_ID_BYTES, "ncclUniqueId size");
     ncclUniqueId u;
-    VP_NCCL(nullptr, ncclGetUniqueId(&u));
+    VP_NCCL(nullptr, nccl().GetUniqueId(&u));
     std::memcpy(id, &u, sizeof u);
     return VP_OK;
 }
@@ -108,6 +167,7 @@ int vp_comm_init(vp_ctx *ctx, const uint8_t *id, int32_t n_ranks, int32_t rank, 
         g_comm_err = "vp_comm_init: bad arguments";
         return VP_ERR_USAGE;
     }
+    VP_NEED_NCCL(ctx);
     *out = nullptr;
     vpb::CtxScene sc{};
     int device = 0;
@@ -122,7 +182,7 @@ int vp_comm_init(vp_ctx *ctx, const uint8_t *id, int32_t n_ranks, int32_t rank, 
     std::memcpy(&u, id, sizeof u);
     ncclConfig_t cfg = nccl_config(max_ctas);
     cudaSetDevice(device);
-    const ncclResult_t r = ncclCommInitRankConfig(&c->nc, n_ranks, u, rank, &cfg);
+    const ncclResult_t r = nccl().CommInitRankConfig(&c->nc, n_ranks, u, rank, &cfg);
     if (r != ncclSuccess) {
         const int rc = nccl_fail(ctx, r, "ncclCommInitRankConfig");
         c->nc = nullptr;
@@ -142,18 +202,19 @@ int vp_comm_init_all(int32_t n, vp_ctx *const *ctxs, const int32_t *devices, int
         g_comm_err = "vp_comm_init_all: bad arguments";
         return VP_ERR_USAGE;
     }
+    VP_NEED_NCCL(nullptr);
     std::vector<ncclComm_t> ncs(size_t(n), nullptr);
     // ncclCommInitAll has no config argument: build each rank with ncclCommInitRankConfig
     // inside one group (the documented single-process equivalent), so maxCTAs applies
     ncclUniqueId u;
-    VP_NCCL(nullptr, ncclGetUniqueId(&u));
+    VP_NCCL(nullptr, nccl().GetUniqueId(&u));
     ncclConfig_t cfg = nccl_config(max_ctas);
-    VP_NCCL(nullptr, ncclGroupStart());
+    VP_NCCL(nullptr, nccl().GroupStart());
     for (int i = 0; i < n; ++i) {
         VP_CU(nullptr, cudaSetDevice(devices[i]));
-        VP_NCCL(nullptr, ncclCommInitRankConfig(&ncs[size_t(i)], n, u, i, &cfg));
+        VP_NCCL(nullptr, nccl().CommInitRankConfig(&ncs[size_t(i)], n, u, i, &cfg));
     }
-    VP_NCCL(nullptr, ncclGroupEnd());
+    VP_NCCL(nullptr, nccl().GroupEnd());
     for (int i = 0; i < n; ++i) {
         auto *c = new vp_comm;
         c->ctx = ctxs[i];
@@ -177,11 +238,13 @@ int vp_comm_destroy(vp_comm *comm) {
 }
 
 int vp_group_start(void) {
-    VP_NCCL(nullptr, ncclGroupStart());
+    VP_NEED_NCCL(nullptr);
+    VP_NCCL(nullptr, nccl().GroupStart());
     return VP_OK;
 }
 int vp_group_end(void) {
-    VP_NCCL(nullptr, ncclGroupEnd());
+    VP_NEED_NCCL(nullptr);
+    VP_NCCL(nullptr, nccl().GroupEnd());
     return VP_OK;
 }
 
@@ -204,11 +267,11 @@ int vp_broadcast_scene(vp_comm *comm, int32_t root) {
     VP_CU(ctx, cudaStreamWaitEvent(comm->stream, comm->ev, 0));
     const size_t k = size_t(sc.n_prim);
     if (k > 0) {
-        VP_NCCL(ctx, ncclGroupStart());
-        VP_NCCL(ctx, ncclBroadcast(sc.xf16, sc.xf16, 16 * k, ncclFloat32, root, comm->nc, comm->stream));
-        VP_NCCL(ctx, ncclBroadcast(sc.payload, sc.payload, 4 * k * size_t(sc.m) * sc.m * sc.m, ncclFloat32, root,
+        VP_NCCL(ctx, nccl().GroupStart());
+        VP_NCCL(ctx, nccl().Broadcast(sc.xf16, sc.xf16, 16 * k, ncclFloat32, root, comm->nc, comm->stream));
+        VP_NCCL(ctx, nccl().Broadcast(sc.payload, sc.payload, 4 * k * size_t(sc.m) * sc.m * sc.m, ncclFloat32, root,
                                    comm->nc, comm->stream));
-        VP_NCCL(ctx, ncclGroupEnd());
+        VP_NCCL(ctx, nccl().GroupEnd());
     }
     if (comm->rank != root) return vpb::ctx_scene_written(ctx, comm->stream);
     return VP_OK;
@@ -237,23 +300,23 @@ int vp_gather_views(vp_comm *comm, int32_t root, int32_t n_views, int64_t n_px, 
     if (int rc = vpb::ctx_wait_renders(ctx, comm->stream)) return rc;
     const size_t px = size_t(n_px);
     cudaStream_t st = comm->stream;
-    VP_NCCL(ctx, ncclGroupStart());
+    VP_NCCL(ctx, nccl().GroupStart());
     for (int j = 0; j < n_views; ++j) {
         if (!is_root) {
-            VP_NCCL(ctx, ncclSend(rgb[j], 3 * px, ncclFloat32, root, comm->nc, st));
-            VP_NCCL(ctx, ncclSend(alpha[j], px, ncclFloat32, root, comm->nc, st));
-            if (samples) VP_NCCL(ctx, ncclSend(samples[j], px, ncclInt32, root, comm->nc, st));
+            VP_NCCL(ctx, nccl().Send(rgb[j], 3 * px, ncclFloat32, root, comm->nc, st));
+            VP_NCCL(ctx, nccl().Send(alpha[j], px, ncclFloat32, root, comm->nc, st));
+            if (samples) VP_NCCL(ctx, nccl().Send(samples[j], px, ncclInt32, root, comm->nc, st));
             continue;
         }
         for (int r = 0; r < comm->n_ranks; ++r) {
             const size_t d = size_t(r) * n_views + j;
             if (r == root) continue;
-            VP_NCCL(ctx, ncclRecv(dst_rgb[d], 3 * px, ncclFloat32, r, comm->nc, st));
-            VP_NCCL(ctx, ncclRecv(dst_alpha[d], px, ncclFloat32, r, comm->nc, st));
-            if (samples) VP_NCCL(ctx, ncclRecv(dst_samples[d], px, ncclInt32, r, comm->nc, st));
+            VP_NCCL(ctx, nccl().Recv(dst_rgb[d], 3 * px, ncclFloat32, r, comm->nc, st));
+            VP_NCCL(ctx, nccl().Recv(dst_alpha[d], px, ncclFloat32, r, comm->nc, st));
+            if (samples) VP_NCCL(ctx, nccl().Recv(dst_samples[d], px, ncclInt32, r, comm->nc, st));
         }
     }
-    VP_NCCL(ctx, ncclGroupEnd());
+    VP_NCCL(ctx, nccl().GroupEnd());
     if (is_root)
         for (int j = 0; j < n_views; ++j) {
             const size_t d = size_t(root) * n_views + j;
