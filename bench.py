@@ -593,8 +593,11 @@ def main():
         flush.fill_(i & 0xff)                 # evict L2 (untimed)
         evs[i][0].record(stream)
         step(args.warmup + i)
-        if gather and i == args.steps - 1:
-            vg.finish()                       # the last step's gathers end inside the timed region
+        if gather and i == args.steps - 1:    # the last step's gathers end inside the timed region
+            if native:
+                vg.wait_slot(0, sh)           # the render stream (and its end event) waits for them
+            else:
+                vg.finish()
         evs[i][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
