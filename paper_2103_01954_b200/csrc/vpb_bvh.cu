@@ -6,7 +6,8 @@
 //   k_bvh_bounds    one CTA: bounds of the box centres
 //   k_bvh_keys      (30-bit Morton code of the centre << 32) | primitive
 //   k_radix_*       stable LSD radix sort of the keys on their 30 Morton bits (in-house: four
-//                   8-bit digit passes of tile histogram -> digit-major scan -> stable scatter)
+//                   8-bit digit passes of tile histogram -> digit-major scan -> stable scatter;
+//                   up to 8192 keys in one CTA out of shared memory)
 //   k_bvh_internal  Karras (2012) hierarchy from the sorted keys: one thread per internal node
 //   k_bvh_refit     bottom-up child boxes (second arrival at a node computes it)
 //
@@ -286,6 +287,105 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const unsigned 
     }
 }
 
+// Up to kSmallSort keys: the whole sort in ONE CTA out of shared memory (the four passes of
+// the same stable LSD scheme: histogram, scan, warp-ranked scatter), so a per-pose rebuild at
+// K = 4096 costs one launch instead of twelve (the multi-CTA path is launch-latency bound there).
+constexpr int kSmallSort = 8192, kSmallThreads = 1024, kSmallWarps = kSmallThreads / 32;
+
+size_t small_sort_smem(int n) { return (size_t)2 * n * 8 + (size_t)kSmallWarps * kRadixBins * 4; }
+
+__global__ void __launch_bounds__(kSmallThreads) k_radix_sort_small(unsigned long long *keys, int n) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(smem), *b = a + n;
+    unsigned *wcnt = reinterpret_cast<unsigned *>(b + n);  // [kSmallWarps][kRadixBins]
+    __shared__ unsigned run[kRadixBins];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < n; i += kSmallThreads) a[i] = keys[i];
+    for (int shift = 32; shift < 62; shift += 8) {
+        for (int q = tid; q < kRadixBins; q += kSmallThreads) run[q] = 0u;
+        __syncthreads();
+        for (int i = tid; i < n; i += kSmallThreads) atomicAdd(&run[radix_digit(a[i], shift)], 1u);
+        __syncthreads();
+        if (wid == 0) {  // exclusive scan of the 256 counts, 8 per lane
+            unsigned v[kRadixBins / 32], sum = 0;
+#pragma unroll
+            for (int q = 0; q < kRadixBins / 32; ++q) {
+                v[q] = run[lane * (kRadixBins / 32) + q];
+                sum += v[q];
+            }
+            unsigned incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            unsigned acc = incl - sum;
+#pragma unroll
+            for (int q = 0; q < kRadixBins / 32; ++q) {
+                run[lane * (kRadixBins / 32) + q] = acc;
+                acc += v[q];
+            }
+        }
+        __syncthreads();
+        for (int base = 0; base < n; base += kSmallThreads) {  // stable: chunks in index order
+            for (int q = tid; q < kSmallWarps * kRadixBins; q += kSmallThreads) wcnt[q] = 0u;
+            __syncthreads();
+            const int i = base + tid;
+            const bool valid = i < n;
+            const unsigned long long key = valid ? a[i] : 0ull;
+            const unsigned dg = valid ? radix_digit(key, shift) : kRadixBins;
+            const unsigned peers = __match_any_sync(0xffffffffu, dg);
+            const unsigned below = __popc(peers & ((1u << lane) - 1u));
+            if (valid && below == 0) wcnt[wid * kRadixBins + dg] = __popc(peers);
+            __syncthreads();
+            for (int q = tid; q < kRadixBins; q += kSmallThreads) {
+                unsigned acc = run[q];
+                for (int w = 0; w < kSmallWarps; ++w) {
+                    const unsigned c = wcnt[w * kRadixBins + q];
+                    wcnt[w * kRadixBins + q] = acc;
+                    acc += c;
+                }
+                run[q] = acc;
+            }
+            __syncthreads();
+            if (valid) b[wcnt[wid * kRadixBins + dg] + below] = key;
+            __syncthreads();
+        }
+        unsigned long long *t = a;
+        a = b;
+        b = t;
+    }
+    for (int i = tid; i < n; i += kSmallThreads) keys[i] = a[i];  // four passes: back in the first buffer
+}
+
+// Stable sort of n keys on bits [32, 62) into `keys` (tmp / hist: the multi-CTA path's scratch).
+cudaError_t radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n, cudaStream_t st) {
+    if (n <= 1) return cudaSuccess;
+    if (n <= kSmallSort) {
+        static bool attr_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+            cudaFuncSetAttribute(k_radix_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)small_sort_smem(kSmallSort));
+            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+        }
+        k_radix_sort_small<<<1, kSmallThreads, small_sort_smem(n), st>>>(keys, n);
+        return cudaGetLastError();
+    }
+    const int nt = (n + kRadixTile - 1) / kRadixTile;
+    unsigned long long *src = keys, *dst = tmp;
+    for (int shift = 32; shift < 62; shift += 8) {
+        k_radix_hist<<<nt, kRadixThreads, 0, st>>>(src, n, shift, hist, nt);
+        k_radix_scan<<<1, 1024, 0, st>>>(hist, kRadixBins * nt);
+        k_radix_scatter<<<nt, kRadixThreads, 0, st>>>(src, dst, n, shift, hist, nt);
+        unsigned long long *t = src;
+        src = dst;
+        dst = t;
+    }
+    return cudaGetLastError();  // an even number of passes: the result is back in keys
+}
+
 // Scratch carve-up, shared by the size query and the build.
 struct BvhScratch {
     float4 *lo, *hi, *nlo, *nhi;
@@ -326,18 +426,7 @@ size_t bvh_scratch_bytes(int n) { return n > 1 ? bvh_layout(n, nullptr).total : 
 // The BVH's key sort alone (testing): sorts n keys on bits [32, 62), stable; keys/tmp device.
 cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n,
                                 cudaStream_t st) {
-    if (n <= 1) return cudaSuccess;
-    const int nt = (n + kRadixTile - 1) / kRadixTile;
-    unsigned long long *src = keys, *dst = tmp;
-    for (int shift = 32; shift < 62; shift += 8) {
-        k_radix_hist<<<nt, kRadixThreads, 0, st>>>(src, n, shift, hist, nt);
-        k_radix_scan<<<1, 1024, 0, st>>>(hist, kRadixBins * nt);
-        k_radix_scatter<<<nt, kRadixThreads, 0, st>>>(src, dst, n, shift, hist, nt);
-        unsigned long long *t = src;
-        src = dst;
-        dst = t;
-    }
-    return cudaGetLastError();  // an even number of passes: the result is back in keys
+    return radix_sort30(keys, tmp, hist, n, st);
 }
 
 cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
@@ -356,20 +445,11 @@ cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scr
     k_bvh_keys<<<b, 256, 0, st>>>(xf16, n, bounds, k0);
     // Only the 30 Morton bits are sorted (digits at bits 32, 40, 48, 56): the keys start in
     // primitive order and the sort is stable, so equal codes stay in index order, which is the
-    // full 62-bit key order. Four passes ping-pong k0 -> k1 -> k0 -> k1 -> k0.
-    const int nt = sc.n_tiles;
-    unsigned long long *src = k0, *dst = k1;
-    for (int shift = 32; shift < 62; shift += 8) {
-        k_radix_hist<<<nt, kRadixThreads, 0, st>>>(src, n, shift, sc.hist, nt);
-        k_radix_scan<<<1, 1024, 0, st>>>(sc.hist, kRadixBins * nt);
-        k_radix_scatter<<<nt, kRadixThreads, 0, st>>>(src, dst, n, shift, sc.hist, nt);
-        unsigned long long *t = src;
-        src = dst;
-        dst = t;
-    }
-    k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(src, n, nodes, parent);
+    // full 62-bit key order. The sorted keys end up in k0.
+    if (cudaError_t e = radix_sort30(k0, k1, sc.hist, n, st)) return e;
+    k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(k0, n, nodes, parent);
     cudaMemsetAsync(flags, 0, (size_t)n * 4, st);
-    k_bvh_refit<<<b, 256, 0, st>>>(src, n, lo, hi, nodes, nlo, nhi, parent, flags);
+    k_bvh_refit<<<b, 256, 0, st>>>(k0, n, lo, hi, nodes, nlo, nhi, parent, flags);
     return cudaGetLastError();
 }
 
