@@ -299,6 +299,7 @@ int vp_comm_init(vp_ctx *ctx, const uint8_t *id, int32_t n_ranks, int32_t rank, 
  * communicator (the ncclCommInitAll pattern); out receives n communicators. Collectives of this
  * mode are issued for every rank between vp_group_start and vp_group_end. */
 int vp_comm_init_all(int32_t n, vp_ctx *const *ctxs, const int32_t *devices, int32_t max_ctas, vp_comm **out);
+/* Destroy a communicator before the context it was created for. */
 int vp_comm_destroy(vp_comm *comm);
 int vp_group_start(void);
 int vp_group_end(void);

@@ -486,6 +486,8 @@ int check_cam(vp_ctx *ctx, const vp_camera *cam) {
 
 namespace vpb {
 
+int ctx_device(const vp_ctx *ctx) { return ctx->device; }
+
 int ctx_scene(vp_ctx *ctx, CtxScene *out) {
     if (!ctx) return fail(nullptr, VP_ERR_USAGE, "null context");
     if (!ctx->has_scene) return fail(ctx, VP_ERR_USAGE, "no scene set (vp_set_scene first)");

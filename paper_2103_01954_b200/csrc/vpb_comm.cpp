@@ -169,10 +169,7 @@ int vp_comm_init(vp_ctx *ctx, const uint8_t *id, int32_t n_ranks, int32_t rank, 
     }
     VP_NEED_NCCL(ctx);
     *out = nullptr;
-    vpb::CtxScene sc{};
-    int device = 0;
-    if (vpb::ctx_scene(ctx, &sc) == VP_OK) device = sc.device;
-    else VP_CU(ctx, cudaGetDevice(&device));
+    const int device = vpb::ctx_device(ctx);
     auto *c = new vp_comm;
     c->ctx = ctx;
     c->n_ranks = n_ranks;

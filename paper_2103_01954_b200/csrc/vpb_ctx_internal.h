@@ -20,6 +20,8 @@ struct CtxScene {
     int n_prim, m, device;
     cudaStream_t stream;
 };
+// The CUDA device the context was created on.
+int ctx_device(const vp_ctx *ctx);
 // VP_ERR_USAGE when the context holds no scene (vp_set_scene first).
 int ctx_scene(vp_ctx *ctx, CtxScene *out);
 // The scene's transforms and payload are written on `st` by another agent (a broadcast): the
