@@ -793,6 +793,18 @@ int vp_get_transforms(vp_ctx *ctx, float *xf15) {
 // copies of the next chunks overlap the transfer and repack of chunk i (four slots: the host
 // copy outruns PCIe, so the copy engine never waits). Page-locked callers skip the
 // host copy. The staging buffers persist in the context.
+// The host copy threads (up to 7 besides the caller). If threads cannot be created the pool has
+// none and copies run on the calling thread (an exception must not cross the C-ABI).
+static void ensure_copy_pool(vp_ctx *ctx) {
+    if (ctx->copy_pool) return;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    try {
+        ctx->copy_pool = std::make_unique<CopyPool>(int(std::min(7u, hw > 1 ? hw - 1 : 0u)));
+    } catch (...) {
+        ctx->copy_pool = std::make_unique<CopyPool>(0);
+    }
+}
+
 static int upload_planar_host(vp_ctx *ctx, const float *payload, int64_t n_prim, int64_t m3) {
     cudaStream_t st = ctx->stream;
     const size_t per_prim = 4 * size_t(m3);  // floats
@@ -812,10 +824,7 @@ static int upload_planar_host(vp_ctx *ctx, const float *payload, int64_t n_prim,
             ctx->stage_h_floats[i] = chunk_floats;
         }
     }
-    if (!pinned && !ctx->copy_pool) {
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        ctx->copy_pool = std::make_unique<CopyPool>(int(std::min(7u, hw > 1 ? hw - 1 : 0u)));
-    }
+    if (!pinned) ensure_copy_pool(ctx);
     int slot = 0;
     for (size_t k0 = 0; k0 < size_t(n_prim); k0 += chunk_prims, slot = (slot + 1) % vp_ctx::kStageSlots) {
         const size_t nk = std::min(chunk_prims, size_t(n_prim) - k0), nfl = nk * per_prim;
@@ -858,10 +867,7 @@ static int copy_out_host(vp_ctx *ctx, const HostOut *outs, int n, cudaStream_t s
         VP_CUDA(ctx, cudaMallocHost(&ctx->out_stage, staged));
         ctx->out_stage_bytes = staged;
     }
-    if (staged && !ctx->copy_pool) {
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        ctx->copy_pool = std::make_unique<CopyPool>(int(std::min(7u, hw > 1 ? hw - 1 : 0u)));
-    }
+    if (staged) ensure_copy_pool(ctx);
     size_t off = 0;
     unsigned char *stage = static_cast<unsigned char *>(ctx->out_stage);
     for (int i = 0; i < n; ++i) {

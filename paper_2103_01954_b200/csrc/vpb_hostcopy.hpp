@@ -18,18 +18,17 @@ namespace vpb {
 // Fixed pool of workers splitting one memcpy at a time.
 class CopyPool {
   public:
+    // Throws (std::system_error) when a thread cannot be created; the threads started so far
+    // are stopped and joined first.
     explicit CopyPool(int n_threads) {
-        for (int i = 0; i < n_threads; ++i) workers_.emplace_back([this, i] { run(i); });
-    }
-    ~CopyPool() {
-        {
-            std::lock_guard<std::mutex> g(mu_);
-            stop_ = true;
-            ++gen_;
+        try {
+            for (int i = 0; i < n_threads; ++i) workers_.emplace_back([this, i] { run(i); });
+        } catch (...) {
+            shutdown();
+            throw;
         }
-        cv_.notify_all();
-        for (std::thread &t : workers_) t.join();
     }
+    ~CopyPool() { shutdown(); }
     CopyPool(const CopyPool &) = delete;
     CopyPool &operator=(const CopyPool &) = delete;
 
@@ -55,6 +54,16 @@ class CopyPool {
     }
 
   private:
+    void shutdown() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (std::thread &t : workers_) t.join();
+        workers_.clear();
+    }
     void slice(int i, int parts) const {
         const size_t per = (bytes_ / size_t(parts) + 4095) & ~size_t(4095);
         const size_t lo = std::min(bytes_, per * size_t(i)), hi = std::min(bytes_, lo + per);
