@@ -330,7 +330,7 @@ def workload_config(args, world, gather):
             "l2": "flushed (256 MiB write) before every timed step; payload 268 MB > 126 MB L2"}
 
 
-def run_tile_shard(args, rank, world, local, device):
+def run_tile_shard(args, rank, world, local, device, native=False):
     """--tile-shard: one view per step split by tile over the ranks (single-view
     configs). Step = this rank's shard render + the gather of every shard to rank 0 + rank 0
     placing the tiles into the image. value = the view's ray-samples / max-over-ranks time."""
@@ -338,7 +338,7 @@ def run_tile_shard(args, rank, world, local, device):
     import torch.distributed as dist
 
     from paper_2103_01954_b200 import Renderer, api, synthetic
-    from paper_2103_01954_b200.dist import TileShardGather, broadcast_scene
+    from paper_2103_01954_b200.dist import NativeComm, TileShardGather, broadcast_scene
 
     k, m, w = args.k, args.m, args.width
     r = Renderer(local)
@@ -348,7 +348,11 @@ def run_tile_shard(args, rank, world, local, device):
         xf = api.compose(tr)
         slab = api.PrimitiveSlab(k, m, pay)
     win = api.WindowParams()
-    if world > 1:
+    comm = None
+    if native:  # libvpb's NCCL: the shard buffers travel as one "view" of slots_max * 256 pixels
+        comm = NativeComm(r, world, rank, max_ctas=args.nccl_max_ctas)
+        comm.broadcast_scene(xf, slab, win, k, m)
+    elif world > 1:
         broadcast_scene(r, xf, slab, win, k, m, device)
     else:
         r.set_scene_composed(xf, slab, win)
@@ -359,10 +363,21 @@ def run_tile_shard(args, rank, world, local, device):
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)
 
+    dst = None
+    if native and rank == 0:  # rank r's shard lands in g.recv[r]: [rgb 3n | alpha n | samples n]
+        n = g.n
+        dst = ([t.data_ptr() for t in g.recv], [t[3 * n:].data_ptr() for t in g.recv],
+               [t[4 * n:].data_ptr() for t in g.recv])
+
     def step():
+        if native:
+            comm.wait(stream.cuda_stream)  # the previous gather has read this rank's buffer
         r.render_shard_device(cam, cfg, rank, world, rgb.data_ptr(), alpha.data_ptr(), samp.data_ptr(),
                               stream.cuda_stream)
-        if world > 1:
+        if native:
+            comm.gather_views(1, g.n, [rgb.data_ptr()], [alpha.data_ptr()], [samp.data_ptr()], dst)
+            comm.wait(stream.cuda_stream)  # rank 0 places the tiles after the gather
+        elif world > 1:
             g.gather()
             g.wait()
         if rank == 0:
@@ -394,8 +409,9 @@ def run_tile_shard(args, rank, world, local, device):
     clk = clocks.stop()
     t_local = sum(a.elapsed_time(b) for a, b in evs) / 1e3
     march_ms = r.kernel_times(4096)
-    t = torch.tensor([t_local], dtype=torch.float64, device=device)
-    tot = torch.tensor([mine["ray_samples"], mine["prim_samples"]], dtype=torch.float64, device=device)
+    cdev = "cpu" if native else device  # gloo (the native data plane's control plane) reduces CPU tensors
+    t = torch.tensor([t_local], dtype=torch.float64, device=cdev)
+    tot = torch.tensor([mine["ray_samples"], mine["prim_samples"]], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot)
@@ -414,6 +430,8 @@ def run_tile_shard(args, rank, world, local, device):
                                        f"{world} GPU(s) (BASELINE config {3 if k == 4096 else 'n/a'}, tile-sharded)",
                            "K": k, "M": m, "width": w, "height": w, "parallelism": f"tile-shard x{world}",
                            "gather_to_rank0": world > 1,
+                           "data_plane": ("libvpb vp_comm_* (NCCL)" if native else
+                                          ("torch.distributed NCCL" if world > 1 else "none (1 GPU)")),
                            "l2": "flushed (256 MiB write) before every timed step"},
                 "frames_per_s": round(args.steps / t_max, 2),
                 "prim_samples_per_s": round(prim_view * args.steps / t_max / 1e6, 3),
@@ -425,6 +443,8 @@ def run_tile_shard(args, rank, world, local, device):
                 # per step: 6 binning stages, the raymarch and its fallback (one view)
                 "gpu_launches": 8 * args.steps, "clocks": clk}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     r.close()
 
 
@@ -450,14 +470,14 @@ def main():
     # data plane: libvpb's own NCCL (vp_comm_*), so torch.distributed is only the control plane
     # (rendezvous, the NCCL id, barriers, the max-over-ranks timing): gloo on CPU tensors.
     # --torch-comm (and the tile-shard mode) move the data plane to torch.distributed NCCL.
-    native = (world > 1 or args.comm_at_1) and not (args.torch_comm or args.tile_shard)
+    native = (world > 1 or args.comm_at_1) and not args.torch_comm
     if world > 1:
         if native:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=device)
     if args.tile_shard:
-        run_tile_shard(args, rank, world, local, device)
+        run_tile_shard(args, rank, world, local, device, native=native)
         if world > 1:
             dist.destroy_process_group()
         return
