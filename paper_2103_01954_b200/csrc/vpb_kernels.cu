@@ -386,7 +386,7 @@ __global__ void k_tile_sort_big(const __grid_constant__ BinBatch bb) {
 // window index slots per thread (16-bit units): Window::C word-interleaves the indices, so
 // the region is rounded up to whole words of every width
 template <int CAP>
-constexpr size_t kWcSlots = (size_t)((CAP + 3) / 4 * 4);
+constexpr size_t kWcSlots = VPB_WC_INTERLEAVE ? (size_t)((CAP + 3) / 4 * 4) : (size_t)CAP;
 
 struct TileSmem {
     float4 *xf4;       // CC * 4
