@@ -10,8 +10,14 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -prec-div=true -prec-sq
             -Xcompiler -fPIC,-ffp-contract=off,-O3 -Xptxas -v
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.hpp $(SRC)/*.cuh) include/vpb.h
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean examples
 all: lib oracle
+# a C++ multi-GPU caller of the C-ABI (integration/ring_multi_gpu.cpp)
+examples: build/ring_multi_gpu
+build/ring_multi_gpu: integration/ring_multi_gpu.cpp include/vpb.h $(PKG)/libvpb.so
+	@mkdir -p build
+	g++ -O2 -std=c++17 -Iinclude -I/usr/local/cuda/include $< -L$(PKG) -lvpb -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 lib: $(PKG)/libvpb.so
 oracle:
 	$(MAKE) -C oracle all
