@@ -653,7 +653,12 @@ def main():
                 "alg_bytes_per_launch": int(alg_bytes_per_launch), "avg_launch_ms": round(march_avg_s * 1e3, 4),
                 "march_share_of_step": round(march_avg_s * V / views_per_launch * args.steps / max(t_local, 1e-12), 4),
                 "frame_ms": round(frame_s * 1e3, 4),
-                "frame_frac": round(alg_bytes_per_launch / views_per_launch / frame_s / 1e9 / hbm, 4)}
+                "frame_frac": round(alg_bytes_per_launch / views_per_launch / frame_s / 1e9 / hbm, 4),
+                # the bytes a launch cannot avoid (the payload read once, the
+                # outputs written once) and the time they take at the peak
+                "compulsory_bytes_per_launch": int(k * m ** 3 * 16 + BYTES_PER_PIXEL * w * w * views_per_launch),
+                "compulsory_ms_at_peak": round((k * m ** 3 * 16 + BYTES_PER_PIXEL * w * w * views_per_launch)
+                                               / (hbm * 1e9) * 1e3, 4)}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
