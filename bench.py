@@ -440,8 +440,8 @@ def run_tile_shard(args, rank, world, local, device, native=False):
                              "kernel": "k_march_tiles (+k_march_fallback_views), rank 0's shard",
                              "peak_kind": pk_kind, "avg_launch_ms": round(march_s * 1e3, 4)},
                 "cpu_baseline": None, "e2e": None,
-                # per step: 6 binning stages, the raymarch and its fallback (one view)
-                "gpu_launches": 8 * args.steps, "clocks": clk}
+                # per step: 6 binning stages, the raymarch, its fallback and the last-resort pass
+                "gpu_launches": 9 * args.steps, "clocks": clk}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
@@ -754,9 +754,9 @@ def main():
                 "digest_ok": digest_ok,  # every timed view bit-equal to the reference's digest
                 "ray_samples_per_view": ray_samples // V, "prim_samples_per_view": prim_samples // V,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sweep": sweep,
-                # per step, batched: 6 binning stages for all views, the cross-view tile order, one
-                # raymarch and one fallback launch; per view: 6 + 2 launches for each view
-                "gpu_launches": (9 if batch else 8 * V) * args.steps,
+                # per step, batched: 6 binning stages for all views, the cross-view tile order, the
+                # raymarch, the fallback and the last-resort pass; per view: 6 + 3 for each view
+                "gpu_launches": (10 if batch else 9 * V) * args.steps,
                 "clocks": clk, "scene_broadcast_bytes": bcast_bytes,
                 "data_plane": ("libvpb vp_comm_* (NCCL: vp_broadcast_scene once, one grouped vp_gather_views per "
                                f"step, maxCTAs {args.nccl_max_ctas}; torch.distributed gloo for control only)"

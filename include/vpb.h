@@ -81,7 +81,7 @@ typedef struct vp_stats {
     int64_t keys;          /* (tile, depth) keys emitted by the binning pass */
     int64_t refills;       /* per-ray window refills (rays with > window hits) */
     float ms;              /* device time of the render (CUDA events), ms */
-    float reserved;
+    int32_t huge_rays;     /* rays marched by the last-resort pass (> 256 live segments) */
 } vp_stats;
 
 int vp_version(void);

@@ -39,10 +39,10 @@ class vp_stats(C.Structure):
                 ("hit_rays", C.c_int64), ("early_exits", C.c_int64),
                 ("saturated", C.c_int64), ("overflow_rays", C.c_int64),
                 ("keys", C.c_int64), ("refills", C.c_int64), ("ms", C.c_float),
-                ("reserved", C.c_float)]
+                ("huge_rays", C.c_int32)]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_}
 
 
 # name -> (restype, argtypes): every entry point of include/vpb.h

@@ -82,7 +82,7 @@ struct BinSlot {
     DBuf<int4> rects, prects;
     DBuf<uint32_t> keys, tile_counts, offsets, cursor, order;
     DBuf<unsigned long long> entries;
-    DBuf<int> ovf;
+    DBuf<int> ovf, huge;  // window-overflow pixels; pixels for the huge pass (kHugeListCap)
     int ovf_cap = 0;
     DevCounters *d_ctr = nullptr;
     cudaEvent_t ev_binned = nullptr, ev_marched = nullptr;
@@ -129,6 +129,8 @@ struct vp_ctx {
     DBuf<int> out_samples, ovf_list;
     DBuf<float> fb_e, fb_x;
     DBuf<int> fb_c;
+    DBuf<float> hg_e, hg_x;  // K5c (k_march_huge_views) windows
+    DBuf<int> hg_c;
     DBuf<float> ray_o, ray_d, ray_j;
     DevCounters *d_ctr = nullptr, *h_ctr = nullptr;
     DevCounters *last_ctr[kMaxViews] = {};  // the counters of the latest render launch's views
@@ -263,6 +265,10 @@ int ensure_fallback(vp_ctx *ctx) {
     VP_CUDA(ctx, ctx->fb_e.ensure(n));
     VP_CUDA(ctx, ctx->fb_x.ensure(n));
     VP_CUDA(ctx, ctx->fb_c.ensure(n));
+    const size_t nh = size_t(kHugeThreads) * kHugeCap;  // K5c windows (29 MB)
+    VP_CUDA(ctx, ctx->hg_e.ensure(nh));
+    VP_CUDA(ctx, ctx->hg_x.ensure(nh));
+    VP_CUDA(ctx, ctx->hg_c.ensure(nh));
     return VP_OK;
 }
 
@@ -295,6 +301,7 @@ int ensure_slot_buffers(vp_ctx *ctx, BinSlot &b, const CamDev &cam) {
         VP_CUDA(ctx, b.ovf.ensure(n_px));
         b.ovf_cap = int(n_px);
     }
+    VP_CUDA(ctx, b.huge.ensure(size_t(kHugeListCap)));
     return ensure_fallback(ctx);
 }
 
@@ -358,7 +365,8 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
         unsigned long long *kh = ctx->h_keys + ctx->group * kMaxViews + v;  // grow_key_capacity reads it
         bb.v[v] = BinView{cams[v], b.rects.p, b.prects.p, b.keys.p, b.tile_counts.p, b.offsets.p, b.cursor.p,
                           b.order.p, b.entries.p, b.d_ctr, ctx->d_keys + (kh - ctx->h_keys)};
-        vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap};
+        vb.v[v] = ViewDev{cams[v], ods[v], b.prects.p, b.offsets.p, b.entries.p, b.d_ctr, b.ovf.p, b.ovf_cap,
+                          b.huge.p, kHugeListCap};
         counts[v] = b.tile_counts.p;
         n_tiles[v] = cams[v].tiles_x * cams[v].tiles_y;
         total += n_tiles[v];
@@ -401,6 +409,8 @@ int enqueue_views(vp_ctx *ctx, int n, const CamDev *cams, const MarchDev &mp, co
                                     ctx->tile_cfg < 0 ? ctx->tier : TileTier(ctx->tile_cfg), st));
     VP_CUDA(ctx, launch_march_fallback_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->fb_e.p,
                                              ctx->fb_x.p, ctx->fb_c.p, ctx->ovf_tile_lists.p, st));
+    VP_CUDA(ctx, launch_march_huge_views(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, vb, ctx->hg_e.p,
+                                         ctx->hg_x.p, ctx->hg_c.p, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->t_ev[2 * slot + 1], st));
     for (int v = 0; v < n; ++v) VP_CUDA(ctx, cudaEventRecord(grp[v].ev_marched, st));
     VP_CUDA(ctx, cudaEventRecord(ctx->ev_last_marched, st));
@@ -440,13 +450,14 @@ void fill_stats(const DevCounters &c, float ms, vp_stats *s) {
     s->keys = int64_t(c.keys);
     s->refills = int64_t(c.refills);
     s->ms = ms;
-    s->reserved = 0;
+    s->huge_rays = int32_t(c.huge_rays);
 }
 
 int check_counters(vp_ctx *ctx, const DevCounters &c) {
     if (c.fallback_fail)
         return fail(ctx, VP_ERR_NUMERIC,
-                    "a ray has more than 256 simultaneously live primitive segments");
+                    "a ray has more simultaneously live primitive segments than the widest window holds "
+                    "(4096 for camera renders, 256 for ray batches)");
     if (c.numeric_fail) return fail(ctx, VP_ERR_NUMERIC, "quadrature did not terminate");
     return VP_OK;
 }
@@ -634,6 +645,7 @@ int vp_destroy(vp_ctx *ctx) {
         for (auto *u : {&b.keys, &b.tile_counts, &b.offsets, &b.cursor, &b.order}) u->release();
         b.entries.release();
         b.ovf.release();
+        b.huge.release();
         if (b.d_ctr) cudaFree(b.d_ctr);
         if (b.ev_binned) cudaEventDestroy(b.ev_binned);
         if (b.ev_marched) cudaEventDestroy(b.ev_marched);
@@ -654,7 +666,9 @@ int vp_destroy(vp_ctx *ctx) {
         if (ctx->ev_brendered[g]) cudaEventDestroy(ctx->ev_brendered[g]);
         if (ctx->ev_bcopied[g]) cudaEventDestroy(ctx->ev_bcopied[g]);
     }
-    for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c}) b->release();
+    for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c, &ctx->hg_c}) b->release();
+    ctx->hg_e.release();
+    ctx->hg_x.release();
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->h_keys) cudaFreeHost(ctx->h_keys);
     for (cudaEvent_t ev : ctx->ev_keys)
@@ -1164,6 +1178,7 @@ int vp_read_stats(vp_ctx *ctx, vp_stats *stats) {
         c.nonempty_tiles += q.nonempty_tiles;
         c.key_overflow |= q.key_overflow;
         c.fallback_fail |= q.fallback_fail;
+        c.huge_rays += q.huge_rays;
     }
     note_density(ctx, c);
     fill_stats(c, 0.f, stats);

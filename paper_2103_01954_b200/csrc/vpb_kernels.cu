@@ -930,11 +930,82 @@ __device__ __forceinline__ void fallback_pixel(const ViewDev &vd, const MarchDev
         ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, tab);
     }
     ok = !ro.overflow;
-    if (!ok) {
-        atomicAdd(&vd.ctr->fallback_fail, 1);
+    if (!ok) {  // more live segments than kFallbackCap: the huge pass takes the pixel
+        const unsigned slot = atomicAdd(&vd.ctr->huge_rays, 1u);
+        if ((int)slot < vd.huge_cap) vd.huge_list[slot] = p;
+        else atomicAdd(&vd.ctr->fallback_fail, 1);
         return;
     }
     write_pixel(vd.od, p, ro);
+}
+
+// All K primitives as candidates, filtered by their pixel rectangles (k_march_huge_views).
+struct AllCands {
+    const float *xf_g;
+    const int4 *prects_g;
+    const float4 *payload;
+    unsigned m3;
+    int n;
+    static constexpr bool kRs = false;
+    __device__ __forceinline__ int prim(int c) const { return c; }
+    __device__ __forceinline__ const float *xf(int c) const { return xf_g + (size_t)c * kXfStride; }
+    __device__ __forceinline__ Xf16 xfv(int c) const { return ldg_xf(xf(c)); }
+    __device__ __forceinline__ const float4 *base(int c) const { return payload + (size_t)c * m3; }
+    __device__ __forceinline__ bool covers(int c, int2 px) const {
+        const int4 r = prects_g[c];
+        return px.x >= r.x && px.x <= r.z && px.y >= r.y && px.y <= r.w;
+    }
+    __device__ __forceinline__ bool hit(int c, V3 o, V3 d, float &tE, float &tX) const {
+        return intersect_obb(xf(c), o, d, tE, tX);
+    }
+};
+
+// K5c: camera pixels with more than kFallbackCap live segments, marched with kHugeCap-entry
+// windows over all primitives (the window keeps the smallest (tEnter, prim) keys whatever the
+// candidate order, so the segment lists are the tile kernel's). Beyond kHugeCap: Numeric.
+__global__ void __launch_bounds__(32)
+k_march_huge_views(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+                   ViewBatch views, float *scratch_e, float *scratch_x, int *scratch_c) {
+    __shared__ unsigned long long s_tab[32];
+    load_exp_tab(s_tab);
+    __syncthreads();
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const unsigned m3 = (unsigned)(mp.m * mp.m * mp.m);
+    for (int v = 0; v < views.n; ++v) {
+        const ViewDev &vd = views.v[v];
+        DevCounters *ctr = vd.ctr;
+        const int n = (int)min((unsigned)vd.huge_cap, ctr->huge_rays);
+        const CamDev &cam = vd.cam;
+        const AllCands all{xf_g, vd.prects, payload, m3, n_prim};
+        for (int q = gtid; q < n; q += nthreads) {
+            const int p = vd.huge_list[q];
+            const int px = p % cam.width, py = p / cam.width;
+            V3 o, d;
+            generate_ray(cam, (float)px + 0.5f, (float)py + 0.5f, o, d);
+            const float jit = mp.jitter ? hash_to_unit(hash_combine(mp.seed, (uint64_t)(uint32_t)p)) : 0.5f;
+            const RayOut ro = march_ray<kHugeCap>(all, w, o, d, make_int2(px, py), jit, mp, s_tab);
+            if (ro.overflow) {
+                atomicAdd(&ctr->fallback_fail, 1);
+                continue;
+            }
+            write_pixel(vd.od, p, ro);
+            atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);  // rare path: plain atomics
+            atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
+            atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
+            atomicAdd(&ctr->early_exits, (unsigned long long)ro.early);
+            atomicAdd(&ctr->saturated, (unsigned long long)ro.saturated);
+            atomicAdd(&ctr->refills, (unsigned long long)ro.refills);
+            if (ro.numeric) atomicAdd(&ctr->numeric_fail, 1ull);
+        }
+    }
+}
+
+cudaError_t launch_march_huge_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                    const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st) {
+    k_march_huge_views<<<kHugeThreads / 32, 32, 0, st>>>(mp, xf16, n_prim, payload, views, se, sx, sc);
+    return cudaGetLastError();
 }
 
 // K5b over every view of a launch.

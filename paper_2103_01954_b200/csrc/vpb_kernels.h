@@ -22,7 +22,7 @@ struct DevCounters {
     // primitives' pixel rectangles instead of its (unwritten) bucket
     unsigned key_cap;
     unsigned bwd_long;  // K6: rays whose segment list the forward did not keep (k_backward_rays_list)
-    unsigned pad_;
+    unsigned huge_rays;  // camera pixels for k_march_huge_views (more than kFallbackCap live segments)
 };
 
 // A tile whose bucket [offsets[t], offsets[t+1]) does not fit the entries buffer. K2 saturates
@@ -84,6 +84,8 @@ struct ViewDev {
     DevCounters *ctr;
     int *ovf_list;
     int ovf_cap;
+    int *huge_list;  // pixels whose live segments overflow even K5b's window (k_march_huge_views)
+    int huge_cap;
 };
 constexpr int kMaxViews = 16;
 struct ViewBatch {
@@ -139,6 +141,12 @@ struct AdamDev {
 constexpr int kFallbackCap = 256;      // segment window of the fallback re-march
 constexpr int kRaySegs = 96;  // segments per ray held by the warp-per-ray kernels
 constexpr int kFallbackBlocks = 148;   // one CTA per SM
+// The last resort for camera rays: more than kFallbackCap primitives live at one sample (the
+// reference has no limit). One thread per such pixel over ALL primitives (their pixel rectangles
+// filter them), with kHugeCap-entry windows in global scratch: rare, so a small grid.
+constexpr int kHugeCap = 4096;
+constexpr int kHugeThreads = 148 * 4;
+constexpr int kHugeListCap = 1 << 16;  // per view
 constexpr int kFallbackThreads = 128;
 // key-overflowed tiles (tile_key_overflowed): a fallback CTA rebuilds such a tile's candidate
 // list from all K pixel rectangles into its own slice of K entries of global scratch
@@ -177,6 +185,10 @@ cudaError_t launch_build_pairs(const float4 *payload, float4 *pairs, int64_t n_p
 cudaError_t launch_march_fallback_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
                                         const ViewBatch &views, float *se, float *sx, int *sc,
                                         uint32_t *tile_scratch, cudaStream_t st);
+// The views' huge pixels (ViewDev::huge_list, ctr->huge_rays), kHugeCap windows in se/sx/sc
+// (kHugeThreads * kHugeCap entries each).
+cudaError_t launch_march_huge_views(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                    const ViewBatch &views, float *se, float *sx, int *sc, cudaStream_t st);
 // Heaviest-first order over the tiles of several views (counting sort of their candidate counts).
 cudaError_t launch_batch_order(const uint32_t *const *tile_counts, const int *n_tiles, int n_views, uint32_t *order,
                                cudaStream_t st);

@@ -87,3 +87,31 @@ def test_random_scene_key_overflow_matches_restatement(oracle, case):
     assert np.array_equal(out.sample_counts, samples), "sample counts differ"
     assert np.array_equal(_bits(out.alpha), _bits(alpha)), "alpha differs"
     assert np.array_equal(_bits(out.color), _bits(rgb)), "rgb differs"
+
+
+@pytest.mark.parametrize("n_boxes", [300, 700])
+def test_more_live_segments_than_the_fallback_window(oracle, n_boxes):
+    """More than kFallbackCap (256) primitives live at one sample: boxes stacked on the same
+    region. The reference has no limit; camera renders take the last-resort pass (K5c,
+    4096-entry windows over all primitives) and still equal the restatement bit for bit."""
+    rng = np.random.default_rng(n_boxes)
+    t = rng.uniform(-0.02, 0.02, (n_boxes, 3))
+    s = rng.uniform(0.2, 0.3, (n_boxes, 3))
+    tr = api.transform_records(t, np.tile(np.eye(3), (n_boxes, 1, 1)), s, delta_r=rng.uniform(-0.3, 0.3, (n_boxes, 3)))
+    m = 2
+    pay = rng.uniform(0, 1, n_boxes * 4 * m ** 3).astype(np.float32)
+    pay.reshape(n_boxes, 4, -1)[:, 3] *= np.float32(0.02)  # thin: rays cross the whole stack
+    xf = api.compose(tr)
+    cam, _ = synthetic.look_at_camera((0.1, 0.2, -2.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 60.0, 40, 36)
+    cfg = api.MarchConfig(step_size=0.005)
+    r = Renderer(0)
+    try:
+        r.set_scene_composed(xf, api.PrimitiveSlab(n_boxes, m, pay), api.WindowParams())
+        out = r.render(cam, cfg)
+    finally:
+        r.close()
+    rgb, alpha, samples = oracle.render(xf, m, pay, api.WindowParams(), cam, cfg)
+    assert out.stats["overflow_rays"] > 0 and out.stats["huge_rays"] > 0, out.stats
+    assert np.array_equal(out.sample_counts, samples), "sample counts differ"
+    assert np.array_equal(_bits(out.alpha), _bits(alpha)), "alpha differs"
+    assert np.array_equal(_bits(out.color), _bits(rgb)), "rgb differs"
