@@ -129,8 +129,9 @@ struct vp_ctx {
     DBuf<int> out_samples, ovf_list;
     DBuf<float> fb_e, fb_x;
     DBuf<int> fb_c;
-    DBuf<float> hg_e, hg_x;  // K5c (k_march_huge_views) windows
+    DBuf<float> hg_e, hg_x;  // K5c (k_march_huge_views / _rays, k_backward_rays_huge) windows
     DBuf<int> hg_c;
+    DBuf<int> huge_ray_list;  // ray batches: the rays for the last-resort passes
     DBuf<float> ray_o, ray_d, ray_j;
     DevCounters *d_ctr = nullptr, *h_ctr = nullptr;
     DevCounters *last_ctr[kMaxViews] = {};  // the counters of the latest render launch's views
@@ -266,6 +267,7 @@ int ensure_fallback(vp_ctx *ctx) {
     VP_CUDA(ctx, ctx->fb_x.ensure(n));
     VP_CUDA(ctx, ctx->fb_c.ensure(n));
     const size_t nh = size_t(kHugeThreads) * kHugeCap;  // K5c windows (29 MB)
+    VP_CUDA(ctx, ctx->huge_ray_list.ensure(size_t(kHugeListCap)));
     VP_CUDA(ctx, ctx->hg_e.ensure(nh));
     VP_CUDA(ctx, ctx->hg_x.ensure(nh));
     VP_CUDA(ctx, ctx->hg_c.ensure(nh));
@@ -457,7 +459,7 @@ int check_counters(vp_ctx *ctx, const DevCounters &c) {
     if (c.fallback_fail)
         return fail(ctx, VP_ERR_NUMERIC,
                     "a ray has more simultaneously live primitive segments than the widest window holds "
-                    "(4096 for camera renders, 256 for ray batches)");
+                    "(4096)");
     if (c.numeric_fail) return fail(ctx, VP_ERR_NUMERIC, "quadrature did not terminate");
     return VP_OK;
 }
@@ -669,6 +671,7 @@ int vp_destroy(vp_ctx *ctx) {
     for (auto *b : {&ctx->out_samples, &ctx->ovf_list, &ctx->fb_c, &ctx->hg_c}) b->release();
     ctx->hg_e.release();
     ctx->hg_x.release();
+    ctx->huge_ray_list.release();
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->h_keys) cudaFreeHost(ctx->h_keys);
     for (cudaEvent_t ev : ctx->ev_keys)
@@ -1300,7 +1303,11 @@ int vp_march_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         const CamDev none{};
         VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, ctx->n_prim, ctx->payload.p,
                                            nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p,
-                                           ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+                                           ctx->ovf_cap, ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st,
+                                           ctx->huge_ray_list.p, kHugeListCap));
+        VP_CUDA(ctx, launch_march_huge_rays(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, od, rays, ctx->d_ctr,
+                                            ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p, ctx->hg_x.p, ctx->hg_c.p,
+                                            st));
     }
     if (!d_rgb) VP_CUDA(ctx, cudaMemcpyAsync(rgb, od.rgb, 12 * n, cudaMemcpyDeviceToHost, st));
     if (!d_alpha) VP_CUDA(ctx, cudaMemcpyAsync(alpha, od.alpha, 4 * n, cudaMemcpyDeviceToHost, st));
@@ -1482,7 +1489,11 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             const CamDev none{};
             VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, k, ctx->payload.p, nullptr,
                                                nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
-                                               ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+                                               ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st, ctx->huge_ray_list.p,
+                                               kHugeListCap));
+            VP_CUDA(ctx, launch_march_huge_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, od, rays, ctx->d_ctr,
+                                                ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p, ctx->hg_x.p,
+                                                ctx->hg_c.p, st));
             fwd_state = od.state;
             fwd_segs = od.segs;
         }
@@ -1494,7 +1505,8 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->bwd_list.p, int(n), ctx->fb_e.p, ctx->fb_x.p,
-                                          ctx->fb_c.p, st));
+                                          ctx->fb_c.p, st, ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p,
+                                          ctx->hg_x.p, ctx->hg_c.p));
         if (v4)
             VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(ctx->g_pay4.p), dg, ctx->g_touched.p, k,
                                                unsigned(size_t(m) * m * m), accumulate != 0, st));
@@ -1614,7 +1626,11 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
         const CamDev none{};
         VP_CUDA(ctx, launch_march_fallback(true, none, mp, ctx->xfb[ctx->xfi].p, nullptr, ctx->n_prim, ctx->payload.p,
                                            nullptr, nullptr, od, rays, ctx->d_ctr, ctx->ovf_list.p, ctx->ovf_cap,
-                                           ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st));
+                                           ctx->fb_e.p, ctx->fb_x.p, ctx->fb_c.p, st, ctx->huge_ray_list.p,
+                                           kHugeListCap));
+        VP_CUDA(ctx, launch_march_huge_rays(mp, ctx->xfb[ctx->xfi].p, ctx->n_prim, ctx->payload.p, od, rays, ctx->d_ctr,
+                                            ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p, ctx->hg_x.p, ctx->hg_c.p,
+                                            st));
     }
     // lossPho (losses.cpp:12-25): residuals and adjoints on the device, the scalar sum on the
     // host in the reference's sequential order

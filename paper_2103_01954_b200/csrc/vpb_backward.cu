@@ -466,14 +466,14 @@ __device__ __forceinline__ void load_fwd_state(FwdReplay<BvhCands> &fwd, const f
 
 // backwardRay of one ray by one thread with a kFallbackCap-entry window; returns 0, or 1 / 2
 // (window overflow / runaway walk).
-template <class Win>
+template <int CAP, class Win>
 __device__ int backward_one_ray(const BvhCands &cands, const Win &w, const MarchDev &mp,
                                 const unsigned long long *tab, const BwdDev &bd, V3 o, V3 d, float jit,
                                 int64_t r) {
     const int2 px = make_int2(0, 0);
     int cnt = 0;
     bool more = false;
-    window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+    window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     if (cnt == 0) return 0;
     const int k0 = cands.prim(w.C(0));
     const float tMin = w.E(0);
@@ -483,16 +483,16 @@ __device__ int backward_one_ray(const BvhCands &cands, const Win &w, const March
     if (have_fwd)  // the forward pass of this very ray recorded the replay's results
         load_fwd_state(fwd, bd.fwd_state + 8 * r);
     else
-        st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
+        st = walk_steps<CAP>(cands, w, cnt, more, o, d, px, jit, mp.dt, 1ll << 62, fwd);
     if (st != 0 || fwd.lastStep < 0) return st;
     const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
     BwdWalk<BvhCands> bw(cands, mp, tab, fwd, bd, d, aRgb, bd.adj_alpha[r]);
     if (!have_fwd) {  // the replay consumed the window
         cnt = 0;
         more = false;
-        window_scan<kFallbackCap>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
+        window_scan<CAP>(w, cands, cnt, more, o, d, px, true, 0.f, 0);
     }
-    st = walk_steps<kFallbackCap>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
+    st = walk_steps<CAP>(cands, w, cnt, more, o, d, px, jit, mp.dt, fwd.lastStep, bw);
     if (st == 0) anchor_chain(bw, cands, bd, k0, tMin, bw.gTmin, o, d);
     bw.flush();
     return st;
@@ -518,7 +518,32 @@ k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const int st = backward_one_ray(cands, w, mp, s_tab, bd, o, d, jit, r);
+        const int st = backward_one_ray<kFallbackCap>(cands, w, mp, s_tab, bd, o, d, jit, r);
+        if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
+        if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
+    }
+}
+
+// The rays whose forward needed the last-resort pass (more than kFallbackCap live segments:
+// forward state[7] == -2): the per-thread walk with kHugeCap-entry windows.
+__global__ void __launch_bounds__(32)
+k_backward_rays_huge(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
+                     const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
+                     const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
+    __shared__ unsigned long long s_tab[32];
+    load_exp_tab(s_tab);
+    __syncthreads();
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const Window<int> w{se, sx, sc, nthreads, gtid};
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
+    const int n = (int)min((unsigned)list_cap, ctr->bwd_huge);
+    for (int q = gtid; q < n; q += nthreads) {
+        const int64_t r = ray_list[q];
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        const int st = backward_one_ray<kHugeCap>(cands, w, mp, s_tab, bd, o, d, jit, r);
         if (st == 1) atomicAdd(&ctr->fallback_fail, 1);
         if (st == 2) atomicAdd(&ctr->numeric_fail, 1ull);
     }
@@ -545,7 +570,7 @@ constexpr int kWarpCandBwd = 256;
 __global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, int *__restrict__ ray_list,
-                     int list_cap) {
+                     int list_cap, int *__restrict__ huge_list, int huge_cap) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];
@@ -564,8 +589,14 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
         const int nh = __float_as_int(bd.fwd_state[8 * r + 7]);
         if (nh < 0) {
             if (lane == 0) {
-                const unsigned slot = atomicAdd(&ctr->bwd_long, 1u);
-                if ((int)slot < list_cap) ray_list[slot] = (int)r;
+                if (nh == -2 && huge_list) {  // the forward needed more than kFallbackCap live segments
+                    const unsigned slot = atomicAdd(&ctr->bwd_huge, 1u);
+                    if ((int)slot < huge_cap) huge_list[slot] = (int)r;
+                    else atomicAdd(&ctr->fallback_fail, 1);
+                } else {
+                    const unsigned slot = atomicAdd(&ctr->bwd_long, 1u);
+                    if ((int)slot < list_cap) ray_list[slot] = (int)r;
+                }
             }
             continue;
         }
@@ -748,7 +779,8 @@ cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *tou
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
-                                 float *sx, int *sc, cudaStream_t st) {
+                                 float *sx, int *sc, cudaStream_t st, int *huge_list, int huge_cap, float *he,
+                                 float *hx, int *hc) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
     // The adjoint walk goes warp-per-ray for every batch size (the forward's state and segment
     // lists are required): one ray per thread leaves 27 % of the lanes busy (the rays' walks
@@ -756,10 +788,15 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
     if (!bd.fwd_state || !bd.fwd_segs) return cudaErrorInvalidValue;
     const int64_t blocks = (n_rays + 3) / 4;
     k_backward_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
-        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap);
+        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap);
     if (cudaError_t e = cudaGetLastError()) return e;
     k_backward_rays_list<<<kBackwardWarps, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, ray_list,
                                                          list_cap, se, sx, sc);
+    if (huge_list) {
+        if (cudaError_t e = cudaGetLastError()) return e;
+        k_backward_rays_huge<<<kHugeThreads / 32, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, huge_list,
+                                                                huge_cap, he, hx, hc);
+    }
     return cudaGetLastError();
 }
 

@@ -563,7 +563,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
                  const int4 *__restrict__ prects, int n_prim, const float4 *__restrict__ payload,
                  const uint32_t *__restrict__ offsets, const unsigned long long *__restrict__ entries,
                  OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ ovf_list,
-                 int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c) {
+                 int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c, int *huge_list, int huge_cap) {
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
@@ -595,8 +595,10 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
                                          nullptr};
             ro = march_ray<kFallbackCap>(cands, w, o, d, make_int2(px, py), jit, mp, s_tab);
         }
-        if (ro.overflow) {
-            atomicAdd(&ctr->fallback_fail, 1);
+        if (ro.overflow) {  // more live segments than kFallbackCap: the last-resort pass
+            const unsigned slot = atomicAdd(&ctr->huge_rays, 1u);
+            if (huge_list && (int)slot < huge_cap) huge_list[slot] = p;
+            else atomicAdd(&ctr->fallback_fail, 1);
             continue;
         }
         write_ray(od, p, ro);  // (od.state is null for camera renders)
@@ -1159,11 +1161,56 @@ cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const March
                                   const float4 *payload, const uint32_t *offsets,
                                   const unsigned long long *entries, const OutDev &od,
                                   const RaysDev &rays, DevCounters *ctr, const int *ovf_list,
-                                  int ovf_cap, float *se, float *sx, int *sc, cudaStream_t st) {
+                                  int ovf_cap, float *se, float *sx, int *sc, cudaStream_t st, int *huge_list,
+                                  int huge_cap) {
     // camera renders re-march their overflow rays in k_march_fallback_views
     if (!rays_mode) return cudaErrorInvalidValue;
     k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-        cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc);
+        cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc,
+        huge_list, huge_cap);
+    return cudaGetLastError();
+}
+
+// K5c for arbitrary rays: kHugeCap-entry windows through the BVH, one thread per ray.
+__global__ void __launch_bounds__(32)
+k_march_huge_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+                  OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ huge_list, int huge_cap,
+                  float *scratch_e, float *scratch_x, int *scratch_c) {
+    __shared__ unsigned long long s_tab[32];
+    load_exp_tab(s_tab);
+    __syncthreads();
+    const int nthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
+    const int n = (int)min((unsigned)huge_cap, ctr->huge_rays);
+    for (int q = gtid; q < n; q += nthreads) {
+        const int p = huge_list[q];
+        const V3 o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
+        const V3 d = mk3(rays.dirs[3 * p], rays.dirs[3 * p + 1], rays.dirs[3 * p + 2]);
+        const float jit = rays.jitter ? rays.jitter[p] : 0.5f;
+        const RayOut ro = march_ray<kHugeCap>(cands, w, o, d, make_int2(0, 0), jit, mp, s_tab);
+        if (ro.overflow) {
+            atomicAdd(&ctr->fallback_fail, 1);
+            continue;
+        }
+        write_ray(od, p, ro);
+        if (od.state) od.state[8 * (size_t)p + 7] = __int_as_float(-2);  // the backward's huge pass
+        atomicAdd(&ctr->ray_samples, (unsigned long long)ro.samples);
+        atomicAdd(&ctr->prim_samples, (unsigned long long)ro.prim_samples);
+        atomicAdd(&ctr->hit_rays, (unsigned long long)ro.hit);
+        atomicAdd(&ctr->early_exits, (unsigned long long)ro.early);
+        atomicAdd(&ctr->saturated, (unsigned long long)ro.saturated);
+        atomicAdd(&ctr->refills, (unsigned long long)ro.refills);
+        if (ro.numeric) atomicAdd(&ctr->numeric_fail, 1ull);
+    }
+}
+
+cudaError_t launch_march_huge_rays(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                   const OutDev &od, const RaysDev &rays, DevCounters *ctr, const int *huge_list,
+                                   int huge_cap, float *se, float *sx, int *sc, cudaStream_t st) {
+    k_march_huge_rays<<<kHugeThreads / 32, 32, 0, st>>>(mp, xf16, n_prim, payload, od, rays, ctr, huge_list, huge_cap,
+                                                        se, sx, sc);
     return cudaGetLastError();
 }
 

@@ -22,7 +22,9 @@ struct DevCounters {
     // primitives' pixel rectangles instead of its (unwritten) bucket
     unsigned key_cap;
     unsigned bwd_long;  // K6: rays whose segment list the forward did not keep (k_backward_rays_list)
-    unsigned huge_rays;  // camera pixels for k_march_huge_views (more than kFallbackCap live segments)
+    unsigned huge_rays;  // pixels / rays for the last-resort passes (more than kFallbackCap live segments)
+    unsigned bwd_huge;   // K6: rays whose forward took the last-resort pass (k_backward_rays_huge)
+    unsigned pad_;
 };
 
 // A tile whose bucket [offsets[t], offsets[t+1]) does not fit the entries buffer. K2 saturates
@@ -197,7 +199,12 @@ cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const March
                                   const uint32_t *offsets, const unsigned long long *entries,
                                   const OutDev &od, const RaysDev &rays, DevCounters *ctr,
                                   const int *ovf_list, int ovf_cap, float *se, float *sx,
-                                  int *sc, cudaStream_t st);
+                                  int *sc, cudaStream_t st, int *huge_list = nullptr, int huge_cap = 0);
+// Arbitrary rays the fallback could not hold (ctr->huge_rays of huge_list): kHugeCap windows
+// through the BVH; a ray's forward state records it (state[7] = -2) for the backward.
+cudaError_t launch_march_huge_rays(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
+                                   const OutDev &od, const RaysDev &rays, DevCounters *ctr, const int *huge_list,
+                                   int huge_cap, float *se, float *sx, int *sc, cudaStream_t st);
 cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               const float4 *payload, const RaysDev &rays, int64_t n_rays,
                               const OutDev &od, DevCounters *ctr, int *ovf_list, int ovf_cap,
@@ -207,7 +214,8 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
-                                 float *sx, int *sc, cudaStream_t st);
+                                 float *sx, int *sc, cudaStream_t st, int *huge_list = nullptr, int huge_cap = 0,
+                                 float *he = nullptr, float *hx = nullptr, int *hc = nullptr);
 // vpb_backward.cu: interleaved payload gradient -> planar GradBuffer (touched primitives)
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
                                   bool accumulate, cudaStream_t st);

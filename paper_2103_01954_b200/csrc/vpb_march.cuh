@@ -606,7 +606,7 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
         __syncwarp();
     }
     return 0;
-#endif
+#else
     while (sp > 0) {
         const int take = sp < 32 ? sp : 32, b = sp - take;
         const bool act = lane < take;
@@ -641,6 +641,7 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
         __syncwarp();
     }
     return 0;
+#endif
 }
 
 // The complete sorted segment list of one ray, built by a warp: the warp walks the BVH

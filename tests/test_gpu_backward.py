@@ -94,3 +94,40 @@ def test_long_rays_take_the_overflow_paths(renderer, oracle):
     n_pay = k * 4 * m ** 3
     _check_close("long.payload", got[:n_pay], want[:n_pay])
     _check_close("long.pose", got[n_pay:], want[n_pay:])
+
+
+@pytest.mark.parametrize("n_boxes", [300, 600])
+def test_rays_with_more_live_segments_than_the_fallback_window(renderer, oracle, n_boxes):
+    """More than kFallbackCap (256) primitives live at one sample of a ray batch: boxes stacked
+    on the same region. The reference has no limit; those rays take the last-resort passes
+    (k_march_huge_rays forward, k_backward_rays_huge backward; 4096-entry windows). Forward bit-
+    exact, gradients within the reordering bound."""
+    rng = np.random.default_rng(n_boxes)
+    tr = api.transform_records(rng.uniform(-0.02, 0.02, (n_boxes, 3)), np.tile(np.eye(3), (n_boxes, 1, 1)),
+                               rng.uniform(0.2, 0.3, (n_boxes, 3)), delta_r=rng.uniform(-0.3, 0.3, (n_boxes, 3)))
+    m = 2
+    pay = rng.uniform(0, 1, n_boxes * 4 * m ** 3).astype(np.float32)
+    pay.reshape(n_boxes, 4, -1)[:, 3] *= np.float32(0.02)  # thin: rays cross the whole stack
+    win, cfg = api.WindowParams(), api.MarchConfig(step_size=0.005)
+    xf = api.compose(tr)
+    renderer.set_scene_composed(xf, api.PrimitiveSlab(n_boxes, m, pay), win)
+    n = 40
+    o = np.zeros((n, 3), np.float32)
+    o[:, :2] = rng.uniform(-0.1, 0.1, size=(n, 2))
+    o[:, 2] = -2.0
+    d = np.stack([rng.uniform(-0.2, 0.2, n), rng.uniform(-0.2, 0.2, n), np.ones(n)], 1).astype(np.float32)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rgb, alpha, samples = renderer.march_rays(o, d, cfg)
+    st = renderer.read_stats()
+    assert st["huge_rays"] > 0, st
+    rgb_o, alpha_o, samples_o = oracle.march_rays(xf, m, pay, win, o, d, cfg)
+    assert np.array_equal(samples, samples_o)
+    assert np.array_equal(rgb.view(np.uint32), rgb_o.view(np.uint32))
+    assert np.array_equal(alpha.view(np.uint32), alpha_o.view(np.uint32))
+    ar = rng.normal(size=(n, 3)).astype(np.float32)
+    aa = rng.normal(size=n).astype(np.float32)
+    got = renderer.backward_rays(o, d, ar, aa, cfg, tr)
+    want = oracle.backward_rays(tr, m, pay, win, o, d, ar, aa, cfg)
+    n_pay = n_boxes * 4 * m ** 3
+    _check_close("huge.payload", got[:n_pay], want[:n_pay])
+    _check_close("huge.pose", got[n_pay:], want[n_pay:])
