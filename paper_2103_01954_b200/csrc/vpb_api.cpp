@@ -154,6 +154,16 @@ struct vp_ctx {
     DBuf<float> g_pay4;
     DBuf<unsigned> g_touched;
     DBuf<int> bwd_list;  // K6: rays whose segment lists the forward did not keep
+    // K6a-c pair workspace (BwdPairs); pair_cap grows to the planned count after a call that
+    // overflowed it (the overflowing rays take the warp walk, so results never depend on it)
+    DBuf<int4> bp_rec;
+    DBuf<int2> bp_ent;
+    DBuf<float> bp_terms;
+    DBuf<int4> bp_span;
+    DBuf<int> bp_fb;
+    size_t pair_cap = 0;
+    bool pair_cap_fixed = false;
+    bool bwd_warp_walk = false;  // VPB_BWD_MODE=warp: the warp-per-ray walk for every ray (A/B)
     // host slab uploads (upload_planar_host): page-locked + device staging chunks, their
     // transfer events, and the host copy threads
     static constexpr int kStageSlots = 4;
@@ -167,7 +177,10 @@ struct vp_ctx {
     cudaEvent_t ev_out[3] = {};
     // off by default: the kernel runs 14 % faster with vector reductions, but the transpose
     // into the planar GradBuffer costs more than that (K6); VPB_BWD_LAYOUT=v4 enables it
-    bool bwd_v4 = false;
+    // payload gradient layout of the backward: 0 planar, 1 interleaved + vector reductions
+    // (transposed at the C-ABI), -1 auto (interleaved for batches of kV4MinRays rays or more,
+    // where the 4x fewer reductions outweigh the transpose)
+    int bwd_v4 = -1;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
     // vp_render_async into host memory: two device output slots; the device->host copy of
@@ -557,7 +570,13 @@ int vp_create(int32_t device, vp_ctx **out) {
     vp_ctx *ctx = new vp_ctx();
     ctx->device = device;
     if (const char *bl = std::getenv("VPB_BWD_LAYOUT"))  // A/B: "v4" = interleaved + vector reductions
-        ctx->bwd_v4 = std::strcmp(bl, "v4") == 0;
+        ctx->bwd_v4 = std::strcmp(bl, "v4") == 0 ? 1 : std::strcmp(bl, "planar") == 0 ? 0 : -1;
+    if (const char *bm = std::getenv("VPB_BWD_MODE"))  // A/B: "warp" = the warp-per-ray walk for every ray
+        ctx->bwd_warp_walk = std::strcmp(bm, "warp") == 0;
+    if (const char *pc = std::getenv("VPB_BWD_PAIR_CAP")) {  // tests: a fixed (small) pair capacity
+        ctx->pair_cap = size_t(std::strtoull(pc, nullptr, 10));
+        ctx->pair_cap_fixed = true;
+    }
     if (const char *tc = std::getenv("VPB_TILE_CFG"))  // tuning override: light | normal | dense
         ctx->tile_cfg = std::strcmp(tc, "light") == 0    ? int(TileTier::Light)
                         : std::strcmp(tc, "normal") == 0 ? int(TileTier::Normal)
@@ -680,6 +699,11 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->g_pay4.release();
     ctx->g_touched.release();
     ctx->bwd_list.release();
+    ctx->bp_rec.release();
+    ctx->bp_ent.release();
+    ctx->bp_terms.release();
+    ctx->bp_span.release();
+    ctx->bp_fb.release();
     for (int i = 0; i < vp_ctx::kStageSlots; ++i) {
         if (ctx->stage_h[i]) cudaFreeHost(ctx->stage_h[i]);
         ctx->stage_d[i].release();
@@ -1420,7 +1444,9 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     }
     // v4: the payload gradient is scattered channel-interleaved (one 16-byte reduction per
     // corner) into ctx->g_pay4, kept zeroed between calls, then transposed into dg
-    const bool v4 = ctx->bwd_v4 && k > 0 && n_rays > 0;
+    constexpr int64_t kV4MinRays = 16384;
+    const bool v4 = k > 0 && n_rays > 0 &&
+                    (ctx->bwd_v4 == 1 || (ctx->bwd_v4 < 0 && !ctx->bwd_warp_walk && n_rays >= kV4MinRays));
     if (v4) {
         if (ctx->g_pay4.n < n_pay) {
             VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
@@ -1503,10 +1529,23 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             bd.touched = ctx->g_touched.p;
         }
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
+        BwdPairs bp{};
+        const bool pairs = !ctx->bwd_warp_walk;
+        if (pairs) {
+            if (!ctx->pair_cap_fixed) ctx->pair_cap = std::max(ctx->pair_cap, std::max<size_t>(size_t(1) << 20, 64 * n));
+            const size_t cap = std::max<size_t>(ctx->pair_cap, 1);
+            VP_CUDA(ctx, ctx->bp_rec.ensure(cap));
+            VP_CUDA(ctx, ctx->bp_terms.ensure(3 * cap));
+            VP_CUDA(ctx, ctx->bp_span.ensure(n));
+            VP_CUDA(ctx, ctx->bp_ent.ensure(n * kRaySegs));
+            VP_CUDA(ctx, ctx->bp_fb.ensure(n));
+            bp = BwdPairs{ctx->bp_rec.p, ctx->bp_terms.p, ctx->bp_span.p, ctx->bp_ent.p, ctx->bp_fb.p,
+                          unsigned(std::min<size_t>(cap, 0xffffffffu))};
+        }
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->bwd_list.p, int(n), ctx->fb_e.p, ctx->fb_x.p,
                                           ctx->fb_c.p, st, ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p,
-                                          ctx->hg_x.p, ctx->hg_c.p));
+                                          ctx->hg_x.p, ctx->hg_c.p, pairs ? &bp : nullptr));
         if (v4)
             VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(ctx->g_pay4.p), dg, ctx->g_touched.p, k,
                                                unsigned(size_t(m) * m * m), accumulate != 0, st));
@@ -1514,7 +1553,12 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     }
     if (!d_grads) VP_CUDA(ctx, cudaMemcpyAsync(grads, dg, n_grad * 4, cudaMemcpyDeviceToHost, st));
     VP_CUDA(ctx, cudaStreamSynchronize(st));
-    if (k > 0 && n_rays > 0) return check_counters(ctx, *ctx->h_ctr);
+    if (k > 0 && n_rays > 0) {
+        // the next call gets room for this call's samples (this one was exact either way)
+        if (!ctx->pair_cap_fixed && ctx->h_ctr->bwd_pairs > ctx->pair_cap)
+            ctx->pair_cap = size_t(ctx->h_ctr->bwd_pairs) + size_t(ctx->h_ctr->bwd_pairs) / 4;
+        return check_counters(ctx, *ctx->h_ctr);
+    }
     return VP_OK;
 }
 }  // namespace

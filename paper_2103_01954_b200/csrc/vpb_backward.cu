@@ -161,6 +161,8 @@ __device__ __forceinline__ void eval_primitive(const float4 *__restrict__ pbase,
 __device__ __forceinline__ V3 window_gradient(V3 p, float alpha, int beta, float wv) {
     if (alpha == 0.0f) return mk3(0.f, 0.f, 0.f);
     const float c = -alpha * (float)beta * wv;
+    if (beta == 8)  // pow_even(x, 6) multiplies out to b^2 * b^4 (same products, same bits)
+        return mk3(c * (pow6(p.x) * p.x), c * (pow6(p.y) * p.y), c * (pow6(p.z) * p.z));
     return mk3(c * (pow_even(p.x, beta - 2) * p.x), c * (pow_even(p.y, beta - 2) * p.y),
                c * (pow_even(p.z, beta - 2) * p.z));
 }
@@ -228,6 +230,79 @@ __device__ __forceinline__ void scatter_payload(const BwdDev &bd, int k, size_t 
     red_add(gk + m3 + v, g);
     red_add(gk + 2 * m3 + v, b);
     red_add(gk + 3 * m3 + v, s);
+}
+
+// One primitive-sample's adjoint (grad.cpp:96-161): the colour/opacity adjoints, the payload
+// scatter over the 8 corners, the spatial gradient through the stencil and the fade window,
+// and the pose terms: rotG = R (gP ./ s) (deltaT gets -rotG, gPWorldStep +rotG), the rotation
+// term (deltaR) and the scale term (deltaS). Returns false when gP == 0 (no pose terms).
+template <class Cands>
+__device__ __forceinline__ bool sample_adjoint(const Cands &cands, const MarchDev &mp, const unsigned long long *tab,
+                                               const FwdReplay<Cands> &fwd, const BwdDev &bd, V3 aRgb, float aAlpha,
+                                               bool satStep, int k, int c, V3 pw, V3 &rotG, V3 &rTerm, V3 &sTerm) {
+    const int m = mp.m;
+    const float *xf = cands.xf(c);
+    PrimEval e;
+    eval_primitive(cands.base(c), m, xf, pw, mp.alpha, mp.beta, tab, e);
+    const float dt = mp.dt;
+    const float sigmaW = e.sigmaRaw * e.win;
+    V3 gRgb;
+    float gSigmaW;
+    if (satStep) {  // grad.cpp:104-108 (rgbWeighted of this step == satRgbWeighted)
+        const float budget = 1.0f - fwd.satTPrev;
+        const float inv = 1.0f / fwd.satSigmaSum;
+        gRgb = aRgb * (sigmaW * budget * inv);
+        const V3 diff = e.rgb * fwd.satSigmaSum - mk3(fwd.satR, fwd.satG, fwd.satB);
+        gSigmaW = dot3(aRgb, diff) * budget * inv * inv;
+    } else {  // grad.cpp:109-118
+        gRgb = aRgb * (sigmaW * dt);
+        gSigmaW = dot3(aRgb, e.rgb) * dt;
+        if (fwd.saturated)
+            gSigmaW -= dot3(aRgb, mk3(fwd.satR, fwd.satG, fwd.satB)) / fwd.satSigmaSum * dt;
+        else
+            gSigmaW += aAlpha * dt;
+    }
+    // payload scatter (grad.cpp:121-134): corner weights in the reference's product order
+    const size_t m3 = (size_t)m * m * m;
+    const float gsw = gSigmaW * e.win;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
+        const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
+        const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
+        const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
+        const float wgt = wx * wy * wz;
+        if (wgt == 0.0f) continue;
+        const int z = min(e.lo[2] + cz, m - 1), y = min(e.lo[1] + cy, m - 1), x = min(e.lo[0] + cx, m - 1);
+        scatter_payload(bd, k, m3, ((size_t)z * m + y) * m + x, gRgb.x * wgt, gRgb.y * wgt, gRgb.z * wgt,
+                        gsw * wgt);
+    }
+    V3 sgrad[4];
+    const float sh = 0.5f * (float)m;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch)
+        sgrad[ch] = m == 1 ? mk3(0.f, 0.f, 0.f)
+                           : mk3(e.clamped[0] ? 0.f : e.sgx[ch] * sh, e.clamped[1] ? 0.f : e.sgy[ch] * sh,
+                                 e.clamped[2] ? 0.f : e.sgz[ch] * sh);
+    // spatial gradient (grad.cpp:136-145)
+    const V3 gradW = window_gradient(e.pm, mp.alpha, mp.beta, e.win);
+    V3 gP = (sgrad[3] * e.win + gradW * e.sigmaRaw) * gSigmaW;
+    gP = gP + sgrad[0] * gRgb.x;
+    gP = gP + sgrad[1] * gRgb.y;
+    gP = gP + sgrad[2] * gRgb.z;
+    if (e.cube[0]) gP.x = 0.f;
+    if (e.cube[1]) gP.y = 0.f;
+    if (e.cube[2]) gP.z = 0.f;
+    if (gP.x == 0.f && gP.y == 0.f && gP.z == 0.f) return false;
+    // pose Jacobians (grad.cpp:147-161)
+    const V3 gOverS = mk3(gP.x / xf[12], gP.y / xf[13], gP.z / xf[14]);
+    rotG = matvec(xf + 3, gOverS);
+    sTerm = mk3(-gP.x * e.pm.x / xf[12], -gP.y * e.pm.y / xf[13], -gP.z * e.pm.z / xf[14]);
+    const V3 u = pw - mk3(xf[0], xf[1], xf[2]);
+    const float *pose = bd.pose36 + 36 * (size_t)k;  // rBase[9], dR/dv_i [3][9]
+    const V3 v = matvec(pose, gOverS);
+    rTerm = mk3(dot3(matvec(pose + 9, v), u), dot3(matvec(pose + 18, v), u), dot3(matvec(pose + 27, v), u));
+    return true;
 }
 
 #ifndef VPB_BWD_WARP_AGG
@@ -311,74 +386,15 @@ struct BwdWalk {
         satStep = fwd.saturated && i == fwd.lastStep;
     }
     __device__ void prim(int k, int c) {
-        const int m = mp.m;
-        const float *xf = cands.xf(c);
         if (bd.touched && k != last_touched) {  // primitives with gradient entries (the transpose's set)
             bd.touched[k] = 1u;
             last_touched = k;
         }
-        PrimEval e;
-        eval_primitive(cands.base(c), m, xf, pw, mp.alpha, mp.beta, tab, e);
-        const float dt = mp.dt;
-        const float sigmaW = e.sigmaRaw * e.win;
-        V3 gRgb;
-        float gSigmaW;
-        if (satStep) {  // grad.cpp:104-108 (rgbWeighted of this step == satRgbWeighted)
-            const float budget = 1.0f - fwd.satTPrev;
-            const float inv = 1.0f / fwd.satSigmaSum;
-            gRgb = aRgb * (sigmaW * budget * inv);
-            const V3 diff = e.rgb * fwd.satSigmaSum - mk3(fwd.satR, fwd.satG, fwd.satB);
-            gSigmaW = dot3(aRgb, diff) * budget * inv * inv;
-        } else {  // grad.cpp:109-118
-            gRgb = aRgb * (sigmaW * dt);
-            gSigmaW = dot3(aRgb, e.rgb) * dt;
-            if (fwd.saturated)
-                gSigmaW -= dot3(aRgb, mk3(fwd.satR, fwd.satG, fwd.satB)) / fwd.satSigmaSum * dt;
-            else
-                gSigmaW += aAlpha * dt;
-        }
-        // payload scatter (grad.cpp:121-134): corner weights in the reference's product order
-        const size_t m3 = (size_t)m * m * m;
-        const float gsw = gSigmaW * e.win;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
-            const float wx = cx ? e.fr[0] : 1.0f - e.fr[0];
-            const float wy = cy ? e.fr[1] : 1.0f - e.fr[1];
-            const float wz = cz ? e.fr[2] : 1.0f - e.fr[2];
-            const float wgt = wx * wy * wz;
-            if (wgt == 0.0f) continue;
-            const int z = min(e.lo[2] + cz, m - 1), y = min(e.lo[1] + cy, m - 1), x = min(e.lo[0] + cx, m - 1);
-            scatter_payload(bd, k, m3, ((size_t)z * m + y) * m + x, gRgb.x * wgt, gRgb.y * wgt, gRgb.z * wgt,
-                            gsw * wgt);
-        }
-        V3 sgrad[4];
-        const float sh = 0.5f * (float)m;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-            sgrad[ch] = m == 1 ? mk3(0.f, 0.f, 0.f)
-                               : mk3(e.clamped[0] ? 0.f : e.sgx[ch] * sh, e.clamped[1] ? 0.f : e.sgy[ch] * sh,
-                                     e.clamped[2] ? 0.f : e.sgz[ch] * sh);
-        // spatial gradient (grad.cpp:136-145)
-        const V3 gradW = window_gradient(e.pm, mp.alpha, mp.beta, e.win);
-        V3 gP = (sgrad[3] * e.win + gradW * e.sigmaRaw) * gSigmaW;
-        gP = gP + sgrad[0] * gRgb.x;
-        gP = gP + sgrad[1] * gRgb.y;
-        gP = gP + sgrad[2] * gRgb.z;
-        if (e.cube[0]) gP.x = 0.f;
-        if (e.cube[1]) gP.y = 0.f;
-        if (e.cube[2]) gP.z = 0.f;
-        if (gP.x == 0.f && gP.y == 0.f && gP.z == 0.f) return;
-        // pose Jacobians (grad.cpp:147-161)
-        const V3 gOverS = mk3(gP.x / xf[12], gP.y / xf[13], gP.z / xf[14]);
-        const V3 rotG = matvec(xf + 3, gOverS);
+        V3 rotG, rTerm, sTerm;
+        if (!sample_adjoint(cands, mp, tab, fwd, bd, aRgb, aAlpha, satStep, k, c, pw, rotG, rTerm, sTerm)) return;
         pose_add(k, 0, mk3(-rotG.x, -rotG.y, -rotG.z));
-        pose_add(k, 6, mk3(-gP.x * e.pm.x / xf[12], -gP.y * e.pm.y / xf[13], -gP.z * e.pm.z / xf[14]));
-        const V3 u = pw - mk3(xf[0], xf[1], xf[2]);
-        const float *pose = bd.pose36 + 36 * (size_t)k;  // rBase[9], dR/dv_i [3][9]
-        const V3 v = matvec(pose, gOverS);
-        pose_add(k, 3, mk3(dot3(matvec(pose + 9, v), u), dot3(matvec(pose + 18, v), u),
-                           dot3(matvec(pose + 27, v), u)));
+        pose_add(k, 6, sTerm);
+        pose_add(k, 3, rTerm);
         gPWorldStep = gPWorldStep + rotG;
     }
     __device__ bool step_end(long long) {
@@ -420,30 +436,27 @@ __device__ __forceinline__ bool intersect_face(const float *xf, V3 o, V3 d, int 
 }
 
 // The t_min anchor chain (grad.cpp:166-194): the first hit's entry depends on the pose of the
-// first primitive (k0) through its entry face.
-template <class Cands>
-__device__ void anchor_chain(BwdWalk<Cands> &bw, const Cands &cands, const BwdDev &bd, int k0, float tMin,
-                             float gTmin, V3 o, V3 d) {
-    if (gTmin == 0.f) return;
-    const float *xf = cands.xf(k0);
+// first primitive (k0) through its entry face. Returns false when it contributes nothing;
+// otherwise the deltaT, deltaR and deltaS terms of k0.
+__device__ __forceinline__ bool anchor_terms(const float *xf, const float *pose, float tMin, float gTmin, V3 o,
+                                             V3 d, V3 &gT3, V3 &gR3, V3 &gS3) {
+    if (gTmin == 0.f) return false;
     int axis, sign;
     bool clamped;
-    if (!intersect_face(xf, o, d, axis, sign, clamped) || clamped) return;
+    if (!intersect_face(xf, o, d, axis, sign, clamped) || clamped) return false;
     const int j = axis;
     const float c = (float)sign;
     const V3 q = mk3(xf[3 + 3 * j], xf[4 + 3 * j], xf[5 + 3 * j]);
     const float qd = dot3(q, d);
-    if (qd == 0.0f) return;
+    if (qd == 0.0f) return false;
     const float gT = gTmin;
-    bw.pose_add(k0, 0, q * (gT / qd));
-    V3 gS = mk3(0.f, 0.f, 0.f);
+    gT3 = q * (gT / qd);
+    gS3 = mk3(0.f, 0.f, 0.f);
     const float gsj = gT * c / qd;
-    if (j == 0) gS.x = gsj;
-    else if (j == 1) gS.y = gsj;
-    else gS.z = gsj;
-    bw.pose_add(k0, 6, gS);
+    if (j == 0) gS3.x = gsj;
+    else if (j == 1) gS3.y = gsj;
+    else gS3.z = gsj;
     const V3 toT = mk3(xf[0], xf[1], xf[2]) - o;
-    const float *pose = bd.pose36 + 36 * (size_t)k0;
     const V3 rj = mk3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2]);
     float gR[3];
 #pragma unroll
@@ -451,7 +464,18 @@ __device__ void anchor_chain(BwdWalk<Cands> &bw, const Cands &cands, const BwdDe
         const V3 qp = matvec(pose + 9 + 9 * ii, rj);
         gR[ii] = gT * (dot3(qp, toT) - tMin * dot3(qp, d)) / qd;
     }
-    bw.pose_add(k0, 3, mk3(gR[0], gR[1], gR[2]));
+    gR3 = mk3(gR[0], gR[1], gR[2]);
+    return true;
+}
+
+template <class Cands>
+__device__ void anchor_chain(BwdWalk<Cands> &bw, const Cands &cands, const BwdDev &bd, int k0, float tMin,
+                             float gTmin, V3 o, V3 d) {
+    V3 gT3, gR3, gS3;
+    if (!anchor_terms(cands.xf(k0), bd.pose36 + 36 * (size_t)k0, tMin, gTmin, o, d, gT3, gR3, gS3)) return;
+    bw.pose_add(k0, 0, gT3);
+    bw.pose_add(k0, 6, gS3);
+    bw.pose_add(k0, 3, gR3);
 }
 
 __device__ __forceinline__ void load_fwd_state(FwdReplay<BvhCands> &fwd, const float *s) {
@@ -557,12 +581,14 @@ k_backward_rays_huge(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
 // per-thread walk); gTmin, the only sequential sum, is accumulated over the chunk's steps in
 // step order. Rays with more than kWarpListBwd segments take the per-thread path.
 constexpr int kWarpListBwd = kRaySegs;
-constexpr int kWarpCandBwd = 256;
 // 3 CTAs/SM (162 registers, no spills). 4 CTAs (128 registers, 28 B of spills) and 5 (96,
 // 180 B) measured 2.05 and 2.14 ms for the 65,536-ray row against 2.03: more resident warps
 // do not help this walk (K6, tools/bwd_sweep.sh)
 #ifndef VPB_BWD_PAIRS
 #define VPB_BWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
+#endif
+#ifndef VPB_BWD_PAIRS_MINB
+#define VPB_BWD_PAIRS_MINB 2
 #endif
 #ifndef VPB_BWD_WARP_MINB
 #define VPB_BWD_WARP_MINB 3
@@ -570,7 +596,7 @@ constexpr int kWarpCandBwd = 256;
 __global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, int *__restrict__ ray_list,
-                     int list_cap, int *__restrict__ huge_list, int huge_cap) {
+                     int list_cap, int *__restrict__ huge_list, int huge_cap, const int *__restrict__ only) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];
@@ -580,7 +606,10 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
     const int nwarps = gridDim.x * 4, gw = blockIdx.x * 4 + wid;
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
     const float dt = mp.dt;
-    for (int64_t r = gw; r < n_rays; r += nwarps) {
+    // only: the rays K6a left to this walk (ctr->bwd_fb of them), else every ray
+    const int64_t n_iter = only ? (int64_t)min((unsigned long long)ctr->bwd_fb, (unsigned long long)n_rays) : n_rays;
+    for (int64_t q = gw; q < n_iter; q += nwarps) {
+        const int64_t r = only ? (int64_t)only[q] : q;
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
         const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
@@ -722,6 +751,313 @@ k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, co
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// K6a-c: the backward as passes over primitive-samples (the default path). The warp-per-ray
+// walk above keeps its lanes busy only 60 % of the time (19 threads per instruction): a ray
+// has ~50 samples spread over chunks of 32 lattice steps. Here one thread evaluates one
+// sample, so every lane works, and the per-ray bookkeeping is two light thread-per-ray passes.
+
+// Rays the forward could not keep a list for go to the per-thread kernels (as in the warp walk).
+__device__ __forceinline__ void route_long_ray(int nh, int64_t r, DevCounters *ctr, int *ray_list, int list_cap,
+                                               int *huge_list, int huge_cap) {
+    if (nh == -2 && huge_list) {  // the forward needed more than kFallbackCap live segments
+        const unsigned slot = atomicAdd(&ctr->bwd_huge, 1u);
+        if ((int)slot < huge_cap) huge_list[slot] = (int)r;
+        else atomicAdd(&ctr->fallback_fail, 1);
+    } else {
+        const unsigned slot = atomicAdd(&ctr->bwd_long, 1u);
+        if ((int)slot < list_cap) ray_list[slot] = (int)r;
+    }
+}
+
+// K6a, one warp per ray: the lattice walk of march.cpp:27-58 over the forward's segment list
+// (admission, gap skip; steps 0..lastStep), 32 steps per round as march_warp steps it, without
+// sampling. Entry j is admitted at step a_j and is live on the n_j consecutive steps from there
+// (while it is live the active set is not empty, so no gap skip intervenes), so the ray's
+// primitive-samples are (j, a_j + t), t < n_j. They get the range [base, base + sum n_j) of
+// the pair arrays, entry-major; each record carries what K6b needs without further lookups.
+__global__ void __launch_bounds__(128)
+k_bwd_plan(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, DevCounters *ctr,
+           int *__restrict__ ray_list, int list_cap, int *__restrict__ huge_list, int huge_cap) {
+    __shared__ float s_E[4][kRaySegs], s_X[4][kRaySegs];
+    __shared__ int s_a[4][kRaySegs], s_off[4][kRaySegs + 1];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *E = s_E[wid], *X = s_X[wid];
+    int *A = s_a[wid], *OFF = s_off[wid];
+    const float dt = mp.dt;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t r = (int64_t)blockIdx.x * 4 + wid; r < n_rays; r += nwarps) {
+        const float *state = bd.fwd_state + 8 * r;
+        const int nh = __float_as_int(state[7]);
+        const int lastStep = __float_as_int(state[0]);
+        if (nh < 0 || nh == 0 || lastStep < 0) {
+            if (lane == 0) {
+                if (nh < 0) route_long_ray(nh, r, ctr, ray_list, list_cap, huge_list, huge_cap);
+                pp.span[r] = make_int4(0, nh < 0 ? -1 : 0, 0, 0);
+            }
+            continue;
+        }
+        const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
+        for (int j = lane; j < nh; j += 32) {
+            E[j] = sg[j];
+            X[j] = sg[kRaySegs + j];
+            A[j] = -1;
+        }
+        __syncwarp();
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        const float t0 = E[0];
+        int base = 0, nadm_prev = 0;  // entries admitted before this round
+        for (;;) {
+            const int i = base + lane;
+            const bool valid = i <= lastStep;
+            const float ts = t0 + (__int2float_rn(i) + jit) * dt;
+            int na = 0, nadm = 0;
+            for (int j = 0; j < nh && valid; ++j) {
+                if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
+                nadm = j + 1;
+                na += X[j] > ts;
+            }
+            const unsigned empty = __ballot_sync(0xffffffffu, !(valid && na > 0));
+            const int L = empty ? __ffs(empty) - 1 : 32;
+            // the steps visited this round: s < L, and s == L when it is a real (empty) step
+            int before = __shfl_up_sync(0xffffffffu, nadm, 1);
+            if (lane == 0) before = nadm_prev;
+            if (valid && lane <= L)
+                for (int j = before; j < nadm; ++j) A[j] = base + lane;
+            if (L == 32) {
+                nadm_prev = __shfl_sync(0xffffffffu, nadm, 31);
+                base += 32;
+                if (base > lastStep) break;
+                continue;
+            }
+            const int iL = base + L;
+            if (iL > lastStep) break;
+            const int nadmL = __shfl_sync(0xffffffffu, nadm, L);
+            if (nadmL >= nh) break;  // nothing left to admit: march.cpp:43-44
+            nadm_prev = nadmL;
+            const double sk = ceil((double)((E[nadmL] - t0) / dt) - (double)jit);  // gap skip, march.cpp:45-49
+            const int skipTo = sk > (double)(1 << 30) ? (1 << 30) + 1 : (int)sk;
+            base = skipTo > iL + 1 ? skipTo : iL + 1;
+            if (base > lastStep) break;
+        }
+        __syncwarp();
+        // n_j (the live steps from a_j, up to lastStep), then offsets in entry order
+        int carry = 0;
+        for (int j0 = 0; j0 < nh; j0 += 32) {
+            const int j = j0 + lane;
+            int n = 0;
+            if (j < nh && A[j] >= 0) {
+                const float x = X[j];
+                int e = A[j];
+                while (e <= lastStep && t0 + (__int2float_rn(e) + jit) * dt < x) ++e;
+                n = e - A[j];
+            }
+            int incl = n;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            if (j < nh) OFF[j] = carry + incl - n;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        const int total = carry;
+        if (lane == 0) OFF[nh] = total;
+        __syncwarp();
+        unsigned long long pbase = 0;
+        if (lane == 0 && total > 0) pbase = atomicAdd(&ctr->bwd_pairs, (unsigned long long)total);
+        pbase = __shfl_sync(0xffffffffu, pbase, 0);
+        int4 sp = make_int4(0, total, nh, 0);
+        if (total > 0 && pbase + (unsigned long long)total > pp.cap) {  // no room: the warp walk takes the ray
+            sp.y = -1;
+            if (lane == 0) pp.fb_list[atomicAdd(&ctr->bwd_fb, 1u)] = (int)r;
+            // the one range that straddles the capacity: K6b skips its records
+            for (unsigned long long t = pbase + lane; t < pp.cap; t += 32) pp.rec[t] = make_int4(-1, 0, 0, 0);
+        } else if (total > 0) {
+            sp.x = (int)pbase;
+            const bool sat = __float_as_int(state[1]) != 0;
+            for (int p = lane; p < total; p += 32) {
+                int lo = 0, hi = nh - 1;  // the last entry with OFF[j] <= p
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (OFF[mid] <= p) lo = mid;
+                    else hi = mid - 1;
+                }
+                const int step = A[lo] + (p - OFF[lo]);
+                const float ts = t0 + (__int2float_rn(step) + jit) * dt;
+                const int c = __float_as_int(sg[2 * kRaySegs + lo]);
+                pp.rec[pbase + p] = make_int4((int)r, c, __float_as_int(ts), (sat && step == lastStep) ? 1 : 0);
+            }
+            int2 *ent = pp.ent + (size_t)r * kRaySegs;
+            for (int j = lane; j < nh; j += 32) ent[j] = make_int2(A[j], OFF[j]);
+        }
+        if (lane == 0) pp.span[r] = sp;
+        __syncwarp();
+    }
+}
+
+// K6b, one thread per primitive-sample: the sample's adjoint (sample_adjoint: payload scatter
+// as reductions). The pose terms go to the primitive's deltaT/deltaR/deltaS: the samples are
+// entry-major, so a warp's lanes form runs of one (ray, primitive); each run is summed with a
+// segmented shuffle scan and its last lane issues the nine reductions (SURVEY.md §8 a-20:
+// warp-aggregated atomics). rotG is kept for K6c's t_min chain (terms[3][cap]).
+__global__ void __launch_bounds__(256, VPB_BWD_PAIRS_MINB)
+k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
+            RaysDev rays, BwdDev bd, BwdPairs pp, const DevCounters *__restrict__ ctr) {
+    __shared__ unsigned long long s_tab[32];
+    load_exp_tab(s_tab);
+    __syncthreads();
+    const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
+    const unsigned long long n = min(ctr->bwd_pairs, (unsigned long long)pp.cap);
+    const size_t cap = pp.cap;
+    const int lane = threadIdx.x & 31;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    // warp-uniform loop: every lane takes part in the shuffles
+    for (size_t p0 = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); p0 < n; p0 += stride) {
+        const size_t p = p0 + lane;
+        int4 rec = make_int4(-1, -1, 0, 0);
+        if (p < n) rec = pp.rec[p];
+        float v[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = 0.f;
+        if (rec.x >= 0) {  // (rec.x < 0: the unwritten part of a ray that did not fit, k_bwd_plan)
+            const int64_t r = rec.x;
+            const int c = rec.y;
+            const float ts = __int_as_float(rec.z);
+            const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+            const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+            FwdReplay<BvhCands> fwd(cands, mp, s_tab);
+            load_fwd_state(fwd, bd.fwd_state + 8 * r);
+            const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
+            if (bd.touched) bd.touched[c] = 1u;
+            V3 rotG, rTerm, sTerm;
+            if (sample_adjoint(cands, mp, s_tab, fwd, bd, aRgb, bd.adj_alpha[r], rec.w != 0, c, c, o + d * ts, rotG,
+                               rTerm, sTerm)) {
+                v[0] = -rotG.x;
+                v[1] = -rotG.y;
+                v[2] = -rotG.z;
+                v[3] = rTerm.x;
+                v[4] = rTerm.y;
+                v[5] = rTerm.z;
+                v[6] = sTerm.x;
+                v[7] = sTerm.y;
+                v[8] = sTerm.z;
+            }
+            float *t = pp.terms + p;
+            t[0] = -v[0];  // rotG (+0 without pose terms)
+            t[cap] = -v[1];
+            t[2 * cap] = -v[2];
+        }
+        // runs of equal (ray, primitive) over the lanes: segmented inclusive scan
+        const int prev_x = __shfl_up_sync(0xffffffffu, rec.x, 1), prev_y = __shfl_up_sync(0xffffffffu, rec.y, 1);
+        const bool head = lane == 0 || prev_x != rec.x || prev_y != rec.y;
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        const int seg = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // this lane's run starts here
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float u = __shfl_up_sync(0xffffffffu, v[q], off);
+                if (lane - off >= seg) v[q] += u;
+            }
+        }
+        const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+        if (tail && rec.x >= 0) {
+            float *g = bd.g_pose + 9 * (size_t)rec.y;
+#pragma unroll
+            for (int q = 0; q < 9; ++q)
+                if (v[q] != 0.f) red_add(g + q, v[q]);
+        }
+    }
+}
+
+// K6c, one warp per ray: gTmin = the sum over the visited steps, in step order, of
+// dot(gPWorldStep, d), gPWorldStep = the step's rotG summed in list order from 0 (grad.cpp:66-
+// 164). The ray's rotG (entry-major) is staged in shared memory; lanes take 32 consecutive
+// steps, each forms its step's sum in list order, and the lanes' dot products are added in
+// step order (a step without samples, or a sample without pose terms, adds +0, which leaves a
+// sum that started at +0 unchanged). Then the t_min anchor chain onto the first entry.
+constexpr int kFoldStage = 512;   // samples per ray staged in shared memory (more: read from global)
+__global__ void __launch_bounds__(128)
+k_bwd_fold(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp) {
+    __shared__ int s_a[4][kRaySegs], s_off[4][kRaySegs + 1];
+    __shared__ float s_rot[4][3][kFoldStage];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int *A = s_a[wid], *OFF = s_off[wid];
+    const size_t cap = pp.cap;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t r = (int64_t)blockIdx.x * 4 + wid; r < n_rays; r += nwarps) {
+        const int4 sp = pp.span[r];
+        if (sp.y <= 0) continue;
+        const int total = sp.y, nh = sp.z;
+        const int2 *ent = pp.ent + (size_t)r * kRaySegs;
+        for (int j = lane; j < nh; j += 32) {
+            const int2 e = ent[j];
+            A[j] = e.x;
+            OFF[j] = e.y;
+        }
+        if (lane == 0) OFF[nh] = total;
+        const float *T = pp.terms + (size_t)sp.x;
+        const bool staged = total <= kFoldStage;
+        if (staged)
+            for (int t = lane; t < total; t += 32) {
+                s_rot[wid][0][t] = T[t];
+                s_rot[wid][1][t] = T[cap + t];
+                s_rot[wid][2][t] = T[2 * cap + t];
+            }
+        __syncwarp();
+        const float *R0 = staged ? s_rot[wid][0] : T, *R1 = staged ? s_rot[wid][1] : T + cap,
+                    *R2 = staged ? s_rot[wid][2] : T + 2 * cap;
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        float gTmin = 0.f;
+        int jlo = 0, sb = 0;  // entry 0 is admitted at step 0 (ts(0) >= tEnter of the first entry)
+        for (;;) {
+            const int s = sb + lane;
+            V3 g = mk3(0.f, 0.f, 0.f);
+            bool any = false;
+            for (int j = jlo; j < nh; ++j) {
+                const int a = A[j];
+                if (a > sb + 31) break;  // admission steps grow with j (unadmitted entries are -1)
+                const int o = OFF[j], n = OFF[j + 1] - o;
+                if (a >= 0 && s >= a && s < a + n) {
+                    const int idx = o + (s - a);
+                    g = g + mk3(R0[idx], R1[idx], R2[idx]);
+                    any = true;
+                }
+            }
+            const float contrib = any ? dot3(g, d) : 0.f;
+            const unsigned used = __ballot_sync(0xffffffffu, any);
+            for (unsigned m = used; m; m &= m - 1) gTmin += __shfl_sync(used, contrib, __ffs(m) - 1);
+            // the next step with a live entry, at or after sb + 32
+            const int nb = sb + 32;
+            while (jlo < nh && (A[jlo] < 0 || A[jlo] + (OFF[jlo + 1] - OFF[jlo]) <= nb)) ++jlo;
+            int next = 0x7fffffff;
+            for (int j = jlo + lane; j < nh; j += 32) {
+                const int a = A[j], n = OFF[j + 1] - OFF[j];
+                if (a >= 0 && n > 0 && a + n > nb) next = min(next, max(a, nb));
+            }
+            next = __reduce_min_sync(0xffffffffu, next);
+            if (next == 0x7fffffff) break;
+            sb = next;
+        }
+        if (lane == 0) {  // the t_min anchor chain onto the first hit's primitive
+            const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
+            const int k0 = __float_as_int(sg[2 * kRaySegs]);
+            const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+            V3 gT3, gR3, gS3;
+            if (anchor_terms(xf_g + (size_t)k0 * kXfStride, bd.pose36 + 36 * (size_t)k0, sg[0], gTmin, o, d, gT3, gR3,
+                             gS3)) {
+                float *g = bd.g_pose + 9 * (size_t)k0;
+                const float an[9] = {gT3.x, gT3.y, gT3.z, gR3.x, gR3.y, gR3.z, gS3.x, gS3.y, gS3.z};
+#pragma unroll
+                for (int q = 0; q < 9; ++q)
+                    if (an[q] != 0.f) red_add(g + q, an[q]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // The channel-interleaved payload gradient (VPB_BWD_V4 layout) into the caller's planar
 // GradBuffer (params.h:12-27): primitives the walk touched are transposed (assigned, or added
 // when accumulating) and their interleaved slots cleared for the next call; untouched ones get
@@ -768,9 +1104,72 @@ __global__ void __launch_bounds__(256) k_grad_transpose(float4 *__restrict__ g4,
     }
 }
 
+// The same for m3 % 4 == 0, flattened over (primitive, 4 consecutive voxels) in tiles of 256
+// quads per CTA, touched primitives only (the caller has zeroed the planar buffer unless it
+// accumulates): the tile's interleaved voxels are loaded with coalesced 16-byte accesses and
+// staged in shared memory; after the barrier the slots are cleared (a store to an address
+// whose load is still in flight stalls the warp: 6x slower when the clear followed each load)
+// and each thread writes its quad as one 16-byte vector per channel plane.
+__global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4, float4 *__restrict__ planar,
+                                                         const unsigned *__restrict__ touched, unsigned nq,
+                                                         unsigned q3, int accumulate) {
+    __shared__ float4 sm[4 * 256 + 4 * 8];  // padded: a float4 every 8 keeps the quad reads conflict-light
+    const int t = threadIdx.x;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (unsigned i0 = blockIdx.x * 256u; i0 < nq; i0 += gridDim.x * 256u) {
+        const unsigned k_first = i0 / q3, k_last = min(i0 + 255u, nq - 1) / q3;
+        bool any = false;  // block-uniform: is a primitive of this tile touched?
+        for (unsigned k = k_first; k <= k_last && !any; ++k) any = touched[k] != 0u;
+        if (!any) continue;
+        bool tch[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned l = t + 256 * u, iq = i0 + (l >> 2);  // voxel 4 * i0 + l is in quad iq
+            tch[u] = iq < nq && touched[iq / q3];
+            sm[l + (l >> 5)] = tch[u] ? g4[4 * (size_t)i0 + l] : z;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (tch[u]) g4[4 * (size_t)i0 + t + 256 * u] = z;
+        const unsigned i = i0 + t;
+        if (i < nq) {
+            const unsigned k = i / q3, qv = i - k * q3;
+            float4 *dst = planar + (size_t)k * 4 * q3 + qv;  // plane c at dst[c * q3]
+            if (touched[k]) {
+                const int l = 4 * t;
+                const float4 a = sm[l + (l >> 5)], b = sm[l + 1 + ((l + 1) >> 5)], c = sm[l + 2 + ((l + 2) >> 5)],
+                             d = sm[l + 3 + ((l + 3) >> 5)];
+                float4 p0 = make_float4(a.x, b.x, c.x, d.x), p1 = make_float4(a.y, b.y, c.y, d.y);
+                float4 p2 = make_float4(a.z, b.z, c.z, d.z), p3 = make_float4(a.w, b.w, c.w, d.w);
+                if (accumulate) {
+                    const float4 o0 = dst[0], o1 = dst[q3], o2 = dst[2 * q3], o3 = dst[3 * q3];
+                    p0 = make_float4(o0.x + p0.x, o0.y + p0.y, o0.z + p0.z, o0.w + p0.w);
+                    p1 = make_float4(o1.x + p1.x, o1.y + p1.y, o1.z + p1.z, o1.w + p1.w);
+                    p2 = make_float4(o2.x + p2.x, o2.y + p2.y, o2.z + p2.z, o2.w + p2.w);
+                    p3 = make_float4(o3.x + p3.x, o3.y + p3.y, o3.z + p3.z, o3.w + p3.w);
+                }
+                dst[0] = p0;
+                dst[q3] = p1;
+                dst[2 * q3] = p2;
+                dst[3 * q3] = p3;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
                                   bool accumulate, cudaStream_t st) {
     if (n_prim == 0 || m3 == 0) return cudaSuccess;
+    const size_t nq = size_t(n_prim) * (m3 / 4);
+    if (m3 % 4 == 0 && (reinterpret_cast<uintptr_t>(planar) & 15) == 0 && nq < (size_t(1) << 32) - 256) {
+        if (!accumulate)
+            if (cudaError_t e = cudaMemsetAsync(planar, 0, nq * 64, st)) return e;
+        k_grad_transpose4<<<148 * 16, 256, 0, st>>>(g4, reinterpret_cast<float4 *>(planar), touched, unsigned(nq),
+                                                   m3 / 4, accumulate ? 1 : 0);
+        return cudaGetLastError();
+    }
     const int blocks = n_prim < 148 * 8 ? n_prim : 148 * 8;
     k_grad_transpose<<<blocks, 256, 0, st>>>(g4, planar, touched, n_prim, m3, accumulate ? 1 : 0);
     return cudaGetLastError();
@@ -780,15 +1179,26 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
                                  float *sx, int *sc, cudaStream_t st, int *huge_list, int huge_cap, float *he,
-                                 float *hx, int *hc) {
+                                 float *hx, int *hc, const BwdPairs *pairs) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
     // The adjoint walk goes warp-per-ray for every batch size (the forward's state and segment
     // lists are required): one ray per thread leaves 27 % of the lanes busy (the rays' walks
     // diverge); then the rays with lists too long for the forward to keep, one per thread.
     if (!bd.fwd_state || !bd.fwd_segs) return cudaErrorInvalidValue;
     const int64_t blocks = (n_rays + 3) / 4;
-    k_backward_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
-        mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap);
+    if (pairs) {
+        const unsigned ray_blocks = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);  // a warp per ray
+        k_bwd_plan<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr, ray_list, list_cap, huge_list,
+                                               huge_cap);
+        k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
+        k_bwd_fold<<<ray_blocks, 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
+        // the rays that found no room in the pair arrays (none once the capacity has grown)
+        k_backward_rays_warp<<<(unsigned)(blocks < 148 * 4 ? blocks : 148 * 4), 128, 0, st>>>(
+            mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, pairs->fb_list);
+    } else {
+        k_backward_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
+            mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, nullptr);
+    }
     if (cudaError_t e = cudaGetLastError()) return e;
     k_backward_rays_list<<<kBackwardWarps, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, ray_list,
                                                          list_cap, se, sx, sc);

@@ -206,6 +206,11 @@ __device__ __forceinline__ float pow8(float x) { // pow_even(x, 8): r = 1 * b^8 
     const float b4 = b2 * b2;
     return b4 * b4;
 }
+__device__ __forceinline__ float pow6(float x) { // pow_even(x, 6): r = (1 * b^2) * b^4
+    const float b = fabsf(x);
+    const float b2 = b * b;
+    return b2 * (b2 * b2);
+}
 
 // primitive.cpp:25-28
 __device__ __forceinline__ float window_value(V3 p, float alpha, int beta,

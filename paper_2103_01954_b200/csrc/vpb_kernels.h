@@ -14,6 +14,7 @@ namespace vpb {
 struct DevCounters {
     unsigned long long ray_samples, prim_samples, hit_rays, early_exits, saturated;
     unsigned long long overflow_rays, refills, keys, numeric_fail, nonempty_tiles;
+    unsigned long long bwd_pairs;  // K6a: primitive-samples planned (the pair cursor; may pass the capacity)
     int key_overflow;
     int fallback_fail;
     unsigned big_buckets;  // K3b: tile buckets past 256 keys (sorted by k_tile_sort_big)
@@ -24,7 +25,7 @@ struct DevCounters {
     unsigned bwd_long;  // K6: rays whose segment list the forward did not keep (k_backward_rays_list)
     unsigned huge_rays;  // pixels / rays for the last-resort passes (more than kFallbackCap live segments)
     unsigned bwd_huge;   // K6: rays whose forward took the last-resort pass (k_backward_rays_huge)
-    unsigned pad_;
+    unsigned bwd_fb;     // K6a: rays left to the warp-per-ray walk (pair capacity exhausted)
 };
 
 // A tile whose bucket [offsets[t], offsets[t+1]) does not fit the entries buffer. K2 saturates
@@ -135,6 +136,19 @@ struct BwdDev {
     unsigned *touched = nullptr;  // with g_pay4: per primitive, set when the walk scatters into it
 };
 
+// K6 pair workspace (vpb_backward.cu): the backward as three passes over primitive-samples.
+// K6a plans each ray's samples (ray, step, entry) entry-major into [base, base + total);
+// K6b evaluates one sample per thread (payload scatter, pose terms); K6c folds each ray's
+// pose terms per entry and the t_min chain in step order.
+struct BwdPairs {
+    int4 *rec;             // [cap] ray, primitive, ts (bits), saturating step (0/1)
+    float *terms;          // [3][cap] rotG per sample (K6c's t_min chain)
+    int4 *span;            // [n_rays] base, total (-1: not planned), admitted entries, -
+    int2 *ent;             // [n_rays][kRaySegs] admission step, offset in the ray's range
+    int *fb_list;          // [n_rays] rays for the warp-per-ray walk
+    unsigned cap;
+};
+
 // Adam step constants (losses.cpp:70-104); bc1/bc2 = 1 - beta^step computed on the host.
 struct AdamDev {
     float lr, beta1, beta2, eps, lr_delta_scale, bc1, bc2;
@@ -211,11 +225,13 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               cudaStream_t st);
 // K6: needs bd.fwd_state and bd.fwd_segs (the forward of the same rays, k_march_rays_warp);
 // ray_list (list_cap entries) collects the rays whose lists the forward could not keep.
+// pairs: the K6a-c workspace; null runs the warp-per-ray walk over every ray.
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
                                  float *sx, int *sc, cudaStream_t st, int *huge_list = nullptr, int huge_cap = 0,
-                                 float *he = nullptr, float *hx = nullptr, int *hc = nullptr);
+                                 float *he = nullptr, float *hx = nullptr, int *hc = nullptr,
+                                 const BwdPairs *pairs = nullptr);
 // vpb_backward.cu: interleaved payload gradient -> planar GradBuffer (touched primitives)
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
                                   bool accumulate, cudaStream_t st);

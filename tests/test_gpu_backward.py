@@ -131,3 +131,28 @@ def test_rays_with_more_live_segments_than_the_fallback_window(renderer, oracle,
     n_pay = n_boxes * 4 * m ** 3
     _check_close("huge.payload", got[:n_pay], want[:n_pay])
     _check_close("huge.pose", got[n_pay:], want[n_pay:])
+
+
+@pytest.mark.parametrize("mode", ["warp", "cap64"])
+def test_backward_paths_agree(monkeypatch, mode):
+    """The default backward runs as passes over primitive-samples (K6a plan, K6b one sample per
+    thread, K6c per-ray fold). The warp-per-ray walk is the same adjoint, used for rays that
+    find no room in the pair arrays: forced for every ray (VPB_BWD_MODE=warp) or for most of
+    them (a 64-sample capacity). Both equal the reference within the reordering bound."""
+    from paper_2103_01954_b200 import Renderer
+    if mode == "warp":
+        monkeypatch.setenv("VPB_BWD_MODE", "warp")
+    else:
+        monkeypatch.setenv("VPB_BWD_PAIR_CAP", "64")
+    r = Renderer(0)
+    try:
+        for case, g in sorted(load_groups("backward").items()):
+            win, cfg = _inputs(g)
+            k, m = g["tr"].shape[0], int(g["m"])
+            r.set_scene_composed(api.compose(g["tr"]), api.PrimitiveSlab(k, m, g["payload"]), win)
+            got = r.backward_rays(g["o"], g["d"], g["adj_rgb"], g["adj_alpha"], cfg, g["tr"], g["jit"])
+            n_pay = k * 4 * m ** 3
+            _check_close(f"{mode}.{case}.payload", got[:n_pay], g["grads"][:n_pay])
+            _check_close(f"{mode}.{case}.pose", got[n_pay:], g["grads"][n_pay:])
+    finally:
+        r.close()
