@@ -175,8 +175,6 @@ struct vp_ctx {
     void *out_stage = nullptr;  // copy_out_host: page-locked staging of pageable outputs
     size_t out_stage_bytes = 0;
     cudaEvent_t ev_out[3] = {};
-    // off by default: the kernel runs 14 % faster with vector reductions, but the transpose
-    // into the planar GradBuffer costs more than that (K6); VPB_BWD_LAYOUT=v4 enables it
     // payload gradient layout of the backward: 0 planar, 1 interleaved + vector reductions
     // (transposed at the C-ABI), -1 auto (interleaved for batches of kV4MinRays rays or more,
     // where the 4x fewer reductions outweigh the transpose)

@@ -573,24 +573,34 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
         const bool act = f < take;
         const int node = act ? fr[b + f] : 0;
         __syncwarp();
-        bool hit = false;
+        // each lane picks its box first, then ONE slab test runs on all of them (four call
+        // sites, one per (leaf, c, g) case, ran at 5 threads per instruction)
+        bool test = false;
         int id = 0;
+        float lx = 0.f, ly = 0.f, lz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
         if (act) {
             const BvhNode n = bvh.nodes[node];
             const int child = c ? n.d.y : n.d.x;
             if (child < 0) {
-                if (g == 0) {
-                    hit = c ? ray_box(o, d, inv, n.b.z, n.b.w, n.c.x, n.c.y, n.c.z, n.c.w)
-                            : ray_box(o, d, inv, n.a.x, n.a.y, n.a.z, n.a.w, n.b.x, n.b.y);
-                    id = child;
+                test = g == 0;
+                id = child;
+                if (c) {
+                    lx = n.b.z, ly = n.b.w, lz = n.c.x, hx = n.c.y, hy = n.c.z, hz = n.c.w;
+                } else {
+                    lx = n.a.x, ly = n.a.y, lz = n.a.z, hx = n.a.w, hy = n.b.x, hz = n.b.y;
                 }
             } else {
                 const BvhNode cn = bvh.nodes[child];
-                hit = g ? ray_box(o, d, inv, cn.b.z, cn.b.w, cn.c.x, cn.c.y, cn.c.z, cn.c.w)
-                        : ray_box(o, d, inv, cn.a.x, cn.a.y, cn.a.z, cn.a.w, cn.b.x, cn.b.y);
+                test = true;
                 id = g ? cn.d.y : cn.d.x;
+                if (g) {
+                    lx = cn.b.z, ly = cn.b.w, lz = cn.c.x, hx = cn.c.y, hy = cn.c.z, hz = cn.c.w;
+                } else {
+                    lx = cn.a.x, ly = cn.a.y, lz = cn.a.z, hx = cn.a.w, hy = cn.b.x, hz = cn.b.y;
+                }
             }
         }
+        const bool hit = test && ray_box(o, d, inv, lx, ly, lz, hx, hy, hz);
         const unsigned pi = __ballot_sync(0xffffffffu, hit && id >= 0);
         const unsigned pl = __ballot_sync(0xffffffffu, hit && id < 0);
         const int np = __popc(pi);
@@ -673,8 +683,9 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
         cx[q] = tX;
     }
     __syncwarp();
-    int nh = 0;
-    for (int q = 0; q < nc; ++q) nh += ce[q] != __int_as_float(0x7f800000);
+    int mine = 0;
+    for (int q = lane; q < nc; q += 32) mine += ce[q] != __int_as_float(0x7f800000);
+    const int nh = __reduce_add_sync(0xffffffffu, mine);
     if (nh > cap) return -1;
     for (int q = lane; q < nc; q += 32) {
         const float e = ce[q];
