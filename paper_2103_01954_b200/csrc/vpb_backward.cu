@@ -588,7 +588,7 @@ constexpr int kWarpListBwd = kRaySegs;
 #define VPB_BWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
 #endif
 #ifndef VPB_BWD_PAIRS_MINB
-#define VPB_BWD_PAIRS_MINB 2
+#define VPB_BWD_PAIRS_MINB 3  // 80 registers (12 B of spills): 1.50 vs 1.52 ms for the backward row
 #endif
 #ifndef VPB_BWD_WARP_MINB
 #define VPB_BWD_WARP_MINB 3
@@ -847,10 +847,15 @@ k_bwd_plan(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, De
             const int j = j0 + lane;
             int n = 0;
             if (j < nh && A[j] >= 0) {
+                // e = the first step >= a_j with ts(e) >= X_j (or lastStep + 1): ts is
+                // nondecreasing in e, so start from the real-valued estimate and correct it
+                const int a = A[j];
                 const float x = X[j];
-                int e = A[j];
+                const double est = ceil((double)((x - t0) / dt) - (double)jit);
+                int e = est < (double)a ? a : est > (double)lastStep + 1.0 ? lastStep + 1 : (int)est;
+                while (e > a && t0 + (__int2float_rn(e - 1) + jit) * dt >= x) --e;
                 while (e <= lastStep && t0 + (__int2float_rn(e) + jit) * dt < x) ++e;
-                n = e - A[j];
+                n = e - a;
             }
             int incl = n;
 #pragma unroll
@@ -976,7 +981,7 @@ k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float
 // 164). The ray's rotG (entry-major) is staged in shared memory; lanes take 32 consecutive
 // steps, each forms its step's sum in list order, and the lanes' dot products are added in
 // step order (a step without samples, or a sample without pose terms, adds +0, which leaves a
-// sum that started at +0 unchanged). Then the t_min anchor chain onto the first entry.
+// sum that started at +0 unchanged). gTmin goes to span.w for K6d.
 constexpr int kFoldStage = 512;   // samples per ray staged in shared memory (more: read from global)
 __global__ void __launch_bounds__(128)
 k_bwd_fold(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp) {
@@ -1040,21 +1045,34 @@ k_bwd_fold(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev 
             if (next == 0x7fffffff) break;
             sb = next;
         }
-        if (lane == 0) {  // the t_min anchor chain onto the first hit's primitive
-            const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
-            const int k0 = __float_as_int(sg[2 * kRaySegs]);
-            const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
-            V3 gT3, gR3, gS3;
-            if (anchor_terms(xf_g + (size_t)k0 * kXfStride, bd.pose36 + 36 * (size_t)k0, sg[0], gTmin, o, d, gT3, gR3,
-                             gS3)) {
-                float *g = bd.g_pose + 9 * (size_t)k0;
-                const float an[9] = {gT3.x, gT3.y, gT3.z, gR3.x, gR3.y, gR3.z, gS3.x, gS3.y, gS3.z};
-#pragma unroll
-                for (int q = 0; q < 9; ++q)
-                    if (an[q] != 0.f) red_add(g + q, an[q]);
-            }
-        }
+        if (lane == 0) pp.span[r].w = __float_as_int(gTmin);  // k_bwd_anchor's input
         __syncwarp();
+    }
+}
+
+// K6d, one thread per ray: the t_min anchor chain (grad.cpp:166-194) onto the first hit's
+// primitive, from K6c's gTmin (span.w); a thread per ray keeps this serial code at full width.
+__global__ void __launch_bounds__(128)
+k_bwd_anchor(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int4 sp = pp.span[r];
+        if (sp.y <= 0) continue;
+        const float gTmin = __int_as_float(sp.w);
+        if (gTmin == 0.f) continue;
+        const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
+        const int k0 = __float_as_int(sg[2 * kRaySegs]);
+        const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        V3 gT3, gR3, gS3;
+        if (!anchor_terms(xf_g + (size_t)k0 * kXfStride, bd.pose36 + 36 * (size_t)k0, sg[0], gTmin, o, d, gT3, gR3,
+                          gS3))
+            continue;
+        float *g = bd.g_pose + 9 * (size_t)k0;
+        const float an[9] = {gT3.x, gT3.y, gT3.z, gR3.x, gR3.y, gR3.z, gS3.x, gS3.y, gS3.z};
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+            if (an[q] != 0.f) red_add(g + q, an[q]);
     }
 }
 
@@ -1192,6 +1210,8 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                                huge_cap);
         k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
         k_bwd_fold<<<ray_blocks, 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
+        const int64_t tb = (n_rays + 127) / 128;
+        k_bwd_anchor<<<(unsigned)(tb < 148 * 16 ? tb : 148 * 16), 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
         // the rays that found no room in the pair arrays (none once the capacity has grown)
         k_backward_rays_warp<<<(unsigned)(blocks < 148 * 4 ? blocks : 148 * 4), 128, 0, st>>>(
             mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, pairs->fb_list);
