@@ -618,7 +618,10 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
 // wide-window fallback like window overflows.
 constexpr int kWarpList = kRaySegs;  // segments per ray held by the warp
 constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp path gives up
-__global__ void __launch_bounds__(128)
+#ifndef VPB_RAYS_MINB
+#define VPB_RAYS_MINB 5
+#endif
+__global__ void __launch_bounds__(128, VPB_RAYS_MINB)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
                   int ovf_cap) {
@@ -627,6 +630,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
     __shared__ int s_c[4][kWarpList];
     __shared__ int s_cand[4][kWarpCand];
     __shared__ float s_ce[4][kWarpCand], s_cx[4][kWarpCand];
+    __shared__ float s_sv[4][128];  // march_warp: a chunk's per-step sums
     load_exp_tab(s_tab);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,7 +651,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
                 if (slot < ovf_cap) ovf_list[slot] = (int)r;
             }
         } else {
-            ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane);
+            ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane, s_sv[wid]);
             if (lane == 0) write_ray(od, r, ro);
             if (od.segs) {  // keep the list for the backward pass of the same rays
                 float *sg = od.segs + (size_t)r * (3 * kRaySegs);

@@ -719,7 +719,8 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
 #endif
 template <class Cands>
 __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X, const int *P, int cnt, V3 o,
-                             V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane) {
+                             V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane,
+                             float *sv) {
     RayOut out{0.f, 0.f, 0.f, 0.f, 0, 0, 0, 0, 0, 0, 0, 0};
     if (cnt == 0) return out;
     out.hit = 1;
@@ -835,42 +836,61 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         const unsigned empty = __ballot_sync(0xffffffffu, !(in_range && na > 0));
         const int L = empty ? __ffs(empty) - 1 : 32;
 #endif
-        for (int s = 0; s < L; ++s) {  // the chunk's visited steps, in order (march.cpp:71-88)
-            const float s_sig = __shfl_sync(0xffffffffu, sig, s);
-            const float s_rw = __shfl_sync(0xffffffffu, rw, s);
-            const float s_gw = __shfl_sync(0xffffffffu, gw, s);
-            const float s_bw = __shfl_sync(0xffffffffu, bw, s);
-            const int s_na = __shfl_sync(0xffffffffu, na, s);
-            if (done) continue;
-            ++out.samples;
-            out.prim_samples += s_na;
-            out.last_step = base + s;
-            const float dT = s_sig * dt;
+        // The chunk's visited steps, in order (march.cpp:71-88). The step sums go to shared
+        // memory; the transmittance chain (every lane, the same values) finds where the ray
+        // stops, then lanes 0-2 run the r, g, b chains side by side: the same additions in
+        // the same order as one loop carrying all four sums, in fewer instructions per step.
+        sv[lane] = sig;
+        sv[32 + lane] = rw;
+        sv[64 + lane] = gw;
+        sv[96 + lane] = bw;
+        __syncwarp();
+        int stop = L;  // steps before `stop` take dt in full; stop < L: the ray ends at step `stop`
+        bool sat = false;
+        float Tprev = T;
+        for (int s = 0; s < L; ++s) {
+            const float dT = sv[s] * dt;
             if (T + dT >= 1.0f) {
-                const float frac = (1.0f - T) / dT;
-                const float f = dt * frac;
-                cr += s_rw * f;
-                cg += s_gw * f;
-                cb += s_bw * f;
-                out.sat_tprev = T;
-                out.sat_sigma = s_sig;
-                out.sat_r = s_rw;
-                out.sat_g = s_gw;
-                out.sat_b = s_bw;
-                T = 1.0f;
-                out.saturated = 1;
-                done = true;
-                continue;
+                sat = true;
+                stop = s;
+                Tprev = T;
+                break;
             }
-            cr += s_rw * dt;
-            cg += s_gw * dt;
-            cb += s_bw * dt;
             T += dT;
             if (T > 1.0f - mp.eps) {
                 out.early = 1;
-                done = true;
+                stop = s;
+                break;
             }
         }
+        const int n_steps = stop < L ? stop + 1 : L;  // steps sampled in this chunk
+        const int n_full = sat ? stop : n_steps;     // ... of which with the full dt
+        {
+            const float *cv = sv + 32 * (1 + (lane < 2 ? lane : 2));
+            float c = lane == 0 ? cr : (lane == 1 ? cg : cb);
+            for (int s = 0; s < n_full; ++s) c += cv[s] * dt;
+            if (sat) {
+                const float frac = (1.0f - Tprev) / (sv[stop] * dt);  // march.cpp:75-82: (1 - T) / dT
+                c += cv[stop] * (dt * frac);
+            }
+            cr = __shfl_sync(0xffffffffu, c, 0);
+            cg = __shfl_sync(0xffffffffu, c, 1);
+            cb = __shfl_sync(0xffffffffu, c, 2);
+        }
+        out.samples += n_steps;
+        out.prim_samples += __reduce_add_sync(0xffffffffu, lane < n_steps ? na : 0);
+        if (n_steps > 0) out.last_step = base + n_steps - 1;
+        if (sat) {
+            out.sat_tprev = Tprev;
+            out.sat_sigma = sv[stop];
+            out.sat_r = sv[32 + stop];
+            out.sat_g = sv[64 + stop];
+            out.sat_b = sv[96 + stop];
+            T = 1.0f;
+            out.saturated = 1;
+        }
+        done = stop < L;
+        __syncwarp();
         if (done) break;
         if (L == 32) {
             base += 32;
