@@ -848,6 +848,20 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         int stop = L;  // steps before `stop` take dt in full; stop < L: the ray ends at step `stop`
         bool sat = false;
         float Tprev = T;
+        // Quiet chunk: when T plus every positive dT of the chunk stays clear of both stopping
+        // thresholds (by far more than the chain's rounding), no step can stop the ray, and the
+        // chain runs without its tests. NaN or inf terms make the bound fail: the tested loop.
+        float pos = 0.f;
+        if (lane < L) {
+            const float dT = sig * dt;
+            pos = dT > 0.0f ? dT : (dT == dT ? 0.0f : __int_as_float(0x7f800000));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
+        const float lim = fminf(1.0f - mp.eps, 1.0f);
+        if (T >= 0.0f && T + pos * 1.0001f + 1e-5f < lim) {
+            for (int s = 0; s < L; ++s) T += sv[s] * dt;
+        } else
         for (int s = 0; s < L; ++s) {
             const float dT = sv[s] * dt;
             if (T + dT >= 1.0f) {
