@@ -160,7 +160,7 @@ struct vp_ctx {
     DBuf<int2> bp_ent;
     DBuf<float> bp_terms;
     DBuf<int4> bp_span;
-    DBuf<int> bp_fb;
+    DBuf<int> bp_fb, bp_tiles;
     size_t pair_cap = 0;
     bool pair_cap_fixed = false;
     bool bwd_warp_walk = false;  // VPB_BWD_MODE=warp: the warp-per-ray walk for every ray (A/B)
@@ -702,6 +702,7 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->bp_terms.release();
     ctx->bp_span.release();
     ctx->bp_fb.release();
+    ctx->bp_tiles.release();
     for (int i = 0; i < vp_ctx::kStageSlots; ++i) {
         if (ctx->stage_h[i]) cudaFreeHost(ctx->stage_h[i]);
         ctx->stage_d[i].release();
@@ -1537,8 +1538,9 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             VP_CUDA(ctx, ctx->bp_span.ensure(n));
             VP_CUDA(ctx, ctx->bp_ent.ensure(n * kRaySegs));
             VP_CUDA(ctx, ctx->bp_fb.ensure(n));
+            VP_CUDA(ctx, ctx->bp_tiles.ensure(n / 4096 + 1));
             bp = BwdPairs{ctx->bp_rec.p, ctx->bp_terms.p, ctx->bp_span.p, ctx->bp_ent.p, ctx->bp_fb.p,
-                          unsigned(std::min<size_t>(cap, 0xffffffffu))};
+                          ctx->bp_tiles.p, unsigned(std::min<size_t>(cap, 0x7fffffffu))};
         }
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->bwd_list.p, int(n), ctx->fb_e.p, ctx->fb_x.p,

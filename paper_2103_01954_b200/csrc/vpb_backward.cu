@@ -869,34 +869,146 @@ k_bwd_plan(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, De
         const int total = carry;
         if (lane == 0) OFF[nh] = total;
         __syncwarp();
-        unsigned long long pbase = 0;
-        if (lane == 0 && total > 0) pbase = atomicAdd(&ctr->bwd_pairs, (unsigned long long)total);
-        pbase = __shfl_sync(0xffffffffu, pbase, 0);
-        int4 sp = make_int4(0, total, nh, 0);
-        if (total > 0 && pbase + (unsigned long long)total > pp.cap) {  // no room: the warp walk takes the ray
-            sp.y = -1;
-            if (lane == 0) pp.fb_list[atomicAdd(&ctr->bwd_fb, 1u)] = (int)r;
-            // the one range that straddles the capacity: K6b skips its records
-            for (unsigned long long t = pbase + lane; t < pp.cap; t += 32) pp.rec[t] = make_int4(-1, 0, 0, 0);
-        } else if (total > 0) {
-            sp.x = (int)pbase;
-            const bool sat = __float_as_int(state[1]) != 0;
-            for (int p = lane; p < total; p += 32) {
-                int lo = 0, hi = nh - 1;  // the last entry with OFF[j] <= p
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (OFF[mid] <= p) lo = mid;
-                    else hi = mid - 1;
-                }
-                const int step = A[lo] + (p - OFF[lo]);
-                const float ts = t0 + (__int2float_rn(step) + jit) * dt;
-                const int c = __float_as_int(sg[2 * kRaySegs + lo]);
-                pp.rec[pbase + p] = make_int4((int)r, c, __float_as_int(ts), (sat && step == lastStep) ? 1 : 0);
-            }
-            int2 *ent = pp.ent + (size_t)r * kRaySegs;
-            for (int j = lane; j < nh; j += 32) ent[j] = make_int2(A[j], OFF[j]);
-        }
+        int2 *ent = pp.ent + (size_t)r * kRaySegs;
+        for (int j = lane; j < nh; j += 32) ent[j] = make_int2(A[j], OFF[j]);
+        const int4 sp = make_int4(0, total, nh, 0);  // base: k_bwd_scan_* (ray order)
         if (lane == 0) pp.span[r] = sp;
+        __syncwarp();
+    }
+}
+
+// Pair bases in ray order (so K6b's lanes and resident warps walk neighbouring rays, whose
+// samples share payload and gradient lines in L2): an exclusive scan of the rays' sample
+// counts. k_bwd_scan_tiles scans 1024 rays per CTA (span.x = offset within the tile, tile_sums
+// = the tile's total); k_bwd_scan_top turns tile_sums into tile bases and stores the grand
+// total as the pair count.
+constexpr int kScanTile = 4096;  // rays per CTA of k_bwd_scan_tiles: 1024 threads x 4
+__global__ void __launch_bounds__(1024) k_bwd_scan_tiles(int64_t n_rays, BwdPairs pp, DevCounters *ctr) {
+    __shared__ int s_w[32];
+    const int64_t r0 = (int64_t)blockIdx.x * kScanTile + 4 * threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int v[4], mine = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        v[u] = r0 + u < n_rays ? max(pp.span[r0 + u].y, 0) : 0;
+        mine += v[u];
+    }
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += u;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int w = s_w[lane], wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += u;
+        }
+        s_w[lane] = wi - w;  // exclusive warp bases
+        if (lane == 31) {
+            pp.tile_sums[blockIdx.x] = gridDim.x == 1 ? 0 : wi;
+            if (gridDim.x == 1) ctr->bwd_pairs = (unsigned long long)wi;  // one tile: no k_bwd_scan_top
+        }
+    }
+    __syncthreads();
+    int off = s_w[wid] + incl - mine;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (r0 + u < n_rays) pp.span[r0 + u].x = off;
+        off += v[u];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_bwd_scan_top(int n_tiles, BwdPairs pp, DevCounters *ctr) {
+    __shared__ long long s_w[32];
+    __shared__ long long s_carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
+        const int t = t0 + threadIdx.x;
+        const long long v = t < n_tiles ? pp.tile_sums[t] : 0;
+        long long incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long u = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += u;
+        }
+        if (lane == 31) s_w[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            long long w = s_w[lane], wi = w;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long u = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= off) wi += u;
+            }
+            s_w[lane] = wi - w;
+        }
+        __syncthreads();
+        const long long base = s_carry + s_w[wid] + incl - v;
+        // bases past 2^31 cannot be pair indices: those rays take the warp walk (capacity < 2^31)
+        if (t < n_tiles) pp.tile_sums[t] = (int)min(base, (long long)0x7fffffff);
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = base + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ctr->bwd_pairs = (unsigned long long)s_carry;
+}
+
+// K6a (records), one warp per ray: the ray's samples (j, a_j + t), entry-major, at its base in
+// ray order; a ray past the capacity goes to the warp walk (the one straddling it leaves
+// sentinels that K6b skips).
+__global__ void __launch_bounds__(128)
+k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, DevCounters *ctr) {
+    __shared__ int s_a[4][kRaySegs], s_off[4][kRaySegs + 1];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int *A = s_a[wid], *OFF = s_off[wid];
+    const float dt = mp.dt;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t r = (int64_t)blockIdx.x * 4 + wid; r < n_rays; r += nwarps) {
+        int4 sp = pp.span[r];
+        if (sp.y <= 0) continue;
+        const int total = sp.y, nh = sp.z;
+        const long long base = (long long)pp.tile_sums[r / kScanTile] + sp.x;
+        if (base + total > (long long)pp.cap) {  // no room: the warp walk takes the ray
+            if (lane == 0) {
+                pp.fb_list[atomicAdd(&ctr->bwd_fb, 1u)] = (int)r;
+                pp.span[r] = make_int4(0, -1, nh, 0);
+            }
+            for (long long t = base + lane; t < (long long)pp.cap; t += 32) pp.rec[t] = make_int4(-1, 0, 0, 0);
+            continue;
+        }
+        const int2 *ent = pp.ent + (size_t)r * kRaySegs;
+        for (int j = lane; j < nh; j += 32) {
+            const int2 e = ent[j];
+            A[j] = e.x;
+            OFF[j] = e.y;
+        }
+        __syncwarp();
+        const float *state = bd.fwd_state + 8 * r;
+        const int lastStep = __float_as_int(state[0]);
+        const bool sat = __float_as_int(state[1]) != 0;
+        const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
+        const float t0 = sg[0];
+        const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        for (int p = lane; p < total; p += 32) {
+            int lo = 0, hi = nh - 1;  // the last entry with OFF[j] <= p
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (OFF[mid] <= p) lo = mid;
+                else hi = mid - 1;
+            }
+            const int step = A[lo] + (p - OFF[lo]);
+            const float ts = t0 + (__int2float_rn(step) + jit) * dt;
+            const int c = __float_as_int(sg[2 * kRaySegs + lo]);
+            pp.rec[base + p] = make_int4((int)r, c, __float_as_int(ts), (sat && step == lastStep) ? 1 : 0);
+        }
+        if (lane == 0) pp.span[r].x = (int)base;
         __syncwarp();
     }
 }
@@ -1208,6 +1320,10 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
         const unsigned ray_blocks = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);  // a warp per ray
         k_bwd_plan<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr, ray_list, list_cap, huge_list,
                                                huge_cap);
+        const int64_t n_tiles = (n_rays + kScanTile - 1) / kScanTile;
+        k_bwd_scan_tiles<<<(unsigned)n_tiles, 1024, 0, st>>>(n_rays, *pairs, ctr);
+        if (n_tiles > 1) k_bwd_scan_top<<<1, 1024, 0, st>>>((int)n_tiles, *pairs, ctr);
+        k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
         k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
         k_bwd_fold<<<ray_blocks, 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
         const int64_t tb = (n_rays + 127) / 128;

@@ -146,6 +146,7 @@ struct BwdPairs {
     int4 *span;            // [n_rays] base, total (-1: not planned), admitted entries, -
     int2 *ent;             // [n_rays][kRaySegs] admission step, offset in the ray's range
     int *fb_list;          // [n_rays] rays for the warp-per-ray walk
+    int *tile_sums;        // [n_rays / 4096 + 1] per 4096 rays: sample count, then base
     unsigned cap;
 };
 
