@@ -156,3 +156,42 @@ def test_backward_paths_agree(monkeypatch, mode):
             _check_close(f"{mode}.{case}.pose", got[n_pay:], g["grads"][n_pay:])
     finally:
         r.close()
+
+
+def test_large_batch_interleaved_gradient_any_alignment(renderer):
+    """Batches of >= 16,384 rays scatter an interleaved gradient with vector reductions and
+    transpose it into the planar GradBuffer at the C-ABI: a 16-byte aligned destination takes
+    the vectorized transpose, a caller's device pointer that is only 4-byte aligned the scalar
+    one. Both equal the reference's gradient of the replicated batch (linear in the rays)."""
+    import ctypes as C
+    import torch
+    from paper_2103_01954_b200 import _lib
+    g = load_groups("backward")["boxes_unsaturated"]
+    win, cfg = _inputs(g)
+    k, m = g["tr"].shape[0], int(g["m"])
+    renderer.set_scene_composed(api.compose(g["tr"]), api.PrimitiveSlab(k, m, g["payload"]), win)
+    n0 = g["o"].shape[0]
+    rep = -(-16384 // n0)
+    o, d = np.tile(g["o"], (rep, 1)), np.tile(g["d"], (rep, 1))
+    ar, aa, jit = np.tile(g["adj_rgb"], (rep, 1)), np.tile(g["adj_alpha"], rep), np.tile(g["jit"], rep)
+    host = renderer.backward_rays(o, d, ar, aa, cfg, g["tr"], jit)
+    want = g["grads"].astype(np.float64) * rep
+    n_pay = k * 4 * m ** 3
+    _check_close("aligned.payload", host[:n_pay], want[:n_pay])
+    _check_close("aligned.pose", host[n_pay:], want[n_pay:])
+    lib = _lib.load()
+    f32p = C.POINTER(C.c_float)
+    P = lambda t: C.cast(C.c_void_p(t.data_ptr()), f32p)  # noqa: E731
+    dev = {nm: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+           for nm, a in (("o", o), ("d", d), ("ar", ar), ("aa", aa), ("j", jit))}
+    buf = torch.zeros(host.size + 1, dtype=torch.float32, device="cuda")
+    view = buf[1:]  # 4-byte aligned only
+    assert view.data_ptr() % 16 != 0
+    mc = cfg.to_c()
+    tr = np.ascontiguousarray(g["tr"], np.float32)
+    rc = lib.vp_backward_rays(renderer.ctx, o.shape[0], P(dev["o"]), P(dev["d"]), P(dev["j"]), P(dev["ar"]),
+                              P(dev["aa"]), C.byref(mc), tr.ctypes.data_as(f32p), P(view), 0)
+    assert rc == 0, lib.vp_last_error(renderer.ctx)
+    got = view.cpu().numpy()
+    _check_close("unaligned.payload", got[:n_pay], want[:n_pay])
+    _check_close("unaligned.pose", got[n_pay:], want[n_pay:])
