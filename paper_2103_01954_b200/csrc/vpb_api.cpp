@@ -158,7 +158,7 @@ struct vp_ctx {
     // overflowed it (the overflowing rays take the warp walk, so results never depend on it)
     DBuf<int4> bp_rec;
     DBuf<int2> bp_ent;
-    DBuf<float> bp_terms;
+    DBuf<float4> bp_terms;
     DBuf<int4> bp_span;
     DBuf<int> bp_fb, bp_tiles;
     size_t pair_cap = 0;
@@ -1534,7 +1534,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             if (!ctx->pair_cap_fixed) ctx->pair_cap = std::max(ctx->pair_cap, std::max<size_t>(size_t(1) << 20, 64 * n));
             const size_t cap = std::max<size_t>(ctx->pair_cap, 1);
             VP_CUDA(ctx, ctx->bp_rec.ensure(cap));
-            VP_CUDA(ctx, ctx->bp_terms.ensure(3 * cap));
+            VP_CUDA(ctx, ctx->bp_terms.ensure(cap));
             VP_CUDA(ctx, ctx->bp_span.ensure(n));
             VP_CUDA(ctx, ctx->bp_ent.ensure(n * kRaySegs));
             VP_CUDA(ctx, ctx->bp_fb.ensure(n));

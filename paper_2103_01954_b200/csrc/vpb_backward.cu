@@ -996,6 +996,8 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
         const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
         const float t0 = sg[0];
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
+        if (lane == 0) OFF[nh] = total;
+        __syncwarp();
         for (int p = lane; p < total; p += 32) {
             int lo = 0, hi = nh - 1;  // the last entry with OFF[j] <= p
             while (lo < hi) {
@@ -1004,9 +1006,20 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
                 else hi = mid - 1;
             }
             const int step = A[lo] + (p - OFF[lo]);
+            // the sample's place in step-major order (steps in order, each step's live entries
+            // in list order): samples of every entry at earlier steps, then the entries before
+            // this one live at this step
+            int sm = 0;
+            for (int j = 0; j < nh; ++j) {
+                const int a = A[j], n = OFF[j + 1] - OFF[j];
+                if (a < 0 || n == 0) continue;
+                sm += min(max(step - a, 0), n) + (j < lo && step >= a && step < a + n ? 1 : 0);
+            }
             const float ts = t0 + (__int2float_rn(step) + jit) * dt;
             const int c = __float_as_int(sg[2 * kRaySegs + lo]);
-            pp.rec[base + p] = make_int4((int)r, c, __float_as_int(ts), (sat && step == lastStep) ? 1 : 0);
+            const unsigned w = (unsigned)(base + sm) | ((sat && step == lastStep) ? 0x80000000u : 0u);
+            pp.rec[base + p] = make_int4((int)r, c, __float_as_int(ts), (int)w);
+            pp.terms[base + sm].w = __int_as_float(step);  // K6b fills in rotG
         }
         if (lane == 0) pp.span[r].x = (int)base;
         __syncwarp();
@@ -1017,7 +1030,7 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
 // as reductions). The pose terms go to the primitive's deltaT/deltaR/deltaS: the samples are
 // entry-major, so a warp's lanes form runs of one (ray, primitive); each run is summed with a
 // segmented shuffle scan and its last lane issues the nine reductions (SURVEY.md §8 a-20:
-// warp-aggregated atomics). rotG is kept for K6c's t_min chain (terms[3][cap]).
+// warp-aggregated atomics). rotG is kept for K6c's t_min chain (terms, step-major).
 __global__ void __launch_bounds__(256, VPB_BWD_PAIRS_MINB)
 k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
             RaysDev rays, BwdDev bd, BwdPairs pp, const DevCounters *__restrict__ ctr) {
@@ -1048,7 +1061,7 @@ k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float
             const V3 aRgb = mk3(bd.adj_rgb[3 * r], bd.adj_rgb[3 * r + 1], bd.adj_rgb[3 * r + 2]);
             if (bd.touched) bd.touched[c] = 1u;
             V3 rotG, rTerm, sTerm;
-            if (sample_adjoint(cands, mp, s_tab, fwd, bd, aRgb, bd.adj_alpha[r], rec.w != 0, c, c, o + d * ts, rotG,
+            if (sample_adjoint(cands, mp, s_tab, fwd, bd, aRgb, bd.adj_alpha[r], rec.w < 0, c, c, o + d * ts, rotG,
                                rTerm, sTerm)) {
                 v[0] = -rotG.x;
                 v[1] = -rotG.y;
@@ -1060,10 +1073,11 @@ k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float
                 v[7] = sTerm.y;
                 v[8] = sTerm.z;
             }
-            float *t = pp.terms + p;
-            t[0] = -v[0];  // rotG (+0 without pose terms)
-            t[cap] = -v[1];
-            t[2 * cap] = -v[2];
+            // rotG (+0 without pose terms) at the sample's step-major place, with its step
+            float4 *t = pp.terms + (rec.w & 0x7fffffff);
+            t->x = -v[0];
+            t->y = -v[1];
+            t->z = -v[2];
         }
         // runs of equal (ray, primitive) over the lanes: segmented inclusive scan
         const int prev_x = __shfl_up_sync(0xffffffffu, rec.x, 1), prev_y = __shfl_up_sync(0xffffffffu, rec.y, 1);
@@ -1088,103 +1102,47 @@ k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float
     }
 }
 
-// K6c, one warp per ray: gTmin = the sum over the visited steps, in step order, of
+// K6c, one thread per ray: gTmin = the sum over the visited steps, in step order, of
 // dot(gPWorldStep, d), gPWorldStep = the step's rotG summed in list order from 0 (grad.cpp:66-
-// 164). The ray's rotG (entry-major) is staged in shared memory; lanes take 32 consecutive
-// steps, each forms its step's sum in list order, and the lanes' dot products are added in
-// step order (a step without samples, or a sample without pose terms, adds +0, which leaves a
-// sum that started at +0 unchanged). gTmin goes to span.w for K6d.
-constexpr int kFoldStage = 512;   // samples per ray staged in shared memory (more: read from global)
+// 164). The ray's samples are read in step-major order (k_bwd_records placed each sample's
+// rotG there, with its step), so both sums are one sequential pass (a sample without pose
+// terms adds +0, which leaves a sum that started at +0 unchanged). Then the t_min anchor chain
+// (grad.cpp:166-194) onto the first hit's primitive.
 __global__ void __launch_bounds__(128)
 k_bwd_fold(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp) {
-    __shared__ int s_a[4][kRaySegs], s_off[4][kRaySegs + 1];
-    __shared__ float s_rot[4][3][kFoldStage];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int *A = s_a[wid], *OFF = s_off[wid];
-    const size_t cap = pp.cap;
-    const int64_t nwarps = (int64_t)gridDim.x * 4;
-    for (int64_t r = (int64_t)blockIdx.x * 4 + wid; r < n_rays; r += nwarps) {
-        const int4 sp = pp.span[r];
-        if (sp.y <= 0) continue;
-        const int total = sp.y, nh = sp.z;
-        const int2 *ent = pp.ent + (size_t)r * kRaySegs;
-        for (int j = lane; j < nh; j += 32) {
-            const int2 e = ent[j];
-            A[j] = e.x;
-            OFF[j] = e.y;
-        }
-        if (lane == 0) OFF[nh] = total;
-        const float *T = pp.terms + (size_t)sp.x;
-        const bool staged = total <= kFoldStage;
-        if (staged)
-            for (int t = lane; t < total; t += 32) {
-                s_rot[wid][0][t] = T[t];
-                s_rot[wid][1][t] = T[cap + t];
-                s_rot[wid][2][t] = T[2 * cap + t];
-            }
-        __syncwarp();
-        const float *R0 = staged ? s_rot[wid][0] : T, *R1 = staged ? s_rot[wid][1] : T + cap,
-                    *R2 = staged ? s_rot[wid][2] : T + 2 * cap;
-        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
-        float gTmin = 0.f;
-        int jlo = 0, sb = 0;  // entry 0 is admitted at step 0 (ts(0) >= tEnter of the first entry)
-        for (;;) {
-            const int s = sb + lane;
-            V3 g = mk3(0.f, 0.f, 0.f);
-            bool any = false;
-            for (int j = jlo; j < nh; ++j) {
-                const int a = A[j];
-                if (a > sb + 31) break;  // admission steps grow with j (unadmitted entries are -1)
-                const int o = OFF[j], n = OFF[j + 1] - o;
-                if (a >= 0 && s >= a && s < a + n) {
-                    const int idx = o + (s - a);
-                    g = g + mk3(R0[idx], R1[idx], R2[idx]);
-                    any = true;
-                }
-            }
-            const float contrib = any ? dot3(g, d) : 0.f;
-            const unsigned used = __ballot_sync(0xffffffffu, any);
-            for (unsigned m = used; m; m &= m - 1) gTmin += __shfl_sync(used, contrib, __ffs(m) - 1);
-            // the next step with a live entry, at or after sb + 32
-            const int nb = sb + 32;
-            while (jlo < nh && (A[jlo] < 0 || A[jlo] + (OFF[jlo + 1] - OFF[jlo]) <= nb)) ++jlo;
-            int next = 0x7fffffff;
-            for (int j = jlo + lane; j < nh; j += 32) {
-                const int a = A[j], n = OFF[j + 1] - OFF[j];
-                if (a >= 0 && n > 0 && a + n > nb) next = min(next, max(a, nb));
-            }
-            next = __reduce_min_sync(0xffffffffu, next);
-            if (next == 0x7fffffff) break;
-            sb = next;
-        }
-        if (lane == 0) pp.span[r].w = __float_as_int(gTmin);  // k_bwd_anchor's input
-        __syncwarp();
-    }
-}
-
-// K6d, one thread per ray: the t_min anchor chain (grad.cpp:166-194) onto the first hit's
-// primitive, from K6c's gTmin (span.w); a thread per ray keeps this serial code at full width.
-__global__ void __launch_bounds__(128)
-k_bwd_anchor(const float *__restrict__ xf_g, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
          r += (int64_t)gridDim.x * blockDim.x) {
         const int4 sp = pp.span[r];
         if (sp.y <= 0) continue;
-        const float gTmin = __int_as_float(sp.w);
+        const float4 *T = pp.terms + (size_t)sp.x;
+        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
+        float gTmin = 0.f;
+        V3 g = mk3(0.f, 0.f, 0.f);
+        int cur = __float_as_int(T[0].w);
+        for (int t = 0; t < sp.y; ++t) {
+            const float4 v = T[t];
+            const int step = __float_as_int(v.w);
+            if (step != cur) {  // the previous step is complete
+                gTmin += dot3(g, d);
+                g = mk3(0.f, 0.f, 0.f);
+                cur = step;
+            }
+            g = g + mk3(v.x, v.y, v.z);
+        }
+        gTmin += dot3(g, d);
         if (gTmin == 0.f) continue;
         const float *sg = bd.fwd_segs + (size_t)r * (3 * kRaySegs);
         const int k0 = __float_as_int(sg[2 * kRaySegs]);
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
-        const V3 d = mk3(rays.dirs[3 * r], rays.dirs[3 * r + 1], rays.dirs[3 * r + 2]);
         V3 gT3, gR3, gS3;
         if (!anchor_terms(xf_g + (size_t)k0 * kXfStride, bd.pose36 + 36 * (size_t)k0, sg[0], gTmin, o, d, gT3, gR3,
                           gS3))
             continue;
-        float *g = bd.g_pose + 9 * (size_t)k0;
+        float *gp = bd.g_pose + 9 * (size_t)k0;
         const float an[9] = {gT3.x, gT3.y, gT3.z, gR3.x, gR3.y, gR3.z, gS3.x, gS3.y, gS3.z};
 #pragma unroll
         for (int q = 0; q < 9; ++q)
-            if (an[q] != 0.f) red_add(g + q, an[q]);
+            if (an[q] != 0.f) red_add(gp + q, an[q]);
     }
 }
 
@@ -1325,9 +1283,8 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
         if (n_tiles > 1) k_bwd_scan_top<<<1, 1024, 0, st>>>((int)n_tiles, *pairs, ctr);
         k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
         k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
-        k_bwd_fold<<<ray_blocks, 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
         const int64_t tb = (n_rays + 127) / 128;
-        k_bwd_anchor<<<(unsigned)(tb < 148 * 16 ? tb : 148 * 16), 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
+        k_bwd_fold<<<(unsigned)(tb < 148 * 16 ? tb : 148 * 16), 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
         // the rays that found no room in the pair arrays (none once the capacity has grown)
         k_backward_rays_warp<<<(unsigned)(blocks < 148 * 4 ? blocks : 148 * 4), 128, 0, st>>>(
             mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, pairs->fb_list);

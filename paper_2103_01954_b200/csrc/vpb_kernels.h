@@ -141,8 +141,8 @@ struct BwdDev {
 // K6b evaluates one sample per thread (payload scatter, pose terms); K6c folds each ray's
 // pose terms per entry and the t_min chain in step order.
 struct BwdPairs {
-    int4 *rec;             // [cap] ray, primitive, ts (bits), saturating step (0/1)
-    float *terms;          // [3][cap] rotG per sample (K6c's t_min chain)
+    int4 *rec;             // [cap] ray, primitive, ts (bits), step-major slot | saturating step << 31
+    float4 *terms;         // [cap] rotG and the lattice step per sample, step-major per ray (K6c)
     int4 *span;            // [n_rays] base, total (-1: not planned), admitted entries, -
     int2 *ent;             // [n_rays][kRaySegs] admission step, offset in the ray's range
     int *fb_list;          // [n_rays] rays for the warp-per-ray walk
