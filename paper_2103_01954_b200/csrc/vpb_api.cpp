@@ -181,6 +181,7 @@ struct vp_ctx {
     int bwd_v4 = -1;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
+    DBuf<BvhWide> bvh_wide;  // the same hierarchy two levels per record (warp walks)
     // vp_render_async into host memory: two device output slots; the device->host copy of
     // one view (copy_stream) overlaps the rendering of the next
     cudaStream_t copy_stream = nullptr;
@@ -263,12 +264,14 @@ int ensure_bvh(vp_ctx *ctx, MarchDev &mp) {
     const int n = ctx->n_prim;
     if (ctx->bvh_dirty && n > 1) {
         VP_CUDA(ctx, ctx->bvh_nodes.ensure(size_t(n - 1)));
+        VP_CUDA(ctx, ctx->bvh_wide.ensure(size_t(n - 1)));
         const size_t bytes = bvh_scratch_bytes(n);
         VP_CUDA(ctx, ctx->bvh_scratch.ensure(bytes));
-        VP_CUDA(ctx, launch_bvh_build(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_scratch.p, bytes, ctx->stream));
+        VP_CUDA(ctx, launch_bvh_build(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_wide.p, ctx->bvh_scratch.p, bytes,
+                                      ctx->stream));
     }
     ctx->bvh_dirty = false;
-    mp.bvh = BvhDev{ctx->bvh_nodes.p, n};
+    mp.bvh = BvhDev{ctx->bvh_nodes.p, n, ctx->bvh_wide.p};
     return VP_OK;
 }
 

@@ -429,8 +429,36 @@ cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tm
     return radix_sort30(keys, tmp, hist, n, st);
 }
 
-cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
-                             cudaStream_t st) {
+// BvhWide record of every internal node (after the refit): its four grandchild slots.
+__global__ void k_bvh_widen(const BvhNode *__restrict__ nodes, int n_internal, BvhWide *__restrict__ wide) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_internal) return;
+    const BvhNode nd = nodes[i];
+    const float inv = __int_as_float(0x7f800000);
+    BvhWide w;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int child = c ? nd.d.y : nd.d.x;
+        if (child < 0) {  // a leaf child: the leaf in slot 2c, slot 2c + 1 empty
+            const float4 lo_hi0 = c ? make_float4(nd.b.z, nd.b.w, nd.c.x, nd.c.y) : nd.a;
+            const float2 hi12 = c ? make_float2(nd.c.z, nd.c.w) : make_float2(nd.b.x, nd.b.y);
+            w.s[4 * c] = lo_hi0;
+            w.s[4 * c + 1] = make_float4(hi12.x, hi12.y, __int_as_float(child), 1.0f);
+            w.s[4 * c + 2] = make_float4(inv, inv, inv, -inv);
+            w.s[4 * c + 3] = make_float4(-inv, -inv, __int_as_float(0), 0.0f);
+        } else {
+            const BvhNode cn = nodes[child];
+            w.s[4 * c] = cn.a;
+            w.s[4 * c + 1] = make_float4(cn.b.x, cn.b.y, __int_as_float(cn.d.x), 1.0f);
+            w.s[4 * c + 2] = make_float4(cn.b.z, cn.b.w, cn.c.x, cn.c.y);
+            w.s[4 * c + 3] = make_float4(cn.c.z, cn.c.w, __int_as_float(cn.d.y), 1.0f);
+        }
+    }
+    wide[i] = w;
+}
+
+cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
+                             size_t scratch_bytes, cudaStream_t st) {
     if (n <= 1) return cudaSuccess;
     const BvhScratch sc = bvh_layout(n, scratch);
     if (sc.total > scratch_bytes) return cudaErrorInvalidValue;
@@ -450,6 +478,7 @@ cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scr
     k_bvh_internal<<<(n - 1 + 255) / 256, 256, 0, st>>>(k0, n, nodes, parent);
     cudaMemsetAsync(flags, 0, (size_t)n * 4, st);
     k_bvh_refit<<<b, 256, 0, st>>>(k0, n, lo, hi, nodes, nlo, nhi, parent, flags);
+    if (wide) k_bvh_widen<<<(n - 1 + 255) / 256, 256, 0, st>>>(nodes, n - 1, wide);
     return cudaGetLastError();
 }
 

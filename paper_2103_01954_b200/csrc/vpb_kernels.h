@@ -47,9 +47,17 @@ struct BvhNode {
     float4 c;  // right lo.z, right hi.xyz
     int4 d;    // left, right, -, -
 };
+// The same hierarchy two levels at a time (k_bvh_widen): record i holds the four grandchild
+// slots of internal node i, slot 2c + g = child c's child g (or, for a leaf child c, the leaf
+// itself in g = 0 and an empty g = 1): lo.xyz hi.x | hi.yz, index (int bits), valid. One 128-byte
+// record per frontier node replaces the node + child loads of the two-level warp walk.
+struct BvhWide {
+    float4 s[8];
+};
 struct BvhDev {
     const BvhNode *nodes;
     int n_prim;  // 1 -> the root is primitive 0 itself
+    const BvhWide *wide = nullptr;
 };
 
 struct MarchDev {
@@ -255,8 +263,8 @@ cudaError_t launch_gather_deltas(const float *tr24, int n_prim, float *deltas, c
 cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_t st);
 // vpb_bvh.cu: BVH build over the resident transforms (n - 1 nodes)
 size_t bvh_scratch_bytes(int n);
-cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, void *scratch, size_t scratch_bytes,
-                             cudaStream_t st);
+cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
+                             size_t scratch_bytes, cudaStream_t st);
 // the BVH's stable radix sort on key bits [32, 62) (testing); hist: 256 * ceil(n / 2048) words
 cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n,
                                 cudaStream_t st);

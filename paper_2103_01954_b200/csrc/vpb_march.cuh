@@ -578,7 +578,13 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
         bool test = false;
         int id = 0;
         float lx = 0.f, ly = 0.f, lz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
-        if (act) {
+        if (act && bvh.wide) {  // the node's grandchild slots in one 128-byte record (k_bvh_widen)
+            const float4 *ws = bvh.wide[node].s + 2 * (lane & 3);
+            const float4 sa = ws[0], sb = ws[1];
+            lx = sa.x, ly = sa.y, lz = sa.z, hx = sa.w, hy = sb.x, hz = sb.y;
+            id = __float_as_int(sb.z);
+            test = sb.w != 0.0f;
+        } else if (act) {
             const BvhNode n = bvh.nodes[node];
             const int child = c ? n.d.y : n.d.x;
             if (child < 0) {
