@@ -195,3 +195,36 @@ def test_large_batch_interleaved_gradient_any_alignment(renderer):
     got = view.cpu().numpy()
     _check_close("unaligned.payload", got[:n_pay], want[:n_pay])
     _check_close("unaligned.pose", got[n_pay:], want[n_pay:])
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_random_scenes_backward_matches_restatement(renderer, oracle, seed):
+    """Randomized scenes and rays through K6a-c: sparse clouds (rays with gaps between their
+    segments, so the walk takes gap skips), dense ones (several live entries per step, step-major
+    slots that interleave entries), saturating and unsaturated rays, jitter. Gradients within
+    the reordering bound of the restatement's sequential backwardRay."""
+    rng = np.random.default_rng(seed)
+    k, m = (60, 4) if seed == 11 else ((400, 3) if seed == 12 else (150, 2))
+    spread = 0.6 if seed != 12 else 0.25
+    t = rng.uniform(-spread, spread, (k, 3))
+    s = rng.uniform(0.02, 0.12, (k, 3))
+    tr = api.transform_records(t, np.tile(np.eye(3), (k, 1, 1)), s, delta_r=rng.uniform(-1, 1, (k, 3)))
+    pay = rng.uniform(0.0, 1.0, k * 4 * m ** 3).astype(np.float32)
+    pay.reshape(k, 4, -1)[:, 3] *= np.float32(40.0 if seed == 12 else 8.0)
+    win = api.WindowParams()
+    cfg = api.MarchConfig(step_size=0.004, jitter=seed == 13, seed=seed)
+    xf = api.compose(tr)
+    renderer.set_scene_composed(xf, api.PrimitiveSlab(k, m, pay), win)
+    n = 512
+    o = np.tile(np.float32([0.05, -0.03, -2.0]), (n, 1)) + rng.uniform(-0.02, 0.02, (n, 3)).astype(np.float32)
+    tgt = rng.uniform(-spread, spread, (n, 3)).astype(np.float32)
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    jit = rng.uniform(0, 1, n).astype(np.float32) if cfg.jitter else None
+    ar = rng.normal(size=(n, 3)).astype(np.float32)
+    aa = rng.normal(size=n).astype(np.float32)
+    got = renderer.backward_rays(o, d, ar, aa, cfg, tr, jit)
+    want = oracle.backward_rays(tr, m, pay, win, o, d, ar, aa, cfg, jit)
+    n_pay = k * 4 * m ** 3
+    _check_close(f"rand{seed}.payload", got[:n_pay], want[:n_pay])
+    _check_close(f"rand{seed}.pose", got[n_pay:], want[n_pay:])
