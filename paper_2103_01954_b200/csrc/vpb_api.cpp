@@ -8,6 +8,10 @@
 // fallback kernel reads the overflow count on the device), so vp_render_async can be
 // captured or overlapped; vp_render adds the host copies and one final synchronisation.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1751,6 +1755,31 @@ int vp_load_slab(vp_ctx *ctx, const char *path, int32_t n_prim, const float *xf1
     if (int rc = vp_set_scene(ctx, k, m, xf15, nullptr, window_alpha, window_beta)) return rc;
     ctx->has_scene = false;  // until the payload is complete
     const size_t m3 = size_t(m) * m * m, per_prim = 4 * m3;
+    {
+        // The file mapped read-only: the payload goes through the same pipeline as a pageable
+        // caller slab (upload_planar_host: the copy pool's threads move page-cache pages into
+        // the page-locked staging slots while the copy engine and K0 take the previous chunk).
+        // A file that cannot be mapped takes the double-buffered fread path below.
+        const size_t need = 16 + size_t(k) * per_prim * 4;
+        struct stat stt{};
+        if (fstat(fileno(f), &stt) == 0 && S_ISREG(stt.st_mode)) {
+            if (size_t(stt.st_size) < need)
+                return fail(ctx, VP_ERR_FORMAT, std::string("truncated slab payload: ") + path);
+            void *map = mmap(nullptr, need, PROT_READ, MAP_PRIVATE, fileno(f), 0);
+            if (map != MAP_FAILED) {
+                madvise(map, need, MADV_SEQUENTIAL);
+                madvise(map, need, MADV_WILLNEED);
+                const int rc = upload_planar_host(ctx, reinterpret_cast<const float *>(
+                                                           static_cast<const unsigned char *>(map) + 16),
+                                                  k, int64_t(m3));
+                munmap(map, need);
+                if (rc) return rc;
+                ctx->pairs_dirty = true;
+                ctx->has_scene = true;
+                return VP_OK;
+            }
+        }
+    }
     const size_t chunk_prims = std::max<size_t>(1, (size_t(64) << 20) / (per_prim * 4));
     float *pinned[2] = {nullptr, nullptr};
     DBuf<float> dev[2];
