@@ -1011,9 +1011,10 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
             // this one live at this step
             int sm = 0;
             for (int j = 0; j < nh; ++j) {
-                const int a = A[j], n = OFF[j + 1] - OFF[j];
-                if (a < 0 || n == 0) continue;
-                sm += min(max(step - a, 0), n) + (j < lo && step >= a && step < a + n ? 1 : 0);
+                const int a = A[j];
+                if (a < 0 || a > step) break;  // admission steps grow with j; unadmitted entries last
+                const int n = OFF[j + 1] - OFF[j];
+                sm += min(step - a, n) + (j < lo && step < a + n ? 1 : 0);
             }
             const float ts = t0 + (__int2float_rn(step) + jit) * dt;
             const int c = __float_as_int(sg[2 * kRaySegs + lo]);
