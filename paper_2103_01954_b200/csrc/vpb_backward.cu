@@ -1194,8 +1194,8 @@ __global__ void __launch_bounds__(256) k_grad_transpose(float4 *__restrict__ g4,
 }
 
 // The same for m3 % 4 == 0, flattened over (primitive, 4 consecutive voxels) in tiles of 256
-// quads per CTA, touched primitives only (the caller has zeroed the planar buffer unless it
-// accumulates): the tile's interleaved voxels are loaded with coalesced 16-byte accesses and
+// quads per CTA (untouched primitives: zero vectors, or nothing when accumulating; touched
+// ones): the tile's interleaved voxels are loaded with coalesced 16-byte accesses and
 // staged in shared memory; after the barrier the slots are cleared (a store to an address
 // whose load is still in flight stalls the warp: 6x slower when the clear followed each load)
 // and each thread writes its quad as one 16-byte vector per channel plane.
@@ -1209,7 +1209,18 @@ __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4
         const unsigned k_first = i0 / q3, k_last = min(i0 + 255u, nq - 1) / q3;
         bool any = false;  // block-uniform: is a primitive of this tile touched?
         for (unsigned k = k_first; k <= k_last && !any; ++k) any = touched[k] != 0u;
-        if (!any) continue;
+        if (!any) {  // untouched primitives: zeros (or the caller's values when accumulating)
+            const unsigned i = i0 + t;
+            if (!accumulate && i < nq) {
+                const unsigned k = i / q3;
+                float4 *dst = planar + (size_t)k * 4 * q3 + (i - k * q3);
+                dst[0] = z;
+                dst[q3] = z;
+                dst[2 * q3] = z;
+                dst[3 * q3] = z;
+            }
+            continue;
+        }
         bool tch[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1242,6 +1253,11 @@ __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4
                 dst[q3] = p1;
                 dst[2 * q3] = p2;
                 dst[3 * q3] = p3;
+            } else if (!accumulate) {
+                dst[0] = z;
+                dst[q3] = z;
+                dst[2 * q3] = z;
+                dst[3 * q3] = z;
             }
         }
         __syncthreads();
@@ -1253,8 +1269,6 @@ cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *tou
     if (n_prim == 0 || m3 == 0) return cudaSuccess;
     const size_t nq = size_t(n_prim) * (m3 / 4);
     if (m3 % 4 == 0 && (reinterpret_cast<uintptr_t>(planar) & 15) == 0 && nq < (size_t(1) << 32) - 256) {
-        if (!accumulate)
-            if (cudaError_t e = cudaMemsetAsync(planar, 0, nq * 64, st)) return e;
         k_grad_transpose4<<<148 * 16, 256, 0, st>>>(g4, reinterpret_cast<float4 *>(planar), touched, unsigned(nq),
                                                    m3 / 4, accumulate ? 1 : 0);
         return cudaGetLastError();
