@@ -429,29 +429,63 @@ cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tm
     return radix_sort30(keys, tmp, hist, n, st);
 }
 
-// BvhWide record of every internal node (after the refit): its four grandchild slots.
+// BvhWide record of every internal node (after the refit): its eight great-grandchild slots.
+__device__ __forceinline__ void wide_slot(BvhWide &w, int q, float4 a, float2 hyz, int id, bool valid) {
+    w.s[2 * q] = a;
+    w.s[2 * q + 1] = make_float4(hyz.x, hyz.y, __int_as_float(id), valid ? 1.0f : 0.0f);
+}
+// child c of a binary node: its box (lo.xyz hi.x | hi.yz) and index
+__device__ __forceinline__ void node_child(const BvhNode &nd, int c, float4 &a, float2 &hyz, int &id) {
+    if (c) {
+        a = make_float4(nd.b.z, nd.b.w, nd.c.x, nd.c.y);
+        hyz = make_float2(nd.c.z, nd.c.w);
+        id = nd.d.y;
+    } else {
+        a = nd.a;
+        hyz = make_float2(nd.b.x, nd.b.y);
+        id = nd.d.x;
+    }
+}
 __global__ void k_bvh_widen(const BvhNode *__restrict__ nodes, int n_internal, BvhWide *__restrict__ wide) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_internal) return;
+    const float inf = __int_as_float(0x7f800000);
+    const float4 ea = make_float4(inf, inf, inf, -inf);
+    const float2 eh = make_float2(-inf, -inf);
     const BvhNode nd = nodes[i];
-    const float inv = __int_as_float(0x7f800000);
     BvhWide w;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-        const int child = c ? nd.d.y : nd.d.x;
-        if (child < 0) {  // a leaf child: the leaf in slot 2c, slot 2c + 1 empty
-            const float4 lo_hi0 = c ? make_float4(nd.b.z, nd.b.w, nd.c.x, nd.c.y) : nd.a;
-            const float2 hi12 = c ? make_float2(nd.c.z, nd.c.w) : make_float2(nd.b.x, nd.b.y);
-            w.s[4 * c] = lo_hi0;
-            w.s[4 * c + 1] = make_float4(hi12.x, hi12.y, __int_as_float(child), 1.0f);
-            w.s[4 * c + 2] = make_float4(inv, inv, inv, -inv);
-            w.s[4 * c + 3] = make_float4(-inv, -inv, __int_as_float(0), 0.0f);
-        } else {
-            const BvhNode cn = nodes[child];
-            w.s[4 * c] = cn.a;
-            w.s[4 * c + 1] = make_float4(cn.b.x, cn.b.y, __int_as_float(cn.d.x), 1.0f);
-            w.s[4 * c + 2] = make_float4(cn.b.z, cn.b.w, cn.c.x, cn.c.y);
-            w.s[4 * c + 3] = make_float4(cn.c.z, cn.c.w, __int_as_float(cn.d.y), 1.0f);
+        float4 ca;
+        float2 ch;
+        int cid;
+        node_child(nd, c, ca, ch, cid);
+        if (cid < 0) {  // a leaf child: slot 4c, the rest of its group empty
+            wide_slot(w, 4 * c, ca, ch, cid, true);
+            for (int q = 1; q < 4; ++q) wide_slot(w, 4 * c + q, ea, eh, 0, false);
+            continue;
+        }
+        const BvhNode cn = nodes[cid];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            float4 ga;
+            float2 gh;
+            int gid;
+            node_child(cn, g, ga, gh, gid);
+            if (gid < 0) {  // a leaf grandchild: slot 4c + 2g, its pair empty
+                wide_slot(w, 4 * c + 2 * g, ga, gh, gid, true);
+                wide_slot(w, 4 * c + 2 * g + 1, ea, eh, 0, false);
+                continue;
+            }
+            const BvhNode gn = nodes[gid];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float4 ha;
+                float2 hh;
+                int hid;
+                node_child(gn, h, ha, hh, hid);
+                wide_slot(w, 4 * c + 2 * g + h, ha, hh, hid, true);
+            }
         }
     }
     wide[i] = w;

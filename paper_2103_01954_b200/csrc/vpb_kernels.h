@@ -47,12 +47,14 @@ struct BvhNode {
     float4 c;  // right lo.z, right hi.xyz
     int4 d;    // left, right, -, -
 };
-// The same hierarchy two levels at a time (k_bvh_widen): record i holds the four grandchild
-// slots of internal node i, slot 2c + g = child c's child g (or, for a leaf child c, the leaf
-// itself in g = 0 and an empty g = 1): lo.xyz hi.x | hi.yz, index (int bits), valid. One 128-byte
-// record per frontier node replaces the node + child loads of the two-level warp walk.
+// The same hierarchy three levels at a time (k_bvh_widen): record i holds the eight great-
+// grandchild slots of internal node i, slot 4c + 2g + h = child c's child g's child h; a leaf
+// met earlier sits in the first slot of its group (h = 0, and g = 0 for a leaf child) with the
+// rest of the group empty. A slot is lo.xyz hi.x | hi.yz, index (int bits), valid. One
+// 256-byte record per frontier node replaces the node, child and grandchild loads of a
+// three-level round of the warp walk.
 struct BvhWide {
-    float4 s[8];
+    float4 s[16];
 };
 struct BvhDev {
     const BvhNode *nodes;

@@ -561,6 +561,44 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
     int sp = 1;
     nc = 0;
 #if VPB_BVH_2LEVEL
+    if (bvh.wide) {
+        // Three levels per round from the wide records (k_bvh_widen): up to 4 frontier nodes,
+        // 8 lanes each (lane = 8 f + slot); lane tests great-grandchild slot `slot` of its
+        // frontier node. A parent's box is the union of its children's, so the leaves found
+        // are those of the one-level walk (never fewer: the exact test after the walk decides).
+        while (sp > 0) {
+            const int take = sp < 4 ? sp : 4, b = sp - take;
+            const int f = lane >> 3;
+            const bool act = f < take;
+            const int node = act ? fr[b + f] : 0;
+            __syncwarp();
+            bool test = false;
+            int id = 0;
+            float lx = 0.f, ly = 0.f, lz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
+            if (act) {
+                const float4 *ws = bvh.wide[node].s + 2 * (lane & 7);
+                const float4 sa = ws[0], sb = ws[1];
+                lx = sa.x, ly = sa.y, lz = sa.z, hx = sa.w, hy = sb.x, hz = sb.y;
+                id = __float_as_int(sb.z);
+                test = sb.w != 0.0f;
+            }
+            const bool hit = test && ray_box(o, d, inv, lx, ly, lz, hx, hy, hz);
+            const unsigned pi = __ballot_sync(0xffffffffu, hit && id >= 0);
+            const unsigned pl = __ballot_sync(0xffffffffu, hit && id < 0);
+            const int np = __popc(pi);
+            if (b + np > cap_fr) return -1;
+            if (hit && id >= 0) fr[b + __popc(pi & below)] = id;
+            if (hit && id < 0) {
+                const int q = nc + __popc(pl & below);
+                if (q < cap_cand) cand[q] = -id - 1;
+            }
+            nc += __popc(pl);
+            if (nc > cap_cand) return -1;
+            sp = b + np;
+            __syncwarp();
+        }
+        return 0;
+    }
     // Two levels per round: up to 8 frontier nodes, 4 lanes each (lane = 4 f + 2 c + g): lane
     // (c, g) tests grandchild g of child c directly (a leaf child: its own box, g == 0). A
     // parent's box is the union of its children's, so a ray that hits a grandchild box hits its
@@ -578,13 +616,7 @@ __device__ __forceinline__ int warp_bvh_leaves(const BvhDev &bvh, V3 o, V3 d, in
         bool test = false;
         int id = 0;
         float lx = 0.f, ly = 0.f, lz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
-        if (act && bvh.wide) {  // the node's grandchild slots in one 128-byte record (k_bvh_widen)
-            const float4 *ws = bvh.wide[node].s + 2 * (lane & 3);
-            const float4 sa = ws[0], sb = ws[1];
-            lx = sa.x, ly = sa.y, lz = sa.z, hx = sa.w, hy = sb.x, hz = sb.y;
-            id = __float_as_int(sb.z);
-            test = sb.w != 0.0f;
-        } else if (act) {
+        if (act) {
             const BvhNode n = bvh.nodes[node];
             const int child = c ? n.d.y : n.d.x;
             if (child < 0) {
