@@ -185,7 +185,8 @@ struct vp_ctx {
     int bwd_v4 = -1;
     // BVH over the resident transforms for arbitrary rays, rebuilt lazily after a pose change
     DBuf<BvhNode> bvh_nodes;
-    DBuf<BvhWide> bvh_wide;  // the same hierarchy two levels per record (warp walks)
+    DBuf<BvhWide> bvh_wide;  // the same hierarchy three levels per record (warp walks)
+    int bvh_built_n = 0, bvh_refits = 0;  // the topology in bvh_scratch: primitives, refits since
     // vp_render_async into host memory: two device output slots; the device->host copy of
     // one view (copy_stream) overlaps the rendering of the next
     cudaStream_t copy_stream = nullptr;
@@ -271,8 +272,19 @@ int ensure_bvh(vp_ctx *ctx, MarchDev &mp) {
         VP_CUDA(ctx, ctx->bvh_wide.ensure(size_t(n - 1)));
         const size_t bytes = bvh_scratch_bytes(n);
         VP_CUDA(ctx, ctx->bvh_scratch.ensure(bytes));
-        VP_CUDA(ctx, launch_bvh_build(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_wide.p, ctx->bvh_scratch.p, bytes,
-                                      ctx->stream));
+        // A pose change (an Adam step, a new frame of the same primitives) refits the last
+        // build's topology; the Morton order and hierarchy are rebuilt every kBvhRefits poses
+        constexpr int kBvhRefits = 16;
+        if (ctx->bvh_built_n == n && ctx->bvh_refits < kBvhRefits) {
+            VP_CUDA(ctx, launch_bvh_refit(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_wide.p,
+                                          ctx->bvh_scratch.p, bytes, ctx->stream));
+            ++ctx->bvh_refits;
+        } else {
+            VP_CUDA(ctx, launch_bvh_build(ctx->xfb[ctx->xfi].p, n, ctx->bvh_nodes.p, ctx->bvh_wide.p,
+                                          ctx->bvh_scratch.p, bytes, ctx->stream));
+            ctx->bvh_built_n = n;
+            ctx->bvh_refits = 0;
+        }
     }
     ctx->bvh_dirty = false;
     mp.bvh = BvhDev{ctx->bvh_nodes.p, n, ctx->bvh_wide.p};
@@ -534,6 +546,7 @@ int ctx_scene(vp_ctx *ctx, CtxScene *out) {
 int ctx_scene_written(vp_ctx *ctx, cudaStream_t st) {
     ctx->has_xf = true;
     ctx->bvh_dirty = true;
+    ctx->bvh_built_n = 0;  // a new scene: rebuild the BVH topology, not just refit it
     ctx->pairs_dirty = true;
     // The writer's work may not be enqueued yet (a broadcast inside a caller's NCCL group is
     // launched at vp_group_end), so the context waits for `st` when it next uses the scene
@@ -943,6 +956,7 @@ int vp_set_scene(vp_ctx *ctx, int32_t n_prim, int32_t m, const float *xf15,
     if (n_prim > 0 && m < 1) return fail(ctx, VP_ERR_USAGE, "voxels per axis must be >= 1");
     if (!std::isfinite(window_alpha)) return fail(ctx, VP_ERR_USAGE, "window alpha must be finite");
     ctx->has_scene = false;
+    ctx->bvh_built_n = 0;  // a new scene: rebuild the BVH topology, not just refit it
     ctx->n_prim = n_prim;
     ctx->m = m;
     ctx->w_alpha = window_alpha;

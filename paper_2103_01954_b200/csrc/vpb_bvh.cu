@@ -491,6 +491,23 @@ __global__ void k_bvh_widen(const BvhNode *__restrict__ nodes, int n_internal, B
     wide[i] = w;
 }
 
+// New boxes in the topology of the last launch_bvh_build over the same n primitives (its sorted
+// keys and parent links are still in the scratch): the leaves' boxes from the current
+// transforms, then the bottom-up refit and the wide records. The hierarchy stays exact (every
+// box bounds its subtree), so walks find the same leaves; only its quality ages.
+cudaError_t launch_bvh_refit(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
+                             size_t scratch_bytes, cudaStream_t st) {
+    if (n <= 1) return cudaSuccess;
+    const BvhScratch sc = bvh_layout(n, scratch);
+    if (sc.total > scratch_bytes) return cudaErrorInvalidValue;
+    const int b = (n + 255) / 256;
+    k_bvh_boxes<<<b, 256, 0, st>>>(xf16, n, sc.lo, sc.hi);
+    cudaMemsetAsync(sc.flags, 0, (size_t)n * 4, st);
+    k_bvh_refit<<<b, 256, 0, st>>>(sc.k0, n, sc.lo, sc.hi, nodes, sc.nlo, sc.nhi, sc.parent, sc.flags);
+    if (wide) k_bvh_widen<<<(n - 1 + 255) / 256, 256, 0, st>>>(nodes, n - 1, wide);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
                              size_t scratch_bytes, cudaStream_t st) {
     if (n <= 1) return cudaSuccess;

@@ -267,6 +267,8 @@ cudaError_t launch_pose36(const float *tr24, int n_prim, float *p36, cudaStream_
 size_t bvh_scratch_bytes(int n);
 cudaError_t launch_bvh_build(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
                              size_t scratch_bytes, cudaStream_t st);
+cudaError_t launch_bvh_refit(const float *xf16, int n, BvhNode *nodes, BvhWide *wide, void *scratch,
+                             size_t scratch_bytes, cudaStream_t st);
 // the BVH's stable radix sort on key bits [32, 62) (testing); hist: 256 * ceil(n / 2048) words
 cudaError_t launch_radix_sort30(unsigned long long *keys, unsigned long long *tmp, unsigned *hist, int n,
                                 cudaStream_t st);
