@@ -167,7 +167,10 @@ struct vp_ctx {
     DBuf<int> bp_fb, bp_tiles;
     size_t pair_cap = 0;
     bool pair_cap_fixed = false;
-    bool bwd_warp_walk = false;  // VPB_BWD_MODE=warp: the warp-per-ray walk for every ray (A/B)
+    // backward path: 1 the warp-per-ray walk for every ray, 0 the passes over primitive-samples
+    // (K6a-c), -1 auto (K6a-c from kPairsMinRays rays: below, its per-ray passes leave the GPU
+    // mostly idle and the one-kernel walk is quicker); VPB_BWD_MODE=warp|pairs
+    int bwd_warp_walk = -1;
     // host slab uploads (upload_planar_host): page-locked + device staging chunks, their
     // transfer events, and the host copy threads
     static constexpr int kStageSlots = 4;
@@ -590,7 +593,7 @@ int vp_create(int32_t device, vp_ctx **out) {
     if (const char *bl = std::getenv("VPB_BWD_LAYOUT"))  // A/B: "v4" = interleaved + vector reductions
         ctx->bwd_v4 = std::strcmp(bl, "v4") == 0 ? 1 : std::strcmp(bl, "planar") == 0 ? 0 : -1;
     if (const char *bm = std::getenv("VPB_BWD_MODE"))  // A/B: "warp" = the warp-per-ray walk for every ray
-        ctx->bwd_warp_walk = std::strcmp(bm, "warp") == 0;
+        ctx->bwd_warp_walk = std::strcmp(bm, "warp") == 0 ? 1 : std::strcmp(bm, "pairs") == 0 ? 0 : -1;
     if (const char *pc = std::getenv("VPB_BWD_PAIR_CAP")) {  // tests: a fixed (small) pair capacity
         ctx->pair_cap = size_t(std::strtoull(pc, nullptr, 10));
         ctx->pair_cap_fixed = true;
@@ -1464,9 +1467,9 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     }
     // v4: the payload gradient is scattered channel-interleaved (one 16-byte reduction per
     // corner) into ctx->g_pay4, kept zeroed between calls, then transposed into dg
-    constexpr int64_t kV4MinRays = 16384;
-    const bool v4 = k > 0 && n_rays > 0 &&
-                    (ctx->bwd_v4 == 1 || (ctx->bwd_v4 < 0 && !ctx->bwd_warp_walk && n_rays >= kV4MinRays));
+    constexpr int64_t kV4MinRays = 16384, kPairsMinRays = 8192;
+    const bool pairs = ctx->bwd_warp_walk == 0 || (ctx->bwd_warp_walk < 0 && n_rays >= kPairsMinRays);
+    const bool v4 = k > 0 && n_rays > 0 && (ctx->bwd_v4 == 1 || (ctx->bwd_v4 < 0 && pairs && n_rays >= kV4MinRays));
     if (v4) {
         if (ctx->g_pay4.n < n_pay) {
             VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
@@ -1550,7 +1553,6 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
         BwdPairs bp{};
-        const bool pairs = !ctx->bwd_warp_walk;
         if (pairs) {
             if (!ctx->pair_cap_fixed) ctx->pair_cap = std::max(ctx->pair_cap, std::max<size_t>(size_t(1) << 20, 64 * n));
             const size_t cap = std::max<size_t>(ctx->pair_cap, 1);

@@ -133,16 +133,16 @@ def test_rays_with_more_live_segments_than_the_fallback_window(renderer, oracle,
     _check_close("huge.pose", got[n_pay:], want[n_pay:])
 
 
-@pytest.mark.parametrize("mode", ["warp", "cap64"])
+@pytest.mark.parametrize("mode", ["warp", "pairs", "cap64"])
 def test_backward_paths_agree(monkeypatch, mode):
-    """The default backward runs as passes over primitive-samples (K6a plan, K6b one sample per
-    thread, K6c per-ray fold). The warp-per-ray walk is the same adjoint, used for rays that
-    find no room in the pair arrays: forced for every ray (VPB_BWD_MODE=warp) or for most of
-    them (a 64-sample capacity). Both equal the reference within the reordering bound."""
+    """Batches of 8,192 rays or more run the backward as passes over primitive-samples (K6a
+    plan, K6b one sample per thread, K6c per-ray fold); smaller ones take the warp-per-ray walk,
+    which is also the path for rays that find no room in the pair arrays. Each path forced on
+    the golden cases (VPB_BWD_MODE), and the pairs with a 64-sample capacity (most rays spill
+    to the walk): all equal the reference within the reordering bound."""
     from paper_2103_01954_b200 import Renderer
-    if mode == "warp":
-        monkeypatch.setenv("VPB_BWD_MODE", "warp")
-    else:
+    monkeypatch.setenv("VPB_BWD_MODE", "warp" if mode == "warp" else "pairs")
+    if mode == "cap64":
         monkeypatch.setenv("VPB_BWD_PAIR_CAP", "64")
     r = Renderer(0)
     try:
@@ -197,9 +197,10 @@ def test_large_batch_interleaved_gradient_any_alignment(renderer):
     _check_close("unaligned.pose", got[n_pay:], want[n_pay:])
 
 
+@pytest.mark.parametrize("mode", ["pairs", "warp"])
 @pytest.mark.parametrize("seed", [11, 12, 13])
-def test_random_scenes_backward_matches_restatement(renderer, oracle, seed):
-    """Randomized scenes and rays through K6a-c: sparse clouds (rays with gaps between their
+def test_random_scenes_backward_matches_restatement(monkeypatch, oracle, seed, mode):
+    """Randomized scenes and rays through both backward paths (K6a-c and the warp walk): sparse clouds (rays with gaps between their
     segments, so the walk takes gap skips), dense ones (several live entries per step, step-major
     slots that interleave entries), saturating and unsaturated rays, jitter. Gradients within
     the reordering bound of the restatement's sequential backwardRay."""
@@ -214,6 +215,9 @@ def test_random_scenes_backward_matches_restatement(renderer, oracle, seed):
     win = api.WindowParams()
     cfg = api.MarchConfig(step_size=0.004, jitter=seed == 13, seed=seed)
     xf = api.compose(tr)
+    from paper_2103_01954_b200 import Renderer
+    monkeypatch.setenv("VPB_BWD_MODE", mode)
+    renderer = Renderer(0)
     renderer.set_scene_composed(xf, api.PrimitiveSlab(k, m, pay), win)
     n = 512
     o = np.tile(np.float32([0.05, -0.03, -2.0]), (n, 1)) + rng.uniform(-0.02, 0.02, (n, 3)).astype(np.float32)
@@ -223,7 +227,10 @@ def test_random_scenes_backward_matches_restatement(renderer, oracle, seed):
     jit = rng.uniform(0, 1, n).astype(np.float32) if cfg.jitter else None
     ar = rng.normal(size=(n, 3)).astype(np.float32)
     aa = rng.normal(size=n).astype(np.float32)
-    got = renderer.backward_rays(o, d, ar, aa, cfg, tr, jit)
+    try:
+        got = renderer.backward_rays(o, d, ar, aa, cfg, tr, jit)
+    finally:
+        renderer.close()
     want = oracle.backward_rays(tr, m, pay, win, o, d, ar, aa, cfg, jit)
     n_pay = k * 4 * m ** 3
     _check_close(f"rand{seed}.payload", got[:n_pay], want[:n_pay])
