@@ -193,6 +193,8 @@ struct vp_ctx {
     // vp_render_async into host memory: two device output slots; the device->host copy of
     // one view (copy_stream) overlaps the rendering of the next
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;  // the backward's K6c beside the transpose
+    cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
     cudaEvent_t ev_rendered[2] = {}, ev_copied[2] = {};
     DBuf<float> ring_rgb[2], ring_alpha[2];
     DBuf<int> ring_samples[2];
@@ -673,6 +675,12 @@ int vp_destroy(vp_ctx *ctx) {
         if (ctx->ev_copied[q]) cudaEventDestroy(ctx->ev_copied[q]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->aux_stream) {
+        cudaStreamSynchronize(ctx->aux_stream);
+        cudaStreamDestroy(ctx->aux_stream);
+    }
+    if (ctx->ev_aux_fork) cudaEventDestroy(ctx->ev_aux_fork);
+    if (ctx->ev_aux_join) cudaEventDestroy(ctx->ev_aux_join);
     ctx->tr24.release();
     for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_bwd_fwd, &ctx->s_adam})
         b->release();
@@ -1553,6 +1561,15 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
         BwdPairs bp{};
+        bool aux_ok = false;
+        if (pairs) {
+            if (!ctx->aux_stream) {
+                VP_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_fork, cudaEventDisableTiming));
+                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_join, cudaEventDisableTiming));
+            }
+            aux_ok = true;
+        }
         if (pairs) {
             if (!ctx->pair_cap_fixed) ctx->pair_cap = std::max(ctx->pair_cap, std::max<size_t>(size_t(1) << 20, 64 * n));
             const size_t cap = std::max<size_t>(ctx->pair_cap, 1);
@@ -1568,10 +1585,12 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         VP_CUDA(ctx, launch_backward_rays(mp, ctx->xfb[ctx->xfi].p, k, ctx->payload.p, rays, n_rays,
                                           bd, ctx->d_ctr, ctx->bwd_list.p, int(n), ctx->fb_e.p, ctx->fb_x.p,
                                           ctx->fb_c.p, st, ctx->huge_ray_list.p, kHugeListCap, ctx->hg_e.p,
-                                          ctx->hg_x.p, ctx->hg_c.p, pairs ? &bp : nullptr));
+                                          ctx->hg_x.p, ctx->hg_c.p, pairs ? &bp : nullptr, aux_ok ? ctx->aux_stream : nullptr,
+                                          ctx->ev_aux_fork, ctx->ev_aux_join));
         if (v4)
             VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(ctx->g_pay4.p), dg, ctx->g_touched.p, k,
                                                unsigned(size_t(m) * m * m), accumulate != 0, st));
+        if (aux_ok) VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));  // K6c joins
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
     }
     if (!d_grads) VP_CUDA(ctx, cudaMemcpyAsync(grads, dg, n_grad * 4, cudaMemcpyDeviceToHost, st));

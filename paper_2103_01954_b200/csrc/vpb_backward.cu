@@ -1282,7 +1282,8 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
                                  float *sx, int *sc, cudaStream_t st, int *huge_list, int huge_cap, float *he,
-                                 float *hx, int *hc, const BwdPairs *pairs) {
+                                 float *hx, int *hc, const BwdPairs *pairs, cudaStream_t st2, cudaEvent_t ev_fork,
+                                 cudaEvent_t ev_join) {
     if (n_rays == 0 || n_prim == 0) return cudaSuccess;
     // The adjoint walk goes warp-per-ray for every batch size (the forward's state and segment
     // lists are required): one ray per thread leaves 27 % of the lanes busy (the rays' walks
@@ -1299,7 +1300,16 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
         k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
         k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
         const int64_t tb = (n_rays + 127) / 128;
-        k_bwd_fold<<<(unsigned)(tb < 148 * 16 ? tb : 148 * 16), 128, 0, st>>>(xf16, rays, n_rays, bd, *pairs);
+        // K6c reads only K6b's rotG and writes pose reductions: it runs beside the walk for the
+        // spilled rays and the gradient transpose (the caller joins ev_join)
+        cudaStream_t sf = st;
+        if (st2 && ev_fork && ev_join) {
+            cudaEventRecord(ev_fork, st);
+            cudaStreamWaitEvent(st2, ev_fork, 0);
+            sf = st2;
+        }
+        k_bwd_fold<<<(unsigned)(tb < 148 * 16 ? tb : 148 * 16), 128, 0, sf>>>(xf16, rays, n_rays, bd, *pairs);
+        if (sf != st) cudaEventRecord(ev_join, sf);
         // the rays that found no room in the pair arrays (none once the capacity has grown)
         k_backward_rays_warp<<<(unsigned)(blocks < 148 * 4 ? blocks : 148 * 4), 128, 0, st>>>(
             mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, pairs->fb_list);

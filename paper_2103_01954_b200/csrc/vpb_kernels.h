@@ -236,13 +236,15 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
                               cudaStream_t st);
 // K6: needs bd.fwd_state and bd.fwd_segs (the forward of the same rays, k_march_rays_warp);
 // ray_list (list_cap entries) collects the rays whose lists the forward could not keep.
-// pairs: the K6a-c workspace; null runs the warp-per-ray walk over every ray.
+// pairs: the K6a-c workspace; null runs the warp-per-ray walk over every ray. With st2 and
+// both events, K6c runs on st2 after ev_fork; the caller makes st wait for ev_join.
 cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_prim,
                                  const float4 *payload, const RaysDev &rays, int64_t n_rays,
                                  const BwdDev &bd, DevCounters *ctr, int *ray_list, int list_cap, float *se,
                                  float *sx, int *sc, cudaStream_t st, int *huge_list = nullptr, int huge_cap = 0,
                                  float *he = nullptr, float *hx = nullptr, int *hc = nullptr,
-                                 const BwdPairs *pairs = nullptr);
+                                 const BwdPairs *pairs = nullptr, cudaStream_t st2 = nullptr,
+                                 cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr);
 // vpb_backward.cu: interleaved payload gradient -> planar GradBuffer (touched primitives)
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
                                   bool accumulate, cudaStream_t st);
