@@ -75,7 +75,10 @@ struct NvtxRange {
     explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
     ~NvtxRange() { nvtxRangePop(); }
 };
-constexpr size_t kStageBytes = size_t(8) << 20;  // host slab upload chunk (upload_planar_host)
+#ifndef VPB_STAGE_MB
+#define VPB_STAGE_MB 8
+#endif
+constexpr size_t kStageBytes = size_t(VPB_STAGE_MB) << 20;  // host slab upload chunk (upload_planar_host)
 
 }  // namespace
 
