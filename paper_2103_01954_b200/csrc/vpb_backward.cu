@@ -1,19 +1,21 @@
 // vpb_backward.cu — K6, the backward pass: backwardRay (grad.cpp:34-195) for a batch of rays.
 //
-// Per ray (one thread, grid-stride over the batch):
-//   1. the exact segment window (intersect over all primitives, lbvh.cpp:207-234);
-//   2. a bit-exact replay of march() recording the MarchResult bookkeeping the adjoints need
-//      (lastStep, saturated, satTPrev, satSigmaSum, satRgbWeighted; march.h:22-33);
-//   3. the adjoint walk over steps 0..lastStep (grad.cpp:66-164): per primitive-sample the
-//      colour/opacity adjoints, the payload scatter over 8 corners x 4 channels, the spatial
-//      gradient through the trilinear stencil and the fade window, and the pose Jacobians
-//      (deltaT, deltaS, deltaR via rotationDerivative);
-//   4. the t_min anchor chain onto the first-hit primitive (grad.cpp:166-194).
-// Every per-sample value is computed with the reference's operation order (same bits); the
-// global sums use device atomics (RED.ADD.F32), so only their summation order differs from
-// the reference's sequential loop. Pose gradients are first summed in registers over each
-// run of consecutive samples of the same primitive along the ray (a segment usually spans
-// tens of steps), cutting pose atomics by about an order of magnitude.
+// backwardRay per ray: (1) the ray's sorted segment list (intersect, lbvh.cpp:207-234) and
+// (2) march()'s bookkeeping the adjoints need (lastStep, saturated, satTPrev, satSigmaSum,
+// satRgbWeighted; march.h:22-33) come from the forward march of the same rays
+// (k_march_rays_warp keeps them); (3) the adjoint walk over steps 0..lastStep (grad.cpp:66-164):
+// per primitive-sample the colour/opacity adjoints, the payload scatter over 8 corners x 4
+// channels, the spatial gradient through the stencil and the fade window, and the pose
+// Jacobians (deltaT, deltaS, deltaR via rotationDerivative); (4) the t_min anchor chain onto the
+// first-hit primitive (grad.cpp:166-194).
+//
+// Paths: batches of >= 8,192 rays run K6a-c, passes over primitive-samples (k_bwd_plan,
+// k_bwd_scan_*, k_bwd_records, k_bwd_pairs, k_bwd_fold); smaller batches, and rays that find no
+// room in the pair arrays, the warp-per-ray walk (k_backward_rays_warp); rays the forward could
+// not keep a list for, the per-thread walks (k_backward_rays_list / _huge).
+// Every per-sample value is computed with the reference's operation order (same bits), and so
+// is gTmin; the global sums use device reductions, so only their summation order differs from
+// the reference's sequential loop.
 #include <cuda_runtime.h>
 
 #include <cstdint>
