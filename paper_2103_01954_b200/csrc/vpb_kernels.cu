@@ -621,6 +621,7 @@ constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp pa
 #ifndef VPB_RAYS_MINB
 #define VPB_RAYS_MINB 5
 #endif
+template <int MT>
 __global__ void __launch_bounds__(128, VPB_RAYS_MINB)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
@@ -651,7 +652,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
                 if (slot < ovf_cap) ovf_list[slot] = (int)r;
             }
         } else {
-            ro = march_warp(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane, s_sv[wid]);
+            ro = march_warp<BvhCands, MT>(cands, s_e[wid], s_x[wid], s_c[wid], cnt, o, d, jit, mp, s_tab, lane, s_sv[wid]);
             if (lane == 0) write_ray(od, r, ro);
             if (od.segs) {  // keep the list for the backward pass of the same rays
                 float *sg = od.segs + (size_t)r * (3 * kRaySegs);
@@ -1228,8 +1229,13 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
     // every batch size measured (65,536 rays: 1.05 -> 0.7 ms against one thread per ray, a
     // kernel since removed).
     const int64_t blocks = (n_rays + 3) / 4;
-    k_march_rays_warp<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(
-        mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap);
+    const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+    switch (mp.m) {  // compile-time voxel counts for the common grids (immediate corner offsets)
+    case 8: k_march_rays_warp<8><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
+    case 16: k_march_rays_warp<16><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
+    case 32: k_march_rays_warp<32><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
+    default: k_march_rays_warp<0><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
+    }
     return cudaGetLastError();
 }
 

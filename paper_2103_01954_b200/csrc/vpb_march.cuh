@@ -755,7 +755,7 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
 #ifndef VPB_FWD_PAIRS
 #define VPB_FWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
 #endif
-template <class Cands>
+template <class Cands, int MT = 0>
 __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X, const int *P, int cnt, V3 o,
                              V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane,
                              float *sv) {
@@ -819,7 +819,7 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
                 const int c = P[j];
                 float sg, r, g, b;
                 const Xf16 xr = cands.xfv(c);
-                sample_primitive<0>(cands.base(c), mp.m, xr.v, o + d * tsp, mp.alpha, mp.beta, tab, sg, r, g, b);
+                sample_primitive<MT>(cands.base(c), mp.m, xr.v, o + d * tsp, mp.alpha, mp.beta, tab, sg, r, g, b);
                 a[0] = sg;
                 a[1] = r * sg;
                 a[2] = g * sg;
