@@ -197,6 +197,8 @@ struct vp_ctx {
     // one view (copy_stream) overlaps the rendering of the next
     cudaStream_t copy_stream = nullptr;
     cudaStream_t aux_stream = nullptr;  // the backward's K6c beside the transpose
+    float *h_loss = nullptr;  // evalLoss: page-locked staging of host ray-batch inputs
+    size_t h_loss_floats = 0;
     cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
     cudaEvent_t ev_rendered[2] = {}, ev_copied[2] = {};
     DBuf<float> ring_rgb[2], ring_alpha[2];
@@ -684,6 +686,7 @@ int vp_destroy(vp_ctx *ctx) {
     }
     if (ctx->ev_aux_fork) cudaEventDestroy(ctx->ev_aux_fork);
     if (ctx->ev_aux_join) cudaEventDestroy(ctx->ev_aux_join);
+    if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
     ctx->tr24.release();
     for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_bwd_fwd, &ctx->s_adam})
         b->release();
@@ -1676,12 +1679,35 @@ int vp_eval_loss_pho(vp_ctx *ctx, int32_t n_cams, const vp_camera *cams, int64_t
     float *d_state = p; p += 8 * nn;  // forward MarchResult bookkeeping for the backward
     float *d_segs = n_seg ? p : nullptr; p += n_seg * nn;
     int *d_bad = reinterpret_cast<int *>(p);
-    VP_CUDA(ctx, cudaMemcpyAsync(d_cams, cd.data(), sizeof(CamDev) * cd.size(), cudaMemcpyHostToDevice, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_ci, cam_index, 4 * nn, cudaMemcpyDefault, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_pid, pixel_id, 4 * nn, cudaMemcpyDefault, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_xy, pixel_xy, 8 * nn, cudaMemcpyDefault, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_tg, target, 12 * nn, cudaMemcpyDefault, st));
-    VP_CUDA(ctx, cudaMemcpyAsync(d_bg, background, 12 * nn, cudaMemcpyDefault, st));
+    const bool host_in = host_check && !is_device_ptr(pixel_id) && !is_device_ptr(target) &&
+                         !is_device_ptr(background);
+    if (host_in) {
+        // host inputs packed into one page-locked block in the device layout, one transfer
+        // (six pageable copies each paid the driver's staging)
+        const size_t in_f = size_t(d_bg + 3 * nn - buf.p);
+        if (ctx->h_loss_floats < in_f) {
+            if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
+            ctx->h_loss = nullptr;
+            ctx->h_loss_floats = 0;
+            VP_CUDA(ctx, cudaMallocHost(&ctx->h_loss, in_f * sizeof(float)));
+            ctx->h_loss_floats = in_f;
+        }
+        float *h = ctx->h_loss;
+        std::memcpy(h, cd.data(), sizeof(CamDev) * cd.size());
+        std::memcpy(h + (d_ci - reinterpret_cast<int *>(buf.p)), cam_index, 4 * nn);
+        std::memcpy(h + (d_pid - reinterpret_cast<int *>(buf.p)), pixel_id, 4 * nn);
+        std::memcpy(h + (d_xy - buf.p), pixel_xy, 8 * nn);
+        std::memcpy(h + (d_tg - buf.p), target, 12 * nn);
+        std::memcpy(h + (d_bg - buf.p), background, 12 * nn);
+        VP_CUDA(ctx, cudaMemcpyAsync(buf.p, h, in_f * sizeof(float), cudaMemcpyHostToDevice, st));
+    } else {
+        VP_CUDA(ctx, cudaMemcpyAsync(d_cams, cd.data(), sizeof(CamDev) * cd.size(), cudaMemcpyHostToDevice, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(d_ci, cam_index, 4 * nn, cudaMemcpyDefault, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(d_pid, pixel_id, 4 * nn, cudaMemcpyDefault, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(d_xy, pixel_xy, 8 * nn, cudaMemcpyDefault, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(d_tg, target, 12 * nn, cudaMemcpyDefault, st));
+        VP_CUDA(ctx, cudaMemcpyAsync(d_bg, background, 12 * nn, cudaMemcpyDefault, st));
+    }
     VP_CUDA(ctx, cudaMemsetAsync(d_bad, 0, 4, st));
     VP_CUDA(ctx, launch_eval_rays(d_cams, n_cams, d_ci, d_xy, d_pid, n, cfg->jitter, cfg->seed, d_o, d_d, d_j,
                                   d_bad, st));
