@@ -179,6 +179,9 @@ def test_large_batch_interleaved_gradient_any_alignment(renderer):
     n_pay = k * 4 * m ** 3
     _check_close("aligned.payload", host[:n_pay], want[:n_pay])
     _check_close("aligned.pose", host[n_pay:], want[n_pay:])
+    # accumulating into a caller's buffer (the transpose adds instead of writing)
+    acc = renderer.backward_rays(o, d, ar, aa, cfg, g["tr"], jit, grads=host.copy())
+    _check_close("accumulated", acc, 2 * want)
     lib = _lib.load()
     f32p = C.POINTER(C.c_float)
     P = lambda t: C.cast(C.c_void_p(t.data_ptr()), f32p)  # noqa: E731
