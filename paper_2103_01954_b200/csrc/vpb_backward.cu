@@ -589,6 +589,12 @@ constexpr int kWarpListBwd = kRaySegs;
 #ifndef VPB_BWD_PAIRS
 #define VPB_BWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
 #endif
+#ifndef VPB_BWD_RAY_GRID
+#define VPB_BWD_RAY_GRID 64  // CTAs per SM of the warp-per-ray passes (K6a walk, records; 16 -> 64: +1.5 %)
+#endif
+#ifndef VPB_BWD_PAIR_GRID
+#define VPB_BWD_PAIR_GRID 32  // CTAs per SM of K6b (samples grid-strided; 8 -> 32: +0.8 %, 128: -4 %)
+#endif
 #ifndef VPB_BWD_PAIRS_MINB
 #define VPB_BWD_PAIRS_MINB 3  // 80 registers (12 B of spills): 1.50 vs 1.52 ms for the backward row
 #endif
@@ -1293,14 +1299,14 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
     if (!bd.fwd_state || !bd.fwd_segs) return cudaErrorInvalidValue;
     const int64_t blocks = (n_rays + 3) / 4;
     if (pairs) {
-        const unsigned ray_blocks = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);  // a warp per ray
+        const unsigned ray_blocks = (unsigned)(blocks < 148 * VPB_BWD_RAY_GRID ? blocks : 148 * VPB_BWD_RAY_GRID);
         k_bwd_plan<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr, ray_list, list_cap, huge_list,
                                                huge_cap);
         const int64_t n_tiles = (n_rays + kScanTile - 1) / kScanTile;
         k_bwd_scan_tiles<<<(unsigned)n_tiles, 1024, 0, st>>>(n_rays, *pairs, ctr);
         if (n_tiles > 1) k_bwd_scan_top<<<1, 1024, 0, st>>>((int)n_tiles, *pairs, ctr);
         k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
-        k_bwd_pairs<<<148 * 8, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
+        k_bwd_pairs<<<148 * VPB_BWD_PAIR_GRID, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
         const int64_t tb = (n_rays + 127) / 128;
         // K6c reads only K6b's rotG and writes pose reductions: it runs beside the walk for the
         // spilled rays and the gradient transpose (the caller joins ev_join)
