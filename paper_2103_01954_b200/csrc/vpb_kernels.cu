@@ -619,10 +619,10 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
 constexpr int kWarpList = kRaySegs;  // segments per ray held by the warp
 constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp path gives up
 #ifndef VPB_RAYS_MINB
-#define VPB_RAYS_MINB 5
+#define VPB_RAYS_MINB 7  // 72 registers, no spills (5: 58.4M, 6: 59.4M, 7: 60.0M, 8 spills: 60.0M backward rays/s)
 #endif
-template <int MT>
-__global__ void __launch_bounds__(128, VPB_RAYS_MINB)
+template <int MT>  // a runtime voxel count needs more registers: two CTAs fewer per SM instead of spills
+__global__ void __launch_bounds__(128, MT == 0 && VPB_RAYS_MINB > 2 ? VPB_RAYS_MINB - 2 : VPB_RAYS_MINB)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
                   int ovf_cap) {
