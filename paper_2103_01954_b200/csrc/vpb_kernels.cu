@@ -621,8 +621,11 @@ constexpr int kWarpCand = 256;  // BVH leaves a ray may cross before the warp pa
 #ifndef VPB_RAYS_MINB
 #define VPB_RAYS_MINB 7  // 72 registers, no spills (5: 58.4M, 6: 59.4M, 7: 60.0M, 8 spills: 60.0M backward rays/s)
 #endif
-template <int MT>  // a runtime voxel count needs more registers: two CTAs fewer per SM instead of spills
-__global__ void __launch_bounds__(128, MT == 0 && VPB_RAYS_MINB > 2 ? VPB_RAYS_MINB - 2 : VPB_RAYS_MINB)
+// MINB: CTAs per SM. Large batches run at VPB_RAYS_MINB (more rays in flight); small ones (a
+// single wave) at 5, where the extra registers shorten each ray's chain (evalLoss's 2,048 rays:
+// 0.365 vs 0.38 ms); a runtime voxel count needs the registers too (no spills at 5).
+template <int MT, int MINB>
+__global__ void __launch_bounds__(128, MINB)
 k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   RaysDev rays, int64_t n_rays, OutDev od, DevCounters *ctr, int *__restrict__ ovf_list,
                   int ovf_cap) {
@@ -1233,12 +1236,17 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
 #define VPB_RAYS_GRID 64  // CTAs per SM in the grid (16: 54.4M, 64: 56.8M, one ray per warp: 55.9M backward rays/s)
 #endif
     const unsigned grid = (unsigned)(blocks < 148 * VPB_RAYS_GRID ? blocks : 148 * VPB_RAYS_GRID);
+    const bool big = n_rays >= 8192;
+#define VPB_RAYS_LAUNCH(MT, MB)                                                                               \
+    k_march_rays_warp<MT, MB><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, \
+                                                    ovf_cap)
     switch (mp.m) {  // compile-time voxel counts for the common grids (immediate corner offsets)
-    case 8: k_march_rays_warp<8><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
-    case 16: k_march_rays_warp<16><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
-    case 32: k_march_rays_warp<32><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
-    default: k_march_rays_warp<0><<<grid, 128, 0, st>>>(mp, xf16, n_prim, payload, rays, n_rays, od, ctr, ovf_list, ovf_cap); break;
+    case 8: big ? VPB_RAYS_LAUNCH(8, VPB_RAYS_MINB) : VPB_RAYS_LAUNCH(8, 5); break;
+    case 16: big ? VPB_RAYS_LAUNCH(16, VPB_RAYS_MINB) : VPB_RAYS_LAUNCH(16, 5); break;
+    case 32: big ? VPB_RAYS_LAUNCH(32, VPB_RAYS_MINB) : VPB_RAYS_LAUNCH(32, 5); break;
+    default: VPB_RAYS_LAUNCH(0, 5); break;
     }
+#undef VPB_RAYS_LAUNCH
     return cudaGetLastError();
 }
 
