@@ -1496,16 +1496,6 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
     }
     if (k > 0 && n_rays > 0) {
-        // pose data on the device (k_pose36, the reference's operation order): rBase and
-        // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host]
-        VP_CUDA(ctx, pose.ensure(36 * size_t(k) + 24 * size_t(k)));
-        const float *d_tr = transforms24;
-        if (!is_device_ptr(transforms24)) {
-            VP_CUDA(ctx, cudaMemcpyAsync(pose.p + 36 * size_t(k), transforms24, 96 * size_t(k),
-                                         cudaMemcpyHostToDevice, st));
-            d_tr = pose.p + 36 * size_t(k);
-        }
-        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, st));
         const size_t n = size_t(n_rays);
         RaysDev rays{origins, dirs, jitter01};
         if (!is_device_ptr(origins)) {
@@ -1560,6 +1550,17 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             fwd_state = od.state;
             fwd_segs = od.segs;
         }
+        // pose data on the device (k_pose36, the reference's operation order): rBase and
+        // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host].
+        // Queued after the forward, so a pageable upload of the records overlaps it.
+        VP_CUDA(ctx, pose.ensure(36 * size_t(k) + 24 * size_t(k)));
+        const float *d_tr = transforms24;
+        if (!is_device_ptr(transforms24)) {
+            VP_CUDA(ctx, cudaMemcpyAsync(pose.p + 36 * size_t(k), transforms24, 96 * size_t(k),
+                                         cudaMemcpyHostToDevice, st));
+            d_tr = pose.p + 36 * size_t(k);
+        }
+        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, st));
         BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
         if (v4) {
             bd.g_pay4 = ctx->g_pay4.p;
