@@ -1484,17 +1484,23 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     constexpr int64_t kV4MinRays = 16384, kPairsMinRays = 8192;
     const bool pairs = ctx->bwd_warp_walk == 0 || (ctx->bwd_warp_walk < 0 && n_rays >= kPairsMinRays);
     const bool v4 = k > 0 && n_rays > 0 && (ctx->bwd_v4 == 1 || (ctx->bwd_v4 < 0 && pairs && n_rays >= kV4MinRays));
-    if (v4) {
-        if (ctx->g_pay4.n < n_pay) {
-            VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
-            VP_CUDA(ctx, cudaMemsetAsync(ctx->g_pay4.p, 0, n_pay * 4, st));
+    // the gradient buffers are cleared once the forward is queued (below), or here without rays
+    auto clear_grads = [&]() -> int {
+        if (v4) {
+            if (ctx->g_pay4.n < n_pay) {
+                VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
+                VP_CUDA(ctx, cudaMemsetAsync(ctx->g_pay4.p, 0, n_pay * 4, st));
+            }
+            VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
+            VP_CUDA(ctx, cudaMemsetAsync(ctx->g_touched.p, 0, 4 * size_t(k), st));
+            if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg + n_pay, 0, (n_grad - n_pay) * 4, st));
+        } else if (!accumulate) {
+            VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
         }
-        VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
-        VP_CUDA(ctx, cudaMemsetAsync(ctx->g_touched.p, 0, 4 * size_t(k), st));
-        if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg + n_pay, 0, (n_grad - n_pay) * 4, st));
-    } else if (!accumulate) {
-        VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
-    }
+        return VP_OK;
+    };
+    if (!(k > 0 && n_rays > 0))
+        if (int rc = clear_grads()) return rc;
     if (k > 0 && n_rays > 0) {
         const size_t n = size_t(n_rays);
         RaysDev rays{origins, dirs, jitter01};
@@ -1550,6 +1556,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             fwd_state = od.state;
             fwd_segs = od.segs;
         }
+        if (int rc = clear_grads()) return rc;
         // pose data on the device (k_pose36, the reference's operation order): rBase and
         // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host].
         // Queued after the forward, so a pageable upload of the records overlaps it.
