@@ -199,7 +199,7 @@ struct vp_ctx {
     cudaStream_t aux_stream = nullptr;  // the backward's K6c beside the transpose
     float *h_loss = nullptr;  // evalLoss: page-locked staging of host ray-batch inputs
     size_t h_loss_floats = 0;
-    cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr;
+    cudaEvent_t ev_aux_fork = nullptr, ev_aux_join = nullptr, ev_aux_pose = nullptr;
     cudaEvent_t ev_rendered[2] = {}, ev_copied[2] = {};
     DBuf<float> ring_rgb[2], ring_alpha[2];
     DBuf<int> ring_samples[2];
@@ -686,6 +686,7 @@ int vp_destroy(vp_ctx *ctx) {
     }
     if (ctx->ev_aux_fork) cudaEventDestroy(ctx->ev_aux_fork);
     if (ctx->ev_aux_join) cudaEventDestroy(ctx->ev_aux_join);
+    if (ctx->ev_aux_pose) cudaEventDestroy(ctx->ev_aux_pose);
     if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
     ctx->tr24.release();
     for (auto *b : {&ctx->s_loss, &ctx->s_bwd_g, &ctx->s_bwd_pose, &ctx->s_bwd_adj, &ctx->s_bwd_fwd, &ctx->s_adam})
@@ -1532,6 +1533,17 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         ctx->last_n = 1;
         MarchDev mp = make_march(ctx, cfg);
         if (int rc = ensure_bvh(ctx, mp)) return rc;
+        // the auxiliary stream (the pose data beside the forward; K6c beside the transpose):
+        // ev_aux_pose marks the ray stream's work before the forward
+        if (pairs) {
+            if (!ctx->aux_stream) {
+                VP_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_fork, cudaEventDisableTiming));
+                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_join, cudaEventDisableTiming));
+                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_pose, cudaEventDisableTiming));
+            }
+            VP_CUDA(ctx, cudaEventRecord(ctx->ev_aux_pose, st));
+        }
         if (!fwd_state) {
             // forward march of the same rays first, recording the MarchResult bookkeeping, so
             // the backward kernel does not replay march() itself
@@ -1559,15 +1571,26 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         if (int rc = clear_grads()) return rc;
         // pose data on the device (k_pose36, the reference's operation order): rBase and
         // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host].
-        // Queued after the forward, so a pageable upload of the records overlaps it.
+        // Queued after the forward, on the auxiliary stream when there is one: it runs beside
+        // the forward (a pageable upload of the records included), and the ray stream waits for
+        // it before anything reads it.
+        cudaStream_t sp = st;
+        if (pairs) {
+            VP_CUDA(ctx, cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_aux_pose, 0));  // st before the forward
+            sp = ctx->aux_stream;
+        }
         VP_CUDA(ctx, pose.ensure(36 * size_t(k) + 24 * size_t(k)));
         const float *d_tr = transforms24;
         if (!is_device_ptr(transforms24)) {
             VP_CUDA(ctx, cudaMemcpyAsync(pose.p + 36 * size_t(k), transforms24, 96 * size_t(k),
-                                         cudaMemcpyHostToDevice, st));
+                                         cudaMemcpyHostToDevice, sp));
             d_tr = pose.p + 36 * size_t(k);
         }
-        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, st));
+        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
+        if (sp != st) {
+            VP_CUDA(ctx, cudaEventRecord(ctx->ev_aux_join, sp));
+            VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));
+        }
         BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
         if (v4) {
             bd.g_pay4 = ctx->g_pay4.p;
@@ -1575,15 +1598,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
         BwdPairs bp{};
-        bool aux_ok = false;
-        if (pairs) {
-            if (!ctx->aux_stream) {
-                VP_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
-                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_fork, cudaEventDisableTiming));
-                VP_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_aux_join, cudaEventDisableTiming));
-            }
-            aux_ok = true;
-        }
+        const bool aux_ok = pairs;
         if (pairs) {
             if (!ctx->pair_cap_fixed) ctx->pair_cap = std::max(ctx->pair_cap, std::max<size_t>(size_t(1) << 20, 64 * n));
             const size_t cap = std::max<size_t>(ctx->pair_cap, 1);

@@ -598,6 +598,9 @@ constexpr int kWarpListBwd = kRaySegs;
 #ifndef VPB_BWD_PAIR_GRID
 #define VPB_BWD_PAIR_GRID 32  // CTAs per SM of K6b (samples grid-strided; 8 -> 32: +0.8 %, 128: -4 %)
 #endif
+#ifndef VPB_BWD_PAIRS_NT
+#define VPB_BWD_PAIRS_NT 256  // threads per CTA of K6b
+#endif
 #ifndef VPB_BWD_PAIRS_MINB
 #define VPB_BWD_PAIRS_MINB 3  // 80 registers (12 B of spills): 1.50 vs 1.52 ms for the backward row
 #endif
@@ -1043,7 +1046,7 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
 // entry-major, so a warp's lanes form runs of one (ray, primitive); each run is summed with a
 // segmented shuffle scan and its last lane issues the nine reductions (SURVEY.md §8 a-20:
 // warp-aggregated atomics). rotG is kept for K6c's t_min chain (terms, step-major).
-__global__ void __launch_bounds__(256, VPB_BWD_PAIRS_MINB)
+__global__ void __launch_bounds__(VPB_BWD_PAIRS_NT, VPB_BWD_PAIRS_MINB)
 k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
             RaysDev rays, BwdDev bd, BwdPairs pp, const DevCounters *__restrict__ ctr) {
     __shared__ unsigned long long s_tab[32];
@@ -1309,7 +1312,7 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
         k_bwd_scan_tiles<<<(unsigned)n_tiles, 1024, 0, st>>>(n_rays, *pairs, ctr);
         if (n_tiles > 1) k_bwd_scan_top<<<1, 1024, 0, st>>>((int)n_tiles, *pairs, ctr);
         k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
-        k_bwd_pairs<<<148 * VPB_BWD_PAIR_GRID, 256, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
+        k_bwd_pairs<<<148 * VPB_BWD_PAIR_GRID, VPB_BWD_PAIRS_NT, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
         const int64_t tb = (n_rays + 127) / 128;
         // K6c reads only K6b's rotG and writes pose reductions: it runs beside the walk for the
         // spilled rays and the gradient transpose (the caller joins ev_join)
