@@ -784,6 +784,81 @@ __device__ __forceinline__ void route_long_ray(int nh, int64_t r, DevCounters *c
     }
 }
 
+// K6a's walk for one ray by its warp: the lattice walk of march.cpp:27-58 over the ray's segment
+// list E/X (admission, gap skip; steps 0..lastStep), 32 steps per round, without sampling.
+// Entry j is admitted at step A[j] (-1: never) and is live on the n_j consecutive steps from
+// there; OFF[j] is the exclusive prefix of n_j in entry order, OFF[nh] the total (returned).
+__device__ __forceinline__ int plan_ray_walk(int lane, const float *E, const float *X, int *A, int *OFF, int nh,
+                                             int lastStep, float jit, float dt) {
+    for (int j = lane; j < nh; j += 32) A[j] = -1;
+    __syncwarp();
+    const float t0 = E[0];
+    int base = 0, nadm_prev = 0;  // entries admitted before this round
+    for (;;) {
+        const int i = base + lane;
+        const bool valid = i <= lastStep;
+        const float ts = t0 + (__int2float_rn(i) + jit) * dt;
+        int na = 0, nadm = 0;
+        for (int j = 0; j < nh && valid; ++j) {
+            if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
+            nadm = j + 1;
+            na += X[j] > ts;
+        }
+        const unsigned empty = __ballot_sync(0xffffffffu, !(valid && na > 0));
+        const int L = empty ? __ffs(empty) - 1 : 32;
+        // the steps visited this round: s < L, and s == L when it is a real (empty) step
+        int before = __shfl_up_sync(0xffffffffu, nadm, 1);
+        if (lane == 0) before = nadm_prev;
+        if (valid && lane <= L)
+            for (int j = before; j < nadm; ++j) A[j] = base + lane;
+        if (L == 32) {
+            nadm_prev = __shfl_sync(0xffffffffu, nadm, 31);
+            base += 32;
+            if (base > lastStep) break;
+            continue;
+        }
+        const int iL = base + L;
+        if (iL > lastStep) break;
+        const int nadmL = __shfl_sync(0xffffffffu, nadm, L);
+        if (nadmL >= nh) break;  // nothing left to admit: march.cpp:43-44
+        nadm_prev = nadmL;
+        const double sk = ceil((double)((E[nadmL] - t0) / dt) - (double)jit);  // gap skip, march.cpp:45-49
+        const int skipTo = sk > (double)(1 << 30) ? (1 << 30) + 1 : (int)sk;
+        base = skipTo > iL + 1 ? skipTo : iL + 1;
+        if (base > lastStep) break;
+    }
+    __syncwarp();
+    // n_j (the live steps from a_j, up to lastStep), then offsets in entry order
+    int carry = 0;
+    for (int j0 = 0; j0 < nh; j0 += 32) {
+        const int j = j0 + lane;
+        int n = 0;
+        if (j < nh && A[j] >= 0) {
+            // e = the first step >= a_j with ts(e) >= X_j (or lastStep + 1): ts is
+            // nondecreasing in e, so start from the real-valued estimate and correct it
+            const int a = A[j];
+            const float x = X[j];
+            const double est = ceil((double)((x - t0) / dt) - (double)jit);
+            int e = est < (double)a ? a : est > (double)lastStep + 1.0 ? lastStep + 1 : (int)est;
+            while (e > a && t0 + (__int2float_rn(e - 1) + jit) * dt >= x) --e;
+            while (e <= lastStep && t0 + (__int2float_rn(e) + jit) * dt < x) ++e;
+            n = e - a;
+        }
+        int incl = n;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        if (j < nh) OFF[j] = carry + incl - n;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const int total = carry;
+    if (lane == 0) OFF[nh] = total;
+    __syncwarp();
+    return total;
+}
+
 // K6a, one warp per ray: the lattice walk of march.cpp:27-58 over the forward's segment list
 // (admission, gap skip; steps 0..lastStep), 32 steps per round as march_warp steps it, without
 // sampling. Entry j is admitted at step a_j and is live on the n_j consecutive steps from there
@@ -815,74 +890,10 @@ k_bwd_plan(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, De
         for (int j = lane; j < nh; j += 32) {
             E[j] = sg[j];
             X[j] = sg[kRaySegs + j];
-            A[j] = -1;
         }
         __syncwarp();
         const float jit = rays.jitter ? rays.jitter[r] : 0.5f;
-        const float t0 = E[0];
-        int base = 0, nadm_prev = 0;  // entries admitted before this round
-        for (;;) {
-            const int i = base + lane;
-            const bool valid = i <= lastStep;
-            const float ts = t0 + (__int2float_rn(i) + jit) * dt;
-            int na = 0, nadm = 0;
-            for (int j = 0; j < nh && valid; ++j) {
-                if (!(E[j] <= ts)) break;  // sorted by tEnter: the admitted entries are a prefix
-                nadm = j + 1;
-                na += X[j] > ts;
-            }
-            const unsigned empty = __ballot_sync(0xffffffffu, !(valid && na > 0));
-            const int L = empty ? __ffs(empty) - 1 : 32;
-            // the steps visited this round: s < L, and s == L when it is a real (empty) step
-            int before = __shfl_up_sync(0xffffffffu, nadm, 1);
-            if (lane == 0) before = nadm_prev;
-            if (valid && lane <= L)
-                for (int j = before; j < nadm; ++j) A[j] = base + lane;
-            if (L == 32) {
-                nadm_prev = __shfl_sync(0xffffffffu, nadm, 31);
-                base += 32;
-                if (base > lastStep) break;
-                continue;
-            }
-            const int iL = base + L;
-            if (iL > lastStep) break;
-            const int nadmL = __shfl_sync(0xffffffffu, nadm, L);
-            if (nadmL >= nh) break;  // nothing left to admit: march.cpp:43-44
-            nadm_prev = nadmL;
-            const double sk = ceil((double)((E[nadmL] - t0) / dt) - (double)jit);  // gap skip, march.cpp:45-49
-            const int skipTo = sk > (double)(1 << 30) ? (1 << 30) + 1 : (int)sk;
-            base = skipTo > iL + 1 ? skipTo : iL + 1;
-            if (base > lastStep) break;
-        }
-        __syncwarp();
-        // n_j (the live steps from a_j, up to lastStep), then offsets in entry order
-        int carry = 0;
-        for (int j0 = 0; j0 < nh; j0 += 32) {
-            const int j = j0 + lane;
-            int n = 0;
-            if (j < nh && A[j] >= 0) {
-                // e = the first step >= a_j with ts(e) >= X_j (or lastStep + 1): ts is
-                // nondecreasing in e, so start from the real-valued estimate and correct it
-                const int a = A[j];
-                const float x = X[j];
-                const double est = ceil((double)((x - t0) / dt) - (double)jit);
-                int e = est < (double)a ? a : est > (double)lastStep + 1.0 ? lastStep + 1 : (int)est;
-                while (e > a && t0 + (__int2float_rn(e - 1) + jit) * dt >= x) --e;
-                while (e <= lastStep && t0 + (__int2float_rn(e) + jit) * dt < x) ++e;
-                n = e - a;
-            }
-            int incl = n;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += v;
-            }
-            if (j < nh) OFF[j] = carry + incl - n;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        const int total = carry;
-        if (lane == 0) OFF[nh] = total;
-        __syncwarp();
+        const int total = plan_ray_walk(lane, E, X, A, OFF, nh, lastStep, jit, dt);
         int2 *ent = pp.ent + (size_t)r * kRaySegs;
         for (int j = lane; j < nh; j += 32) ent[j] = make_int2(A[j], OFF[j]);
         const int4 sp = make_int4(0, total, nh, 0);  // base: k_bwd_scan_* (ray order)
