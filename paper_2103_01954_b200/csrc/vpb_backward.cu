@@ -596,7 +596,7 @@ constexpr int kWarpListBwd = kRaySegs;
 #define VPB_BWD_RAY_GRID 64  // CTAs per SM of the warp-per-ray passes (K6a walk, records; 16 -> 64: +1.5 %)
 #endif
 #ifndef VPB_BWD_PAIR_GRID
-#define VPB_BWD_PAIR_GRID 32  // CTAs per SM of K6b (samples grid-strided; 8 -> 32: +0.8 %, 128: -4 %)
+#define VPB_BWD_PAIR_GRID 24  // CTAs per SM of K6b (samples grid-strided; 8: 57.0M, 20-24: 62.2M, 32: 61.4M, 48: 60.3M)
 #endif
 #ifndef VPB_BWD_PAIRS_NT
 #define VPB_BWD_PAIRS_NT 256  // threads per CTA of K6b
