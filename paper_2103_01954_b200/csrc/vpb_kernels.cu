@@ -1233,7 +1233,7 @@ cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,
     // kernel since removed).
     const int64_t blocks = (n_rays + 3) / 4;
 #ifndef VPB_RAYS_GRID
-#define VPB_RAYS_GRID 64  // CTAs per SM in the grid (16: 54.4M, 64: 56.8M, one ray per warp: 55.9M backward rays/s)
+#define VPB_RAYS_GRID 96  // CTAs per SM in the grid (backward rays/s at 5 CTAs/SM: 16 54.4M, 64 56.8M, one ray per warp 55.9M; at 7: 64 63.0M, 96 63.4M, 128 62.4M)
 #endif
     const unsigned grid = (unsigned)(blocks < 148 * VPB_RAYS_GRID ? blocks : 148 * VPB_RAYS_GRID);
     const bool big = n_rays >= 8192;
