@@ -159,6 +159,12 @@ struct vp_ctx {
     DBuf<float> s_loss, s_bwd_g, s_bwd_pose, s_bwd_adj, s_bwd_fwd, s_adam;
     // backward payload gradient, channel-interleaved (zero between calls) + touched flags
     DBuf<float> g_pay4;
+    // batches with the auxiliary stream alternate between two interleaved gradient buffers:
+    // the one a call used is cleared on the auxiliary stream during the next call's forward,
+    // so the transpose only reads it (g4_dirty: holds a previous call's gradient)
+    DBuf<float> g_pay4b;
+    int g4_cur = 0;
+    bool g4_dirty[2] = {false, false};
     DBuf<unsigned> g_touched;
     DBuf<int> bwd_list;  // K6: rays whose segment lists the forward did not keep
     // K6a-c pair workspace (BwdPairs); pair_cap grows to the planned count after a call that
@@ -733,6 +739,7 @@ int vp_destroy(vp_ctx *ctx) {
         if (ev) cudaEventDestroy(ev);
     ctx->ovf_tile_lists.release();
     ctx->g_pay4.release();
+    ctx->g_pay4b.release();
     ctx->g_touched.release();
     ctx->bwd_list.release();
     ctx->bp_rec.release();
@@ -1491,6 +1498,18 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             if (ctx->g_pay4.n < n_pay) {
                 VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
                 VP_CUDA(ctx, cudaMemsetAsync(ctx->g_pay4.p, 0, n_pay * 4, st));
+                ctx->g4_dirty[0] = false;
+            }
+            if (pairs && ctx->g_pay4b.n < n_pay) {
+                VP_CUDA(ctx, ctx->g_pay4b.ensure(n_pay));
+                VP_CUDA(ctx, cudaMemsetAsync(ctx->g_pay4b.p, 0, n_pay * 4, st));
+                ctx->g4_dirty[1] = false;
+            }
+            if (!pairs) ctx->g4_cur = 0;  // the single-buffer path clears in the transpose
+            float *g4 = ctx->g4_cur ? ctx->g_pay4b.p : ctx->g_pay4.p;
+            if (ctx->g4_dirty[ctx->g4_cur]) {  // not cleared during an earlier call
+                VP_CUDA(ctx, cudaMemsetAsync(g4, 0, n_pay * 4, st));
+                ctx->g4_dirty[ctx->g4_cur] = false;
             }
             VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
             VP_CUDA(ctx, cudaMemsetAsync(ctx->g_touched.p, 0, 4 * size_t(k), st));
@@ -1587,13 +1606,18 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             d_tr = pose.p + 36 * size_t(k);
         }
         VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
+        if (v4 && sp != st && ctx->g4_dirty[ctx->g4_cur ^ 1]) {  // the idle gradient buffer, beside the forward
+            VP_CUDA(ctx, cudaMemsetAsync(ctx->g4_cur ? ctx->g_pay4.p : ctx->g_pay4b.p, 0, n_pay * 4, sp));
+            ctx->g4_dirty[ctx->g4_cur ^ 1] = false;
+        }
         if (sp != st) {
             VP_CUDA(ctx, cudaEventRecord(ctx->ev_aux_join, sp));
             VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));
         }
         BwdDev bd{dg, dg + n_pay, pose.p, a_rgb, a_alpha, fwd_state, fwd_segs};
         if (v4) {
-            bd.g_pay4 = ctx->g_pay4.p;
+            bd.g_pay4 = ctx->g4_cur ? ctx->g_pay4b.p : ctx->g_pay4.p;
+            if (pairs) ctx->g4_dirty[ctx->g4_cur] = true;  // (before any launch: an error later leaves it marked)
             bd.touched = ctx->g_touched.p;
         }
         VP_CUDA(ctx, ctx->bwd_list.ensure(n));
@@ -1617,8 +1641,9 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                                           ctx->hg_x.p, ctx->hg_c.p, pairs ? &bp : nullptr, aux_ok ? ctx->aux_stream : nullptr,
                                           ctx->ev_aux_fork, ctx->ev_aux_join));
         if (v4)
-            VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(ctx->g_pay4.p), dg, ctx->g_touched.p, k,
-                                               unsigned(size_t(m) * m * m), accumulate != 0, st));
+            VP_CUDA(ctx, launch_grad_transpose(reinterpret_cast<float4 *>(bd.g_pay4), dg, ctx->g_touched.p, k,
+                                               unsigned(size_t(m) * m * m), accumulate != 0, st, !pairs));
+        if (v4 && pairs) ctx->g4_cur ^= 1;  // this call's buffer is cleared during the next call's forward
         if (aux_ok) VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));  // K6c joins
         VP_CUDA(ctx, cudaMemcpyAsync(ctx->h_ctr, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
     }

@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(256) k_grad_transpose(float4 *__restrict__ g4,
 // and each thread writes its quad as one 16-byte vector per channel plane.
 __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4, float4 *__restrict__ planar,
                                                          const unsigned *__restrict__ touched, unsigned nq,
-                                                         unsigned q3, int accumulate) {
+                                                         unsigned q3, int accumulate, int clear) {
     __shared__ float4 sm[4 * 256 + 4 * 8];  // padded: a float4 every 8 keeps the quad reads conflict-light
     const int t = threadIdx.x;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1254,9 +1254,10 @@ __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4
             sm[l + (l >> 5)] = tch[u] ? g4[4 * (size_t)i0 + l] : z;
         }
         __syncthreads();
+        if (clear)
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (tch[u]) g4[4 * (size_t)i0 + t + 256 * u] = z;
+            for (int u = 0; u < 4; ++u)
+                if (tch[u]) g4[4 * (size_t)i0 + t + 256 * u] = z;
         const unsigned i = i0 + t;
         if (i < nq) {
             const unsigned k = i / q3, qv = i - k * q3;
@@ -1290,12 +1291,12 @@ __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4
 }
 
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
-                                  bool accumulate, cudaStream_t st) {
+                                  bool accumulate, cudaStream_t st, bool clear) {
     if (n_prim == 0 || m3 == 0) return cudaSuccess;
     const size_t nq = size_t(n_prim) * (m3 / 4);
     if (m3 % 4 == 0 && (reinterpret_cast<uintptr_t>(planar) & 15) == 0 && nq < (size_t(1) << 32) - 256) {
         k_grad_transpose4<<<148 * VPB_TR_GRID, 256, 0, st>>>(g4, reinterpret_cast<float4 *>(planar), touched, unsigned(nq),
-                                                   m3 / 4, accumulate ? 1 : 0);
+                                                   m3 / 4, accumulate ? 1 : 0, clear ? 1 : 0);
         return cudaGetLastError();
     }
     const int blocks = n_prim < 148 * 8 ? n_prim : 148 * 8;

@@ -246,8 +246,9 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
                                  const BwdPairs *pairs = nullptr, cudaStream_t st2 = nullptr,
                                  cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr);
 // vpb_backward.cu: interleaved payload gradient -> planar GradBuffer (touched primitives)
+// clear = false: g4 is left as it is (the caller clears it later, e.g. on another stream)
 cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *touched, int n_prim, unsigned m3,
-                                  bool accumulate, cudaStream_t st);
+                                  bool accumulate, cudaStream_t st, bool clear = true);
 cudaError_t launch_eval_rays(const CamDev *cams, int n_cams, const int *cam_index, const float *pixel_xy,
                              const int *pixel_id, int64_t n, int jitter, unsigned long long seed,
                              float *origins, float *dirs, float *jit, int *bad, cudaStream_t st);

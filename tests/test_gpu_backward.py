@@ -198,6 +198,11 @@ def test_large_batch_interleaved_gradient_any_alignment(renderer):
     got = view.cpu().numpy()
     _check_close("unaligned.payload", got[:n_pay], want[:n_pay])
     _check_close("unaligned.pose", got[n_pay:], want[n_pay:])
+    # calls alternate between two interleaved gradient buffers (each cleared during a later
+    # call's forward): zero adjoints after all of the above must give exact zeros
+    for _ in range(2):
+        z = renderer.backward_rays(o, d, np.zeros_like(ar), np.zeros_like(aa), cfg, g["tr"], jit)
+        assert not z.any()
 
 
 @pytest.mark.parametrize("mode", ["pairs", "warp"])
