@@ -593,7 +593,7 @@ constexpr int kWarpListBwd = kRaySegs;
 #define VPB_TR_GRID 64  // CTAs per SM of k_grad_transpose4 (16 -> 64: +0.8 %)
 #endif
 #ifndef VPB_BWD_RAY_GRID
-#define VPB_BWD_RAY_GRID 64  // CTAs per SM of the warp-per-ray passes (K6a walk, records; 16 -> 64: +1.5 %)
+#define VPB_BWD_RAY_GRID 96  // CTAs per SM of the warp-per-ray passes (K6a walk, records; 16 -> 64: +1.5 %, 96: +0.5 %)
 #endif
 #ifndef VPB_BWD_PAIR_GRID
 #define VPB_BWD_PAIR_GRID 24  // CTAs per SM of K6b (samples grid-strided; 8: 57.0M, 20-24: 62.2M, 32: 61.4M, 48: 60.3M)
