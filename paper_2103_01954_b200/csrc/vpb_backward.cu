@@ -531,6 +531,8 @@ __global__ void __launch_bounds__(32, 12)
 k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                      const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
                      const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
+    const int n = (int)min((unsigned)list_cap, ctr->bwd_long);
+    if (n == 0) return;  // the common case: every list fit (no table load, no barrier)
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
@@ -538,7 +540,6 @@ k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{se, sx, sc, nthreads, gtid};
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
-    const int n = (int)min((unsigned)list_cap, ctr->bwd_long);
     for (int q = gtid; q < n; q += nthreads) {
         const int64_t r = ray_list[q];
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
@@ -556,6 +557,8 @@ __global__ void __launch_bounds__(32)
 k_backward_rays_huge(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                      const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
                      const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
+    const int n = (int)min((unsigned)list_cap, ctr->bwd_huge);
+    if (n == 0) return;
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
@@ -563,7 +566,6 @@ k_backward_rays_huge(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{se, sx, sc, nthreads, gtid};
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
-    const int n = (int)min((unsigned)list_cap, ctr->bwd_huge);
     for (int q = gtid; q < n; q += nthreads) {
         const int64_t r = ray_list[q];
         const V3 o = mk3(rays.origins[3 * r], rays.origins[3 * r + 1], rays.origins[3 * r + 2]);
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, int *__restrict__ ray_list,
                      int list_cap, int *__restrict__ huge_list, int huge_cap, const int *__restrict__ only) {
+    if (only && ctr->bwd_fb == 0) return;  // no spilled rays (the common case)
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
     __shared__ int s_c[4][kWarpListBwd];

@@ -564,11 +564,12 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
                  const uint32_t *__restrict__ offsets, const unsigned long long *__restrict__ entries,
                  OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ ovf_list,
                  int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c, int *huge_list, int huge_cap) {
+    if (!kRays && ctr->key_overflow) return;
+    const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
+    if (n_ovf == 0) return;  // the common case: no window overflowed (no table load, no barrier)
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
-    if (!kRays && ctr->key_overflow) return;
-    const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
     const int nthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
@@ -1184,6 +1185,8 @@ __global__ void __launch_bounds__(32)
 k_march_huge_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ huge_list, int huge_cap,
                   float *scratch_e, float *scratch_x, int *scratch_c) {
+    const int n = (int)min((unsigned)huge_cap, ctr->huge_rays);
+    if (n == 0) return;
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
@@ -1191,7 +1194,6 @@ k_march_huge_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const Window<int> w{scratch_e, scratch_x, scratch_c, nthreads, gtid};
     const BvhCands cands{xf_g, payload, (unsigned)(mp.m * mp.m * mp.m), n_prim, mp.bvh};
-    const int n = (int)min((unsigned)huge_cap, ctr->huge_rays);
     for (int q = gtid; q < n; q += nthreads) {
         const int p = huge_list[q];
         const V3 o = mk3(rays.origins[3 * p], rays.origins[3 * p + 1], rays.origins[3 * p + 2]);
