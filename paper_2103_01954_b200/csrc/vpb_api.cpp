@@ -1506,9 +1506,10 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                 ctx->g4_dirty[1] = false;
             }
             if (!pairs) ctx->g4_cur = 0;  // the single-buffer path clears in the transpose
-            float *g4 = ctx->g4_cur ? ctx->g_pay4b.p : ctx->g_pay4.p;
+            // a dirty buffer is cleared whole: an earlier, larger scene may have written past n_pay
+            DBuf<float> &g4b = ctx->g4_cur ? ctx->g_pay4b : ctx->g_pay4;
             if (ctx->g4_dirty[ctx->g4_cur]) {  // not cleared during an earlier call
-                VP_CUDA(ctx, cudaMemsetAsync(g4, 0, n_pay * 4, st));
+                VP_CUDA(ctx, cudaMemsetAsync(g4b.p, 0, g4b.n * 4, st));
                 ctx->g4_dirty[ctx->g4_cur] = false;
             }
             VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
@@ -1607,7 +1608,8 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         }
         VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
         if (v4 && sp != st && ctx->g4_dirty[ctx->g4_cur ^ 1]) {  // the idle gradient buffer, beside the forward
-            VP_CUDA(ctx, cudaMemsetAsync(ctx->g4_cur ? ctx->g_pay4.p : ctx->g_pay4b.p, 0, n_pay * 4, sp));
+            DBuf<float> &idle = ctx->g4_cur ? ctx->g_pay4 : ctx->g_pay4b;
+            VP_CUDA(ctx, cudaMemsetAsync(idle.p, 0, idle.n * 4, sp));
             ctx->g4_dirty[ctx->g4_cur ^ 1] = false;
         }
         if (sp != st) {

@@ -243,3 +243,38 @@ def test_random_scenes_backward_matches_restatement(monkeypatch, oracle, seed, m
     n_pay = k * 4 * m ** 3
     _check_close(f"rand{seed}.payload", got[:n_pay], want[:n_pay])
     _check_close(f"rand{seed}.pose", got[n_pay:], want[n_pay:])
+
+
+def test_large_batch_gradient_buffers_across_scene_sizes(renderer):
+    """The interleaved gradient buffers outlive scenes: a larger scene's gradient, then a
+    smaller scene's, then the larger one again must give the first result again (a buffer
+    cleared only as far as the smaller scene would leak the larger one's tail)."""
+    rng = np.random.default_rng(3)
+
+    def scene(k, m):
+        t = rng.uniform(-0.3, 0.3, (k, 3))
+        s = rng.uniform(0.05, 0.15, (k, 3))
+        tr = api.transform_records(t, np.tile(np.eye(3), (k, 1, 1)), s, delta_r=rng.uniform(-1, 1, (k, 3)))
+        pay = rng.uniform(0, 1, k * 4 * m ** 3).astype(np.float32)
+        return tr, pay
+
+    n = 16384
+    o = np.tile(np.float32([0.0, 0.0, -2.0]), (n, 1))
+    d = rng.normal(scale=0.12, size=(n, 3)).astype(np.float32)
+    d[:, 2] = 1.0
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ar = rng.normal(size=(n, 3)).astype(np.float32)
+    aa = rng.normal(size=n).astype(np.float32)
+    cfg, win = api.MarchConfig(step_size=0.004), api.WindowParams()
+    big, small = scene(160, 4), scene(40, 4)
+
+    def run(sc):
+        tr, pay = sc
+        renderer.set_scene_composed(api.compose(tr), api.PrimitiveSlab(tr.shape[0], 4, pay), win)
+        return renderer.backward_rays(o, d, ar, aa, cfg, tr)
+
+    first = run(big)
+    run(small)
+    again = run(big)
+    assert np.abs(first).max() > 0
+    _check_close("big.again", again, first.astype(np.float64))
