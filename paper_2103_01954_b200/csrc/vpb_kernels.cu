@@ -635,7 +635,7 @@ k_march_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
     __shared__ int s_c[4][kWarpList];
     __shared__ int s_cand[4][kWarpCand];
     __shared__ float s_ce[4][kWarpCand], s_cx[4][kWarpCand];
-    __shared__ float s_sv[4][128];  // march_warp: a chunk's per-step sums
+    __shared__ float s_sv[4][4 * kSvStride];  // march_warp: a chunk's per-step sums
     load_exp_tab(s_tab);
     __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;

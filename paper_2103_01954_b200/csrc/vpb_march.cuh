@@ -755,6 +755,9 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
 #ifndef VPB_FWD_PAIRS
 #define VPB_FWD_PAIRS 1  // deal primitive-samples (not steps) out to the lanes
 #endif
+// march_warp's per-warp step sums: sigma, r, g, b rows of kSvStride floats (33: row k's
+// step s sits in bank (s + k) % 32, so the four chains' lanes read distinct banks)
+constexpr int kSvStride = 33;
 template <class Cands, int MT = 0>
 __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X, const int *P, int cnt, V3 o,
                              V3 d, float jit, const MarchDev &mp, const unsigned long long *tab, int lane,
@@ -879,9 +882,9 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         // stops, then lanes 0-2 run the r, g, b chains side by side: the same additions in
         // the same order as one loop carrying all four sums, in fewer instructions per step.
         sv[lane] = sig;
-        sv[32 + lane] = rw;
-        sv[64 + lane] = gw;
-        sv[96 + lane] = bw;
+        sv[kSvStride + lane] = rw;
+        sv[2 * kSvStride + lane] = gw;
+        sv[3 * kSvStride + lane] = bw;
         __syncwarp();
         int stop = L;  // steps before `stop` take dt in full; stop < L: the ray ends at step `stop`
         bool sat = false;
@@ -897,8 +900,17 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
         const float lim = fminf(1.0f - mp.eps, 1.0f);
-        if (T >= 0.0f && T + pos * 1.0001f + 1e-5f < lim) {
-            for (int s = 0; s < L; ++s) T += sv[s] * dt;
+        const bool quiet = T >= 0.0f && T + pos * 1.0001f + 1e-5f < lim;
+        if (quiet) {
+            // every step takes dt in full: lanes 0-2 run the r, g, b chains and the others the
+            // transmittance chain, all in one loop (the same additions in the same order)
+            const float *cv = sv + kSvStride * (lane < 3 ? 1 + lane : 0);
+            float c = lane == 0 ? cr : (lane == 1 ? cg : (lane == 2 ? cb : T));
+            for (int s = 0; s < L; ++s) c += cv[s] * dt;
+            cr = __shfl_sync(0xffffffffu, c, 0);
+            cg = __shfl_sync(0xffffffffu, c, 1);
+            cb = __shfl_sync(0xffffffffu, c, 2);
+            T = __shfl_sync(0xffffffffu, c, 3);
         } else
         for (int s = 0; s < L; ++s) {
             const float dT = sv[s] * dt;
@@ -917,8 +929,8 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         }
         const int n_steps = stop < L ? stop + 1 : L;  // steps sampled in this chunk
         const int n_full = sat ? stop : n_steps;     // ... of which with the full dt
-        {
-            const float *cv = sv + 32 * (1 + (lane < 2 ? lane : 2));
+        if (!quiet) {
+            const float *cv = sv + kSvStride * (1 + (lane < 2 ? lane : 2));
             float c = lane == 0 ? cr : (lane == 1 ? cg : cb);
             for (int s = 0; s < n_full; ++s) c += cv[s] * dt;
             if (sat) {
@@ -935,9 +947,9 @@ __device__ RayOut march_warp(const Cands &cands, const float *E, const float *X,
         if (sat) {
             out.sat_tprev = Tprev;
             out.sat_sigma = sv[stop];
-            out.sat_r = sv[32 + stop];
-            out.sat_g = sv[64 + stop];
-            out.sat_b = sv[96 + stop];
+            out.sat_r = sv[kSvStride + stop];
+            out.sat_g = sv[2 * kSvStride + stop];
+            out.sat_b = sv[3 * kSvStride + stop];
             T = 1.0f;
             out.saturated = 1;
         }
