@@ -721,19 +721,36 @@ __device__ __forceinline__ int warp_segment_list(const BvhCands &cands, V3 o, V3
         cx[q] = tX;
     }
     __syncwarp();
-    int mine = 0;
-    for (int q = lane; q < nc; q += 32) mine += ce[q] != __int_as_float(0x7f800000);
-    const int nh = __reduce_add_sync(0xffffffffu, mine);
+    // the hits moved to the front in candidate order (in place: a round's reads precede its
+    // writes, and no write passes the round's own slots), then ranked among themselves
+    int nh = 0;
+    for (int q0 = 0; q0 < nc; q0 += 32) {
+        const int q = q0 + lane;
+        float e = __int_as_float(0x7f800000), x = 0.f;
+        int c = 0;
+        if (q < nc) {
+            e = ce[q];
+            x = cx[q];
+            c = cand[q];
+        }
+        const bool h = e != __int_as_float(0x7f800000);
+        const unsigned b = __ballot_sync(0xffffffffu, h);
+        __syncwarp();
+        if (h) {
+            const int dst = nh + __popc(b & ((1u << lane) - 1u));
+            ce[dst] = e;
+            cx[dst] = x;
+            cand[dst] = c;
+        }
+        nh += __popc(b);
+    }
+    __syncwarp();
     if (nh > cap) return -1;
-    for (int q = lane; q < nc; q += 32) {
+    for (int q = lane; q < nh; q += 32) {
         const float e = ce[q];
-        if (e == __int_as_float(0x7f800000)) continue;
         const int pq = cand[q];
         int rank = 0;
-        for (int u = 0; u < nc; ++u) {
-            const float eu = ce[u];
-            rank += eu != __int_as_float(0x7f800000) && key_less(eu, cand[u], e, pq);
-        }
+        for (int u = 0; u < nh; ++u) rank += key_less(ce[u], cand[u], e, pq);
         E[rank] = e;
         X[rank] = cx[q];
         P[rank] = pq;
