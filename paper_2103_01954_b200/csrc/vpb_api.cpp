@@ -1493,7 +1493,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
     const bool pairs = ctx->bwd_warp_walk == 0 || (ctx->bwd_warp_walk < 0 && n_rays >= kPairsMinRays);
     const bool v4 = k > 0 && n_rays > 0 && (ctx->bwd_v4 == 1 || (ctx->bwd_v4 < 0 && pairs && n_rays >= kV4MinRays));
     // the gradient buffers are cleared once the forward is queued (below), or here without rays
-    auto clear_grads = [&]() -> int {
+    auto clear_grads = [&](cudaStream_t st) -> int {
         if (v4) {
             if (ctx->g_pay4.n < n_pay) {
                 VP_CUDA(ctx, ctx->g_pay4.ensure(n_pay));
@@ -1521,7 +1521,7 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
         return VP_OK;
     };
     if (!(k > 0 && n_rays > 0))
-        if (int rc = clear_grads()) return rc;
+        if (int rc = clear_grads(st)) return rc;
     if (k > 0 && n_rays > 0) {
         const size_t n = size_t(n_rays);
         RaysDev rays{origins, dirs, jitter01};
@@ -1588,7 +1588,6 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             fwd_state = od.state;
             fwd_segs = od.segs;
         }
-        if (int rc = clear_grads()) return rc;
         // pose data on the device (k_pose36, the reference's operation order): rBase and
         // dR(deltaR)/dv_i per primitive; pose = [36 K | the records, if they are on the host].
         // Queued after the forward, on the auxiliary stream when there is one: it runs beside
@@ -1599,6 +1598,8 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             VP_CUDA(ctx, cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_aux_pose, 0));  // st before the forward
             sp = ctx->aux_stream;
         }
+        // order on the auxiliary stream: the records' upload (copy engine, at once), then the
+        // kernels, which find SM slots only as the forward's last CTAs retire
         VP_CUDA(ctx, pose.ensure(36 * size_t(k) + 24 * size_t(k)));
         const float *d_tr = transforms24;
         if (!is_device_ptr(transforms24)) {
@@ -1606,12 +1607,13 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                                          cudaMemcpyHostToDevice, sp));
             d_tr = pose.p + 36 * size_t(k);
         }
-        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
+        if (int rc = clear_grads(sp)) return rc;  // (beside the forward: it reads none of these)
         if (v4 && sp != st && ctx->g4_dirty[ctx->g4_cur ^ 1]) {  // the idle gradient buffer, beside the forward
             DBuf<float> &idle = ctx->g4_cur ? ctx->g_pay4 : ctx->g_pay4b;
             VP_CUDA(ctx, cudaMemsetAsync(idle.p, 0, idle.n * 4, sp));
             ctx->g4_dirty[ctx->g4_cur ^ 1] = false;
         }
+        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
         if (sp != st) {
             VP_CUDA(ctx, cudaEventRecord(ctx->ev_aux_join, sp));
             VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));

@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(32, 12)
 k_backward_rays_list(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                      const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
                      const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     const int n = (int)min((unsigned)list_cap, ctr->bwd_long);
     if (n == 0) return;  // the common case: every list fit (no table load, no barrier)
     __shared__ unsigned long long s_tab[32];
@@ -557,6 +558,7 @@ __global__ void __launch_bounds__(32)
 k_backward_rays_huge(MarchDev mp, const float *__restrict__ xf_g, int n_prim,
                      const float4 *__restrict__ payload, RaysDev rays, BwdDev bd, DevCounters *ctr,
                      const int *__restrict__ ray_list, int list_cap, float *se, float *sx, int *sc) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     const int n = (int)min((unsigned)list_cap, ctr->bwd_huge);
     if (n == 0) return;
     __shared__ unsigned long long s_tab[32];
@@ -613,6 +615,7 @@ __global__ void __launch_bounds__(128, VPB_BWD_WARP_MINB)
 k_backward_rays_warp(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                      RaysDev rays, int64_t n_rays, BwdDev bd, DevCounters *ctr, int *__restrict__ ray_list,
                      int list_cap, int *__restrict__ huge_list, int huge_cap, const int *__restrict__ only) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     if (only && ctr->bwd_fb == 0) return;  // no spilled rays (the common case)
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_e[4][kWarpListBwd], s_x[4][kWarpListBwd];
@@ -912,6 +915,7 @@ k_bwd_plan(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, De
 // total as the pair count.
 constexpr int kScanTile = 4096;  // rays per CTA of k_bwd_scan_tiles: 1024 threads x 4
 __global__ void __launch_bounds__(1024) k_bwd_scan_tiles(int64_t n_rays, BwdPairs pp, DevCounters *ctr) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     __shared__ int s_w[32];
     const int64_t r0 = (int64_t)blockIdx.x * kScanTile + 4 * threadIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -952,6 +956,7 @@ __global__ void __launch_bounds__(1024) k_bwd_scan_tiles(int64_t n_rays, BwdPair
 }
 
 __global__ void __launch_bounds__(1024) k_bwd_scan_top(int n_tiles, BwdPairs pp, DevCounters *ctr) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     __shared__ long long s_w[32];
     __shared__ long long s_carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -993,6 +998,7 @@ __global__ void __launch_bounds__(1024) k_bwd_scan_top(int n_tiles, BwdPairs pp,
 // sentinels that K6b skips).
 __global__ void __launch_bounds__(128)
 k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp, DevCounters *ctr) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     __shared__ int s_a[4][kRaySegs], s_off[4][kRaySegs + 1];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int *A = s_a[wid], *OFF = s_off[wid];
@@ -1063,6 +1069,7 @@ k_bwd_records(MarchDev mp, RaysDev rays, int64_t n_rays, BwdDev bd, BwdPairs pp,
 __global__ void __launch_bounds__(VPB_BWD_PAIRS_NT, VPB_BWD_PAIRS_MINB)
 k_bwd_pairs(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
             RaysDev rays, BwdDev bd, BwdPairs pp, const DevCounters *__restrict__ ctr) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     __shared__ unsigned long long s_tab[32];
     load_exp_tab(s_tab);
     __syncthreads();
@@ -1230,6 +1237,7 @@ __global__ void __launch_bounds__(256) k_grad_transpose(float4 *__restrict__ g4,
 __global__ void __launch_bounds__(256) k_grad_transpose4(float4 *__restrict__ g4, float4 *__restrict__ planar,
                                                          const unsigned *__restrict__ touched, unsigned nq,
                                                          unsigned q3, int accumulate, int clear) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     __shared__ float4 sm[4 * 256 + 4 * 8];  // padded: a float4 every 8 keeps the quad reads conflict-light
     const int t = threadIdx.x;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1298,9 +1306,9 @@ cudaError_t launch_grad_transpose(float4 *g4, float *planar, const unsigned *tou
     if (n_prim == 0 || m3 == 0) return cudaSuccess;
     const size_t nq = size_t(n_prim) * (m3 / 4);
     if (m3 % 4 == 0 && (reinterpret_cast<uintptr_t>(planar) & 15) == 0 && nq < (size_t(1) << 32) - 256) {
-        k_grad_transpose4<<<148 * VPB_TR_GRID, 256, 0, st>>>(g4, reinterpret_cast<float4 *>(planar), touched, unsigned(nq),
-                                                   m3 / 4, accumulate ? 1 : 0, clear ? 1 : 0);
-        return cudaGetLastError();
+        return launch_pdl(k_grad_transpose4, dim3(148 * VPB_TR_GRID), dim3(256), 0, st, g4,
+                          reinterpret_cast<float4 *>(planar), touched, unsigned(nq), m3 / 4, accumulate ? 1 : 0,
+                          clear ? 1 : 0);
     }
     const int blocks = n_prim < 148 * 8 ? n_prim : 148 * 8;
     k_grad_transpose<<<blocks, 256, 0, st>>>(g4, planar, touched, n_prim, m3, accumulate ? 1 : 0);
@@ -1324,10 +1332,19 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
         k_bwd_plan<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr, ray_list, list_cap, huge_list,
                                                huge_cap);
         const int64_t n_tiles = (n_rays + kScanTile - 1) / kScanTile;
-        k_bwd_scan_tiles<<<(unsigned)n_tiles, 1024, 0, st>>>(n_rays, *pairs, ctr);
-        if (n_tiles > 1) k_bwd_scan_top<<<1, 1024, 0, st>>>((int)n_tiles, *pairs, ctr);
-        k_bwd_records<<<ray_blocks, 128, 0, st>>>(mp, rays, n_rays, bd, *pairs, ctr);
-        k_bwd_pairs<<<148 * VPB_BWD_PAIR_GRID, VPB_BWD_PAIRS_NT, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, *pairs, ctr);
+        // the chain from here on launches programmatically (each kernel waits for its producer)
+        if (cudaError_t e = cudaGetLastError()) return e;
+        if (cudaError_t e = launch_pdl(k_bwd_scan_tiles, dim3((unsigned)n_tiles), dim3(1024), 0, st, n_rays, *pairs, ctr))
+            return e;
+        if (n_tiles > 1)
+            if (cudaError_t e = launch_pdl(k_bwd_scan_top, dim3(1), dim3(1024), 0, st, (int)n_tiles, *pairs, ctr))
+                return e;
+        if (cudaError_t e = launch_pdl(k_bwd_records, dim3(ray_blocks), dim3(128), 0, st, mp, rays, n_rays, bd, *pairs,
+                                       ctr))
+            return e;
+        if (cudaError_t e = launch_pdl(k_bwd_pairs, dim3(148 * VPB_BWD_PAIR_GRID), dim3(VPB_BWD_PAIRS_NT), 0, st, mp,
+                                       xf16, n_prim, payload, rays, bd, *pairs, ctr))
+            return e;
         const int64_t tb = (n_rays + 127) / 128;
         // K6c reads only K6b's rotG and writes pose reductions: it runs beside the walk for the
         // spilled rays and the gradient transpose (the caller joins ev_join)
@@ -1347,14 +1364,13 @@ cudaError_t launch_backward_rays(const MarchDev &mp, const float *xf16, int n_pr
             mp, xf16, n_prim, payload, rays, n_rays, bd, ctr, ray_list, list_cap, huge_list, huge_cap, nullptr);
     }
     if (cudaError_t e = cudaGetLastError()) return e;
-    k_backward_rays_list<<<kBackwardWarps, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, ray_list,
-                                                         list_cap, se, sx, sc);
-    if (huge_list) {
-        if (cudaError_t e = cudaGetLastError()) return e;
-        k_backward_rays_huge<<<kHugeThreads / 32, 32, 0, st>>>(mp, xf16, n_prim, payload, rays, bd, ctr, huge_list,
-                                                                huge_cap, he, hx, hc);
-    }
-    return cudaGetLastError();
+    if (cudaError_t e = launch_pdl(k_backward_rays_list, dim3(kBackwardWarps), dim3(32), 0, st, mp, xf16, n_prim,
+                                   payload, rays, bd, ctr, ray_list, list_cap, se, sx, sc))
+        return e;
+    if (huge_list)
+        return launch_pdl(k_backward_rays_huge, dim3(kHugeThreads / 32), dim3(32), 0, st, mp, xf16, n_prim, payload,
+                          rays, bd, ctr, huge_list, huge_cap, he, hx, hc);
+    return cudaSuccess;
 }
 
 }  // namespace vpb

@@ -564,6 +564,7 @@ k_march_fallback(CamDev cam, MarchDev mp, const float *__restrict__ xf_g,
                  const uint32_t *__restrict__ offsets, const unsigned long long *__restrict__ entries,
                  OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ ovf_list,
                  int ovf_cap, float *scratch_e, float *scratch_x, int *scratch_c, int *huge_list, int huge_cap) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     if (!kRays && ctr->key_overflow) return;
     const int n_ovf = (int)min((unsigned long long)ovf_cap, ctr->overflow_rays);
     if (n_ovf == 0) return;  // the common case: no window overflowed (no table load, no barrier)
@@ -1174,10 +1175,9 @@ cudaError_t launch_march_fallback(bool rays_mode, const CamDev &cam, const March
                                   int huge_cap) {
     // camera renders re-march their overflow rays in k_march_fallback_views
     if (!rays_mode) return cudaErrorInvalidValue;
-    k_march_fallback<true><<<kFallbackBlocks, kFallbackThreads, 0, st>>>(
-        cam, mp, xf16, prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc,
-        huge_list, huge_cap);
-    return cudaGetLastError();
+    return launch_pdl(k_march_fallback<true>, dim3(kFallbackBlocks), dim3(kFallbackThreads), 0, st, cam, mp, xf16,
+                      prects, n_prim, payload, offsets, entries, od, rays, ctr, ovf_list, ovf_cap, se, sx, sc,
+                      huge_list, huge_cap);
 }
 
 // K5c for arbitrary rays: kHugeCap-entry windows through the BVH, one thread per ray.
@@ -1185,6 +1185,7 @@ __global__ void __launch_bounds__(32)
 k_march_huge_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const float4 *__restrict__ payload,
                   OutDev od, RaysDev rays, DevCounters *ctr, const int *__restrict__ huge_list, int huge_cap,
                   float *scratch_e, float *scratch_x, int *scratch_c) {
+    VPB_PDL_WAIT();  // launched after its producer with programmatic serialization
     const int n = (int)min((unsigned)huge_cap, ctr->huge_rays);
     if (n == 0) return;
     __shared__ unsigned long long s_tab[32];
@@ -1219,9 +1220,8 @@ k_march_huge_rays(MarchDev mp, const float *__restrict__ xf_g, int n_prim, const
 cudaError_t launch_march_huge_rays(const MarchDev &mp, const float *xf16, int n_prim, const float4 *payload,
                                    const OutDev &od, const RaysDev &rays, DevCounters *ctr, const int *huge_list,
                                    int huge_cap, float *se, float *sx, int *sc, cudaStream_t st) {
-    k_march_huge_rays<<<kHugeThreads / 32, 32, 0, st>>>(mp, xf16, n_prim, payload, od, rays, ctr, huge_list, huge_cap,
-                                                        se, sx, sc);
-    return cudaGetLastError();
+    return launch_pdl(k_march_huge_rays, dim3(kHugeThreads / 32), dim3(32), 0, st, mp, xf16, n_prim, payload, od, rays,
+                      ctr, huge_list, huge_cap, se, sx, sc);
 }
 
 cudaError_t launch_march_rays(const MarchDev &mp, const float *xf16, int n_prim,

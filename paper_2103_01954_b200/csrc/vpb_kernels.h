@@ -11,6 +11,27 @@
 
 namespace vpb {
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be scheduled while its
+// stream predecessor drains (hiding the launch gap); it must start with VPB_PDL_WAIT(), which
+// returns once the predecessor has completed and its writes are visible (a no-op otherwise).
+#define VPB_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+
 struct DevCounters {
     unsigned long long ray_samples, prim_samples, hit_rays, early_exits, saturated;
     unsigned long long overflow_rays, refills, keys, numeric_fail, nonempty_tiles;
