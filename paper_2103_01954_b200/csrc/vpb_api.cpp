@@ -163,6 +163,8 @@ struct vp_ctx {
     // the one a call used is cleared on the auxiliary stream during the next call's forward,
     // so the transpose only reads it (g4_dirty: holds a previous call's gradient)
     DBuf<float> g_pay4b;
+    float *h_zeros = nullptr;  // page-locked zeros: small clears as copy-engine uploads (no SM slots)
+    size_t h_zeros_n = 0;
     int g4_cur = 0;
     bool g4_dirty[2] = {false, false};
     DBuf<unsigned> g_touched;
@@ -740,6 +742,8 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->ovf_tile_lists.release();
     ctx->g_pay4.release();
     ctx->g_pay4b.release();
+    if (ctx->h_zeros) cudaFreeHost(ctx->h_zeros);
+    ctx->h_zeros = nullptr;
     ctx->g_touched.release();
     ctx->bwd_list.release();
     ctx->bp_rec.release();
@@ -1513,8 +1517,19 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
                 ctx->g4_dirty[ctx->g4_cur] = false;
             }
             VP_CUDA(ctx, ctx->g_touched.ensure(size_t(k)));
-            VP_CUDA(ctx, cudaMemsetAsync(ctx->g_touched.p, 0, 4 * size_t(k), st));
-            if (!accumulate) VP_CUDA(ctx, cudaMemsetAsync(dg + n_pay, 0, (n_grad - n_pay) * 4, st));
+            // the flags and the pose part are cleared by copies from a zero block: on the
+            // auxiliary stream they then run at once instead of waiting for the forward's SMs
+            if (ctx->h_zeros_n < 9 * size_t(k)) {
+                if (ctx->h_zeros) cudaFreeHost(ctx->h_zeros);
+                ctx->h_zeros = nullptr;
+                ctx->h_zeros_n = 0;
+                VP_CUDA(ctx, cudaMallocHost(&ctx->h_zeros, 9 * size_t(k) * 4));
+                memset(ctx->h_zeros, 0, 9 * size_t(k) * 4);
+                ctx->h_zeros_n = 9 * size_t(k);
+            }
+            VP_CUDA(ctx, cudaMemcpyAsync(ctx->g_touched.p, ctx->h_zeros, 4 * size_t(k), cudaMemcpyHostToDevice, st));
+            if (!accumulate)
+                VP_CUDA(ctx, cudaMemcpyAsync(dg + n_pay, ctx->h_zeros, (n_grad - n_pay) * 4, cudaMemcpyHostToDevice, st));
         } else if (!accumulate) {
             VP_CUDA(ctx, cudaMemsetAsync(dg, 0, n_grad * 4, st));
         }
@@ -1608,12 +1623,12 @@ int backward_rays(vp_ctx *ctx, int64_t n_rays, const float *origins, const float
             d_tr = pose.p + 36 * size_t(k);
         }
         if (int rc = clear_grads(sp)) return rc;  // (beside the forward: it reads none of these)
+        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
         if (v4 && sp != st && ctx->g4_dirty[ctx->g4_cur ^ 1]) {  // the idle gradient buffer, beside the forward
             DBuf<float> &idle = ctx->g4_cur ? ctx->g_pay4 : ctx->g_pay4b;
             VP_CUDA(ctx, cudaMemsetAsync(idle.p, 0, idle.n * 4, sp));
             ctx->g4_dirty[ctx->g4_cur ^ 1] = false;
         }
-        VP_CUDA(ctx, launch_pose36(d_tr, k, pose.p, sp));
         if (sp != st) {
             VP_CUDA(ctx, cudaEventRecord(ctx->ev_aux_join, sp));
             VP_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_aux_join, 0));
