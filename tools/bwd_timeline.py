@@ -1,6 +1,6 @@
 """Device timeline of the backward row's last calls (torch.profiler / CUPTI sees libvpb's
 kernels too): start offset, duration and stream of every kernel, memset and copy, to find the
-idle gaps between launches. Usage: python tools/bwd_timeline.py [out.txt]"""
+idle gaps between launches. Usage: python tools/bwd_timeline.py [out.txt] [backward|fit]"""
 import json
 import pathlib
 import sys
@@ -14,11 +14,12 @@ import bench_rows  # noqa: E402
 from paper_2103_01954_b200 import Renderer, api, synthetic  # noqa: E402
 
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/bwd_timeline.txt"
+row = sys.argv[2] if len(sys.argv) > 2 else "backward"
 r = Renderer(0)
 args = types.SimpleNamespace(steps=3, warmup=3, no_cpu_baseline=True)
 bench_rows.emit = lambda row: None
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-    bench_rows.row_backward(args, torch, r, r._lib, api, synthetic, None)
+    getattr(bench_rows, "row_" + row)(args, torch, r, r._lib, api, synthetic, None)
 tr = pathlib.Path(tempfile.mkdtemp()) / "t.json"
 prof.export_chrome_trace(str(tr))
 ev = [e for e in json.load(open(tr))["traceEvents"]
