@@ -744,6 +744,7 @@ int vp_destroy(vp_ctx *ctx) {
     ctx->g_pay4b.release();
     if (ctx->h_zeros) cudaFreeHost(ctx->h_zeros);
     ctx->h_zeros = nullptr;
+    ctx->h_zeros_n = 0;
     ctx->g_touched.release();
     ctx->bwd_list.release();
     ctx->bp_rec.release();
